@@ -1,0 +1,334 @@
+"""CPU oracle for the PLMSS hot path — TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s CPU-baseline /
+``--impl reference`` legs import this package, and only as the checker. The
+product (``paper_2303_15491_b200``) never imports it.
+
+Two independent CPU implementations share one numpy-level API:
+
+* :class:`Restatement` — ``plmss_oracle.c``, a plain-C restatement of the
+  reference algorithm (each function cites the reference file:line);
+* :class:`Reference` — the reference library itself, compiled unchanged from
+  ``/root/reference/proj/src`` into ``oracle/_ref/libplmss_ref.so`` (namespace
+  ``plmss_ref``) by ``oracle/Makefile``.
+
+The restatement is pinned against the reference's golden vectors and against
+:class:`Reference` in ``tests/test_oracle_pin.py``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SO = os.path.join(HERE, "_build", "libplmss_oracle.so")
+REF_SO = os.path.join(HERE, "_ref", "libplmss_ref.so")
+REF_SRC = "/root/reference/proj"
+
+_i64p = np.ctypeslib.ndpointer(np.int64, flags="C_CONTIGUOUS")
+_f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
+_u8p = np.ctypeslib.ndpointer(np.uint8, flags="C_CONTIGUOUS")
+
+
+def build(reference: bool = True) -> None:
+    """Build the restatement (always) and the compiled reference (only where
+    /root/reference exists — i.e. in the build container; the .so travels)."""
+    subprocess.run(["make", "-s", "-C", HERE, "oracle"], check=True)
+    if reference and os.path.isdir(REF_SRC):
+        subprocess.run(["make", "-s", "-j8", "-C", HERE, "ref"], check=True)
+
+
+def _dims(d):
+    return np.ascontiguousarray(np.asarray(d, dtype=np.int64).reshape(3))
+
+
+def _vec3(v, default):
+    return np.ascontiguousarray(np.asarray(default if v is None else v, dtype=np.float64).reshape(3))
+
+
+class Restatement:
+    """ctypes front-end of plmss_oracle.c."""
+
+    def __init__(self, path: str = ORACLE_SO):
+        if not os.path.exists(path):
+            build(reference=False)
+        L = self.lib = C.CDLL(path)
+        L.orc_compute_order.restype = C.c_int64
+        L.orc_compute_order.argtypes = [_f64p, C.c_int64, _i64p]
+        L.orc_seed_hops.restype = None
+        L.orc_seed_hops.argtypes = [_i64p, C.c_void_p, C.c_int, _i64p, _i64p]
+        L.orc_compress.restype = C.c_int
+        L.orc_compress.argtypes = [C.c_int64, _i64p, _i64p]
+        L.orc_extrema.restype = C.c_int64
+        L.orc_extrema.argtypes = [C.c_int64, _i64p, C.c_void_p]
+        L.orc_combine_ms.restype = C.c_int64
+        L.orc_combine_ms.argtypes = [C.c_int64, _i64p, _i64p, _i64p, C.c_void_p]
+        L.orc_tetra_code.restype = C.c_int
+        L.orc_tetra_code.argtypes = [_i64p, C.c_void_p]
+        L.orc_triangle_code.restype = C.c_int
+        L.orc_triangle_code.argtypes = [_i64p]
+        L.orc_tetra_case.restype = C.c_int
+        L.orc_tetra_case.argtypes = [C.c_int, C.c_void_p]
+        L.orc_triangle_case.restype = C.c_int
+        L.orc_triangle_case.argtypes = [C.c_int, C.c_void_p]
+        L.orc_num_cells.restype = C.c_int64
+        L.orc_num_cells.argtypes = [_i64p]
+        L.orc_cell.restype = C.c_int
+        L.orc_cell.argtypes = [_i64p, C.c_int64, _i64p]
+        L.orc_index_separators.restype = C.c_int64
+        L.orc_index_separators.argtypes = [_i64p, _i64p, C.c_void_p]
+        L.orc_emit_geometry.restype = None
+        L.orc_emit_geometry.argtypes = [_i64p, _f64p, _f64p, _i64p, _u8p, _f64p, _i64p, _i64p]
+        L.orc_emit_boundaries.restype = None
+        L.orc_emit_boundaries.argtypes = [_i64p, _f64p, _f64p, _i64p, C.c_int, C.c_int64, _i64p] + [C.c_void_p] * 5
+
+    # -- order / segmentation -------------------------------------------------
+    def compute_order(self, values):
+        v = np.ascontiguousarray(values, dtype=np.float64).ravel()
+        rank = np.empty(v.size, np.int64)
+        bad = self.lib.orc_compute_order(v, v.size, rank)
+        if bad >= 0:
+            raise ValueError(f"non-finite scalar value at vertex {bad}")
+        return rank
+
+    def seed_hops(self, dims, values=None, rank=None):
+        d = _dims(dims)
+        n = int(np.prod(d))
+        desc = np.empty(n, np.int64)
+        asc = np.empty(n, np.int64)
+        if rank is not None:
+            keys = np.ascontiguousarray(rank, dtype=np.int64).ravel()
+            kind = 1
+        else:
+            keys = np.ascontiguousarray(values, dtype=np.float64).ravel()
+            kind = 0
+        assert keys.size == n
+        self.lib.orc_seed_hops(d, keys.ctypes.data, kind, desc, asc)
+        return desc, asc
+
+    def segment(self, dims, values=None, rank=None):
+        desc, asc = self.seed_hops(dims, values=values, rank=rank)
+        sweeps = self.lib.orc_compress(desc.size, desc, asc)
+        return dict(desc=desc, asc=asc, maxima=self.extrema(desc), minima=self.extrema(asc), sweeps=sweeps)
+
+    def extrema(self, labels):
+        lab = np.ascontiguousarray(labels, dtype=np.int64)
+        k = self.lib.orc_extrema(lab.size, lab, None)
+        out = np.empty(k, np.int64)
+        self.lib.orc_extrema(lab.size, lab, out.ctypes.data)
+        return out
+
+    def combine_ms(self, asc, desc):
+        a = np.ascontiguousarray(asc, dtype=np.int64)
+        d = np.ascontiguousarray(desc, dtype=np.int64)
+        ms = np.empty(a.size, np.int64)
+        keys = np.empty(2 * max(a.size, 1), np.int64)
+        r = self.lib.orc_combine_ms(a.size, a, d, ms, keys.ctypes.data)
+        return ms, keys[: 2 * r].reshape(r, 2)
+
+    # -- marching -------------------------------------------------------------
+    def tetra_code(self, labels4):
+        loc = np.zeros(4, np.int32)
+        c = self.lib.orc_tetra_code(np.ascontiguousarray(labels4, dtype=np.int64), loc.ctypes.data)
+        return c, loc
+
+    def triangle_code(self, labels3):
+        return self.lib.orc_triangle_code(np.ascontiguousarray(labels3, dtype=np.int64))
+
+    def tetra_case(self, code):
+        buf = np.zeros(12 * 5, np.uint8)
+        k = self.lib.orc_tetra_case(code, buf.ctypes.data)
+        return buf[: 5 * k].reshape(k, 5)
+
+    def triangle_case(self, code):
+        buf = np.zeros(3 * 4, np.uint8)
+        k = self.lib.orc_triangle_case(code, buf.ctypes.data)
+        return buf[: 4 * k].reshape(k, 4)
+
+    def num_cells(self, dims):
+        return self.lib.orc_num_cells(_dims(dims))
+
+    def cell(self, dims, c):
+        out = np.zeros(4, np.int64)
+        ar = self.lib.orc_cell(_dims(dims), c, out)
+        return out[:ar]
+
+    def index_separators(self, dims, labels):
+        d = _dims(dims)
+        lab = np.ascontiguousarray(labels, dtype=np.int64).ravel()
+        codes = np.empty(self.num_cells(d), np.uint8)
+        total = self.lib.orc_index_separators(d, lab, codes.ctypes.data)
+        return codes, total
+
+    def emit_separators(self, dims, labels, spacing=None, origin=None):
+        d = _dims(dims)
+        lab = np.ascontiguousarray(labels, dtype=np.int64).ravel()
+        codes, total = self.index_separators(d, lab)
+        ar = 3 if int((d >= 2).sum()) == 3 else 2
+        pts = np.zeros(3 * ar * max(total, 1), np.float64)
+        reg = np.zeros(2 * max(total, 1), np.int64)
+        src = np.zeros(max(total, 1), np.int64)
+        self.lib.orc_emit_geometry(d, _vec3(spacing, (1, 1, 1)), _vec3(origin, (0, 0, 0)), lab, codes, pts, reg, src)
+        return dict(
+            codes=codes,
+            points=pts[: 3 * ar * total].reshape(ar * total, 3),
+            indices=np.arange(ar * total, dtype=np.int64),
+            regions=reg[: 2 * total].reshape(total, 2),
+            source_cells=src[:total],
+            arity=ar,
+        )
+
+    def emit_boundaries(self, dims, labels, region_filter=None, spacing=None, origin=None):
+        d = _dims(dims)
+        lab = np.ascontiguousarray(labels, dtype=np.int64).ravel()
+        sp, og = _vec3(spacing, (1, 1, 1)), _vec3(origin, (0, 0, 0))
+        hf = 0 if region_filter is None else 1
+        flt = 0 if region_filter is None else int(region_filter)
+        sizes = np.zeros(2, np.int64)
+        self.lib.orc_emit_boundaries(d, sp, og, lab, hf, flt, sizes, None, None, None, None, None)
+        nf, npnt = int(sizes[0]), int(sizes[1])
+        ar = 3 if int((d >= 2).sum()) == 3 else 2
+        faces = np.zeros(ar * max(nf, 1), np.int64)
+        tags = np.zeros(max(nf, 1), np.int64)
+        cells = np.zeros(max(nf, 1), np.int64)
+        pts = np.zeros(3 * max(npnt, 1), np.float64)
+        idx = np.zeros(ar * max(nf, 1), np.int64)
+        self.lib.orc_emit_boundaries(d, sp, og, lab, hf, flt, sizes, faces.ctypes.data, tags.ctypes.data,
+                                     cells.ctypes.data, pts.ctypes.data, idx.ctypes.data)
+        regions = np.stack([tags[:nf], np.full(nf, -1, np.int64)], axis=1)
+        return dict(faces=faces[: ar * nf].reshape(nf, ar), points=pts[: 3 * npnt].reshape(npnt, 3),
+                    indices=idx[: ar * nf], regions=regions, source_cells=cells[:nf], arity=ar)
+
+
+class ReferenceError_(RuntimeError):
+    pass
+
+
+_KIND = {1: ValueError, 2: RuntimeError, 3: IndexError, 4: RuntimeError}
+
+
+class Reference:
+    """ctypes front-end of the reference library compiled unchanged
+    (oracle/_ref/libplmss_ref.so), through oracle/ref_capi.cpp. The same class
+    also fronts build/libplmss_dropin_harness.so (reference API -> B200)."""
+
+    def __init__(self, path: str = REF_SO):
+        if not os.path.exists(path):
+            raise FileNotFoundError(f"{path} missing: run `make -C oracle ref` where /root/reference exists")
+        L = self.lib = C.CDLL(path)
+        L.cap_last_error.restype = C.c_char_p
+        L.cap_compute_order.argtypes = [_f64p, C.c_int64, _i64p]
+        L.cap_segment.argtypes = [_i64p, _i64p, C.c_int64, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)]
+        L.cap_seg_size.restype = C.c_int64
+        L.cap_seg_size.argtypes = [C.c_void_p, C.c_int]
+        L.cap_seg_copy.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
+        L.cap_seg_free.argtypes = [C.c_void_p]
+        L.cap_oracle_walk.argtypes = [_i64p, _i64p, C.c_int64, C.c_int64, C.c_int, C.POINTER(C.c_int64)]
+        L.cap_tetra_code.argtypes = [_i64p, C.c_void_p, C.c_void_p]
+        L.cap_triangle_code.argtypes = [_i64p, C.c_void_p]
+        L.cap_tetra_case.argtypes = [C.c_int, C.c_void_p]
+        L.cap_triangle_case.argtypes = [C.c_int, C.c_void_p]
+        L.cap_emit.argtypes = [_i64p, _f64p, _f64p, _i64p, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_int64,
+                               C.POINTER(C.c_void_p)]
+        L.cap_mesh_sizes.argtypes = [C.c_void_p, _i64p]
+        L.cap_mesh_copy.argtypes = [C.c_void_p] + [C.c_void_p] * 5
+        L.cap_mesh_free.argtypes = [C.c_void_p]
+        L.cap_run_benchmark.argtypes = [_i64p, _f64p, C.c_int, C.c_int, C.c_int, _f64p]
+
+    def _check(self, st):
+        if st != 0:
+            raise _KIND.get(st, RuntimeError)(self.lib.cap_last_error().decode())
+
+    def compute_order(self, values):
+        v = np.ascontiguousarray(values, dtype=np.float64).ravel()
+        rank = np.empty(v.size, np.int64)
+        self._check(self.lib.cap_compute_order(v, v.size, rank))
+        return rank
+
+    def segment(self, dims, rank, direction=2, workers=1, combine=False):
+        d = _dims(dims)
+        r = np.ascontiguousarray(rank, dtype=np.int64).ravel()
+        h = C.c_void_p()
+        self._check(self.lib.cap_segment(d, r, r.size, direction, workers, int(combine), C.byref(h)))
+        try:
+            out = {}
+            for i, name in enumerate(["desc", "asc", "maxima", "minima", "ms_region", "region_keys", "sweeps"]):
+                k = self.lib.cap_seg_size(h, i)
+                buf = np.empty(max(k, 1), np.int64)
+                self.lib.cap_seg_copy(h, i, buf.ctypes.data)
+                out[name] = buf[:k]
+            out["region_keys"] = out["region_keys"].reshape(-1, 2)
+            out["sweeps"] = int(out["sweeps"][0])
+            return out
+        finally:
+            self.lib.cap_seg_free(h)
+
+    def oracle_walk(self, dims, rank, v, direction):
+        r = np.ascontiguousarray(rank, dtype=np.int64).ravel()
+        out = C.c_int64()
+        self._check(self.lib.cap_oracle_walk(_dims(dims), r, r.size, v, direction, C.byref(out)))
+        return out.value
+
+    def tetra_code(self, labels4):
+        code = C.c_int32()
+        loc = np.zeros(4, np.int32)
+        self._check(self.lib.cap_tetra_code(np.ascontiguousarray(labels4, dtype=np.int64), C.byref(code),
+                                            loc.ctypes.data))
+        return code.value, loc
+
+    def triangle_code(self, labels3):
+        code = C.c_int32()
+        self._check(self.lib.cap_triangle_code(np.ascontiguousarray(labels3, dtype=np.int64), C.byref(code)))
+        return code.value
+
+    def tetra_case(self, code):
+        buf = np.zeros(12 * 5, np.uint8)
+        k = self.lib.cap_tetra_case(code, buf.ctypes.data)
+        return buf[: 5 * k].reshape(k, 5)
+
+    def triangle_case(self, code):
+        buf = np.zeros(3 * 4, np.uint8)
+        k = self.lib.cap_triangle_case(code, buf.ctypes.data)
+        return buf[: 4 * k].reshape(k, 4)
+
+    def _emit(self, dims, labels, kind, workers, region_filter, spacing, origin):
+        d = _dims(dims)
+        lab = np.ascontiguousarray(labels, dtype=np.int64).ravel()
+        h = C.c_void_p()
+        hf = 0 if region_filter is None else 1
+        flt = 0 if region_filter is None else int(region_filter)
+        self._check(self.lib.cap_emit(d, _vec3(spacing, (1, 1, 1)), _vec3(origin, (0, 0, 0)), lab, lab.size, kind,
+                                      workers, hf, flt, C.byref(h)))
+        try:
+            s = np.zeros(5, np.int64)
+            self.lib.cap_mesh_sizes(h, s)
+            nprim, npnt, ar, ncodes = (int(x) for x in s[:4])
+            pts = np.zeros(3 * max(npnt, 1), np.float64)
+            idx = np.zeros(ar * max(nprim, 1), np.int64)
+            reg = np.zeros(2 * max(nprim, 1), np.int64)
+            src = np.zeros(max(nprim, 1), np.int64)
+            codes = np.zeros(max(ncodes, 1), np.uint8)
+            self.lib.cap_mesh_copy(h, pts.ctypes.data, idx.ctypes.data, reg.ctypes.data, src.ctypes.data,
+                                   codes.ctypes.data)
+            return dict(points=pts[: 3 * npnt].reshape(npnt, 3), indices=idx[: ar * nprim],
+                        regions=reg[: 2 * nprim].reshape(nprim, 2), source_cells=src[:nprim], arity=ar,
+                        codes=codes[:ncodes], plan_total=int(s[4]))
+        finally:
+            self.lib.cap_mesh_free(h)
+
+    def emit_separators(self, dims, labels, workers=1, spacing=None, origin=None):
+        return self._emit(dims, labels, 0, workers, None, spacing, origin)
+
+    def emit_boundaries(self, dims, labels, region_filter=None, workers=1, spacing=None, origin=None):
+        return self._emit(dims, labels, 1, workers, region_filter, spacing, origin)
+
+    def run_benchmark(self, dims, values, workers, repeats=3, mode=2):
+        """Reference protocol (proj/src/bench.cpp:46-103), one worker count;
+        returns the trimmed-mean phase times in seconds."""
+        v = np.ascontiguousarray(values, dtype=np.float64).ravel()
+        out = np.zeros(5, np.float64)
+        self._check(self.lib.cap_run_benchmark(_dims(dims), v, workers, repeats, mode, out))
+        return dict(zip(["order", "segmentation", "combine", "index", "geometry"], out.tolist()))

@@ -1,0 +1,277 @@
+// ctypes-facing C wrapper around the reference PLMSS library — TEST
+// INFRASTRUCTURE ONLY (oracle). Never linked into the product library.
+//
+// It is compiled twice by oracle/Makefile:
+//   * with -Dplmss=plmss_ref against the UNMODIFIED reference sources under
+//     /root/reference/proj/src  -> oracle/_ref/libplmss_ref.so  (CPU oracle and
+//     the `bench.py --impl reference` arm);
+//   * with the reference's own complex/bench sources plus the GPU drop-in facade
+//     (paper_2303_15491_b200/csrc/dropin/) in place of orderfield/segmentation/
+//     marching -> build/libplmss_dropin_harness.so, so the very same calls run the
+//     reference API against the B200 implementation.
+//
+// Every entry point forwards to the reference public API declared in
+// proj/include/plmss/{orderfield,segmentation,marching,bench}.hpp and converts
+// C++ exceptions into (status, message): 1 invalid_argument, 2 logic_error,
+// 3 out_of_range, 4 other.
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "plmss/bench.hpp"
+#include "plmss/complex.hpp"
+#include "plmss/marching.hpp"
+#include "plmss/orderfield.hpp"
+#include "plmss/segmentation.hpp"
+
+namespace {
+
+thread_local std::string g_error;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const std::invalid_argument& e) {
+    g_error = e.what();
+    return 1;
+  } catch (const std::out_of_range& e) {
+    g_error = e.what();
+    return 3;
+  } catch (const std::logic_error& e) {
+    g_error = e.what();
+    return 2;
+  } catch (const std::exception& e) {
+    g_error = e.what();
+    return 4;
+  }
+}
+
+plmss::SimplicialComplex3 make_grid(const int64_t* dims, const double* spacing,
+                                    const double* origin) {
+  Eigen::Vector3d sp = spacing ? Eigen::Vector3d(spacing[0], spacing[1], spacing[2])
+                               : Eigen::Vector3d::Ones();
+  Eigen::Vector3d og = origin ? Eigen::Vector3d(origin[0], origin[1], origin[2])
+                              : Eigen::Vector3d::Zero();
+  return plmss::SimplicialComplex3::implicit_grid({dims[0], dims[1], dims[2]}, sp, og);
+}
+
+plmss::OrderField order_from(const int64_t* rank, int64_t n) {
+  plmss::OrderField o;
+  o.rank.assign(rank, rank + n);
+  return o;
+}
+
+struct MeshOut {
+  plmss::SeparatingMesh mesh;
+  plmss::EmitPlan plan;
+  std::vector<std::uint8_t> codes;
+};
+
+}  // namespace
+
+extern "C" {
+
+const char* cap_last_error() { return g_error.c_str(); }
+
+int cap_compute_order(const double* values, int64_t n, int64_t* rank_out) {
+  return guarded([&] {
+    plmss::ScalarField f;
+    f.values.resize(n);
+    for (int64_t i = 0; i < n; ++i) f.values[i] = values[i];
+    const plmss::OrderField o = plmss::compute_order(f);
+    std::memcpy(rank_out, o.rank.data(), sizeof(int64_t) * static_cast<size_t>(n));
+  });
+}
+
+// direction: 0 ascending, 1 descending, 2 both (plmss::Direction order).
+int cap_segment(const int64_t* dims, const int64_t* rank, int64_t n, int direction,
+                int workers, int do_combine, void** handle) {
+  return guarded([&] {
+    const auto grid = make_grid(dims, nullptr, nullptr);
+    auto* seg = new plmss::SegmentationResult(plmss::segment(
+        grid, order_from(rank, n), static_cast<plmss::Direction>(direction), workers));
+    if (do_combine) {
+      try {
+        plmss::combine_ms(*seg, workers);
+      } catch (...) {
+        delete seg;
+        throw;
+      }
+    }
+    *handle = seg;
+  });
+}
+
+// which: 0 desc, 1 asc, 2 maxima, 3 minima, 4 ms_region, 5 region_keys (2 x u64
+// per key: min then max), 6 sweeps (1 value).
+int64_t cap_seg_size(void* handle, int which) {
+  auto* s = static_cast<plmss::SegmentationResult*>(handle);
+  switch (which) {
+    case 0: return static_cast<int64_t>(s->desc.size());
+    case 1: return static_cast<int64_t>(s->asc.size());
+    case 2: return static_cast<int64_t>(s->maxima.size());
+    case 3: return static_cast<int64_t>(s->minima.size());
+    case 4: return static_cast<int64_t>(s->ms_region.size());
+    case 5: return static_cast<int64_t>(s->region_keys.size()) * 2;
+    case 6: return 1;
+  }
+  return -1;
+}
+
+void cap_seg_copy(void* handle, int which, int64_t* out) {
+  auto* s = static_cast<plmss::SegmentationResult*>(handle);
+  auto cp = [&](const std::vector<int64_t>& v) {
+    if (!v.empty()) std::memcpy(out, v.data(), sizeof(int64_t) * v.size());
+  };
+  switch (which) {
+    case 0: cp(s->desc); break;
+    case 1: cp(s->asc); break;
+    case 2: cp(s->maxima); break;
+    case 3: cp(s->minima); break;
+    case 4: cp(s->ms_region); break;
+    case 5:
+      for (size_t i = 0; i < s->region_keys.size(); ++i) {
+        out[2 * i] = plmss::ms_key_min(s->region_keys[i]);
+        out[2 * i + 1] = plmss::ms_key_max(s->region_keys[i]);
+      }
+      break;
+    case 6: out[0] = s->sweeps; break;
+  }
+}
+
+void cap_seg_free(void* handle) { delete static_cast<plmss::SegmentationResult*>(handle); }
+
+int cap_oracle_walk(const int64_t* dims, const int64_t* rank, int64_t n, int64_t v,
+                    int direction, int64_t* out) {
+  return guarded([&] {
+    const auto grid = make_grid(dims, nullptr, nullptr);
+    *out = plmss::oracle_integral_walk(grid, order_from(rank, n), v,
+                                       static_cast<plmss::Direction>(direction));
+  });
+}
+
+int cap_tetra_code(const int64_t* labels4, int32_t* code, int32_t* local4) {
+  return guarded([&] {
+    const auto c = plmss::tetra_code({labels4[0], labels4[1], labels4[2], labels4[3]});
+    *code = c.code;
+    for (int i = 0; i < 4; ++i) local4[i] = c.local[i];
+  });
+}
+
+int cap_triangle_code(const int64_t* labels3, int32_t* code) {
+  return guarded([&] { *code = plmss::triangle_code({labels3[0], labels3[1], labels3[2]}).code; });
+}
+
+// Table rows for a tetra code as 5 bytes each (p0,p1,p2,pairA,pairB). Returns count.
+int cap_tetra_case(int code, uint8_t* out) {
+  const auto rows = plmss::tables::tetra_case(static_cast<std::uint8_t>(code));
+  int i = 0;
+  for (const auto& r : rows) {
+    out[5 * i + 0] = r.p[0];
+    out[5 * i + 1] = r.p[1];
+    out[5 * i + 2] = r.p[2];
+    out[5 * i + 3] = r.pairA;
+    out[5 * i + 4] = r.pairB;
+    ++i;
+  }
+  return i;
+}
+
+int cap_triangle_case(int code, uint8_t* out) {
+  const auto rows = plmss::tables::triangle_case(static_cast<std::uint8_t>(code));
+  int i = 0;
+  for (const auto& r : rows) {
+    out[4 * i + 0] = r.p[0];
+    out[4 * i + 1] = r.p[1];
+    out[4 * i + 2] = r.pairA;
+    out[4 * i + 3] = r.pairB;
+    ++i;
+  }
+  return i;
+}
+
+// kind: 0 separators (index_separators + emit_geometry), 1 boundaries.
+int cap_emit(const int64_t* dims, const double* spacing, const double* origin,
+             const int64_t* labels, int64_t n, int kind, int workers, int has_filter,
+             int64_t filter, void** handle) {
+  return guarded([&] {
+    const auto grid = make_grid(dims, spacing, origin);
+    std::span<const plmss::Label> lab(labels, static_cast<size_t>(n));
+    auto* out = new MeshOut();
+    try {
+      if (kind == 0) {
+        plmss::SeparatorIndex index = plmss::index_separators(grid, lab, workers);
+        out->mesh = plmss::emit_geometry(grid, lab, index);
+        out->plan = index.plan;
+        out->codes = index.codes;
+      } else {
+        std::optional<plmss::Label> f;
+        if (has_filter) f = filter;
+        out->mesh = plmss::emit_boundaries(grid, lab, f, workers);
+      }
+    } catch (...) {
+      delete out;
+      throw;
+    }
+    *handle = out;
+  });
+}
+
+// sizes: [n_primitives, n_points, verts_per_primitive, n_codes, plan_total]
+void cap_mesh_sizes(void* handle, int64_t* sizes) {
+  auto* m = static_cast<MeshOut*>(handle);
+  sizes[0] = m->mesh.num_primitives();
+  sizes[1] = m->mesh.num_points();
+  sizes[2] = m->mesh.verts_per_primitive;
+  sizes[3] = static_cast<int64_t>(m->codes.size());
+  sizes[4] = m->plan.total();
+}
+
+void cap_mesh_copy(void* handle, double* points, int64_t* indices, int64_t* regions,
+                   int64_t* source_cells, uint8_t* codes) {
+  auto* m = static_cast<MeshOut*>(handle);
+  const auto& mesh = m->mesh;
+  if (points && mesh.num_points() > 0)
+    std::memcpy(points, mesh.points.data(), sizeof(double) * 3 * static_cast<size_t>(mesh.num_points()));
+  if (indices && !mesh.indices.empty())
+    std::memcpy(indices, mesh.indices.data(), sizeof(int64_t) * mesh.indices.size());
+  if (regions)
+    for (size_t i = 0; i < mesh.regions.size(); ++i) {
+      regions[2 * i] = mesh.regions[i][0];
+      regions[2 * i + 1] = mesh.regions[i][1];
+    }
+  if (source_cells && !mesh.source_cells.empty())
+    std::memcpy(source_cells, mesh.source_cells.data(), sizeof(int64_t) * mesh.source_cells.size());
+  if (codes && !m->codes.empty()) std::memcpy(codes, m->codes.data(), m->codes.size());
+}
+
+void cap_mesh_free(void* handle) { delete static_cast<MeshOut*>(handle); }
+
+// Runs the reference benchmark protocol (proj/src/bench.cpp:46-103) on one
+// worker count; phases_out = trimmed-mean [order, seg, combine, index, geometry].
+int cap_run_benchmark(const int64_t* dims, const double* values, int workers, int repeats,
+                      int mode, double* phases_out) {
+  return guarded([&] {
+    const auto grid = make_grid(dims, nullptr, nullptr);
+    plmss::ScalarField f;
+    const int64_t n = dims[0] * dims[1] * dims[2];
+    f.values.resize(n);
+    for (int64_t i = 0; i < n; ++i) f.values[i] = values[i];
+    const auto rep = plmss::run_benchmark(grid, f, {workers}, repeats, "cap",
+                                          static_cast<plmss::SegMode>(mode));
+    const auto& m = rep.rows.front().mean;
+    phases_out[0] = m.order;
+    phases_out[1] = m.segmentation;
+    phases_out[2] = m.combine;
+    phases_out[3] = m.index;
+    phases_out[4] = m.geometry;
+  });
+}
+
+}  // extern "C"
