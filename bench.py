@@ -1,0 +1,360 @@
+#!/usr/bin/env python
+"""Benchmark: full Morse-Smale segmentation throughput (Gvertices/s) on B200.
+
+One step = one pass of the hot path over one synthetic volume: f32 field in
+HBM -> desc/asc labels, sorted extrema, dense MS ids + region table, MS
+separator records (run_benchmark's MorseSmale pass, proj/src/bench.cpp:66-87,
+minus the order-field sort the B200 path does not need).
+
+Workload: BASELINE.json configs[4] (cfg5, 1024^3 Gaussian sum) — the config
+the north-star roofline target is quoted on; it fits one GPU. The field is
+generated on the device (seeded, csrc/synth.cu).
+
+Arms:
+  default            : this repo's B200 path (libplmss_b200.so).
+  --impl reference   : the reference CPU implementation (oracle/_ref, the
+                       reference sources compiled unchanged) on the host's
+                       cores, one bounded z-slab sample of the same field per
+                       step. Rank 0 only under torchrun.
+
+Prints ONE JSON line (rank 0).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Gvertices/s full MS segmentation (1/2/4/8 B200) & % of HBM roofline"
+UNIT = "Gvertices/s"
+# Algorithmic bytes: 16 B per vertex (read f, write asc,
+# desc, ms_region as u32) + 16 B per emitted separator triangle.
+B_PER_VERTEX = 16
+B_PER_TRI = 16
+# Per-stage algorithmic bytes per vertex.
+STAGES = ["hops", "compress", "extrema", "combine", "marching"]
+STAGE_BYTES_PER_VERTEX = {"hops": 12, "compress": 16, "extrema": 8, "combine": 12, "marching": 4}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = float(parts[1])
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[3:7]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_setup():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def cpu_sample(cfg, field_host_fn, target_vertices):
+    """A bounded sample of the workload: the first k z-layers of the field."""
+    X, Y, Z = cfg.dims
+    k = max(2, min(Z, target_vertices // (X * Y)))
+    return (X, Y, k), field_host_fn(k)
+
+
+def run_reference_arm(args, rank, world):
+    import oracle
+    from paper_2303_15491_b200.configs import CONFIGS
+
+    if rank != 0:
+        return 0
+    cfg = CONFIGS[args.config]
+    ref = oracle.Reference()
+    cores = os.cpu_count() or 1
+    dims, f = reference_sample(cfg, args.ref_sample)
+    nv = int(np.prod(dims))
+    for _ in range(args.warmup):
+        ref.run_once(dims, f, cores)
+    times = []
+    phases_acc = np.zeros(5)
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        ph, regions, prims = ref.run_once(dims, f, cores)
+        times.append(time.perf_counter() - t0)
+        phases_acc += np.array(list(ph.values()))
+    t = float(np.mean(times))
+    value = nv / t / 1e9
+    sample = (f"z-slab {dims[0]}x{dims[1]}x{dims[2]} ({nv} vertices) of {cfg.name}; reference run_benchmark pass "
+              f"(compute_order+segment+combine_ms+index+geometry, MorseSmale) per step")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64/int64", "data": "synthetic",
+        "config": {"workload": cfg.name, "dims": list(cfg.dims), "sample_dims": list(dims)},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "phases_s": dict(zip(["order", "segmentation", "combine", "index", "geometry"],
+                             (phases_acc / max(args.steps, 1)).round(4).tolist())),
+        "regions": regions, "primitives": prims,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def reference_sample(cfg, target):
+    """Host copy of the first k z-layers of the configured field (generated on
+    the GPU when one is present, else on the host at the sample size)."""
+    from paper_2303_15491_b200.configs import Config, host_field
+
+    X, Y, Z = cfg.dims
+    k = max(2, min(Z, target // (X * Y)))
+    dims = (X, Y, k)
+    try:
+        import torch
+
+        if torch.cuda.is_available():
+            import paper_2303_15491_b200 as P
+
+            f = P.synth_field(cfg.dims if k == Z else dims, kind=cfg.kind, gaussians=cfg.gaussians()
+                              if cfg.kind == "gaussians" else None, noise_amp=cfg.noise, seed=cfg.seed,
+                              levels=cfg.levels)
+            return dims, f[: X * Y * k].cpu().numpy()
+    except Exception:
+        pass
+    sub = Config(cfg.name, dims, cfg.kind, cfg.n_gauss, cfg.sigma, cfg.noise, cfg.levels, cfg.seed)
+    return dims, host_field(sub)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="cfg5")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-sample", type=int, default=1 << 23, help="vertices in the CPU-baseline sample")
+    ap.add_argument("--ref-sample", type=int, default=1 << 23, help="vertices per --impl reference step")
+    args = ap.parse_args()
+    rank, world, local = dist_setup()
+
+    if args.impl == "reference":
+        return run_reference_arm(args, rank, world)
+
+    import torch
+
+    import paper_2303_15491_b200 as P
+    from paper_2303_15491_b200.configs import CONFIGS
+
+    torch.cuda.set_device(local)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl")
+        pg = dist
+    cfg = CONFIGS[args.config]
+    ctx = P.Context(local)
+    stream = ctx.stream
+    dims = cfg.dims
+    nv = cfg.n
+    field = P.synth_field(dims, kind=cfg.kind, gaussians=cfg.gaussians() if cfg.kind == "gaussians" else None,
+                          noise_amp=cfg.noise, seed=cfg.seed, levels=cfg.levels, ctx=ctx)
+    torch.cuda.synchronize()
+
+    for _ in range(max(args.warmup, 0)):
+        P.pipeline(dims, field, ctx=ctx)
+    torch.cuda.synchronize()
+
+    ctx.set_timing(True)
+    stage_ms = np.zeros(8)
+    launches0 = P.api.launch_count()
+    clocks = Clocks(local)
+    clocks.start()
+    time.sleep(0.3)
+    if pg:
+        pg.barrier()
+    torch.cuda.synchronize()
+    start = torch.cuda.Event(enable_timing=True)
+    stop = torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        start.record(stream)
+        res = None
+        for _ in range(args.steps):
+            res = P.pipeline(dims, field, ctx=ctx)
+            stage_ms += ctx.stage_ms()
+        stop.record(stream)
+    torch.cuda.synchronize()
+    if pg:
+        pg.barrier()
+    clk = clocks.stop()
+    launches = P.api.launch_count() - launches0
+    ctx.set_timing(False)
+    ms = start.elapsed_time(stop) / args.steps
+    if pg:
+        t = torch.tensor([ms], device="cuda")
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        ms = float(t.item())
+    value = world * nv / (ms * 1e-3) / 1e9
+
+    peak, peak_src = peaks()
+    n_tris = res.n_tris
+    b_alg = B_PER_VERTEX * nv + B_PER_TRI * n_tris
+    stage_ms /= args.steps
+    stage = {STAGES[i]: round(float(stage_ms[i]), 4) for i in range(5)}
+    dom = max(STAGES, key=lambda s: stage[s])
+    dom_bytes = STAGE_BYTES_PER_VERTEX[dom] * nv + (B_PER_TRI * n_tris if dom == "marching" else 0)
+    dom_gbs = dom_bytes / (stage[dom] * 1e-3) / 1e9
+    pipe_gbs = b_alg / (ms * 1e-3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get(dom)
+
+    # ---- end to end through the C-ABI over pinned host buffers -----------
+    e2e = None
+    if not args.no_e2e:
+        h_field = torch.empty(nv, dtype=torch.float32, pin_memory=True)
+        h_field.copy_(field.cpu())
+        bufs = {k: torch.empty(nv, dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
+                for k in ("desc", "asc", "ms")}
+        bufs["maxima"] = torch.empty(max(res.n_maxima, 1), dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
+        bufs["minima"] = torch.empty(max(res.n_minima, 1), dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
+        bufs["region_keys"] = torch.empty(max(res.n_regions, 1), dtype=torch.int64,
+                                          pin_memory=True).numpy().view(np.uint64)
+        bufs["tris"] = torch.empty((max(n_tris, 1), 2), dtype=torch.int64, pin_memory=True).numpy().view(np.uint64)
+        hf = h_field.numpy()
+        P.pipeline_host(dims, hf, ctx=ctx, out_buffers=bufs)  # warm
+        torch.cuda.synchronize()
+        if pg:
+            pg.barrier()
+        e_start = torch.cuda.Event(enable_timing=True)
+        e_stop = torch.cuda.Event(enable_timing=True)
+        e_start.record(stream)
+        for _ in range(args.e2e_steps):
+            r2, _ = P.pipeline_host(dims, hf, ctx=ctx, out_buffers=bufs)
+        e_stop.record(stream)
+        torch.cuda.synchronize()
+        e_ms = e_start.elapsed_time(e_stop) / args.e2e_steps
+        if pg:
+            t = torch.tensor([e_ms], device="cuda")
+            pg.all_reduce(t, op=pg.ReduceOp.MAX)
+            e_ms = float(t.item())
+        d2h = 3 * 4 * nv + 4 * (r2.n_maxima + r2.n_minima) + 8 * r2.n_regions + 16 * r2.n_tris
+        e2e = {"value": world * nv / (e_ms * 1e-3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": 4 * nv,
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": round(e_ms, 3)}
+
+    cpu = None
+    if not args.no_cpu_baseline and rank == 0:
+        try:
+            import oracle
+
+            ref = oracle.Reference()
+            X, Y, Z = dims
+            k = max(2, min(Z, args.cpu_sample // (X * Y)))
+            fs = field[: X * Y * k].cpu().numpy()
+            cores = os.cpu_count() or 1
+            ts = []
+            for _ in range(3):
+                t0 = time.perf_counter()
+                ref.run_once((X, Y, k), fs, cores)
+                ts.append(time.perf_counter() - t0)
+            ts.sort()
+            tcpu = ts[1]  # drop best and worst (bench.cpp:22-44)
+            cpu = {"value": X * Y * k / tcpu / 1e9, "unit": UNIT, "cores": cores, "kind": "reference",
+                   "sample": f"z-slab {X}x{Y}x{k} of {cfg.name}, reference pipeline pass (compute_order, segment, "
+                             f"combine_ms, index_separators, emit_geometry; MorseSmale), median of 3 runs"}
+        except Exception as e:  # reported, never fatal
+            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic",
+        "config": {"workload": cfg.name, "dims": list(dims), "input": "float32 field resident in HBM",
+                   "l2": "inputs larger than L2 (4 GiB field vs 126 MB L2)",
+                   "parallelism": f"replica x{world}" if world > 1 else "1 GPU",
+                   "vertices": nv, "triangles": n_tris, "regions": res.n_regions, "maxima": res.n_maxima,
+                   "minima": res.n_minima, "sweeps": res.sweeps},
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(dom_gbs, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(dom_gbs / peak, 4), "traffic": traffic, "peak_source": peak_src,
+                     "alg_bytes": dom_bytes},
+        "roofline_pipeline": {"bound": "hbm", "achieved": round(pipe_gbs, 1), "peak": peak, "unit": "GB/s",
+                              "frac": round(pipe_gbs / peak, 4), "alg_bytes": b_alg},
+        "stage_ms": stage,
+        "clocks": clk,
+        "gpu_launches": launches,
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if pg:
+        pg.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,216 @@
+/* plmss_b200 — B200-native (sm_100a) PL Morse-Smale segmentation hot path.
+ *
+ * C-ABI drop-in boundary. Plain pointers, sizes and status codes; no C++ or
+ * torch types cross it. Each entry point names the reference interface it
+ * replaces (paths relative to the reference repo, proj/include/plmss/...).
+ * The C++ facade (paper_2303_15491_b200/csrc/dropin/plmss_dropin.cpp) maps
+ * these back onto the reference's own C++ signatures and exception types.
+ *
+ * Conventions
+ *  - dims = {X, Y, Z}; vertex id v = x + X*(y + Y*z) (x fastest), as
+ *    SimplicialComplex3::implicit_grid (complex.hpp:52-55, complex.cpp:91-126).
+ *    Only 3-D grids (all dims >= 2) with X*Y*Z < 2^32 are accepted.
+ *  - Device pointers are prefixed d_, host pointers h_. All device work is
+ *    issued on the context's stream; functions return after the work that
+ *    produces host-visible scalars (counts) has completed.
+ *  - Vertex ids, extremum labels and dense region ids are uint32 on device;
+ *    the reference's int64 VertexId/Label (types.hpp:9-16) are widened by the
+ *    facade.
+ *  - Status: PLMSS_OK, or an error whose text plmss_b200_last_error() returns
+ *    (thread-local). Error classes mirror the reference exceptions:
+ *    INVALID_ARGUMENT <-> std::invalid_argument, LOGIC <-> std::logic_error,
+ *    OUT_OF_RANGE <-> std::out_of_range.
+ *  - There is no CPU fallback: without a CUDA device every call fails with
+ *    PLMSS_ERR_CUDA.
+ */
+#ifndef PLMSS_B200_H
+#define PLMSS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum plmss_status {
+  PLMSS_OK = 0,
+  PLMSS_ERR_INVALID_ARGUMENT = 1,
+  PLMSS_ERR_LOGIC = 2,
+  PLMSS_ERR_OUT_OF_RANGE = 3,
+  PLMSS_ERR_CUDA = 4,
+  PLMSS_ERR_NOMEM = 5
+};
+
+/* Scalar key types accepted by segmentation. */
+enum plmss_key_type {
+  PLMSS_KEY_F32 = 0,  /* float values, compared as (value, id)            */
+  PLMSS_KEY_F64 = 1,  /* double values, compared as (value, id)           */
+  PLMSS_KEY_RANK = 2  /* int64 OrderField ranks (orderfield.hpp:23-30)    */
+};
+
+/* plmss::Direction (segmentation.hpp:14). */
+enum plmss_direction { PLMSS_ASCENDING = 0, PLMSS_DESCENDING = 1, PLMSS_BOTH = 2 };
+
+/* Compact separator record (16 B), written in the reference's output order:
+ * cell-major, then table row (marching.cpp:136-206, F7 in SURVEY.md).
+ *   cell_row = cell_id << 6 | row, row in [0, 52) indexes the recipe table
+ *              of marching_tables.cpp:48-116 regrouped by ascending code
+ *              (plmss_b200_tet_table() exports it);
+ *   lo, hi   = sorted region pair (marching.cpp:84-90).
+ * plmss_b200_materialize_separators() expands it to the reference layout. */
+typedef struct plmss_tri {
+  uint64_t cell_row;
+  uint32_t lo, hi;
+} plmss_tri;
+
+/* Same record for int64 label fields (API path with arbitrary labels). */
+typedef struct plmss_tri64 {
+  uint64_t cell_row;
+  int64_t lo, hi;
+} plmss_tri64;
+
+typedef struct plmss_ctx plmss_ctx;
+
+/* Host copy of the device recipe table: rows[52] packed as
+ * p0 | p1<<4 | p2<<8 | pairA<<12 | pairB<<14, cases[32] = first_row<<4 | count.
+ * Needs no GPU (used by the CPU tests to pin the table to the reference). */
+void plmss_b200_tet_table(uint32_t rows[52], uint16_t cases[32]);
+
+const char* plmss_b200_last_error(void);
+/* Library version string and the SM architecture it was compiled for. */
+const char* plmss_b200_version(void);
+/* Total kernel launches issued by this library so far (all contexts). */
+unsigned long long plmss_b200_launch_count(void);
+
+/* Context = device + stream + grow-only scratch arena. stream may be NULL
+ * (the context then creates its own non-blocking stream). */
+int plmss_b200_ctx_create(int device, void* stream, plmss_ctx** out);
+void plmss_b200_ctx_destroy(plmss_ctx* ctx);
+/* Bytes of device scratch currently held by the context. */
+size_t plmss_b200_ctx_scratch_bytes(const plmss_ctx* ctx);
+/* Device time (ms) of the last kernel stage named by `stage` (see
+ * plmss_b200_pipeline): 0 hops, 1 compress, 2 extrema, 3 combine, 4 marching.
+ * Only filled when timing is enabled. */
+int plmss_b200_ctx_set_timing(plmss_ctx* ctx, int enable);
+int plmss_b200_ctx_stage_ms(const plmss_ctx* ctx, float out[8]);
+
+/* ---- order field --------------------------------------------------------
+ * Replaces compute_order (orderfield.hpp:35, orderfield.cpp:12-32): d_rank[v]
+ * = position of v in the sort by (value, id). Fails with INVALID_ARGUMENT
+ * "non-finite scalar value at vertex i" (lowest i). key_type F32 or F64. */
+int plmss_b200_compute_order(plmss_ctx* ctx, int key_type, const void* d_values, int64_t n,
+                             int64_t* d_rank);
+
+/* ---- segmentation -------------------------------------------------------
+ * Replaces segment() (segmentation.hpp:74-76, segmentation.cpp:109-168):
+ * steepest-neighbour hops over the 14-neighbour Freudenthal stencil with
+ * (key, id) simulation of simplicity, then path compression to the fixpoint.
+ * d_desc / d_asc (N each) may be NULL when the direction does not ask for
+ * them. d_maxima / d_minima receive the extrema ascending (capacity N) and
+ * may be NULL; counts go to *n_maxima / *n_minima. *sweeps = compression
+ * sweeps (schedule-dependent, not part of parity). */
+int plmss_b200_segment(plmss_ctx* ctx, const int64_t dims[3], int key_type, const void* d_keys,
+                       int direction, uint32_t* d_desc, uint32_t* d_asc, uint32_t* d_maxima,
+                       uint32_t* d_minima, int64_t* n_maxima, int64_t* n_minima, int32_t* sweeps);
+
+/* Step 1 only (detail::seed_hops_both, segmentation.cpp:60-85): hop targets. */
+int plmss_b200_seed_hops(plmss_ctx* ctx, const int64_t dims[3], int key_type, const void* d_keys,
+                         uint32_t* d_desc, uint32_t* d_asc);
+
+/* ---- Morse-Smale combine ------------------------------------------------
+ * Replaces combine_ms (segmentation.hpp:80, segmentation.cpp:170-196):
+ * d_ms[v] = rank of (asc[v], desc[v]) among the distinct pairs in
+ * lexicographic order; d_region_keys[r] = asc << 32 | desc of region r
+ * (the reference's MsKey = min << 64 | max, segmentation.hpp:21-24, narrowed
+ * to u32 halves). d_region_keys capacity: N. */
+int plmss_b200_combine_ms(plmss_ctx* ctx, int64_t n, const uint32_t* d_asc, const uint32_t* d_desc,
+                          uint32_t* d_ms, uint64_t* d_region_keys, int64_t* n_regions);
+
+/* ---- marching tetrahedra ------------------------------------------------
+ * label_type: 0 = uint32 labels, 1 = int64 labels.
+ * index_separators (marching.hpp:101-102, marching.cpp:104-134): per-cell
+ * codes (d_codes, 6(X-1)(Y-1)(Z-1) bytes, may be NULL) and the total. */
+int plmss_b200_index_separators(plmss_ctx* ctx, const int64_t dims[3], int label_type,
+                                const void* d_labels, uint8_t* d_codes, int64_t* total);
+
+/* emit_separators (marching.hpp:115-117, marching.cpp:136-215): compact
+ * records in reference order. d_out has room for `capacity` records
+ * (plmss_tri for label_type 0, plmss_tri64 for 1); *total is always set; if
+ * total > capacity nothing is written and PLMSS_ERR_LOGIC is returned. */
+int plmss_b200_emit_separators(plmss_ctx* ctx, const int64_t dims[3], int label_type,
+                               const void* d_labels, void* d_out, int64_t capacity,
+                               int64_t* total);
+
+/* Expand records to the reference SeparatingMesh layout (marching.hpp:65-76):
+ * d_points 9 doubles per triangle (3 corners x xyz, Eigen column-major),
+ * d_regions 2 int64, d_source_cells 1 int64 (any may be NULL). Points follow
+ * recipe_point (marching.cpp:71-82) bit for bit: ascending-corner sum from
+ * +0.0 of origin + spacing*coord, divided by the corner count. */
+int plmss_b200_materialize_separators(plmss_ctx* ctx, const int64_t dims[3], const double spacing[3],
+                                      const double origin[3], int label_type, const void* d_tris,
+                                      int64_t n, double* d_points, int64_t* d_regions,
+                                      int64_t* d_source_cells);
+
+/* emit_boundaries (marching.hpp:123-126, marching.cpp:236-326): faces whose
+ * 3 vertices share a label that the 4th tet vertex lacks, one per face
+ * (lowest generating cell), in (v0, v1, v2) order. Two calls: with
+ * d_faces == NULL only *n_faces / *n_points are computed. Outputs: d_faces
+ * 3 uint32 vertex ids per face, d_tags (label_type width), d_cells int64,
+ * d_points 3 doubles per sorted unique used vertex, d_indices 3 int64 per
+ * face. */
+int plmss_b200_emit_boundaries(plmss_ctx* ctx, const int64_t dims[3], const double spacing[3],
+                               const double origin[3], int label_type, const void* d_labels,
+                               int has_filter, int64_t filter, uint32_t* d_faces, void* d_tags,
+                               int64_t* d_cells, double* d_points, int64_t* d_indices,
+                               int64_t* n_faces, int64_t* n_points);
+
+/* ---- fused full pipeline (the benchmarked path) --------------------------
+ * run_benchmark's MorseSmale pass (bench.cpp:66-87) minus compute_order:
+ * f32 field -> desc, asc, maxima, minima, ms_region, region_keys, separator
+ * records. Outputs live in the context until the next call; fetch with
+ * plmss_b200_result(). */
+typedef struct plmss_result {
+  const uint32_t* d_desc;
+  const uint32_t* d_asc;
+  const uint32_t* d_ms;
+  const uint32_t* d_maxima;
+  const uint32_t* d_minima;
+  const uint64_t* d_region_keys;
+  const plmss_tri* d_tris;
+  int64_t n_vertices, n_maxima, n_minima, n_regions, n_tris;
+  int32_t sweeps;
+} plmss_result;
+
+int plmss_b200_pipeline(plmss_ctx* ctx, const int64_t dims[3], const float* d_field);
+int plmss_b200_result(const plmss_ctx* ctx, plmss_result* out);
+/* Copies `bytes` from a device pointer (e.g. a plmss_result array) to dst
+ * (host when to_host != 0, else device) on the context stream, then syncs. */
+int plmss_b200_copy(plmss_ctx* ctx, void* dst, const void* d_src, int64_t bytes, int to_host);
+
+/* Tuning / test options: PLMSS_OPT_COMBINE_PATH 0 auto, 1 bitmap, 2 hash. */
+enum plmss_option { PLMSS_OPT_COMBINE_PATH = 1 };
+int plmss_b200_ctx_set_option(plmss_ctx* ctx, int option, int64_t value);
+
+/* End-to-end variant over HOST buffers: pinned or pageable h_field in; the
+ * label arrays (N each, any may be NULL), extrema, region keys and separator
+ * records are copied back to host buffers of the given capacities (counts are
+ * always reported in *out). */
+int plmss_b200_pipeline_host(plmss_ctx* ctx, const int64_t dims[3], const float* h_field,
+                             uint32_t* h_desc, uint32_t* h_asc, uint32_t* h_ms,
+                             uint32_t* h_maxima, uint32_t* h_minima, uint64_t* h_region_keys,
+                             plmss_tri* h_tris, int64_t tri_capacity, plmss_result* out);
+
+/* ---- synthetic inputs (benchmark/test harness utility) -------------------
+ * value(x,y,z) = sum_k amp_k * exp(-|p - c_k|^2 / (2 sigma_k^2)) + noise_amp *
+ * u(seed, v), u uniform in [-1, 1) from a splitmix64 hash of (seed, v);
+ * kind 1 = i.i.d. uniform [0, 1) from the same hash (no Gaussians);
+ * levels > 0 quantises to that many levels over [min, max].
+ * gaussians: n_gauss x 5 doubles (cx, cy, cz, sigma, amp). */
+int plmss_b200_synth(plmss_ctx* ctx, const int64_t dims[3], int kind, const double* h_gaussians,
+                     int n_gauss, double noise_amp, uint64_t seed, int levels, float* d_field);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PLMSS_B200_H */

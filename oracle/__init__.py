@@ -237,6 +237,18 @@ class Reference:
         L.cap_mesh_copy.argtypes = [C.c_void_p] + [C.c_void_p] * 5
         L.cap_mesh_free.argtypes = [C.c_void_p]
         L.cap_run_benchmark.argtypes = [_i64p, _f64p, C.c_int, C.c_int, C.c_int, _f64p]
+        L.cap_run_once.argtypes = [_i64p, np.ctypeslib.ndpointer(np.float32, flags="C_CONTIGUOUS"), C.c_int,
+                                   C.c_int, _f64p, _i64p]
+
+    def run_once(self, dims, values_f32, workers, mode=2):
+        """One reference pipeline pass (bench.cpp:62-87); returns (phase
+        seconds dict, regions, primitives)."""
+        v = np.ascontiguousarray(values_f32, dtype=np.float32).ravel()
+        ph = np.zeros(5, np.float64)
+        cnt = np.zeros(2, np.int64)
+        self._check(self.lib.cap_run_once(_dims(dims), v, workers, mode, ph, cnt))
+        return dict(zip(["order", "segmentation", "combine", "index", "geometry"], ph.tolist())), int(cnt[0]), \
+            int(cnt[1])
 
     def _check(self, st):
         if st != 0:

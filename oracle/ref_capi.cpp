@@ -14,6 +14,7 @@
 // proj/include/plmss/{orderfield,segmentation,marching,bench}.hpp and converts
 // C++ exceptions into (status, message): 1 invalid_argument, 2 logic_error,
 // 3 out_of_range, 4 other.
+#include <chrono>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -271,6 +272,44 @@ int cap_run_benchmark(const int64_t* dims, const double* values, int workers, in
     phases_out[2] = m.combine;
     phases_out[3] = m.index;
     phases_out[4] = m.geometry;
+  });
+}
+
+// One pass of the benchmarked pipeline exactly as run_benchmark's inner loop
+// (proj/src/bench.cpp:62-87): compute_order, segment(Both), combine_ms,
+// select_labels(mode), index_separators + emit_geometry per field. Phase
+// wall times (s) go to phases_out[5]; counts_out = [regions, primitives].
+int cap_run_once(const int64_t* dims, const float* values, int workers, int mode, double* phases_out,
+                 int64_t* counts_out) {
+  return guarded([&] {
+    using clk = std::chrono::steady_clock;
+    auto secs = [](clk::time_point a) { return std::chrono::duration<double>(clk::now() - a).count(); };
+    const auto grid = make_grid(dims, nullptr, nullptr);
+    plmss::ScalarField f;
+    const int64_t n = dims[0] * dims[1] * dims[2];
+    f.values.resize(n);
+    for (int64_t i = 0; i < n; ++i) f.values[i] = values[i];
+    auto mark = clk::now();
+    const plmss::OrderField order = plmss::compute_order(f);
+    phases_out[0] = secs(mark);
+    mark = clk::now();
+    plmss::SegmentationResult seg = plmss::segment(grid, order, plmss::Direction::Both, workers);
+    phases_out[1] = secs(mark);
+    mark = clk::now();
+    plmss::combine_ms(seg, workers);
+    phases_out[2] = secs(mark);
+    phases_out[3] = phases_out[4] = 0;
+    int64_t prims = 0;
+    for (const auto& labels : plmss::select_labels(seg, static_cast<plmss::SegMode>(mode))) {
+      mark = clk::now();
+      plmss::SeparatorIndex index = plmss::index_separators(grid, labels, workers);
+      phases_out[3] += secs(mark);
+      mark = clk::now();
+      prims += plmss::emit_geometry(grid, labels, index).num_primitives();
+      phases_out[4] += secs(mark);
+    }
+    counts_out[0] = seg.num_regions();
+    counts_out[1] = prims;
   });
 }
 

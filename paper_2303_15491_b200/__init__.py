@@ -1,0 +1,14 @@
+"""plmss_b200 — B200-native (sm_100a) PL Morse-Smale segmentation hot path.
+
+Drop-in for the PLMSS reference's segmentation path (arXiv 2303.15491):
+steepest ascent/descent over the 14-neighbour Freudenthal grid with
+simulation of simplicity, path compression, Morse-Smale dense ids and
+multi-label marching tetrahedra. The compute runs in hand-written CUDA
+kernels (csrc/, libplmss_b200.so) behind the C-ABI of include/plmss_b200.h;
+this package is the Python mirror of the reference interface on top of it.
+"""
+from .api import (  # noqa: F401
+    ASCENDING, BOTH, DESCENDING, Context, SegmentationResult, combine_ms, compute_order, default_context,
+    emit_boundaries, emit_separators, fetch, index_separators, lib, materialize_separators, pipeline, pipeline_host,
+    result, seed_hops, segment, select_labels, synth_field, tet_table,
+)

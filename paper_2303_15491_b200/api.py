@@ -1,0 +1,517 @@
+"""Python host mirror of the reference's hot-path interface, over the C-ABI.
+
+Same names and argument meaning as the reference's C++ entry points
+(proj/include/plmss/{orderfield,segmentation,marching}.hpp); device memory
+comes from torch (plumbing only). Every call runs on the B200 through
+``libplmss_b200.so``; there is no CPU fallback — a missing library or a
+missing CUDA device raises immediately.
+
+Error behaviour mirrors the reference exceptions: std::invalid_argument ->
+ValueError, std::logic_error -> RuntimeError, std::out_of_range -> IndexError.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "libplmss_b200.so")
+
+KEY_F32, KEY_F64, KEY_RANK = 0, 1, 2
+ASCENDING, DESCENDING, BOTH = 0, 1, 2
+OPT_COMBINE_PATH = 1
+
+_ERR = {1: ValueError, 2: RuntimeError, 3: IndexError, 4: RuntimeError, 5: MemoryError}
+
+HEADER_FUNCTIONS = [
+    "plmss_b200_tet_table", "plmss_b200_last_error", "plmss_b200_version", "plmss_b200_ctx_create",
+    "plmss_b200_ctx_destroy", "plmss_b200_ctx_scratch_bytes", "plmss_b200_ctx_set_timing",
+    "plmss_b200_ctx_stage_ms", "plmss_b200_compute_order", "plmss_b200_segment", "plmss_b200_seed_hops",
+    "plmss_b200_combine_ms", "plmss_b200_index_separators", "plmss_b200_emit_separators",
+    "plmss_b200_materialize_separators", "plmss_b200_emit_boundaries", "plmss_b200_pipeline",
+    "plmss_b200_result", "plmss_b200_copy", "plmss_b200_ctx_set_option", "plmss_b200_pipeline_host",
+    "plmss_b200_synth", "plmss_b200_launch_count",
+]
+
+
+class PlmssResult(C.Structure):
+    _fields_ = [
+        ("d_desc", C.c_void_p), ("d_asc", C.c_void_p), ("d_ms", C.c_void_p), ("d_maxima", C.c_void_p),
+        ("d_minima", C.c_void_p), ("d_region_keys", C.c_void_p), ("d_tris", C.c_void_p),
+        ("n_vertices", C.c_int64), ("n_maxima", C.c_int64), ("n_minima", C.c_int64),
+        ("n_regions", C.c_int64), ("n_tris", C.c_int64), ("sweeps", C.c_int32),
+    ]
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load libplmss_b200.so (in-tree build). Raises if it is missing."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() (nvcc, sm_100a)")
+        L = C.CDLL(LIB_PATH)
+        vp, i64, i32 = C.c_void_p, C.c_int64, C.c_int
+        L.plmss_b200_last_error.restype = C.c_char_p
+        L.plmss_b200_version.restype = C.c_char_p
+        L.plmss_b200_ctx_create.argtypes = [i32, vp, C.POINTER(vp)]
+        L.plmss_b200_ctx_destroy.argtypes = [vp]
+        L.plmss_b200_ctx_destroy.restype = None
+        L.plmss_b200_ctx_scratch_bytes.argtypes = [vp]
+        L.plmss_b200_ctx_scratch_bytes.restype = C.c_size_t
+        L.plmss_b200_ctx_set_timing.argtypes = [vp, i32]
+        L.plmss_b200_ctx_stage_ms.argtypes = [vp, vp]
+        L.plmss_b200_ctx_set_option.argtypes = [vp, i32, i64]
+        L.plmss_b200_compute_order.argtypes = [vp, i32, vp, i64, vp]
+        L.plmss_b200_segment.argtypes = [vp, vp, i32, vp, i32, vp, vp, vp, vp, vp, vp, vp]
+        L.plmss_b200_seed_hops.argtypes = [vp, vp, i32, vp, vp, vp]
+        L.plmss_b200_combine_ms.argtypes = [vp, i64, vp, vp, vp, vp, vp]
+        L.plmss_b200_index_separators.argtypes = [vp, vp, i32, vp, vp, vp]
+        L.plmss_b200_emit_separators.argtypes = [vp, vp, i32, vp, vp, i64, vp]
+        L.plmss_b200_materialize_separators.argtypes = [vp, vp, vp, vp, i32, vp, i64, vp, vp, vp]
+        L.plmss_b200_emit_boundaries.argtypes = [vp, vp, vp, vp, i32, vp, i32, i64, vp, vp, vp, vp, vp, vp, vp]
+        L.plmss_b200_pipeline.argtypes = [vp, vp, vp]
+        L.plmss_b200_result.argtypes = [vp, C.POINTER(PlmssResult)]
+        L.plmss_b200_copy.argtypes = [vp, vp, vp, i64, i32]
+        L.plmss_b200_pipeline_host.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i64, C.POINTER(PlmssResult)]
+        L.plmss_b200_synth.argtypes = [vp, vp, i32, vp, i32, C.c_double, C.c_uint64, i32, vp]
+        L.plmss_b200_tet_table.argtypes = [vp, vp]
+        L.plmss_b200_tet_table.restype = None
+        L.plmss_b200_launch_count.restype = C.c_ulonglong
+        _lib = L
+    return _lib
+
+
+def _check(status: int) -> None:
+    if status != 0:
+        raise _ERR.get(status, RuntimeError)(lib().plmss_b200_last_error().decode())
+
+
+def tet_table():
+    """Host copy of the device recipe table (no GPU needed)."""
+    rows = np.zeros(52, np.uint32)
+    cases = np.zeros(32, np.uint16)
+    lib().plmss_b200_tet_table(rows.ctypes.data, cases.ctypes.data)
+    return rows, cases
+
+
+def launch_count() -> int:
+    """Kernel launches issued by libplmss_b200 so far (process-wide)."""
+    return int(lib().plmss_b200_launch_count())
+
+
+def _dims(d) -> np.ndarray:
+    a = np.ascontiguousarray(np.asarray(d, dtype=np.int64).reshape(3))
+    return a
+
+
+def _vec3(v, default):
+    return np.ascontiguousarray(np.asarray(default if v is None else v, dtype=np.float64).reshape(3))
+
+
+def _torch():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise RuntimeError("plmss_b200 needs a CUDA device (B200, sm_100a); there is no CPU fallback")
+    return torch
+
+
+class Context:
+    """Device + stream + scratch arena (plmss_ctx). By default the context
+    issues work on torch's current stream so torch events time it."""
+
+    def __init__(self, device: int = 0, stream=None):
+        torch = _torch()
+        self.device = device
+        if stream is None:
+            stream = torch.cuda.current_stream(device)
+        self.stream = stream
+        h = C.c_void_p()
+        _check(lib().plmss_b200_ctx_create(device, C.c_void_p(stream.cuda_stream), C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().plmss_b200_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_timing(self, on: bool):
+        _check(lib().plmss_b200_ctx_set_timing(self.h, int(on)))
+
+    def stage_ms(self):
+        out = np.zeros(8, np.float32)
+        _check(lib().plmss_b200_ctx_stage_ms(self.h, out.ctypes.data))
+        return out
+
+    def set_option(self, option: int, value: int):
+        _check(lib().plmss_b200_ctx_set_option(self.h, option, value))
+
+    def scratch_bytes(self) -> int:
+        return lib().plmss_b200_ctx_scratch_bytes(self.h)
+
+
+_default: dict = {}
+
+
+def default_context(device: int = 0) -> Context:
+    ctx = _default.get(device)
+    if ctx is None:
+        ctx = _default[device] = Context(device)
+    return ctx
+
+
+def _ptr(t) -> C.c_void_p:
+    return C.c_void_p(t.data_ptr()) if t is not None else C.c_void_p(0)
+
+
+def _as_u32(t):
+    """int32 device storage holding uint32 values -> int64 values."""
+    torch = _torch()
+    return t.to(torch.int64) & 0xFFFFFFFF
+
+
+# --------------------------------------------------------------- order ----
+def compute_order(values, ctx: Optional[Context] = None):
+    """compute_order (orderfield.hpp:35): int64 ranks of (value, id)."""
+    torch = _torch()
+    ctx = ctx or default_context()
+    v = values.contiguous()
+    kt = KEY_F32 if v.dtype == torch.float32 else KEY_F64
+    if v.dtype not in (torch.float32, torch.float64):
+        raise ValueError("values must be float32 or float64")
+    rank = torch.empty(v.numel(), dtype=torch.int64, device=v.device)
+    _check(lib().plmss_b200_compute_order(ctx.h, kt, _ptr(v), v.numel(), _ptr(rank)))
+    return rank
+
+
+# -------------------------------------------------------- segmentation ----
+@dataclass
+class SegmentationResult:
+    """Mirror of plmss::SegmentationResult (segmentation.hpp:35-58); label
+    arrays are int32 device tensors holding uint32 vertex ids."""
+    desc: object = None
+    asc: object = None
+    maxima: object = None
+    minima: object = None
+    ms_region: object = None
+    region_keys: object = None  # int64: asc << 32 | desc
+    sweeps: int = 0
+    dims: tuple = ()
+
+    def num_regions(self) -> int:
+        return 0 if self.region_keys is None else int(self.region_keys.numel())
+
+
+def _key_type(keys):
+    torch = _torch()
+    if keys.dtype == torch.float32:
+        return KEY_F32
+    if keys.dtype == torch.float64:
+        return KEY_F64
+    if keys.dtype == torch.int64:
+        return KEY_RANK
+    raise ValueError("keys must be float32, float64 values or int64 ranks")
+
+
+def seed_hops(dims, keys, ctx: Optional[Context] = None):
+    """detail::seed_hops_both (segmentation.hpp:108-113): step-1 hop targets."""
+    torch = _torch()
+    ctx = ctx or default_context()
+    d = _dims(dims)
+    n = int(np.prod(d))
+    k = keys.contiguous().view(-1)
+    if k.numel() != n:
+        raise ValueError("order field size does not match complex")
+    desc = torch.empty(n, dtype=torch.int32, device=k.device)
+    asc = torch.empty(n, dtype=torch.int32, device=k.device)
+    _check(lib().plmss_b200_seed_hops(ctx.h, d.ctypes.data, _key_type(k), _ptr(k), _ptr(desc), _ptr(asc)))
+    return desc, asc
+
+
+def segment(dims, keys, direction: int = BOTH, workers: int = 1, ctx: Optional[Context] = None) -> SegmentationResult:
+    """segment (segmentation.hpp:74-76). `keys`: float32/float64 scalar
+    values (compared as (value, id)) or int64 OrderField ranks. `workers` is
+    accepted for signature parity and must be >= 1, as in the reference."""
+    torch = _torch()
+    if workers < 1:
+        raise ValueError("workers must be >= 1")
+    ctx = ctx or default_context()
+    d = _dims(dims)
+    n = int(np.prod(d))
+    k = keys.contiguous().view(-1)
+    if k.numel() != n:
+        raise ValueError("order field size does not match complex")
+    dev = k.device
+    want_desc, want_asc = direction != ASCENDING, direction != DESCENDING
+    desc = torch.empty(n, dtype=torch.int32, device=dev) if want_desc else None
+    asc = torch.empty(n, dtype=torch.int32, device=dev) if want_asc else None
+    mx = torch.empty(n, dtype=torch.int32, device=dev) if want_desc else None
+    mn = torch.empty(n, dtype=torch.int32, device=dev) if want_asc else None
+    nmax, nmin, sweeps = C.c_int64(), C.c_int64(), C.c_int32()
+    _check(lib().plmss_b200_segment(ctx.h, d.ctypes.data, _key_type(k), _ptr(k), direction, _ptr(desc), _ptr(asc),
+                                    _ptr(mx), _ptr(mn), C.byref(nmax), C.byref(nmin), C.byref(sweeps)))
+    return SegmentationResult(desc=desc, asc=asc, maxima=None if mx is None else mx[: nmax.value],
+                              minima=None if mn is None else mn[: nmin.value], sweeps=sweeps.value,
+                              dims=tuple(int(x) for x in d))
+
+
+def combine_ms(seg: SegmentationResult, workers: int = 1, ctx: Optional[Context] = None) -> SegmentationResult:
+    """combine_ms (segmentation.hpp:80): fills ms_region and region_keys."""
+    torch = _torch()
+    if seg.desc is None or seg.asc is None:
+        raise ValueError("combine_ms needs both ascending and descending labels")
+    ctx = ctx or default_context()
+    n = seg.desc.numel()
+    ms = torch.empty(n, dtype=torch.int32, device=seg.desc.device)
+    keys = torch.empty(n, dtype=torch.int64, device=seg.desc.device)
+    r = C.c_int64()
+    _check(lib().plmss_b200_combine_ms(ctx.h, n, _ptr(seg.asc), _ptr(seg.desc), _ptr(ms), _ptr(keys), C.byref(r)))
+    seg.ms_region = ms
+    seg.region_keys = keys[: r.value]
+    return seg
+
+
+# -------------------------------------------------------------- marching ---
+def _label_type(labels):
+    torch = _torch()
+    if labels.dtype == torch.int32:
+        return 0
+    if labels.dtype == torch.int64:
+        return 1
+    raise ValueError("labels must be int32 (uint32 ids) or int64")
+
+
+def index_separators(dims, labels, workers: int = 1, ctx: Optional[Context] = None):
+    """index_separators (marching.hpp:101-102): per-cell codes + total."""
+    torch = _torch()
+    ctx = ctx or default_context()
+    d = _dims(dims)
+    lab = labels.contiguous().view(-1)
+    if lab.numel() != int(np.prod(d)):
+        raise ValueError("label field size does not match vertex count")
+    ncells = 6 * int((d[0] - 1) * (d[1] - 1) * (d[2] - 1))
+    codes = torch.empty(max(ncells, 1), dtype=torch.uint8, device=lab.device)
+    total = C.c_int64()
+    _check(lib().plmss_b200_index_separators(ctx.h, d.ctypes.data, _label_type(lab), _ptr(lab), _ptr(codes),
+                                             C.byref(total)))
+    return codes[:ncells], total.value
+
+
+def emit_separators(dims, labels, workers: int = 1, ctx: Optional[Context] = None):
+    """emit_separators (marching.hpp:115-117) as compact records in the
+    reference order: int64 tensor (T, 2) = [cell << 6 | row, lo | hi << 32]
+    for int32 labels, (T, 3) = [cell << 6 | row, lo, hi] for int64 labels."""
+    torch = _torch()
+    ctx = ctx or default_context()
+    d = _dims(dims)
+    lab = labels.contiguous().view(-1)
+    if lab.numel() != int(np.prod(d)):
+        raise ValueError("label field size does not match vertex count")
+    lt = _label_type(lab)
+    width = 2 if lt == 0 else 3
+    _, total = index_separators(d, lab, ctx=ctx)
+    out = torch.empty((max(total, 1), width), dtype=torch.int64, device=lab.device)
+    t = C.c_int64()
+    _check(lib().plmss_b200_emit_separators(ctx.h, d.ctypes.data, lt, _ptr(lab), _ptr(out), total, C.byref(t)))
+    return out[: t.value]
+
+
+def materialize_separators(dims, records, spacing=None, origin=None, ctx: Optional[Context] = None):
+    """Reference SeparatingMesh layout (marching.hpp:65-76) from records:
+    points (3T, 3) float64, indices (identity soup), regions (T, 2) int64,
+    source_cells (T,) int64."""
+    torch = _torch()
+    ctx = ctx or default_context()
+    d = _dims(dims)
+    recs = records.contiguous()
+    T = recs.shape[0]
+    lt = 0 if recs.shape[1] == 2 else 1
+    dev = recs.device
+    pts = torch.empty((max(3 * T, 1), 3), dtype=torch.float64, device=dev)
+    reg = torch.empty((max(T, 1), 2), dtype=torch.int64, device=dev)
+    src = torch.empty(max(T, 1), dtype=torch.int64, device=dev)
+    sp, og = _vec3(spacing, (1, 1, 1)), _vec3(origin, (0, 0, 0))
+    _check(lib().plmss_b200_materialize_separators(ctx.h, d.ctypes.data, sp.ctypes.data, og.ctypes.data, lt,
+                                                   _ptr(recs), T, _ptr(pts), _ptr(reg), _ptr(src)))
+    return dict(points=pts[: 3 * T], indices=torch.arange(3 * T, device=dev), regions=reg[:T], source_cells=src[:T])
+
+
+def emit_boundaries(dims, labels, region_filter=None, workers: int = 1, spacing=None, origin=None,
+                    ctx: Optional[Context] = None):
+    """emit_boundaries (marching.hpp:123-126), reference order and layout."""
+    torch = _torch()
+    ctx = ctx or default_context()
+    d = _dims(dims)
+    lab = labels.contiguous().view(-1)
+    if lab.numel() != int(np.prod(d)):
+        raise ValueError("label field size does not match vertex count")
+    lt = _label_type(lab)
+    sp, og = _vec3(spacing, (1, 1, 1)), _vec3(origin, (0, 0, 0))
+    hf = 0 if region_filter is None else 1
+    flt = 0 if region_filter is None else int(region_filter)
+    nf, npnt = C.c_int64(), C.c_int64()
+    L = lib()
+    _check(L.plmss_b200_emit_boundaries(ctx.h, d.ctypes.data, sp.ctypes.data, og.ctypes.data, lt, _ptr(lab), hf, flt,
+                                        None, None, None, None, None, C.byref(nf), C.byref(npnt)))
+    F, P = nf.value, npnt.value
+    dev = lab.device
+    faces = torch.empty((max(F, 1), 3), dtype=torch.int32, device=dev)
+    tags = torch.empty(max(F, 1), dtype=lab.dtype, device=dev)
+    cells = torch.empty(max(F, 1), dtype=torch.int64, device=dev)
+    pts = torch.empty((max(P, 1), 3), dtype=torch.float64, device=dev)
+    idx = torch.empty(max(3 * F, 1), dtype=torch.int64, device=dev)
+    _check(L.plmss_b200_emit_boundaries(ctx.h, d.ctypes.data, sp.ctypes.data, og.ctypes.data, lt, _ptr(lab), hf, flt,
+                                        _ptr(faces), _ptr(tags), _ptr(cells), _ptr(pts), _ptr(idx), C.byref(nf),
+                                        C.byref(npnt)))
+    tg = tags[:F].to(torch.int64)
+    if lt == 0:
+        tg = tg & 0xFFFFFFFF
+    regions = torch.stack([tg, torch.full_like(tg, -1)], dim=1)
+    return dict(faces=faces[:F], points=pts[:P], indices=idx[: 3 * F], regions=regions, source_cells=cells[:F])
+
+
+def select_labels(seg: SegmentationResult, mode: str):
+    """select_labels (marching.hpp:132-133): 'ascending', 'descending',
+    'morse_smale' or 'union' (asc then desc)."""
+    if mode == "ascending":
+        if seg.asc is None:
+            raise RuntimeError("ascending labels missing")
+        return [seg.asc]
+    if mode == "descending":
+        if seg.desc is None:
+            raise RuntimeError("descending labels missing")
+        return [seg.desc]
+    if mode == "morse_smale":
+        if seg.ms_region is None:
+            raise RuntimeError("combine_ms has not been run")
+        return [seg.ms_region]
+    if mode == "union":
+        if seg.asc is None or seg.desc is None:
+            raise RuntimeError("union needs both directions")
+        return [seg.asc, seg.desc]
+    raise RuntimeError("unknown segmentation mode")
+
+
+# ------------------------------------------------------- fused pipeline ---
+@dataclass
+class PipelineResult:
+    n_vertices: int
+    n_maxima: int
+    n_minima: int
+    n_regions: int
+    n_tris: int
+    sweeps: int
+    raw: PlmssResult = field(repr=False, default=None)
+
+
+def pipeline(dims, field_f32, ctx: Optional[Context] = None) -> PipelineResult:
+    """run_benchmark's MorseSmale pass (bench.cpp:66-87) on a device-resident
+    float32 field: asc, desc, extrema, dense MS ids + region table, separator
+    records. Results stay in the context (see fetch())."""
+    ctx = ctx or default_context()
+    d = _dims(dims)
+    f = field_f32
+    if f.numel() != int(np.prod(d)):
+        raise ValueError("field size does not match dims")
+    _check(lib().plmss_b200_pipeline(ctx.h, d.ctypes.data, _ptr(f)))
+    return result(ctx)
+
+
+def result(ctx: Context) -> PipelineResult:
+    r = PlmssResult()
+    _check(lib().plmss_b200_result(ctx.h, C.byref(r)))
+    return PipelineResult(r.n_vertices, r.n_maxima, r.n_minima, r.n_regions, r.n_tris, r.sweeps, r)
+
+
+def fetch(ctx: Context, res: PipelineResult, names=("desc", "asc", "ms", "maxima", "minima", "region_keys", "tris")):
+    """Copy pipeline outputs from the context into fresh torch tensors."""
+    torch = _torch()
+    r = res.raw
+    spec = {
+        "desc": (r.d_desc, r.n_vertices, torch.int32, 1),
+        "asc": (r.d_asc, r.n_vertices, torch.int32, 1),
+        "ms": (r.d_ms, r.n_vertices, torch.int32, 1),
+        "maxima": (r.d_maxima, r.n_maxima, torch.int32, 1),
+        "minima": (r.d_minima, r.n_minima, torch.int32, 1),
+        "region_keys": (r.d_region_keys, r.n_regions, torch.int64, 1),
+        "tris": (r.d_tris, r.n_tris, torch.int64, 2),
+    }
+    out = {}
+    for name in names:
+        ptr, n, dt, w = spec[name]
+        t = torch.empty((n, w) if w > 1 else n, dtype=dt, device=f"cuda:{ctx.device}")
+        if n:
+            _check(lib().plmss_b200_copy(ctx.h, _ptr(t), C.c_void_p(ptr), t.numel() * t.element_size(), 0))
+        out[name] = t
+    return out
+
+
+def pipeline_host(dims, h_field: np.ndarray, ctx: Optional[Context] = None, want=("desc", "asc", "ms", "maxima",
+                                                                                  "minima", "region_keys", "tris"),
+                  out_buffers: Optional[dict] = None):
+    """End-to-end call over host buffers (H2D of the field, D2H of every
+    requested output). out_buffers may hold preallocated (pinned) arrays."""
+    ctx = ctx or default_context()
+    d = _dims(dims)
+    n = int(np.prod(d))
+    f = np.ascontiguousarray(h_field, dtype=np.float32).reshape(-1)
+    if f.size != n:
+        raise ValueError("field size does not match dims")
+    bufs = dict(out_buffers or {})
+    for name in ("desc", "asc", "ms"):
+        if name in want and name not in bufs:
+            bufs[name] = np.empty(n, np.uint32)
+    for name in ("maxima", "minima"):
+        if name in want and name not in bufs:
+            bufs[name] = np.empty(n, np.uint32)
+    if "region_keys" in want and "region_keys" not in bufs:
+        bufs["region_keys"] = np.empty(n, np.uint64)
+    tri_cap = 0
+    if "tris" in want:
+        if "tris" not in bufs:
+            raise ValueError("pass out_buffers['tris'] (uint64 array of shape (cap, 2)) to fetch separators")
+        tri_cap = bufs["tris"].shape[0]
+    r = PlmssResult()
+
+    def p(name):
+        b = bufs.get(name) if name in want else None
+        return C.c_void_p(b.ctypes.data) if b is not None else C.c_void_p(0)
+
+    _check(lib().plmss_b200_pipeline_host(ctx.h, d.ctypes.data, f.ctypes.data, p("desc"), p("asc"), p("ms"),
+                                          p("maxima"), p("minima"), p("region_keys"), p("tris"), tri_cap,
+                                          C.byref(r)))
+    res = PipelineResult(r.n_vertices, r.n_maxima, r.n_minima, r.n_regions, r.n_tris, r.sweeps, r)
+    out = {k: v for k, v in bufs.items() if k in want}
+    for name, cnt in (("maxima", r.n_maxima), ("minima", r.n_minima), ("region_keys", r.n_regions),
+                      ("tris", r.n_tris)):
+        if name in out:
+            out[name] = out[name][:cnt]
+    return res, out
+
+
+def synth_field(dims, kind: str = "gaussians", gaussians=None, noise_amp: float = 0.0, seed: int = 0,
+                levels: int = 0, ctx: Optional[Context] = None):
+    """Seeded synthetic float32 field on the device (harness utility)."""
+    torch = _torch()
+    ctx = ctx or default_context()
+    d = _dims(dims)
+    n = int(np.prod(d))
+    f = torch.empty(n, dtype=torch.float32, device=f"cuda:{ctx.device}")
+    g = np.ascontiguousarray(np.zeros((0, 5)) if gaussians is None else gaussians, dtype=np.float64)
+    k = {"gaussians": 0, "uniform": 1}[kind]
+    _check(lib().plmss_b200_synth(ctx.h, d.ctypes.data, k, g.ctypes.data, g.shape[0], noise_amp, seed, levels,
+                                  _ptr(f)))
+    return f

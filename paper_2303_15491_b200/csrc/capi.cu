@@ -1,0 +1,412 @@
+// extern "C" boundary of libplmss_b200.so (declared in include/plmss_b200.h).
+// Converts internal exceptions to status codes + a thread-local message.
+#include <string.h>
+
+#include <string>
+
+#include "common.cuh"
+#include "tet_tables.h"
+
+using namespace plmss_b200;
+
+unsigned long long plmss_b200::g_launches = 0;
+
+struct plmss_ctx {
+  Ctx c;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return PLMSS_OK;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return e.status;
+  } catch (const std::bad_alloc&) {
+    g_err = "host allocation failed";
+    return PLMSS_ERR_NOMEM;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return PLMSS_ERR_CUDA;
+  }
+}
+
+Ctx& C(plmss_ctx* p) {
+  if (!p) fail(PLMSS_ERR_INVALID_ARGUMENT, "null context");
+  return p->c;
+}
+
+void set_device(Ctx& c) { CK(cudaSetDevice(c.device)); }
+
+void finish_timing(Ctx& c, int marks) {
+  if (!c.timing) return;
+  c.sync();
+  for (int i = 0; i + 1 < marks; ++i) CK(cudaEventElapsedTime(&c.stage_ms[i], c.ev[i], c.ev[i + 1]));
+}
+
+// Segmentation stages shared by plmss_b200_segment and the pipeline.
+struct SegOut {
+  int64_t n_max = 0, n_min = 0;
+  int sweeps = 0;
+};
+
+SegOut run_segment(Ctx& c, const Grid& g, int key_type, const void* keys, int direction, uint32_t* desc,
+                   uint32_t* asc, const std::function<uint32_t*(int64_t)>& get_maxima,
+                   const std::function<uint32_t*(int64_t)>& get_minima, uint32_t* rank_max, uint32_t* rank_min) {
+  SegOut o;
+  const bool want_desc = direction != PLMSS_ASCENDING, want_asc = direction != PLMSS_DESCENDING;
+  uint32_t* bad = static_cast<uint32_t*>(c.get(S_FLAGS, 64)) + 8;
+  if (key_type != PLMSS_KEY_RANK) CK(cudaMemsetAsync(bad, 0xff, sizeof(uint32_t), c.stream));
+  c.mark(0);
+  seed_hops(c, g, key_type, keys, want_desc ? desc : nullptr, want_asc ? asc : nullptr,
+            key_type != PLMSS_KEY_RANK ? bad : nullptr);
+  c.mark(1);
+  if (key_type != PLMSS_KEY_RANK) {
+    CK(cudaMemcpyAsync(c.h_pinned + 2, bad, sizeof(uint32_t), cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    const uint32_t b = *reinterpret_cast<uint32_t*>(c.h_pinned + 2);
+    if (b != 0xffffffffu) fail(PLMSS_ERR_INVALID_ARGUMENT, "non-finite scalar value at vertex " + std::to_string(b));
+  }
+  o.sweeps = compress(c, g.n, want_desc ? desc : nullptr, want_asc ? asc : nullptr);
+  c.mark(2);
+  if (want_desc) {
+    o.n_max = count_extrema(c, g.n, desc);
+    write_extrema(c, g.n, desc, get_maxima(o.n_max), rank_max);
+  }
+  if (want_asc) {
+    o.n_min = count_extrema(c, g.n, asc);
+    write_extrema(c, g.n, asc, get_minima(o.n_min), rank_min);
+  }
+  c.mark(3);
+  return o;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* plmss_b200_last_error(void) { return g_err.c_str(); }
+
+const char* plmss_b200_version(void) { return "plmss_b200 0.1 (sm_100a)"; }
+
+unsigned long long plmss_b200_launch_count(void) { return __atomic_load_n(&g_launches, __ATOMIC_RELAXED); }
+
+void plmss_b200_tet_table(uint32_t rows[52], uint16_t cases[32]) {
+  memcpy(rows, kTetRowsPacked, sizeof(kTetRowsPacked));
+  memcpy(cases, kTetCasePacked, sizeof(kTetCasePacked));
+}
+
+int plmss_b200_ctx_create(int device, void* stream, plmss_ctx** out) {
+  return guarded([&] {
+    if (!out) fail(PLMSS_ERR_INVALID_ARGUMENT, "null out");
+    int n = 0;
+    CK(cudaGetDeviceCount(&n));
+    if (device < 0 || device >= n) fail(PLMSS_ERR_INVALID_ARGUMENT, "no such CUDA device");
+    auto* p = new plmss_ctx();
+    Ctx& c = p->c;
+    c.device = device;
+    try {
+      CK(cudaSetDevice(device));
+      if (stream) {
+        c.stream = static_cast<cudaStream_t>(stream);
+      } else {
+        CK(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+        c.own_stream = true;
+      }
+      CK(cudaMallocHost(&c.h_pinned, 64 * sizeof(uint64_t)));
+      for (auto& e : c.ev) CK(cudaEventCreate(&e));
+      CK(cudaDeviceGetAttribute(&c.sm_count, cudaDevAttrMultiProcessorCount, device));
+    } catch (...) {
+      delete p;
+      throw;
+    }
+    *out = p;
+  });
+}
+
+void plmss_b200_ctx_destroy(plmss_ctx* p) {
+  if (!p) return;
+  Ctx& c = p->c;
+  cudaSetDevice(c.device);
+  cudaStreamSynchronize(c.stream);
+  for (auto& b : c.buf)
+    if (b) cudaFreeAsync(b, c.stream);
+  cudaStreamSynchronize(c.stream);
+  for (auto& e : c.ev)
+    if (e) cudaEventDestroy(e);
+  if (c.h_pinned) cudaFreeHost(c.h_pinned);
+  if (c.own_stream) cudaStreamDestroy(c.stream);
+  delete p;
+}
+
+size_t plmss_b200_ctx_scratch_bytes(const plmss_ctx* p) {
+  if (!p) return 0;
+  size_t s = 0;
+  for (size_t x : p->c.cap) s += x;
+  return s;
+}
+
+int plmss_b200_ctx_set_timing(plmss_ctx* p, int enable) {
+  return guarded([&] { C(p).timing = enable != 0; });
+}
+
+int plmss_b200_ctx_stage_ms(const plmss_ctx* p, float out[8]) {
+  return guarded([&] {
+    if (!p) fail(PLMSS_ERR_INVALID_ARGUMENT, "null context");
+    memcpy(out, p->c.stage_ms, sizeof(p->c.stage_ms));
+  });
+}
+
+int plmss_b200_compute_order(plmss_ctx* p, int key_type, const void* d_values, int64_t n, int64_t* d_rank) {
+  return guarded([&] {
+    Ctx& c = C(p);
+    set_device(c);
+    if (n < 0) fail(PLMSS_ERR_INVALID_ARGUMENT, "negative size");
+    compute_order(c, key_type, d_values, n, d_rank);
+    c.sync();
+  });
+}
+
+int plmss_b200_seed_hops(plmss_ctx* p, const int64_t dims[3], int key_type, const void* d_keys, uint32_t* d_desc,
+                         uint32_t* d_asc) {
+  return guarded([&] {
+    Ctx& c = C(p);
+    set_device(c);
+    const Grid g = make_grid(dims);
+    seed_hops(c, g, key_type, d_keys, d_desc, d_asc, nullptr);
+    c.sync();
+  });
+}
+
+int plmss_b200_segment(plmss_ctx* p, const int64_t dims[3], int key_type, const void* d_keys, int direction,
+                       uint32_t* d_desc, uint32_t* d_asc, uint32_t* d_maxima, uint32_t* d_minima,
+                       int64_t* n_maxima, int64_t* n_minima, int32_t* sweeps) {
+  return guarded([&] {
+    Ctx& c = C(p);
+    set_device(c);
+    const Grid g = make_grid(dims);
+    if (direction < 0 || direction > 2) fail(PLMSS_ERR_INVALID_ARGUMENT, "bad direction");
+    if (direction != PLMSS_ASCENDING && !d_desc) fail(PLMSS_ERR_INVALID_ARGUMENT, "d_desc required");
+    if (direction != PLMSS_DESCENDING && !d_asc) fail(PLMSS_ERR_INVALID_ARGUMENT, "d_asc required");
+    SegOut o = run_segment(
+        c, g, key_type, d_keys, direction, d_desc, d_asc, [&](int64_t) { return d_maxima; },
+        [&](int64_t) { return d_minima; }, nullptr, nullptr);
+    c.sync();
+    if (n_maxima) *n_maxima = o.n_max;
+    if (n_minima) *n_minima = o.n_min;
+    if (sweeps) *sweeps = o.sweeps;
+  });
+}
+
+int plmss_b200_combine_ms(plmss_ctx* p, int64_t n, const uint32_t* d_asc, const uint32_t* d_desc, uint32_t* d_ms,
+                          uint64_t* d_region_keys, int64_t* n_regions) {
+  return guarded([&] {
+    Ctx& c = C(p);
+    set_device(c);
+    if (!d_asc || !d_desc) fail(PLMSS_ERR_INVALID_ARGUMENT, "combine_ms needs both ascending and descending labels");
+    if (n <= 0 || n >= (int64_t(1) << 32) - 1) fail(PLMSS_ERR_INVALID_ARGUMENT, "bad vertex count");
+    // Extremum lists and rank maps from the (converged) label arrays.
+    uint32_t* rmax = c.get_t<uint32_t>(S_RANK_MAX, n);
+    uint32_t* rmin = c.get_t<uint32_t>(S_RANK_MIN, n);
+    const int64_t nmax = count_extrema(c, n, d_desc);
+    uint32_t* maxima = c.get_t<uint32_t>(S_MAXIMA, nmax);
+    write_extrema(c, n, d_desc, maxima, rmax);
+    const int64_t nmin = count_extrema(c, n, d_asc);
+    uint32_t* minima = c.get_t<uint32_t>(S_MINIMA, nmin);
+    write_extrema(c, n, d_asc, minima, rmin);
+    const int64_t R = combine_ms(
+        c, n, d_asc, d_desc, d_ms, [&](int64_t) { return d_region_keys; }, minima, nmin, maxima, nmax, rmin, rmax);
+    c.sync();
+    if (n_regions) *n_regions = R;
+  });
+}
+
+int plmss_b200_index_separators(plmss_ctx* p, const int64_t dims[3], int label_type, const void* d_labels,
+                                uint8_t* d_codes, int64_t* total) {
+  return guarded([&] {
+    Ctx& c = C(p);
+    set_device(c);
+    const Grid g = make_grid(dims);
+    const int64_t t = index_separators(c, g, label_type, d_labels, d_codes);
+    c.sync();
+    if (total) *total = t;
+  });
+}
+
+int plmss_b200_emit_separators(plmss_ctx* p, const int64_t dims[3], int label_type, const void* d_labels,
+                               void* d_out, int64_t capacity, int64_t* total) {
+  int64_t t = 0;
+  int st = guarded([&] {
+    Ctx& c = C(p);
+    set_device(c);
+    const Grid g = make_grid(dims);
+    t = emit_separators(c, g, label_type, d_labels,
+                        [&](int64_t tot) -> void* { return tot <= capacity ? d_out : nullptr; });
+    c.sync();
+    if (total) *total = t;
+    if (t > capacity)
+      fail(PLMSS_ERR_LOGIC, "geometry phase exceeds indexed primitive count (capacity " + std::to_string(capacity) +
+                                ", need " + std::to_string(t) + ")");
+  });
+  return st;
+}
+
+int plmss_b200_materialize_separators(plmss_ctx* p, const int64_t dims[3], const double spacing[3],
+                                      const double origin[3], int label_type, const void* d_tris, int64_t n,
+                                      double* d_points, int64_t* d_regions, int64_t* d_source_cells) {
+  return guarded([&] {
+    Ctx& c = C(p);
+    set_device(c);
+    const Grid g = make_grid(dims);
+    materialize(c, g, spacing, origin, label_type, d_tris, n, d_points, d_regions, d_source_cells);
+    c.sync();
+  });
+}
+
+int plmss_b200_emit_boundaries(plmss_ctx* p, const int64_t dims[3], const double spacing[3], const double origin[3],
+                               int label_type, const void* d_labels, int has_filter, int64_t filter,
+                               uint32_t* d_faces, void* d_tags, int64_t* d_cells, double* d_points,
+                               int64_t* d_indices, int64_t* n_faces, int64_t* n_points) {
+  return guarded([&] {
+    Ctx& c = C(p);
+    set_device(c);
+    const Grid g = make_grid(dims);
+    int64_t nf = 0, np = 0;
+    if (label_type == 0 && has_filter && (filter < 0 || filter > int64_t(0xffffffffu))) {
+      // No uint32 label can carry this tag: empty result.
+    } else {
+      emit_boundaries(c, g, spacing, origin, label_type, d_labels, has_filter, filter, d_faces, d_tags, d_cells,
+                      d_points, d_indices, &nf, &np);
+      c.sync();
+    }
+    if (n_faces) *n_faces = nf;
+    if (n_points) *n_points = np;
+  });
+}
+
+int plmss_b200_pipeline(plmss_ctx* p, const int64_t dims[3], const float* d_field) {
+  return guarded([&] {
+    Ctx& c = C(p);
+    set_device(c);
+    const Grid g = make_grid(dims);
+    uint32_t* desc = c.get_t<uint32_t>(S_DESC, g.n);
+    uint32_t* asc = c.get_t<uint32_t>(S_ASC, g.n);
+    uint32_t* ms = c.get_t<uint32_t>(S_MS, g.n);
+    uint32_t* rmax = c.get_t<uint32_t>(S_RANK_MAX, g.n);
+    uint32_t* rmin = c.get_t<uint32_t>(S_RANK_MIN, g.n);
+    uint32_t *maxima = nullptr, *minima = nullptr;
+    SegOut o = run_segment(
+        c, g, PLMSS_KEY_F32, d_field, PLMSS_BOTH, desc, asc,
+        [&](int64_t k) { return maxima = c.get_t<uint32_t>(S_MAXIMA, k); },
+        [&](int64_t k) { return minima = c.get_t<uint32_t>(S_MINIMA, k); }, rmax, rmin);
+    uint64_t* keys = nullptr;
+    const int64_t R = combine_ms(
+        c, g.n, asc, desc, ms, [&](int64_t r) { return keys = c.get_t<uint64_t>(S_KEYS, r); }, minima, o.n_min,
+        maxima, o.n_max, rmin, rmax);
+    c.mark(4);
+    plmss_tri* tris = nullptr;
+    const int64_t T = emit_separators(c, g, 0, ms, [&](int64_t t) -> void* {
+      return tris = c.get_t<plmss_tri>(S_TRIS, t);
+    });
+    c.mark(5);
+    c.sync();
+    finish_timing(c, 6);
+    plmss_result& r = c.result;
+    r.d_desc = desc;
+    r.d_asc = asc;
+    r.d_ms = ms;
+    r.d_maxima = maxima;
+    r.d_minima = minima;
+    r.d_region_keys = keys;
+    r.d_tris = tris;
+    r.n_vertices = g.n;
+    r.n_maxima = o.n_max;
+    r.n_minima = o.n_min;
+    r.n_regions = R;
+    r.n_tris = T;
+    r.sweeps = o.sweeps;
+  });
+}
+
+int plmss_b200_copy(plmss_ctx* p, void* dst, const void* d_src, int64_t bytes, int to_host) {
+  return guarded([&] {
+    Ctx& c = C(p);
+    set_device(c);
+    if (bytes < 0) fail(PLMSS_ERR_INVALID_ARGUMENT, "negative size");
+    if (bytes == 0) return;
+    if (!dst || !d_src) fail(PLMSS_ERR_INVALID_ARGUMENT, "null pointer");
+    CK(cudaMemcpyAsync(dst, d_src, size_t(bytes), to_host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice,
+                       c.stream));
+    c.sync();
+  });
+}
+
+int plmss_b200_ctx_set_option(plmss_ctx* p, int option, int64_t value) {
+  return guarded([&] {
+    Ctx& c = C(p);
+    if (option == PLMSS_OPT_COMBINE_PATH) {
+      if (value < 0 || value > 2) fail(PLMSS_ERR_INVALID_ARGUMENT, "combine path must be 0, 1 or 2");
+      c.combine_path = int(value);
+      return;
+    }
+    fail(PLMSS_ERR_INVALID_ARGUMENT, "unknown option");
+  });
+}
+
+int plmss_b200_result(const plmss_ctx* p, plmss_result* out) {
+  return guarded([&] {
+    if (!p || !out) fail(PLMSS_ERR_INVALID_ARGUMENT, "null argument");
+    *out = p->c.result;
+  });
+}
+
+int plmss_b200_pipeline_host(plmss_ctx* p, const int64_t dims[3], const float* h_field, uint32_t* h_desc,
+                             uint32_t* h_asc, uint32_t* h_ms, uint32_t* h_maxima, uint32_t* h_minima,
+                             uint64_t* h_region_keys, plmss_tri* h_tris, int64_t tri_capacity, plmss_result* out) {
+  int st = guarded([&] {
+    Ctx& c = C(p);
+    set_device(c);
+    const Grid g = make_grid(dims);
+    if (!h_field) fail(PLMSS_ERR_INVALID_ARGUMENT, "null field");
+    float* f = c.get_t<float>(S_FIELD, g.n);
+    CK(cudaMemcpyAsync(f, h_field, g.n * sizeof(float), cudaMemcpyHostToDevice, c.stream));
+  });
+  if (st) return st;
+  st = plmss_b200_pipeline(p, dims, static_cast<const float*>(p->c.buf[S_FIELD]));
+  if (st) return st;
+  return guarded([&] {
+    Ctx& c = p->c;
+    const plmss_result& r = c.result;
+    auto d2h = [&](void* dst, const void* src, size_t bytes) {
+      if (dst && bytes) CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c.stream));
+    };
+    d2h(h_desc, r.d_desc, r.n_vertices * 4);
+    d2h(h_asc, r.d_asc, r.n_vertices * 4);
+    d2h(h_ms, r.d_ms, r.n_vertices * 4);
+    d2h(h_maxima, r.d_maxima, r.n_maxima * 4);
+    d2h(h_minima, r.d_minima, r.n_minima * 4);
+    d2h(h_region_keys, r.d_region_keys, r.n_regions * 8);
+    if (h_tris && r.n_tris <= tri_capacity) d2h(h_tris, r.d_tris, r.n_tris * sizeof(plmss_tri));
+    c.sync();
+    if (out) *out = r;
+    if (h_tris && r.n_tris > tri_capacity)
+      fail(PLMSS_ERR_LOGIC, "separator records exceed the host capacity (" + std::to_string(r.n_tris) + ")");
+  });
+}
+
+int plmss_b200_synth(plmss_ctx* p, const int64_t dims[3], int kind, const double* h_gaussians, int n_gauss,
+                     double noise_amp, uint64_t seed, int levels, float* d_field) {
+  return guarded([&] {
+    Ctx& c = C(p);
+    set_device(c);
+    const Grid g = make_grid(dims);
+    synth(c, g, kind, h_gaussians, n_gauss, noise_amp, seed, levels, d_field);
+  });
+}
+
+}  // extern "C"

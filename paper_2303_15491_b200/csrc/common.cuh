@@ -1,0 +1,159 @@
+// Shared definitions of the plmss_b200 library (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <functional>
+#include <stdexcept>
+#include <string>
+
+#include "plmss_b200.h"
+
+namespace plmss_b200 {
+
+// ---------------------------------------------------------------- errors ---
+// Exceptions inside the library; capi.cu converts them to status codes.
+struct Error : std::runtime_error {
+  int status;
+  Error(int s, const std::string& m) : std::runtime_error(m), status(s) {}
+};
+
+[[noreturn]] inline void fail(int status, const std::string& msg) { throw Error(status, msg); }
+
+inline void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    fail(e == cudaErrorMemoryAllocation ? PLMSS_ERR_NOMEM : PLMSS_ERR_CUDA,
+         std::string(what) + ": " + cudaGetErrorString(e));
+}
+// Kernel launches issued by this library (reported by bench.py).
+extern unsigned long long g_launches;
+#define CK(x) ::plmss_b200::cuda_check((x), #x)
+#define CK_LAUNCH(name)                                      \
+  do {                                                       \
+    __atomic_fetch_add(&::plmss_b200::g_launches, 1ull, __ATOMIC_RELAXED); \
+    ::plmss_b200::cuda_check(cudaGetLastError(), name);      \
+  } while (0)
+
+// ------------------------------------------------------------------ grid ---
+struct Grid {
+  int64_t X, Y, Z;   // vertex extents
+  int64_t n;         // vertices
+  int64_t cubes;     // (X-1)(Y-1)(Z-1)
+  int64_t cells;     // 6 * cubes
+};
+
+inline Grid make_grid(const int64_t* dims) {
+  if (!dims) fail(PLMSS_ERR_INVALID_ARGUMENT, "dims is null");
+  for (int a = 0; a < 3; ++a)
+    if (dims[a] < 1)
+      fail(PLMSS_ERR_INVALID_ARGUMENT, "grid dims must be positive, got " + std::to_string(dims[a]) +
+                                           " on axis " + std::to_string(a));
+  for (int a = 0; a < 3; ++a)
+    if (dims[a] < 2)
+      fail(PLMSS_ERR_INVALID_ARGUMENT,
+           "the B200 path handles 3-D implicit grids only (every dim >= 2)");
+  Grid g;
+  g.X = dims[0];
+  g.Y = dims[1];
+  g.Z = dims[2];
+  g.n = g.X * g.Y * g.Z;
+  if (g.n >= (int64_t(1) << 32) - 1)
+    fail(PLMSS_ERR_INVALID_ARGUMENT, "grid has >= 2^32-1 vertices; uint32 vertex ids required");
+  g.cubes = (g.X - 1) * (g.Y - 1) * (g.Z - 1);
+  g.cells = 6 * g.cubes;
+  return g;
+}
+
+// --------------------------------------------------------------- context ---
+enum Slot {
+  S_DESC, S_ASC, S_MS, S_MAXIMA, S_MINIMA, S_KEYS, S_TRIS,  // pipeline results
+  S_FLAGS,        // small device counters / flags
+  S_SCAN_A, S_SCAN_B, S_SCAN_C,  // scan partials
+  S_RANK_MAX, S_RANK_MIN,        // extremum -> rank maps (N, sparse use)
+  S_BITMAP, S_HASH_K, S_HASH_V, S_SORT_A, S_SORT_B, S_SORT_C, S_SORT_D,
+  S_TMP0, S_TMP1, S_TMP2, S_FIELD,
+  S_COUNT
+};
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  void* buf[S_COUNT] = {};
+  size_t cap[S_COUNT] = {};
+  uint64_t* h_pinned = nullptr;  // small pinned host staging for counters
+  bool timing = false;
+  float stage_ms[8] = {};
+  cudaEvent_t ev[9] = {};
+  plmss_result result{};
+  int sm_count = 148;
+  int combine_path = 0;  // PLMSS_OPT_COMBINE_PATH
+
+  void* get(Slot s, size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    if (cap[s] < bytes) {
+      if (buf[s]) CK(cudaFreeAsync(buf[s], stream));
+      buf[s] = nullptr;
+      cap[s] = 0;
+      size_t want = bytes + bytes / 8;  // headroom for repeated growth
+      CK(cudaMallocAsync(&buf[s], want, stream));
+      cap[s] = want;
+    }
+    return buf[s];
+  }
+  template <class T>
+  T* get_t(Slot s, size_t count) {
+    return static_cast<T*>(get(s, count * sizeof(T)));
+  }
+  void sync() { CK(cudaStreamSynchronize(stream)); }
+  void mark(int i) {
+    if (timing) CK(cudaEventRecord(ev[i], stream));
+  }
+};
+
+inline unsigned blocks_for(int64_t n, int threads, int64_t cap = int64_t(1) << 31) {
+  int64_t b = (n + threads - 1) / threads;
+  if (b < 1) b = 1;
+  return static_cast<unsigned>(b < cap ? b : cap);
+}
+
+// --------------------------------------------- internal entry points ------
+// segment.cu
+void seed_hops(Ctx& c, const Grid& g, int key_type, const void* keys, uint32_t* desc, uint32_t* asc,
+               uint32_t* bad_vertex /*device, may be null*/);
+int compress(Ctx& c, int64_t n, uint32_t* desc, uint32_t* asc);
+// Ordered compaction of self-pointing vertices: count (keeps block offsets
+// in S_TMP1), then write the list and/or the extremum -> rank map.
+int64_t count_extrema(Ctx& c, int64_t n, const uint32_t* labels);
+void write_extrema(Ctx& c, int64_t n, const uint32_t* labels, uint32_t* out, uint32_t* rank_map);
+void compute_order(Ctx& c, int key_type, const void* values, int64_t n, int64_t* rank);
+
+// combine.cu
+// get_keys(R) returns the region-key buffer (or nullptr).
+int64_t combine_ms(Ctx& c, int64_t n, const uint32_t* asc, const uint32_t* desc, uint32_t* ms,
+                   const std::function<uint64_t*(int64_t)>& get_keys, const uint32_t* minima, int64_t n_min, const uint32_t* maxima,
+                   int64_t n_max, const uint32_t* rank_min, const uint32_t* rank_max);
+
+// marching.cu
+int64_t index_separators(Ctx& c, const Grid& g, int label_type, const void* labels, uint8_t* codes);
+// get_out(total) returns the record buffer (or nullptr to only count).
+int64_t emit_separators(Ctx& c, const Grid& g, int label_type, const void* labels,
+                        const std::function<void*(int64_t)>& get_out);
+void materialize(Ctx& c, const Grid& g, const double* sp, const double* og, int label_type,
+                 const void* tris, int64_t n, double* points, int64_t* regions, int64_t* cells);
+void emit_boundaries(Ctx& c, const Grid& g, const double* sp, const double* og, int label_type,
+                     const void* labels, int has_filter, int64_t filter, uint32_t* faces, void* tags,
+                     int64_t* cells, double* points, int64_t* indices, int64_t* n_faces,
+                     int64_t* n_points);
+
+// scan.cu — device-wide exclusive scan of uint64 (in place allowed); returns total.
+uint64_t exclusive_scan_u64(Ctx& c, uint64_t* data, int64_t n, bool want_total = true);
+// stable LSD radix sort of (u64 key, u64 value) pairs; `bits` significant key bits.
+void radix_sort_pairs(Ctx& c, uint64_t* keys, uint64_t* vals, int64_t n, int bits);
+
+// synth.cu
+void synth(Ctx& c, const Grid& g, int kind, const double* h_gauss, int n_gauss, double noise_amp,
+           uint64_t seed, int levels, float* field);
+
+}  // namespace plmss_b200
