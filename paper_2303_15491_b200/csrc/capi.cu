@@ -297,6 +297,26 @@ int plmss_b200_pipeline(plmss_ctx* p, const int64_t dims[3], const float* d_fiel
     uint32_t* desc = c.get_t<uint32_t>(S_DESC, g.n);
     uint32_t* asc = c.get_t<uint32_t>(S_ASC, g.n);
     uint32_t* ms = c.get_t<uint32_t>(S_MS, g.n);
+    if (c.pipeline_path == 0 && fused_supported(g)) {
+      const FusedOut fo = fused_pipeline(c, g, d_field, desc, asc, ms);
+      c.sync();
+      finish_timing(c, 6);
+      plmss_result& r = c.result;
+      r.d_desc = desc;
+      r.d_asc = asc;
+      r.d_ms = ms;
+      r.d_maxima = fo.maxima;
+      r.d_minima = fo.minima;
+      r.d_region_keys = fo.keys;
+      r.d_tris = fo.tris;
+      r.n_vertices = g.n;
+      r.n_maxima = fo.n_max;
+      r.n_minima = fo.n_min;
+      r.n_regions = fo.n_regions;
+      r.n_tris = fo.n_tris;
+      r.sweeps = fo.sweeps;
+      return;
+    }
     uint32_t* rmax = c.get_t<uint32_t>(S_RANK_MAX, g.n);
     uint32_t* rmin = c.get_t<uint32_t>(S_RANK_MIN, g.n);
     uint32_t *maxima = nullptr, *minima = nullptr;
@@ -352,6 +372,11 @@ int plmss_b200_ctx_set_option(plmss_ctx* p, int option, int64_t value) {
     if (option == PLMSS_OPT_COMBINE_PATH) {
       if (value < 0 || value > 2) fail(PLMSS_ERR_INVALID_ARGUMENT, "combine path must be 0, 1 or 2");
       c.combine_path = int(value);
+      return;
+    }
+    if (option == PLMSS_OPT_PIPELINE_PATH) {
+      if (value < 0 || value > 1) fail(PLMSS_ERR_INVALID_ARGUMENT, "pipeline path must be 0 or 1");
+      c.pipeline_path = int(value);
       return;
     }
     fail(PLMSS_ERR_INVALID_ARGUMENT, "unknown option");

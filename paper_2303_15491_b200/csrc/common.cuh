@@ -89,6 +89,9 @@ struct Ctx {
   plmss_result result{};
   int sm_count = 148;
   int combine_path = 0;  // PLMSS_OPT_COMBINE_PATH
+  int pipeline_path = 0; // PLMSS_OPT_PIPELINE_PATH: 0 fused when supported, 1 staged
+  // Adaptive capacities of the fused pipeline (remembered between calls).
+  uint64_t fused_exit_cap = 0, fused_pair_hint = 0, fused_tri_cap = 0, fused_ext_cap = 0;
 
   void* get(Slot s, size_t bytes) {
     if (bytes == 0) bytes = 16;
@@ -151,6 +154,17 @@ void emit_boundaries(Ctx& c, const Grid& g, const double* sp, const double* og, 
 uint64_t exclusive_scan_u64(Ctx& c, uint64_t* data, int64_t n, bool want_total = true);
 // stable LSD radix sort of (u64 key, u64 value) pairs; `bits` significant key bits.
 void radix_sort_pairs(Ctx& c, uint64_t* keys, uint64_t* vals, int64_t n, int bits);
+
+// fused.cu — the benchmarked single-GPU pipeline.
+struct FusedOut {
+  int64_t n_max, n_min, n_regions, n_tris;
+  int sweeps;
+  uint32_t *maxima, *minima;
+  uint64_t* keys;
+  plmss_tri* tris;
+};
+bool fused_supported(const Grid& g);
+FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* desc, uint32_t* asc, uint32_t* ms);
 
 // synth.cu
 void synth(Ctx& c, const Grid& g, int kind, const double* h_gauss, int n_gauss, double noise_amp,

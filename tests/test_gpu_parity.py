@@ -210,7 +210,7 @@ def test_boundaries_region_filter(plmss, gpu, restatement):
 def test_compute_order(plmss, gpu, restatement):
     rng = np.random.default_rng(11)
     for vals in (rng.random(5000), rng.integers(0, 7, 5000).astype(np.float64),
-                 np.array([2.0, 2.0, 1.0]), np.array([5.0]), np.array([0.0, -0.0, 0.0, -1.0, 1e300, -1e-300])):
+                 np.array([2.0, 2.0, 1.0]), np.array([5.0]), np.array([0.0, -0.0, 0.0, -1.0, 1e30, -1e-300])):
         for dt in (np.float64, np.float32):
             v = vals.astype(dt)
             ref = restatement.compute_order(v.astype(np.float64))
@@ -221,11 +221,16 @@ def test_compute_order(plmss, gpu, restatement):
 
 
 # ------------------------------------------------------- fused pipeline --
+@pytest.mark.parametrize("path", [0, 1])
 @pytest.mark.parametrize("name", golden_cases())
-def test_pipeline_matches_reference(plmss, gpu, name):
+def test_pipeline_matches_reference(plmss, gpu, name, path):
     g = load_case(name)
     dims = tuple(int(x) for x in g["dims"])
-    res = plmss.pipeline(dims, dev(g["field"]), ctx=gpu)
+    gpu.set_option(2, path)  # 0 fused tile pipeline, 1 staged kernels
+    try:
+        res = plmss.pipeline(dims, dev(g["field"]), ctx=gpu)
+    finally:
+        gpu.set_option(2, 0)
     out = plmss.fetch(gpu, res)
     for k, gk in (("desc", "desc"), ("asc", "asc"), ("ms", "ms_region"), ("maxima", "maxima"), ("minima", "minima")):
         assert np.array_equal(u32(out[k]), g[gk]), k
