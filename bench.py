@@ -42,8 +42,12 @@ UNIT = "Gvertices/s"
 B_PER_VERTEX = 16
 B_PER_TRI = 16
 # Per-stage algorithmic bytes per vertex.
-STAGES = ["hops", "compress", "extrema", "combine", "marching"]
-STAGE_BYTES_PER_VERTEX = {"hops": 12, "compress": 16, "extrema": 8, "combine": 12, "marching": 4}
+STAGES = ["tile_segment", "exit_resolve", "extrema_sort", "region_ids", "finalize_march"]
+# Compulsory bytes per vertex of each fused stage: tile_segment
+# reads f and writes the two partial-label arrays; region_ids reads both label
+# arrays; finalize_march reads both and writes desc, asc, ms (+16 B/triangle).
+STAGE_BYTES_PER_VERTEX = {"tile_segment": 12, "exit_resolve": 0, "extrema_sort": 0, "region_ids": 8,
+                          "finalize_march": 20}
 
 
 def peaks():
@@ -263,7 +267,8 @@ def main():
     stage_ms /= args.steps
     stage = {STAGES[i]: round(float(stage_ms[i]), 4) for i in range(5)}
     dom = max(STAGES, key=lambda s: stage[s])
-    dom_bytes = STAGE_BYTES_PER_VERTEX[dom] * nv + (B_PER_TRI * n_tris if dom == "marching" else 0)
+    dom_bytes = STAGE_BYTES_PER_VERTEX[dom] * nv + (B_PER_TRI * n_tris if dom == "finalize_march" else 0)
+    stats = ctx.stats().tolist()
     dom_gbs = dom_bytes / (stage[dom] * 1e-3) / 1e9
     pipe_gbs = b_alg / (ms * 1e-3) / 1e9
     traffic = None
@@ -336,7 +341,7 @@ def main():
                    "l2": "inputs larger than L2 (4 GiB field vs 126 MB L2)",
                    "parallelism": f"replica x{world}" if world > 1 else "1 GPU",
                    "vertices": nv, "triangles": n_tris, "regions": res.n_regions, "maxima": res.n_maxima,
-                   "minima": res.n_minima, "sweeps": res.sweeps},
+                   "minima": res.n_minima, "sweeps": res.sweeps, "exit_entries": stats[0]},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(dom_gbs, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(dom_gbs / peak, 4), "traffic": traffic, "peak_source": peak_src,
                      "alg_bytes": dom_bytes},

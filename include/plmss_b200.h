@@ -94,6 +94,9 @@ size_t plmss_b200_ctx_scratch_bytes(const plmss_ctx* ctx);
  * Only filled when timing is enabled. */
 int plmss_b200_ctx_set_timing(plmss_ctx* ctx, int enable);
 int plmss_b200_ctx_stage_ms(const plmss_ctx* ctx, float out[8]);
+/* Diagnostics of the last fused pipeline call: [0] exit-graph entries,
+ * [1] pass-A capacity retries, [2] region-set capacity, [3] finalize retries. */
+int plmss_b200_ctx_stats(const plmss_ctx* ctx, int64_t out[8]);
 
 /* ---- order field --------------------------------------------------------
  * Replaces compute_order (orderfield.hpp:35, orderfield.cpp:12-32): d_rank[v]

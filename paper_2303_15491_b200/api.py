@@ -34,7 +34,7 @@ HEADER_FUNCTIONS = [
     "plmss_b200_combine_ms", "plmss_b200_index_separators", "plmss_b200_emit_separators",
     "plmss_b200_materialize_separators", "plmss_b200_emit_boundaries", "plmss_b200_pipeline",
     "plmss_b200_result", "plmss_b200_copy", "plmss_b200_ctx_set_option", "plmss_b200_pipeline_host",
-    "plmss_b200_synth", "plmss_b200_launch_count",
+    "plmss_b200_synth", "plmss_b200_launch_count", "plmss_b200_ctx_stats",
 ]
 
 
@@ -67,6 +67,7 @@ def lib() -> C.CDLL:
         L.plmss_b200_ctx_scratch_bytes.restype = C.c_size_t
         L.plmss_b200_ctx_set_timing.argtypes = [vp, i32]
         L.plmss_b200_ctx_stage_ms.argtypes = [vp, vp]
+        L.plmss_b200_ctx_stats.argtypes = [vp, vp]
         L.plmss_b200_ctx_set_option.argtypes = [vp, i32, i64]
         L.plmss_b200_compute_order.argtypes = [vp, i32, vp, i64, vp]
         L.plmss_b200_segment.argtypes = [vp, vp, i32, vp, i32, vp, vp, vp, vp, vp, vp, vp]
@@ -154,6 +155,11 @@ class Context:
     def stage_ms(self):
         out = np.zeros(8, np.float32)
         _check(lib().plmss_b200_ctx_stage_ms(self.h, out.ctypes.data))
+        return out
+
+    def stats(self):
+        out = np.zeros(8, np.int64)
+        _check(lib().plmss_b200_ctx_stats(self.h, out.ctypes.data))
         return out
 
     def set_option(self, option: int, value: int):

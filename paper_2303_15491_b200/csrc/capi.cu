@@ -162,6 +162,13 @@ int plmss_b200_ctx_stage_ms(const plmss_ctx* p, float out[8]) {
   });
 }
 
+int plmss_b200_ctx_stats(const plmss_ctx* p, int64_t out[8]) {
+  return guarded([&] {
+    if (!p) fail(PLMSS_ERR_INVALID_ARGUMENT, "null context");
+    memcpy(out, p->c.stats, sizeof(p->c.stats));
+  });
+}
+
 int plmss_b200_compute_order(plmss_ctx* p, int key_type, const void* d_values, int64_t n, int64_t* d_rank) {
   return guarded([&] {
     Ctx& c = C(p);

@@ -92,6 +92,9 @@ struct Ctx {
   int pipeline_path = 0; // PLMSS_OPT_PIPELINE_PATH: 0 fused when supported, 1 staged
   // Adaptive capacities of the fused pipeline (remembered between calls).
   uint64_t fused_exit_cap = 0, fused_pair_hint = 0, fused_tri_cap = 0, fused_ext_cap = 0;
+  // Diagnostics of the last fused call: [0] exit entries, [1] pass-A retries,
+  // [2] region-set capacity, [3] finalize retries.
+  int64_t stats[8] = {};
 
   void* get(Slot s, size_t bytes) {
     if (bytes == 0) bytes = 16;

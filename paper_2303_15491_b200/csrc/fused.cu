@@ -94,8 +94,7 @@ __global__ void __launch_bounds__(A_THREADS, 2)
     k_tile_segment(const float* __restrict__ field, FDims d, uint32_t* __restrict__ desc,
                    uint32_t* __restrict__ asc, uint32_t* __restrict__ maxima, uint32_t* __restrict__ minima,
                    uint64_t ext_cap, uint32_t* __restrict__ exits, uint64_t exit_cap,
-                   unsigned long long* __restrict__ pairs,
-                   uint64_t pair_mask, ACounters* __restrict__ ctr) {
+                   ACounters* __restrict__ ctr) {
   extern __shared__ __align__(16) unsigned char a_smem[];
   float* f = reinterpret_cast<float*>(a_smem);                   // HN floats
   uint16_t* Pd = reinterpret_cast<uint16_t*>(a_smem + 4 * HN);   // TN
@@ -245,11 +244,6 @@ __global__ void __launch_bounds__(A_THREADS, 2)
       const uint64_t pos = base + __popc(m & ((1u << lane) - 1));
       if (is_min && pos < ext_cap) minima[pos] = la;
     }
-    // distinct partial pairs (warp dedup, then the global set)
-    const uint64_t key = valid ? ((uint64_t(la) << 32) | ld) : kEmpty;
-    const unsigned peers = __match_any_sync(0xffffffffu, key);
-    if (valid && (peers & ((1u << lane) - 1)) == 0)
-      if (!set_insert(pairs, pair_mask, key)) ctr->overflow = 1;
   }
 
   // 5. exit targets of this tile -> E
@@ -367,21 +361,23 @@ __global__ void __launch_bounds__(kCThreads) k_write_occ(const unsigned long lon
   }
 }
 
-__global__ void __launch_bounds__(256) k_final_pairs(const uint64_t* __restrict__ partial, int64_t np,
-                                                     const uint32_t* __restrict__ desc,
-                                                     const uint32_t* __restrict__ asc,
-                                                     unsigned long long* __restrict__ fset, uint64_t fmask,
-                                                     int* __restrict__ overflow) {
-  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  const bool ok = i < np;
-  uint64_t key = kEmpty;
-  if (ok) {
-    const uint64_t p = partial[i];
-    key = (uint64_t(asc[uint32_t(p >> 32)]) << 32) | desc[uint32_t(p)];
+// Final (asc, desc) pair of every vertex = (asc[asc[v]], desc[desc[v]])
+// (partial labels point at roots or at resolved exit vertices), inserted into
+// the region set with warp-level dedup.
+__global__ void __launch_bounds__(256) k_mark_pairs(uint32_t n, const uint32_t* __restrict__ desc,
+                                                    const uint32_t* __restrict__ asc,
+                                                    unsigned long long* __restrict__ fset, uint64_t fmask,
+                                                    int* __restrict__ overflow) {
+  const int lane = threadIdx.x & 31;
+  for (uint32_t base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
+    const uint32_t v = base + threadIdx.x;
+    const bool ok = v < n;
+    uint64_t key = kEmpty;
+    if (ok) key = (uint64_t(__ldg(asc + __ldg(asc + v))) << 32) | __ldg(desc + __ldg(desc + v));
+    const unsigned peers = __match_any_sync(0xffffffffu, key);
+    if (ok && (peers & ((1u << lane) - 1)) == 0)
+      if (!set_insert(fset, fmask, key)) *overflow = 1;
   }
-  const unsigned peers = __match_any_sync(0xffffffffu, key);
-  if (ok && (peers & ((1u << (threadIdx.x & 31)) - 1)) == 0)
-    if (!set_insert(fset, fmask, key)) *overflow = 1;
 }
 
 __global__ void k_set_ids(const uint64_t* __restrict__ sorted_slots, int64_t r, uint32_t* __restrict__ slot_id) {
@@ -632,17 +628,12 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
     uint32_t* maxima = c.get_t<uint32_t>(S_MAXIMA, ext_cap);
     uint32_t* minima = c.get_t<uint32_t>(S_MINIMA, ext_cap);
     const uint64_t exit_cap = c.fused_exit_cap ? c.fused_exit_cap : uint64_t(g.n / 4 + 1024);
-    uint64_t pcap = 1024;
-    const uint64_t want = c.fused_pair_hint ? c.fused_pair_hint * 2 : std::min<uint64_t>(g.n / 8 + 1024, 1u << 22);
-    while (pcap < want) pcap <<= 1;
     uint32_t* E = c.get_t<uint32_t>(S_TMP0, exit_cap);
-    auto* pairs = c.get_t<unsigned long long>(S_HASH_K, pcap);
-    CK(cudaMemsetAsync(pairs, 0xff, pcap * 8, c.stream));
     CK(cudaMemsetAsync(ctr, 0, sizeof(ACounters), c.stream));
     CK(cudaMemsetAsync(&ctr->bad, 0xff, 4, c.stream));
     c.mark(0);
     k_tile_segment<<<unsigned(ntiles), A_THREADS, kASmem, c.stream>>>(field, d, desc, asc, maxima, minima, ext_cap, E,
-                                                                  exit_cap, pairs, pcap - 1, ctr);
+                                                                  exit_cap, ctr);
     CK_LAUNCH("k_tile_segment");
     c.mark(1);
     ACounters h;
@@ -656,10 +647,6 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
       c.fused_exit_cap = h.n_exit + h.n_exit / 4 + 1024;
       retry = true;
     }
-    if (h.overflow) {
-      c.fused_pair_hint = pcap * 2;
-      retry = true;
-    }
     if (h.n_max > ext_cap || h.n_min > ext_cap) {
       c.fused_ext_cap = std::max(h.n_max, h.n_min) + 1024;
       retry = true;
@@ -668,6 +655,8 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
       if (attempt > 6) fail(PLMSS_ERR_LOGIC, "fused pipeline capacity retries exhausted");
       continue;
     }
+    c.stats[0] = int64_t(h.n_exit);
+    c.stats[1] = attempt;
     o.n_max = int64_t(h.n_max);
     o.n_min = int64_t(h.n_min);
     // ---- B: exit graph to the fixpoint
@@ -702,28 +691,32 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
       }
     }
     c.mark(3);
-    // ---- C: partial pairs -> final pairs -> dense ids
-    const int64_t tb = int64_t((pcap + kCTile - 1) / kCTile);
-    uint64_t* counts = c.get_t<uint64_t>(S_TMP1, tb);
-    k_count_occ<<<unsigned(tb), kCThreads, 0, c.stream>>>(pairs, pcap, counts);
-    CK_LAUNCH("k_count_occ");
-    const int64_t np = int64_t(exclusive_scan_u64(c, counts, tb, true));
-    c.fused_pair_hint = uint64_t(np);
-    uint64_t* plist = c.get_t<uint64_t>(S_SORT_A, np);
-    k_write_occ<<<unsigned(tb), kCThreads, 0, c.stream>>>(pairs, pcap, counts, plist, nullptr);
-    CK_LAUNCH("k_write_occ");
+    // ---- C: final pairs of all vertices -> unique, sorted -> dense ids
     uint64_t fcap = 1024;
-    while (fcap < uint64_t(np) * 2) fcap <<= 1;
-    auto* fset = c.get_t<unsigned long long>(S_HASH_V, fcap);
-    CK(cudaMemsetAsync(fset, 0xff, fcap * 8, c.stream));
-    CK(cudaMemsetAsync(flag, 0, 4, c.stream));
-    k_final_pairs<<<blocks_for(np, 256), 256, 0, c.stream>>>(plist, np, desc, asc, fset, fcap - 1, flag);
-    CK_LAUNCH("k_final_pairs");
+    {
+      const uint64_t want = c.fused_pair_hint ? c.fused_pair_hint * 2 : uint64_t(1) << 20;
+      while (fcap < want) fcap <<= 1;
+    }
+    unsigned long long* fset = nullptr;
+    for (int tries = 0;; ++tries) {
+      fset = c.get_t<unsigned long long>(S_HASH_V, fcap);
+      CK(cudaMemsetAsync(fset, 0xff, fcap * 8, c.stream));
+      CK(cudaMemsetAsync(flag, 0, 4, c.stream));
+      k_mark_pairs<<<unsigned(std::min<int64_t>((g.n + 255) / 256, int64_t(c.sm_count) * 16)), 256, 0, c.stream>>>(
+          d.n, desc, asc, fset, fcap - 1, flag);
+      CK_LAUNCH("k_mark_pairs");
+      CK(cudaMemcpyAsync(c.h_pinned, flag, 4, cudaMemcpyDeviceToHost, c.stream));
+      c.sync();
+      if (*reinterpret_cast<int*>(c.h_pinned) == 0) break;
+      if (fcap >= 4 * uint64_t(g.n) || tries > 8) fail(PLMSS_ERR_LOGIC, "region set overflow");
+      fcap <<= 2;
+    }
     const int64_t fb = int64_t((fcap + kCTile - 1) / kCTile);
     uint64_t* fcounts = c.get_t<uint64_t>(S_TMP2, fb);
     k_count_occ<<<unsigned(fb), kCThreads, 0, c.stream>>>(fset, fcap, fcounts);
     CK_LAUNCH("k_count_occ");
     const int64_t R = int64_t(exclusive_scan_u64(c, fcounts, fb, true));
+    c.fused_pair_hint = uint64_t(R);
     uint64_t* keys = c.get_t<uint64_t>(S_KEYS, R);
     uint64_t* slots = c.get_t<uint64_t>(S_SORT_B, R);
     k_write_occ<<<unsigned(fb), kCThreads, 0, c.stream>>>(fset, fcap, fcounts, keys, slots);
@@ -735,6 +728,7 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
     k_set_ids<<<blocks_for(R, 256), 256, 0, c.stream>>>(slots, R, slot_id);
     CK_LAUNCH("k_set_ids");
     o.n_regions = R;
+    c.stats[2] = int64_t(fcap);
     c.mark(4);
     // ---- D: ordered finalize + MS ids + marching
     DDims dd;
