@@ -42,12 +42,13 @@ UNIT = "Gvertices/s"
 B_PER_VERTEX = 16
 B_PER_TRI = 16
 # Per-stage algorithmic bytes per vertex.
-STAGES = ["tile_segment", "exit_resolve", "extrema_sort", "region_ids", "finalize_march"]
+STAGES = ["tile_segment", "exit_resolve", "extrema_sort", "finalize_ids", "march"]
 # Compulsory bytes per vertex of each fused stage: tile_segment
-# reads f and writes the two partial-label arrays; region_ids reads both label
-# arrays; finalize_march reads both and writes desc, asc, ms (+16 B/triangle).
-STAGE_BYTES_PER_VERTEX = {"tile_segment": 12, "exit_resolve": 0, "extrema_sort": 0, "region_ids": 8,
-                          "finalize_march": 20}
+# reads f, writes the two partial-label arrays; finalize_ids reads the partial
+# labels, writes final desc/asc, reads them again and writes ms; march reads
+# ms and writes 16 B per separator triangle.
+STAGE_BYTES_PER_VERTEX = {"tile_segment": 12, "exit_resolve": 0, "extrema_sort": 0, "finalize_ids": 28,
+                          "march": 4}
 
 
 def peaks():
@@ -267,7 +268,7 @@ def main():
     stage_ms /= args.steps
     stage = {STAGES[i]: round(float(stage_ms[i]), 4) for i in range(5)}
     dom = max(STAGES, key=lambda s: stage[s])
-    dom_bytes = STAGE_BYTES_PER_VERTEX[dom] * nv + (B_PER_TRI * n_tris if dom == "finalize_march" else 0)
+    dom_bytes = STAGE_BYTES_PER_VERTEX[dom] * nv + (B_PER_TRI * n_tris if dom == "march" else 0)
     stats = ctx.stats().tolist()
     dom_gbs = dom_bytes / (stage[dom] * 1e-3) / 1e9
     pipe_gbs = b_alg / (ms * 1e-3) / 1e9

@@ -48,9 +48,6 @@ struct FDims {
   uint32_t tx, ty, tz;  // tile counts
 };
 
-__device__ __forceinline__ bool higher(float ku, uint32_t u, float kv, uint32_t v) {
-  return ku > kv || (ku == kv && u > v);
-}
 
 __device__ __forceinline__ uint64_t mix64(uint64_t x) {
   x ^= x >> 33;
@@ -83,6 +80,19 @@ __device__ __forceinline__ uint64_t set_find(const unsigned long long* __restric
   return s;
 }
 
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// Stencil offset s as 2-bit-per-axis code (x low), selected without local
+// memory: a 14-entry x 6-bit table packed into two 64-bit immediates.
+__device__ __forceinline__ uint32_t kOffTable(int s) {
+  constexpr uint64_t lo = 0x00ull | 0x01ull << 6 | 0x04ull << 12 | 0x05ull << 18 | 0x10ull << 24 | 0x11ull << 30 |
+                          0x14ull << 36 | 0x16ull << 42 | 0x19ull << 48 | 0x1aull << 54;
+  constexpr uint64_t hi = 0x25ull | 0x26ull << 6 | 0x29ull << 12 | 0x2aull << 18;
+  return s < 10 ? uint32_t((lo >> (6 * s)) & 63) : uint32_t((hi >> (6 * (s - 10))) & 63);
+}
+
 struct ACounters {
   unsigned long long n_max, n_min, n_exit;
   int overflow;
@@ -107,11 +117,13 @@ __global__ void __launch_bounds__(A_THREADS, 2)
   const uint32_t tx = bt % d.tx, ty = (bt / d.tx) % d.ty, tz = bt / (d.tx * d.ty);
   const int gx0 = int(tx * TX), gy0 = int(ty * TY), gz0 = int(tz * TZ);
 
-  // 1. halo'd tile of f (x-rows are contiguous in global memory)
+  // 1. halo'd tile of f (x-rows are contiguous in global memory). Vertices
+  //    outside the volume hold NaN: fmaxf/fminf ignore NaN and NaN == x is
+  //    false, so a missing neighbour can never be selected.
   for (int i = threadIdx.x; i < HN; i += A_THREADS) {
     const int hx = i % HX, hy = (i / HX) % HY, hz = i / (HX * HY);
     const int gx = gx0 + hx - 1, gy = gy0 + hy - 1, gz = gz0 + hz - 1;
-    float val = 0.f;
+    float val = __int_as_float(0x7fc00000);
     if (gx >= 0 && gx < int(d.X) && gy >= 0 && gy < int(d.Y) && gz >= 0 && gz < int(d.Z))
       val = __ldg(field + (uint32_t(gx) + d.X * (uint32_t(gy) + d.Y * uint32_t(gz))));
     f[i] = val;
@@ -120,9 +132,12 @@ __global__ void __launch_bounds__(A_THREADS, 2)
   if (threadIdx.x == 0) s_cnt = 0;
   __syncthreads();
 
-  // 2. hops
-  // The 14 stencil offsets (nonzero components share a sign), as bit codes:
-  // per offset 2 bits per axis (0 = -1, 1 = 0, 2 = +1), x low.
+  // 2. hops. Stencil s = 0..13 in ascending id-delta order (complex.cpp:78-88);
+  //    the vertex itself sits between s = 6 and s = 7. With M = max f over the
+  //    neighbours, the steepest-up vertex under (f, id) order is the highest s
+  //    with f == M when M > f(v), or when M == f(v) and that s > 6 (a larger
+  //    id); otherwise v itself. Steepest-down mirrors it (lowest s, s < 7).
+  //    bit codes: 2 bits per axis (0 = -1, 1 = 0, 2 = +1), x low.
   constexpr uint32_t kOff[14] = {0x00, 0x01, 0x04, 0x05, 0x10, 0x11, 0x14,
                                  0x16, 0x19, 0x1a, 0x25, 0x26, 0x29, 0x2a};
 #pragma unroll 1
@@ -136,38 +151,37 @@ __global__ void __launch_bounds__(A_THREADS, 2)
       continue;
     }
     const int h = (lz + 1) * HX * HY + (ly + 1) * HX + (lx + 1);
-    const uint32_t gv = uint32_t(gx) + d.X * (uint32_t(gy) + d.Y * uint32_t(gz));
     const float fv = f[h];
-    if (!isfinite(fv)) atomicMin(&ctr->bad, gv);
-    float fu = fv, fd = fv;
-    uint32_t iu = gv, id = gv;
-    uint16_t pu = TERM | uint16_t(l), pd = TERM | uint16_t(l);
+    if (!isfinite(fv)) atomicMin(&ctr->bad, uint32_t(gx) + d.X * (uint32_t(gy) + d.Y * uint32_t(gz)));
+    float fn[14];
 #pragma unroll
     for (int s = 0; s < 14; ++s) {
       const int dx = int(kOff[s] & 3) - 1, dy = int((kOff[s] >> 2) & 3) - 1, dz = int((kOff[s] >> 4) & 3) - 1;
-      const int nx = gx + dx, ny = gy + dy, nz = gz + dz;
-      const bool ok = nx >= 0 && nx < int(d.X) && ny >= 0 && ny < int(d.Y) && nz >= 0 && nz < int(d.Z);
-      if (!ok) continue;
-      const int ho = dx + HX * dy + HX * HY * dz;
-      const float fn = f[h + ho];
-      const uint32_t gn = uint32_t(int(gv) + dx + int(d.X) * dy + int(d.XY) * dz);
-      const bool up = higher(fn, gn, fu, iu), dn = higher(fd, id, fn, gn);
-      if (up || dn) {
-        const int mx = lx + dx, my = ly + dy, mz = lz + dz;
-        const bool inside = mx >= 0 && mx < TX && my >= 0 && my < TY && mz >= 0 && mz < TZ;
-        const uint16_t e = inside ? uint16_t(l + dx + TX * dy + TX * TY * dz) : uint16_t(TERM | EXIT | (h + ho));
-        if (up) {
-          fu = fn;
-          iu = gn;
-          pu = e;
-        }
-        if (dn) {
-          fd = fn;
-          id = gn;
-          pd = e;
-        }
-      }
+      fn[s] = f[h + dx + HX * dy + HX * HY * dz];
     }
+    float M = fn[0], m = fn[0];
+#pragma unroll
+    for (int s = 1; s < 14; ++s) {
+      M = fmaxf(M, fn[s]);
+      m = fminf(m, fn[s]);
+    }
+    int su = -1, sd = -1;
+#pragma unroll
+    for (int s = 0; s < 14; ++s) su = fn[s] == M ? s : su;  // highest s attaining M
+#pragma unroll
+    for (int s = 13; s >= 0; --s) sd = fn[s] == m ? s : sd;  // lowest s attaining m
+    if (!(M > fv || (M == fv && su > 6))) su = -1;
+    if (!(m < fv || (m == fv && sd < 7))) sd = -1;
+    auto enc = [&](int s) -> uint16_t {
+      if (s < 0) return TERM | uint16_t(l);
+      const uint32_t o = kOffTable(s);
+      const int dx = int(o & 3) - 1, dy = int((o >> 2) & 3) - 1, dz = int((o >> 4) & 3) - 1;
+      const int mx = lx + dx, my = ly + dy, mz = lz + dz;
+      const bool inside = mx >= 0 && mx < TX && my >= 0 && my < TY && mz >= 0 && mz < TZ;
+      return inside ? uint16_t(l + dx + TX * dy + TX * TY * dz)
+                    : uint16_t(TERM | EXIT | (h + dx + HX * dy + HX * HY * dz));
+    };
+    const uint16_t pu = enc(su), pd = enc(sd);
     Pd[l] = pu;
     Pa[l] = pd;
     if ((pu & (TERM | EXIT)) == (TERM | EXIT)) xflag[pu & 0x3fff] = 1;
@@ -275,7 +289,12 @@ __global__ void __launch_bounds__(A_THREADS, 2)
 }
 
 // ---------------------------------------------------------------- pass B --
-constexpr int kExitHops = 8;
+// Chain following on the live arrays: each exit vertex walks up to kChase
+// links (both directions interleaved for memory-level parallelism) and
+// stores the furthest vertex reached. Values read from entries other
+// threads have already advanced only shorten the walk; every value lies on
+// the vertex's chain, so concurrent updates are safe.
+constexpr int kChase = 16;
 
 __global__ void __launch_bounds__(256) k_exit_jump(const uint32_t* __restrict__ E, uint64_t ne,
                                                    uint32_t* __restrict__ desc, uint32_t* __restrict__ asc,
@@ -284,21 +303,21 @@ __global__ void __launch_bounds__(256) k_exit_jump(const uint32_t* __restrict__ 
   bool ch = false;
   if (i < ne) {
     const uint32_t e = E[i];
-#pragma unroll
-    for (int dir = 0; dir < 2; ++dir) {
-      uint32_t* lab = dir ? asc : desc;
-      const uint32_t l0 = lab[e];
-      uint32_t l = l0;
-      for (int k = 0; k < kExitHops; ++k) {
-        const uint32_t nx = lab[l];
-        if (nx == l) break;
-        l = nx;
-      }
-      if (l != l0) {
-        lab[e] = l;
-        ch |= lab[l] != l;
-      }
+    const uint32_t d0 = desc[e], a0 = asc[e];
+    uint32_t xd = d0, xa = a0;
+    bool dd = false, da = false;
+#pragma unroll 4
+    for (int k = 0; k < kChase && !(dd && da); ++k) {
+      const uint32_t nd = dd ? xd : desc[xd];
+      const uint32_t na = da ? xa : asc[xa];
+      dd = nd == xd;
+      da = na == xa;
+      xd = nd;
+      xa = na;
     }
+    if (xd != d0) desc[e] = xd;
+    if (xa != a0) asc[e] = xa;
+    ch = !(dd && da);
   }
   if (__any_sync(0xffffffffu, ch) && (threadIdx.x & 31) == 0) *changed = 1;
 }
@@ -361,22 +380,51 @@ __global__ void __launch_bounds__(kCThreads) k_write_occ(const unsigned long lon
   }
 }
 
-// Final (asc, desc) pair of every vertex = (asc[asc[v]], desc[desc[v]])
-// (partial labels point at roots or at resolved exit vertices), inserted into
-// the region set with warp-level dedup.
-__global__ void __launch_bounds__(256) k_mark_pairs(uint32_t n, const uint32_t* __restrict__ desc,
-                                                    const uint32_t* __restrict__ asc,
+// Pass C: final labels in place, desc[v] <- desc[desc[v]] (partial labels
+// point at roots or at exit vertices already resolved by pass B, and those
+// entries never change value here), and every final (asc, desc) pair into
+// the region set with warp-level dedup. 4 vertices per thread per step keep
+// enough independent loads in flight.
+constexpr int C_VPT = 4;
+// Vertices are visited in pass-A tile order (32x16x16 bricks, x-rows of 32
+// inside), so the gathers desc[desc[v]] hit the few exit vertices around the
+// brick while they are still in L2.
+__global__ void __launch_bounds__(256) k_mark_pairs(FDims dm, uint32_t* __restrict__ desc,
+                                                    uint32_t* __restrict__ asc,
                                                     unsigned long long* __restrict__ fset, uint64_t fmask,
                                                     int* __restrict__ overflow) {
   const int lane = threadIdx.x & 31;
-  for (uint32_t base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
-    const uint32_t v = base + threadIdx.x;
-    const bool ok = v < n;
-    uint64_t key = kEmpty;
-    if (ok) key = (uint64_t(__ldg(asc + __ldg(asc + v))) << 32) | __ldg(desc + __ldg(desc + v));
-    const unsigned peers = __match_any_sync(0xffffffffu, key);
-    if (ok && (peers & ((1u << lane) - 1)) == 0)
-      if (!set_insert(fset, fmask, key)) *overflow = 1;
+  const uint64_t total = uint64_t(dm.tx) * dm.ty * dm.tz * TN;
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x * C_VPT;
+  for (uint64_t base = uint64_t(blockIdx.x) * blockDim.x * C_VPT; base < total; base += stride) {
+    uint32_t v[C_VPT], pd[C_VPT], pa[C_VPT], fd[C_VPT], fa[C_VPT];
+    bool okv[C_VPT];
+#pragma unroll
+    for (int k = 0; k < C_VPT; ++k) {
+      const uint64_t idx = base + uint64_t(k) * blockDim.x + threadIdx.x;
+      const uint32_t t = uint32_t(idx / TN), l = uint32_t(idx % TN);
+      const uint32_t tx = t % dm.tx, ty = (t / dm.tx) % dm.ty, tz = t / (dm.tx * dm.ty);
+      const uint32_t x = tx * TX + (l % TX), y = ty * TY + ((l / TX) % TY), z = tz * TZ + l / (TX * TY);
+      okv[k] = idx < total && x < dm.X && y < dm.Y && z < dm.Z;
+      v[k] = x + dm.X * (y + dm.Y * z);
+      pd[k] = okv[k] ? desc[v[k]] : 0;
+      pa[k] = okv[k] ? asc[v[k]] : 0;
+    }
+#pragma unroll
+    for (int k = 0; k < C_VPT; ++k) {
+      fd[k] = okv[k] ? desc[pd[k]] : 0;
+      fa[k] = okv[k] ? asc[pa[k]] : 0;
+    }
+#pragma unroll
+    for (int k = 0; k < C_VPT; ++k) {
+      const bool ok = okv[k];
+      if (ok && fd[k] != pd[k]) desc[v[k]] = fd[k];
+      if (ok && fa[k] != pa[k]) asc[v[k]] = fa[k];
+      const uint64_t key = ok ? ((uint64_t(fa[k]) << 32) | fd[k]) : kEmpty;
+      const unsigned peers = __match_any_sync(0xffffffffu, key);
+      if (ok && (peers & ((1u << lane) - 1)) == 0)
+        if (!set_insert(fset, fmask, key)) *overflow = 1;
+    }
   }
 }
 
@@ -400,6 +448,38 @@ __global__ void k_u32_to_u64(const uint32_t* __restrict__ in, int64_t n, uint64_
 }
 
 // ---------------------------------------------------------------- pass D --
+// D1: ms[v] = dense id of the final pair (hash value slot), warp-deduped
+// lookups, 4 vertices per thread per step.
+__global__ void __launch_bounds__(256) k_assign_ms(uint32_t n, const uint32_t* __restrict__ desc,
+                                                   const uint32_t* __restrict__ asc,
+                                                   const unsigned long long* __restrict__ fset, uint64_t fmask,
+                                                   const uint32_t* __restrict__ slot_id, uint32_t* __restrict__ ms) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t stride = gridDim.x * blockDim.x * C_VPT;
+  for (uint32_t base = blockIdx.x * blockDim.x * C_VPT; base < n; base += stride) {
+    uint64_t key[C_VPT];
+#pragma unroll
+    for (int k = 0; k < C_VPT; ++k) {
+      const uint32_t v = base + k * blockDim.x + threadIdx.x;
+      key[k] = v < n ? ((uint64_t(__ldg(asc + v)) << 32) | __ldg(desc + v)) : kEmpty;
+    }
+#pragma unroll
+    for (int k = 0; k < C_VPT; ++k) {
+      const uint32_t v = base + k * blockDim.x + threadIdx.x;
+      const unsigned peers = __match_any_sync(0xffffffffu, key[k]);
+      const int leader = __ffs(peers) - 1;
+      uint32_t id = 0;
+      if (lane == leader && key[k] != kEmpty) id = __ldg(slot_id + set_find(fset, fmask, key[k]));
+      id = __shfl_sync(0xffffffffu, id, leader);
+      if (v < n) ms[v] = id;
+    }
+  }
+}
+
+// D2: ordered single-pass marching over row slabs in the reference cell
+// order (cube-major, x fastest): ms rows of the slab plus the +y row and +z
+// layer staged in shared memory, 6 tet codes per cube, block scan, decoupled
+// look-back across slabs for the output offset, records in reference order.
 constexpr int D_THREADS = 512;
 constexpr int D_CUBES = 8192;  // cubes per row-slab tile (target)
 
@@ -422,91 +502,148 @@ __device__ __forceinline__ int tet_code(uint32_t a, uint32_t b, uint32_t c, uint
 
 constexpr uint64_t FLAG_A = uint64_t(1) << 62, FLAG_P = uint64_t(2) << 62, VAL_MASK = (uint64_t(1) << 62) - 1;
 
-__global__ void __launch_bounds__(D_THREADS)
-    k_finalize_march(DDims d, uint32_t* __restrict__ desc, uint32_t* __restrict__ asc, uint32_t* __restrict__ ms,
-                     const unsigned long long* __restrict__ fset, uint64_t fmask,
-                     const uint32_t* __restrict__ slot_id, unsigned long long* __restrict__ tile_state,
-                     unsigned int* __restrict__ ticket, plmss_tri* __restrict__ out, uint64_t out_cap,
-                     unsigned long long* __restrict__ total_out) {
-  extern __shared__ uint32_t s_ms[];  // (ty + 1) rows x 2 layers x X
+__device__ __forceinline__ uint32_t pick4(int i, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  return i == 0 ? a : (i == 1 ? b : (i == 2 ? c : d));
+}
+
+__device__ __forceinline__ int case_count6(uint32_t code6, const uint16_t* cases) {
+  return (cases[code6 & 31] & 15) + (cases[(code6 >> 5) & 31] & 15) + (cases[(code6 >> 10) & 31] & 15) +
+         (cases[(code6 >> 15) & 31] & 15) + (cases[(code6 >> 20) & 31] & 15) + (cases[(code6 >> 25) & 31] & 15);
+}
+
+// Cubes are processed in 32-cube chunks (lane i <-> cube 32*chunk + i), so
+// consecutive lanes touch consecutive shared-memory words (no bank
+// conflicts) and a warp's records land in one contiguous output range.
+constexpr int D_CHUNKS = D_CUBES / 32;
+
+__global__ void __launch_bounds__(D_THREADS, 2)
+    k_march(DDims d, const uint32_t* __restrict__ ms, unsigned long long* __restrict__ tile_state,
+            unsigned int* __restrict__ ticket, plmss_tri* __restrict__ out, uint64_t out_cap, float inv_cx,
+            uint32_t ms_words) {
+  extern __shared__ uint32_t dsm[];
+  uint32_t* s_ms = dsm;                 // (ty + 1) rows x 2 layers x X
+  uint32_t* s_code = dsm + ms_words;    // packed 6 x 5-bit tet codes per cube
+  __shared__ uint32_t s_rows[PLMSS_TET_ROWS];
+  __shared__ uint16_t s_cases[32];
+  __shared__ uint32_t s_chunk[D_CHUNKS];
   __shared__ uint32_t s_tile;
-  __shared__ uint32_t s_wsum[D_THREADS / 32];
   __shared__ unsigned long long s_excl;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+  if (threadIdx.x < PLMSS_TET_ROWS) s_rows[threadIdx.x] = c_rows[threadIdx.x];
+  if (threadIdx.x < 32) s_cases[threadIdx.x] = c_cases[threadIdx.x];
   __syncthreads();
   const uint32_t tile = s_tile;
   const uint32_t z = tile / d.nyb, yb = tile % d.nyb;
   const uint32_t y0 = yb * d.ty, y1 = min(d.Y, y0 + d.ty);
-  const uint32_t rows = min(d.Y, y1 + 1) - y0;     // rows loaded (incl. +1 halo row)
-  const uint32_t layers = z + 1 < d.Z ? 2u : 1u;
-  const uint32_t X = d.X;
+  const uint32_t rows = min(d.Y, y1 + 1) - y0;  // rows staged (incl. the +1 halo row)
+  const bool has_cubes = z + 1 < d.Z && y0 + 1 < d.Y;
+  const uint32_t X = d.X, CX = d.X - 1;
 
-  // 1. finals + dense ids for the slab and its +y / +z halo
-  const uint32_t nload = rows * layers * X;
-  for (uint32_t i = threadIdx.x; i < nload; i += D_THREADS) {
-    const uint32_t x = i % X, r = (i / X) % rows, lz = i / (X * rows);
-    const uint32_t v = x + X * ((y0 + r) + d.Y * (z + lz));
-    const uint32_t pd = desc[v], pa = asc[v];
-    const uint32_t fd = desc[pd], fa = asc[pa];
-    const uint64_t key = (uint64_t(fa) << 32) | fd;
-    // warp dedup of the lookup (neighbouring vertices mostly share a pair)
-    const unsigned peers = __match_any_sync(__activemask(), key);
-    const int leader = __ffs(peers) - 1;
-    uint32_t id = 0;
-    if (lane == leader) id = slot_id[set_find(fset, fmask, key)];
-    id = __shfl_sync(peers, id, leader);
-    s_ms[i] = id;
-    if (lz == 0 && y0 + r < y1) {
-      desc[v] = fd;
-      asc[v] = fa;
-      ms[v] = id;
+  // Stage the slab: two contiguous runs (layer z rows y0.., layer z+1 rows
+  // y0..). With 16-byte alignment they go through the bulk-copy (TMA) engine
+  // on an mbarrier; otherwise an unrolled vector-free loop.
+  __shared__ __align__(8) uint64_t s_bar;
+  if (has_cubes) {
+    const uint32_t rx = rows * X;
+    const uint32_t* src0 = ms + uint64_t(X) * (y0 + uint64_t(d.Y) * z);
+    const uint32_t* src1 = src0 + d.XY;
+    const bool bulk = ((reinterpret_cast<uintptr_t>(src0) | reinterpret_cast<uintptr_t>(src1)) & 15) == 0 &&
+                      (rx & 3) == 0;
+    if (bulk) {
+      const uint32_t bar = smem_u32(&s_bar);
+      if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(rx * 8) : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                smem_u32(s_ms)),
+            "l"(src0), "r"(rx * 4), "r"(bar)
+            : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                smem_u32(s_ms + rx)),
+            "l"(src1), "r"(rx * 4), "r"(bar)
+            : "memory");
+      }
+      asm volatile(
+          "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n @!p bra WAIT_%=;\n}" ::"r"(
+              bar)
+          : "memory");
+    } else {
+      const uint32_t nload = 2 * rx;
+      for (uint32_t i0 = 0; i0 < nload; i0 += 8 * D_THREADS) {
+        uint32_t v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t i = i0 + k * D_THREADS + threadIdx.x;
+          v[k] = i < nload ? __ldg(i < rx ? src0 + i : src1 + (i - rx)) : 0u;
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t i = i0 + k * D_THREADS + threadIdx.x;
+          if (i < nload) s_ms[i] = v[k];
+        }
+      }
     }
   }
   __syncthreads();
 
-  // 2. cubes of this slab: codes and counts
-  const bool has_cubes = z + 1 < d.Z && y0 < d.Y - 1;
   const uint32_t cy1 = min(y1, d.Y - 1);
-  const uint32_t ncubes = has_cubes ? (X - 1) * (cy1 - y0) : 0;
-  constexpr int CPT = (D_CUBES + D_THREADS - 1) / D_THREADS;  // cubes per thread, consecutive
-  const uint32_t per = (ncubes + D_THREADS - 1) / D_THREADS;
-  const uint32_t c0 = threadIdx.x * per, c1 = min(ncubes, c0 + per);
-  uint32_t cnt = 0;
-  for (uint32_t q = c0; q < c1; ++q) {
-    const uint32_t cx = q % (X - 1), cr = q / (X - 1);
-    const uint32_t b = cx + X * cr;
-    const uint32_t o[8] = {b, b + 1, b + X, b + X + 1, b + rows * X, b + rows * X + 1, b + rows * X + X,
-                           b + rows * X + X + 1};
-    uint32_t l[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) l[k] = s_ms[o[k]];
-    cnt += (c_cases[tet_code(l[0], l[1], l[3], l[7])] & 15) + (c_cases[tet_code(l[0], l[1], l[5], l[7])] & 15) +
-           (c_cases[tet_code(l[0], l[2], l[3], l[7])] & 15) + (c_cases[tet_code(l[0], l[2], l[6], l[7])] & 15) +
-           (c_cases[tet_code(l[0], l[4], l[5], l[7])] & 15) + (c_cases[tet_code(l[0], l[4], l[6], l[7])] & 15);
+  const uint32_t ncubes = has_cubes ? CX * (cy1 - y0) : 0;
+  const uint32_t nchunks = (ncubes + 31) / 32;
+  const uint32_t LZ = rows * X;
+  // phase 2: codes and per-chunk counts
+  for (uint32_t ch = w; ch < nchunks; ch += D_THREADS / 32) {
+    const uint32_t q = ch * 32 + lane;
+    uint32_t code6 = 0;
+    int cnt = 0;
+    if (q < ncubes) {
+      const uint32_t cr = uint32_t((float(q) + 0.5f) * inv_cx), cx = q - cr * CX;
+      const uint32_t b = cx + X * cr;
+      const uint32_t l0 = s_ms[b], l1 = s_ms[b + 1], l2 = s_ms[b + X], l3 = s_ms[b + X + 1];
+      const uint32_t l4 = s_ms[b + LZ], l5 = s_ms[b + LZ + 1], l6 = s_ms[b + LZ + X], l7 = s_ms[b + LZ + X + 1];
+      if (!(l0 == l7 && l1 == l7 && l2 == l7 && l3 == l7 && l4 == l7 && l5 == l7 && l6 == l7)) {
+        code6 = uint32_t(tet_code(l0, l1, l3, l7)) | uint32_t(tet_code(l0, l1, l5, l7)) << 5 |
+                uint32_t(tet_code(l0, l2, l3, l7)) << 10 | uint32_t(tet_code(l0, l2, l6, l7)) << 15 |
+                uint32_t(tet_code(l0, l4, l5, l7)) << 20 | uint32_t(tet_code(l0, l4, l6, l7)) << 25;
+        cnt = case_count6(code6, s_cases);
+      }
+      s_code[q] = code6;
+    }
+    const uint32_t tot = __reduce_add_sync(0xffffffffu, uint32_t(cnt));
+    if (lane == 0) s_chunk[ch] = tot;
   }
-  (void)CPT;
-  // block exclusive scan of cnt
-  uint32_t inc = cnt;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
-    if (lane >= o) inc += t;
-  }
-  if (lane == 31) s_wsum[w] = inc;
   __syncthreads();
+  // chunk offsets (warp 0) + decoupled look-back across slabs
   if (w == 0) {
-    const uint32_t t = lane < D_THREADS / 32 ? s_wsum[lane] : 0;
-    uint32_t ti = t;
+    constexpr int PER = D_CHUNKS / 32;
+    uint32_t v[PER], sum = 0;
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const uint32_t ch = lane * PER + k;
+      v[k] = ch < nchunks ? s_chunk[ch] : 0;
+      sum += v[k];
+    }
+    uint32_t inc = sum;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t u = __shfl_up_sync(0xffffffffu, ti, o);
-      if (lane >= o) ti += u;
+      const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += t;
     }
-    if (lane < D_THREADS / 32) s_wsum[lane] = ti - t;
-    // block total = inclusive of the last warp
-    const uint32_t total = __shfl_sync(0xffffffffu, ti, D_THREADS / 32 - 1);
-    // 3. decoupled look-back (warp 0)
+    uint32_t run = inc - sum;
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const uint32_t ch = lane * PER + k;
+      if (ch < nchunks) s_chunk[ch] = run;
+      run += v[k];
+    }
+    const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
+    // tile 0 always publishes a prefix, so a window reaching it stops there
     if (lane == 0) {
       if (tile == 0) {
         atomicExch(tile_state, FLAG_P | uint64_t(total));
@@ -519,9 +656,6 @@ __global__ void __launch_bounds__(D_THREADS)
       uint64_t excl = 0;
       int64_t j = int64_t(tile) - 1;
       for (;;) {
-        // lanes inspect predecessors j - lane
-        // Tile 0 always publishes a prefix, so the window that reaches it
-        // stops there; lanes before tile 0 read nothing and add nothing.
         const int64_t jj = j - lane;
         uint64_t st = 0;
         if (jj >= 0) {
@@ -530,11 +664,11 @@ __global__ void __launch_bounds__(D_THREADS)
           } while ((st >> 62) == 0);
         }
         const unsigned pmask = __ballot_sync(0xffffffffu, (st >> 62) == 2);
-        const int stop = pmask ? __ffs(pmask) - 1 : 32;  // first lane with a prefix
-        uint64_t v = (lane <= stop && jj >= 0) ? (st & VAL_MASK) : 0;
+        const int stop = pmask ? __ffs(pmask) - 1 : 32;
+        uint64_t vv = (lane <= stop && jj >= 0) ? (st & VAL_MASK) : 0;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        excl += v;
+        for (int o = 16; o > 0; o >>= 1) vv += __shfl_xor_sync(0xffffffffu, vv, o);
+        excl += vv;
         if (pmask) break;
         j -= 32;
       }
@@ -545,37 +679,46 @@ __global__ void __launch_bounds__(D_THREADS)
     }
   }
   __syncthreads();
-  // 4. emit
-  uint64_t pos = s_excl + s_wsum[w] + (inc - cnt);
-  if (cnt == 0) return;
-  const uint64_t cell_base = 6ull * (uint64_t(X - 1) * (uint64_t(y0) + uint64_t(d.Y - 1) * z));
-  for (uint32_t q = c0; q < c1; ++q) {
-    const uint32_t cx = q % (X - 1), cr = q / (X - 1);
-    const uint32_t b = cx + X * cr;
-    const uint32_t o[8] = {b, b + 1, b + X, b + X + 1, b + rows * X, b + rows * X + 1, b + rows * X + X,
-                           b + rows * X + X + 1};
-    uint32_t l[8];
+  // phase 3: emission in reference order
+  const uint64_t cell_base = 6ull * (uint64_t(CX) * (uint64_t(y0) + uint64_t(d.Y - 1) * z));
+  const uint64_t tile_base = s_excl;
+  for (uint32_t ch = w; ch < nchunks; ch += D_THREADS / 32) {
+    const uint32_t q = ch * 32 + lane;
+    const uint32_t code6 = q < ncubes ? s_code[q] : 0;
+    const uint32_t cnt = code6 ? uint32_t(case_count6(code6, s_cases)) : 0u;
+    if (!__any_sync(0xffffffffu, cnt != 0)) continue;
+    uint32_t inc = cnt;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) l[k] = s_ms[o[k]];
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += t;
+    }
+    if (!cnt) continue;
+    uint64_t pos = tile_base + s_chunk[ch] + (inc - cnt);
+    const uint32_t cr = uint32_t((float(q) + 0.5f) * inv_cx), cx = q - cr * CX;
+    const uint32_t b = cx + X * cr;
+    const uint32_t l0 = s_ms[b], l1 = s_ms[b + 1], l2 = s_ms[b + X], l3 = s_ms[b + X + 1];
+    const uint32_t l4 = s_ms[b + LZ], l5 = s_ms[b + LZ + 1], l6 = s_ms[b + LZ + X], l7 = s_ms[b + LZ + X + 1];
     const uint64_t cube_cell = cell_base + 6ull * q;
 #pragma unroll
     for (int t = 0; t < 6; ++t) {
-      const int cb = (t < 2) ? 1 : (t < 4 ? 2 : 4);
-      const int cc = (t == 0 || t == 2) ? 3 : (t == 1 || t == 4 ? 5 : 6);
-      const int code = tet_code(l[0], l[cb], l[cc], l[7]);
-      const int n = c_cases[code] & 15;
-      if (!n) continue;
-      const int first = c_cases[code] >> 4;
-      const int corner[4] = {0, cb, cc, 7};
+      const uint32_t vb = t < 2 ? l1 : (t < 4 ? l2 : l4);
+      const uint32_t vc = (t == 0 || t == 2) ? l3 : ((t == 1 || t == 4) ? l5 : l6);
+      const uint32_t cs = s_cases[(code6 >> (5 * t)) & 31];
+      const int n = cs & 15;
+      const int first = cs >> 4;
       for (int r = 0; r < n; ++r) {
-        const uint32_t row = c_rows[first + r];
-        const uint32_t la = l[corner[(row >> 12) & 3]], lb = l[corner[(row >> 14) & 3]];
+        const uint32_t row = s_rows[first + r];
+        const uint32_t la = pick4((row >> 12) & 3, l0, vb, vc, l7);
+        const uint32_t lb = pick4((row >> 14) & 3, l0, vb, vc, l7);
         if (pos < out_cap) {
-          plmss_tri rec;
-          rec.cell_row = ((cube_cell + t) << 6) | uint64_t(first + r);
-          rec.lo = la < lb ? la : lb;
-          rec.hi = la < lb ? lb : la;
-          out[pos] = rec;
+          const uint64_t cr64 = ((cube_cell + t) << 6) | uint64_t(first + r);
+          uint4 rec;
+          rec.x = uint32_t(cr64);
+          rec.y = uint32_t(cr64 >> 32);
+          rec.z = min(la, lb);
+          rec.w = max(la, lb);
+          *reinterpret_cast<uint4*>(out + pos) = rec;
         }
         ++pos;
       }
@@ -598,10 +741,11 @@ bool fused_supported(const Grid& g) { return g.X - 1 <= D_CUBES && g.n < (int64_
 
 FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* desc, uint32_t* asc, uint32_t* ms) {
   FusedOut o{};
+  for (auto& s : c.stats) s = 0;
   if (c.device >= 0 && c.device < 64 && !g_consts_ready[c.device]) {
     CK(cudaMemcpyToSymbol(c_rows, kTetRowsPacked, sizeof(kTetRowsPacked)));
     CK(cudaMemcpyToSymbol(c_cases, kTetCasePacked, sizeof(kTetCasePacked)));
-    CK(cudaFuncSetAttribute(k_finalize_march, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CK(cudaFuncSetAttribute(k_march, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CK(cudaFuncSetAttribute(k_tile_segment, cudaFuncAttributeMaxDynamicSharedMemorySize, kASmem));
     g_consts_ready[c.device] = true;
   }
@@ -702,8 +846,8 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
       fset = c.get_t<unsigned long long>(S_HASH_V, fcap);
       CK(cudaMemsetAsync(fset, 0xff, fcap * 8, c.stream));
       CK(cudaMemsetAsync(flag, 0, 4, c.stream));
-      k_mark_pairs<<<unsigned(std::min<int64_t>((g.n + 255) / 256, int64_t(c.sm_count) * 16)), 256, 0, c.stream>>>(
-          d.n, desc, asc, fset, fcap - 1, flag);
+      k_mark_pairs<<<unsigned(std::min<int64_t>((g.n + 1023) / 1024, int64_t(c.sm_count) * 16)), 256, 0,
+                     c.stream>>>(d, desc, asc, fset, fcap - 1, flag);
       CK_LAUNCH("k_mark_pairs");
       CK(cudaMemcpyAsync(c.h_pinned, flag, 4, cudaMemcpyDeviceToHost, c.stream));
       c.sync();
@@ -729,8 +873,12 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
     CK_LAUNCH("k_set_ids");
     o.n_regions = R;
     c.stats[2] = int64_t(fcap);
+    // ---- D1: dense MS ids per vertex
+    k_assign_ms<<<unsigned(std::min<int64_t>((g.n + 1023) / 1024, int64_t(c.sm_count) * 16)), 256, 0, c.stream>>>(
+        d.n, desc, asc, fset, fcap - 1, slot_id, ms);
+    CK_LAUNCH("k_assign_ms");
     c.mark(4);
-    // ---- D: ordered finalize + MS ids + marching
+    // ---- D2: ordered marching
     DDims dd;
     dd.X = d.X;
     dd.Y = d.Y;
@@ -741,7 +889,8 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
     dd.ty = std::min<uint32_t>(dd.ty, d.Y);
     dd.nyb = (d.Y + dd.ty - 1) / dd.ty;
     dd.ntiles = dd.nyb * d.Z;
-    const size_t smem = size_t(dd.ty + 1) * 2 * d.X * sizeof(uint32_t);
+    const uint32_t ms_words = (dd.ty + 1) * 2 * d.X;
+    const size_t smem = size_t(ms_words + D_CUBES) * sizeof(uint32_t);
     if (smem > 200 * 1024) fail(PLMSS_ERR_LOGIC, "row slab exceeds shared memory");
     auto* tstate = c.get_t<unsigned long long>(S_SCAN_C, dd.ntiles + 1);
     for (int pass = 0;; ++pass) {
@@ -749,9 +898,9 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
       plmss_tri* tris = c.get_t<plmss_tri>(S_TRIS, cap);
       CK(cudaMemsetAsync(tstate, 0, (dd.ntiles + 1) * 8, c.stream));
       CK(cudaMemsetAsync(ticket, 0, 4, c.stream));
-      k_finalize_march<<<dd.ntiles, D_THREADS, smem, c.stream>>>(dd, desc, asc, ms, fset, fcap - 1, slot_id, tstate,
-                                                                 ticket, tris, cap, tot);
-      CK_LAUNCH("k_finalize_march");
+      k_march<<<dd.ntiles, D_THREADS, smem, c.stream>>>(dd, ms, tstate, ticket, tris, cap,
+                                                        1.0f / float(std::max<int64_t>(1, g.X - 1)), ms_words);
+      CK_LAUNCH("k_march");
       k_read_total<<<1, 1, 0, c.stream>>>(tstate, dd.ntiles - 1, tot);
       CK_LAUNCH("k_read_total");
       CK(cudaMemcpyAsync(c.h_pinned, tot, 8, cudaMemcpyDeviceToHost, c.stream));
@@ -760,7 +909,8 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
       if (T > cap) {
         c.fused_tri_cap = T + T / 20 + 1024;
         if (pass > 2) fail(PLMSS_ERR_LOGIC, "separator capacity retries exhausted");
-        continue;  // re-run D only: it is idempotent on finalized labels
+        ++c.stats[3];
+        continue;  // re-run D2 only
       }
       o.n_tris = int64_t(T);
       o.tris = tris;
