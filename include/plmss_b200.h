@@ -194,8 +194,10 @@ int plmss_b200_copy(plmss_ctx* ctx, void* dst, const void* d_src, int64_t bytes,
 /* Tuning / test options:
  *   PLMSS_OPT_COMBINE_PATH  0 auto, 1 bitmap, 2 hash (staged combine_ms);
  *   PLMSS_OPT_PIPELINE_PATH 0 fused tile pipeline when the dims allow it,
- *                           1 staged kernels (segment/combine/emit). */
-enum plmss_option { PLMSS_OPT_COMBINE_PATH = 1, PLMSS_OPT_PIPELINE_PATH = 2 };
+ *                           1 staged kernels (segment/combine/emit);
+ *   PLMSS_OPT_TMA           1 (default) TMA tensor loads of the field bricks,
+ *                           0 plain load loop (both are exact). */
+enum plmss_option { PLMSS_OPT_COMBINE_PATH = 1, PLMSS_OPT_PIPELINE_PATH = 2, PLMSS_OPT_TMA = 3 };
 int plmss_b200_ctx_set_option(plmss_ctx* ctx, int option, int64_t value);
 
 /* End-to-end variant over HOST buffers: pinned or pageable h_field in; the

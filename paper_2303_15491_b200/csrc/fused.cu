@@ -26,6 +26,8 @@
 
 #include <algorithm>
 
+#include <cuda.h>
+
 #include "common.cuh"
 #include "tet_tables.h"
 
@@ -33,14 +35,17 @@ namespace plmss_b200 {
 
 namespace {
 
-constexpr int TX = 32, TY = 16, TZ = 16;
-constexpr int HX = TX + 2, HY = TY + 2, HZ = TZ + 2;
-constexpr int HN = HX * HY * HZ;  // 11016
-constexpr int TN = TX * TY * TZ;  // 8192
-constexpr int A_THREADS = 512;
-constexpr int A_PER = TN / A_THREADS;  // 16
-constexpr uint16_t TERM = 0x8000, EXIT = 0x4000;
-constexpr int kASmem = 4 * HN + 2 * 2 * TN + HN;  // f, Pd, Pa, exit flags
+constexpr int TX = 32, TY = 32, TZ = 32;
+// Halo brick in shared memory: x from gx0-4 (the TMA start coordinate in x
+// must be 16-byte aligned on this platform, tools/tma_probe2.cu) to gx0+35,
+// y and z from g0-1 to g0+32.
+constexpr int HX = TX + 8, HY = TY + 2, HZ = TZ + 2;
+constexpr int HXO = 4;            // x offset of the brick inside the halo box
+constexpr int HN = HX * HY * HZ;  // 46240
+constexpr int TN = TX * TY * TZ;  // 32768
+constexpr int A_THREADS = 1024;
+constexpr int kASmem = 4 * HN + TN + 1024;  // f (later the two u16 pointer arrays), hop codes, alignment slack
+static_assert(2 * 2 * TN <= 4 * HN, "pointer arrays must fit in the f region");
 constexpr uint64_t kEmpty = ~uint64_t(0);
 
 struct FDims {
@@ -100,57 +105,98 @@ struct ACounters {
 };
 
 // ---------------------------------------------------------------- pass A --
-__global__ void __launch_bounds__(A_THREADS, 2)
-    k_tile_segment(const float* __restrict__ field, FDims d, uint32_t* __restrict__ desc,
-                   uint32_t* __restrict__ asc, uint32_t* __restrict__ maxima, uint32_t* __restrict__ minima,
-                   uint64_t ext_cap, uint32_t* __restrict__ exits, uint64_t exit_cap,
-                   ACounters* __restrict__ ctr) {
-  extern __shared__ __align__(16) unsigned char a_smem[];
-  float* f = reinterpret_cast<float*>(a_smem);                   // HN floats
-  uint16_t* Pd = reinterpret_cast<uint16_t*>(a_smem + 4 * HN);   // TN
-  uint16_t* Pa = Pd + TN;                                        // TN
-  uint8_t* xflag = reinterpret_cast<uint8_t*>(Pa + TN);          // HN
-  __shared__ uint32_t s_cnt;
-  __shared__ unsigned long long s_base;
+// One CTA (1024 threads, one per (x, y) column of 32 vertices) per 32^3
+// brick. The halo'd brick of f (36 x 34 x 34, x padded to a 16-byte multiple)
+// arrives by one TMA tensor copy whose out-of-volume elements are NaN
+// (fmaxf/fminf ignore NaN and NaN == x is false, so a missing neighbour is
+// never selected). Phase 1 stores each vertex's steepest up/down stencil code
+// (4 bits each) — f is then dead and its shared memory becomes the two u16
+// pointer arrays of phase 2, where a vertex points at its in-brick hop target
+// or at itself when it is a root or its hop leaves the brick. Pointer jumping
+// to the fixpoint leaves every vertex pointing at its terminal u; the partial
+// label is u (root) or u's out-of-brick hop target (an exit vertex).
+template <bool kTMA>
+__global__ void __launch_bounds__(A_THREADS, 1)
+    k_tile_segment(const __grid_constant__ CUtensorMap tmap, const float* __restrict__ field, FDims d,
+                   uint32_t* __restrict__ desc, uint32_t* __restrict__ asc, uint32_t* __restrict__ maxima,
+                   uint32_t* __restrict__ minima, uint64_t ext_cap, uint32_t* __restrict__ exits,
+                   uint64_t exit_cap, ACounters* __restrict__ ctr) {
+  extern __shared__ __align__(16) unsigned char a_smem_raw[];
+  // TMA destinations must be 128-byte aligned: round the window up (the
+  // launch reserves kASmemAlign extra bytes for this).
+  unsigned char* a_smem = a_smem_raw + ((1024u - (smem_u32(a_smem_raw) & 1023u)) & 1023u);
+  float* f = reinterpret_cast<float*>(a_smem);          // HN floats (phase 1)
+  uint16_t* Pd = reinterpret_cast<uint16_t*>(a_smem);   // TN (phase 2+, aliases f)
+  uint16_t* Pa = Pd + TN;                               // TN
+  uint8_t* hop = a_smem + 4 * HN;                       // TN: up | down << 4 (15 = self)
+  __shared__ __align__(8) uint64_t s_bar;
 
   const uint32_t bt = blockIdx.x;
   const uint32_t tx = bt % d.tx, ty = (bt / d.tx) % d.ty, tz = bt / (d.tx * d.ty);
   const int gx0 = int(tx * TX), gy0 = int(ty * TY), gz0 = int(tz * TZ);
+  const int lane = threadIdx.x & 31;
+  const int lx = threadIdx.x & 31, ly = threadIdx.x >> 5;
 
-  // 1. halo'd tile of f (x-rows are contiguous in global memory). Vertices
-  //    outside the volume hold NaN: fmaxf/fminf ignore NaN and NaN == x is
-  //    false, so a missing neighbour can never be selected.
-  for (int i = threadIdx.x; i < HN; i += A_THREADS) {
-    const int hx = i % HX, hy = (i / HX) % HY, hz = i / (HX * HY);
-    const int gx = gx0 + hx - 1, gy = gy0 + hy - 1, gz = gz0 + hz - 1;
-    float val = __int_as_float(0x7fc00000);
-    if (gx >= 0 && gx < int(d.X) && gy >= 0 && gy < int(d.Y) && gz >= 0 && gz < int(d.Z))
-      val = __ldg(field + (uint32_t(gx) + d.X * (uint32_t(gy) + d.Y * uint32_t(gz))));
-    f[i] = val;
-    xflag[i] = 0;
+  // 1. halo'd brick of f
+  if (kTMA) {
+    const uint32_t bar = smem_u32(&s_bar);
+    if (threadIdx.x == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(uint32_t(HN * 4))
+                   : "memory");
+      asm volatile(
+          "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+          "%4}], [%5];" ::"r"(smem_u32(f)),
+          "l"(&tmap), "r"(gx0 - HXO), "r"(gy0 - 1), "r"(gz0 - 1), "r"(bar)
+          : "memory");
+    }
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n @!p bra WAIT_%=;\n}" ::"r"(
+            bar)
+        : "memory");
+  } else {
+    for (int i0 = 0; i0 < HN; i0 += 8 * A_THREADS) {
+      float v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int i = i0 + k * A_THREADS + int(threadIdx.x);
+        const int hx = i % HX, hy = (i / HX) % HY, hz = i / (HX * HY);
+        const int gx = gx0 + hx - HXO, gy = gy0 + hy - 1, gz = gz0 + hz - 1;
+        v[k] = __int_as_float(0x7fc00000);
+        if (i < HN && gx >= 0 && gx < int(d.X) && gy >= 0 && gy < int(d.Y) && gz >= 0 && gz < int(d.Z))
+          v[k] = __ldg(field + (uint32_t(gx) + d.X * (uint32_t(gy) + d.Y * uint32_t(gz))));
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int i = i0 + k * A_THREADS + int(threadIdx.x);
+        if (i < HN) f[i] = v[k];
+      }
+    }
   }
-  if (threadIdx.x == 0) s_cnt = 0;
   __syncthreads();
 
-  // 2. hops. Stencil s = 0..13 in ascending id-delta order (complex.cpp:78-88);
-  //    the vertex itself sits between s = 6 and s = 7. With M = max f over the
-  //    neighbours, the steepest-up vertex under (f, id) order is the highest s
-  //    with f == M when M > f(v), or when M == f(v) and that s > 6 (a larger
-  //    id); otherwise v itself. Steepest-down mirrors it (lowest s, s < 7).
-  //    bit codes: 2 bits per axis (0 = -1, 1 = 0, 2 = +1), x low.
+  // 2. steepest hops. Stencil s = 0..13 in ascending id-delta order
+  //    (complex.cpp:78-88); the vertex itself sits between s = 6 and s = 7.
+  //    With M = max f over the neighbours, steepest-up under (f, id) order is
+  //    the highest s with f == M when M > f(v), or when M == f(v) and s > 6;
+  //    otherwise v. Steepest-down mirrors it (lowest s, s < 7).
   constexpr uint32_t kOff[14] = {0x00, 0x01, 0x04, 0x05, 0x10, 0x11, 0x14,
                                  0x16, 0x19, 0x1a, 0x25, 0x26, 0x29, 0x2a};
+  const int gx = gx0 + lx, gy = gy0 + ly;
+  const bool col_ok = gx < int(d.X) && gy < int(d.Y);
 #pragma unroll 1
-  for (int k = 0; k < A_PER; ++k) {
-    const int l = threadIdx.x + k * A_THREADS;
-    const int lx = l % TX, ly = (l / TX) % TY, lz = l / (TX * TY);
-    const int gx = gx0 + lx, gy = gy0 + ly, gz = gz0 + lz;
-    if (gx >= int(d.X) || gy >= int(d.Y) || gz >= int(d.Z)) {
-      Pd[l] = TERM | uint16_t(l);
-      Pa[l] = TERM | uint16_t(l);
+  for (int lz = 0; lz < TZ; ++lz) {
+    const int l = lx + TX * ly + TX * TY * lz;
+    const int gz = gz0 + lz;
+    if (!col_ok || gz >= int(d.Z)) {
+      hop[l] = 0xff;
       continue;
     }
-    const int h = (lz + 1) * HX * HY + (ly + 1) * HX + (lx + 1);
+    const int h = (lz + 1) * HX * HY + (ly + 1) * HX + (lx + HXO);
     const float fv = f[h];
     if (!isfinite(fv)) atomicMin(&ctr->bad, uint32_t(gx) + d.X * (uint32_t(gy) + d.Y * uint32_t(gz)));
     float fn[14];
@@ -165,126 +211,97 @@ __global__ void __launch_bounds__(A_THREADS, 2)
       M = fmaxf(M, fn[s]);
       m = fminf(m, fn[s]);
     }
-    int su = -1, sd = -1;
+    uint32_t su = 15, sd = 15;
 #pragma unroll
-    for (int s = 0; s < 14; ++s) su = fn[s] == M ? s : su;  // highest s attaining M
+    for (int s = 0; s < 14; ++s) su = fn[s] == M ? uint32_t(s) : su;  // highest s attaining M
 #pragma unroll
-    for (int s = 13; s >= 0; --s) sd = fn[s] == m ? s : sd;  // lowest s attaining m
-    if (!(M > fv || (M == fv && su > 6))) su = -1;
-    if (!(m < fv || (m == fv && sd < 7))) sd = -1;
-    auto enc = [&](int s) -> uint16_t {
-      if (s < 0) return TERM | uint16_t(l);
-      const uint32_t o = kOffTable(s);
-      const int dx = int(o & 3) - 1, dy = int((o >> 2) & 3) - 1, dz = int((o >> 4) & 3) - 1;
-      const int mx = lx + dx, my = ly + dy, mz = lz + dz;
-      const bool inside = mx >= 0 && mx < TX && my >= 0 && my < TY && mz >= 0 && mz < TZ;
-      return inside ? uint16_t(l + dx + TX * dy + TX * TY * dz)
-                    : uint16_t(TERM | EXIT | (h + dx + HX * dy + HX * HY * dz));
-    };
-    const uint16_t pu = enc(su), pd = enc(sd);
-    Pd[l] = pu;
-    Pa[l] = pd;
-    if ((pu & (TERM | EXIT)) == (TERM | EXIT)) xflag[pu & 0x3fff] = 1;
-    if ((pd & (TERM | EXIT)) == (TERM | EXIT)) xflag[pd & 0x3fff] = 1;
+    for (int s = 13; s >= 0; --s) sd = fn[s] == m ? uint32_t(s) : sd;  // lowest s attaining m
+    if (!(M > fv || (M == fv && su > 6))) su = 15;
+    if (!(m < fv || (m == fv && sd < 7))) sd = 15;
+    hop[l] = uint8_t(su | (sd << 4));
   }
   __syncthreads();
 
-  // 3. in-tile pointer jumping to terminals
+  // 3. pointers (f is dead from here on)
+  auto target = [&](int l, uint32_t s) -> int {  // in-brick hop target or l itself
+    if (s == 15) return l;
+    const uint32_t o = kOffTable(int(s));
+    const int dx = int(o & 3) - 1, dy = int((o >> 2) & 3) - 1, dz = int((o >> 4) & 3) - 1;
+    const int mx = (l & 31) + dx, my = ((l >> 5) & 31) + dy, mz = (l >> 10) + dz;
+    const bool inside = mx >= 0 && mx < TX && my >= 0 && my < TY && mz >= 0 && mz < TZ;
+    return inside ? l + dx + TX * dy + TX * TY * dz : l;
+  };
+#pragma unroll 4
+  for (int lz = 0; lz < TZ; ++lz) {
+    const int l = lx + TX * ly + TX * TY * lz;
+    const uint32_t c = hop[l];
+    Pd[l] = uint16_t(target(l, c & 15));
+    Pa[l] = uint16_t(target(l, c >> 4));
+  }
+  __syncthreads();
   for (;;) {
     bool changed = false;
-#pragma unroll 4
-    for (int k = 0; k < A_PER; ++k) {
-      const int l = threadIdx.x + k * A_THREADS;
-      uint16_t p = Pd[l];
-      if (!(p & TERM)) {
-        const uint16_t q = Pd[p];
+#pragma unroll 8
+    for (int lz = 0; lz < TZ; ++lz) {
+      const int l = lx + TX * ly + TX * TY * lz;
+      const uint16_t p = Pd[l], q = Pd[p];
+      if (q != p) {
         Pd[l] = q;
-        changed |= !(q & TERM);
+        changed = true;
       }
-      p = Pa[l];
-      if (!(p & TERM)) {
-        const uint16_t q = Pa[p];
-        Pa[l] = q;
-        changed |= !(q & TERM);
+      const uint16_t pa = Pa[l], qa = Pa[pa];
+      if (qa != pa) {
+        Pa[l] = qa;
+        changed = true;
       }
     }
     if (!__syncthreads_or(changed)) break;
   }
 
-  // 4. partial labels, roots, partial pairs
-  auto gid_of = [&](uint16_t p) -> uint32_t {
-    if (p & EXIT) {
-      const int hh = p & 0x3fff;
-      const int hx = hh % HX, hy = (hh / HX) % HY, hz = hh / (HX * HY);
-      return uint32_t(gx0 + hx - 1) + d.X * (uint32_t(gy0 + hy - 1) + d.Y * uint32_t(gz0 + hz - 1));
-    }
-    const int ll = p & 0x1fff;
-    const int lx = ll % TX, ly = (ll / TX) % TY, lz = ll / (TX * TY);
-    return uint32_t(gx0 + lx) + d.X * (uint32_t(gy0 + ly) + d.Y * uint32_t(gz0 + lz));
+  // 4. partial labels, roots, exit vertices
+  const uint32_t base_g = uint32_t(gx0) + d.X * (uint32_t(gy0) + d.Y * uint32_t(gz0));
+  auto gid = [&](int u) -> uint32_t { return base_g + uint32_t(u & 31) + d.X * (uint32_t((u >> 5) & 31) + d.Y * uint32_t(u >> 10)); };
+  auto gdelta = [&](uint32_t s) -> int {
+    const uint32_t o = kOffTable(int(s));
+    return (int(o & 3) - 1) + int(d.X) * (int((o >> 2) & 3) - 1) + int(d.XY) * (int((o >> 4) & 3) - 1);
   };
-  const int lane = threadIdx.x & 31;
+  auto append = [&](bool hit, uint32_t value, unsigned long long* counter, uint32_t* list, uint64_t cap) {
+    const unsigned m = __ballot_sync(0xffffffffu, hit);
+    if (!m) return;
+    unsigned long long b0 = 0;
+    const int leader = __ffs(m) - 1;
+    if (lane == leader) b0 = atomicAdd(counter, (unsigned long long)__popc(m));
+    b0 = __shfl_sync(0xffffffffu, b0, leader);
+    const uint64_t pos = b0 + __popc(m & ((1u << lane) - 1));
+    if (hit && pos < cap) list[pos] = value;
+  };
 #pragma unroll 1
-  for (int k = 0; k < A_PER; ++k) {
-    const int l = threadIdx.x + k * A_THREADS;
-    const int lx = l % TX, ly = (l / TX) % TY, lz = l / (TX * TY);
-    const int gx = gx0 + lx, gy = gy0 + ly, gz = gz0 + lz;
-    const bool valid = gx < int(d.X) && gy < int(d.Y) && gz < int(d.Z);
+  for (int lz = 0; lz < TZ; ++lz) {
+    const int l = lx + TX * ly + TX * TY * lz;
+    const uint32_t c = hop[l];
+    const bool valid = c != 0xff;
+    const uint32_t gv = gid(l);
     uint32_t ld = 0, la = 0;
-    bool is_max = false, is_min = false;
+    bool xd = false, xa = false;
+    uint32_t ed = 0, ea = 0;
     if (valid) {
-      const uint32_t gv = uint32_t(gx) + d.X * (uint32_t(gy) + d.Y * uint32_t(gz));
-      const uint16_t pd = Pd[l], pa = Pa[l];
-      ld = gid_of(pd);
-      la = gid_of(pa);
+      const int ud = Pd[l], ua = Pa[l];
+      const uint32_t cd = hop[ud] & 15, ca = hop[ua] >> 4;
+      ld = gid(ud) + (cd == 15 ? 0 : uint32_t(gdelta(cd)));
+      la = gid(ua) + (ca == 15 ? 0 : uint32_t(gdelta(ca)));
       desc[gv] = ld;
       asc[gv] = la;
-      is_max = ld == gv;
-      is_min = la == gv;
+      // this vertex's own hop leaves the brick -> its target is an exit vertex
+      const uint32_t sd = c & 15, sa = c >> 4;
+      xd = sd != 15 && target(l, sd) == l;
+      xa = sa != 15 && target(l, sa) == l;
+      if (xd) ed = gv + uint32_t(gdelta(sd));
+      if (xa) ea = gv + uint32_t(gdelta(sa));
     }
-    // warp-aggregated extremum appends
-    unsigned m = __ballot_sync(0xffffffffu, is_max);
-    if (m) {
-      unsigned long long base = 0;
-      if (lane == __ffs(m) - 1) base = atomicAdd(&ctr->n_max, (unsigned long long)__popc(m));
-      base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
-      const uint64_t pos = base + __popc(m & ((1u << lane) - 1));
-      if (is_max && pos < ext_cap) maxima[pos] = ld;
-    }
-    m = __ballot_sync(0xffffffffu, is_min);
-    if (m) {
-      unsigned long long base = 0;
-      if (lane == __ffs(m) - 1) base = atomicAdd(&ctr->n_min, (unsigned long long)__popc(m));
-      base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
-      const uint64_t pos = base + __popc(m & ((1u << lane) - 1));
-      if (is_min && pos < ext_cap) minima[pos] = la;
-    }
-  }
-
-  // 5. exit targets of this tile -> E
-  uint32_t mine = 0;
-  for (int i = threadIdx.x; i < HN; i += A_THREADS) mine += xflag[i];
-  mine = __reduce_add_sync(0xffffffffu, mine);
-  if (lane == 0 && mine) atomicAdd(&s_cnt, mine);
-  __syncthreads();
-  if (threadIdx.x == 0) s_base = s_cnt ? atomicAdd(&ctr->n_exit, (unsigned long long)s_cnt) : 0;
-  __syncthreads();
-  if (s_cnt == 0) return;
-  __shared__ uint32_t s_pos;
-  if (threadIdx.x == 0) s_pos = 0;
-  __syncthreads();
-  for (int i0 = 0; i0 < HN; i0 += A_THREADS) {
-    const int i = i0 + threadIdx.x;
-    const bool hit = i < HN && xflag[i];
-    const unsigned m = __ballot_sync(0xffffffffu, hit);
-    uint32_t wbase = 0;
-    if (lane == 0 && m) wbase = atomicAdd(&s_pos, __popc(m));
-    wbase = __shfl_sync(0xffffffffu, wbase, 0);
-    if (hit) {
-      const uint64_t pos = s_base + wbase + __popc(m & ((1u << lane) - 1));
-      const int hx = i % HX, hy = (i / HX) % HY, hz = i / (HX * HY);
-      if (pos < exit_cap)
-        exits[pos] = uint32_t(gx0 + hx - 1) + d.X * (uint32_t(gy0 + hy - 1) + d.Y * uint32_t(gz0 + hz - 1));
-    }
+    append(valid && (c & 15) == 15, gv, &ctr->n_max, maxima, ext_cap);
+    append(valid && (c >> 4) == 15, gv, &ctr->n_min, minima, ext_cap);
+    append(xd, ed, &ctr->n_exit, exits, exit_cap);
+    append(xa && !(xd && ea == ed), ea, &ctr->n_exit, exits, exit_cap);
   }
 }
 
@@ -502,9 +519,6 @@ __device__ __forceinline__ int tet_code(uint32_t a, uint32_t b, uint32_t c, uint
 
 constexpr uint64_t FLAG_A = uint64_t(1) << 62, FLAG_P = uint64_t(2) << 62, VAL_MASK = (uint64_t(1) << 62) - 1;
 
-__device__ __forceinline__ uint32_t pick4(int i, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
-  return i == 0 ? a : (i == 1 ? b : (i == 2 ? c : d));
-}
 
 __device__ __forceinline__ int case_count6(uint32_t code6, const uint16_t* cases) {
   return (cases[code6 & 31] & 15) + (cases[(code6 >> 5) & 31] & 15) + (cases[(code6 >> 10) & 31] & 15) +
@@ -693,34 +707,53 @@ __global__ void __launch_bounds__(D_THREADS, 2)
       const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
       if (lane >= o) inc += t;
     }
-    if (!cnt) continue;
-    uint64_t pos = tile_base + s_chunk[ch] + (inc - cnt);
+    // Warp-cooperative emission: the chunk's T records are dealt out one per
+    // lane, so every store instruction writes 32 consecutive records.
+    const uint32_t T = __shfl_sync(0xffffffffu, inc, 31);
+    const uint64_t chunk_base = tile_base + s_chunk[ch];
     const uint32_t cr = uint32_t((float(q) + 0.5f) * inv_cx), cx = q - cr * CX;
-    const uint32_t b = cx + X * cr;
-    const uint32_t l0 = s_ms[b], l1 = s_ms[b + 1], l2 = s_ms[b + X], l3 = s_ms[b + X + 1];
-    const uint32_t l4 = s_ms[b + LZ], l5 = s_ms[b + LZ + 1], l6 = s_ms[b + LZ + X], l7 = s_ms[b + LZ + X + 1];
-    const uint64_t cube_cell = cell_base + 6ull * q;
+    const uint32_t bq = cx + X * cr;  // cube base index in the staged slab
+    for (uint32_t j0 = 0; j0 < T; j0 += 32) {
+      const uint32_t j = j0 + lane;
+      // lane owning record j = number of lanes whose inclusive count is <= j
+      // (binary search over the warp's nondecreasing prefix via shuffles)
+      int src = 0;
 #pragma unroll
-    for (int t = 0; t < 6; ++t) {
-      const uint32_t vb = t < 2 ? l1 : (t < 4 ? l2 : l4);
-      const uint32_t vc = (t == 0 || t == 2) ? l3 : ((t == 1 || t == 4) ? l5 : l6);
-      const uint32_t cs = s_cases[(code6 >> (5 * t)) & 31];
-      const int n = cs & 15;
-      const int first = cs >> 4;
-      for (int r = 0; r < n; ++r) {
-        const uint32_t row = s_rows[first + r];
-        const uint32_t la = pick4((row >> 12) & 3, l0, vb, vc, l7);
-        const uint32_t lb = pick4((row >> 14) & 3, l0, vb, vc, l7);
-        if (pos < out_cap) {
-          const uint64_t cr64 = ((cube_cell + t) << 6) | uint64_t(first + r);
-          uint4 rec;
-          rec.x = uint32_t(cr64);
-          rec.y = uint32_t(cr64 >> 32);
-          rec.z = min(la, lb);
-          rec.w = max(la, lb);
-          *reinterpret_cast<uint4*>(out + pos) = rec;
-        }
-        ++pos;
+      for (int step = 16; step >= 1; step >>= 1) {
+        const uint32_t v = __shfl_sync(0xffffffffu, inc, src + step - 1);
+        if (v <= j) src += step;
+      }
+      const uint32_t c6 = __shfl_sync(0xffffffffu, code6, src & 31);
+      const uint32_t ex = __shfl_sync(0xffffffffu, inc - cnt, src & 31);
+      const uint32_t b = __shfl_sync(0xffffffffu, bq, src & 31);
+      if (j >= T) continue;
+      uint32_t k = j - ex;
+      int t = 0;
+      uint32_t cs = s_cases[c6 & 31];
+#pragma unroll
+      for (int tt = 0; tt < 5; ++tt) {
+        if (k < (cs & 15)) break;
+        k -= cs & 15;
+        ++t;
+        cs = s_cases[(c6 >> (5 * t)) & 31];
+      }
+      const uint32_t rowi = (cs >> 4) + k;
+      const uint32_t row = s_rows[rowi];
+      // tet t = cube corners {0, cb, cc, 7}; corner c -> slab offset
+      const uint32_t cb = (0x442211u >> (4 * t)) & 15, cc = (0x656353u >> (4 * t)) & 15;
+      auto corner = [&](uint32_t p) { return p == 0 ? 0u : (p == 1 ? cb : (p == 2 ? cc : 7u)); };
+      auto off = [&](uint32_t c) { return (c & 1) + X * ((c >> 1) & 1) + LZ * (c >> 2); };
+      const uint32_t la = s_ms[b + off(corner((row >> 12) & 3))];
+      const uint32_t lb = s_ms[b + off(corner((row >> 14) & 3))];
+      const uint64_t pos = chunk_base + j;
+      if (pos < out_cap) {
+        const uint64_t cr64 = ((cell_base + 6ull * (ch * 32 + uint32_t(src)) + t) << 6) | uint64_t(rowi);
+        uint4 rec;
+        rec.x = uint32_t(cr64);
+        rec.y = uint32_t(cr64 >> 32);
+        rec.z = min(la, lb);
+        rec.w = max(la, lb);
+        *reinterpret_cast<uint4*>(out + pos) = rec;
       }
     }
   }
@@ -746,7 +779,8 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
     CK(cudaMemcpyToSymbol(c_rows, kTetRowsPacked, sizeof(kTetRowsPacked)));
     CK(cudaMemcpyToSymbol(c_cases, kTetCasePacked, sizeof(kTetCasePacked)));
     CK(cudaFuncSetAttribute(k_march, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    CK(cudaFuncSetAttribute(k_tile_segment, cudaFuncAttributeMaxDynamicSharedMemorySize, kASmem));
+    CK(cudaFuncSetAttribute(k_tile_segment<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kASmem));
+    CK(cudaFuncSetAttribute(k_tile_segment<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kASmem));
     g_consts_ready[c.device] = true;
   }
   FDims d;
@@ -760,9 +794,38 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
   d.tz = uint32_t((g.Z + TZ - 1) / TZ);
   const uint64_t ntiles = uint64_t(d.tx) * d.ty * d.tz;
 
+  // TMA descriptor of the field (3-D, float32, NaN out-of-bounds fill). The
+  // global row pitch must be a 16-byte multiple, i.e. X % 4 == 0; otherwise
+  // the brick is staged by an unrolled load loop.
+  CUtensorMap tmap;
+  memset(&tmap, 0, sizeof tmap);
+  bool use_tma = (g.X % 4) == 0 && (reinterpret_cast<uintptr_t>(field) & 15) == 0 && c.use_tma;
+  if (use_tma) {
+    using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static EncodeFn encode = nullptr;
+    if (!encode) {
+      void* fn = nullptr;
+      cudaDriverEntryPointQueryResult q;
+      if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+          q == cudaDriverEntryPointSuccess)
+        encode = reinterpret_cast<EncodeFn>(fn);
+    }
+    const cuuint64_t gdim[3] = {cuuint64_t(g.X), cuuint64_t(g.Y), cuuint64_t(g.Z)};
+    const cuuint64_t gstride[2] = {cuuint64_t(g.X) * 4, cuuint64_t(g.X) * cuuint64_t(g.Y) * 4};
+    const cuuint32_t box[3] = {HX, HY, HZ};
+    const cuuint32_t estride[3] = {1, 1, 1};
+    use_tma = encode && encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(field), gdim, gstride,
+                               box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NAN_REQUEST_ZERO_FMA) == CUDA_SUCCESS;
+  }
+  c.stats[4] = use_tma ? 1 : 0;
+
   // Device counters: [0, 64) ACounters, int flag at +128, ticket at +160,
   // triangle total at +192 (bytes).
-  char* ctr_base = static_cast<char*>(c.get(S_FLAGS, 256));
+  char* ctr_base = static_cast<char*>(c.get(S_FLAGS, 1024));
   ACounters* ctr = reinterpret_cast<ACounters*>(ctr_base);
   int* flag = reinterpret_cast<int*>(ctr_base + 128);
   unsigned int* ticket = reinterpret_cast<unsigned int*>(ctr_base + 160);
@@ -776,8 +839,12 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
     CK(cudaMemsetAsync(ctr, 0, sizeof(ACounters), c.stream));
     CK(cudaMemsetAsync(&ctr->bad, 0xff, 4, c.stream));
     c.mark(0);
-    k_tile_segment<<<unsigned(ntiles), A_THREADS, kASmem, c.stream>>>(field, d, desc, asc, maxima, minima, ext_cap, E,
-                                                                  exit_cap, ctr);
+    if (use_tma)
+      k_tile_segment<true><<<unsigned(ntiles), A_THREADS, kASmem, c.stream>>>(tmap, field, d, desc, asc, maxima,
+                                                                           minima, ext_cap, E, exit_cap, ctr);
+    else
+      k_tile_segment<false><<<unsigned(ntiles), A_THREADS, kASmem, c.stream>>>(tmap, field, d, desc, asc, maxima,
+                                                                            minima, ext_cap, E, exit_cap, ctr);
     CK_LAUNCH("k_tile_segment");
     c.mark(1);
     ACounters h;
