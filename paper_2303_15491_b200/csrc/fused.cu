@@ -231,77 +231,150 @@ __global__ void __launch_bounds__(A_THREADS, 1)
     const bool inside = mx >= 0 && mx < TX && my >= 0 && my < TY && mz >= 0 && mz < TZ;
     return inside ? l + dx + TX * dy + TX * TY * dz : l;
   };
+  // Per-thread masks (bit lz) of column vertices whose pointer is not yet a
+  // terminal. A vertex is done once its pointer target is a terminal
+  // (P[t] == t); only live vertices are revisited in later rounds.
+  uint32_t live_d = 0, live_a = 0;
 #pragma unroll 4
   for (int lz = 0; lz < TZ; ++lz) {
     const int l = lx + TX * ly + TX * TY * lz;
     const uint32_t c = hop[l];
-    Pd[l] = uint16_t(target(l, c & 15));
-    Pa[l] = uint16_t(target(l, c >> 4));
+    const int td = target(l, c & 15), ta = target(l, c >> 4);
+    Pd[l] = uint16_t(td);
+    Pa[l] = uint16_t(ta);
+    live_d |= uint32_t(td != l) << lz;
+    live_a |= uint32_t(ta != l) << lz;
   }
   __syncthreads();
   for (;;) {
-    bool changed = false;
-#pragma unroll 8
-    for (int lz = 0; lz < TZ; ++lz) {
+    uint32_t m = live_d;
+    while (m) {
+      const int lz = __ffs(m) - 1;
+      m &= m - 1;
       const int l = lx + TX * ly + TX * TY * lz;
       const uint16_t p = Pd[l], q = Pd[p];
-      if (q != p) {
+      if (q == p)
+        live_d &= ~(1u << lz);
+      else
         Pd[l] = q;
-        changed = true;
-      }
-      const uint16_t pa = Pa[l], qa = Pa[pa];
-      if (qa != pa) {
-        Pa[l] = qa;
-        changed = true;
-      }
     }
-    if (!__syncthreads_or(changed)) break;
+    m = live_a;
+    while (m) {
+      const int lz = __ffs(m) - 1;
+      m &= m - 1;
+      const int l = lx + TX * ly + TX * TY * lz;
+      const uint16_t p = Pa[l], q = Pa[p];
+      if (q == p)
+        live_a &= ~(1u << lz);
+      else
+        Pa[l] = q;
+    }
+    if (!__syncthreads_or((live_d | live_a) != 0)) break;
   }
 
-  // 4. partial labels, roots, exit vertices
+  // 4. partial labels, roots, exit vertices. Appends are aggregated per
+  //    brick: count, block scan, one atomic per list, then write.
+  __shared__ int s_gdelta[16];
+  __shared__ uint32_t s_wcnt[A_THREADS / 32][3];
+  __shared__ unsigned long long s_lbase[3];
+  if (threadIdx.x < 16) {
+    int g = 0;
+    if (threadIdx.x < 14) {
+      const uint32_t o = kOffTable(int(threadIdx.x));
+      g = (int(o & 3) - 1) + int(d.X) * (int((o >> 2) & 3) - 1) + int(d.XY) * (int((o >> 4) & 3) - 1);
+    }
+    s_gdelta[threadIdx.x] = g;  // code 15 (self) -> 0
+  }
   const uint32_t base_g = uint32_t(gx0) + d.X * (uint32_t(gy0) + d.Y * uint32_t(gz0));
-  auto gid = [&](int u) -> uint32_t { return base_g + uint32_t(u & 31) + d.X * (uint32_t((u >> 5) & 31) + d.Y * uint32_t(u >> 10)); };
-  auto gdelta = [&](uint32_t s) -> int {
-    const uint32_t o = kOffTable(int(s));
-    return (int(o & 3) - 1) + int(d.X) * (int((o >> 2) & 3) - 1) + int(d.XY) * (int((o >> 4) & 3) - 1);
+  auto gid = [&](int u) -> uint32_t {
+    return base_g + uint32_t(u & 31) + d.X * (uint32_t((u >> 5) & 31) + d.Y * uint32_t(u >> 10));
   };
-  auto append = [&](bool hit, uint32_t value, unsigned long long* counter, uint32_t* list, uint64_t cap) {
-    const unsigned m = __ballot_sync(0xffffffffu, hit);
-    if (!m) return;
-    unsigned long long b0 = 0;
-    const int leader = __ffs(m) - 1;
-    if (lane == leader) b0 = atomicAdd(counter, (unsigned long long)__popc(m));
-    b0 = __shfl_sync(0xffffffffu, b0, leader);
-    const uint64_t pos = b0 + __popc(m & ((1u << lane) - 1));
-    if (hit && pos < cap) list[pos] = value;
-  };
-#pragma unroll 1
+  // terminal vertices keep P[l] == l; with a real hop that means an exit
+  uint32_t mmax = 0, mmin = 0, mxd = 0, mxa = 0;
+#pragma unroll 4
   for (int lz = 0; lz < TZ; ++lz) {
     const int l = lx + TX * ly + TX * TY * lz;
     const uint32_t c = hop[l];
-    const bool valid = c != 0xff;
-    const uint32_t gv = gid(l);
-    uint32_t ld = 0, la = 0;
-    bool xd = false, xa = false;
-    uint32_t ed = 0, ea = 0;
-    if (valid) {
-      const int ud = Pd[l], ua = Pa[l];
-      const uint32_t cd = hop[ud] & 15, ca = hop[ua] >> 4;
-      ld = gid(ud) + (cd == 15 ? 0 : uint32_t(gdelta(cd)));
-      la = gid(ua) + (ca == 15 ? 0 : uint32_t(gdelta(ca)));
-      desc[gv] = ld;
-      asc[gv] = la;
-      // this vertex's own hop leaves the brick -> its target is an exit vertex
-      const uint32_t sd = c & 15, sa = c >> 4;
-      xd = sd != 15 && target(l, sd) == l;
-      xa = sa != 15 && target(l, sa) == l;
-      if (xd) ed = gv + uint32_t(gdelta(sd));
-      if (xa) ea = gv + uint32_t(gdelta(sa));
+    if (c == 0xff) continue;
+    const uint32_t sd = c & 15, sa = c >> 4;
+    mmax |= uint32_t(sd == 15) << lz;
+    mmin |= uint32_t(sa == 15) << lz;
+    mxd |= uint32_t(sd != 15 && Pd[l] == l) << lz;
+    mxa |= uint32_t(sa != 15 && Pa[l] == l) << lz;
+  }
+  __syncthreads();  // s_gdelta ready
+  // an exit vertex reached in both directions is listed once
+  {
+    uint32_t both = mxd & mxa, m = both;
+    while (m) {
+      const int lz = __ffs(m) - 1;
+      m &= m - 1;
+      const uint32_t c = hop[lx + TX * ly + TX * TY * lz];
+      if (s_gdelta[c & 15] == s_gdelta[c >> 4]) mxa &= ~(1u << lz);
     }
-    append(valid && (c & 15) == 15, gv, &ctr->n_max, maxima, ext_cap);
-    append(valid && (c >> 4) == 15, gv, &ctr->n_min, minima, ext_cap);
-    append(xd, ed, &ctr->n_exit, exits, exit_cap);
-    append(xa && !(xd && ea == ed), ea, &ctr->n_exit, exits, exit_cap);
+  }
+  uint32_t cnt[3] = {uint32_t(__popc(mmax)), uint32_t(__popc(mmin)), uint32_t(__popc(mxd) + __popc(mxa))};
+  uint32_t pre[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    uint32_t inc = cnt[k];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += t;
+    }
+    pre[k] = inc - cnt[k];
+    if (lane == 31) s_wcnt[threadIdx.x >> 5][k] = inc;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const uint32_t t = s_wcnt[lane][k];
+      uint32_t inc = t;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += u;
+      }
+      s_wcnt[lane][k] = inc - t;
+      const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
+      if (lane == 0) {
+        unsigned long long* ctrk = k == 0 ? &ctr->n_max : (k == 1 ? &ctr->n_min : &ctr->n_exit);
+        s_lbase[k] = total ? atomicAdd(ctrk, (unsigned long long)total) : 0ull;
+      }
+    }
+  }
+  __syncthreads();
+  uint64_t pos[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) pos[k] = s_lbase[k] + s_wcnt[threadIdx.x >> 5][k] + pre[k];
+#pragma unroll 2
+  for (int lz = 0; lz < TZ; ++lz) {
+    const int l = lx + TX * ly + TX * TY * lz;
+    const uint32_t c = hop[l];
+    if (c == 0xff) continue;
+    const uint32_t gv = gid(l);
+    const int ud = Pd[l], ua = Pa[l];
+    desc[gv] = gid(ud) + uint32_t(s_gdelta[hop[ud] & 15]);
+    asc[gv] = gid(ua) + uint32_t(s_gdelta[hop[ua] >> 4]);
+    const uint32_t bit = 1u << lz;
+    if (mmax & bit) {
+      if (pos[0] < ext_cap) maxima[pos[0]] = gv;
+      ++pos[0];
+    }
+    if (mmin & bit) {
+      if (pos[1] < ext_cap) minima[pos[1]] = gv;
+      ++pos[1];
+    }
+    if (mxd & bit) {
+      if (pos[2] < exit_cap) exits[pos[2]] = gv + uint32_t(s_gdelta[c & 15]);
+      ++pos[2];
+    }
+    if (mxa & bit) {
+      if (pos[2] < exit_cap) exits[pos[2]] = gv + uint32_t(s_gdelta[c >> 4]);
+      ++pos[2];
+    }
   }
 }
 
@@ -467,11 +540,20 @@ __global__ void k_u32_to_u64(const uint32_t* __restrict__ in, int64_t n, uint64_
 // ---------------------------------------------------------------- pass D --
 // D1: ms[v] = dense id of the final pair (hash value slot), warp-deduped
 // lookups, 4 vertices per thread per step.
-__global__ void __launch_bounds__(256) k_assign_ms(uint32_t n, const uint32_t* __restrict__ desc,
+// Also writes the vertex's edge-equality mask: bit k-1 (k = 1..7, k = dx |
+// dy << 1 | dz << 2) is set when the vertex and its +offset-k neighbour share
+// a Morse-Smale region (equal (asc, desc) pair <=> equal dense id). Every tet
+// edge is such a positive stencil edge, so a cube is one region iff its min
+// corner's mask is 0x7f, and all 19 label equalities the 6 tet codes need
+// are mask bits of the cube's corners 0..6.
+__global__ void __launch_bounds__(256) k_assign_ms(uint32_t n, uint32_t X, uint32_t Y, uint32_t Z,
+                                                   const uint32_t* __restrict__ desc,
                                                    const uint32_t* __restrict__ asc,
                                                    const unsigned long long* __restrict__ fset, uint64_t fmask,
-                                                   const uint32_t* __restrict__ slot_id, uint32_t* __restrict__ ms) {
+                                                   const uint32_t* __restrict__ slot_id, uint32_t* __restrict__ ms,
+                                                   uint8_t* __restrict__ emask) {
   const int lane = threadIdx.x & 31;
+  const uint32_t XY = X * Y;
   const uint32_t stride = gridDim.x * blockDim.x * C_VPT;
   for (uint32_t base = blockIdx.x * blockDim.x * C_VPT; base < n; base += stride) {
     uint64_t key[C_VPT];
@@ -488,280 +570,24 @@ __global__ void __launch_bounds__(256) k_assign_ms(uint32_t n, const uint32_t* _
       uint32_t id = 0;
       if (lane == leader && key[k] != kEmpty) id = __ldg(slot_id + set_find(fset, fmask, key[k]));
       id = __shfl_sync(0xffffffffu, id, leader);
-      if (v < n) ms[v] = id;
-    }
-  }
-}
-
-// D2: ordered single-pass marching over row slabs in the reference cell
-// order (cube-major, x fastest): ms rows of the slab plus the +y row and +z
-// layer staged in shared memory, 6 tet codes per cube, block scan, decoupled
-// look-back across slabs for the output offset, records in reference order.
-constexpr int D_THREADS = 512;
-constexpr int D_CUBES = 8192;  // cubes per row-slab tile (target)
-
-__constant__ uint32_t c_rows[PLMSS_TET_ROWS];
-__constant__ uint16_t c_cases[32];
-
-struct DDims {
-  uint32_t X, Y, Z, XY, n;
-  uint32_t ty;      // rows per slab
-  uint32_t nyb;     // slabs per z layer
-  uint32_t ntiles;  // Z * nyb
-};
-
-__device__ __forceinline__ int tet_code(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
-  const int l1 = b == a ? 0 : 1;
-  const int l2 = c == a ? 0 : (c == b ? l1 : 2);
-  const int l3 = d == a ? 0 : (d == b ? l1 : (d == c ? l2 : 3));
-  return (l1 << 4) | (l2 << 2) | l3;
-}
-
-constexpr uint64_t FLAG_A = uint64_t(1) << 62, FLAG_P = uint64_t(2) << 62, VAL_MASK = (uint64_t(1) << 62) - 1;
-
-
-__device__ __forceinline__ int case_count6(uint32_t code6, const uint16_t* cases) {
-  return (cases[code6 & 31] & 15) + (cases[(code6 >> 5) & 31] & 15) + (cases[(code6 >> 10) & 31] & 15) +
-         (cases[(code6 >> 15) & 31] & 15) + (cases[(code6 >> 20) & 31] & 15) + (cases[(code6 >> 25) & 31] & 15);
-}
-
-// Cubes are processed in 32-cube chunks (lane i <-> cube 32*chunk + i), so
-// consecutive lanes touch consecutive shared-memory words (no bank
-// conflicts) and a warp's records land in one contiguous output range.
-constexpr int D_CHUNKS = D_CUBES / 32;
-
-__global__ void __launch_bounds__(D_THREADS, 2)
-    k_march(DDims d, const uint32_t* __restrict__ ms, unsigned long long* __restrict__ tile_state,
-            unsigned int* __restrict__ ticket, plmss_tri* __restrict__ out, uint64_t out_cap, float inv_cx,
-            uint32_t ms_words) {
-  extern __shared__ uint32_t dsm[];
-  uint32_t* s_ms = dsm;                 // (ty + 1) rows x 2 layers x X
-  uint32_t* s_code = dsm + ms_words;    // packed 6 x 5-bit tet codes per cube
-  __shared__ uint32_t s_rows[PLMSS_TET_ROWS];
-  __shared__ uint16_t s_cases[32];
-  __shared__ uint32_t s_chunk[D_CHUNKS];
-  __shared__ uint32_t s_tile;
-  __shared__ unsigned long long s_excl;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
-  if (threadIdx.x < PLMSS_TET_ROWS) s_rows[threadIdx.x] = c_rows[threadIdx.x];
-  if (threadIdx.x < 32) s_cases[threadIdx.x] = c_cases[threadIdx.x];
-  __syncthreads();
-  const uint32_t tile = s_tile;
-  const uint32_t z = tile / d.nyb, yb = tile % d.nyb;
-  const uint32_t y0 = yb * d.ty, y1 = min(d.Y, y0 + d.ty);
-  const uint32_t rows = min(d.Y, y1 + 1) - y0;  // rows staged (incl. the +1 halo row)
-  const bool has_cubes = z + 1 < d.Z && y0 + 1 < d.Y;
-  const uint32_t X = d.X, CX = d.X - 1;
-
-  // Stage the slab: two contiguous runs (layer z rows y0.., layer z+1 rows
-  // y0..). With 16-byte alignment they go through the bulk-copy (TMA) engine
-  // on an mbarrier; otherwise an unrolled vector-free loop.
-  __shared__ __align__(8) uint64_t s_bar;
-  if (has_cubes) {
-    const uint32_t rx = rows * X;
-    const uint32_t* src0 = ms + uint64_t(X) * (y0 + uint64_t(d.Y) * z);
-    const uint32_t* src1 = src0 + d.XY;
-    const bool bulk = ((reinterpret_cast<uintptr_t>(src0) | reinterpret_cast<uintptr_t>(src1)) & 15) == 0 &&
-                      (rx & 3) == 0;
-    if (bulk) {
-      const uint32_t bar = smem_u32(&s_bar);
-      if (threadIdx.x == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-      }
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(rx * 8) : "memory");
-        asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                smem_u32(s_ms)),
-            "l"(src0), "r"(rx * 4), "r"(bar)
-            : "memory");
-        asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                smem_u32(s_ms + rx)),
-            "l"(src1), "r"(rx * 4), "r"(bar)
-            : "memory");
-      }
-      asm volatile(
-          "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n @!p bra WAIT_%=;\n}" ::"r"(
-              bar)
-          : "memory");
-    } else {
-      const uint32_t nload = 2 * rx;
-      for (uint32_t i0 = 0; i0 < nload; i0 += 8 * D_THREADS) {
-        uint32_t v[8];
+      if (v < n) {
+        ms[v] = id;
+        const uint32_t x = v % X, y = (v / X) % Y, z = v / XY;
+        const bool bx = x + 1 < X, by = y + 1 < Y, bz = z + 1 < Z;
+        uint32_t m = 0;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const uint32_t i = i0 + k * D_THREADS + threadIdx.x;
-          v[k] = i < nload ? __ldg(i < rx ? src0 + i : src1 + (i - rx)) : 0u;
+        for (int o = 1; o < 8; ++o) {
+          const bool ok = (!(o & 1) || bx) && (!(o & 2) || by) && (!(o & 4) || bz);
+          if (ok) {
+            const uint32_t u = v + ((o & 1) ? 1u : 0u) + ((o & 2) ? X : 0u) + ((o & 4) ? XY : 0u);
+            const uint64_t ku = (uint64_t(__ldg(asc + u)) << 32) | __ldg(desc + u);
+            m |= uint32_t(ku == key[k]) << (o - 1);
+          }
         }
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const uint32_t i = i0 + k * D_THREADS + threadIdx.x;
-          if (i < nload) s_ms[i] = v[k];
-        }
+        emask[v] = uint8_t(m);
       }
     }
   }
-  __syncthreads();
-
-  const uint32_t cy1 = min(y1, d.Y - 1);
-  const uint32_t ncubes = has_cubes ? CX * (cy1 - y0) : 0;
-  const uint32_t nchunks = (ncubes + 31) / 32;
-  const uint32_t LZ = rows * X;
-  // phase 2: codes and per-chunk counts
-  for (uint32_t ch = w; ch < nchunks; ch += D_THREADS / 32) {
-    const uint32_t q = ch * 32 + lane;
-    uint32_t code6 = 0;
-    int cnt = 0;
-    if (q < ncubes) {
-      const uint32_t cr = uint32_t((float(q) + 0.5f) * inv_cx), cx = q - cr * CX;
-      const uint32_t b = cx + X * cr;
-      const uint32_t l0 = s_ms[b], l1 = s_ms[b + 1], l2 = s_ms[b + X], l3 = s_ms[b + X + 1];
-      const uint32_t l4 = s_ms[b + LZ], l5 = s_ms[b + LZ + 1], l6 = s_ms[b + LZ + X], l7 = s_ms[b + LZ + X + 1];
-      if (!(l0 == l7 && l1 == l7 && l2 == l7 && l3 == l7 && l4 == l7 && l5 == l7 && l6 == l7)) {
-        code6 = uint32_t(tet_code(l0, l1, l3, l7)) | uint32_t(tet_code(l0, l1, l5, l7)) << 5 |
-                uint32_t(tet_code(l0, l2, l3, l7)) << 10 | uint32_t(tet_code(l0, l2, l6, l7)) << 15 |
-                uint32_t(tet_code(l0, l4, l5, l7)) << 20 | uint32_t(tet_code(l0, l4, l6, l7)) << 25;
-        cnt = case_count6(code6, s_cases);
-      }
-      s_code[q] = code6;
-    }
-    const uint32_t tot = __reduce_add_sync(0xffffffffu, uint32_t(cnt));
-    if (lane == 0) s_chunk[ch] = tot;
-  }
-  __syncthreads();
-  // chunk offsets (warp 0) + decoupled look-back across slabs
-  if (w == 0) {
-    constexpr int PER = D_CHUNKS / 32;
-    uint32_t v[PER], sum = 0;
-#pragma unroll
-    for (int k = 0; k < PER; ++k) {
-      const uint32_t ch = lane * PER + k;
-      v[k] = ch < nchunks ? s_chunk[ch] : 0;
-      sum += v[k];
-    }
-    uint32_t inc = sum;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
-      if (lane >= o) inc += t;
-    }
-    uint32_t run = inc - sum;
-#pragma unroll
-    for (int k = 0; k < PER; ++k) {
-      const uint32_t ch = lane * PER + k;
-      if (ch < nchunks) s_chunk[ch] = run;
-      run += v[k];
-    }
-    const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
-    // tile 0 always publishes a prefix, so a window reaching it stops there
-    if (lane == 0) {
-      if (tile == 0) {
-        atomicExch(tile_state, FLAG_P | uint64_t(total));
-        s_excl = 0;
-      } else {
-        atomicExch(tile_state + tile, FLAG_A | uint64_t(total));
-      }
-    }
-    if (tile != 0) {
-      uint64_t excl = 0;
-      int64_t j = int64_t(tile) - 1;
-      for (;;) {
-        const int64_t jj = j - lane;
-        uint64_t st = 0;
-        if (jj >= 0) {
-          do {
-            st = *((volatile unsigned long long*)(tile_state + jj));
-          } while ((st >> 62) == 0);
-        }
-        const unsigned pmask = __ballot_sync(0xffffffffu, (st >> 62) == 2);
-        const int stop = pmask ? __ffs(pmask) - 1 : 32;
-        uint64_t vv = (lane <= stop && jj >= 0) ? (st & VAL_MASK) : 0;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) vv += __shfl_xor_sync(0xffffffffu, vv, o);
-        excl += vv;
-        if (pmask) break;
-        j -= 32;
-      }
-      if (lane == 0) {
-        atomicExch(tile_state + tile, FLAG_P | (excl + total));
-        s_excl = excl;
-      }
-    }
-  }
-  __syncthreads();
-  // phase 3: emission in reference order
-  const uint64_t cell_base = 6ull * (uint64_t(CX) * (uint64_t(y0) + uint64_t(d.Y - 1) * z));
-  const uint64_t tile_base = s_excl;
-  for (uint32_t ch = w; ch < nchunks; ch += D_THREADS / 32) {
-    const uint32_t q = ch * 32 + lane;
-    const uint32_t code6 = q < ncubes ? s_code[q] : 0;
-    const uint32_t cnt = code6 ? uint32_t(case_count6(code6, s_cases)) : 0u;
-    if (!__any_sync(0xffffffffu, cnt != 0)) continue;
-    uint32_t inc = cnt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
-      if (lane >= o) inc += t;
-    }
-    // Warp-cooperative emission: the chunk's T records are dealt out one per
-    // lane, so every store instruction writes 32 consecutive records.
-    const uint32_t T = __shfl_sync(0xffffffffu, inc, 31);
-    const uint64_t chunk_base = tile_base + s_chunk[ch];
-    const uint32_t cr = uint32_t((float(q) + 0.5f) * inv_cx), cx = q - cr * CX;
-    const uint32_t bq = cx + X * cr;  // cube base index in the staged slab
-    for (uint32_t j0 = 0; j0 < T; j0 += 32) {
-      const uint32_t j = j0 + lane;
-      // lane owning record j = number of lanes whose inclusive count is <= j
-      // (binary search over the warp's nondecreasing prefix via shuffles)
-      int src = 0;
-#pragma unroll
-      for (int step = 16; step >= 1; step >>= 1) {
-        const uint32_t v = __shfl_sync(0xffffffffu, inc, src + step - 1);
-        if (v <= j) src += step;
-      }
-      const uint32_t c6 = __shfl_sync(0xffffffffu, code6, src & 31);
-      const uint32_t ex = __shfl_sync(0xffffffffu, inc - cnt, src & 31);
-      const uint32_t b = __shfl_sync(0xffffffffu, bq, src & 31);
-      if (j >= T) continue;
-      uint32_t k = j - ex;
-      int t = 0;
-      uint32_t cs = s_cases[c6 & 31];
-#pragma unroll
-      for (int tt = 0; tt < 5; ++tt) {
-        if (k < (cs & 15)) break;
-        k -= cs & 15;
-        ++t;
-        cs = s_cases[(c6 >> (5 * t)) & 31];
-      }
-      const uint32_t rowi = (cs >> 4) + k;
-      const uint32_t row = s_rows[rowi];
-      // tet t = cube corners {0, cb, cc, 7}; corner c -> slab offset
-      const uint32_t cb = (0x442211u >> (4 * t)) & 15, cc = (0x656353u >> (4 * t)) & 15;
-      auto corner = [&](uint32_t p) { return p == 0 ? 0u : (p == 1 ? cb : (p == 2 ? cc : 7u)); };
-      auto off = [&](uint32_t c) { return (c & 1) + X * ((c >> 1) & 1) + LZ * (c >> 2); };
-      const uint32_t la = s_ms[b + off(corner((row >> 12) & 3))];
-      const uint32_t lb = s_ms[b + off(corner((row >> 14) & 3))];
-      const uint64_t pos = chunk_base + j;
-      if (pos < out_cap) {
-        const uint64_t cr64 = ((cell_base + 6ull * (ch * 32 + uint32_t(src)) + t) << 6) | uint64_t(rowi);
-        uint4 rec;
-        rec.x = uint32_t(cr64);
-        rec.y = uint32_t(cr64 >> 32);
-        rec.z = min(la, lb);
-        rec.w = max(la, lb);
-        *reinterpret_cast<uint4*>(out + pos) = rec;
-      }
-    }
-  }
-}
-
-__global__ void k_read_total(const unsigned long long* __restrict__ tile_state, uint32_t last,
-                             unsigned long long* __restrict__ out) {
-  *out = tile_state[last] & VAL_MASK;
 }
 
 bool g_consts_ready[64] = {};
@@ -770,15 +596,12 @@ bool g_consts_ready[64] = {};
 
 // Host driver of the fused pipeline. Returns false when the dims are outside
 // the fused path's envelope (then the caller uses the staged kernels).
-bool fused_supported(const Grid& g) { return g.X - 1 <= D_CUBES && g.n < (int64_t(1) << 32) - 1; }
+bool fused_supported(const Grid& g) { return g.n < (int64_t(1) << 32) - 1; }
 
 FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* desc, uint32_t* asc, uint32_t* ms) {
   FusedOut o{};
   for (auto& s : c.stats) s = 0;
   if (c.device >= 0 && c.device < 64 && !g_consts_ready[c.device]) {
-    CK(cudaMemcpyToSymbol(c_rows, kTetRowsPacked, sizeof(kTetRowsPacked)));
-    CK(cudaMemcpyToSymbol(c_cases, kTetCasePacked, sizeof(kTetCasePacked)));
-    CK(cudaFuncSetAttribute(k_march, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CK(cudaFuncSetAttribute(k_tile_segment<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kASmem));
     CK(cudaFuncSetAttribute(k_tile_segment<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kASmem));
     g_consts_ready[c.device] = true;
@@ -823,13 +646,10 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
   }
   c.stats[4] = use_tma ? 1 : 0;
 
-  // Device counters: [0, 64) ACounters, int flag at +128, ticket at +160,
-  // triangle total at +192 (bytes).
+  // Device counters: [0, 64) ACounters, int flag at +128 (bytes).
   char* ctr_base = static_cast<char*>(c.get(S_FLAGS, 1024));
   ACounters* ctr = reinterpret_cast<ACounters*>(ctr_base);
   int* flag = reinterpret_cast<int*>(ctr_base + 128);
-  unsigned int* ticket = reinterpret_cast<unsigned int*>(ctr_base + 160);
-  unsigned long long* tot = reinterpret_cast<unsigned long long*>(ctr_base + 192);
   for (int attempt = 0;; ++attempt) {
     const uint64_t ext_cap = c.fused_ext_cap ? c.fused_ext_cap : uint64_t(g.n / 4 + 1024);
     uint32_t* maxima = c.get_t<uint32_t>(S_MAXIMA, ext_cap);
@@ -941,48 +761,13 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
     o.n_regions = R;
     c.stats[2] = int64_t(fcap);
     // ---- D1: dense MS ids per vertex
+    uint8_t* emask = c.get_t<uint8_t>(S_MASK, g.n + 64);
     k_assign_ms<<<unsigned(std::min<int64_t>((g.n + 1023) / 1024, int64_t(c.sm_count) * 16)), 256, 0, c.stream>>>(
-        d.n, desc, asc, fset, fcap - 1, slot_id, ms);
+        d.n, d.X, d.Y, d.Z, desc, asc, fset, fcap - 1, slot_id, ms, emask);
     CK_LAUNCH("k_assign_ms");
     c.mark(4);
-    // ---- D2: ordered marching
-    DDims dd;
-    dd.X = d.X;
-    dd.Y = d.Y;
-    dd.Z = d.Z;
-    dd.XY = d.XY;
-    dd.n = d.n;
-    dd.ty = std::max<uint32_t>(1, uint32_t(D_CUBES / std::max<int64_t>(1, g.X - 1)));
-    dd.ty = std::min<uint32_t>(dd.ty, d.Y);
-    dd.nyb = (d.Y + dd.ty - 1) / dd.ty;
-    dd.ntiles = dd.nyb * d.Z;
-    const uint32_t ms_words = (dd.ty + 1) * 2 * d.X;
-    const size_t smem = size_t(ms_words + D_CUBES) * sizeof(uint32_t);
-    if (smem > 200 * 1024) fail(PLMSS_ERR_LOGIC, "row slab exceeds shared memory");
-    auto* tstate = c.get_t<unsigned long long>(S_SCAN_C, dd.ntiles + 1);
-    for (int pass = 0;; ++pass) {
-      const uint64_t cap = c.fused_tri_cap ? c.fused_tri_cap : uint64_t(g.n / 2 + 1024);
-      plmss_tri* tris = c.get_t<plmss_tri>(S_TRIS, cap);
-      CK(cudaMemsetAsync(tstate, 0, (dd.ntiles + 1) * 8, c.stream));
-      CK(cudaMemsetAsync(ticket, 0, 4, c.stream));
-      k_march<<<dd.ntiles, D_THREADS, smem, c.stream>>>(dd, ms, tstate, ticket, tris, cap,
-                                                        1.0f / float(std::max<int64_t>(1, g.X - 1)), ms_words);
-      CK_LAUNCH("k_march");
-      k_read_total<<<1, 1, 0, c.stream>>>(tstate, dd.ntiles - 1, tot);
-      CK_LAUNCH("k_read_total");
-      CK(cudaMemcpyAsync(c.h_pinned, tot, 8, cudaMemcpyDeviceToHost, c.stream));
-      c.sync();
-      const uint64_t T = c.h_pinned[0];
-      if (T > cap) {
-        c.fused_tri_cap = T + T / 20 + 1024;
-        if (pass > 2) fail(PLMSS_ERR_LOGIC, "separator capacity retries exhausted");
-        ++c.stats[3];
-        continue;  // re-run D2 only
-      }
-      o.n_tris = int64_t(T);
-      o.tris = tris;
-      break;
-    }
+    // ---- D2: ordered marching (count, scan, emit)
+    o.n_tris = fused_march(c, g, ms, emask, &o.tris);
     c.mark(5);
     o.maxima = maxima;
     o.minima = minima;
