@@ -546,7 +546,9 @@ __global__ void k_u32_to_u64(const uint32_t* __restrict__ in, int64_t n, uint64_
 // edge is such a positive stencil edge, so a cube is one region iff its min
 // corner's mask is 0x7f, and all 19 label equalities the 6 tet codes need
 // are mask bits of the cube's corners 0..6.
-__global__ void __launch_bounds__(256) k_assign_ms(uint32_t n, uint32_t X, uint32_t Y, uint32_t Z,
+// One block per x-row segment (blockIdx.x = segment, blockIdx.y = row
+// y + Y*z), so coordinates need no division.
+__global__ void __launch_bounds__(256) k_assign_ms(uint32_t X, uint32_t Y, uint32_t Z,
                                                    const uint32_t* __restrict__ desc,
                                                    const uint32_t* __restrict__ asc,
                                                    const unsigned long long* __restrict__ fset, uint64_t fmask,
@@ -554,40 +556,36 @@ __global__ void __launch_bounds__(256) k_assign_ms(uint32_t n, uint32_t X, uint3
                                                    uint8_t* __restrict__ emask) {
   const int lane = threadIdx.x & 31;
   const uint32_t XY = X * Y;
-  const uint32_t stride = gridDim.x * blockDim.x * C_VPT;
-  for (uint32_t base = blockIdx.x * blockDim.x * C_VPT; base < n; base += stride) {
-    uint64_t key[C_VPT];
+  const uint32_t nseg = (X + blockDim.x - 1) / blockDim.x;
+  const uint32_t row = blockIdx.x / nseg, seg = blockIdx.x - row * nseg;
+  const uint32_t y = row % Y, z = row / Y;
+  const bool by = y + 1 < Y, bz = z + 1 < Z;
+  const uint32_t x = seg * blockDim.x + threadIdx.x;
+  const bool ok = x < X;
+  const uint32_t v = row * X + x;
+  const uint64_t key = ok ? ((uint64_t(__ldg(asc + v)) << 32) | __ldg(desc + v)) : kEmpty;
+  // neighbour pairs first (independent loads in flight together)
+  uint32_t nd[7], na[7];
+  const bool bx = x + 1 < X;
 #pragma unroll
-    for (int k = 0; k < C_VPT; ++k) {
-      const uint32_t v = base + k * blockDim.x + threadIdx.x;
-      key[k] = v < n ? ((uint64_t(__ldg(asc + v)) << 32) | __ldg(desc + v)) : kEmpty;
-    }
-#pragma unroll
-    for (int k = 0; k < C_VPT; ++k) {
-      const uint32_t v = base + k * blockDim.x + threadIdx.x;
-      const unsigned peers = __match_any_sync(0xffffffffu, key[k]);
-      const int leader = __ffs(peers) - 1;
-      uint32_t id = 0;
-      if (lane == leader && key[k] != kEmpty) id = __ldg(slot_id + set_find(fset, fmask, key[k]));
-      id = __shfl_sync(0xffffffffu, id, leader);
-      if (v < n) {
-        ms[v] = id;
-        const uint32_t x = v % X, y = (v / X) % Y, z = v / XY;
-        const bool bx = x + 1 < X, by = y + 1 < Y, bz = z + 1 < Z;
-        uint32_t m = 0;
-#pragma unroll
-        for (int o = 1; o < 8; ++o) {
-          const bool ok = (!(o & 1) || bx) && (!(o & 2) || by) && (!(o & 4) || bz);
-          if (ok) {
-            const uint32_t u = v + ((o & 1) ? 1u : 0u) + ((o & 2) ? X : 0u) + ((o & 4) ? XY : 0u);
-            const uint64_t ku = (uint64_t(__ldg(asc + u)) << 32) | __ldg(desc + u);
-            m |= uint32_t(ku == key[k]) << (o - 1);
-          }
-        }
-        emask[v] = uint8_t(m);
-      }
-    }
+  for (int o = 1; o < 8; ++o) {
+    const bool in = ok && (!(o & 1) || bx) && (!(o & 2) || by) && (!(o & 4) || bz);
+    const uint32_t u = v + ((o & 1) ? 1u : 0u) + ((o & 2) ? X : 0u) + ((o & 4) ? XY : 0u);
+    nd[o - 1] = in ? __ldg(desc + u) : ~0u;
+    na[o - 1] = in ? __ldg(asc + u) : ~0u;
   }
+  const unsigned peers = __match_any_sync(0xffffffffu, key);
+  const int leader = __ffs(peers) - 1;
+  uint32_t id = 0;
+  if (lane == leader && key != kEmpty) id = __ldg(slot_id + set_find(fset, fmask, key));
+  id = __shfl_sync(0xffffffffu, id, leader);
+  if (!ok) return;
+  ms[v] = id;
+  const uint32_t kd = uint32_t(key), ka = uint32_t(key >> 32);
+  uint32_t m = 0;
+#pragma unroll
+  for (int o = 0; o < 7; ++o) m |= uint32_t(nd[o] == kd && na[o] == ka) << o;
+  emask[v] = uint8_t(m);
 }
 
 bool g_consts_ready[64] = {};
@@ -762,8 +760,10 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
     c.stats[2] = int64_t(fcap);
     // ---- D1: dense MS ids per vertex
     uint8_t* emask = c.get_t<uint8_t>(S_MASK, g.n + 64);
-    k_assign_ms<<<unsigned(std::min<int64_t>((g.n + 1023) / 1024, int64_t(c.sm_count) * 16)), 256, 0, c.stream>>>(
-        d.n, d.X, d.Y, d.Z, desc, asc, fset, fcap - 1, slot_id, ms, emask);
+    {
+      const unsigned grid = unsigned((g.X + 255) / 256 * g.Y * g.Z);
+      k_assign_ms<<<grid, 256, 0, c.stream>>>(d.X, d.Y, d.Z, desc, asc, fset, fcap - 1, slot_id, ms, emask);
+    }
     CK_LAUNCH("k_assign_ms");
     c.mark(4);
     // ---- D2: ordered marching (count, scan, emit)

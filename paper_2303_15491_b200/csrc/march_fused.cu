@@ -23,19 +23,27 @@ __constant__ uint16_t c_mcases[32];
 
 struct MDims {
   uint32_t X, XY, CX, CY;
-  uint64_t cubes;
-  double inv_cx, inv_cy;
+  uint32_t nxc;  // 32-cube chunks per cube row (a row = fixed cy, cz)
 };
 
 constexpr int M_THREADS = 256;
 
-// cube id -> index of its min-corner vertex
-__device__ __forceinline__ uint32_t cube_vertex(uint64_t q, const MDims& d) {
-  const uint64_t r = uint64_t((double(q) + 0.5) * d.inv_cx);  // q / CX (exact: q < 2^33)
-  const uint32_t cx = uint32_t(q - r * d.CX);
-  const uint64_t cz = uint64_t((double(r) + 0.5) * d.inv_cy);
-  const uint32_t cy = uint32_t(r - cz * d.CY);
-  return cx + d.X * cy + d.XY * uint32_t(cz);
+// Chunk ch covers cubes cx = 32*xs + lane of cube row r = cy + CY*cz, with
+// (r, xs) = divmod(ch, nxc): chunk order is the reference cell order.
+struct ChunkPos {
+  uint64_t q0;  // cube id of lane 0
+  uint32_t v0;  // min-corner vertex of lane 0's cube
+  uint32_t n;   // cubes in the chunk
+};
+
+// Warps walk whole cube rows (one division per row, none per chunk).
+__device__ __forceinline__ ChunkPos chunk_pos(uint32_t r, uint32_t cy, uint32_t cz, uint32_t xs,
+                                              const MDims& d) {
+  ChunkPos p;
+  p.q0 = uint64_t(r) * d.CX + 32u * xs;
+  p.v0 = 32u * xs + d.X * cy + d.XY * cz;
+  p.n = min(32u, d.CX - 32u * xs);
+  return p;
 }
 
 __device__ __forceinline__ void load_tables(uint16_t* s_tlut, uint16_t* s_cases, uint32_t* s_rows) {
@@ -85,13 +93,17 @@ __global__ void __launch_bounds__(M_THREADS) k_march_count(MDims d, const uint8_
   load_tables(s_tlut, s_cases, nullptr);
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  const uint64_t warps = uint64_t(gridDim.x) * (M_THREADS / 32);
-  for (uint64_t ch = uint64_t(blockIdx.x) * (M_THREADS / 32) + (threadIdx.x >> 5); ch < nchunks; ch += warps) {
-    const uint64_t q = ch * 32 + lane;
-    uint32_t cnt = 0;
-    if (q < d.cubes) cube_codes(emask, cube_vertex(q, d), d.X, d.XY, s_tlut, cnt);
-    cnt = __reduce_add_sync(0xffffffffu, cnt);
-    if (lane == 0) counts[ch] = cnt;
+  const uint32_t warps = gridDim.x * (M_THREADS / 32);
+  const uint32_t nrows = uint32_t(nchunks / d.nxc);
+  for (uint32_t r = blockIdx.x * (M_THREADS / 32) + (threadIdx.x >> 5); r < nrows; r += warps) {
+    const uint32_t cz = r / d.CY, cy = r - cz * d.CY;
+    for (uint32_t xs = 0; xs < d.nxc; ++xs) {
+      const ChunkPos p = chunk_pos(r, cy, cz, xs, d);
+      uint32_t cnt = 0;
+      if (uint32_t(lane) < p.n) cube_codes(emask, p.v0 + lane, d.X, d.XY, s_tlut, cnt);
+      cnt = __reduce_add_sync(0xffffffffu, cnt);
+      if (lane == 0) counts[uint64_t(r) * d.nxc + xs] = cnt;
+    }
   }
 }
 
@@ -104,17 +116,19 @@ __global__ void __launch_bounds__(M_THREADS) k_march_emit(MDims d, const uint8_t
   load_tables(s_tlut, s_cases, s_rows);
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  const uint64_t warps = uint64_t(gridDim.x) * (M_THREADS / 32);
-  for (uint64_t ch = uint64_t(blockIdx.x) * (M_THREADS / 32) + (threadIdx.x >> 5); ch < nchunks; ch += warps) {
+  const uint32_t warps = gridDim.x * (M_THREADS / 32);
+  const uint32_t nrows = uint32_t(nchunks / d.nxc);
+  for (uint32_t r = blockIdx.x * (M_THREADS / 32) + (threadIdx.x >> 5); r < nrows; r += warps) {
+   const uint32_t cz = r / d.CY, cy = r - cz * d.CY;
+   for (uint32_t xs = 0; xs < d.nxc; ++xs) {
+    const uint64_t ch = uint64_t(r) * d.nxc + xs;
     const uint64_t base = offsets[ch];
     const uint64_t T64 = (ch + 1 < nchunks ? offsets[ch + 1] : total) - base;
     if (T64 == 0) continue;
-    const uint64_t q = ch * 32 + lane;
-    uint32_t cnt = 0, code6 = 0, v0 = 0;
-    if (q < d.cubes) {
-      v0 = cube_vertex(q, d);
-      code6 = cube_codes(emask, v0, d.X, d.XY, s_tlut, cnt);
-    }
+    const ChunkPos p = chunk_pos(r, cy, cz, xs, d);
+    uint32_t cnt = 0, code6 = 0;
+    const uint32_t v0 = p.v0 + lane;
+    if (uint32_t(lane) < p.n) code6 = cube_codes(emask, v0, d.X, d.XY, s_tlut, cnt);
     uint32_t inc = cnt;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -153,7 +167,7 @@ __global__ void __launch_bounds__(M_THREADS) k_march_emit(MDims d, const uint8_t
       auto off = [&](uint32_t c) { return (c & 1) + d.X * ((c >> 1) & 1) + d.XY * (c >> 2); };
       const uint32_t la = __ldg(ms + b + off(corner((row >> 12) & 3)));
       const uint32_t lb = __ldg(ms + b + off(corner((row >> 14) & 3)));
-      const uint64_t cr64 = ((6ull * (ch * 32 + uint32_t(src)) + t) << 6) | uint64_t(rowi);
+      const uint64_t cr64 = ((6ull * (p.q0 + uint32_t(src)) + t) << 6) | uint64_t(rowi);
       uint4 rec;
       rec.x = uint32_t(cr64);
       rec.y = uint32_t(cr64 >> 32);
@@ -161,6 +175,7 @@ __global__ void __launch_bounds__(M_THREADS) k_march_emit(MDims d, const uint8_t
       rec.w = max(la, lb);
       *reinterpret_cast<uint4*>(out + base + j) = rec;
     }
+   }
   }
 }
 
@@ -179,14 +194,13 @@ int64_t fused_march(Ctx& c, const Grid& g, const uint32_t* ms, const uint8_t* em
   d.XY = uint32_t(g.X * g.Y);
   d.CX = uint32_t(g.X - 1);
   d.CY = uint32_t(g.Y - 1);
-  d.cubes = uint64_t(g.cubes);
-  d.inv_cx = 1.0 / double(d.CX);
-  d.inv_cy = 1.0 / double(d.CY);
-  const uint64_t nchunks = (d.cubes + 31) / 32;
+  d.nxc = (d.CX + 31) / 32;
+  const uint64_t nchunks = uint64_t(d.nxc) * uint64_t(g.Y - 1) * uint64_t(g.Z - 1);
   *out = nullptr;
   if (nchunks == 0) return 0;
   uint64_t* counts = c.get_t<uint64_t>(S_TMP1, nchunks);
-  const unsigned grid = unsigned(std::min<uint64_t>((nchunks + 7) / 8, uint64_t(c.sm_count) * 32));
+  const uint64_t nrows = uint64_t(g.Y - 1) * uint64_t(g.Z - 1);
+  const unsigned grid = unsigned(std::min<uint64_t>((nrows + 7) / 8, uint64_t(c.sm_count) * 32));
   k_march_count<<<grid, M_THREADS, 0, c.stream>>>(d, emask, nchunks, counts);
   CK_LAUNCH("k_march_count");
   const uint64_t total = exclusive_scan_u64(c, counts, int64_t(nchunks), true);
