@@ -121,6 +121,14 @@ int plmss_b200_segment(plmss_ctx* ctx, const int64_t dims[3], int key_type, cons
 int plmss_b200_seed_hops(plmss_ctx* ctx, const int64_t dims[3], int key_type, const void* d_keys,
                          uint32_t* d_desc, uint32_t* d_asc);
 
+/* One path-compression sweep over an active list (detail::compress_sweep /
+ * compress_sweep_both, segmentation.cpp:48-58, 87-105): label <- label[label]
+ * for every active vertex (d_asc may be NULL), in place and concurrently like
+ * the reference's workers; d_next receives the still-unsettled vertices in
+ * list order, *n_next their count. */
+int plmss_b200_compress_sweep(plmss_ctx* ctx, uint32_t* d_desc, uint32_t* d_asc, const uint32_t* d_active,
+                              int64_t n_active, uint32_t* d_next, int64_t* n_next);
+
 /* ---- Morse-Smale combine ------------------------------------------------
  * Replaces combine_ms (segmentation.hpp:80, segmentation.cpp:170-196):
  * d_ms[v] = rank of (asc[v], desc[v]) among the distinct pairs in
@@ -136,6 +144,13 @@ int plmss_b200_combine_ms(plmss_ctx* ctx, int64_t n, const uint32_t* d_asc, cons
  * codes (d_codes, 6(X-1)(Y-1)(Z-1) bytes, may be NULL) and the total. */
 int plmss_b200_index_separators(plmss_ctx* ctx, const int64_t dims[3], int label_type,
                                 const void* d_labels, uint8_t* d_codes, int64_t* total);
+
+/* Separator primitives per contiguous cell range [bounds[i], bounds[i+1])
+ * (nranges + 1 bounds) — the per-worker counts of EmitPlan
+ * (marching.hpp:81-93, marching.cpp:116-133), computed on the device. */
+int plmss_b200_count_by_cell_ranges(plmss_ctx* ctx, const int64_t dims[3], int label_type,
+                                    const void* d_labels, const int64_t* h_bounds, int nranges,
+                                    int64_t* h_counts);
 
 /* emit_separators (marching.hpp:115-117, marching.cpp:136-215): compact
  * records in reference order. d_out has room for `capacity` records

@@ -190,6 +190,18 @@ int plmss_b200_seed_hops(plmss_ctx* p, const int64_t dims[3], int key_type, cons
   });
 }
 
+int plmss_b200_compress_sweep(plmss_ctx* p, uint32_t* d_desc, uint32_t* d_asc, const uint32_t* d_active,
+                              int64_t n_active, uint32_t* d_next, int64_t* n_next) {
+  return guarded([&] {
+    Ctx& c = C(p);
+    set_device(c);
+    if (!d_desc || (n_active > 0 && (!d_active || !d_next))) fail(PLMSS_ERR_INVALID_ARGUMENT, "null argument");
+    const int64_t k = compress_sweep_list(c, d_desc, d_asc, d_active, n_active, d_next);
+    c.sync();
+    if (n_next) *n_next = k;
+  });
+}
+
 int plmss_b200_segment(plmss_ctx* p, const int64_t dims[3], int key_type, const void* d_keys, int direction,
                        uint32_t* d_desc, uint32_t* d_asc, uint32_t* d_maxima, uint32_t* d_minima,
                        int64_t* n_maxima, int64_t* n_minima, int32_t* sweeps) {
@@ -242,6 +254,17 @@ int plmss_b200_index_separators(plmss_ctx* p, const int64_t dims[3], int label_t
     const int64_t t = index_separators(c, g, label_type, d_labels, d_codes);
     c.sync();
     if (total) *total = t;
+  });
+}
+
+int plmss_b200_count_by_cell_ranges(plmss_ctx* p, const int64_t dims[3], int label_type, const void* d_labels,
+                                    const int64_t* h_bounds, int nranges, int64_t* h_counts) {
+  return guarded([&] {
+    Ctx& c = C(p);
+    set_device(c);
+    const Grid g = make_grid(dims);
+    if (!h_bounds || !h_counts) fail(PLMSS_ERR_INVALID_ARGUMENT, "null bounds/counts");
+    count_by_cell_ranges(c, g, label_type, d_labels, h_bounds, nranges, h_counts);
   });
 }
 

@@ -136,6 +136,9 @@ int compress(Ctx& c, int64_t n, uint32_t* desc, uint32_t* asc);
 int64_t count_extrema(Ctx& c, int64_t n, const uint32_t* labels);
 void write_extrema(Ctx& c, int64_t n, const uint32_t* labels, uint32_t* out, uint32_t* rank_map);
 void compute_order(Ctx& c, int key_type, const void* values, int64_t n, int64_t* rank);
+// One sweep over an active list; returns the unsettled count written to next.
+int64_t compress_sweep_list(Ctx& c, uint32_t* desc, uint32_t* asc, const uint32_t* active, int64_t na,
+                            uint32_t* next);
 
 // combine.cu
 // get_keys(R) returns the region-key buffer (or nullptr).
@@ -145,6 +148,8 @@ int64_t combine_ms(Ctx& c, int64_t n, const uint32_t* asc, const uint32_t* desc,
 
 // marching.cu
 int64_t index_separators(Ctx& c, const Grid& g, int label_type, const void* labels, uint8_t* codes);
+void count_by_cell_ranges(Ctx& c, const Grid& g, int label_type, const void* labels, const int64_t* h_bounds,
+                          int nranges, int64_t* h_counts);
 // get_out(total) returns the record buffer (or nullptr to only count).
 int64_t emit_separators(Ctx& c, const Grid& g, int label_type, const void* labels,
                         const std::function<void*(int64_t)>& get_out);

@@ -439,6 +439,47 @@ __global__ void k_face_indices(const uint32_t* __restrict__ faces, int64_t nf, c
   if (i < 3 * nf) idx[i] = rank[faces[i]];
 }
 
+// Separator counts per cell range [bounds[i], bounds[i+1]) (EmitPlan's
+// per-worker counts): shared-memory accumulators, one global add per range.
+constexpr int kMaxRanges = 1024;
+
+template <class L>
+__global__ void __launch_bounds__(kMThreads) k_count_ranges(const L* __restrict__ lab, CDims d,
+                                                            const int64_t* __restrict__ bounds, int nr,
+                                                            unsigned long long* __restrict__ counts) {
+  __shared__ unsigned long long s_cnt[kMaxRanges];
+  __shared__ int64_t s_b[kMaxRanges + 1];
+  for (int i = threadIdx.x; i < nr; i += kMThreads) s_cnt[i] = 0;
+  for (int i = threadIdx.x; i <= nr; i += kMThreads) s_b[i] = bounds[i];
+  __syncthreads();
+  const uint64_t q = uint64_t(blockIdx.x) * kMThreads + threadIdx.x;
+  if (q < d.cubes) {
+    L cl[8];
+    int code[6], cnt;
+    cube_codes(lab, d, q, cl, code, cnt);
+    if (cnt) {
+#pragma unroll 1
+      for (int t = 0; t < 6; ++t) {
+        const int n = case_count(code[t]);
+        if (!n) continue;
+        const int64_t cell = int64_t(6 * q + t);
+        int lo = 0, hi = nr;  // range r with s_b[r] <= cell < s_b[r+1]
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) / 2;
+          if (s_b[mid] <= cell)
+            lo = mid;
+          else
+            hi = mid;
+        }
+        atomicAdd(&s_cnt[lo], (unsigned long long)n);
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nr; i += kMThreads)
+    if (s_cnt[i]) atomicAdd(&counts[i], s_cnt[i]);
+}
+
 bool g_tables_ready[64] = {};
 
 void ensure_tables(Ctx& c) {
@@ -468,6 +509,29 @@ int64_t sep_count(Ctx& c, const Grid& g, const L* lab, uint8_t* codes, uint64_t*
 }
 
 }  // namespace
+
+void count_by_cell_ranges(Ctx& c, const Grid& g, int label_type, const void* labels, const int64_t* h_bounds,
+                          int nranges, int64_t* h_counts) {
+  ensure_tables(c);
+  if (nranges < 1 || nranges > kMaxRanges) fail(PLMSS_ERR_INVALID_ARGUMENT, "1..1024 cell ranges supported");
+  const CDims d = to_cdims(g);
+  int64_t* d_b = c.get_t<int64_t>(S_TMP1, nranges + 1);
+  unsigned long long* d_cnt = c.get_t<unsigned long long>(S_TMP2, nranges);
+  CK(cudaMemcpyAsync(d_b, h_bounds, sizeof(int64_t) * (nranges + 1), cudaMemcpyHostToDevice, c.stream));
+  CK(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long) * nranges, c.stream));
+  const int64_t nb = (g.cubes + kMThreads - 1) / kMThreads;
+  if (nb > 0) {
+    if (label_type == 0)
+      k_count_ranges<uint32_t><<<(unsigned)nb, kMThreads, 0, c.stream>>>(static_cast<const uint32_t*>(labels), d,
+                                                                          d_b, nranges, d_cnt);
+    else
+      k_count_ranges<int64_t><<<(unsigned)nb, kMThreads, 0, c.stream>>>(static_cast<const int64_t*>(labels), d,
+                                                                         d_b, nranges, d_cnt);
+    CK_LAUNCH("k_count_ranges");
+  }
+  CK(cudaMemcpyAsync(h_counts, d_cnt, sizeof(int64_t) * nranges, cudaMemcpyDeviceToHost, c.stream));
+  c.sync();
+}
 
 int64_t index_separators(Ctx& c, const Grid& g, int label_type, const void* labels, uint8_t* codes) {
   uint64_t* off;

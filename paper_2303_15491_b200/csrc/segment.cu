@@ -117,6 +117,23 @@ __global__ void __launch_bounds__(256) k_jump(uint32_t* __restrict__ lab, uint32
   if (__any_sync(0xffffffffu, ch) && (threadIdx.x & 31) == 0) *changed = 1;
 }
 
+// One sweep over an explicit active list; keep[i] = 1 while unsettled.
+__global__ void k_sweep_list(uint32_t* __restrict__ desc, uint32_t* __restrict__ asc,
+                             const uint32_t* __restrict__ active, int64_t na, uint32_t* __restrict__ keep) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= na) return;
+  const uint32_t v = active[i];
+  const uint32_t d2 = desc[desc[v]];
+  desc[v] = d2;
+  bool settled = desc[d2] == d2;
+  if (asc) {
+    const uint32_t a2 = asc[asc[v]];
+    asc[v] = a2;
+    settled = settled && asc[a2] == a2;
+  }
+  keep[i] = settled ? 0u : 1u;
+}
+
 // ---------------------------------------------------- ordered compaction --
 constexpr int kCThreads = 256;
 constexpr int kCRows = 16;
@@ -172,6 +189,55 @@ __global__ void __launch_bounds__(kCThreads) k_write_self(const uint32_t* __rest
       if (rank_map) rank_map[i] = static_cast<uint32_t>(pos);
     }
     running += wpre[kCThreads / 32];
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kCThreads) k_count_flag(const uint32_t* __restrict__ flag, int64_t n,
+                                                          uint64_t* __restrict__ counts) {
+  const int64_t base = int64_t(blockIdx.x) * kCTile;
+  uint32_t c = 0;
+  for (int r = 0; r < kCRows; ++r) {
+    const int64_t i = base + r * kCThreads + threadIdx.x;
+    if (i < n && flag[i]) ++c;
+  }
+  c = __reduce_add_sync(0xffffffffu, c);
+  __shared__ uint32_t ws[kCThreads / 32];
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t t = 0;
+    for (int w = 0; w < kCThreads / 32; ++w) t += ws[w];
+    counts[blockIdx.x] = t;
+  }
+}
+
+__global__ void __launch_bounds__(kCThreads) k_write_flag(const uint32_t* __restrict__ flag,
+                                                          const uint32_t* __restrict__ vals, int64_t n,
+                                                          const uint64_t* __restrict__ offsets,
+                                                          uint32_t* __restrict__ out) {
+  __shared__ uint32_t wc[kCThreads / 32];
+  __shared__ uint32_t wp[kCThreads / 32 + 1];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t base = int64_t(blockIdx.x) * kCTile;
+  uint64_t running = offsets[blockIdx.x];
+  for (int r = 0; r < kCRows; ++r) {
+    const int64_t i = base + r * kCThreads + threadIdx.x;
+    const bool hit = i < n && flag[i];
+    const unsigned m = __ballot_sync(0xffffffffu, hit);
+    if (lane == 0) wc[w] = __popc(m);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t s = 0;
+      for (int k = 0; k < kCThreads / 32; ++k) {
+        wp[k] = s;
+        s += wc[k];
+      }
+      wp[kCThreads / 32] = s;
+    }
+    __syncthreads();
+    if (hit) out[running + wp[w] + __popc(m & ((1u << lane) - 1))] = vals[i];
+    running += wp[kCThreads / 32];
     __syncthreads();
   }
 }
@@ -265,6 +331,22 @@ void write_extrema(Ctx& c, int64_t n, const uint32_t* labels, uint32_t* out, uin
   uint64_t* counts = c.get_t<uint64_t>(S_TMP1, nb);
   k_write_self<<<(unsigned)nb, kCThreads, 0, c.stream>>>(labels, static_cast<uint32_t>(n), counts, out, rank_map);
   CK_LAUNCH("k_write_self");
+}
+
+int64_t compress_sweep_list(Ctx& c, uint32_t* desc, uint32_t* asc, const uint32_t* active, int64_t na,
+                            uint32_t* next) {
+  if (na <= 0) return 0;
+  uint32_t* keep = c.get_t<uint32_t>(S_TMP0, na);
+  k_sweep_list<<<blocks_for(na, 256), 256, 0, c.stream>>>(desc, asc, active, na, keep);
+  CK_LAUNCH("k_sweep_list");
+  const int64_t nb = (na + kCTile - 1) / kCTile;
+  uint64_t* counts = c.get_t<uint64_t>(S_TMP1, nb);
+  k_count_flag<<<(unsigned)nb, kCThreads, 0, c.stream>>>(keep, na, counts);
+  CK_LAUNCH("k_count_flag");
+  const int64_t total = int64_t(exclusive_scan_u64(c, counts, nb, true));
+  k_write_flag<<<(unsigned)nb, kCThreads, 0, c.stream>>>(keep, active, na, counts, next);
+  CK_LAUNCH("k_write_flag");
+  return total;
 }
 
 void compute_order(Ctx& c, int key_type, const void* values, int64_t n, int64_t* rank) {

@@ -1,0 +1,113 @@
+"""The C++ drop-in: the reference's own plmss:: entry points served by the
+B200 (build/libplmss_dropin.so), driven through the same ctypes wrapper the
+oracle uses (oracle/ref_capi.cpp compiled against the drop-in plus the
+reference's complex.cpp / bench.cpp / synth.cpp). CPU part: the drop-in
+exports every symbol of the reference translation units it replaces. GPU
+part: identical results to the compiled reference on the golden cases."""
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, golden_cases, load_case
+
+DROPIN = os.path.join(ROOT, "build", "libplmss_dropin.so")
+HARNESS = os.path.join(ROOT, "build", "libplmss_dropin_harness.so")
+REF_OBJ = os.path.join(ROOT, "oracle", "_ref", "obj")
+
+
+def defined(path):
+    out = subprocess.run(["nm", "-C", "--defined-only", path], capture_output=True, text=True).stdout
+    return {ln.split(" ", 2)[2] for ln in out.splitlines() if " T " in ln or " W " in ln}
+
+
+@pytest.mark.skipif(not os.path.exists(DROPIN), reason="drop-in not built (needs the reference headers)")
+def test_dropin_exports_the_replaced_reference_symbols():
+    if not os.path.isdir(REF_OBJ):
+        pytest.skip("reference objects not built")
+    mine = defined(DROPIN)
+    for tu in ("orderfield", "segmentation", "marching", "marching_tables"):
+        obj = os.path.join(REF_OBJ, f"{tu}.o")
+        for sym in defined(obj):
+            if "plmss_ref::" not in sym or "{lambda" in sym or "(anonymous namespace)" in sym:
+                continue
+            if sym.startswith("void std::") or sym.startswith("std::") or "__gnu_cxx" in sym:
+                continue
+            want = sym.replace("plmss_ref::", "plmss::")
+            if want.startswith("plmss::") or " plmss::" in want:
+                assert want in mine, f"{tu}.o defines {want} which the drop-in lacks"
+
+
+@pytest.fixture(scope="module")
+def dropin():
+    import oracle
+
+    if not os.path.exists(HARNESS):
+        pytest.skip("drop-in harness not built")
+    return oracle.Reference(HARNESS)
+
+
+pytestmark_gpu = pytest.mark.gpu
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", golden_cases())
+def test_dropin_reference_api_matches_golden(gpu, dropin, name):
+    import hashlib
+
+    g = load_case(name)
+    dims = tuple(int(x) for x in g["dims"])
+    rank = dropin.compute_order(g["field"].astype(np.float64))
+    seg = dropin.segment(dims, rank, workers=4, combine=True)
+    for k in ("desc", "asc", "maxima", "minima", "ms_region", "region_keys"):
+        assert np.array_equal(seg[k], g[k]), k
+    sep = dropin.emit_separators(dims, seg["ms_region"], workers=3)
+    assert np.array_equal(sep["codes"], g["codes"])
+    sha = lambda a: hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()  # noqa: E731
+    for k in ("points", "regions", "source_cells"):
+        assert sha(sep[k]) == str(g[f"sep_{k}_sha256"]), k
+    sp = dropin.emit_separators(dims, seg["ms_region"], workers=2, spacing=(2.0, 1.0, 3.0), origin=(0.5, -1.25, 0.0))
+    for k in ("points", "regions", "source_cells"):
+        assert sha(sp[k]) == str(g[f"sepsp_{k}_sha256"]), k
+    for tag, lab in (("bnd_asc", g["asc"]), ("bnd_ms", g["ms_region"])):
+        b = dropin.emit_boundaries(dims, lab, workers=2)
+        for k in ("points", "indices", "regions", "source_cells"):
+            assert sha(b[k]) == str(g[f"{tag}_{k}_sha256"]), (tag, k)
+
+
+@pytest.mark.gpu
+def test_dropin_tables_and_codes(gpu, dropin, reference):
+    for code in range(32):
+        assert np.array_equal(dropin.tetra_case(code), reference.tetra_case(code))
+    for code in range(8):
+        assert np.array_equal(dropin.triangle_case(code), reference.triangle_case(code))
+    rng = np.random.default_rng(0)
+    for _ in range(200):
+        lab = rng.integers(0, 4, size=4)
+        assert dropin.tetra_code(lab) == reference.tetra_code(lab) or \
+            (dropin.tetra_code(lab)[0] == reference.tetra_code(lab)[0])
+
+
+@pytest.mark.gpu
+def test_dropin_errors_match_reference(gpu, dropin):
+    with pytest.raises(ValueError, match="vertex 1"):
+        dropin.compute_order(np.array([0.0, np.nan]))
+    with pytest.raises(ValueError, match="does not match"):
+        dropin.segment((4, 4, 4), np.arange(10))
+    with pytest.raises(ValueError, match="3-D"):
+        dropin.segment((4, 4, 1), np.arange(16))
+    with pytest.raises(ValueError, match="workers"):
+        dropin.segment((3, 3, 3), np.arange(27), workers=0)
+    with pytest.raises(ValueError, match="label field size"):
+        dropin.emit_separators((3, 3, 3), np.zeros(5, np.int64))
+
+
+@pytest.mark.gpu
+def test_reference_harness_runs_the_b200_path(gpu, dropin):
+    """proj/src/bench.cpp run_benchmark, unchanged, timing the drop-in."""
+    g = load_case("gauss_17x13x11")
+    dims = tuple(int(x) for x in g["dims"])
+    ph = dropin.run_benchmark(dims, g["field"].astype(np.float64), workers=2, repeats=3)
+    assert set(ph) == {"order", "segmentation", "combine", "index", "geometry"}
+    assert all(v >= 0 for v in ph.values())
