@@ -117,6 +117,15 @@ int plmss_b200_segment(plmss_ctx* ctx, const int64_t dims[3], int key_type, cons
                        int direction, uint32_t* d_desc, uint32_t* d_asc, uint32_t* d_maxima,
                        uint32_t* d_minima, int64_t* n_maxima, int64_t* n_minima, int32_t* sweeps);
 
+/* Slab segmentation for the z-slab multi-GPU decomposition: the grid is one
+ * rank's slab extended by its halo layers; when halo_lo (halo_hi) is set the
+ * first (last) z layer is a copy of the neighbour rank's boundary layer and
+ * its vertices are made terminals (hop = self), so after compression every
+ * owned vertex points at a root of its own slab or at a halo vertex whose
+ * label the neighbour resolves (paper_2303_15491_b200/distributed.py). */
+int plmss_b200_segment_slab(plmss_ctx* ctx, const int64_t dims[3], int key_type, const void* d_keys,
+                            int halo_lo, int halo_hi, uint32_t* d_desc, uint32_t* d_asc, int32_t* sweeps);
+
 /* Step 1 only (detail::seed_hops_both, segmentation.cpp:60-85): hop targets. */
 int plmss_b200_seed_hops(plmss_ctx* ctx, const int64_t dims[3], int key_type, const void* d_keys,
                          uint32_t* d_desc, uint32_t* d_asc);

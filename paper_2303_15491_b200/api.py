@@ -35,7 +35,7 @@ HEADER_FUNCTIONS = [
     "plmss_b200_materialize_separators", "plmss_b200_emit_boundaries", "plmss_b200_pipeline",
     "plmss_b200_result", "plmss_b200_copy", "plmss_b200_ctx_set_option", "plmss_b200_pipeline_host",
     "plmss_b200_synth", "plmss_b200_launch_count", "plmss_b200_ctx_stats", "plmss_b200_count_by_cell_ranges",
-    "plmss_b200_compress_sweep",
+    "plmss_b200_compress_sweep", "plmss_b200_segment_slab",
 ]
 
 
@@ -76,6 +76,8 @@ def lib() -> C.CDLL:
         L.plmss_b200_combine_ms.argtypes = [vp, i64, vp, vp, vp, vp, vp]
         L.plmss_b200_index_separators.argtypes = [vp, vp, i32, vp, vp, vp]
         L.plmss_b200_count_by_cell_ranges.argtypes = [vp, vp, i32, vp, vp, i32, vp]
+        L.plmss_b200_segment_slab.argtypes = [vp, vp, i32, vp, i32, i32, vp, vp, vp]
+        L.plmss_b200_compress_sweep.argtypes = [vp, vp, vp, vp, i64, vp, vp]
         L.plmss_b200_emit_separators.argtypes = [vp, vp, i32, vp, vp, i64, vp]
         L.plmss_b200_materialize_separators.argtypes = [vp, vp, vp, vp, i32, vp, i64, vp, vp, vp]
         L.plmss_b200_emit_boundaries.argtypes = [vp, vp, vp, vp, i32, vp, i32, i64, vp, vp, vp, vp, vp, vp, vp]

@@ -190,6 +190,29 @@ int plmss_b200_seed_hops(plmss_ctx* p, const int64_t dims[3], int key_type, cons
   });
 }
 
+int plmss_b200_segment_slab(plmss_ctx* p, const int64_t dims[3], int key_type, const void* d_keys, int halo_lo,
+                            int halo_hi, uint32_t* d_desc, uint32_t* d_asc, int32_t* sweeps) {
+  return guarded([&] {
+    Ctx& c = C(p);
+    set_device(c);
+    const Grid g = make_grid(dims);
+    if (!d_desc || !d_asc) fail(PLMSS_ERR_INVALID_ARGUMENT, "d_desc and d_asc required");
+    uint32_t* bad = static_cast<uint32_t*>(c.get(S_FLAGS, 64)) + 8;
+    if (key_type != PLMSS_KEY_RANK) CK(cudaMemsetAsync(bad, 0xff, sizeof(uint32_t), c.stream));
+    seed_hops(c, g, key_type, d_keys, d_desc, d_asc, key_type != PLMSS_KEY_RANK ? bad : nullptr);
+    terminal_layers(c, g, halo_lo != 0, halo_hi != 0, d_desc, d_asc);
+    const int s = compress(c, g.n, d_desc, d_asc);
+    if (key_type != PLMSS_KEY_RANK) {
+      CK(cudaMemcpyAsync(c.h_pinned + 2, bad, sizeof(uint32_t), cudaMemcpyDeviceToHost, c.stream));
+      c.sync();
+      const uint32_t b = *reinterpret_cast<uint32_t*>(c.h_pinned + 2);
+      if (b != 0xffffffffu) fail(PLMSS_ERR_INVALID_ARGUMENT, "non-finite scalar value at vertex " + std::to_string(b));
+    }
+    c.sync();
+    if (sweeps) *sweeps = s;
+  });
+}
+
 int plmss_b200_compress_sweep(plmss_ctx* p, uint32_t* d_desc, uint32_t* d_asc, const uint32_t* d_active,
                               int64_t n_active, uint32_t* d_next, int64_t* n_next) {
   return guarded([&] {

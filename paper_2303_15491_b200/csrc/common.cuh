@@ -131,6 +131,7 @@ inline unsigned blocks_for(int64_t n, int threads, int64_t cap = int64_t(1) << 3
 void seed_hops(Ctx& c, const Grid& g, int key_type, const void* keys, uint32_t* desc, uint32_t* asc,
                uint32_t* bad_vertex /*device, may be null*/);
 int compress(Ctx& c, int64_t n, uint32_t* desc, uint32_t* asc);
+void terminal_layers(Ctx& c, const Grid& g, bool lo, bool hi, uint32_t* desc, uint32_t* asc);
 // Ordered compaction of self-pointing vertices: count (keeps block offsets
 // in S_TMP1), then write the list and/or the extremum -> rank map.
 int64_t count_extrema(Ctx& c, int64_t n, const uint32_t* labels);

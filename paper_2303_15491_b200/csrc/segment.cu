@@ -299,6 +299,27 @@ void seed_hops(Ctx& c, const Grid& g, int key_type, const void* keys, uint32_t* 
   CK_LAUNCH("k_seed_hops");
 }
 
+// Slab halo layers become terminals: label = self.
+__global__ void k_terminal_layer(uint32_t* __restrict__ desc, uint32_t* __restrict__ asc, uint32_t first,
+                                 uint32_t count) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  desc[first + i] = first + i;
+  asc[first + i] = first + i;
+}
+
+void terminal_layers(Ctx& c, const Grid& g, bool lo, bool hi, uint32_t* desc, uint32_t* asc) {
+  const uint32_t XY = uint32_t(g.X * g.Y);
+  if (lo) {
+    k_terminal_layer<<<blocks_for(XY, 256), 256, 0, c.stream>>>(desc, asc, 0u, XY);
+    CK_LAUNCH("k_terminal_layer");
+  }
+  if (hi) {
+    k_terminal_layer<<<blocks_for(XY, 256), 256, 0, c.stream>>>(desc, asc, uint32_t(g.n) - XY, XY);
+    CK_LAUNCH("k_terminal_layer");
+  }
+}
+
 int compress(Ctx& c, int64_t n, uint32_t* desc, uint32_t* asc) {
   int* flag = static_cast<int*>(c.get(S_FLAGS, 64));
   int sweeps = 0;

@@ -48,9 +48,6 @@ def dropin():
     return oracle.Reference(HARNESS)
 
 
-pytestmark_gpu = pytest.mark.gpu
-
-
 @pytest.mark.gpu
 @pytest.mark.parametrize("name", golden_cases())
 def test_dropin_reference_api_matches_golden(gpu, dropin, name):
@@ -85,8 +82,9 @@ def test_dropin_tables_and_codes(gpu, dropin, reference):
     rng = np.random.default_rng(0)
     for _ in range(200):
         lab = rng.integers(0, 4, size=4)
-        assert dropin.tetra_code(lab) == reference.tetra_code(lab) or \
-            (dropin.tetra_code(lab)[0] == reference.tetra_code(lab)[0])
+        (c1, l1), (c2, l2) = dropin.tetra_code(lab), reference.tetra_code(lab)
+        assert c1 == c2 and np.array_equal(l1, l2)
+        assert dropin.triangle_code(lab[:3]) == reference.triangle_code(lab[:3])
 
 
 @pytest.mark.gpu

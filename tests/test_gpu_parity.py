@@ -206,6 +206,30 @@ def test_boundaries_region_filter(plmss, gpu, restatement):
             assert np.array_equal(b[k].cpu().numpy(), rb[k]), (flt, k)
 
 
+# ------------------------------------------------ z-slab device backend --
+@pytest.mark.parametrize("lo,hi", [(False, False), (True, False), (False, True), (True, True)])
+def test_slab_backend_matches_oracle_backend(plmss, gpu, lo, hi):
+    """The per-slab device work of the multi-GPU path (halo layers as
+    terminals, int64-label marching) against the CPU test backend."""
+    import torch
+
+    from paper_2303_15491_b200.distributed import B200Backend
+    from test_distributed import OracleBackend
+
+    rng = np.random.default_rng(5)
+    dims = (11, 9, 7)
+    f = rng.integers(0, 4, int(np.prod(dims))).astype(np.float32)
+    gb, cb = B200Backend(gpu), OracleBackend()
+    d1, a1 = gb.segment_slab(dims, torch.from_numpy(f).cuda(), lo, hi)
+    d2, a2 = cb.segment_slab(dims, torch.from_numpy(f), lo, hi)
+    assert np.array_equal(d1.cpu().numpy(), d2.numpy()) and np.array_equal(a1.cpu().numpy(), a2.numpy())
+    ms = torch.from_numpy(rng.integers(0, 5, int(np.prod(dims))).astype(np.int64) * 7 + 3)
+    c1, l1, h1 = gb.march_slab(dims, ms.cuda())
+    c2, l2, h2 = cb.march_slab(dims, ms)
+    for x, y in ((c1, c2), (l1, l2), (h1, h2)):
+        assert np.array_equal(x.cpu().numpy(), y.numpy())
+
+
 # ---------------------------------------------------------- order field --
 def test_compute_order(plmss, gpu, restatement):
     rng = np.random.default_rng(11)
