@@ -151,7 +151,7 @@ def run_reference_arm(args, rank, world):
               f"(compute_order+segment+combine_ms+index+geometry, MorseSmale) per step")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64/int64", "data": "synthetic",
         "config": {"workload": cfg.name, "dims": list(cfg.dims), "sample_dims": list(dims)},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference", "sample": sample},
@@ -434,7 +434,7 @@ def main():
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
         "data": "synthetic",
         "config": {"workload": cfg.name, "dims": list(dims), "input": "float32 field resident in HBM",
                    "l2": "inputs larger than L2 (4 GiB field vs 126 MB L2)",

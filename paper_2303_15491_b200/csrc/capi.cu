@@ -427,10 +427,6 @@ int plmss_b200_ctx_set_option(plmss_ctx* p, int option, int64_t value) {
       c.combine_path = int(value);
       return;
     }
-    if (option == 99) {
-      c.dbg = int(value);
-      return;
-    }
     if (option == PLMSS_OPT_TMA) {
       c.use_tma = value != 0;
       return;

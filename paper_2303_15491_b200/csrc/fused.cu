@@ -36,16 +36,24 @@ namespace plmss_b200 {
 namespace {
 
 constexpr int TX = 32, TY = 32, TZ = 32;
-// Halo brick in shared memory: x from gx0-4 (the TMA start coordinate in x
+// Field box in shared memory: x from gx0-4 (the TMA start coordinate in x
 // must be 16-byte aligned on this platform, tools/tma_probe2.cu) to gx0+35,
 // y and z from g0-1 to g0+32.
 constexpr int HX = TX + 8, HY = TY + 2, HZ = TZ + 2;
-constexpr int HXO = 4;            // x offset of the brick inside the halo box
-constexpr int HN = HX * HY * HZ;  // 46240
-constexpr int TN = TX * TY * TZ;  // 32768
+constexpr int HXO = 4;            // x offset of the brick inside the field box
+constexpr int HXY = HX * HY;
+constexpr int HN = HXY * HZ;      // 46240 floats
+// Pointer / hop-code index space: the brick plus a one-cell shell, 34^3
+// cells (< 2^16, so pointers are u16). Shell cells are terminals: a chain
+// that reaches one has left the brick, and the shell cell is the hop target.
+constexpr int PX = TX + 2, PXY = PX * (TY + 2), PN = PXY * (TZ + 2);  // 34, 1156, 39304
+constexpr int TN = TX * TY * TZ;
 constexpr int A_THREADS = 1024;
-constexpr int kASmem = 4 * HN + TN + 1024;  // f (later the two u16 pointer arrays), hop codes, alignment slack
-static_assert(2 * 2 * TN <= 4 * HN, "pointer arrays must fit in the f region");
+constexpr int kCodeOff = 4 * HN;                // hop codes after the field box
+constexpr int kASmem = 4 * HN + PN + 1024;      // + TMA alignment slack
+static_assert(2 * 2 * PN <= 4 * HN, "pointer arrays must fit in the field box");
+static_assert(kCodeOff % 16 == 0, "code array alignment");
+constexpr uint8_t kExitMark = 0xfe;  // shell cell reached by some brick vertex
 constexpr uint64_t kEmpty = ~uint64_t(0);
 
 struct FDims {
@@ -89,13 +97,13 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-// Stencil offset s as 2-bit-per-axis code (x low), selected without local
-// memory: a 14-entry x 6-bit table packed into two 64-bit immediates.
-__device__ __forceinline__ uint32_t kOffTable(int s) {
-  constexpr uint64_t lo = 0x00ull | 0x01ull << 6 | 0x04ull << 12 | 0x05ull << 18 | 0x10ull << 24 | 0x11ull << 30 |
-                          0x14ull << 36 | 0x16ull << 42 | 0x19ull << 48 | 0x1aull << 54;
-  constexpr uint64_t hi = 0x25ull | 0x26ull << 6 | 0x29ull << 12 | 0x2aull << 18;
-  return s < 10 ? uint32_t((lo >> (6 * s)) & 63) : uint32_t((hi >> (6 * (s - 10))) & 63);
+// Stencil s = 0..13 in ascending id-delta order (complex.cpp:78-88) as
+// 2-bit-per-axis codes (dx+1 | (dy+1) << 2 | (dz+1) << 4); the vertex itself
+// sits between s = 6 and s = 7.
+__host__ __device__ constexpr uint32_t stencil_code(int s) {
+  return s == 0 ? 0x00 : s == 1 ? 0x01 : s == 2 ? 0x04 : s == 3 ? 0x05 : s == 4 ? 0x10 : s == 5 ? 0x11
+       : s == 6 ? 0x14 : s == 7 ? 0x16 : s == 8 ? 0x19 : s == 9 ? 0x1a : s == 10 ? 0x25 : s == 11 ? 0x26
+       : s == 12 ? 0x29 : 0x2a;
 }
 
 struct ACounters {
@@ -106,15 +114,25 @@ struct ACounters {
 
 // ---------------------------------------------------------------- pass A --
 // One CTA (1024 threads, one per (x, y) column of 32 vertices) per 32^3
-// brick. The halo'd brick of f (36 x 34 x 34, x padded to a 16-byte multiple)
-// arrives by one TMA tensor copy whose out-of-volume elements are NaN
-// (fmaxf/fminf ignore NaN and NaN == x is false, so a missing neighbour is
-// never selected). Phase 1 stores each vertex's steepest up/down stencil code
-// (4 bits each) — f is then dead and its shared memory becomes the two u16
-// pointer arrays of phase 2, where a vertex points at its in-brick hop target
-// or at itself when it is a root or its hop leaves the brick. Pointer jumping
-// to the fixpoint leaves every vertex pointing at its terminal u; the partial
-// label is u (root) or u's out-of-brick hop target (an exit vertex).
+// brick.
+//  1. The field box (40 x 34 x 34 floats) arrives by one TMA tensor copy whose
+//     out-of-volume elements are NaN: fmaxf/fminf ignore NaN and NaN == x is
+//     false, so a missing neighbour is never selected.
+//  2. Steepest hops (segmentation.cpp:60-85). Each thread walks its column in
+//     z keeping the 7 stencil columns in registers (7 shared loads per
+//     vertex). With M = max f over the neighbours, steepest-up under the
+//     (f, id) order is the highest s with f == M when M > f(v), or when
+//     M == f(v) and s > 6; otherwise none. Steepest-down mirrors it (lowest
+//     s, s < 7). Result: one byte per cell, up | down << 4 (15 = none).
+//  3. f is dead; its shared memory becomes two u16 pointer arrays over the
+//     34^3 shelled brick. Pointers start two hops ahead; shell cells point at
+//     themselves.
+//  4. Pointer jumping to the fixpoint (segmentation.cpp:87-168 restated as
+//     parallel path compression): every vertex ends at its terminal, an
+//     in-brick extremum or the shell cell where its chain leaves the brick.
+//     The global id of that terminal is the vertex's partial label.
+//  5. Extrema and the distinct exit (shell) cells are appended to global
+//     lists, aggregated per brick.
 template <bool kTMA>
 __global__ void __launch_bounds__(A_THREADS, 1)
     k_tile_segment(const __grid_constant__ CUtensorMap tmap, const float* __restrict__ field, FDims d,
@@ -123,29 +141,33 @@ __global__ void __launch_bounds__(A_THREADS, 1)
                    uint64_t exit_cap, ACounters* __restrict__ ctr) {
   extern __shared__ __align__(16) unsigned char a_smem_raw[];
   // TMA destinations must be 128-byte aligned: round the window up (the
-  // launch reserves kASmemAlign extra bytes for this).
+  // launch reserves 1024 extra bytes for this).
   unsigned char* a_smem = a_smem_raw + ((1024u - (smem_u32(a_smem_raw) & 1023u)) & 1023u);
-  float* f = reinterpret_cast<float*>(a_smem);          // HN floats (phase 1)
-  uint16_t* Pd = reinterpret_cast<uint16_t*>(a_smem);   // TN (phase 2+, aliases f)
-  uint16_t* Pa = Pd + TN;                               // TN
-  uint8_t* hop = a_smem + 4 * HN;                       // TN: up | down << 4 (15 = self)
+  float* f = reinterpret_cast<float*>(a_smem);         // HN floats (steps 1-2)
+  uint16_t* Pd = reinterpret_cast<uint16_t*>(a_smem);  // PN (steps 3+, aliases f)
+  uint16_t* Pa = Pd + PN;                              // PN
+  uint8_t* code = a_smem + kCodeOff;                   // PN
   __shared__ __align__(8) uint64_t s_bar;
+  __shared__ int s_delta[16];
+  __shared__ uint32_t s_wcnt[A_THREADS / 32][3];
+  __shared__ unsigned long long s_lbase[3];
 
   const uint32_t bt = blockIdx.x;
   const uint32_t tx = bt % d.tx, ty = (bt / d.tx) % d.ty, tz = bt / (d.tx * d.ty);
   const int gx0 = int(tx * TX), gy0 = int(ty * TY), gz0 = int(tz * TZ);
-  const int lane = threadIdx.x & 31;
-  const int lx = threadIdx.x & 31, ly = threadIdx.x >> 5;
+  const int tid = int(threadIdx.x);
+  const int lane = tid & 31;
+  const int lx = tid & 31, ly = tid >> 5;
 
-  // 1. halo'd brick of f
+  // 1. field box
   if (kTMA) {
     const uint32_t bar = smem_u32(&s_bar);
-    if (threadIdx.x == 0) {
+    if (tid == 0) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (tid == 0) {
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(uint32_t(HN * 4))
                    : "memory");
       asm volatile(
@@ -154,17 +176,13 @@ __global__ void __launch_bounds__(A_THREADS, 1)
           "l"(&tmap), "r"(gx0 - HXO), "r"(gy0 - 1), "r"(gz0 - 1), "r"(bar)
           : "memory");
     }
-    asm volatile(
-        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n @!p bra WAIT_%=;\n}" ::"r"(
-            bar)
-        : "memory");
   } else {
     for (int i0 = 0; i0 < HN; i0 += 8 * A_THREADS) {
       float v[8];
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
-        const int i = i0 + k * A_THREADS + int(threadIdx.x);
-        const int hx = i % HX, hy = (i / HX) % HY, hz = i / (HX * HY);
+        const int i = i0 + k * A_THREADS + tid;
+        const int hx = i % HX, hy = (i / HX) % HY, hz = i / HXY;
         const int gx = gx0 + hx - HXO, gy = gy0 + hy - 1, gz = gz0 + hz - 1;
         v[k] = __int_as_float(0x7fc00000);
         if (i < HN && gx >= 0 && gx < int(d.X) && gy >= 0 && gy < int(d.Y) && gz >= 0 && gz < int(d.Z))
@@ -172,148 +190,183 @@ __global__ void __launch_bounds__(A_THREADS, 1)
       }
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
-        const int i = i0 + k * A_THREADS + int(threadIdx.x);
+        const int i = i0 + k * A_THREADS + tid;
         if (i < HN) f[i] = v[k];
       }
     }
   }
+  // while the box is in flight: no-hop codes everywhere (step 2 overwrites
+  // the in-volume brick cells) and the stencil deltas of the pointer space
+  for (int i = 4 * tid; i < PN; i += 4 * A_THREADS) *reinterpret_cast<uint32_t*>(code + i) = 0xffffffffu;
+  if (tid < 16) {
+    int dl = 0;
+    if (tid < 14) {
+      const uint32_t o = stencil_code(tid);
+      dl = (int(o & 3) - 1) + PX * (int((o >> 2) & 3) - 1) + PXY * (int((o >> 4) & 3) - 1);
+    }
+    s_delta[tid] = dl;  // code 15 (none) -> 0
+  }
+  if (kTMA)
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n @!p bra WAIT_%=;\n}" ::"r"(
+            smem_u32(&s_bar))
+        : "memory");
   __syncthreads();
 
-  // 2. steepest hops. Stencil s = 0..13 in ascending id-delta order
-  //    (complex.cpp:78-88); the vertex itself sits between s = 6 and s = 7.
-  //    With M = max f over the neighbours, steepest-up under (f, id) order is
-  //    the highest s with f == M when M > f(v), or when M == f(v) and s > 6;
-  //    otherwise v. Steepest-down mirrors it (lowest s, s < 7).
-  constexpr uint32_t kOff[14] = {0x00, 0x01, 0x04, 0x05, 0x10, 0x11, 0x14,
-                                 0x16, 0x19, 0x1a, 0x25, 0x26, 0x29, 0x2a};
+  // 2. steepest hops
   const int gx = gx0 + lx, gy = gy0 + ly;
   const bool col_ok = gx < int(d.X) && gy < int(d.Y);
-#pragma unroll 1
-  for (int lz = 0; lz < TZ; ++lz) {
-    const int l = lx + TX * ly + TX * TY * lz;
-    const int gz = gz0 + lz;
-    if (!col_ok || gz >= int(d.Z)) {
-      hop[l] = 0xff;
-      continue;
+  const int nz = min(TZ, int(d.Z) - gz0);  // in-volume layers of the brick
+  const int hc = (lx + 1) + PX * (ly + 1);  // column in the pointer space (shell layer z = 0)
+  const uint32_t gv0 = uint32_t(gx) + d.X * uint32_t(gy) + d.XY * uint32_t(gz0);
+  if (col_ok) {
+    // stencil columns (dx, dy): c0 (-1,-1) c1 (0,-1) c2 (-1,0) c3 (0,0)
+    // c4 (1,0) c5 (0,1) c6 (1,1); s -> (column, plane):
+    //   s0-3 = c0-c3 @ z-1, s4-6 = c0-c2 @ z, s7-9 = c4-c6 @ z, s10-13 = c3-c6 @ z+1
+    const float* fc = f + (ly + 1) * HX + (lx + HXO);
+    float a0m = fc[-1 - HX], a1m = fc[-HX], a2m = fc[-1], a3m = fc[0];
+    float a0 = fc[HXY - 1 - HX], a1 = fc[HXY - HX], a2 = fc[HXY - 1], a3 = fc[HXY], a4 = fc[HXY + 1],
+          a5 = fc[HXY + HX], a6 = fc[HXY + HX + 1];
+#pragma unroll 4
+    for (int lz = 0; lz < TZ; ++lz) {
+      const float* p = fc + (lz + 2) * HXY;  // plane z+1
+      const float a3p = p[0], a4p = p[1], a5p = p[HX], a6p = p[HX + 1];
+      if (lz < nz) {
+        const float fv = a3;
+        if (!isfinite(fv)) atomicMin(&ctr->bad, gv0 + d.XY * uint32_t(lz));
+        const float fn[14] = {a0m, a1m, a2m, a3m, a0, a1, a2, a4, a5, a6, a3p, a4p, a5p, a6p};
+        float M = fn[0], m = fn[0];
+#pragma unroll
+        for (int s = 1; s < 14; ++s) {
+          M = fmaxf(M, fn[s]);
+          m = fminf(m, fn[s]);
+        }
+        uint32_t eu = 0, ed = 0;
+#pragma unroll
+        for (int s = 0; s < 14; ++s) {
+          eu |= uint32_t(fn[s] == M) << s;
+          ed |= uint32_t(fn[s] == m) << s;
+        }
+        // eu == 0 only when every neighbour is missing (M is NaN): no hop
+        const uint32_t su = (M > fv || (M == fv && eu > 0x7fu)) ? uint32_t(31 - __clz(eu)) : 15u;
+        const uint32_t sd = (m < fv || (m == fv && (ed & 0x7fu) != 0)) ? uint32_t(__ffs(ed) - 1) : 15u;
+        code[hc + (lz + 1) * PXY] = uint8_t(su | (sd << 4));
+      }
+      a0m = a0;
+      a1m = a1;
+      a2m = a2;
+      a3m = a3;
+      a0 = p[-1 - HX];
+      a1 = p[-HX];
+      a2 = p[-1];
+      a3 = a3p;
+      a4 = a4p;
+      a5 = a5p;
+      a6 = a6p;
     }
-    const int h = (lz + 1) * HX * HY + (ly + 1) * HX + (lx + HXO);
-    const float fv = f[h];
-    if (!isfinite(fv)) atomicMin(&ctr->bad, uint32_t(gx) + d.X * (uint32_t(gy) + d.Y * uint32_t(gz)));
-    float fn[14];
-#pragma unroll
-    for (int s = 0; s < 14; ++s) {
-      const int dx = int(kOff[s] & 3) - 1, dy = int((kOff[s] >> 2) & 3) - 1, dz = int((kOff[s] >> 4) & 3) - 1;
-      fn[s] = f[h + dx + HX * dy + HX * HY * dz];
-    }
-    float M = fn[0], m = fn[0];
-#pragma unroll
-    for (int s = 1; s < 14; ++s) {
-      M = fmaxf(M, fn[s]);
-      m = fminf(m, fn[s]);
-    }
-    uint32_t su = 15, sd = 15;
-#pragma unroll
-    for (int s = 0; s < 14; ++s) su = fn[s] == M ? uint32_t(s) : su;  // highest s attaining M
-#pragma unroll
-    for (int s = 13; s >= 0; --s) sd = fn[s] == m ? uint32_t(s) : sd;  // lowest s attaining m
-    if (!(M > fv || (M == fv && su > 6))) su = 15;
-    if (!(m < fv || (m == fv && sd < 7))) sd = 15;
-    hop[l] = uint8_t(su | (sd << 4));
   }
   __syncthreads();
 
-  // 3. pointers (f is dead from here on)
-  auto target = [&](int l, uint32_t s) -> int {  // in-brick hop target or l itself
-    if (s == 15) return l;
-    const uint32_t o = kOffTable(int(s));
-    const int dx = int(o & 3) - 1, dy = int((o >> 2) & 3) - 1, dz = int((o >> 4) & 3) - 1;
-    const int mx = (l & 31) + dx, my = ((l >> 5) & 31) + dy, mz = (l >> 10) + dz;
-    const bool inside = mx >= 0 && mx < TX && my >= 0 && my < TY && mz >= 0 && mz < TZ;
-    return inside ? l + dx + TX * dy + TX * TY * dz : l;
-  };
-  // Per-thread masks (bit lz) of column vertices whose pointer is not yet a
-  // terminal. A vertex is done once its pointer target is a terminal
-  // (P[t] == t); only live vertices are revisited in later rounds.
+  // 3. pointers two hops ahead (f is dead from here on). Shell cells point
+  //    at themselves: the z-shell cells of this column here, the 132 shell
+  //    columns by threads 0..131.
   uint32_t live_d = 0, live_a = 0;
+  Pd[hc] = uint16_t(hc);
+  Pa[hc] = uint16_t(hc);
+  Pd[hc + (TZ + 1) * PXY] = uint16_t(hc + (TZ + 1) * PXY);
+  Pa[hc + (TZ + 1) * PXY] = uint16_t(hc + (TZ + 1) * PXY);
+  int shell_col = -1;
+  if (tid < 4 * (PX - 1)) {  // 132 shell columns: rows y = 0, y = 33, then x = 0, x = 33
+    shell_col = tid < PX ? tid : tid < 2 * PX ? (tid - PX) + PX * (PX - 1) : tid < 2 * PX + TY
+                                                  ? PX * (tid - 2 * PX + 1)
+                                                  : (PX - 1) + PX * (tid - 2 * PX - TY + 1);
+    for (int z = 0; z < TZ + 2; ++z) {
+      const int h = shell_col + z * PXY;
+      Pd[h] = uint16_t(h);
+      Pa[h] = uint16_t(h);
+    }
+  }
 #pragma unroll 4
   for (int lz = 0; lz < TZ; ++lz) {
-    const int l = lx + TX * ly + TX * TY * lz;
-    const uint32_t c = hop[l];
-    const int td = target(l, c & 15), ta = target(l, c >> 4);
-    Pd[l] = uint16_t(td);
-    Pa[l] = uint16_t(ta);
-    live_d |= uint32_t(td != l) << lz;
-    live_a |= uint32_t(ta != l) << lz;
+    const int h = hc + (lz + 1) * PXY;
+    const uint32_t c = code[h];
+    int td = h, ta = h;
+    if ((c & 15) != 15) {
+      const int t1 = h + s_delta[c & 15];
+      const uint32_t c2 = code[t1] & 15;
+      td = t1 + s_delta[c2];
+      live_d |= uint32_t(c2 != 15) << lz;
+    }
+    if ((c >> 4) != 15) {
+      const int t1 = h + s_delta[c >> 4];
+      const uint32_t c2 = code[t1] >> 4;
+      ta = t1 + s_delta[c2];
+      live_a |= uint32_t(c2 != 15) << lz;
+    }
+    Pd[h] = uint16_t(td);
+    Pa[h] = uint16_t(ta);
   }
   __syncthreads();
+
+  // 4. pointer jumping; a vertex retires once its pointer is a terminal
   for (;;) {
     uint32_t m = live_d;
     while (m) {
       const int lz = __ffs(m) - 1;
       m &= m - 1;
-      const int l = lx + TX * ly + TX * TY * lz;
-      const uint16_t p = Pd[l], q = Pd[p];
+      const int h = hc + (lz + 1) * PXY;
+      const uint16_t p = Pd[h], q = Pd[p];
       if (q == p)
         live_d &= ~(1u << lz);
       else
-        Pd[l] = q;
+        Pd[h] = q;
     }
     m = live_a;
     while (m) {
       const int lz = __ffs(m) - 1;
       m &= m - 1;
-      const int l = lx + TX * ly + TX * TY * lz;
-      const uint16_t p = Pa[l], q = Pa[p];
+      const int h = hc + (lz + 1) * PXY;
+      const uint16_t p = Pa[h], q = Pa[p];
       if (q == p)
         live_a &= ~(1u << lz);
       else
-        Pa[l] = q;
+        Pa[h] = q;
     }
     if (!__syncthreads_or((live_d | live_a) != 0)) break;
   }
 
-  // 4. partial labels, roots, exit vertices. Appends are aggregated per
-  //    brick: count, block scan, one atomic per list, then write.
-  __shared__ int s_gdelta[16];
-  __shared__ uint32_t s_wcnt[A_THREADS / 32][3];
-  __shared__ unsigned long long s_lbase[3];
-  if (threadIdx.x < 16) {
-    int g = 0;
-    if (threadIdx.x < 14) {
-      const uint32_t o = kOffTable(int(threadIdx.x));
-      g = (int(o & 3) - 1) + int(d.X) * (int((o >> 2) & 3) - 1) + int(d.XY) * (int((o >> 4) & 3) - 1);
-    }
-    s_gdelta[threadIdx.x] = g;  // code 15 (self) -> 0
-  }
-  const uint32_t base_g = uint32_t(gx0) + d.X * (uint32_t(gy0) + d.Y * uint32_t(gz0));
-  auto gid = [&](int u) -> uint32_t {
-    return base_g + uint32_t(u & 31) + d.X * (uint32_t((u >> 5) & 31) + d.Y * uint32_t(u >> 10));
+  // 5. partial labels; extrema; exit shell cells marked in the code array
+  const uint32_t gbase = uint32_t(gx0 - 1) + d.X * uint32_t(gy0 - 1) + d.XY * uint32_t(gz0 - 1);
+  auto gid = [&](uint32_t t, bool& shell) -> uint32_t {
+    const uint32_t hz = t / PXY, r = t - hz * PXY, hy = r / PX, hx = r - hy * PX;
+    shell = (hx - 1u) >= uint32_t(TX) || (hy - 1u) >= uint32_t(TY) || (hz - 1u) >= uint32_t(TZ);
+    return gbase + hx + d.X * hy + d.XY * hz;
   };
-  // terminal vertices keep P[l] == l; with a real hop that means an exit
-  uint32_t mmax = 0, mmin = 0, mxd = 0, mxa = 0;
-#pragma unroll 4
-  for (int lz = 0; lz < TZ; ++lz) {
-    const int l = lx + TX * ly + TX * TY * lz;
-    const uint32_t c = hop[l];
-    if (c == 0xff) continue;
-    const uint32_t sd = c & 15, sa = c >> 4;
-    mmax |= uint32_t(sd == 15) << lz;
-    mmin |= uint32_t(sa == 15) << lz;
-    mxd |= uint32_t(sd != 15 && Pd[l] == l) << lz;
-    mxa |= uint32_t(sa != 15 && Pa[l] == l) << lz;
-  }
-  __syncthreads();  // s_gdelta ready
-  // an exit vertex reached in both directions is listed once
-  {
-    uint32_t both = mxd & mxa, m = both;
-    while (m) {
-      const int lz = __ffs(m) - 1;
-      m &= m - 1;
-      const uint32_t c = hop[lx + TX * ly + TX * TY * lz];
-      if (s_gdelta[c & 15] == s_gdelta[c >> 4]) mxa &= ~(1u << lz);
+  uint32_t mmax = 0, mmin = 0;
+  if (col_ok) {
+#pragma unroll 2
+    for (int lz = 0; lz < nz; ++lz) {
+      const int h = hc + (lz + 1) * PXY;
+      const uint32_t c = code[h];
+      const uint32_t gv = gv0 + d.XY * uint32_t(lz);
+      bool sh_d, sh_a;
+      const uint32_t td = Pd[h], ta = Pa[h];
+      desc[gv] = gid(td, sh_d);
+      asc[gv] = gid(ta, sh_a);
+      if (sh_d) code[td] = kExitMark;
+      if (sh_a) code[ta] = kExitMark;
+      mmax |= uint32_t((c & 15) == 15) << lz;
+      mmin |= uint32_t((c >> 4) == 15) << lz;
     }
   }
-  uint32_t cnt[3] = {uint32_t(__popc(mmax)), uint32_t(__popc(mmin)), uint32_t(__popc(mxd) + __popc(mxa))};
+  __syncthreads();
+  // exit cells: this column's two z-shell cells (bits 0, 1) and, for threads
+  // 0..131, a whole shell column (bits 2..35)
+  uint64_t mex = uint64_t(code[hc] == kExitMark) | uint64_t(code[hc + (TZ + 1) * PXY] == kExitMark) << 1;
+  if (shell_col >= 0)
+    for (int z = 0; z < TZ + 2; ++z) mex |= uint64_t(code[shell_col + z * PXY] == kExitMark) << (z + 2);
+
+  uint32_t cnt[3] = {uint32_t(__popc(mmax)), uint32_t(__popc(mmin)), uint32_t(__popcll(mex))};
   uint32_t pre[3];
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
@@ -324,10 +377,10 @@ __global__ void __launch_bounds__(A_THREADS, 1)
       if (lane >= o) inc += t;
     }
     pre[k] = inc - cnt[k];
-    if (lane == 31) s_wcnt[threadIdx.x >> 5][k] = inc;
+    if (lane == 31) s_wcnt[tid >> 5][k] = inc;
   }
   __syncthreads();
-  if (threadIdx.x < 32) {
+  if (tid < 32) {
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
       const uint32_t t = s_wcnt[lane][k];
@@ -348,33 +401,28 @@ __global__ void __launch_bounds__(A_THREADS, 1)
   __syncthreads();
   uint64_t pos[3];
 #pragma unroll
-  for (int k = 0; k < 3; ++k) pos[k] = s_lbase[k] + s_wcnt[threadIdx.x >> 5][k] + pre[k];
-#pragma unroll 2
-  for (int lz = 0; lz < TZ; ++lz) {
-    const int l = lx + TX * ly + TX * TY * lz;
-    const uint32_t c = hop[l];
-    if (c == 0xff) continue;
-    const uint32_t gv = gid(l);
-    const int ud = Pd[l], ua = Pa[l];
-    desc[gv] = gid(ud) + uint32_t(s_gdelta[hop[ud] & 15]);
-    asc[gv] = gid(ua) + uint32_t(s_gdelta[hop[ua] >> 4]);
-    const uint32_t bit = 1u << lz;
-    if (mmax & bit) {
-      if (pos[0] < ext_cap) maxima[pos[0]] = gv;
-      ++pos[0];
-    }
-    if (mmin & bit) {
-      if (pos[1] < ext_cap) minima[pos[1]] = gv;
-      ++pos[1];
-    }
-    if (mxd & bit) {
-      if (pos[2] < exit_cap) exits[pos[2]] = gv + uint32_t(s_gdelta[c & 15]);
-      ++pos[2];
-    }
-    if (mxa & bit) {
-      if (pos[2] < exit_cap) exits[pos[2]] = gv + uint32_t(s_gdelta[c >> 4]);
-      ++pos[2];
-    }
+  for (int k = 0; k < 3; ++k) pos[k] = s_lbase[k] + s_wcnt[tid >> 5][k] + pre[k];
+  uint32_t m = mmax;
+  while (m) {
+    const int lz = __ffs(m) - 1;
+    m &= m - 1;
+    if (pos[0] < ext_cap) maxima[pos[0]] = gv0 + d.XY * uint32_t(lz);
+    ++pos[0];
+  }
+  m = mmin;
+  while (m) {
+    const int lz = __ffs(m) - 1;
+    m &= m - 1;
+    if (pos[1] < ext_cap) minima[pos[1]] = gv0 + d.XY * uint32_t(lz);
+    ++pos[1];
+  }
+  while (mex) {
+    const int b = __ffsll(mex) - 1;
+    mex &= mex - 1;
+    const int h = b == 0 ? hc : b == 1 ? hc + (TZ + 1) * PXY : shell_col + (b - 2) * PXY;
+    bool sh;
+    if (pos[2] < exit_cap) exits[pos[2]] = gid(uint32_t(h), sh);
+    ++pos[2];
   }
 }
 
