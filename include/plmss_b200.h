@@ -216,7 +216,8 @@ int plmss_b200_result(const plmss_ctx* ctx, plmss_result* out);
 int plmss_b200_copy(plmss_ctx* ctx, void* dst, const void* d_src, int64_t bytes, int to_host);
 
 /* Tuning / test options:
- *   PLMSS_OPT_COMBINE_PATH  0 auto, 1 bitmap, 2 hash (staged combine_ms);
+ *   PLMSS_OPT_COMBINE_PATH  0 auto, 1 bitmap, 2 hash (staged combine_ms, and the
+ *                           fused pipeline's region keys);
  *   PLMSS_OPT_PIPELINE_PATH 0 fused tile pipeline when the dims allow it,
  *                           1 staged kernels (segment/combine/emit);
  *   PLMSS_OPT_TMA           1 (default) TMA tensor loads of the field bricks,

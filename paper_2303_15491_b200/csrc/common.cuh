@@ -73,6 +73,7 @@ enum Slot {
   S_RANK_MAX, S_RANK_MIN,        // extremum -> rank maps (N, sparse use)
   S_BITMAP, S_HASH_K, S_HASH_V, S_SORT_A, S_SORT_B, S_SORT_C, S_SORT_D,
   S_TMP0, S_TMP1, S_TMP2, S_FIELD, S_MASK,
+  S_LTD, S_LTA, S_TB, S_SD, S_SA, S_RK,  // fused pipeline: terminal indices, brick headers, table labels
   S_COUNT
 };
 
@@ -174,8 +175,6 @@ struct FusedOut {
   plmss_tri* tris;
 };
 bool fused_supported(const Grid& g);
-// march_fused.cu: ordered separator records from the edge-equality masks.
-int64_t fused_march(Ctx& c, const Grid& g, const uint32_t* ms, const uint8_t* emask, plmss_tri** out);
 FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* desc, uint32_t* asc, uint32_t* ms);
 
 // synth.cu

@@ -1,30 +1,34 @@
-// Fused B200 pipeline (the benchmarked path).
+// Fused B200 pipeline (the benchmarked path), four brick passes.
 //
-//  A  k_tile_segment  : 32x16x16-vertex tiles staged in shared memory with a
-//                       1-voxel halo. Steepest up/down hops from the 14-point
-//                       stencil (SoS on (f, id)), then pointer jumping INSIDE
-//                       shared memory until every tile vertex points at a
-//                       terminal: a root (extremum) or an exit vertex outside
-//                       the tile. Writes the partial labels (global ids) into
-//                       desc/asc, appends roots to the extremum lists, exit
-//                       targets to the exit list E, and distinct (asc, desc)
-//                       partial pairs to a hash set.
-//  B  k_exit_jump     : pointer jumping restricted to E (closed under the
-//                       partial-label map), to the global fixpoint.
-//  C  pairs           : partial pairs -> final pairs -> unique, sorted ->
-//                       dense MS ids (hash value slots).
-//  D  k_finalize_march: ordered single pass over row-slab tiles in the
-//                       reference cell order: final labels = L[L[v]], dense
-//                       id lookup, desc/asc/ms writes, 6-tet codes per cube,
-//                       decoupled look-back for output offsets, separator
-//                       records in reference order.
+//  A  k_tile_segment : per 32^3 brick, steepest hops and in-shared-memory path
+//                      compression (segmentation.cpp:60-168). Every vertex
+//                      ends at a brick terminal: an extremum of the brick or
+//                      the shell cell where its chain leaves the brick. Each
+//                      brick writes its terminal table TT (exits, maxima,
+//                      minima as brick-major cell indices) and, per vertex and
+//                      direction, the u16 index of its terminal in that table
+//                      (LT, brick-major), plus the global extremum lists.
+//  B  k_tt_*         : the exit entries of all terminal tables form a forest
+//                      whose roots are the extremum entries: successor of an
+//                      exit = the terminal of that cell in its own brick;
+//                      pointer jumping to the roots, then each entry's final
+//                      label (a global vertex id).
+//  C  k_brick<false> : per brick (+1 halo layer in x, y, z), final labels of
+//                      every vertex = table entry of its LT index; distinct
+//                      (asc, desc) pairs into the region set; separator
+//                      triangles counted per 32-cube row chunk.
+//     unique pairs sorted -> dense MS ids; chunk counts scanned -> offsets.
+//  D  k_brick<true>  : same labels again, MS ids, desc/asc/ms written, and the
+//                      separator records emitted in the reference cell order
+//                      (marching.cpp:116-215) at their chunk offsets.
 //
-// Correctness: every partial label lies on the vertex's steepest chain and
-// the chain's terminal extremum is unique, so any order of
-// these resolutions reproduces the reference labels exactly.
+// Correctness: every table entry lies on its vertex's steepest chain and the
+// chain's terminal extremum is unique, so any order of these
+// resolutions reproduces the reference labels exactly.
 #include <math.h>
 
 #include <algorithm>
+#include <type_traits>
 
 #include <cuda.h>
 
@@ -50,7 +54,8 @@ constexpr int PX = TX + 2, PXY = PX * (TY + 2), PN = PXY * (TZ + 2);  // 34, 115
 constexpr int TN = TX * TY * TZ;
 constexpr int A_THREADS = 1024;
 constexpr int kCodeOff = 4 * HN;                // hop codes after the field box
-constexpr int kASmem = 4 * HN + PN + 1024;      // + TMA alignment slack
+constexpr int kTabOff = kCodeOff + (PN + 15) / 16 * 16;  // code byte -> pointer delta, up and down
+constexpr int kASmem = kTabOff + 2 * 256 * 4 + 1024;      // + TMA alignment slack
 static_assert(2 * 2 * PN <= 4 * HN, "pointer arrays must fit in the field box");
 static_assert(kCodeOff % 16 == 0, "code array alignment");
 constexpr uint8_t kExitMark = 0xfe;  // shell cell reached by some brick vertex
@@ -87,10 +92,15 @@ __device__ __forceinline__ bool set_insert(unsigned long long* __restrict__ t, u
   return false;
 }
 
+// Slot of k, or ~0 when k is absent (a probe that meets an empty slot).
 __device__ __forceinline__ uint64_t set_find(const unsigned long long* __restrict__ t, uint64_t mask, uint64_t k) {
   uint64_t s = mix64(k) & mask;
-  while (t[s] != k) s = (s + 1) & mask;
-  return s;
+  for (;;) {
+    const unsigned long long cur = t[s];
+    if (cur == k) return s;
+    if (cur == kEmpty) return ~uint64_t(0);
+    s = (s + 1) & mask;
+  }
 }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -107,7 +117,7 @@ __host__ __device__ constexpr uint32_t stencil_code(int s) {
 }
 
 struct ACounters {
-  unsigned long long n_max, n_min, n_exit;
+  unsigned long long n_max, n_min, n_exit, n_tt;
   int overflow;
   uint32_t bad;
 };
@@ -136,9 +146,10 @@ struct ACounters {
 template <bool kTMA>
 __global__ void __launch_bounds__(A_THREADS, 1)
     k_tile_segment(const __grid_constant__ CUtensorMap tmap, const float* __restrict__ field, FDims d,
-                   uint32_t* __restrict__ desc, uint32_t* __restrict__ asc, uint32_t* __restrict__ maxima,
-                   uint32_t* __restrict__ minima, uint64_t ext_cap, uint32_t* __restrict__ exits,
-                   uint64_t exit_cap, ACounters* __restrict__ ctr) {
+                   uint32_t* __restrict__ maxima, uint32_t* __restrict__ minima, uint32_t* __restrict__ max_tt,
+                   uint32_t* __restrict__ min_tt, uint64_t ext_cap,
+                   uint32_t* __restrict__ TT, uint64_t tt_cap, uint4* __restrict__ TB, uint16_t* __restrict__ ltd,
+                   uint16_t* __restrict__ lta, ACounters* __restrict__ ctr) {
   extern __shared__ __align__(16) unsigned char a_smem_raw[];
   // TMA destinations must be 128-byte aligned: round the window up (the
   // launch reserves 1024 extra bytes for this).
@@ -147,9 +158,11 @@ __global__ void __launch_bounds__(A_THREADS, 1)
   uint16_t* Pd = reinterpret_cast<uint16_t*>(a_smem);  // PN (steps 3+, aliases f)
   uint16_t* Pa = Pd + PN;                              // PN
   uint8_t* code = a_smem + kCodeOff;                   // PN
+  int* dup = reinterpret_cast<int*>(a_smem + kTabOff);  // 256: pointer delta of the up hop of a code byte
+  int* ddn = dup + 256;                                 // 256: ... of the down hop
   __shared__ __align__(8) uint64_t s_bar;
-  __shared__ int s_delta[16];
   __shared__ uint32_t s_wcnt[A_THREADS / 32][3];
+  __shared__ uint32_t s_tot[3];
   __shared__ unsigned long long s_lbase[3];
 
   const uint32_t bt = blockIdx.x;
@@ -196,15 +209,17 @@ __global__ void __launch_bounds__(A_THREADS, 1)
     }
   }
   // while the box is in flight: no-hop codes everywhere (step 2 overwrites
-  // the in-volume brick cells) and the stencil deltas of the pointer space
+  // the in-volume brick cells) and the pointer delta of each code byte per
+  // direction (0 for "none" and for shell bytes 0xff / kExitMark)
   for (int i = 4 * tid; i < PN; i += 4 * A_THREADS) *reinterpret_cast<uint32_t*>(code + i) = 0xffffffffu;
-  if (tid < 16) {
+  if (tid < 512) {
+    const uint32_t c = uint32_t(tid & 255), sn = tid < 256 ? (c & 15) : (c >> 4);
     int dl = 0;
-    if (tid < 14) {
-      const uint32_t o = stencil_code(tid);
+    if (sn < 14 && c < kExitMark) {
+      const uint32_t o = stencil_code(int(sn));
       dl = (int(o & 3) - 1) + PX * (int((o >> 2) & 3) - 1) + PXY * (int((o >> 4) & 3) - 1);
     }
-    s_delta[tid] = dl;  // code 15 (none) -> 0
+    dup[tid] = dl;  // dup[256 + c] == ddn[c]
   }
   if (kTMA)
     asm volatile(
@@ -267,10 +282,12 @@ __global__ void __launch_bounds__(A_THREADS, 1)
   }
   __syncthreads();
 
-  // 3. pointers two hops ahead (f is dead from here on). Shell cells point
+  // 3. pointers four hops ahead (f is dead from here on). Shell cells point
   //    at themselves: the z-shell cells of this column here, the 132 shell
-  //    columns by threads 0..131.
-  uint32_t live_d = 0, live_a = 0;
+  //    columns by threads 0..131. A shell cell that is the hop target of a
+  //    brick vertex is an exit: its code byte becomes kExitMark (readers
+  //    treat 0xff and kExitMark alike).
+  uint32_t live_d = 0, mmax = 0, mmin = 0;
   Pd[hc] = uint16_t(hc);
   Pa[hc] = uint16_t(hc);
   Pd[hc + (TZ + 1) * PXY] = uint16_t(hc + (TZ + 1) * PXY);
@@ -286,87 +303,65 @@ __global__ void __launch_bounds__(A_THREADS, 1)
       Pa[h] = uint16_t(h);
     }
   }
-#pragma unroll 4
+#pragma unroll 2
   for (int lz = 0; lz < TZ; ++lz) {
     const int h = hc + (lz + 1) * PXY;
     const uint32_t c = code[h];
-    int td = h, ta = h;
-    if ((c & 15) != 15) {
-      const int t1 = h + s_delta[c & 15];
-      const uint32_t c2 = code[t1] & 15;
-      td = t1 + s_delta[c2];
-      live_d |= uint32_t(c2 != 15) << lz;
-    }
-    if ((c >> 4) != 15) {
-      const int t1 = h + s_delta[c >> 4];
-      const uint32_t c2 = code[t1] >> 4;
-      ta = t1 + s_delta[c2];
-      live_a |= uint32_t(c2 != 15) << lz;
-    }
-    Pd[h] = uint16_t(td);
-    Pa[h] = uint16_t(ta);
+    int u = h + dup[c], w = h + ddn[c];
+    const uint32_t cu = code[u], cw = code[w];
+    if (cu >= kExitMark && u != h) code[u] = kExitMark;
+    if (cw >= kExitMark && w != h) code[w] = kExitMark;
+    u += dup[cu];
+    w += ddn[cw];
+    u += dup[code[u]];
+    w += ddn[code[w]];
+    const int du = dup[code[u]], dw = ddn[code[w]];
+    Pd[h] = uint16_t(u + du);
+    Pa[h] = uint16_t(w + dw);
+    live_d |= uint32_t(du != 0 || dw != 0) << lz;  // pointer four hops ahead may not be a terminal
+    mmax |= uint32_t((c & 15) == 15) << lz;
+    mmin |= uint32_t((c >> 4) == 15) << lz;
+  }
+  {
+    const uint32_t vmask = col_ok ? (nz >= 32 ? 0xffffffffu : ((1u << nz) - 1u)) : 0u;
+    mmax &= vmask;
+    mmin &= vmask;
   }
   __syncthreads();
 
-  // 4. pointer jumping; a vertex retires once its pointer is a terminal
+  // 4. pointer jumping, P <- P^4 per round in both directions; a vertex
+  //    retires once both its pointers are terminals
+  uint32_t live = live_d;
   for (;;) {
-    uint32_t m = live_d;
+    uint32_t m = live, next = 0;
     while (m) {
-      const int lz = __ffs(m) - 1;
-      m &= m - 1;
+      const int lz = 31 - __clz(m);
+      const uint32_t bit = 1u << lz;
+      m ^= bit;
       const int h = hc + (lz + 1) * PXY;
-      const uint16_t p = Pd[h], q = Pd[p];
-      if (q == p)
-        live_d &= ~(1u << lz);
-      else
-        Pd[h] = q;
+      const uint32_t p1 = Pd[h], q1 = Pa[h];
+      const uint32_t p2 = Pd[p1], q2 = Pa[q1];
+      const uint32_t p3 = Pd[p2], q3 = Pa[q2];
+      const uint32_t p4 = Pd[p3], q4 = Pa[q3];
+      Pd[h] = uint16_t(p4);
+      Pa[h] = uint16_t(q4);
+      if (p4 != p3 || q4 != q3) next |= bit;
     }
-    m = live_a;
-    while (m) {
-      const int lz = __ffs(m) - 1;
-      m &= m - 1;
-      const int h = hc + (lz + 1) * PXY;
-      const uint16_t p = Pa[h], q = Pa[p];
-      if (q == p)
-        live_a &= ~(1u << lz);
-      else
-        Pa[h] = q;
-    }
-    if (!__syncthreads_or((live_d | live_a) != 0)) break;
+    live = next;
+    if (!__syncthreads_or(live != 0)) break;
   }
 
-  // 5. partial labels; extrema; exit shell cells marked in the code array
-  const uint32_t gbase = uint32_t(gx0 - 1) + d.X * uint32_t(gy0 - 1) + d.XY * uint32_t(gz0 - 1);
-  auto gid = [&](uint32_t t, bool& shell) -> uint32_t {
-    const uint32_t hz = t / PXY, r = t - hz * PXY, hy = r / PX, hx = r - hy * PX;
-    shell = (hx - 1u) >= uint32_t(TX) || (hy - 1u) >= uint32_t(TY) || (hz - 1u) >= uint32_t(TZ);
-    return gbase + hx + d.X * hy + d.XY * hz;
-  };
-  uint32_t mmax = 0, mmin = 0;
-  if (col_ok) {
-#pragma unroll 2
-    for (int lz = 0; lz < nz; ++lz) {
-      const int h = hc + (lz + 1) * PXY;
-      const uint32_t c = code[h];
-      const uint32_t gv = gv0 + d.XY * uint32_t(lz);
-      bool sh_d, sh_a;
-      const uint32_t td = Pd[h], ta = Pa[h];
-      desc[gv] = gid(td, sh_d);
-      asc[gv] = gid(ta, sh_a);
-      if (sh_d) code[td] = kExitMark;
-      if (sh_a) code[ta] = kExitMark;
-      mmax |= uint32_t((c & 15) == 15) << lz;
-      mmin |= uint32_t((c >> 4) == 15) << lz;
-    }
-  }
-  __syncthreads();
-  // exit cells: this column's two z-shell cells (bits 0, 1) and, for threads
-  // 0..131, a whole shell column (bits 2..35)
+  // 5. terminal table of the brick: TT[base ..) = exit cells, then maxima,
+  //    then minima (brick-major cell indices), one atomic per brick. Exit
+  //    cells: this column's two z-shell cells (bits 0, 1) and, for threads
+  //    0..131, a whole shell column (bits 2..35). The local index of every
+  //    terminal is written into the pointer arrays AT the terminal (exits in
+  //    both, extrema in their own direction's array).
   uint64_t mex = uint64_t(code[hc] == kExitMark) | uint64_t(code[hc + (TZ + 1) * PXY] == kExitMark) << 1;
   if (shell_col >= 0)
     for (int z = 0; z < TZ + 2; ++z) mex |= uint64_t(code[shell_col + z * PXY] == kExitMark) << (z + 2);
 
-  uint32_t cnt[3] = {uint32_t(__popc(mmax)), uint32_t(__popc(mmin)), uint32_t(__popcll(mex))};
+  const uint32_t cnt[3] = {uint32_t(__popcll(mex)), uint32_t(__popc(mmax)), uint32_t(__popc(mmin))};
   uint32_t pre[3];
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
@@ -391,76 +386,252 @@ __global__ void __launch_bounds__(A_THREADS, 1)
         if (lane >= o) inc += u;
       }
       s_wcnt[lane][k] = inc - t;
-      const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
-      if (lane == 0) {
-        unsigned long long* ctrk = k == 0 ? &ctr->n_max : (k == 1 ? &ctr->n_min : &ctr->n_exit);
-        s_lbase[k] = total ? atomicAdd(ctrk, (unsigned long long)total) : 0ull;
-      }
+      if (lane == 31) s_tot[k] = inc;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      const uint32_t te = s_tot[0], tm = s_tot[1], tn = s_tot[2];
+      const unsigned long long base = atomicAdd(&ctr->n_tt, (unsigned long long)(te + tm + tn));
+      s_lbase[0] = base;
+      s_lbase[1] = tm ? atomicAdd(&ctr->n_max, (unsigned long long)tm) : 0ull;
+      s_lbase[2] = tn ? atomicAdd(&ctr->n_min, (unsigned long long)tn) : 0ull;
+      if (te) atomicAdd(&ctr->n_exit, (unsigned long long)te);
+      TB[bt] = make_uint4(uint32_t(base), te, tm, tn);
     }
   }
   __syncthreads();
-  uint64_t pos[3];
+  const uint32_t te = s_tot[0], tm = s_tot[1];
+  const uint64_t tbase = s_lbase[0];
+  uint32_t lk[3];
 #pragma unroll
-  for (int k = 0; k < 3; ++k) pos[k] = s_lbase[k] + s_wcnt[tid >> 5][k] + pre[k];
+  for (int k = 0; k < 3; ++k) lk[k] = s_wcnt[tid >> 5][k] + pre[k];
+  lk[1] += te;
+  lk[2] += te + tm;
+  uint64_t gpos_max = s_lbase[1] + (lk[1] - te), gpos_min = s_lbase[2] + (lk[2] - te - tm);
+  const uint32_t bm0 = bt << 15;  // brick-major index of the brick's cell 0
+  while (mex) {
+    const int b = __ffsll(mex) - 1;
+    mex &= mex - 1;
+    const uint32_t h = b == 0 ? uint32_t(hc) : b == 1 ? uint32_t(hc + (TZ + 1) * PXY) : uint32_t(shell_col + (b - 2) * PXY);
+    // the shell cell's brick and local coordinates (shell index 0 -> 31 of
+    // the previous brick, 33 -> 0 of the next)
+    const int hz = int(h / PXY), r = int(h) - hz * PXY, hy = r / PX, hx = r - hy * PX;
+    const uint32_t nb = uint32_t(int(tx) + ((hx - 1) >> 5)) +
+                        d.tx * (uint32_t(int(ty) + ((hy - 1) >> 5)) + d.ty * uint32_t(int(tz) + ((hz - 1) >> 5)));
+    const uint32_t bm = (nb << 15) | uint32_t((hx - 1) & 31) | uint32_t((hy - 1) & 31) << 5 |
+                        uint32_t((hz - 1) & 31) << 10;
+    if (tbase + lk[0] < tt_cap) TT[tbase + lk[0]] = bm;
+    Pd[h] = uint16_t(lk[0]);
+    Pa[h] = uint16_t(lk[0]);
+    ++lk[0];
+  }
   uint32_t m = mmax;
   while (m) {
     const int lz = __ffs(m) - 1;
     m &= m - 1;
-    if (pos[0] < ext_cap) maxima[pos[0]] = gv0 + d.XY * uint32_t(lz);
-    ++pos[0];
+    if (tbase + lk[1] < tt_cap) TT[tbase + lk[1]] = bm0 | uint32_t(lx + TX * ly + TX * TY * lz);
+    if (gpos_max < ext_cap) {
+      maxima[gpos_max] = gv0 + d.XY * uint32_t(lz);
+      max_tt[gpos_max] = uint32_t(tbase + lk[1]);
+    }
+    Pd[hc + (lz + 1) * PXY] = uint16_t(lk[1]);
+    ++lk[1];
+    ++gpos_max;
   }
   m = mmin;
   while (m) {
     const int lz = __ffs(m) - 1;
     m &= m - 1;
-    if (pos[1] < ext_cap) minima[pos[1]] = gv0 + d.XY * uint32_t(lz);
-    ++pos[1];
+    if (tbase + lk[2] < tt_cap) TT[tbase + lk[2]] = bm0 | uint32_t(lx + TX * ly + TX * TY * lz);
+    if (gpos_min < ext_cap) {
+      minima[gpos_min] = gv0 + d.XY * uint32_t(lz);
+      min_tt[gpos_min] = uint32_t(tbase + lk[2]);
+    }
+    Pa[hc + (lz + 1) * PXY] = uint16_t(lk[2]);
+    ++lk[2];
+    ++gpos_min;
   }
-  while (mex) {
-    const int b = __ffsll(mex) - 1;
-    mex &= mex - 1;
-    const int h = b == 0 ? hc : b == 1 ? hc + (TZ + 1) * PXY : shell_col + (b - 2) * PXY;
-    bool sh;
-    if (pos[2] < exit_cap) exits[pos[2]] = gid(uint32_t(h), sh);
-    ++pos[2];
+  __syncthreads();
+
+  // 6. LT: the terminal index of every in-volume vertex (an extremum reads
+  //    its own entry, any other vertex its terminal's)
+  if (col_ok) {
+    uint16_t* od = ltd + bm0 + lx + TX * ly;
+    uint16_t* oa = lta + bm0 + lx + TX * ly;
+#pragma unroll 4
+    for (int lz = 0; lz < nz; ++lz) {
+      const int h = hc + (lz + 1) * PXY;
+      const uint32_t bit = 1u << lz;
+      const uint32_t pd = Pd[h], pa = Pa[h];
+      od[TX * TY * lz] = (mmax & bit) ? uint16_t(pd) : Pd[pd];
+      oa[TX * TY * lz] = (mmin & bit) ? uint16_t(pa) : Pa[pa];
+    }
   }
 }
 
 // ---------------------------------------------------------------- pass B --
-// Chain following on the live arrays: each exit vertex walks up to kChase
+// Terminal-table forest. Entry k of brick b is an exit (shell cell c, a
+// vertex of a neighbouring brick b') or an extremum of b. The successor of an
+// exit is the terminal of c in b': TB[b'].base + LT[c]; an extremum is its
+// own successor. Chains follow the steepest paths, so the graph is a forest
+// rooted at the extremum entries.
+__global__ void __launch_bounds__(256) k_tt_succ(const uint4* __restrict__ TB, const uint32_t* __restrict__ TT,
+                                                 const uint16_t* __restrict__ ltd,
+                                                 const uint16_t* __restrict__ lta, uint32_t* __restrict__ SD,
+                                                 uint32_t* __restrict__ SA) {
+  const uint4 h = TB[blockIdx.x];
+  const uint32_t n = h.y + h.z + h.w;
+  const uint32_t* TBw = reinterpret_cast<const uint32_t*>(TB);
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const uint32_t k = h.x + i;
+    uint32_t sd = k, sa = k;
+    if (i < h.y) {
+      const uint32_t bm = __ldg(TT + k);
+      const uint32_t nb = __ldg(TBw + 4 * (bm >> 15));
+      sd = nb + __ldg(ltd + bm);
+      sa = nb + __ldg(lta + bm);
+    }
+    SD[k] = sd;
+    SA[k] = sa;
+  }
+}
+
+// Chain following on the successor arrays: each entry walks up to kChase
 // links (both directions interleaved for memory-level parallelism) and
-// stores the furthest vertex reached. Values read from entries other
-// threads have already advanced only shorten the walk; every value lies on
-// the vertex's chain, so concurrent updates are safe.
+// stores the furthest entry reached. Values read from entries other threads
+// have already advanced only shorten the walk; every value lies on the
+// entry's chain, so concurrent updates are safe.
 constexpr int kChase = 16;
 
-__global__ void __launch_bounds__(256) k_exit_jump(const uint32_t* __restrict__ E, uint64_t ne,
-                                                   uint32_t* __restrict__ desc, uint32_t* __restrict__ asc,
-                                                   int* __restrict__ changed) {
+__global__ void __launch_bounds__(256) k_tt_jump(uint64_t nt, uint32_t* __restrict__ SD, uint32_t* __restrict__ SA,
+                                                 int* __restrict__ changed) {
   const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   bool ch = false;
-  if (i < ne) {
-    const uint32_t e = E[i];
-    const uint32_t d0 = desc[e], a0 = asc[e];
+  if (i < nt) {
+    const uint32_t d0 = SD[i], a0 = SA[i];
     uint32_t xd = d0, xa = a0;
     bool dd = false, da = false;
 #pragma unroll 4
     for (int k = 0; k < kChase && !(dd && da); ++k) {
-      const uint32_t nd = dd ? xd : desc[xd];
-      const uint32_t na = da ? xa : asc[xa];
+      const uint32_t nd = dd ? xd : SD[xd];
+      const uint32_t na = da ? xa : SA[xa];
       dd = nd == xd;
       da = na == xa;
       xd = nd;
       xa = na;
     }
-    if (xd != d0) desc[e] = xd;
-    if (xa != a0) asc[e] = xa;
+    if (xd != d0) SD[i] = xd;
+    if (xa != a0) SA[i] = xa;
     ch = !(dd && da);
   }
   if (__any_sync(0xffffffffu, ch) && (threadIdx.x & 31) == 0) *changed = 1;
 }
 
-// ---------------------------------------------------------------- pass C --
+// Root entry -> final label as the root's rank in the sorted extremum list
+// (RK, written by k_rank_lists): SD/SA become per-entry ranks.
+__global__ void __launch_bounds__(256) k_tt_final(uint64_t nt, const uint32_t* __restrict__ RK,
+                                                  uint32_t* __restrict__ SD, uint32_t* __restrict__ SA) {
+  const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= nt) return;
+  SD[i] = __ldg(RK + SD[i]);
+  SA[i] = __ldg(RK + SA[i]);
+}
+
+// (gid, table entry) pairs of an extremum list for the radix sort
+__global__ void k_list_pairs(const uint32_t* __restrict__ list, const uint32_t* __restrict__ tt, int64_t n,
+                             uint64_t* __restrict__ keys, uint64_t* __restrict__ vals) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) {
+    keys[i] = list[i];
+    vals[i] = tt[i];
+  }
+}
+
+// sorted pairs -> ascending list and the rank of every extremum table entry
+__global__ void k_rank_lists(const uint64_t* __restrict__ keys, const uint64_t* __restrict__ vals, int64_t n,
+                             uint32_t* __restrict__ list, uint32_t* __restrict__ RK) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) {
+    list[i] = uint32_t(keys[i]);
+    RK[vals[i]] = uint32_t(i);
+  }
+}
+
+// Dense region bitmap (key = rank_min * n_max + rank_max, n_max * n_min <=
+// 2^32): popcount per word, then per-word exclusive prefix (the dense MS id
+// of the word's first set bit) and the region keys (asc << 32 | desc, in
+// ascending order = the reference's sorted pair order).
+constexpr int kWB = 1024;  // words per block
+__global__ void __launch_bounds__(256) k_bitmap_count(const uint32_t* __restrict__ bm, uint64_t nw,
+                                                      uint64_t* __restrict__ bsum) {
+  const uint64_t w0 = uint64_t(blockIdx.x) * kWB;
+  uint32_t c = 0;
+  for (int k = threadIdx.x; k < kWB; k += 256)
+    if (w0 + k < nw) c += __popc(bm[w0 + k]);
+  c = __reduce_add_sync(0xffffffffu, c);
+  __shared__ uint32_t ws[8];
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t t = 0;
+    for (int q = 0; q < 8; ++q) t += ws[q];
+    bsum[blockIdx.x] = t;
+  }
+}
+
+__global__ void __launch_bounds__(kWB) k_bitmap_ids(const uint32_t* __restrict__ bm, uint64_t nw,
+                                                    const uint64_t* __restrict__ boff, uint32_t nmax,
+                                                    const uint32_t* __restrict__ maxs,
+                                                    const uint32_t* __restrict__ mins, uint32_t* __restrict__ prefix,
+                                                    uint64_t* __restrict__ keys) {
+  __shared__ uint32_t ws[kWB / 32];
+  const uint64_t wi = uint64_t(blockIdx.x) * kWB + threadIdx.x;
+  const uint32_t word = wi < nw ? bm[wi] : 0u;
+  const uint32_t c = __popc(word);
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  uint32_t inc = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += t;
+  }
+  if (lane == 31) ws[wp] = inc;
+  __syncthreads();
+  if (wp == 0) {
+    const uint32_t t = ws[lane];
+    uint32_t s2 = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xffffffffu, s2, o);
+      if (lane >= o) s2 += u;
+    }
+    ws[lane] = s2 - t;
+  }
+  __syncthreads();
+  if (wi >= nw) return;
+  uint64_t id = boff[blockIdx.x] + ws[wp] + (inc - c);
+  prefix[wi] = uint32_t(id);
+  uint32_t m = word;
+  while (m) {
+    const uint32_t b = __ffs(m) - 1;
+    m &= m - 1;
+    const uint64_t key = wi * 32 + b;
+    const uint32_t ra = uint32_t(key / nmax), rd = uint32_t(key - uint64_t(ra) * nmax);
+    keys[id++] = (uint64_t(__ldg(mins + ra)) << 32) | __ldg(maxs + rd);
+  }
+}
+
+// hash mode: sorted rank-pair keys -> region keys in vertex ids
+__global__ void k_keys_to_gid(uint64_t* __restrict__ keys, int64_t r, const uint32_t* __restrict__ maxs,
+                              const uint32_t* __restrict__ mins) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < r) {
+    const uint64_t k = keys[i];
+    keys[i] = (uint64_t(__ldg(mins + (k >> 32))) << 32) | __ldg(maxs + uint32_t(k));
+  }
+}
+
+// ------------------------------------------------- region set compaction --
 constexpr int kCThreads = 256;
 constexpr int kCRows = 16;
 constexpr int kCTile = kCThreads * kCRows;
@@ -518,122 +689,278 @@ __global__ void __launch_bounds__(kCThreads) k_write_occ(const unsigned long lon
   }
 }
 
-// Pass C: final labels in place, desc[v] <- desc[desc[v]] (partial labels
-// point at roots or at exit vertices already resolved by pass B, and those
-// entries never change value here), and every final (asc, desc) pair into
-// the region set with warp-level dedup. 4 vertices per thread per step keep
-// enough independent loads in flight.
-constexpr int C_VPT = 4;
-// Vertices are visited in pass-A tile order (32x16x16 bricks, x-rows of 32
-// inside), so the gathers desc[desc[v]] hit the few exit vertices around the
-// brick while they are still in L2.
-__global__ void __launch_bounds__(256) k_mark_pairs(FDims dm, uint32_t* __restrict__ desc,
-                                                    uint32_t* __restrict__ asc,
-                                                    unsigned long long* __restrict__ fset, uint64_t fmask,
-                                                    int* __restrict__ overflow) {
-  const int lane = threadIdx.x & 31;
-  const uint64_t total = uint64_t(dm.tx) * dm.ty * dm.tz * TN;
-  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x * C_VPT;
-  for (uint64_t base = uint64_t(blockIdx.x) * blockDim.x * C_VPT; base < total; base += stride) {
-    uint32_t v[C_VPT], pd[C_VPT], pa[C_VPT], fd[C_VPT], fa[C_VPT];
-    bool okv[C_VPT];
-#pragma unroll
-    for (int k = 0; k < C_VPT; ++k) {
-      const uint64_t idx = base + uint64_t(k) * blockDim.x + threadIdx.x;
-      const uint32_t t = uint32_t(idx / TN), l = uint32_t(idx % TN);
-      const uint32_t tx = t % dm.tx, ty = (t / dm.tx) % dm.ty, tz = t / (dm.tx * dm.ty);
-      const uint32_t x = tx * TX + (l % TX), y = ty * TY + ((l / TX) % TY), z = tz * TZ + l / (TX * TY);
-      okv[k] = idx < total && x < dm.X && y < dm.Y && z < dm.Z;
-      v[k] = x + dm.X * (y + dm.Y * z);
-      pd[k] = okv[k] ? desc[v[k]] : 0;
-      pa[k] = okv[k] ? asc[v[k]] : 0;
-    }
-#pragma unroll
-    for (int k = 0; k < C_VPT; ++k) {
-      fd[k] = okv[k] ? desc[pd[k]] : 0;
-      fa[k] = okv[k] ? asc[pa[k]] : 0;
-    }
-#pragma unroll
-    for (int k = 0; k < C_VPT; ++k) {
-      const bool ok = okv[k];
-      if (ok && fd[k] != pd[k]) desc[v[k]] = fd[k];
-      if (ok && fa[k] != pa[k]) asc[v[k]] = fa[k];
-      const uint64_t key = ok ? ((uint64_t(fa[k]) << 32) | fd[k]) : kEmpty;
-      const unsigned peers = __match_any_sync(0xffffffffu, key);
-      if (ok && (peers & ((1u << lane) - 1)) == 0)
-        if (!set_insert(fset, fmask, key)) *overflow = 1;
-    }
-  }
-}
-
 __global__ void k_set_ids(const uint64_t* __restrict__ sorted_slots, int64_t r, uint32_t* __restrict__ slot_id) {
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i < r) slot_id[sorted_slots[i]] = uint32_t(i);
 }
 
-__global__ void k_u64_to_u32(const uint64_t* __restrict__ in, int64_t n, uint32_t* __restrict__ out) {
-  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i < n) out[i] = uint32_t(in[i]);
-}
+// ------------------------------------------------------------ passes C, D --
+// One CTA per brick of 32^3 cubes; the vertex layers z = 0..32 of the brick
+// plus its +x / +y halo (33 x 33 vertices per layer) are loaded kBatch layers
+// at a time into a ring of kBatch + 1 layers in shared memory (all of a
+// batch's loads in flight together). Every vertex's final pair is the table
+// entry of its LT index: (FA[base + lta[v]], FD[base + ltd[v]]), base = its
+// brick's table. Then warp w handles cube row y = w of each cube layer whose
+// two vertex layers are present, lane = cube x (one 32-cube chunk of the
+// reference cell order).
+constexpr int LW = TX + 1, LQ = LW * (TY + 1);  // 33, 1089 vertices per layer
+constexpr int kBatch = 4, kRing = kBatch + 1;
+__constant__ uint32_t c_mrows[PLMSS_TET_ROWS];
+__constant__ uint16_t c_mcases[32];
 
-__global__ void k_u32_to_u64(const uint32_t* __restrict__ in, int64_t n, uint64_t* __restrict__ out,
-                             uint64_t* __restrict__ vals) {
-  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i < n) {
-    out[i] = in[i];
-    vals[i] = 0;
+// equality pattern (b==a, c==a, c==b, d==a, d==b, d==c) of tet (a,b,c,d)
+// -> tetra_code (marching.cpp:28-44) | separator count << 5
+__device__ __forceinline__ void load_march_tables(uint16_t* s_tlut, uint16_t* s_cases, uint32_t* s_rows) {
+  if (threadIdx.x < 32) s_cases[threadIdx.x] = c_mcases[threadIdx.x];
+  if (threadIdx.x < PLMSS_TET_ROWS) s_rows[threadIdx.x] = c_mrows[threadIdx.x];
+  if (threadIdx.x < 64) {
+    const uint32_t p = threadIdx.x;
+    const int l1 = (p & 1) ? 0 : 1;
+    const int l2 = (p & 2) ? 0 : ((p & 4) ? l1 : 2);
+    const int l3 = (p & 8) ? 0 : ((p & 16) ? l1 : ((p & 32) ? l2 : 3));
+    const int code = (l1 << 4) | (l2 << 2) | l3;
+    s_tlut[p] = uint16_t(code | ((c_mcases[code] & 15) << 5));
   }
 }
 
-// ---------------------------------------------------------------- pass D --
-// D1: ms[v] = dense id of the final pair (hash value slot), warp-deduped
-// lookups, 4 vertices per thread per step.
-// Also writes the vertex's edge-equality mask: bit k-1 (k = 1..7, k = dx |
-// dy << 1 | dz << 2) is set when the vertex and its +offset-k neighbour share
-// a Morse-Smale region (equal (asc, desc) pair <=> equal dense id). Every tet
-// edge is such a positive stencil edge, so a cube is one region iff its min
-// corner's mask is 0x7f, and all 19 label equalities the 6 tet codes need
-// are mask bits of the cube's corners 0..6.
-// One block per x-row segment (blockIdx.x = segment, blockIdx.y = row
-// y + Y*z), so coordinates need no division.
-__global__ void __launch_bounds__(256) k_assign_ms(uint32_t X, uint32_t Y, uint32_t Z,
-                                                   const uint32_t* __restrict__ desc,
-                                                   const uint32_t* __restrict__ asc,
-                                                   const unsigned long long* __restrict__ fset, uint64_t fmask,
-                                                   const uint32_t* __restrict__ slot_id, uint32_t* __restrict__ ms,
-                                                   uint8_t* __restrict__ emask) {
-  const int lane = threadIdx.x & 31;
-  const uint32_t XY = X * Y;
-  const uint32_t nseg = (X + blockDim.x - 1) / blockDim.x;
-  const uint32_t row = blockIdx.x / nseg, seg = blockIdx.x - row * nseg;
-  const uint32_t y = row % Y, z = row / Y;
-  const bool by = y + 1 < Y, bz = z + 1 < Z;
-  const uint32_t x = seg * blockDim.x + threadIdx.x;
-  const bool ok = x < X;
-  const uint32_t v = row * X + x;
-  const uint64_t key = ok ? ((uint64_t(__ldg(asc + v)) << 32) | __ldg(desc + v)) : kEmpty;
-  // neighbour pairs first (independent loads in flight together)
-  uint32_t nd[7], na[7];
-  const bool bx = x + 1 < X;
+// The 6 tet codes (5 bits each) and separator count of a cube from its
+// corner labels, corner c = dx | dy << 1 | dz << 2; tets t = {0,1,3,7}
+// {0,1,5,7} {0,2,3,7} {0,2,6,7} {0,4,5,7} {0,4,6,7} (complex.cpp:203-218).
+template <class L>
+__device__ __forceinline__ uint32_t cube_codes(const L (&c)[8], const uint16_t* s_tlut, uint32_t& cnt) {
+  const uint32_t e01 = c[1] == c[0], e02 = c[2] == c[0], e04 = c[4] == c[0], e07 = (c[7] == c[0]) << 3;
+  const uint32_t e03 = c[3] == c[0], e05 = c[5] == c[0], e06 = c[6] == c[0];
+  const uint32_t e13 = c[3] == c[1], e15 = c[5] == c[1], e23 = c[3] == c[2], e26 = c[6] == c[2];
+  const uint32_t e45 = c[5] == c[4], e46 = c[6] == c[4];
+  const uint32_t e17 = c[7] == c[1], e27 = c[7] == c[2], e47 = c[7] == c[4];
+  const uint32_t e37 = c[7] == c[3], e57 = c[7] == c[5], e67 = c[7] == c[6];
+  const uint32_t t0 = s_tlut[e01 | e03 << 1 | e13 << 2 | e07 | e17 << 4 | e37 << 5];
+  const uint32_t t1 = s_tlut[e01 | e05 << 1 | e15 << 2 | e07 | e17 << 4 | e57 << 5];
+  const uint32_t t2 = s_tlut[e02 | e03 << 1 | e23 << 2 | e07 | e27 << 4 | e37 << 5];
+  const uint32_t t3 = s_tlut[e02 | e06 << 1 | e26 << 2 | e07 | e27 << 4 | e67 << 5];
+  const uint32_t t4 = s_tlut[e04 | e05 << 1 | e45 << 2 | e07 | e47 << 4 | e57 << 5];
+  const uint32_t t5 = s_tlut[e04 | e06 << 1 | e46 << 2 | e07 | e47 << 4 | e67 << 5];
+  cnt = (t0 >> 5) + (t1 >> 5) + (t2 >> 5) + (t3 >> 5) + (t4 >> 5) + (t5 >> 5);
+  return (t0 & 31) | (t1 & 31) << 5 | (t2 & 31) << 10 | (t3 & 31) << 15 | (t4 & 31) << 20 | (t5 & 31) << 25;
+}
+
+struct BrickArgs {
+  FDims d;
+  uint32_t nxc;  // 32-cube chunks per cube row
+  const uint4* TB;
+  const uint16_t *ltd, *lta;
+  const uint32_t *FD, *FA;        // per table entry: rank of the maximum / minimum
+  const uint32_t *maxs, *mins;    // sorted extremum lists (rank -> vertex id)
+  uint32_t nmax;                  // dense mode: key = rank_min * nmax + rank_max
+  uint32_t* bitmap;               // dense mode: region bitmap
+  const uint32_t* prefix;         // dense mode D: per-word dense id of the first set bit
+  unsigned long long* fset;       // hash mode: region set of (rank_min << 32 | rank_max)
+  uint64_t fmask;
+  const uint32_t* slot_id;  // hash mode D: region set slot -> dense id
+  uint64_t* chunk;          // C: counts out; D: exclusive offsets in
+  uint64_t total;           // D: total records
+  uint32_t *desc, *asc, *ms;
+  plmss_tri* out;
+  int* overflow;
+};
+
+// kEmit = false: pass C (region set + chunk counts); true: pass D.
+// kDense: region keys are u32 rank products in a bitmap, else u64 rank pairs
+// in the hash set.
+template <bool kEmit, bool kDense>
+__global__ void __launch_bounds__(1024, 1) k_brick(const BrickArgs a) {
+  using Key = typename std::conditional<kDense, uint32_t, unsigned long long>::type;
+  using Lab = typename std::conditional<kEmit, uint32_t, Key>::type;
+  extern __shared__ __align__(16) unsigned char b_smem[];
+  Lab* ring = reinterpret_cast<Lab*>(b_smem);  // kRing x LQ
+  __shared__ uint16_t s_tlut[64], s_cases[32];
+  __shared__ uint32_t s_rows[PLMSS_TET_ROWS];
+  const FDims& d = a.d;
+  const uint32_t bt = blockIdx.x;
+  const uint32_t tx = bt % d.tx, ty = (bt / d.tx) % d.ty, tz = bt / (d.tx * d.ty);
+  const uint32_t gx0 = tx * TX, gy0 = ty * TY, gz0 = tz * TZ;
+  const int tid = int(threadIdx.x), lane = tid & 31, w = tid >> 5;
+  load_march_tables(s_tlut, s_cases, s_rows);
+  const uint32_t* TBw = reinterpret_cast<const uint32_t*>(a.TB);
+  const int nl = int(min(uint32_t(TZ + 1), d.Z - gz0));  // vertex layers of the brick + halo
+  // this thread's cube column: x = lane, y = w
+  const uint32_t cy = gy0 + uint32_t(w);
+  const bool row_ok = cy + 1 < d.Y && tx < a.nxc;
+  const bool cube_ok = row_ok && gx0 + uint32_t(lane) + 1 < d.X;
+  const Lab kNone = Lab(~Lab(0));
+  // per-thread cache of the last pair seen in each of its two columns (D:
+  // with its id and vertex ids)
+  Key lkey0 = Key(~Key(0)), lkey1 = Key(~Key(0));
+  uint32_t lid0 = 0, lid1 = 0;
+  uint2 lgv0 = make_uint2(0, 0), lgv1 = make_uint2(0, 0);
+
+  for (int z0 = 0; z0 < nl; z0 += kBatch) {
+    const int zn = min(kBatch, nl - z0);
+    // ---- load layers z0 .. z0+zn-1 (threads 0..64 also take q = 1024..1088)
+    auto load_column = [&](const int q, Key& lkey, uint32_t& lid, uint2& lgv) {
+      const int x = q % LW, y = q / LW;
+      const uint32_t gx = gx0 + uint32_t(x), gy = gy0 + uint32_t(y);
+      if (gx >= d.X || gy >= d.Y) {
 #pragma unroll
-  for (int o = 1; o < 8; ++o) {
-    const bool in = ok && (!(o & 1) || bx) && (!(o & 2) || by) && (!(o & 4) || bz);
-    const uint32_t u = v + ((o & 1) ? 1u : 0u) + ((o & 2) ? X : 0u) + ((o & 4) ? XY : 0u);
-    nd[o - 1] = in ? __ldg(desc + u) : ~0u;
-    na[o - 1] = in ? __ldg(asc + u) : ~0u;
+        for (int i = 0; i < kBatch; ++i)
+          if (i < zn) ring[((z0 + i) % kRing) * LQ + q] = kNone;
+        return;
+      }
+      const uint32_t nb_lo = (tx + uint32_t(x >> 5)) + d.tx * ((ty + uint32_t(y >> 5)) + d.ty * tz);
+      const uint32_t nb_hi = nb_lo + d.tx * d.ty;  // layer 32 lives in the next brick up
+      const uint32_t lxy = uint32_t(x & 31) | uint32_t(y & 31) << 5;
+      uint32_t ld[kBatch], la[kBatch];
+#pragma unroll
+      for (int i = 0; i < kBatch; ++i) {
+        const int z = z0 + i;
+        if (i < zn) {
+          const uint32_t bm = ((z < TZ ? nb_lo : nb_hi) << 15) | lxy | uint32_t(z & 31) << 10;
+          ld[i] = __ldg(a.ltd + bm);
+          la[i] = __ldg(a.lta + bm);
+        }
+      }
+      const uint32_t base_lo = __ldg(TBw + 4 * nb_lo);
+      const uint32_t base_hi = z0 + zn > TZ ? __ldg(TBw + 4 * nb_hi) : 0u;
+#pragma unroll
+      for (int i = 0; i < kBatch; ++i) {
+        if (i < zn) {
+          const uint32_t base = z0 + i < TZ ? base_lo : base_hi;
+          ld[i] = __ldg(a.FD + base + ld[i]);  // table entry replaces the index
+          la[i] = __ldg(a.FA + base + la[i]);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < kBatch; ++i) {
+        if (i >= zn) break;
+        const int z = z0 + i;
+        const Key key = kDense ? Key(la[i] * a.nmax + ld[i]) : Key((uint64_t(la[i]) << 32) | ld[i]);
+        const bool own = x < TX && y < TY && z < TZ;
+        Lab* L = ring + (z % kRing) * LQ;
+        if (!kEmit) {
+          // distinct pairs of the owned vertices -> region bitmap / set
+          if (own && key != lkey) {
+            if (kDense) {
+              const uint32_t bit = 1u << (uint32_t(key) & 31);
+              uint32_t* wp = a.bitmap + (uint32_t(key) >> 5);
+              if (!(*wp & bit)) atomicOr(wp, bit);
+            } else if (!set_insert(a.fset, a.fmask, uint64_t(key))) {
+              *a.overflow = 1;
+            }
+            lkey = key;
+          }
+          L[q] = key;
+        } else {
+          if (key != lkey) {
+            if (kDense) {
+              const uint32_t k = uint32_t(key);
+              lid = __ldg(a.prefix + (k >> 5)) + __popc(__ldg(a.bitmap + (k >> 5)) & ((1u << (k & 31)) - 1u));
+            } else {
+              const uint64_t slot = set_find(a.fset, a.fmask, uint64_t(key));
+              if (slot == ~uint64_t(0))
+                *a.overflow = 1;  // a pair the count pass never saw: reported, never a silent id
+              else
+                lid = __ldg(a.slot_id + slot);
+            }
+            lgv = make_uint2(__ldg(a.maxs + ld[i]), __ldg(a.mins + la[i]));
+            lkey = key;
+          }
+          L[q] = lid;
+          if (own) {
+            const uint32_t gv = gx + d.X * (gy + d.Y * (gz0 + uint32_t(z)));
+            a.desc[gv] = lgv.x;
+            a.asc[gv] = lgv.y;
+            a.ms[gv] = lid;
+          }
+        }
+      }
+    };
+    load_column(tid, lkey0, lid0, lgv0);
+    if (tid < LQ - 1024) load_column(tid + 1024, lkey1, lid1, lgv1);
+    // D: this warp's chunk offsets for the batch's cube layers (lane i <->
+    // vertex layer z0 + i, cube layer z0 + i - 1)
+    uint64_t pre_off = 0;
+    if (kEmit && lane < zn && z0 + lane >= 1 && row_ok)
+      pre_off = a.chunk[(uint64_t(cy) + uint64_t(d.Y - 1) * (gz0 + uint32_t(z0 + lane) - 1)) * a.nxc + tx];
+    __syncthreads();
+    // ---- cube layers z-1 whose two vertex layers are loaded
+    for (int z = max(z0, 1); z < z0 + zn; ++z) {
+      const Lab* lo = ring + ((z - 1) % kRing) * LQ;
+      const Lab* cur = ring + (z % kRing) * LQ;
+      const int o = w * LW + lane;
+      uint32_t cnt = 0, code6 = 0;
+      if (cube_ok) {
+        Lab c[8];
+        c[0] = lo[o];
+        c[1] = lo[o + 1];
+        c[2] = lo[o + LW];
+        c[3] = lo[o + LW + 1];
+        c[4] = cur[o];
+        c[5] = cur[o + 1];
+        c[6] = cur[o + LW];
+        c[7] = cur[o + LW + 1];
+        const bool uni = c[1] == c[0] && c[2] == c[0] && c[3] == c[0] && c[4] == c[0] && c[5] == c[0] &&
+                         c[6] == c[0] && c[7] == c[0];
+        if (!uni) code6 = cube_codes(c, s_tlut, cnt);
+      }
+      const uint32_t cz = gz0 + uint32_t(z) - 1;
+      if (!kEmit) {
+        const uint32_t tot = __reduce_add_sync(0xffffffffu, cnt);
+        if (lane == 0 && row_ok) a.chunk[(uint64_t(cy) + uint64_t(d.Y - 1) * cz) * a.nxc + tx] = tot;
+        continue;
+      }
+      uint32_t inc = cnt;
+#pragma unroll
+      for (int s = 1; s < 32; s <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, inc, s);
+        if (lane >= s) inc += t;
+      }
+      const uint32_t T = __shfl_sync(0xffffffffu, inc, 31);
+      const uint64_t base = __shfl_sync(0xffffffffu, pre_off, z - z0);
+      if (T == 0 || !row_ok) continue;
+      const uint64_t q0 = uint64_t(gx0) + uint64_t(d.X - 1) * (uint64_t(cy) + uint64_t(d.Y - 1) * cz);
+      for (uint32_t j0 = 0; j0 < T; j0 += 32) {
+        const uint32_t j = j0 + uint32_t(lane);
+        // owning lane of record j = number of lanes whose inclusive count <= j
+        int src = 0;
+#pragma unroll
+        for (int step = 16; step >= 1; step >>= 1) {
+          const uint32_t vv = __shfl_sync(0xffffffffu, inc, src + step - 1);
+          if (vv <= j) src += step;
+        }
+        const uint32_t c6 = __shfl_sync(0xffffffffu, code6, src & 31);
+        const uint32_t ex = __shfl_sync(0xffffffffu, inc - cnt, src & 31);
+        if (j >= T) continue;
+        uint32_t k = j - ex;
+        int t = 0;
+        uint32_t cs = s_cases[c6 & 31];
+#pragma unroll
+        for (int tt = 0; tt < 5; ++tt) {
+          if (k < (cs & 15)) break;
+          k -= cs & 15;
+          ++t;
+          cs = s_cases[(c6 >> (5 * t)) & 31];
+        }
+        const uint32_t rowi = (cs >> 4) + k;
+        const uint32_t row = s_rows[rowi];
+        // tet t = cube corners {0, cb, cc, 7}; corner p -> ring cell
+        const uint32_t cb = (0x442211u >> (4 * t)) & 15, cc = (0x656353u >> (4 * t)) & 15;
+        auto corner = [&](uint32_t p) { return p == 0 ? 0u : (p == 1 ? cb : (p == 2 ? cc : 7u)); };
+        auto lab = [&](uint32_t cn) -> uint32_t {
+          const Lab* L = (cn & 4) ? cur : lo;
+          return uint32_t(L[w * LW + src + int(cn & 1) + LW * int((cn >> 1) & 1)]);
+        };
+        const uint32_t la = lab(corner((row >> 12) & 3)), lb = lab(corner((row >> 14) & 3));
+        const uint64_t cr64 = ((6ull * (q0 + uint32_t(src)) + uint32_t(t)) << 6) | uint64_t(rowi);
+        uint4 rec;
+        rec.x = uint32_t(cr64);
+        rec.y = uint32_t(cr64 >> 32);
+        rec.z = min(la, lb);
+        rec.w = max(la, lb);
+        *reinterpret_cast<uint4*>(a.out + base + j) = rec;
+      }
+    }
+    __syncthreads();
   }
-  const unsigned peers = __match_any_sync(0xffffffffu, key);
-  const int leader = __ffs(peers) - 1;
-  uint32_t id = 0;
-  if (lane == leader && key != kEmpty) id = __ldg(slot_id + set_find(fset, fmask, key));
-  id = __shfl_sync(0xffffffffu, id, leader);
-  if (!ok) return;
-  ms[v] = id;
-  const uint32_t kd = uint32_t(key), ka = uint32_t(key >> 32);
-  uint32_t m = 0;
-#pragma unroll
-  for (int o = 0; o < 7; ++o) m |= uint32_t(nd[o] == kd && na[o] == ka) << o;
-  emask[v] = uint8_t(m);
 }
 
 bool g_consts_ready[64] = {};
@@ -642,7 +969,11 @@ bool g_consts_ready[64] = {};
 
 // Host driver of the fused pipeline. Returns false when the dims are outside
 // the fused path's envelope (then the caller uses the staged kernels).
-bool fused_supported(const Grid& g) { return g.n < (int64_t(1) << 32) - 1; }
+bool fused_supported(const Grid& g) {
+  // u32 vertex ids, and u32 brick-major cell indices (bricks padded to 32^3)
+  const int64_t bricks = ((g.X + TX - 1) / TX) * ((g.Y + TY - 1) / TY) * ((g.Z + TZ - 1) / TZ);
+  return g.n < (int64_t(1) << 32) - 1 && bricks * TN <= (int64_t(1) << 32);
+}
 
 FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* desc, uint32_t* asc, uint32_t* ms) {
   FusedOut o{};
@@ -650,6 +981,16 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
   if (c.device >= 0 && c.device < 64 && !g_consts_ready[c.device]) {
     CK(cudaFuncSetAttribute(k_tile_segment<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kASmem));
     CK(cudaFuncSetAttribute(k_tile_segment<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kASmem));
+    CK(cudaFuncSetAttribute(k_brick<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            int(kRing * LQ * sizeof(unsigned long long))));
+    CK(cudaFuncSetAttribute(k_brick<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            int(kRing * LQ * sizeof(uint32_t))));
+    CK(cudaFuncSetAttribute(k_brick<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            int(kRing * LQ * sizeof(uint32_t))));
+    CK(cudaFuncSetAttribute(k_brick<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            int(kRing * LQ * sizeof(uint32_t))));
+    CK(cudaMemcpyToSymbol(c_mrows, kTetRowsPacked, sizeof(kTetRowsPacked)));
+    CK(cudaMemcpyToSymbol(c_mcases, kTetCasePacked, sizeof(kTetCasePacked)));
     g_consts_ready[c.device] = true;
   }
   FDims d;
@@ -696,21 +1037,26 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
   char* ctr_base = static_cast<char*>(c.get(S_FLAGS, 1024));
   ACounters* ctr = reinterpret_cast<ACounters*>(ctr_base);
   int* flag = reinterpret_cast<int*>(ctr_base + 128);
+  uint16_t* ltd = c.get_t<uint16_t>(S_LTD, ntiles * TN);
+  uint16_t* lta = c.get_t<uint16_t>(S_LTA, ntiles * TN);
+  uint4* TB = c.get_t<uint4>(S_TB, ntiles);
   for (int attempt = 0;; ++attempt) {
     const uint64_t ext_cap = c.fused_ext_cap ? c.fused_ext_cap : uint64_t(g.n / 4 + 1024);
     uint32_t* maxima = c.get_t<uint32_t>(S_MAXIMA, ext_cap);
     uint32_t* minima = c.get_t<uint32_t>(S_MINIMA, ext_cap);
-    const uint64_t exit_cap = c.fused_exit_cap ? c.fused_exit_cap : uint64_t(g.n / 4 + 1024);
-    uint32_t* E = c.get_t<uint32_t>(S_TMP0, exit_cap);
+    uint32_t* max_tt = c.get_t<uint32_t>(S_RANK_MAX, ext_cap);
+    uint32_t* min_tt = c.get_t<uint32_t>(S_RANK_MIN, ext_cap);
+    const uint64_t tt_cap = c.fused_exit_cap ? c.fused_exit_cap : uint64_t(g.n / 4 + 1024);
+    uint32_t* TT = c.get_t<uint32_t>(S_TMP0, tt_cap);
     CK(cudaMemsetAsync(ctr, 0, sizeof(ACounters), c.stream));
     CK(cudaMemsetAsync(&ctr->bad, 0xff, 4, c.stream));
     c.mark(0);
     if (use_tma)
-      k_tile_segment<true><<<unsigned(ntiles), A_THREADS, kASmem, c.stream>>>(tmap, field, d, desc, asc, maxima,
-                                                                           minima, ext_cap, E, exit_cap, ctr);
+      k_tile_segment<true><<<unsigned(ntiles), A_THREADS, kASmem, c.stream>>>(
+          tmap, field, d, maxima, minima, max_tt, min_tt, ext_cap, TT, tt_cap, TB, ltd, lta, ctr);
     else
-      k_tile_segment<false><<<unsigned(ntiles), A_THREADS, kASmem, c.stream>>>(tmap, field, d, desc, asc, maxima,
-                                                                            minima, ext_cap, E, exit_cap, ctr);
+      k_tile_segment<false><<<unsigned(ntiles), A_THREADS, kASmem, c.stream>>>(
+          tmap, field, d, maxima, minima, max_tt, min_tt, ext_cap, TT, tt_cap, TB, ltd, lta, ctr);
     CK_LAUNCH("k_tile_segment");
     c.mark(1);
     ACounters h;
@@ -720,8 +1066,8 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
     if (h.bad != 0xffffffffu)
       fail(PLMSS_ERR_INVALID_ARGUMENT, "non-finite scalar value at vertex " + std::to_string(h.bad));
     bool retry = false;
-    if (h.n_exit > exit_cap) {
-      c.fused_exit_cap = h.n_exit + h.n_exit / 4 + 1024;
+    if (h.n_tt > tt_cap) {
+      c.fused_exit_cap = h.n_tt + h.n_tt / 4 + 1024;
       retry = true;
     }
     if (h.n_max > ext_cap || h.n_min > ext_cap) {
@@ -736,87 +1082,153 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
     c.stats[1] = attempt;
     o.n_max = int64_t(h.n_max);
     o.n_min = int64_t(h.n_min);
-    // ---- B: exit graph to the fixpoint
+    const uint64_t nt = h.n_tt;
+    // ---- B: terminal-table forest -> final label of every table entry
+    uint32_t* SD = c.get_t<uint32_t>(S_SD, nt);
+    uint32_t* SA = c.get_t<uint32_t>(S_SA, nt);
+    k_tt_succ<<<unsigned(ntiles), 256, 0, c.stream>>>(TB, TT, ltd, lta, SD, SA);
+    CK_LAUNCH("k_tt_succ");
     o.sweeps = 0;
-    if (h.n_exit) {
-      for (;;) {
-        CK(cudaMemsetAsync(flag, 0, 4, c.stream));
-        k_exit_jump<<<blocks_for(h.n_exit, 256), 256, 0, c.stream>>>(E, h.n_exit, desc, asc, flag);
-        CK_LAUNCH("k_exit_jump");
-        ++o.sweeps;
-        CK(cudaMemcpyAsync(c.h_pinned, flag, 4, cudaMemcpyDeviceToHost, c.stream));
-        c.sync();
-        if (*reinterpret_cast<int*>(c.h_pinned) == 0) break;
-        if (o.sweeps > 64) fail(PLMSS_ERR_LOGIC, "exit graph did not converge");
-      }
-    }
-    c.mark(2);
-    // ---- extrema lists sorted ascending
-    for (int dir = 0; dir < 2; ++dir) {
-      uint32_t* list = dir ? minima : maxima;
-      const int64_t k = dir ? o.n_min : o.n_max;
-      if (k > 1) {
-        uint64_t* kk = c.get_t<uint64_t>(S_SORT_A, k);
-        uint64_t* vv = c.get_t<uint64_t>(S_SORT_B, k);
-        k_u32_to_u64<<<blocks_for(k, 256), 256, 0, c.stream>>>(list, k, kk, vv);
-        CK_LAUNCH("k_u32_to_u64");
-        int bits = 0;
-        while ((uint64_t(1) << bits) < uint64_t(g.n)) ++bits;
-        radix_sort_pairs(c, kk, vv, k, bits);
-        k_u64_to_u32<<<blocks_for(k, 256), 256, 0, c.stream>>>(kk, k, list);
-        CK_LAUNCH("k_u64_to_u32");
-      }
-    }
-    c.mark(3);
-    // ---- C: final pairs of all vertices -> unique, sorted -> dense ids
-    uint64_t fcap = 1024;
-    {
-      const uint64_t want = c.fused_pair_hint ? c.fused_pair_hint * 2 : uint64_t(1) << 20;
-      while (fcap < want) fcap <<= 1;
-    }
-    unsigned long long* fset = nullptr;
-    for (int tries = 0;; ++tries) {
-      fset = c.get_t<unsigned long long>(S_HASH_V, fcap);
-      CK(cudaMemsetAsync(fset, 0xff, fcap * 8, c.stream));
+    for (;;) {
       CK(cudaMemsetAsync(flag, 0, 4, c.stream));
-      k_mark_pairs<<<unsigned(std::min<int64_t>((g.n + 1023) / 1024, int64_t(c.sm_count) * 16)), 256, 0,
-                     c.stream>>>(d, desc, asc, fset, fcap - 1, flag);
-      CK_LAUNCH("k_mark_pairs");
+      k_tt_jump<<<blocks_for(int64_t(nt), 256), 256, 0, c.stream>>>(nt, SD, SA, flag);
+      CK_LAUNCH("k_tt_jump");
+      ++o.sweeps;
       CK(cudaMemcpyAsync(c.h_pinned, flag, 4, cudaMemcpyDeviceToHost, c.stream));
       c.sync();
       if (*reinterpret_cast<int*>(c.h_pinned) == 0) break;
-      if (fcap >= 4 * uint64_t(g.n) || tries > 8) fail(PLMSS_ERR_LOGIC, "region set overflow");
-      fcap <<= 2;
+      if (o.sweeps > 64) fail(PLMSS_ERR_LOGIC, "terminal forest did not converge");
     }
-    const int64_t fb = int64_t((fcap + kCTile - 1) / kCTile);
-    uint64_t* fcounts = c.get_t<uint64_t>(S_TMP2, fb);
-    k_count_occ<<<unsigned(fb), kCThreads, 0, c.stream>>>(fset, fcap, fcounts);
-    CK_LAUNCH("k_count_occ");
-    const int64_t R = int64_t(exclusive_scan_u64(c, fcounts, fb, true));
-    c.fused_pair_hint = uint64_t(R);
-    uint64_t* keys = c.get_t<uint64_t>(S_KEYS, R);
-    uint64_t* slots = c.get_t<uint64_t>(S_SORT_B, R);
-    k_write_occ<<<unsigned(fb), kCThreads, 0, c.stream>>>(fset, fcap, fcounts, keys, slots);
-    CK_LAUNCH("k_write_occ");
-    int kb = 32;
-    while ((uint64_t(1) << (kb - 32)) < uint64_t(g.n)) ++kb;
-    radix_sort_pairs(c, keys, slots, R, kb);
-    uint32_t* slot_id = c.get_t<uint32_t>(S_BITMAP, fcap);
-    k_set_ids<<<blocks_for(R, 256), 256, 0, c.stream>>>(slots, R, slot_id);
-    CK_LAUNCH("k_set_ids");
+    c.mark(2);
+    // ---- extrema lists sorted ascending; rank of every extremum table entry
+    uint32_t* RK = c.get_t<uint32_t>(S_RK, nt);
+    for (int dir = 0; dir < 2; ++dir) {
+      uint32_t* list = dir ? minima : maxima;
+      const uint32_t* ltt = dir ? min_tt : max_tt;
+      const int64_t k = dir ? o.n_min : o.n_max;
+      if (k < 1) continue;
+      uint64_t* kk = c.get_t<uint64_t>(S_SORT_A, k);
+      uint64_t* vv = c.get_t<uint64_t>(S_SORT_B, k);
+      k_list_pairs<<<blocks_for(k, 256), 256, 0, c.stream>>>(list, ltt, k, kk, vv);
+      CK_LAUNCH("k_list_pairs");
+      if (k > 1) {
+        int bits = 0;
+        while ((uint64_t(1) << bits) < uint64_t(g.n)) ++bits;
+        radix_sort_pairs(c, kk, vv, k, bits);
+      }
+      k_rank_lists<<<blocks_for(k, 256), 256, 0, c.stream>>>(kk, vv, k, list, RK);
+      CK_LAUNCH("k_rank_lists");
+    }
+    k_tt_final<<<blocks_for(int64_t(nt), 256), 256, 0, c.stream>>>(nt, RK, SD, SA);
+    CK_LAUNCH("k_tt_final");
+    c.mark(3);
+    // ---- C: region keys + separator counts per 32-cube chunk
+    BrickArgs ba{};
+    ba.d = d;
+    ba.nxc = uint32_t((g.X - 1 + 31) / 32);
+    ba.TB = TB;
+    ba.ltd = ltd;
+    ba.lta = lta;
+    ba.FD = SD;
+    ba.FA = SA;
+    ba.maxs = maxima;
+    ba.mins = minima;
+    ba.nmax = uint32_t(o.n_max);
+    ba.desc = desc;
+    ba.asc = asc;
+    ba.ms = ms;
+    ba.overflow = flag;
+    const uint64_t nchunks = uint64_t(ba.nxc) * uint64_t(g.Y - 1) * uint64_t(g.Z - 1);
+    uint64_t* chunk = c.get_t<uint64_t>(S_TMP1, nchunks ? nchunks : 1);
+    ba.chunk = chunk;
+    const uint64_t nbits = uint64_t(o.n_max) * uint64_t(o.n_min);
+    const bool dense = nbits < (uint64_t(1) << 32) && c.combine_path != 2;  // PLMSS_OPT_COMBINE_PATH 2: hash
+    const size_t smem_c = kRing * LQ * (dense ? sizeof(uint32_t) : sizeof(unsigned long long));
+    const size_t smem_d = kRing * LQ * sizeof(uint32_t);
+    uint64_t* keys = nullptr;
+    int64_t R = 0;
+    if (dense) {
+      // rank-product bitmap: no hashing, ids by prefix popcount
+      const uint64_t nw = (nbits + 31) / 32;
+      uint32_t* bitmap = c.get_t<uint32_t>(S_BITMAP, nw);
+      CK(cudaMemsetAsync(bitmap, 0, nw * 4, c.stream));
+      ba.bitmap = bitmap;
+      k_brick<false, true><<<unsigned(ntiles), 1024, smem_c, c.stream>>>(ba);
+      CK_LAUNCH("k_brick<count>");
+      const int64_t nb = int64_t((nw + kWB - 1) / kWB);
+      uint64_t* bsum = c.get_t<uint64_t>(S_HASH_V, nb);
+      k_bitmap_count<<<unsigned(nb), 256, 0, c.stream>>>(bitmap, nw, bsum);
+      CK_LAUNCH("k_bitmap_count");
+      R = int64_t(exclusive_scan_u64(c, bsum, nb, true));
+      keys = c.get_t<uint64_t>(S_KEYS, R);
+      uint32_t* prefix = c.get_t<uint32_t>(S_HASH_K, nw);
+      k_bitmap_ids<<<unsigned(nb), kWB, 0, c.stream>>>(bitmap, nw, bsum, ba.nmax, maxima, minima, prefix, keys);
+      CK_LAUNCH("k_bitmap_ids");
+      ba.prefix = prefix;
+      c.stats[2] = -int64_t(nw);
+    } else {
+      uint64_t fcap = 1024;
+      {
+        const uint64_t want = c.fused_pair_hint ? c.fused_pair_hint * 2 : uint64_t(1) << 20;
+        while (fcap < want) fcap <<= 1;
+      }
+      unsigned long long* fset = nullptr;
+      for (int tries = 0;; ++tries) {
+        fset = c.get_t<unsigned long long>(S_HASH_V, fcap);
+        CK(cudaMemsetAsync(fset, 0xff, fcap * 8, c.stream));
+        CK(cudaMemsetAsync(flag, 0, 4, c.stream));
+        ba.fset = fset;
+        ba.fmask = fcap - 1;
+        k_brick<false, false><<<unsigned(ntiles), 1024, smem_c, c.stream>>>(ba);
+        CK_LAUNCH("k_brick<count>");
+        CK(cudaMemcpyAsync(c.h_pinned, flag, 4, cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
+        if (*reinterpret_cast<int*>(c.h_pinned) == 0) break;
+        if (fcap >= 4 * uint64_t(g.n) || tries > 8) fail(PLMSS_ERR_LOGIC, "region set overflow");
+        fcap <<= 2;
+      }
+      const int64_t fb = int64_t((fcap + kCTile - 1) / kCTile);
+      uint64_t* fcounts = c.get_t<uint64_t>(S_TMP2, fb);
+      k_count_occ<<<unsigned(fb), kCThreads, 0, c.stream>>>(fset, fcap, fcounts);
+      CK_LAUNCH("k_count_occ");
+      R = int64_t(exclusive_scan_u64(c, fcounts, fb, true));
+      c.fused_pair_hint = uint64_t(R);
+      keys = c.get_t<uint64_t>(S_KEYS, R);
+      uint64_t* slots = c.get_t<uint64_t>(S_SORT_B, R);
+      k_write_occ<<<unsigned(fb), kCThreads, 0, c.stream>>>(fset, fcap, fcounts, keys, slots);
+      CK_LAUNCH("k_write_occ");
+      int kb = 32;
+      while ((uint64_t(1) << (kb - 32)) < uint64_t(std::max(o.n_min, int64_t(1)))) ++kb;
+      radix_sort_pairs(c, keys, slots, R, kb);
+      uint32_t* slot_id = c.get_t<uint32_t>(S_BITMAP, fcap);
+      k_set_ids<<<blocks_for(R, 256), 256, 0, c.stream>>>(slots, R, slot_id);
+      CK_LAUNCH("k_set_ids");
+      k_keys_to_gid<<<blocks_for(R, 256), 256, 0, c.stream>>>(keys, R, maxima, minima);
+      CK_LAUNCH("k_keys_to_gid");
+      ba.fset = fset;
+      ba.fmask = fcap - 1;
+      ba.slot_id = slot_id;
+      c.stats[2] = int64_t(fcap);
+    }
     o.n_regions = R;
-    c.stats[2] = int64_t(fcap);
-    // ---- D1: dense MS ids per vertex
-    uint8_t* emask = c.get_t<uint8_t>(S_MASK, g.n + 64);
-    {
-      const unsigned grid = unsigned((g.X + 255) / 256 * g.Y * g.Z);
-      k_assign_ms<<<grid, 256, 0, c.stream>>>(d.X, d.Y, d.Z, desc, asc, fset, fcap - 1, slot_id, ms, emask);
-    }
-    CK_LAUNCH("k_assign_ms");
+    const uint64_t total = nchunks ? exclusive_scan_u64(c, chunk, int64_t(nchunks), true) : 0;
     c.mark(4);
-    // ---- D2: ordered marching (count, scan, emit)
-    o.n_tris = fused_march(c, g, ms, emask, &o.tris);
+    // ---- D: labels, ids, separator records
+    plmss_tri* tris = c.get_t<plmss_tri>(S_TRIS, total ? total : 1);
+    ba.total = total;
+    ba.out = tris;
+    CK(cudaMemsetAsync(flag, 0, 4, c.stream));
+    if (dense)
+      k_brick<true, true><<<unsigned(ntiles), 1024, smem_d, c.stream>>>(ba);
+    else
+      k_brick<true, false><<<unsigned(ntiles), 1024, smem_d, c.stream>>>(ba);
+    CK_LAUNCH("k_brick<emit>");
+    CK(cudaMemcpyAsync(c.h_pinned, flag, 4, cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    if (*reinterpret_cast<int*>(c.h_pinned) != 0) fail(PLMSS_ERR_LOGIC, "region pair missing from the region set");
     c.mark(5);
+    o.n_tris = int64_t(total);
+    o.tris = tris;
     o.maxima = maxima;
     o.minima = minima;
     o.keys = keys;

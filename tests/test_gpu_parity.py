@@ -245,20 +245,27 @@ def test_compute_order(plmss, gpu, restatement):
 
 
 # ------------------------------------------------------- fused pipeline --
-@pytest.mark.parametrize("path", [0, 1])
+# path: 0 fused (dense rank-product region bitmap), 1 staged kernels,
+#       2 fused with the hash-set region keys (the path for n_max * n_min >= 2^32)
+@pytest.mark.parametrize("path", [0, 1, 2])
 @pytest.mark.parametrize("name", golden_cases())
 def test_pipeline_matches_reference(plmss, gpu, name, path):
     g = load_case(name)
     dims = tuple(int(x) for x in g["dims"])
-    gpu.set_option(2, path)  # 0 fused tile pipeline, 1 staged kernels
+    gpu.set_option(2, 1 if path == 1 else 0)  # PIPELINE_PATH: 0 fused, 1 staged
+    gpu.set_option(1, 2 if path == 2 else 0)  # COMBINE_PATH: 2 hash
     try:
         res = plmss.pipeline(dims, dev(g["field"]), ctx=gpu)
     finally:
         gpu.set_option(2, 0)
+        gpu.set_option(1, 0)
     out = plmss.fetch(gpu, res)
     for k, gk in (("desc", "desc"), ("asc", "asc"), ("ms", "ms_region"), ("maxima", "maxima"), ("minima", "minima")):
         assert np.array_equal(u32(out[k]), g[gk]), k
     assert res.n_regions == len(g["region_keys"]) and res.n_tris == int(g["sep_n"])
+    keys = out["region_keys"].cpu().numpy().astype(np.uint64)
+    assert np.array_equal((keys >> np.uint64(32)).astype(np.int64), g["region_keys"][:, 0])
+    assert np.array_equal((keys & np.uint64(0xFFFFFFFF)).astype(np.int64), g["region_keys"][:, 1])
     m = plmss.materialize_separators(dims, out["tris"], ctx=gpu)
     for k in ("points", "regions", "source_cells"):
         assert sha(m[k].cpu().numpy()) == str(g[f"sep_{k}_sha256"]), k
