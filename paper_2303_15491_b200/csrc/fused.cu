@@ -703,7 +703,10 @@ __global__ void k_set_ids(const uint64_t* __restrict__ sorted_slots, int64_t r, 
 // brick's table. Then warp w handles cube row y = w of each cube layer whose
 // two vertex layers are present, lane = cube x (one 32-cube chunk of the
 // reference cell order).
-constexpr int LW = TX + 1, LQ = LW * (TY + 1);  // 33, 1089 vertices per layer
+// A CTA takes half a brick: RY = 16 cube rows (warp w <-> row w), so two
+// CTAs share an SM and one's barriers overlap the other's work.
+constexpr int RY = 16, B_THREADS = 32 * RY;
+constexpr int LW = TX + 1, LQ = LW * (RY + 1);  // 33 x 17 = 561 vertices per layer
 constexpr int kBatch = 4, kRing = kBatch + 1;
 __constant__ uint32_t c_mrows[PLMSS_TET_ROWS];
 __constant__ uint16_t c_mcases[32];
@@ -768,19 +771,33 @@ struct BrickArgs {
 // kDense: region keys are u32 rank products in a bitmap, else u64 rank pairs
 // in the hash set.
 template <bool kEmit, bool kDense>
-__global__ void __launch_bounds__(1024, 1) k_brick(const BrickArgs a) {
+__global__ void __launch_bounds__(B_THREADS, 2) k_brick(const BrickArgs a) {
   using Key = typename std::conditional<kDense, uint32_t, unsigned long long>::type;
   using Lab = typename std::conditional<kEmit, uint32_t, Key>::type;
   extern __shared__ __align__(16) unsigned char b_smem[];
   Lab* ring = reinterpret_cast<Lab*>(b_smem);  // kRing x LQ
   __shared__ uint16_t s_tlut[64], s_cases[32];
   __shared__ uint32_t s_rows[PLMSS_TET_ROWS];
+  __shared__ uint32_t s_two_code[128];  // two-label cubes: corner membership -> 6 tet codes
+  __shared__ uint8_t s_two_cnt[128];    // ... -> separator count
   const FDims& d = a.d;
-  const uint32_t bt = blockIdx.x;
+  const uint32_t bt = blockIdx.x >> 1, yb = (blockIdx.x & 1) * RY;  // brick, first row of the half
   const uint32_t tx = bt % d.tx, ty = (bt / d.tx) % d.ty, tz = bt / (d.tx * d.ty);
-  const uint32_t gx0 = tx * TX, gy0 = ty * TY, gz0 = tz * TZ;
+  const uint32_t gx0 = tx * TX, gy0 = ty * TY + yb, gz0 = tz * TZ;
+  if (gy0 >= d.Y) return;  // upper half of a brick cut by the volume
   const int tid = int(threadIdx.x), lane = tid & 31, w = tid >> 5;
   load_march_tables(s_tlut, s_cases, s_rows);
+  __syncthreads();
+  if (tid < 128) {
+    // corner i carries label 0 when bit i of m8 is set (bit 0 always is)
+    const uint32_t m8 = uint32_t(tid) << 1 | 1u;
+    uint32_t lab[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) lab[i] = (m8 >> i) & 1u ? 0u : 1u;
+    uint32_t cnt;
+    s_two_code[tid] = cube_codes(lab, s_tlut, cnt);
+    s_two_cnt[tid] = uint8_t(cnt);
+  }
   const uint32_t* TBw = reinterpret_cast<const uint32_t*>(a.TB);
   const int nl = int(min(uint32_t(TZ + 1), d.Z - gz0));  // vertex layers of the brick + halo
   // this thread's cube column: x = lane, y = w
@@ -796,45 +813,66 @@ __global__ void __launch_bounds__(1024, 1) k_brick(const BrickArgs a) {
 
   for (int z0 = 0; z0 < nl; z0 += kBatch) {
     const int zn = min(kBatch, nl - z0);
-    // ---- load layers z0 .. z0+zn-1 (threads 0..64 also take q = 1024..1088)
-    auto load_column = [&](const int q, Key& lkey, uint32_t& lid, uint2& lgv) {
+    // ---- load layers z0 .. z0+zn-1 (threads 0..48 also take q = 512..560)
+    // full: kBatch layers, all below the halo layer 32 (no predication)
+    auto load_column = [&](auto full, const int q, Key& lkey, uint32_t& lid, uint2& lgv) {
+      constexpr bool kFull = decltype(full)::value;
       const int x = q % LW, y = q / LW;
       const uint32_t gx = gx0 + uint32_t(x), gy = gy0 + uint32_t(y);
       if (gx >= d.X || gy >= d.Y) {
 #pragma unroll
         for (int i = 0; i < kBatch; ++i)
-          if (i < zn) ring[((z0 + i) % kRing) * LQ + q] = kNone;
+          if (kFull || i < zn) ring[((z0 + i) % kRing) * LQ + q] = kNone;
         return;
       }
-      const uint32_t nb_lo = (tx + uint32_t(x >> 5)) + d.tx * ((ty + uint32_t(y >> 5)) + d.ty * tz);
+      const uint32_t yy = yb + uint32_t(y);  // row within the brick (32: next brick)
+      const uint32_t nb_lo = (tx + uint32_t(x >> 5)) + d.tx * ((ty + (yy >> 5)) + d.ty * tz);
       const uint32_t nb_hi = nb_lo + d.tx * d.ty;  // layer 32 lives in the next brick up
-      const uint32_t lxy = uint32_t(x & 31) | uint32_t(y & 31) << 5;
+      const uint32_t lxy = uint32_t(x & 31) | (yy & 31) << 5;
       uint32_t ld[kBatch], la[kBatch];
+      if (kFull) {
+        const uint16_t* pd = a.ltd + ((size_t(nb_lo) << 15) | lxy | uint32_t(z0) << 10);
+        const uint16_t* pa = a.lta + ((size_t(nb_lo) << 15) | lxy | uint32_t(z0) << 10);
 #pragma unroll
-      for (int i = 0; i < kBatch; ++i) {
-        const int z = z0 + i;
-        if (i < zn) {
-          const uint32_t bm = ((z < TZ ? nb_lo : nb_hi) << 15) | lxy | uint32_t(z & 31) << 10;
-          ld[i] = __ldg(a.ltd + bm);
-          la[i] = __ldg(a.lta + bm);
+        for (int i = 0; i < kBatch; ++i) {
+          ld[i] = __ldg(pd + i * TX * TY);
+          la[i] = __ldg(pa + i * TX * TY);
+        }
+        const uint32_t base = __ldg(TBw + 4 * nb_lo);
+        const uint32_t* fd = a.FD + base;
+        const uint32_t* fa = a.FA + base;
+#pragma unroll
+        for (int i = 0; i < kBatch; ++i) {
+          ld[i] = __ldg(fd + ld[i]);  // table entry replaces the index
+          la[i] = __ldg(fa + la[i]);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < kBatch; ++i) {
+          const int z = z0 + i;
+          if (i < zn) {
+            const uint32_t bm = ((z < TZ ? nb_lo : nb_hi) << 15) | lxy | uint32_t(z & 31) << 10;
+            ld[i] = __ldg(a.ltd + bm);
+            la[i] = __ldg(a.lta + bm);
+          }
+        }
+        const uint32_t base_lo = __ldg(TBw + 4 * nb_lo);
+        const uint32_t base_hi = z0 + zn > TZ ? __ldg(TBw + 4 * nb_hi) : 0u;
+#pragma unroll
+        for (int i = 0; i < kBatch; ++i) {
+          if (i < zn) {
+            const uint32_t base = z0 + i < TZ ? base_lo : base_hi;
+            ld[i] = __ldg(a.FD + base + ld[i]);
+            la[i] = __ldg(a.FA + base + la[i]);
+          }
         }
       }
-      const uint32_t base_lo = __ldg(TBw + 4 * nb_lo);
-      const uint32_t base_hi = z0 + zn > TZ ? __ldg(TBw + 4 * nb_hi) : 0u;
 #pragma unroll
       for (int i = 0; i < kBatch; ++i) {
-        if (i < zn) {
-          const uint32_t base = z0 + i < TZ ? base_lo : base_hi;
-          ld[i] = __ldg(a.FD + base + ld[i]);  // table entry replaces the index
-          la[i] = __ldg(a.FA + base + la[i]);
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < kBatch; ++i) {
-        if (i >= zn) break;
+        if (!kFull && i >= zn) break;
         const int z = z0 + i;
         const Key key = kDense ? Key(la[i] * a.nmax + ld[i]) : Key((uint64_t(la[i]) << 32) | ld[i]);
-        const bool own = x < TX && y < TY && z < TZ;
+        const bool own = x < TX && y < RY && (kFull || z < TZ);
         Lab* L = ring + (z % kRing) * LQ;
         if (!kEmit) {
           // distinct pairs of the owned vertices -> region bitmap / set
@@ -874,8 +912,13 @@ __global__ void __launch_bounds__(1024, 1) k_brick(const BrickArgs a) {
         }
       }
     };
-    load_column(tid, lkey0, lid0, lgv0);
-    if (tid < LQ - 1024) load_column(tid + 1024, lkey1, lid1, lgv1);
+    if (zn == kBatch && z0 + kBatch <= TZ) {
+      load_column(std::true_type{}, tid, lkey0, lid0, lgv0);
+      if (tid < LQ - B_THREADS) load_column(std::true_type{}, tid + B_THREADS, lkey1, lid1, lgv1);
+    } else {
+      load_column(std::false_type{}, tid, lkey0, lid0, lgv0);
+      if (tid < LQ - B_THREADS) load_column(std::false_type{}, tid + B_THREADS, lkey1, lid1, lgv1);
+    }
     // D: this warp's chunk offsets for the batch's cube layers (lane i <->
     // vertex layer z0 + i, cube layer z0 + i - 1)
     uint64_t pre_off = 0;
@@ -898,9 +941,26 @@ __global__ void __launch_bounds__(1024, 1) k_brick(const BrickArgs a) {
         c[5] = cur[o + 1];
         c[6] = cur[o + LW];
         c[7] = cur[o + LW + 1];
-        const bool uni = c[1] == c[0] && c[2] == c[0] && c[3] == c[0] && c[4] == c[0] && c[5] == c[0] &&
-                         c[6] == c[0] && c[7] == c[0];
-        if (!uni) code6 = cube_codes(c, s_tlut, cnt);
+        // corners equal to corner 0 (bit i); 0xff: one region, no separator
+        uint32_t m8 = 1u;
+#pragma unroll
+        for (int i = 1; i < 8; ++i) m8 |= uint32_t(c[i] == c[0]) << i;
+        if (m8 != 0xffu) {
+          // the lowest corner with another label; two labels iff every
+          // corner carries one of the two (the common case on a separator)
+          Lab b = c[7];
+#pragma unroll
+          for (int i = 6; i >= 1; --i) b = (m8 >> i) & 1u ? b : c[i];
+          uint32_t mb = 0u;
+#pragma unroll
+          for (int i = 1; i < 8; ++i) mb |= uint32_t(c[i] == b) << i;
+          if ((m8 | mb) == 0xffu) {
+            code6 = s_two_code[m8 >> 1];
+            cnt = s_two_cnt[m8 >> 1];
+          } else {
+            code6 = cube_codes(c, s_tlut, cnt);
+          }
+        }
       }
       const uint32_t cz = gz0 + uint32_t(z) - 1;
       if (!kEmit) {
@@ -1153,7 +1213,7 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
       uint32_t* bitmap = c.get_t<uint32_t>(S_BITMAP, nw);
       CK(cudaMemsetAsync(bitmap, 0, nw * 4, c.stream));
       ba.bitmap = bitmap;
-      k_brick<false, true><<<unsigned(ntiles), 1024, smem_c, c.stream>>>(ba);
+      k_brick<false, true><<<unsigned(2 * ntiles), B_THREADS, smem_c, c.stream>>>(ba);
       CK_LAUNCH("k_brick<count>");
       const int64_t nb = int64_t((nw + kWB - 1) / kWB);
       uint64_t* bsum = c.get_t<uint64_t>(S_HASH_V, nb);
@@ -1179,7 +1239,7 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
         CK(cudaMemsetAsync(flag, 0, 4, c.stream));
         ba.fset = fset;
         ba.fmask = fcap - 1;
-        k_brick<false, false><<<unsigned(ntiles), 1024, smem_c, c.stream>>>(ba);
+        k_brick<false, false><<<unsigned(2 * ntiles), B_THREADS, smem_c, c.stream>>>(ba);
         CK_LAUNCH("k_brick<count>");
         CK(cudaMemcpyAsync(c.h_pinned, flag, 4, cudaMemcpyDeviceToHost, c.stream));
         c.sync();
@@ -1219,9 +1279,9 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
     ba.out = tris;
     CK(cudaMemsetAsync(flag, 0, 4, c.stream));
     if (dense)
-      k_brick<true, true><<<unsigned(ntiles), 1024, smem_d, c.stream>>>(ba);
+      k_brick<true, true><<<unsigned(2 * ntiles), B_THREADS, smem_d, c.stream>>>(ba);
     else
-      k_brick<true, false><<<unsigned(ntiles), 1024, smem_d, c.stream>>>(ba);
+      k_brick<true, false><<<unsigned(2 * ntiles), B_THREADS, smem_d, c.stream>>>(ba);
     CK_LAUNCH("k_brick<emit>");
     CK(cudaMemcpyAsync(c.h_pinned, flag, 4, cudaMemcpyDeviceToHost, c.stream));
     c.sync();
