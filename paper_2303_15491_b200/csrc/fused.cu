@@ -703,9 +703,9 @@ __global__ void k_set_ids(const uint64_t* __restrict__ sorted_slots, int64_t r, 
 // brick's table. Then warp w handles cube row y = w of each cube layer whose
 // two vertex layers are present, lane = cube x (one 32-cube chunk of the
 // reference cell order).
-// A CTA takes half a brick: RY = 16 cube rows (warp w <-> row w), so two
-// CTAs share an SM and one's barriers overlap the other's work.
-constexpr int RY = 16, B_THREADS = 32 * RY;
+// A CTA takes RY = 4 cube rows of a brick (warp w <-> row w): small CTAs,
+// many per SM, so one CTA's barriers overlap the others' work.
+constexpr int RY = 4, B_THREADS = 32 * RY;
 constexpr int LW = TX + 1, LQ = LW * (RY + 1);  // 33 x 17 = 561 vertices per layer
 constexpr int kBatch = 4, kRing = kBatch + 1;
 __constant__ uint32_t c_mrows[PLMSS_TET_ROWS];
@@ -771,7 +771,7 @@ struct BrickArgs {
 // kDense: region keys are u32 rank products in a bitmap, else u64 rank pairs
 // in the hash set.
 template <bool kEmit, bool kDense>
-__global__ void __launch_bounds__(B_THREADS, 2) k_brick(const BrickArgs a) {
+__global__ void __launch_bounds__(B_THREADS, 8) k_brick(const BrickArgs a) {
   using Key = typename std::conditional<kDense, uint32_t, unsigned long long>::type;
   using Lab = typename std::conditional<kEmit, uint32_t, Key>::type;
   extern __shared__ __align__(16) unsigned char b_smem[];
@@ -781,7 +781,7 @@ __global__ void __launch_bounds__(B_THREADS, 2) k_brick(const BrickArgs a) {
   __shared__ uint32_t s_two_code[128];  // two-label cubes: corner membership -> 6 tet codes
   __shared__ uint8_t s_two_cnt[128];    // ... -> separator count
   const FDims& d = a.d;
-  const uint32_t bt = blockIdx.x >> 1, yb = (blockIdx.x & 1) * RY;  // brick, first row of the half
+  const uint32_t bt = blockIdx.x / (TY / RY), yb = (blockIdx.x % (TY / RY)) * RY;  // brick, first row of this CTA's rows
   const uint32_t tx = bt % d.tx, ty = (bt / d.tx) % d.ty, tz = bt / (d.tx * d.ty);
   const uint32_t gx0 = tx * TX, gy0 = ty * TY + yb, gz0 = tz * TZ;
   if (gy0 >= d.Y) return;  // upper half of a brick cut by the volume
@@ -813,7 +813,7 @@ __global__ void __launch_bounds__(B_THREADS, 2) k_brick(const BrickArgs a) {
 
   for (int z0 = 0; z0 < nl; z0 += kBatch) {
     const int zn = min(kBatch, nl - z0);
-    // ---- load layers z0 .. z0+zn-1 (threads 0..48 also take q = 512..560)
+    // ---- load layers z0 .. z0+zn-1 (threads 0..LQ-B_THREADS-1 also take a second q)
     // full: kBatch layers, all below the halo layer 32 (no predication)
     auto load_column = [&](auto full, const int q, Key& lkey, uint32_t& lid, uint2& lgv) {
       constexpr bool kFull = decltype(full)::value;
@@ -1213,7 +1213,7 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
       uint32_t* bitmap = c.get_t<uint32_t>(S_BITMAP, nw);
       CK(cudaMemsetAsync(bitmap, 0, nw * 4, c.stream));
       ba.bitmap = bitmap;
-      k_brick<false, true><<<unsigned(2 * ntiles), B_THREADS, smem_c, c.stream>>>(ba);
+      k_brick<false, true><<<unsigned((TY / RY) * ntiles), B_THREADS, smem_c, c.stream>>>(ba);
       CK_LAUNCH("k_brick<count>");
       const int64_t nb = int64_t((nw + kWB - 1) / kWB);
       uint64_t* bsum = c.get_t<uint64_t>(S_HASH_V, nb);
@@ -1239,7 +1239,7 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
         CK(cudaMemsetAsync(flag, 0, 4, c.stream));
         ba.fset = fset;
         ba.fmask = fcap - 1;
-        k_brick<false, false><<<unsigned(2 * ntiles), B_THREADS, smem_c, c.stream>>>(ba);
+        k_brick<false, false><<<unsigned((TY / RY) * ntiles), B_THREADS, smem_c, c.stream>>>(ba);
         CK_LAUNCH("k_brick<count>");
         CK(cudaMemcpyAsync(c.h_pinned, flag, 4, cudaMemcpyDeviceToHost, c.stream));
         c.sync();
@@ -1279,9 +1279,9 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
     ba.out = tris;
     CK(cudaMemsetAsync(flag, 0, 4, c.stream));
     if (dense)
-      k_brick<true, true><<<unsigned(2 * ntiles), B_THREADS, smem_d, c.stream>>>(ba);
+      k_brick<true, true><<<unsigned((TY / RY) * ntiles), B_THREADS, smem_d, c.stream>>>(ba);
     else
-      k_brick<true, false><<<unsigned(2 * ntiles), B_THREADS, smem_d, c.stream>>>(ba);
+      k_brick<true, false><<<unsigned((TY / RY) * ntiles), B_THREADS, smem_d, c.stream>>>(ba);
     CK_LAUNCH("k_brick<emit>");
     CK(cudaMemcpyAsync(c.h_pinned, flag, 4, cudaMemcpyDeviceToHost, c.stream));
     c.sync();
