@@ -780,6 +780,8 @@ __global__ void __launch_bounds__(B_THREADS, 8) k_brick(const BrickArgs a) {
   __shared__ uint32_t s_rows[PLMSS_TET_ROWS];
   __shared__ uint32_t s_two_code[128];  // two-label cubes: corner membership -> 6 tet codes
   __shared__ uint8_t s_two_cnt[128];    // ... -> separator count
+  // ... -> its records in order: tet << 8 | recipe row (at most 2 per tet)
+  __shared__ uint16_t s_two_rec[kEmit ? 128 : 1][kEmit ? 12 : 1];
   const FDims& d = a.d;
   const uint32_t bt = blockIdx.x / (TY / RY), yb = (blockIdx.x % (TY / RY)) * RY;  // brick, first row of this CTA's rows
   const uint32_t tx = bt % d.tx, ty = (bt / d.tx) % d.ty, tz = bt / (d.tx * d.ty);
@@ -795,8 +797,16 @@ __global__ void __launch_bounds__(B_THREADS, 8) k_brick(const BrickArgs a) {
 #pragma unroll
     for (int i = 0; i < 8; ++i) lab[i] = (m8 >> i) & 1u ? 0u : 1u;
     uint32_t cnt;
-    s_two_code[tid] = cube_codes(lab, s_tlut, cnt);
+    const uint32_t code6 = cube_codes(lab, s_tlut, cnt);
+    s_two_code[tid] = code6;
     s_two_cnt[tid] = uint8_t(cnt);
+    if (kEmit) {
+      uint32_t r = 0;
+      for (int t = 0; t < 6; ++t) {
+        const uint32_t cs = s_cases[(code6 >> (5 * t)) & 31];
+        for (uint32_t k = 0; k < (cs & 15); ++k) s_two_rec[tid][r++] = uint16_t(uint32_t(t) << 8 | ((cs >> 4) + k));
+      }
+    }
   }
   const uint32_t* TBw = reinterpret_cast<const uint32_t*>(a.TB);
   const int nl = int(min(uint32_t(TZ + 1), d.Z - gz0));  // vertex layers of the brick + halo
@@ -931,6 +941,7 @@ __global__ void __launch_bounds__(B_THREADS, 8) k_brick(const BrickArgs a) {
       const Lab* cur = ring + (z % kRing) * LQ;
       const int o = w * LW + lane;
       uint32_t cnt = 0, code6 = 0;
+      uint32_t lo2 = 0, hi2 = 0;  // D, two-label cubes: the two ids (bit 31 of code6 marks the case)
       if (cube_ok) {
         Lab c[8];
         c[0] = lo[o];
@@ -955,8 +966,14 @@ __global__ void __launch_bounds__(B_THREADS, 8) k_brick(const BrickArgs a) {
 #pragma unroll
           for (int i = 1; i < 8; ++i) mb |= uint32_t(c[i] == b) << i;
           if ((m8 | mb) == 0xffu) {
-            code6 = s_two_code[m8 >> 1];
             cnt = s_two_cnt[m8 >> 1];
+            if (kEmit) {
+              code6 = 0x80000000u | m8;
+              lo2 = min(uint32_t(c[0]), uint32_t(b));
+              hi2 = max(uint32_t(c[0]), uint32_t(b));
+            } else {
+              code6 = s_two_code[m8 >> 1];
+            }
           } else {
             code6 = cube_codes(c, s_tlut, cnt);
           }
@@ -989,8 +1006,17 @@ __global__ void __launch_bounds__(B_THREADS, 8) k_brick(const BrickArgs a) {
         }
         const uint32_t c6 = __shfl_sync(0xffffffffu, code6, src & 31);
         const uint32_t ex = __shfl_sync(0xffffffffu, inc - cnt, src & 31);
+        const uint32_t l2 = __shfl_sync(0xffffffffu, lo2, src & 31);
+        const uint32_t h2 = __shfl_sync(0xffffffffu, hi2, src & 31);
         if (j >= T) continue;
         uint32_t k = j - ex;
+        if (c6 >> 31) {
+          // two-label cube: record list from the table, one region pair
+          const uint32_t e = s_two_rec[(c6 & 0xffu) >> 1][k];
+          const uint64_t cr64 = ((6ull * (q0 + uint32_t(src)) + (e >> 8)) << 6) | uint64_t(e & 0xffu);
+          *reinterpret_cast<uint4*>(a.out + base + j) = make_uint4(uint32_t(cr64), uint32_t(cr64 >> 32), l2, h2);
+          continue;
+        }
         int t = 0;
         uint32_t cs = s_cases[c6 & 31];
 #pragma unroll
