@@ -44,11 +44,12 @@ B_PER_TRI = 16
 # Per-stage algorithmic bytes per vertex.
 STAGES = ["tile_segment", "exit_resolve", "extrema_sort", "finalize_ids", "march"]
 # Compulsory bytes per vertex of each fused stage: tile_segment
-# reads f, writes the two partial-label arrays; finalize_ids reads the partial
-# labels, writes final desc/asc, reads them again and writes ms; march reads
-# ms and writes 16 B per separator triangle.
-STAGE_BYTES_PER_VERTEX = {"tile_segment": 12, "exit_resolve": 0, "extrema_sort": 0, "finalize_ids": 28,
-                          "march": 4}
+# reads f and writes the two u16 terminal-index arrays; exit_resolve and
+# extrema_sort touch only the terminal tables (~0.12 entries per vertex);
+# finalize_ids (pass C) reads the terminal indices; march (pass D) reads them
+# again and writes desc, asc, ms (+ 16 B per separator triangle).
+STAGE_BYTES_PER_VERTEX = {"tile_segment": 8, "exit_resolve": 0, "extrema_sort": 0, "finalize_ids": 4,
+                          "march": 16}
 
 
 def peaks():
