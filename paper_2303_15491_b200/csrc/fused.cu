@@ -707,7 +707,8 @@ __global__ void k_set_ids(const uint64_t* __restrict__ sorted_slots, int64_t r, 
 // many per SM, so one CTA's barriers overlap the others' work.
 constexpr int RY = 4, B_THREADS = 32 * RY;
 constexpr int LW = TX + 1, LQ = LW * (RY + 1);  // 33 x 17 = 561 vertices per layer
-constexpr int kBatch = 4, kRing = kBatch + 1;
+constexpr int kBatch = 4, kRing = 8;  // ring >= kBatch + 1, power of two
+static_assert(kRing >= kBatch + 1 && (kRing & (kRing - 1)) == 0, "ring size");
 __constant__ uint32_t c_mrows[PLMSS_TET_ROWS];
 __constant__ uint16_t c_mcases[32];
 
@@ -774,8 +775,7 @@ template <bool kEmit, bool kDense>
 __global__ void __launch_bounds__(B_THREADS, 8) k_brick(const BrickArgs a) {
   using Key = typename std::conditional<kDense, uint32_t, unsigned long long>::type;
   using Lab = typename std::conditional<kEmit, uint32_t, Key>::type;
-  extern __shared__ __align__(16) unsigned char b_smem[];
-  Lab* ring = reinterpret_cast<Lab*>(b_smem);  // kRing x LQ
+  __shared__ Lab ring[kRing * LQ];
   __shared__ uint16_t s_tlut[64], s_cases[32];
   __shared__ uint32_t s_rows[PLMSS_TET_ROWS];
   __shared__ uint32_t s_two_code[128];  // two-label cubes: corner membership -> 6 tet codes
@@ -832,7 +832,7 @@ __global__ void __launch_bounds__(B_THREADS, 8) k_brick(const BrickArgs a) {
       if (gx >= d.X || gy >= d.Y) {
 #pragma unroll
         for (int i = 0; i < kBatch; ++i)
-          if (kFull || i < zn) ring[((z0 + i) % kRing) * LQ + q] = kNone;
+          if (kFull || i < zn) ring[((z0 + i) & (kRing - 1)) * LQ + q] = kNone;
         return;
       }
       const uint32_t yy = yb + uint32_t(y);  // row within the brick (32: next brick)
@@ -883,7 +883,7 @@ __global__ void __launch_bounds__(B_THREADS, 8) k_brick(const BrickArgs a) {
         const int z = z0 + i;
         const Key key = kDense ? Key(la[i] * a.nmax + ld[i]) : Key((uint64_t(la[i]) << 32) | ld[i]);
         const bool own = x < TX && y < RY && (kFull || z < TZ);
-        Lab* L = ring + (z % kRing) * LQ;
+        Lab* L = ring + (z & (kRing - 1)) * LQ;
         if (!kEmit) {
           // distinct pairs of the owned vertices -> region bitmap / set
           if (own && key != lkey) {
@@ -937,8 +937,8 @@ __global__ void __launch_bounds__(B_THREADS, 8) k_brick(const BrickArgs a) {
     __syncthreads();
     // ---- cube layers z-1 whose two vertex layers are loaded
     for (int z = max(z0, 1); z < z0 + zn; ++z) {
-      const Lab* lo = ring + ((z - 1) % kRing) * LQ;
-      const Lab* cur = ring + (z % kRing) * LQ;
+      const Lab* lo = ring + ((z - 1) & (kRing - 1)) * LQ;
+      const Lab* cur = ring + (z & (kRing - 1)) * LQ;
       const int o = w * LW + lane;
       uint32_t cnt = 0, code6 = 0;
       uint32_t lo2 = 0, hi2 = 0;  // D, two-label cubes: the two ids (bit 31 of code6 marks the case)
@@ -980,11 +980,13 @@ __global__ void __launch_bounds__(B_THREADS, 8) k_brick(const BrickArgs a) {
         }
       }
       const uint32_t cz = gz0 + uint32_t(z) - 1;
+      const bool any = __any_sync(0xffffffffu, cnt != 0);
       if (!kEmit) {
-        const uint32_t tot = __reduce_add_sync(0xffffffffu, cnt);
+        const uint32_t tot = any ? __reduce_add_sync(0xffffffffu, cnt) : 0u;
         if (lane == 0 && row_ok) a.chunk[(uint64_t(cy) + uint64_t(d.Y - 1) * cz) * a.nxc + tx] = tot;
         continue;
       }
+      if (!any) continue;
       uint32_t inc = cnt;
 #pragma unroll
       for (int s = 1; s < 32; s <<= 1) {
@@ -1067,14 +1069,6 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
   if (c.device >= 0 && c.device < 64 && !g_consts_ready[c.device]) {
     CK(cudaFuncSetAttribute(k_tile_segment<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kASmem));
     CK(cudaFuncSetAttribute(k_tile_segment<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kASmem));
-    CK(cudaFuncSetAttribute(k_brick<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            int(kRing * LQ * sizeof(unsigned long long))));
-    CK(cudaFuncSetAttribute(k_brick<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            int(kRing * LQ * sizeof(uint32_t))));
-    CK(cudaFuncSetAttribute(k_brick<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            int(kRing * LQ * sizeof(uint32_t))));
-    CK(cudaFuncSetAttribute(k_brick<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            int(kRing * LQ * sizeof(uint32_t))));
     CK(cudaMemcpyToSymbol(c_mrows, kTetRowsPacked, sizeof(kTetRowsPacked)));
     CK(cudaMemcpyToSymbol(c_mcases, kTetCasePacked, sizeof(kTetCasePacked)));
     g_consts_ready[c.device] = true;
@@ -1229,8 +1223,6 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
     ba.chunk = chunk;
     const uint64_t nbits = uint64_t(o.n_max) * uint64_t(o.n_min);
     const bool dense = nbits < (uint64_t(1) << 32) && c.combine_path != 2;  // PLMSS_OPT_COMBINE_PATH 2: hash
-    const size_t smem_c = kRing * LQ * (dense ? sizeof(uint32_t) : sizeof(unsigned long long));
-    const size_t smem_d = kRing * LQ * sizeof(uint32_t);
     uint64_t* keys = nullptr;
     int64_t R = 0;
     if (dense) {
@@ -1239,7 +1231,7 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
       uint32_t* bitmap = c.get_t<uint32_t>(S_BITMAP, nw);
       CK(cudaMemsetAsync(bitmap, 0, nw * 4, c.stream));
       ba.bitmap = bitmap;
-      k_brick<false, true><<<unsigned((TY / RY) * ntiles), B_THREADS, smem_c, c.stream>>>(ba);
+      k_brick<false, true><<<unsigned((TY / RY) * ntiles), B_THREADS, 0, c.stream>>>(ba);
       CK_LAUNCH("k_brick<count>");
       const int64_t nb = int64_t((nw + kWB - 1) / kWB);
       uint64_t* bsum = c.get_t<uint64_t>(S_HASH_V, nb);
@@ -1265,7 +1257,7 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
         CK(cudaMemsetAsync(flag, 0, 4, c.stream));
         ba.fset = fset;
         ba.fmask = fcap - 1;
-        k_brick<false, false><<<unsigned((TY / RY) * ntiles), B_THREADS, smem_c, c.stream>>>(ba);
+        k_brick<false, false><<<unsigned((TY / RY) * ntiles), B_THREADS, 0, c.stream>>>(ba);
         CK_LAUNCH("k_brick<count>");
         CK(cudaMemcpyAsync(c.h_pinned, flag, 4, cudaMemcpyDeviceToHost, c.stream));
         c.sync();
@@ -1305,9 +1297,9 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
     ba.out = tris;
     CK(cudaMemsetAsync(flag, 0, 4, c.stream));
     if (dense)
-      k_brick<true, true><<<unsigned((TY / RY) * ntiles), B_THREADS, smem_d, c.stream>>>(ba);
+      k_brick<true, true><<<unsigned((TY / RY) * ntiles), B_THREADS, 0, c.stream>>>(ba);
     else
-      k_brick<true, false><<<unsigned((TY / RY) * ntiles), B_THREADS, smem_d, c.stream>>>(ba);
+      k_brick<true, false><<<unsigned((TY / RY) * ntiles), B_THREADS, 0, c.stream>>>(ba);
     CK_LAUNCH("k_brick<emit>");
     CK(cudaMemcpyAsync(c.h_pinned, flag, 4, cudaMemcpyDeviceToHost, c.stream));
     c.sync();
