@@ -707,7 +707,7 @@ __global__ void k_set_ids(const uint64_t* __restrict__ sorted_slots, int64_t r, 
 // many per SM, so one CTA's barriers overlap the others' work.
 constexpr int RY = 4, B_THREADS = 32 * RY;
 constexpr int LW = TX + 1, LQ = LW * (RY + 1);  // 33 x 17 = 561 vertices per layer
-constexpr int kBatch = 4, kRing = 8;  // ring >= kBatch + 1, power of two
+constexpr int kBatch = 8, kRing = 16;  // ring >= kBatch + 1, power of two
 static_assert(kRing >= kBatch + 1 && (kRing & (kRing - 1)) == 0, "ring size");
 __constant__ uint32_t c_mrows[PLMSS_TET_ROWS];
 __constant__ uint16_t c_mcases[32];
