@@ -281,3 +281,45 @@ def test_pipeline_host_e2e(plmss, gpu):
     keys = out["region_keys"]
     assert np.array_equal((keys >> np.uint64(32)).astype(np.int64), g["region_keys"][:, 0])
     assert res.n_tris == len(out["tris"])
+
+
+# Fused pipeline across brick boundaries: partial bricks (dims not multiples
+# of 32), multi-brick chains, tie-heavy and white-noise fields (the latter
+# with many extrema), both region-key modes; oracle = the C restatement.
+def _field(kind, dims, seed):
+    rng = np.random.default_rng(seed)
+    n = int(np.prod(dims))
+    if kind == "noise":
+        return rng.random(n).astype(np.float32)
+    if kind == "ties":
+        return rng.integers(0, 4, n).astype(np.float32)
+    from paper_2303_15491_b200.configs import CONFIGS, host_field, scaled
+
+    return host_field(scaled(CONFIGS["cfg2"], dims))
+
+
+@pytest.mark.parametrize("path", [0, 2])
+@pytest.mark.parametrize("dims,kind", [((97, 66, 40), "gauss"), ((33, 33, 33), "noise"), ((64, 31, 65), "ties"),
+                                       ((128, 96, 70), "gauss"), ((70, 40, 36), "noise")])
+def test_pipeline_brick_geometry(plmss, gpu, restatement, dims, kind, path):
+    f = _field(kind, dims, sum(dims))
+    gpu.set_option(1, 2 if path == 2 else 0)
+    try:
+        res = plmss.pipeline(dims, dev(f), ctx=gpu)
+    finally:
+        gpu.set_option(1, 0)
+    out = plmss.fetch(gpu, res)
+    s = restatement.segment(dims, values=f.astype(np.float64))
+    ms, keys = restatement.combine_ms(s["asc"], s["desc"])
+    for k, ref in (("desc", s["desc"]), ("asc", s["asc"]), ("ms", ms), ("maxima", s["maxima"]),
+                   ("minima", s["minima"])):
+        assert np.array_equal(u32(out[k]), ref), k
+    rk = out["region_keys"].cpu().numpy().astype(np.uint64)
+    assert np.array_equal((rk >> np.uint64(32)).astype(np.int64), keys[:, 0])
+    assert np.array_equal((rk & np.uint64(0xFFFFFFFF)).astype(np.int64), keys[:, 1])
+    e = restatement.emit_separators(dims, ms)
+    assert res.n_tris == len(e["source_cells"])
+    m = plmss.materialize_separators(dims, out["tris"], ctx=gpu)
+    assert np.array_equal(m["source_cells"].cpu().numpy(), e["source_cells"])
+    assert np.array_equal(m["regions"].cpu().numpy(), e["regions"])
+    assert np.array_equal(m["points"].cpu().numpy(), e["points"])
