@@ -76,33 +76,6 @@ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
   return x;
 }
 
-// Insert k into an open-addressing set; returns false on probe overflow.
-__device__ __forceinline__ bool set_insert(unsigned long long* __restrict__ t, uint64_t mask, uint64_t k) {
-  uint64_t s = mix64(k) & mask;
-#pragma unroll 1
-  for (int probe = 0; probe < 1024; ++probe) {
-    const unsigned long long cur = t[s];
-    if (cur == k) return true;
-    if (cur == kEmpty) {
-      const unsigned long long prev = atomicCAS(t + s, kEmpty, k);
-      if (prev == kEmpty || prev == k) return true;
-    }
-    s = (s + 1) & mask;
-  }
-  return false;
-}
-
-// Slot of k, or ~0 when k is absent (a probe that meets an empty slot).
-__device__ __forceinline__ uint64_t set_find(const unsigned long long* __restrict__ t, uint64_t mask, uint64_t k) {
-  uint64_t s = mix64(k) & mask;
-  for (;;) {
-    const unsigned long long cur = t[s];
-    if (cur == k) return s;
-    if (cur == kEmpty) return ~uint64_t(0);
-    s = (s + 1) & mask;
-  }
-}
-
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -748,6 +721,56 @@ __device__ __forceinline__ uint32_t cube_codes(const L (&c)[8], const uint16_t* 
   return (t0 & 31) | (t1 & 31) << 5 | (t2 & 31) << 10 | (t3 & 31) << 15 | (t4 & 31) << 20 | (t5 & 31) << 25;
 }
 
+// Marching tables in global memory (L1-resident), built once per device by
+// k_march_init: equality-pattern LUT, recipe cases and rows, and the
+// two-label cube tables (corner membership m8 with bit 0 set, indexed m8 >> 1:
+// separator count, records as tet << 8 | recipe row).
+__device__ uint16_t g_tlut[64], g_cases[32];
+__device__ uint32_t g_rows[PLMSS_TET_ROWS];
+__device__ uint8_t g_two_cnt[128];
+__device__ uint16_t g_two_rec[128 * 12];
+
+__global__ void k_march_init() {
+  __shared__ uint16_t s_tlut[64], s_cases[32];
+  __shared__ uint32_t s_rows[PLMSS_TET_ROWS];
+  load_march_tables(s_tlut, s_cases, s_rows);
+  __syncthreads();
+  const int tid = int(threadIdx.x);
+  if (tid < 64) g_tlut[tid] = s_tlut[tid];
+  if (tid < 32) g_cases[tid] = s_cases[tid];
+  if (tid < PLMSS_TET_ROWS) g_rows[tid] = s_rows[tid];
+  if (tid < 128) {
+    // corner i carries label 0 when bit i of m8 is set (bit 0 always is)
+    const uint32_t m8 = uint32_t(tid) << 1 | 1u;
+    uint32_t lab[8];
+    for (int i = 0; i < 8; ++i) lab[i] = (m8 >> i) & 1u ? 0u : 1u;
+    uint32_t cnt;
+    const uint32_t code6 = cube_codes(lab, s_tlut, cnt);
+    g_two_cnt[tid] = uint8_t(cnt);
+    uint32_t r = 0;
+    for (int t = 0; t < 6; ++t) {
+      const uint32_t cs = s_cases[(code6 >> (5 * t)) & 31];
+      for (uint32_t k = 0; k < (cs & 15); ++k) g_two_rec[tid * 12 + r++] = uint16_t(uint32_t(t) << 8 | ((cs >> 4) + k));
+    }
+  }
+}
+
+// Insert k; returns its slot (new or existing), ~0 on probe overflow.
+__device__ __forceinline__ uint64_t set_insert_slot(unsigned long long* __restrict__ t, uint64_t mask, uint64_t k) {
+  uint64_t s = mix64(k) & mask;
+#pragma unroll 1
+  for (int probe = 0; probe < 1024; ++probe) {
+    const unsigned long long cur = t[s];
+    if (cur == k) return s;
+    if (cur == kEmpty) {
+      const unsigned long long prev = atomicCAS(t + s, kEmpty, k);
+      if (prev == kEmpty || prev == k) return s;
+    }
+    s = (s + 1) & mask;
+  }
+  return ~uint64_t(0);
+}
+
 struct BrickArgs {
   FDims d;
   uint32_t nxc;  // 32-cube chunks per cube row
@@ -757,82 +780,52 @@ struct BrickArgs {
   const uint32_t *maxs, *mins;    // sorted extremum lists (rank -> vertex id)
   uint32_t nmax;                  // dense mode: key = rank_min * nmax + rank_max
   uint32_t* bitmap;               // dense mode: region bitmap
-  const uint32_t* prefix;         // dense mode D: per-word dense id of the first set bit
   unsigned long long* fset;       // hash mode: region set of (rank_min << 32 | rank_max)
   uint64_t fmask;
-  const uint32_t* slot_id;  // hash mode D: region set slot -> dense id
-  uint64_t* chunk;          // C: counts out; D: exclusive offsets in
-  uint64_t total;           // D: total records
-  uint32_t *desc, *asc, *ms;
-  plmss_tri* out;
+  uint64_t* chunk;                // separator count per 32-cube chunk
+  uint8_t* cls;                   // per cube: 0 one region, m8 two labels, 0xff more
+  uint32_t *desc, *asc, *ms;      // ms holds the region token until k_ms_ids
   int* overflow;
 };
 
-// kEmit = false: pass C (region set + chunk counts); true: pass D.
-// kDense: region keys are u32 rank products in a bitmap, else u64 rank pairs
-// in the hash set.
-template <bool kEmit, bool kDense>
+// Pass C. Region token of a vertex: its dense key (rank_min * nmax +
+// rank_max) or its slot in the region hash set; equal tokens <=> equal
+// (asc, desc) pairs. Writes desc/asc (vertex ids of the two extrema), the
+// token into ms, the bitmap/set, each cube's class and each chunk's count.
+template <bool kDense>
 __global__ void __launch_bounds__(B_THREADS, 8) k_brick(const BrickArgs a) {
   using Key = typename std::conditional<kDense, uint32_t, unsigned long long>::type;
-  using Lab = typename std::conditional<kEmit, uint32_t, Key>::type;
-  __shared__ Lab ring[kRing * LQ];
-  __shared__ uint16_t s_tlut[64], s_cases[32];
-  __shared__ uint32_t s_rows[PLMSS_TET_ROWS];
-  __shared__ uint32_t s_two_code[128];  // two-label cubes: corner membership -> 6 tet codes
-  __shared__ uint8_t s_two_cnt[128];    // ... -> separator count
-  // ... -> its records in order: tet << 8 | recipe row (at most 2 per tet)
-  __shared__ uint16_t s_two_rec[kEmit ? 128 : 1][kEmit ? 12 : 1];
+  __shared__ uint32_t ring[kRing * LQ];
   const FDims& d = a.d;
-  const uint32_t bt = blockIdx.x / (TY / RY), yb = (blockIdx.x % (TY / RY)) * RY;  // brick, first row of this CTA's rows
+  const uint32_t bt = blockIdx.x / (TY / RY), yb = (blockIdx.x % (TY / RY)) * RY;  // brick, first row of this CTA
   const uint32_t tx = bt % d.tx, ty = (bt / d.tx) % d.ty, tz = bt / (d.tx * d.ty);
   const uint32_t gx0 = tx * TX, gy0 = ty * TY + yb, gz0 = tz * TZ;
-  if (gy0 >= d.Y) return;  // upper half of a brick cut by the volume
+  if (gy0 >= d.Y) return;  // rows of a brick cut by the volume
   const int tid = int(threadIdx.x), lane = tid & 31, w = tid >> 5;
-  load_march_tables(s_tlut, s_cases, s_rows);
-  __syncthreads();
-  if (tid < 128) {
-    // corner i carries label 0 when bit i of m8 is set (bit 0 always is)
-    const uint32_t m8 = uint32_t(tid) << 1 | 1u;
-    uint32_t lab[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) lab[i] = (m8 >> i) & 1u ? 0u : 1u;
-    uint32_t cnt;
-    const uint32_t code6 = cube_codes(lab, s_tlut, cnt);
-    s_two_code[tid] = code6;
-    s_two_cnt[tid] = uint8_t(cnt);
-    if (kEmit) {
-      uint32_t r = 0;
-      for (int t = 0; t < 6; ++t) {
-        const uint32_t cs = s_cases[(code6 >> (5 * t)) & 31];
-        for (uint32_t k = 0; k < (cs & 15); ++k) s_two_rec[tid][r++] = uint16_t(uint32_t(t) << 8 | ((cs >> 4) + k));
-      }
-    }
-  }
   const uint32_t* TBw = reinterpret_cast<const uint32_t*>(a.TB);
   const int nl = int(min(uint32_t(TZ + 1), d.Z - gz0));  // vertex layers of the brick + halo
   // this thread's cube column: x = lane, y = w
   const uint32_t cy = gy0 + uint32_t(w);
   const bool row_ok = cy + 1 < d.Y && tx < a.nxc;
   const bool cube_ok = row_ok && gx0 + uint32_t(lane) + 1 < d.X;
-  const Lab kNone = Lab(~Lab(0));
-  // per-thread cache of the last pair seen in each of its two columns (D:
-  // with its id and vertex ids)
+  // per-thread cache of the last pair seen in each of its two columns: key,
+  // token, vertex ids of its maximum / minimum
   Key lkey0 = Key(~Key(0)), lkey1 = Key(~Key(0));
-  uint32_t lid0 = 0, lid1 = 0;
+  uint32_t ltok0 = 0, ltok1 = 0;
   uint2 lgv0 = make_uint2(0, 0), lgv1 = make_uint2(0, 0);
 
   for (int z0 = 0; z0 < nl; z0 += kBatch) {
     const int zn = min(kBatch, nl - z0);
     // ---- load layers z0 .. z0+zn-1 (threads 0..LQ-B_THREADS-1 also take a second q)
     // full: kBatch layers, all below the halo layer 32 (no predication)
-    auto load_column = [&](auto full, const int q, Key& lkey, uint32_t& lid, uint2& lgv) {
+    auto load_column = [&](auto full, const int q, Key& lkey, uint32_t& ltok, uint2& lgv) {
       constexpr bool kFull = decltype(full)::value;
       const int x = q % LW, y = q / LW;
       const uint32_t gx = gx0 + uint32_t(x), gy = gy0 + uint32_t(y);
       if (gx >= d.X || gy >= d.Y) {
 #pragma unroll
         for (int i = 0; i < kBatch; ++i)
-          if (kFull || i < zn) ring[((z0 + i) & (kRing - 1)) * LQ + q] = kNone;
+          if (kFull || i < zn) ring[((z0 + i) & (kRing - 1)) * LQ + q] = ~0u;
         return;
       }
       const uint32_t yy = yb + uint32_t(y);  // row within the brick (32: next brick)
@@ -882,68 +875,47 @@ __global__ void __launch_bounds__(B_THREADS, 8) k_brick(const BrickArgs a) {
         if (!kFull && i >= zn) break;
         const int z = z0 + i;
         const Key key = kDense ? Key(la[i] * a.nmax + ld[i]) : Key((uint64_t(la[i]) << 32) | ld[i]);
-        const bool own = x < TX && y < RY && (kFull || z < TZ);
-        Lab* L = ring + (z & (kRing - 1)) * LQ;
-        if (!kEmit) {
-          // distinct pairs of the owned vertices -> region bitmap / set
-          if (own && key != lkey) {
-            if (kDense) {
-              const uint32_t bit = 1u << (uint32_t(key) & 31);
-              uint32_t* wp = a.bitmap + (uint32_t(key) >> 5);
-              if (!(*wp & bit)) atomicOr(wp, bit);
-            } else if (!set_insert(a.fset, a.fmask, uint64_t(key))) {
-              *a.overflow = 1;
-            }
-            lkey = key;
+        if (key != lkey) {
+          // a new pair for this column: token, region set, extremum ids
+          if (kDense) {
+            ltok = uint32_t(key);
+            const uint32_t bit = 1u << (ltok & 31);
+            uint32_t* wp = a.bitmap + (ltok >> 5);
+            if (!(*wp & bit)) atomicOr(wp, bit);
+          } else {
+            const uint64_t slot = set_insert_slot(a.fset, a.fmask, uint64_t(key));
+            if (slot == ~uint64_t(0)) *a.overflow = 1;
+            ltok = uint32_t(slot);
           }
-          L[q] = key;
-        } else {
-          if (key != lkey) {
-            if (kDense) {
-              const uint32_t k = uint32_t(key);
-              lid = __ldg(a.prefix + (k >> 5)) + __popc(__ldg(a.bitmap + (k >> 5)) & ((1u << (k & 31)) - 1u));
-            } else {
-              const uint64_t slot = set_find(a.fset, a.fmask, uint64_t(key));
-              if (slot == ~uint64_t(0))
-                *a.overflow = 1;  // a pair the count pass never saw: reported, never a silent id
-              else
-                lid = __ldg(a.slot_id + slot);
-            }
-            lgv = make_uint2(__ldg(a.maxs + ld[i]), __ldg(a.mins + la[i]));
-            lkey = key;
-          }
-          L[q] = lid;
-          if (own) {
-            const uint32_t gv = gx + d.X * (gy + d.Y * (gz0 + uint32_t(z)));
-            a.desc[gv] = lgv.x;
-            a.asc[gv] = lgv.y;
-            a.ms[gv] = lid;
-          }
+          lgv = make_uint2(__ldg(a.maxs + ld[i]), __ldg(a.mins + la[i]));
+          lkey = key;
+        }
+        ring[(z & (kRing - 1)) * LQ + q] = ltok;
+        if (x < TX && y < RY && (kFull || z < TZ)) {
+          const uint32_t gv = gx + d.X * (gy + d.Y * (gz0 + uint32_t(z)));
+          a.desc[gv] = lgv.x;
+          a.asc[gv] = lgv.y;
+          a.ms[gv] = ltok;
         }
       }
     };
     if (zn == kBatch && z0 + kBatch <= TZ) {
-      load_column(std::true_type{}, tid, lkey0, lid0, lgv0);
-      if (tid < LQ - B_THREADS) load_column(std::true_type{}, tid + B_THREADS, lkey1, lid1, lgv1);
+      load_column(std::true_type{}, tid, lkey0, ltok0, lgv0);
+      if (tid < LQ - B_THREADS) load_column(std::true_type{}, tid + B_THREADS, lkey1, ltok1, lgv1);
     } else {
-      load_column(std::false_type{}, tid, lkey0, lid0, lgv0);
-      if (tid < LQ - B_THREADS) load_column(std::false_type{}, tid + B_THREADS, lkey1, lid1, lgv1);
+      load_column(std::false_type{}, tid, lkey0, ltok0, lgv0);
+      if (tid < LQ - B_THREADS) load_column(std::false_type{}, tid + B_THREADS, lkey1, ltok1, lgv1);
     }
-    // D: this warp's chunk offsets for the batch's cube layers (lane i <->
-    // vertex layer z0 + i, cube layer z0 + i - 1)
-    uint64_t pre_off = 0;
-    if (kEmit && lane < zn && z0 + lane >= 1 && row_ok)
-      pre_off = a.chunk[(uint64_t(cy) + uint64_t(d.Y - 1) * (gz0 + uint32_t(z0 + lane) - 1)) * a.nxc + tx];
     __syncthreads();
     // ---- cube layers z-1 whose two vertex layers are loaded
     for (int z = max(z0, 1); z < z0 + zn; ++z) {
-      const Lab* lo = ring + ((z - 1) & (kRing - 1)) * LQ;
-      const Lab* cur = ring + (z & (kRing - 1)) * LQ;
+      const uint32_t* lo = ring + ((z - 1) & (kRing - 1)) * LQ;
+      const uint32_t* cur = ring + (z & (kRing - 1)) * LQ;
       const int o = w * LW + lane;
-      uint32_t cnt = 0, code6 = 0;
-      uint32_t lo2 = 0, hi2 = 0;  // D, two-label cubes: the two ids (bit 31 of code6 marks the case)
+      const uint32_t cz = gz0 + uint32_t(z) - 1;
+      uint32_t cnt = 0;
       if (cube_ok) {
-        Lab c[8];
+        uint32_t c[8];
         c[0] = lo[o];
         c[1] = lo[o + 1];
         c[2] = lo[o + LW];
@@ -956,47 +928,97 @@ __global__ void __launch_bounds__(B_THREADS, 8) k_brick(const BrickArgs a) {
         uint32_t m8 = 1u;
 #pragma unroll
         for (int i = 1; i < 8; ++i) m8 |= uint32_t(c[i] == c[0]) << i;
+        uint32_t cls = 0;
         if (m8 != 0xffu) {
           // the lowest corner with another label; two labels iff every
           // corner carries one of the two (the common case on a separator)
-          Lab b = c[7];
+          uint32_t b = c[7];
 #pragma unroll
           for (int i = 6; i >= 1; --i) b = (m8 >> i) & 1u ? b : c[i];
           uint32_t mb = 0u;
 #pragma unroll
           for (int i = 1; i < 8; ++i) mb |= uint32_t(c[i] == b) << i;
           if ((m8 | mb) == 0xffu) {
-            cnt = s_two_cnt[m8 >> 1];
-            if (kEmit) {
-              code6 = 0x80000000u | m8;
-              lo2 = min(uint32_t(c[0]), uint32_t(b));
-              hi2 = max(uint32_t(c[0]), uint32_t(b));
-            } else {
-              code6 = s_two_code[m8 >> 1];
-            }
+            cnt = g_two_cnt[m8 >> 1];
+            cls = m8;
           } else {
-            code6 = cube_codes(c, s_tlut, cnt);
+            cube_codes(c, g_tlut, cnt);
+            cls = 0xffu;
           }
         }
+        a.cls[uint64_t(gx0 + uint32_t(lane)) + uint64_t(d.X - 1) * (uint64_t(cy) + uint64_t(d.Y - 1) * cz)] =
+            uint8_t(cls);
       }
-      const uint32_t cz = gz0 + uint32_t(z) - 1;
-      const bool any = __any_sync(0xffffffffu, cnt != 0);
-      if (!kEmit) {
-        const uint32_t tot = any ? __reduce_add_sync(0xffffffffu, cnt) : 0u;
-        if (lane == 0 && row_ok) a.chunk[(uint64_t(cy) + uint64_t(d.Y - 1) * cz) * a.nxc + tx] = tot;
-        continue;
+      const uint32_t tot = __any_sync(0xffffffffu, cnt != 0) ? __reduce_add_sync(0xffffffffu, cnt) : 0u;
+      if (lane == 0 && row_ok) a.chunk[(uint64_t(cy) + uint64_t(d.Y - 1) * cz) * a.nxc + tx] = tot;
+    }
+    __syncthreads();
+  }
+}
+
+// Region token -> dense MS id.
+template <bool kDense>
+__device__ __forceinline__ uint32_t token_id(uint32_t k, const uint32_t* __restrict__ bitmap,
+                                             const uint32_t* __restrict__ prefix, const uint32_t* __restrict__ slot_id) {
+  if (kDense) return __ldg(prefix + (k >> 5)) + __popc(__ldg(bitmap + (k >> 5)) & ((1u << (k & 31)) - 1u));
+  return __ldg(slot_id + k);
+}
+
+struct EmitArgs {
+  uint32_t X, Y, Z, nxc;
+  uint64_t nchunks, total;
+  const uint64_t* off;   // exclusive chunk offsets
+  const uint8_t* cls;
+  const uint32_t* tok;   // ms, still holding region tokens
+  const uint32_t *bitmap, *prefix, *slot_id;
+  plmss_tri* out;
+};
+
+// Pass D: separator records of every chunk with records, at its offset, in
+// the reference order (cube-major, tets in order, recipe rows in order:
+// marching.cpp:116-215). Warps walk whole cube rows; lane = cube of the chunk;
+// records are dealt out one per lane (consecutive lanes write consecutive
+// 16-byte records).
+template <bool kDense>
+__global__ void __launch_bounds__(256) k_emit_chunks(const EmitArgs a) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t CX = a.X - 1, CY = a.Y - 1, XY = a.X * a.Y;
+  const uint32_t nrows = uint32_t(a.nchunks / a.nxc);
+  const uint32_t warps = gridDim.x * (blockDim.x / 32);
+  for (uint32_t r = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); r < nrows; r += warps) {
+    const uint32_t cz = r / CY, cy = r - cz * CY;
+    for (uint32_t xs = 0; xs < a.nxc; ++xs) {
+      const uint64_t ch = uint64_t(r) * a.nxc + xs;
+      const uint64_t base = a.off[ch];
+      const uint32_t T = uint32_t((ch + 1 < a.nchunks ? a.off[ch + 1] : a.total) - base);
+      if (T == 0) continue;
+      const uint32_t cx = 32 * xs + uint32_t(lane);
+      const uint64_t q0 = uint64_t(32 * xs) + uint64_t(CX) * r;  // cube id of lane 0's cube
+      const uint32_t v0 = cx + a.X * cy + XY * cz;                // this lane's min corner
+      const uint32_t cls = cx < CX ? a.cls[q0 + lane] : 0u;
+      uint32_t cnt = 0, code6 = 0, lo2 = 0, hi2 = 0;
+      auto corner_off = [&](uint32_t cn) { return (cn & 1) + a.X * ((cn >> 1) & 1) + XY * (cn >> 2); };
+      if (cls == 0xffu) {
+        uint32_t c[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) c[i] = __ldg(a.tok + v0 + corner_off(uint32_t(i)));
+        code6 = cube_codes(c, g_tlut, cnt);
+      } else if (cls != 0) {
+        // two labels: corner 0's and that of the lowest corner outside its set
+        cnt = g_two_cnt[cls >> 1];
+        code6 = 0x80000000u | cls;
+        const uint32_t i0 = token_id<kDense>(__ldg(a.tok + v0), a.bitmap, a.prefix, a.slot_id);
+        const uint32_t ib = token_id<kDense>(__ldg(a.tok + v0 + corner_off(uint32_t(__ffs(~cls) - 1))), a.bitmap,
+                                             a.prefix, a.slot_id);
+        lo2 = min(i0, ib);
+        hi2 = max(i0, ib);
       }
-      if (!any) continue;
       uint32_t inc = cnt;
 #pragma unroll
       for (int s = 1; s < 32; s <<= 1) {
         const uint32_t t = __shfl_up_sync(0xffffffffu, inc, s);
         if (lane >= s) inc += t;
       }
-      const uint32_t T = __shfl_sync(0xffffffffu, inc, 31);
-      const uint64_t base = __shfl_sync(0xffffffffu, pre_off, z - z0);
-      if (T == 0 || !row_ok) continue;
-      const uint64_t q0 = uint64_t(gx0) + uint64_t(d.X - 1) * (uint64_t(cy) + uint64_t(d.Y - 1) * cz);
       for (uint32_t j0 = 0; j0 < T; j0 += 32) {
         const uint32_t j = j0 + uint32_t(lane);
         // owning lane of record j = number of lanes whose inclusive count <= j
@@ -1012,42 +1034,67 @@ __global__ void __launch_bounds__(B_THREADS, 8) k_brick(const BrickArgs a) {
         const uint32_t h2 = __shfl_sync(0xffffffffu, hi2, src & 31);
         if (j >= T) continue;
         uint32_t k = j - ex;
+        uint32_t t, rowi, la, lb;
         if (c6 >> 31) {
           // two-label cube: record list from the table, one region pair
-          const uint32_t e = s_two_rec[(c6 & 0xffu) >> 1][k];
-          const uint64_t cr64 = ((6ull * (q0 + uint32_t(src)) + (e >> 8)) << 6) | uint64_t(e & 0xffu);
-          *reinterpret_cast<uint4*>(a.out + base + j) = make_uint4(uint32_t(cr64), uint32_t(cr64 >> 32), l2, h2);
-          continue;
-        }
-        int t = 0;
-        uint32_t cs = s_cases[c6 & 31];
+          const uint32_t e = g_two_rec[((c6 & 0xffu) >> 1) * 12 + k];
+          t = e >> 8;
+          rowi = e & 0xffu;
+          la = l2;
+          lb = h2;
+        } else {
+          t = 0;
+          uint32_t cs = g_cases[c6 & 31];
 #pragma unroll
-        for (int tt = 0; tt < 5; ++tt) {
-          if (k < (cs & 15)) break;
-          k -= cs & 15;
-          ++t;
-          cs = s_cases[(c6 >> (5 * t)) & 31];
+          for (int tt = 0; tt < 5; ++tt) {
+            if (k < (cs & 15)) break;
+            k -= cs & 15;
+            ++t;
+            cs = g_cases[(c6 >> (5 * t)) & 31];
+          }
+          rowi = (cs >> 4) + k;
+          const uint32_t row = g_rows[rowi];
+          // tet t = cube corners {0, cb, cc, 7}
+          const uint32_t cb = (0x442211u >> (4 * t)) & 15, cc = (0x656353u >> (4 * t)) & 15;
+          auto corner = [&](uint32_t p) { return p == 0 ? 0u : (p == 1 ? cb : (p == 2 ? cc : 7u)); };
+          const uint32_t vs = v0 - uint32_t(lane) + uint32_t(src);
+          la = token_id<kDense>(__ldg(a.tok + vs + corner_off(corner((row >> 12) & 3))), a.bitmap, a.prefix,
+                                a.slot_id);
+          lb = token_id<kDense>(__ldg(a.tok + vs + corner_off(corner((row >> 14) & 3))), a.bitmap, a.prefix,
+                                a.slot_id);
         }
-        const uint32_t rowi = (cs >> 4) + k;
-        const uint32_t row = s_rows[rowi];
-        // tet t = cube corners {0, cb, cc, 7}; corner p -> ring cell
-        const uint32_t cb = (0x442211u >> (4 * t)) & 15, cc = (0x656353u >> (4 * t)) & 15;
-        auto corner = [&](uint32_t p) { return p == 0 ? 0u : (p == 1 ? cb : (p == 2 ? cc : 7u)); };
-        auto lab = [&](uint32_t cn) -> uint32_t {
-          const Lab* L = (cn & 4) ? cur : lo;
-          return uint32_t(L[w * LW + src + int(cn & 1) + LW * int((cn >> 1) & 1)]);
-        };
-        const uint32_t la = lab(corner((row >> 12) & 3)), lb = lab(corner((row >> 14) & 3));
-        const uint64_t cr64 = ((6ull * (q0 + uint32_t(src)) + uint32_t(t)) << 6) | uint64_t(rowi);
-        uint4 rec;
-        rec.x = uint32_t(cr64);
-        rec.y = uint32_t(cr64 >> 32);
-        rec.z = min(la, lb);
-        rec.w = max(la, lb);
-        *reinterpret_cast<uint4*>(a.out + base + j) = rec;
+        const uint64_t cr64 = ((6ull * (q0 + uint32_t(src)) + t) << 6) | uint64_t(rowi);
+        *reinterpret_cast<uint4*>(a.out + base + j) =
+            make_uint4(uint32_t(cr64), uint32_t(cr64 >> 32), min(la, lb), max(la, lb));
       }
     }
-    __syncthreads();
+  }
+}
+
+// ms: region token -> dense id, in place (4 vertices per thread, the last
+// lookup cached: runs of one region are the norm).
+template <bool kDense>
+__global__ void __launch_bounds__(256) k_ms_ids(uint32_t* __restrict__ ms, uint64_t n,
+                                                const uint32_t* __restrict__ bitmap,
+                                                const uint32_t* __restrict__ prefix,
+                                                const uint32_t* __restrict__ slot_id) {
+  const uint64_t i0 = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
+  if (i0 >= n) return;
+  uint32_t lt = ~0u, lid = 0;
+  if (i0 + 4 <= n) {
+    uint4 v = *reinterpret_cast<const uint4*>(ms + i0);
+    uint32_t* e = reinterpret_cast<uint32_t*>(&v);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (e[k] != lt) {
+        lt = e[k];
+        lid = token_id<kDense>(lt, bitmap, prefix, slot_id);
+      }
+      e[k] = lid;
+    }
+    *reinterpret_cast<uint4*>(ms + i0) = v;
+  } else {
+    for (uint64_t i = i0; i < n; ++i) ms[i] = token_id<kDense>(ms[i], bitmap, prefix, slot_id);
   }
 }
 
@@ -1071,6 +1118,8 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
     CK(cudaFuncSetAttribute(k_tile_segment<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kASmem));
     CK(cudaMemcpyToSymbol(c_mrows, kTetRowsPacked, sizeof(kTetRowsPacked)));
     CK(cudaMemcpyToSymbol(c_mcases, kTetCasePacked, sizeof(kTetCasePacked)));
+    k_march_init<<<1, 128, 0, c.stream>>>();
+    CK_LAUNCH("k_march_init");
     g_consts_ready[c.device] = true;
   }
   FDims d;
@@ -1202,7 +1251,7 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
     k_tt_final<<<blocks_for(int64_t(nt), 256), 256, 0, c.stream>>>(nt, RK, SD, SA);
     CK_LAUNCH("k_tt_final");
     c.mark(3);
-    // ---- C: region keys + separator counts per 32-cube chunk
+    // ---- C: region tokens, desc/asc, cube classes, separator counts per chunk
     BrickArgs ba{};
     ba.d = d;
     ba.nxc = uint32_t((g.X - 1 + 31) / 32);
@@ -1221,28 +1270,30 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
     const uint64_t nchunks = uint64_t(ba.nxc) * uint64_t(g.Y - 1) * uint64_t(g.Z - 1);
     uint64_t* chunk = c.get_t<uint64_t>(S_TMP1, nchunks ? nchunks : 1);
     ba.chunk = chunk;
+    ba.cls = c.get_t<uint8_t>(S_MASK, uint64_t(g.cubes ? g.cubes : 1));
+    const unsigned cgrid = unsigned((TY / RY) * ntiles);
     const uint64_t nbits = uint64_t(o.n_max) * uint64_t(o.n_min);
     const bool dense = nbits < (uint64_t(1) << 32) && c.combine_path != 2;  // PLMSS_OPT_COMBINE_PATH 2: hash
     uint64_t* keys = nullptr;
     int64_t R = 0;
+    uint32_t *bitmap = nullptr, *prefix = nullptr, *slot_id = nullptr;
     if (dense) {
       // rank-product bitmap: no hashing, ids by prefix popcount
       const uint64_t nw = (nbits + 31) / 32;
-      uint32_t* bitmap = c.get_t<uint32_t>(S_BITMAP, nw);
+      bitmap = c.get_t<uint32_t>(S_BITMAP, nw);
       CK(cudaMemsetAsync(bitmap, 0, nw * 4, c.stream));
       ba.bitmap = bitmap;
-      k_brick<false, true><<<unsigned((TY / RY) * ntiles), B_THREADS, 0, c.stream>>>(ba);
-      CK_LAUNCH("k_brick<count>");
+      k_brick<true><<<cgrid, B_THREADS, 0, c.stream>>>(ba);
+      CK_LAUNCH("k_brick");
       const int64_t nb = int64_t((nw + kWB - 1) / kWB);
       uint64_t* bsum = c.get_t<uint64_t>(S_HASH_V, nb);
       k_bitmap_count<<<unsigned(nb), 256, 0, c.stream>>>(bitmap, nw, bsum);
       CK_LAUNCH("k_bitmap_count");
       R = int64_t(exclusive_scan_u64(c, bsum, nb, true));
       keys = c.get_t<uint64_t>(S_KEYS, R);
-      uint32_t* prefix = c.get_t<uint32_t>(S_HASH_K, nw);
+      prefix = c.get_t<uint32_t>(S_HASH_K, nw);
       k_bitmap_ids<<<unsigned(nb), kWB, 0, c.stream>>>(bitmap, nw, bsum, ba.nmax, maxima, minima, prefix, keys);
       CK_LAUNCH("k_bitmap_ids");
-      ba.prefix = prefix;
       c.stats[2] = -int64_t(nw);
     } else {
       uint64_t fcap = 1024;
@@ -1252,13 +1303,15 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
       }
       unsigned long long* fset = nullptr;
       for (int tries = 0;; ++tries) {
+        // tokens are u32 slots
+        if (fcap > (uint64_t(1) << 32)) fail(PLMSS_ERR_LOGIC, "region set larger than 2^32 slots");
         fset = c.get_t<unsigned long long>(S_HASH_V, fcap);
         CK(cudaMemsetAsync(fset, 0xff, fcap * 8, c.stream));
         CK(cudaMemsetAsync(flag, 0, 4, c.stream));
         ba.fset = fset;
         ba.fmask = fcap - 1;
-        k_brick<false, false><<<unsigned((TY / RY) * ntiles), B_THREADS, 0, c.stream>>>(ba);
-        CK_LAUNCH("k_brick<count>");
+        k_brick<false><<<cgrid, B_THREADS, 0, c.stream>>>(ba);
+        CK_LAUNCH("k_brick");
         CK(cudaMemcpyAsync(c.h_pinned, flag, 4, cudaMemcpyDeviceToHost, c.stream));
         c.sync();
         if (*reinterpret_cast<int*>(c.h_pinned) == 0) break;
@@ -1278,32 +1331,49 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
       int kb = 32;
       while ((uint64_t(1) << (kb - 32)) < uint64_t(std::max(o.n_min, int64_t(1)))) ++kb;
       radix_sort_pairs(c, keys, slots, R, kb);
-      uint32_t* slot_id = c.get_t<uint32_t>(S_BITMAP, fcap);
+      slot_id = c.get_t<uint32_t>(S_BITMAP, fcap);
       k_set_ids<<<blocks_for(R, 256), 256, 0, c.stream>>>(slots, R, slot_id);
       CK_LAUNCH("k_set_ids");
       k_keys_to_gid<<<blocks_for(R, 256), 256, 0, c.stream>>>(keys, R, maxima, minima);
       CK_LAUNCH("k_keys_to_gid");
-      ba.fset = fset;
-      ba.fmask = fcap - 1;
-      ba.slot_id = slot_id;
       c.stats[2] = int64_t(fcap);
     }
     o.n_regions = R;
     const uint64_t total = nchunks ? exclusive_scan_u64(c, chunk, int64_t(nchunks), true) : 0;
     c.mark(4);
-    // ---- D: labels, ids, separator records
+    // ---- D: separator records at their chunk offsets; ms tokens -> ids
     plmss_tri* tris = c.get_t<plmss_tri>(S_TRIS, total ? total : 1);
-    ba.total = total;
-    ba.out = tris;
-    CK(cudaMemsetAsync(flag, 0, 4, c.stream));
-    if (dense)
-      k_brick<true, true><<<unsigned((TY / RY) * ntiles), B_THREADS, 0, c.stream>>>(ba);
-    else
-      k_brick<true, false><<<unsigned((TY / RY) * ntiles), B_THREADS, 0, c.stream>>>(ba);
-    CK_LAUNCH("k_brick<emit>");
-    CK(cudaMemcpyAsync(c.h_pinned, flag, 4, cudaMemcpyDeviceToHost, c.stream));
-    c.sync();
-    if (*reinterpret_cast<int*>(c.h_pinned) != 0) fail(PLMSS_ERR_LOGIC, "region pair missing from the region set");
+    if (total) {
+      EmitArgs ea{};
+      ea.X = d.X;
+      ea.Y = d.Y;
+      ea.Z = d.Z;
+      ea.nxc = ba.nxc;
+      ea.nchunks = nchunks;
+      ea.total = total;
+      ea.off = chunk;
+      ea.cls = ba.cls;
+      ea.tok = ms;
+      ea.bitmap = bitmap;
+      ea.prefix = prefix;
+      ea.slot_id = slot_id;
+      ea.out = tris;
+      const uint64_t nrows = uint64_t(g.Y - 1) * uint64_t(g.Z - 1);
+      const unsigned egrid = unsigned(std::min<uint64_t>((nrows + 7) / 8, uint64_t(c.sm_count) * 64));
+      if (dense)
+        k_emit_chunks<true><<<egrid, 256, 0, c.stream>>>(ea);
+      else
+        k_emit_chunks<false><<<egrid, 256, 0, c.stream>>>(ea);
+      CK_LAUNCH("k_emit_chunks");
+    }
+    {
+      const unsigned mgrid = unsigned((uint64_t(g.n) + 1023) / 1024);
+      if (dense)
+        k_ms_ids<true><<<mgrid, 256, 0, c.stream>>>(ms, uint64_t(g.n), bitmap, prefix, slot_id);
+      else
+        k_ms_ids<false><<<mgrid, 256, 0, c.stream>>>(ms, uint64_t(g.n), bitmap, prefix, slot_id);
+      CK_LAUNCH("k_ms_ids");
+    }
     c.mark(5);
     o.n_tris = int64_t(total);
     o.tris = tris;
