@@ -680,7 +680,7 @@ __global__ void k_set_ids(const uint64_t* __restrict__ sorted_slots, int64_t r, 
 // many per SM, so one CTA's barriers overlap the others' work.
 constexpr int RY = 4, B_THREADS = 32 * RY;
 constexpr int LW = TX + 1, LQ = LW * (RY + 1);  // 33 x 17 = 561 vertices per layer
-constexpr int kBatch = 8, kRing = 16;  // ring >= kBatch + 1, power of two
+constexpr int kBatch = 4, kRing = 8;  // ring >= kBatch + 1, power of two
 static_assert(kRing >= kBatch + 1 && (kRing & (kRing - 1)) == 0, "ring size");
 __constant__ uint32_t c_mrows[PLMSS_TET_ROWS];
 __constant__ uint16_t c_mcases[32];
@@ -808,6 +808,12 @@ __global__ void __launch_bounds__(B_THREADS, 8) k_brick(const BrickArgs a) {
   const uint32_t cy = gy0 + uint32_t(w);
   const bool row_ok = cy + 1 < d.Y && tx < a.nxc;
   const bool cube_ok = row_ok && gx0 + uint32_t(lane) + 1 < d.X;
+  // this thread's cube class and its row's chunk count, advanced one cube
+  // layer at a time
+  const uint64_t CX = d.X - 1, CXY = uint64_t(d.X - 1) * (d.Y - 1);
+  uint8_t* clsp = a.cls + (uint64_t(gx0) + lane + CX * cy + CXY * gz0);
+  uint64_t* chp = a.chunk + (uint64_t(cy) + uint64_t(d.Y - 1) * gz0) * a.nxc + tx;
+  const uint64_t chstep = uint64_t(d.Y - 1) * a.nxc;
   // per-thread cache of the last pair seen in each of its two columns: key,
   // token, vertex ids of its maximum / minimum
   Key lkey0 = Key(~Key(0)), lkey1 = Key(~Key(0));
@@ -912,7 +918,6 @@ __global__ void __launch_bounds__(B_THREADS, 8) k_brick(const BrickArgs a) {
       const uint32_t* lo = ring + ((z - 1) & (kRing - 1)) * LQ;
       const uint32_t* cur = ring + (z & (kRing - 1)) * LQ;
       const int o = w * LW + lane;
-      const uint32_t cz = gz0 + uint32_t(z) - 1;
       uint32_t cnt = 0;
       if (cube_ok) {
         uint32_t c[8];
@@ -946,11 +951,12 @@ __global__ void __launch_bounds__(B_THREADS, 8) k_brick(const BrickArgs a) {
             cls = 0xffu;
           }
         }
-        a.cls[uint64_t(gx0 + uint32_t(lane)) + uint64_t(d.X - 1) * (uint64_t(cy) + uint64_t(d.Y - 1) * cz)] =
-            uint8_t(cls);
+        *clsp = uint8_t(cls);
       }
       const uint32_t tot = __any_sync(0xffffffffu, cnt != 0) ? __reduce_add_sync(0xffffffffu, cnt) : 0u;
-      if (lane == 0 && row_ok) a.chunk[(uint64_t(cy) + uint64_t(d.Y - 1) * cz) * a.nxc + tx] = tot;
+      if (lane == 0 && row_ok) *chp = tot;
+      clsp += CXY;
+      chp += chstep;
     }
     __syncthreads();
   }
