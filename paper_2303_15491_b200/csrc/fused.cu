@@ -307,18 +307,25 @@ __global__ void __launch_bounds__(A_THREADS, 1)
   uint32_t live = live_d;
   for (;;) {
     uint32_t m = live, next = 0;
+    // two vertices per iteration: four independent load chains in flight
     while (m) {
       const int lz = 31 - __clz(m);
       const uint32_t bit = 1u << lz;
       m ^= bit;
-      const int h = hc + (lz + 1) * PXY;
-      const uint32_t p1 = Pd[h], q1 = Pa[h];
-      const uint32_t p2 = Pd[p1], q2 = Pa[q1];
-      const uint32_t p3 = Pd[p2], q3 = Pa[q2];
-      const uint32_t p4 = Pd[p3], q4 = Pa[q3];
+      const int lz2 = m ? 31 - __clz(m) : lz;  // a second live vertex, or the first again
+      const uint32_t bit2 = 1u << lz2;
+      m &= ~bit2;
+      const int h = hc + (lz + 1) * PXY, h2 = hc + (lz2 + 1) * PXY;
+      const uint32_t p1 = Pd[h], q1 = Pa[h], r1 = Pd[h2], s1 = Pa[h2];
+      const uint32_t p2 = Pd[p1], q2 = Pa[q1], r2 = Pd[r1], s2 = Pa[s1];
+      const uint32_t p3 = Pd[p2], q3 = Pa[q2], r3 = Pd[r2], s3 = Pa[s2];
+      const uint32_t p4 = Pd[p3], q4 = Pa[q3], r4 = Pd[r3], s4 = Pa[s3];
       Pd[h] = uint16_t(p4);
       Pa[h] = uint16_t(q4);
+      Pd[h2] = uint16_t(r4);
+      Pa[h2] = uint16_t(s4);
       if (p4 != p3 || q4 != q3) next |= bit;
+      if (r4 != r3 || s4 != s3) next |= bit2;
     }
     live = next;
     if (!__syncthreads_or(live != 0)) break;
