@@ -89,6 +89,19 @@ __host__ __device__ constexpr uint32_t stencil_code(int s) {
        : s == 12 ? 0x29 : 0x2a;
 }
 
+// Shell cell j of the 34^3 pointer space, j in [0, kShell): the z = 0 and
+// z = 33 layers, then the side walls layer by layer (rows y = 0, y = 33,
+// then columns x = 0, x = 33).
+constexpr int kShell = 2 * 34 * 34 + 32 * 4 * 33;  // 6536
+__device__ __forceinline__ uint32_t shell_cell(uint32_t j) {
+  constexpr uint32_t L = 34 * 34, W = 4 * 33;
+  if (j < 2 * L) return j < L ? j : j - L + 33 * L;
+  const uint32_t k = j - 2 * L, hz = 1 + k / W, c = k - (hz - 1) * W;
+  const uint32_t col = c < 34 ? c : c < 68 ? (c - 34) + 34 * 33 : c < 100 ? 34 * (c - 67) : 33 + 34 * (c - 99);
+  return col + hz * L;
+}
+constexpr int kShellPerThread = (kShell + 1023) / 1024;  // 7
+
 struct ACounters {
   unsigned long long n_max, n_min, n_exit, n_tt;
   int overflow;
@@ -261,17 +274,11 @@ __global__ void __launch_bounds__(A_THREADS, 1)
   //    brick vertex is an exit: its code byte becomes kExitMark (readers
   //    treat 0xff and kExitMark alike).
   uint32_t live_d = 0, mmax = 0, mmin = 0;
-  Pd[hc] = uint16_t(hc);
-  Pa[hc] = uint16_t(hc);
-  Pd[hc + (TZ + 1) * PXY] = uint16_t(hc + (TZ + 1) * PXY);
-  Pa[hc + (TZ + 1) * PXY] = uint16_t(hc + (TZ + 1) * PXY);
-  int shell_col = -1;
-  if (tid < 4 * (PX - 1)) {  // 132 shell columns: rows y = 0, y = 33, then x = 0, x = 33
-    shell_col = tid < PX ? tid : tid < 2 * PX ? (tid - PX) + PX * (PX - 1) : tid < 2 * PX + TY
-                                                  ? PX * (tid - 2 * PX + 1)
-                                                  : (PX - 1) + PX * (tid - 2 * PX - TY + 1);
-    for (int z = 0; z < TZ + 2; ++z) {
-      const int h = shell_col + z * PXY;
+#pragma unroll
+  for (int i = 0; i < kShellPerThread; ++i) {
+    const uint32_t j = uint32_t(tid + i * A_THREADS);
+    if (j < uint32_t(kShell)) {
+      const uint32_t h = shell_cell(j);
       Pd[h] = uint16_t(h);
       Pa[h] = uint16_t(h);
     }
@@ -333,15 +340,17 @@ __global__ void __launch_bounds__(A_THREADS, 1)
 
   // 5. terminal table of the brick: TT[base ..) = exit cells, then maxima,
   //    then minima (brick-major cell indices), one atomic per brick. Exit
-  //    cells: this column's two z-shell cells (bits 0, 1) and, for threads
-  //    0..131, a whole shell column (bits 2..35). The local index of every
+  //    cells: shell cells tid + 1024 i (kShellPerThread per thread). The local index of every
   //    terminal is written into the pointer arrays AT the terminal (exits in
   //    both, extrema in their own direction's array).
-  uint64_t mex = uint64_t(code[hc] == kExitMark) | uint64_t(code[hc + (TZ + 1) * PXY] == kExitMark) << 1;
-  if (shell_col >= 0)
-    for (int z = 0; z < TZ + 2; ++z) mex |= uint64_t(code[shell_col + z * PXY] == kExitMark) << (z + 2);
+  uint32_t mex = 0;  // bit i: shell cell tid + 1024 i is an exit
+#pragma unroll
+  for (int i = 0; i < kShellPerThread; ++i) {
+    const uint32_t j = uint32_t(tid + i * A_THREADS);
+    if (j < uint32_t(kShell)) mex |= uint32_t(code[shell_cell(j)] == kExitMark) << i;
+  }
 
-  const uint32_t cnt[3] = {uint32_t(__popcll(mex)), uint32_t(__popc(mmax)), uint32_t(__popc(mmin))};
+  const uint32_t cnt[3] = {uint32_t(__popc(mex)), uint32_t(__popc(mmax)), uint32_t(__popc(mmin))};
   uint32_t pre[3];
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
@@ -390,9 +399,9 @@ __global__ void __launch_bounds__(A_THREADS, 1)
   uint64_t gpos_max = s_lbase[1] + (lk[1] - te), gpos_min = s_lbase[2] + (lk[2] - te - tm);
   const uint32_t bm0 = bt << 15;  // brick-major index of the brick's cell 0
   while (mex) {
-    const int b = __ffsll(mex) - 1;
+    const int b = __ffs(mex) - 1;
     mex &= mex - 1;
-    const uint32_t h = b == 0 ? uint32_t(hc) : b == 1 ? uint32_t(hc + (TZ + 1) * PXY) : uint32_t(shell_col + (b - 2) * PXY);
+    const uint32_t h = shell_cell(uint32_t(tid + b * A_THREADS));
     // the shell cell's brick and local coordinates (shell index 0 -> 31 of
     // the previous brick, 33 -> 0 of the next)
     const int hz = int(h / PXY), r = int(h) - hz * PXY, hy = r / PX, hx = r - hy * PX;
