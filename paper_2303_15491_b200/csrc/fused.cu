@@ -804,13 +804,80 @@ struct BrickArgs {
   int* overflow;
 };
 
-// Pass C. Region token of a vertex: its dense key (rank_min * nmax +
-// rank_max) or its slot in the region hash set; equal tokens <=> equal
-// (asc, desc) pairs. Writes desc/asc (vertex ids of the two extrema), the
-// token into ms, the bitmap/set, each cube's class and each chunk's count.
+// Pass C1 (k_tokens): every vertex's final pair from its LT indices and its
+// brick's table, written as desc/asc (vertex ids of the two extrema) and as
+// a region token in ms: the dense key (rank_min * nmax + rank_max) or the
+// vertex's slot in the region hash set; equal tokens <=> equal (asc, desc)
+// pairs. Thread per (x, y) column of a brick, kTokZ layers of loads in
+// flight per step; the last pair of the column is cached (runs along z).
+constexpr int kTokRows = 8, kTokZ = 8;
+
 template <bool kDense>
-__global__ void __launch_bounds__(B_THREADS, 8) k_brick(const BrickArgs a) {
+__global__ void __launch_bounds__(32 * kTokRows) k_tokens(const BrickArgs a) {
   using Key = typename std::conditional<kDense, uint32_t, unsigned long long>::type;
+  const FDims& d = a.d;
+  const uint32_t bt = blockIdx.x / (TY / kTokRows);
+  const uint32_t tx = bt % d.tx, ty = (bt / d.tx) % d.ty, tz = bt / (d.tx * d.ty);
+  const uint32_t lx = threadIdx.x & 31, ly = (blockIdx.x % (TY / kTokRows)) * kTokRows + (threadIdx.x >> 5);
+  const uint32_t gx = tx * TX + lx, gy = ty * TY + ly, gz0 = tz * TZ;
+  if (gx >= d.X || gy >= d.Y) return;
+  const int nz = int(min(uint32_t(TZ), d.Z - gz0));
+  const uint32_t base = __ldg(reinterpret_cast<const uint32_t*>(a.TB) + 4 * bt);
+  const uint16_t* pd = a.ltd + ((size_t(bt) << 15) | ly << 5 | lx);
+  const uint16_t* pa = a.lta + ((size_t(bt) << 15) | ly << 5 | lx);
+  const uint32_t* fd = a.FD + base;
+  const uint32_t* fa = a.FA + base;
+  uint32_t gv = gx + d.X * (gy + d.Y * gz0);
+  Key lkey = Key(~Key(0));
+  uint32_t ltok = 0;
+  uint2 lgv = make_uint2(0, 0);
+  for (int z0 = 0; z0 < nz; z0 += kTokZ) {
+    uint32_t ld[kTokZ], la[kTokZ];
+#pragma unroll
+    for (int i = 0; i < kTokZ; ++i) {
+      if (z0 + i < nz) {
+        ld[i] = __ldg(pd + (z0 + i) * TX * TY);
+        la[i] = __ldg(pa + (z0 + i) * TX * TY);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < kTokZ; ++i) {
+      if (z0 + i < nz) {
+        ld[i] = __ldg(fd + ld[i]);  // rank of the maximum
+        la[i] = __ldg(fa + la[i]);  // rank of the minimum
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < kTokZ; ++i) {
+      if (z0 + i >= nz) break;
+      const Key key = kDense ? Key(la[i] * a.nmax + ld[i]) : Key((uint64_t(la[i]) << 32) | ld[i]);
+      if (key != lkey) {
+        if (kDense) {
+          ltok = uint32_t(key);
+          const uint32_t bit = 1u << (ltok & 31);
+          uint32_t* wp = a.bitmap + (ltok >> 5);
+          if (!(*wp & bit)) atomicOr(wp, bit);
+        } else {
+          const uint64_t slot = set_insert_slot(a.fset, a.fmask, uint64_t(key));
+          if (slot == ~uint64_t(0)) *a.overflow = 1;
+          ltok = uint32_t(slot);
+        }
+        lgv = make_uint2(__ldg(a.maxs + ld[i]), __ldg(a.mins + la[i]));
+        lkey = key;
+      }
+      a.desc[gv] = lgv.x;
+      a.asc[gv] = lgv.y;
+      a.ms[gv] = ltok;
+      gv += d.XY;
+    }
+  }
+}
+
+// Pass C2 (k_brick): cube classes and separator counts per 32-cube chunk
+// from the region tokens. CTA = RY cube rows of a brick; the vertex layers
+// z = 0..32 of those rows plus the +x / +y halo stream through a shared-memory
+// ring kBatch layers at a time; warp w handles cube row w, lane = cube x.
+__global__ void __launch_bounds__(B_THREADS, 8) k_brick(const BrickArgs a) {
   __shared__ uint32_t ring[kRing * LQ];
   const FDims& d = a.d;
   const uint32_t bt = blockIdx.x / (TY / RY), yb = (blockIdx.x % (TY / RY)) * RY;  // brick, first row of this CTA
@@ -818,7 +885,6 @@ __global__ void __launch_bounds__(B_THREADS, 8) k_brick(const BrickArgs a) {
   const uint32_t gx0 = tx * TX, gy0 = ty * TY + yb, gz0 = tz * TZ;
   if (gy0 >= d.Y) return;  // rows of a brick cut by the volume
   const int tid = int(threadIdx.x), lane = tid & 31, w = tid >> 5;
-  const uint32_t* TBw = reinterpret_cast<const uint32_t*>(a.TB);
   const int nl = int(min(uint32_t(TZ + 1), d.Z - gz0));  // vertex layers of the brick + halo
   // this thread's cube column: x = lane, y = w
   const uint32_t cy = gy0 + uint32_t(w);
@@ -830,103 +896,32 @@ __global__ void __launch_bounds__(B_THREADS, 8) k_brick(const BrickArgs a) {
   uint8_t* clsp = a.cls + (uint64_t(gx0) + lane + CX * cy + CXY * gz0);
   uint64_t* chp = a.chunk + (uint64_t(cy) + uint64_t(d.Y - 1) * gz0) * a.nxc + tx;
   const uint64_t chstep = uint64_t(d.Y - 1) * a.nxc;
-  // per-thread cache of the last pair seen in each of its two columns: key,
-  // token, vertex ids of its maximum / minimum
-  Key lkey0 = Key(~Key(0)), lkey1 = Key(~Key(0));
-  uint32_t ltok0 = 0, ltok1 = 0;
-  uint2 lgv0 = make_uint2(0, 0), lgv1 = make_uint2(0, 0);
+  // the (up to two) ring columns this thread loads: q = tid, tid + B_THREADS
+  const uint32_t* col[2];
+  bool col_ok[2];
+#pragma unroll
+  for (int p = 0; p < 2; ++p) {
+    const int q = tid + p * B_THREADS;
+    const int x = q % LW, y = q / LW;
+    const uint32_t gx = gx0 + uint32_t(x), gy = gy0 + uint32_t(y);
+    col_ok[p] = q < LQ && gx < d.X && gy < d.Y;
+    col[p] = a.ms + (uint64_t(gx) + uint64_t(d.X) * (uint64_t(gy) + uint64_t(d.Y) * gz0));
+  }
 
   for (int z0 = 0; z0 < nl; z0 += kBatch) {
     const int zn = min(kBatch, nl - z0);
-    // ---- load layers z0 .. z0+zn-1 (threads 0..LQ-B_THREADS-1 also take a second q)
-    // full: kBatch layers, all below the halo layer 32 (no predication)
-    auto load_column = [&](auto full, const int q, Key& lkey, uint32_t& ltok, uint2& lgv) {
-      constexpr bool kFull = decltype(full)::value;
-      const int x = q % LW, y = q / LW;
-      const uint32_t gx = gx0 + uint32_t(x), gy = gy0 + uint32_t(y);
-      if (gx >= d.X || gy >= d.Y) {
+    // ---- load layers z0 .. z0+zn-1 of the tokens
 #pragma unroll
-        for (int i = 0; i < kBatch; ++i)
-          if (kFull || i < zn) ring[((z0 + i) & (kRing - 1)) * LQ + q] = ~0u;
-        return;
-      }
-      const uint32_t yy = yb + uint32_t(y);  // row within the brick (32: next brick)
-      const uint32_t nb_lo = (tx + uint32_t(x >> 5)) + d.tx * ((ty + (yy >> 5)) + d.ty * tz);
-      const uint32_t nb_hi = nb_lo + d.tx * d.ty;  // layer 32 lives in the next brick up
-      const uint32_t lxy = uint32_t(x & 31) | (yy & 31) << 5;
-      uint32_t ld[kBatch], la[kBatch];
-      if (kFull) {
-        const uint16_t* pd = a.ltd + ((size_t(nb_lo) << 15) | lxy | uint32_t(z0) << 10);
-        const uint16_t* pa = a.lta + ((size_t(nb_lo) << 15) | lxy | uint32_t(z0) << 10);
+    for (int p = 0; p < 2; ++p) {
+      const int q = tid + p * B_THREADS;
+      if (q >= LQ) break;
+      uint32_t t[kBatch];
 #pragma unroll
-        for (int i = 0; i < kBatch; ++i) {
-          ld[i] = __ldg(pd + i * TX * TY);
-          la[i] = __ldg(pa + i * TX * TY);
-        }
-        const uint32_t base = __ldg(TBw + 4 * nb_lo);
-        const uint32_t* fd = a.FD + base;
-        const uint32_t* fa = a.FA + base;
+      for (int i = 0; i < kBatch; ++i)
+        t[i] = (i < zn && col_ok[p]) ? __ldg(col[p] + uint64_t(z0 + i) * d.XY) : ~0u;
 #pragma unroll
-        for (int i = 0; i < kBatch; ++i) {
-          ld[i] = __ldg(fd + ld[i]);  // table entry replaces the index
-          la[i] = __ldg(fa + la[i]);
-        }
-      } else {
-#pragma unroll
-        for (int i = 0; i < kBatch; ++i) {
-          const int z = z0 + i;
-          if (i < zn) {
-            const uint32_t bm = ((z < TZ ? nb_lo : nb_hi) << 15) | lxy | uint32_t(z & 31) << 10;
-            ld[i] = __ldg(a.ltd + bm);
-            la[i] = __ldg(a.lta + bm);
-          }
-        }
-        const uint32_t base_lo = __ldg(TBw + 4 * nb_lo);
-        const uint32_t base_hi = z0 + zn > TZ ? __ldg(TBw + 4 * nb_hi) : 0u;
-#pragma unroll
-        for (int i = 0; i < kBatch; ++i) {
-          if (i < zn) {
-            const uint32_t base = z0 + i < TZ ? base_lo : base_hi;
-            ld[i] = __ldg(a.FD + base + ld[i]);
-            la[i] = __ldg(a.FA + base + la[i]);
-          }
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < kBatch; ++i) {
-        if (!kFull && i >= zn) break;
-        const int z = z0 + i;
-        const Key key = kDense ? Key(la[i] * a.nmax + ld[i]) : Key((uint64_t(la[i]) << 32) | ld[i]);
-        if (key != lkey) {
-          // a new pair for this column: token, region set, extremum ids
-          if (kDense) {
-            ltok = uint32_t(key);
-            const uint32_t bit = 1u << (ltok & 31);
-            uint32_t* wp = a.bitmap + (ltok >> 5);
-            if (!(*wp & bit)) atomicOr(wp, bit);
-          } else {
-            const uint64_t slot = set_insert_slot(a.fset, a.fmask, uint64_t(key));
-            if (slot == ~uint64_t(0)) *a.overflow = 1;
-            ltok = uint32_t(slot);
-          }
-          lgv = make_uint2(__ldg(a.maxs + ld[i]), __ldg(a.mins + la[i]));
-          lkey = key;
-        }
-        ring[(z & (kRing - 1)) * LQ + q] = ltok;
-        if (x < TX && y < RY && (kFull || z < TZ)) {
-          const uint32_t gv = gx + d.X * (gy + d.Y * (gz0 + uint32_t(z)));
-          a.desc[gv] = lgv.x;
-          a.asc[gv] = lgv.y;
-          a.ms[gv] = ltok;
-        }
-      }
-    };
-    if (zn == kBatch && z0 + kBatch <= TZ) {
-      load_column(std::true_type{}, tid, lkey0, ltok0, lgv0);
-      if (tid < LQ - B_THREADS) load_column(std::true_type{}, tid + B_THREADS, lkey1, ltok1, lgv1);
-    } else {
-      load_column(std::false_type{}, tid, lkey0, ltok0, lgv0);
-      if (tid < LQ - B_THREADS) load_column(std::false_type{}, tid + B_THREADS, lkey1, ltok1, lgv1);
+      for (int i = 0; i < kBatch; ++i)
+        if (i < zn) ring[((z0 + i) & (kRing - 1)) * LQ + q] = t[i];
     }
     __syncthreads();
     // ---- cube layers z-1 whose two vertex layers are loaded
@@ -1294,6 +1289,7 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
     ba.chunk = chunk;
     ba.cls = c.get_t<uint8_t>(S_MASK, uint64_t(g.cubes ? g.cubes : 1));
     const unsigned cgrid = unsigned((TY / RY) * ntiles);
+    const unsigned tgrid = unsigned((TY / kTokRows) * ntiles);
     const uint64_t nbits = uint64_t(o.n_max) * uint64_t(o.n_min);
     const bool dense = nbits < (uint64_t(1) << 32) && c.combine_path != 2;  // PLMSS_OPT_COMBINE_PATH 2: hash
     uint64_t* keys = nullptr;
@@ -1305,8 +1301,8 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
       bitmap = c.get_t<uint32_t>(S_BITMAP, nw);
       CK(cudaMemsetAsync(bitmap, 0, nw * 4, c.stream));
       ba.bitmap = bitmap;
-      k_brick<true><<<cgrid, B_THREADS, 0, c.stream>>>(ba);
-      CK_LAUNCH("k_brick");
+      k_tokens<true><<<tgrid, 32 * kTokRows, 0, c.stream>>>(ba);
+      CK_LAUNCH("k_tokens");
       const int64_t nb = int64_t((nw + kWB - 1) / kWB);
       uint64_t* bsum = c.get_t<uint64_t>(S_HASH_V, nb);
       k_bitmap_count<<<unsigned(nb), 256, 0, c.stream>>>(bitmap, nw, bsum);
@@ -1332,8 +1328,8 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
         CK(cudaMemsetAsync(flag, 0, 4, c.stream));
         ba.fset = fset;
         ba.fmask = fcap - 1;
-        k_brick<false><<<cgrid, B_THREADS, 0, c.stream>>>(ba);
-        CK_LAUNCH("k_brick");
+        k_tokens<false><<<tgrid, 32 * kTokRows, 0, c.stream>>>(ba);
+        CK_LAUNCH("k_tokens");
         CK(cudaMemcpyAsync(c.h_pinned, flag, 4, cudaMemcpyDeviceToHost, c.stream));
         c.sync();
         if (*reinterpret_cast<int*>(c.h_pinned) == 0) break;
@@ -1361,6 +1357,9 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
       c.stats[2] = int64_t(fcap);
     }
     o.n_regions = R;
+    // cube classes and separator counts from the tokens
+    k_brick<<<cgrid, B_THREADS, 0, c.stream>>>(ba);
+    CK_LAUNCH("k_brick");
     const uint64_t total = nchunks ? exclusive_scan_u64(c, chunk, int64_t(nchunks), true) : 0;
     c.mark(4);
     // ---- D: separator records at their chunk offsets; ms tokens -> ids
