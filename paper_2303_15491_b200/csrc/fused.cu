@@ -896,6 +896,8 @@ __global__ void __launch_bounds__(B_THREADS, 8) k_brick(const BrickArgs a) {
   uint8_t* clsp = a.cls + (uint64_t(gx0) + lane + CX * cy + CXY * gz0);
   uint64_t* chp = a.chunk + (uint64_t(cy) + uint64_t(d.Y - 1) * gz0) * a.nxc + tx;
   const uint64_t chstep = uint64_t(d.Y - 1) * a.nxc;
+  uint32_t pf[4] = {0, 0, 0, 0};  // top face of this thread's previous cube
+  bool have_prev = false;
   // the (up to two) ring columns this thread loads: q = tid, tid + B_THREADS
   const uint32_t* col[2];
   bool col_ok[2];
@@ -932,20 +934,35 @@ __global__ void __launch_bounds__(B_THREADS, 8) k_brick(const BrickArgs a) {
       uint32_t cnt = 0;
       if (cube_ok) {
         uint32_t c[8];
-        c[0] = lo[o];
-        c[1] = lo[o + 1];
-        c[2] = lo[o + LW];
-        c[3] = lo[o + LW + 1];
+        // bottom face = the previous cube layer's top face (registers)
+        if (have_prev) {
+          c[0] = pf[0];
+          c[1] = pf[1];
+          c[2] = pf[2];
+          c[3] = pf[3];
+        } else {
+          c[0] = lo[o];
+          c[1] = lo[o + 1];
+          c[2] = lo[o + LW];
+          c[3] = lo[o + LW + 1];
+        }
         c[4] = cur[o];
         c[5] = cur[o + 1];
         c[6] = cur[o + LW];
         c[7] = cur[o + LW + 1];
-        // corners equal to corner 0 (bit i); 0xff: one region, no separator
-        uint32_t m8 = 1u;
-#pragma unroll
-        for (int i = 1; i < 8; ++i) m8 |= uint32_t(c[i] == c[0]) << i;
+        pf[0] = c[4];
+        pf[1] = c[5];
+        pf[2] = c[6];
+        pf[3] = c[7];
+        have_prev = true;
+        const bool uni = c[1] == c[0] && c[2] == c[0] && c[3] == c[0] && c[4] == c[0] && c[5] == c[0] &&
+                         c[6] == c[0] && c[7] == c[0];
         uint32_t cls = 0;
-        if (m8 != 0xffu) {
+        if (!uni) {
+          // corners equal to corner 0 (bit i)
+          uint32_t m8 = 1u;
+#pragma unroll
+          for (int i = 1; i < 8; ++i) m8 |= uint32_t(c[i] == c[0]) << i;
           // the lowest corner with another label; two labels iff every
           // corner carries one of the two (the common case on a separator)
           uint32_t b = c[7];
