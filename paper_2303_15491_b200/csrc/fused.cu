@@ -696,7 +696,7 @@ __global__ void k_set_ids(const uint64_t* __restrict__ sorted_slots, int64_t r, 
 // many per SM, so one CTA's barriers overlap the others' work.
 constexpr int RY = 4, B_THREADS = 32 * RY;
 constexpr int LW = TX + 1, LQ = LW * (RY + 1);  // 33 x 17 = 561 vertices per layer
-constexpr int kBatch = 4, kRing = 8;  // ring >= kBatch + 1, power of two
+constexpr int kBatch = 8, kRing = 16;  // ring >= kBatch + 1, power of two
 static_assert(kRing >= kBatch + 1 && (kRing & (kRing - 1)) == 0, "ring size");
 __constant__ uint32_t c_mrows[PLMSS_TET_ROWS];
 __constant__ uint16_t c_mcases[32];
@@ -810,7 +810,7 @@ struct BrickArgs {
 // vertex's slot in the region hash set; equal tokens <=> equal (asc, desc)
 // pairs. Thread per (x, y) column of a brick, kTokZ layers of loads in
 // flight per step; the last pair of the column is cached (runs along z).
-constexpr int kTokRows = 8, kTokZ = 8;
+constexpr int kTokRows = 8, kTokZ = 16;
 
 template <bool kDense>
 __global__ void __launch_bounds__(32 * kTokRows) k_tokens(const BrickArgs a) {
