@@ -1003,8 +1003,7 @@ struct EmitArgs {
   uint64_t nchunks, total;
   const uint64_t* off;   // exclusive chunk offsets
   const uint8_t* cls;
-  const uint32_t* tok;   // ms, still holding region tokens
-  const uint32_t *bitmap, *prefix, *slot_id;
+  const uint32_t* ids;   // ms (dense MS ids)
   plmss_tri* out;
 };
 
@@ -1013,7 +1012,6 @@ struct EmitArgs {
 // marching.cpp:116-215). Warps walk whole cube rows; lane = cube of the chunk;
 // records are dealt out one per lane (consecutive lanes write consecutive
 // 16-byte records).
-template <bool kDense>
 __global__ void __launch_bounds__(256) k_emit_chunks(const EmitArgs a) {
   const int lane = threadIdx.x & 31;
   const uint32_t CX = a.X - 1, CY = a.Y - 1, XY = a.X * a.Y;
@@ -1021,10 +1019,12 @@ __global__ void __launch_bounds__(256) k_emit_chunks(const EmitArgs a) {
   const uint32_t warps = gridDim.x * (blockDim.x / 32);
   for (uint32_t r = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); r < nrows; r += warps) {
     const uint32_t cz = r / CY, cy = r - cz * CY;
+    uint64_t next = a.off[uint64_t(r) * a.nxc];
     for (uint32_t xs = 0; xs < a.nxc; ++xs) {
       const uint64_t ch = uint64_t(r) * a.nxc + xs;
-      const uint64_t base = a.off[ch];
-      const uint32_t T = uint32_t((ch + 1 < a.nchunks ? a.off[ch + 1] : a.total) - base);
+      const uint64_t base = next;
+      next = ch + 1 < a.nchunks ? a.off[ch + 1] : a.total;
+      const uint32_t T = uint32_t(next - base);
       if (T == 0) continue;
       const uint32_t cx = 32 * xs + uint32_t(lane);
       const uint64_t q0 = uint64_t(32 * xs) + uint64_t(CX) * r;  // cube id of lane 0's cube
@@ -1035,15 +1035,14 @@ __global__ void __launch_bounds__(256) k_emit_chunks(const EmitArgs a) {
       if (cls == 0xffu) {
         uint32_t c[8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) c[i] = __ldg(a.tok + v0 + corner_off(uint32_t(i)));
+        for (int i = 0; i < 8; ++i) c[i] = __ldg(a.ids + v0 + corner_off(uint32_t(i)));
         code6 = cube_codes(c, g_tlut, cnt);
       } else if (cls != 0) {
         // two labels: corner 0's and that of the lowest corner outside its set
         cnt = g_two_cnt[cls >> 1];
         code6 = 0x80000000u | cls;
-        const uint32_t i0 = token_id<kDense>(__ldg(a.tok + v0), a.bitmap, a.prefix, a.slot_id);
-        const uint32_t ib = token_id<kDense>(__ldg(a.tok + v0 + corner_off(uint32_t(__ffs(~cls) - 1))), a.bitmap,
-                                             a.prefix, a.slot_id);
+        const uint32_t i0 = __ldg(a.ids + v0);
+        const uint32_t ib = __ldg(a.ids + v0 + corner_off(uint32_t(__ffs(~cls) - 1)));
         lo2 = min(i0, ib);
         hi2 = max(i0, ib);
       }
@@ -1092,10 +1091,8 @@ __global__ void __launch_bounds__(256) k_emit_chunks(const EmitArgs a) {
           const uint32_t cb = (0x442211u >> (4 * t)) & 15, cc = (0x656353u >> (4 * t)) & 15;
           auto corner = [&](uint32_t p) { return p == 0 ? 0u : (p == 1 ? cb : (p == 2 ? cc : 7u)); };
           const uint32_t vs = v0 - uint32_t(lane) + uint32_t(src);
-          la = token_id<kDense>(__ldg(a.tok + vs + corner_off(corner((row >> 12) & 3))), a.bitmap, a.prefix,
-                                a.slot_id);
-          lb = token_id<kDense>(__ldg(a.tok + vs + corner_off(corner((row >> 14) & 3))), a.bitmap, a.prefix,
-                                a.slot_id);
+          la = __ldg(a.ids + vs + corner_off(corner((row >> 12) & 3)));
+          lb = __ldg(a.ids + vs + corner_off(corner((row >> 14) & 3)));
         }
         const uint64_t cr64 = ((6ull * (q0 + uint32_t(src)) + t) << 6) | uint64_t(rowi);
         *reinterpret_cast<uint4*>(a.out + base + j) =
@@ -1379,7 +1376,15 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
     CK_LAUNCH("k_brick");
     const uint64_t total = nchunks ? exclusive_scan_u64(c, chunk, int64_t(nchunks), true) : 0;
     c.mark(4);
-    // ---- D: separator records at their chunk offsets; ms tokens -> ids
+    // ---- D: ms tokens -> dense ids; separator records at their chunk offsets
+    {
+      const unsigned mgrid = unsigned((uint64_t(g.n) + 1023) / 1024);
+      if (dense)
+        k_ms_ids<true><<<mgrid, 256, 0, c.stream>>>(ms, uint64_t(g.n), bitmap, prefix, slot_id);
+      else
+        k_ms_ids<false><<<mgrid, 256, 0, c.stream>>>(ms, uint64_t(g.n), bitmap, prefix, slot_id);
+      CK_LAUNCH("k_ms_ids");
+    }
     plmss_tri* tris = c.get_t<plmss_tri>(S_TRIS, total ? total : 1);
     if (total) {
       EmitArgs ea{};
@@ -1391,26 +1396,12 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
       ea.total = total;
       ea.off = chunk;
       ea.cls = ba.cls;
-      ea.tok = ms;
-      ea.bitmap = bitmap;
-      ea.prefix = prefix;
-      ea.slot_id = slot_id;
+      ea.ids = ms;
       ea.out = tris;
       const uint64_t nrows = uint64_t(g.Y - 1) * uint64_t(g.Z - 1);
       const unsigned egrid = unsigned(std::min<uint64_t>((nrows + 7) / 8, uint64_t(c.sm_count) * 64));
-      if (dense)
-        k_emit_chunks<true><<<egrid, 256, 0, c.stream>>>(ea);
-      else
-        k_emit_chunks<false><<<egrid, 256, 0, c.stream>>>(ea);
+      k_emit_chunks<<<egrid, 256, 0, c.stream>>>(ea);
       CK_LAUNCH("k_emit_chunks");
-    }
-    {
-      const unsigned mgrid = unsigned((uint64_t(g.n) + 1023) / 1024);
-      if (dense)
-        k_ms_ids<true><<<mgrid, 256, 0, c.stream>>>(ms, uint64_t(g.n), bitmap, prefix, slot_id);
-      else
-        k_ms_ids<false><<<mgrid, 256, 0, c.stream>>>(ms, uint64_t(g.n), bitmap, prefix, slot_id);
-      CK_LAUNCH("k_ms_ids");
     }
     c.mark(5);
     o.n_tris = int64_t(total);
