@@ -149,6 +149,7 @@ __global__ void __launch_bounds__(A_THREADS, 1)
   __shared__ __align__(8) uint64_t s_bar;
   __shared__ uint32_t s_wcnt[A_THREADS / 32][3];
   __shared__ uint32_t s_tot[3];
+  __shared__ uint32_t s_eoff[kShellPerThread][A_THREADS / 32];
   __shared__ unsigned long long s_lbase[3];
 
   const uint32_t bt = blockIdx.x;
@@ -349,6 +350,13 @@ __global__ void __launch_bounds__(A_THREADS, 1)
     const uint32_t j = uint32_t(tid + i * A_THREADS);
     if (j < uint32_t(kShell)) mex |= uint32_t(code[shell_cell(j)] == kExitMark) << i;
   }
+  // exits are numbered in shell order (j): per (i, warp) counts, scanned
+  // below by warp 0
+#pragma unroll
+  for (int i = 0; i < kShellPerThread; ++i) {
+    const uint32_t b = __ballot_sync(0xffffffffu, (mex >> i) & 1u);
+    if (lane == 0) s_eoff[i][tid >> 5] = uint32_t(__popc(b));
+  }
 
   const uint32_t cnt[3] = {uint32_t(__popc(mex)), uint32_t(__popc(mmax)), uint32_t(__popc(mmin))};
   uint32_t pre[3];
@@ -377,6 +385,21 @@ __global__ void __launch_bounds__(A_THREADS, 1)
       s_wcnt[lane][k] = inc - t;
       if (lane == 31) s_tot[k] = inc;
     }
+    {
+      uint32_t run = 0;
+#pragma unroll
+      for (int i = 0; i < kShellPerThread; ++i) {
+        const uint32_t v = s_eoff[i][lane];
+        uint32_t inc = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+          if (lane >= o) inc += u;
+        }
+        s_eoff[i][lane] = run + inc - v;
+        run += __shfl_sync(0xffffffffu, inc, 31);
+      }
+    }
     __syncwarp();
     if (lane == 0) {
       const uint32_t te = s_tot[0], tm = s_tot[1], tn = s_tot[2];
@@ -398,9 +421,12 @@ __global__ void __launch_bounds__(A_THREADS, 1)
   lk[2] += te + tm;
   uint64_t gpos_max = s_lbase[1] + (lk[1] - te), gpos_min = s_lbase[2] + (lk[2] - te - tm);
   const uint32_t bm0 = bt << 15;  // brick-major index of the brick's cell 0
-  while (mex) {
-    const int b = __ffs(mex) - 1;
-    mex &= mex - 1;
+#pragma unroll 1
+  for (int b = 0; b < kShellPerThread; ++b) {
+    const bool ex = (mex >> b) & 1u;
+    const uint32_t bal = __ballot_sync(0xffffffffu, ex);
+    if (!ex) continue;
+    lk[0] = s_eoff[b][tid >> 5] + __popc(bal & ((1u << lane) - 1u));
     const uint32_t h = shell_cell(uint32_t(tid + b * A_THREADS));
     // the shell cell's brick and local coordinates (shell index 0 -> 31 of
     // the previous brick, 33 -> 0 of the next)
@@ -412,7 +438,6 @@ __global__ void __launch_bounds__(A_THREADS, 1)
     if (tbase + lk[0] < tt_cap) TT[tbase + lk[0]] = bm;
     Pd[h] = uint16_t(lk[0]);
     Pa[h] = uint16_t(lk[0]);
-    ++lk[0];
   }
   uint32_t m = mmax;
   while (m) {
