@@ -152,21 +152,25 @@ __global__ void __launch_bounds__(A_THREADS, 1)
   __shared__ uint32_t s_eoff[kShellPerThread][A_THREADS / 32];
   __shared__ unsigned long long s_lbase[3];
 
-  const uint32_t bt = blockIdx.x;
-  const uint32_t tx = bt % d.tx, ty = (bt / d.tx) % d.ty, tz = bt / (d.tx * d.ty);
-  const int gx0 = int(tx * TX), gy0 = int(ty * TY), gz0 = int(tz * TZ);
   const int tid = int(threadIdx.x);
   const int lane = tid & 31;
   const int lx = tid & 31, ly = tid >> 5;
+  if (kTMA && tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s_bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const uint32_t ntiles = d.tx * d.ty * d.tz;
+  uint32_t phase = 0;
+  // persistent: one CTA per SM walks the bricks; the next brick's field box
+  // is prefetched into L2 while this one is processed
+  for (uint32_t bt = blockIdx.x; bt < ntiles; bt += gridDim.x, phase ^= 1u) {
+  const uint32_t tx = bt % d.tx, ty = (bt / d.tx) % d.ty, tz = bt / (d.tx * d.ty);
+  const int gx0 = int(tx * TX), gy0 = int(ty * TY), gz0 = int(tz * TZ);
 
   // 1. field box
   if (kTMA) {
     const uint32_t bar = smem_u32(&s_bar);
-    if (tid == 0) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
     if (tid == 0) {
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(uint32_t(HN * 4))
                    : "memory");
@@ -208,11 +212,19 @@ __global__ void __launch_bounds__(A_THREADS, 1)
     }
     dup[tid] = dl;  // dup[256 + c] == ddn[c]
   }
-  if (kTMA)
+  if (kTMA) {
     asm volatile(
-        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n @!p bra WAIT_%=;\n}" ::"r"(
-            smem_u32(&s_bar))
+        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(
+            smem_u32(&s_bar)), "r"(phase)
         : "memory");
+    const uint32_t nx = bt + gridDim.x;
+    if (tid == 0 && nx < ntiles) {
+      const uint32_t ntx = nx % d.tx, nty = (nx / d.tx) % d.ty, ntz = nx / (d.tx * d.ty);
+      asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(&tmap),
+                   "r"(int(ntx * TX) - HXO), "r"(int(nty * TY) - 1), "r"(int(ntz * TZ) - 1)
+                   : "memory");
+    }
+  }
   __syncthreads();
 
   // 2. steepest hops
@@ -480,6 +492,8 @@ __global__ void __launch_bounds__(A_THREADS, 1)
       od[TX * TY * lz] = (mmax & bit) ? uint16_t(pd) : Pd[pd];
       oa[TX * TY * lz] = (mmin & bit) ? uint16_t(pa) : Pa[pa];
     }
+  }
+  __syncthreads();  // shared memory is reused by the next brick
   }
 }
 
@@ -1237,10 +1251,10 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
     CK(cudaMemsetAsync(&ctr->bad, 0xff, 4, c.stream));
     c.mark(0);
     if (use_tma)
-      k_tile_segment<true><<<unsigned(ntiles), A_THREADS, kASmem, c.stream>>>(
+      k_tile_segment<true><<<unsigned(std::min<uint64_t>(ntiles, uint64_t(c.sm_count))), A_THREADS, kASmem, c.stream>>>(
           tmap, field, d, maxima, minima, max_tt, min_tt, ext_cap, TT, tt_cap, TB, ltd, lta, ctr);
     else
-      k_tile_segment<false><<<unsigned(ntiles), A_THREADS, kASmem, c.stream>>>(
+      k_tile_segment<false><<<unsigned(std::min<uint64_t>(ntiles, uint64_t(c.sm_count))), A_THREADS, kASmem, c.stream>>>(
           tmap, field, d, maxima, minima, max_tt, min_tt, ext_cap, TT, tt_cap, TB, ltd, lta, ctr);
     CK_LAUNCH("k_tile_segment");
     c.mark(1);
