@@ -45,11 +45,11 @@ B_PER_TRI = 16
 STAGES = ["tile_segment", "exit_resolve", "extrema_sort", "finalize_ids", "march"]
 # Compulsory bytes per vertex of each fused stage: tile_segment
 # reads f and writes the two u16 terminal-index arrays; exit_resolve and
-# extrema_sort touch only the terminal tables (~0.12 entries per vertex);
-# finalize_ids (pass C) reads the terminal indices; march (pass D) reads them
-# again and writes desc, asc, ms (+ 16 B per separator triangle).
-STAGE_BYTES_PER_VERTEX = {"tile_segment": 8, "exit_resolve": 0, "extrema_sort": 0, "finalize_ids": 4,
-                          "march": 16}
+# extrema_sort touch only the terminal tables (~0.13 entries per vertex);
+# finalize_ids (pass C) reads the terminal indices and writes the final desc
+# and asc; march (pass D) writes ms (+ 16 B per separator triangle).
+STAGE_BYTES_PER_VERTEX = {"tile_segment": 8, "exit_resolve": 0, "extrema_sort": 0, "finalize_ids": 12,
+                          "march": 4}
 
 
 def peaks():

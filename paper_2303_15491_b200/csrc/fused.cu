@@ -162,8 +162,7 @@ __global__ void __launch_bounds__(A_THREADS, 1)
   __syncthreads();
   const uint32_t ntiles = d.tx * d.ty * d.tz;
   uint32_t phase = 0;
-  // persistent: one CTA per SM walks the bricks; the next brick's field box
-  // is prefetched into L2 while this one is processed
+  // persistent: one CTA per SM walks the bricks
   for (uint32_t bt = blockIdx.x; bt < ntiles; bt += gridDim.x, phase ^= 1u) {
   const uint32_t tx = bt % d.tx, ty = (bt / d.tx) % d.ty, tz = bt / (d.tx * d.ty);
   const int gx0 = int(tx * TX), gy0 = int(ty * TY), gz0 = int(tz * TZ);
@@ -217,13 +216,6 @@ __global__ void __launch_bounds__(A_THREADS, 1)
         "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(
             smem_u32(&s_bar)), "r"(phase)
         : "memory");
-    const uint32_t nx = bt + gridDim.x;
-    if (tid == 0 && nx < ntiles) {
-      const uint32_t ntx = nx % d.tx, nty = (nx / d.tx) % d.ty, ntz = nx / (d.tx * d.ty);
-      asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(&tmap),
-                   "r"(int(ntx * TX) - HXO), "r"(int(nty * TY) - 1), "r"(int(ntz * TZ) - 1)
-                   : "memory");
-    }
   }
   __syncthreads();
 
