@@ -1046,17 +1046,24 @@ struct EmitArgs {
 __global__ void __launch_bounds__(256) k_emit_chunks(const EmitArgs a) {
   const int lane = threadIdx.x & 31;
   const uint32_t CX = a.X - 1, CY = a.Y - 1, XY = a.X * a.Y;
-  const uint32_t nrows = uint32_t(a.nchunks / a.nxc);
-  const uint32_t warps = gridDim.x * (blockDim.x / 32);
-  for (uint32_t r = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); r < nrows; r += warps) {
-    const uint32_t cz = r / CY, cy = r - cz * CY;
-    uint64_t next = a.off[uint64_t(r) * a.nxc];
-    for (uint32_t xs = 0; xs < a.nxc; ++xs) {
-      const uint64_t ch = uint64_t(r) * a.nxc + xs;
-      const uint64_t base = next;
-      next = ch + 1 < a.nchunks ? a.off[ch + 1] : a.total;
-      const uint32_t T = uint32_t(next - base);
-      if (T == 0) continue;
+  const uint64_t ngroups = (a.nchunks + 31) / 32;
+  const uint64_t warps = uint64_t(gridDim.x) * (blockDim.x / 32);
+  // warps take groups of 32 consecutive chunks; one coalesced load of their
+  // offsets, then only the chunks with records
+  for (uint64_t grp = uint64_t(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5); grp < ngroups; grp += warps) {
+    const uint64_t chl = grp * 32 + uint64_t(lane);
+    const uint64_t my_off = chl < a.nchunks ? a.off[chl] : a.total;
+    uint64_t nx_off = __shfl_down_sync(0xffffffffu, my_off, 1);
+    if (lane == 31) nx_off = chl + 1 < a.nchunks ? a.off[chl + 1] : a.total;
+    uint32_t todo = __ballot_sync(0xffffffffu, nx_off > my_off);
+    while (todo) {
+      const int k = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const uint64_t ch = grp * 32 + uint64_t(k);
+      const uint64_t base = __shfl_sync(0xffffffffu, my_off, k);
+      const uint32_t T = uint32_t(__shfl_sync(0xffffffffu, nx_off, k) - base);
+      const uint32_t r = uint32_t(ch / a.nxc), xs = uint32_t(ch - uint64_t(r) * a.nxc);
+      const uint32_t cz = r / CY, cy = r - cz * CY;
       const uint32_t cx = 32 * xs + uint32_t(lane);
       const uint64_t q0 = uint64_t(32 * xs) + uint64_t(CX) * r;  // cube id of lane 0's cube
       const uint32_t v0 = cx + a.X * cy + XY * cz;                // this lane's min corner
