@@ -118,6 +118,8 @@ int plmss_b200_ctx_create(int device, void* stream, plmss_ctx** out) {
         CK(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
         c.own_stream = true;
       }
+      CK(cudaStreamCreateWithFlags(&c.side, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&c.join, cudaEventDisableTiming));
       CK(cudaMallocHost(&c.h_pinned, 64 * sizeof(uint64_t)));
       for (auto& e : c.ev) CK(cudaEventCreate(&e));
       CK(cudaDeviceGetAttribute(&c.sm_count, cudaDevAttrMultiProcessorCount, device));
@@ -139,6 +141,12 @@ void plmss_b200_ctx_destroy(plmss_ctx* p) {
   cudaStreamSynchronize(c.stream);
   for (auto& e : c.ev)
     if (e) cudaEventDestroy(e);
+  if (c.side) {
+    cudaStreamSynchronize(c.side);
+    cudaStreamDestroy(c.side);
+  }
+  if (c.join) cudaEventDestroy(c.join);
+  for (auto& e : c.slab_ev) cudaEventDestroy(e);
   if (c.h_pinned) cudaFreeHost(c.h_pinned);
   if (c.own_stream) cudaStreamDestroy(c.stream);
   delete p;

@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include <functional>
+#include <vector>
 #include <stdexcept>
 #include <string>
 
@@ -87,6 +88,18 @@ struct Ctx {
   bool timing = false;
   float stage_ms[8] = {};
   cudaEvent_t ev[9] = {};
+  // side stream for the z-slab pipelining of pass C, with its events
+  cudaStream_t side = nullptr;
+  cudaEvent_t join = nullptr;
+  std::vector<cudaEvent_t> slab_ev;
+  cudaEvent_t slab_event(size_t i) {
+    while (slab_ev.size() <= i) {
+      cudaEvent_t e;
+      CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      slab_ev.push_back(e);
+    }
+    return slab_ev[i];
+  }
   plmss_result result{};
   int sm_count = 148;
   int combine_path = 0;  // PLMSS_OPT_COMBINE_PATH

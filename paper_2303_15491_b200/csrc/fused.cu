@@ -820,6 +820,7 @@ __device__ __forceinline__ uint64_t set_insert_slot(unsigned long long* __restri
 
 struct BrickArgs {
   FDims d;
+  uint32_t brick0;  // first brick of the launch (z-slab pipelining)
   uint32_t nxc;  // 32-cube chunks per cube row
   const uint4* TB;
   const uint16_t *ltd, *lta;
@@ -847,7 +848,7 @@ template <bool kDense>
 __global__ void __launch_bounds__(32 * kTokRows) k_tokens(const BrickArgs a) {
   using Key = typename std::conditional<kDense, uint32_t, unsigned long long>::type;
   const FDims& d = a.d;
-  const uint32_t bt = blockIdx.x / (TY / kTokRows);
+  const uint32_t bt = a.brick0 + blockIdx.x / (TY / kTokRows);
   const uint32_t tx = bt % d.tx, ty = (bt / d.tx) % d.ty, tz = bt / (d.tx * d.ty);
   const uint32_t lx = threadIdx.x & 31, ly = (blockIdx.x % (TY / kTokRows)) * kTokRows + (threadIdx.x >> 5);
   const uint32_t gx = tx * TX + lx, gy = ty * TY + ly, gz0 = tz * TZ;
@@ -911,7 +912,7 @@ __global__ void __launch_bounds__(32 * kTokRows) k_tokens(const BrickArgs a) {
 __global__ void __launch_bounds__(B_THREADS, 8) k_brick(const BrickArgs a) {
   __shared__ uint32_t ring[kRing * LQ];
   const FDims& d = a.d;
-  const uint32_t bt = blockIdx.x / (TY / RY), yb = (blockIdx.x % (TY / RY)) * RY;  // brick, first row of this CTA
+  const uint32_t bt = a.brick0 + blockIdx.x / (TY / RY), yb = (blockIdx.x % (TY / RY)) * RY;  // brick, first row
   const uint32_t tx = bt % d.tx, ty = (bt / d.tx) % d.ty, tz = bt / (d.tx * d.ty);
   const uint32_t gx0 = tx * TX, gy0 = ty * TY + yb, gz0 = tz * TZ;
   if (gy0 >= d.Y) return;  // rows of a brick cut by the volume
@@ -1353,8 +1354,27 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
       bitmap = c.get_t<uint32_t>(S_BITMAP, nw);
       CK(cudaMemsetAsync(bitmap, 0, nw * 4, c.stream));
       ba.bitmap = bitmap;
-      k_tokens<true><<<tgrid, 32 * kTokRows, 0, c.stream>>>(ba);
-      CK_LAUNCH("k_tokens");
+      // z-slab pipeline: tokens of brick layer s on the main stream; the
+      // count pass of layer s-1 (which reads layer s's first vertex layer)
+      // on the side stream as soon as they are written
+      const uint32_t bpl = d.tx * d.ty;
+      for (uint32_t sl = 0; sl <= d.tz; ++sl) {
+        if (sl < d.tz) {
+          BrickArgs bs = ba;
+          bs.brick0 = sl * bpl;
+          k_tokens<true><<<bpl * (TY / kTokRows), 32 * kTokRows, 0, c.stream>>>(bs);
+          CK_LAUNCH("k_tokens");
+          CK(cudaEventRecord(c.slab_event(sl), c.stream));
+        }
+        if (sl >= 1) {
+          BrickArgs bs = ba;
+          bs.brick0 = (sl - 1) * bpl;
+          CK(cudaStreamWaitEvent(c.side, c.slab_event(std::min(sl, d.tz - 1)), 0));
+          k_brick<<<bpl * (TY / RY), B_THREADS, 0, c.side>>>(bs);
+          CK_LAUNCH("k_brick");
+        }
+      }
+      CK(cudaEventRecord(c.join, c.side));
       const int64_t nb = int64_t((nw + kWB - 1) / kWB);
       uint64_t* bsum = c.get_t<uint64_t>(S_HASH_V, nb);
       k_bitmap_count<<<unsigned(nb), 256, 0, c.stream>>>(bitmap, nw, bsum);
@@ -1409,9 +1429,13 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
       c.stats[2] = int64_t(fcap);
     }
     o.n_regions = R;
-    // cube classes and separator counts from the tokens
-    k_brick<<<cgrid, B_THREADS, 0, c.stream>>>(ba);
-    CK_LAUNCH("k_brick");
+    if (dense) {
+      CK(cudaStreamWaitEvent(c.stream, c.join, 0));  // count passes done
+    } else {
+      // cube classes and separator counts from the tokens
+      k_brick<<<cgrid, B_THREADS, 0, c.stream>>>(ba);
+      CK_LAUNCH("k_brick");
+    }
     const uint64_t total = nchunks ? exclusive_scan_u64(c, chunk, int64_t(nchunks), true) : 0;
     c.mark(4);
     // ---- D: ms tokens -> dense ids; separator records at their chunk offsets
