@@ -905,6 +905,90 @@ __global__ void __launch_bounds__(32 * kTokRows) k_tokens(const BrickArgs a) {
   }
 }
 
+// k_tokens with the CTA's terminal indices (8 rows x 32 layers of its brick,
+// 2 x 16 KB) staged by two 2-D TMA tensor copies instead of per-thread loads.
+template <bool kDense>
+__global__ void __launch_bounds__(32 * kTokRows) k_tokens_tma(const __grid_constant__ CUtensorMap mld,
+                                                             const __grid_constant__ CUtensorMap mla,
+                                                             const BrickArgs a) {
+  using Key = typename std::conditional<kDense, uint32_t, unsigned long long>::type;
+  __shared__ __align__(128) uint16_t sd[TZ][32 * kTokRows];
+  __shared__ __align__(128) uint16_t sa[TZ][32 * kTokRows];
+  __shared__ __align__(8) uint64_t s_bar;
+  const FDims& d = a.d;
+  const uint32_t grp = blockIdx.x % (TY / kTokRows);
+  const uint32_t bt = a.brick0 + blockIdx.x / (TY / kTokRows);
+  const uint32_t tx = bt % d.tx, ty = (bt / d.tx) % d.ty, tz = bt / (d.tx * d.ty);
+  const uint32_t lx = threadIdx.x & 31, ly = grp * kTokRows + (threadIdx.x >> 5);
+  const uint32_t bar = smem_u32(&s_bar);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(uint32_t(2 * sizeof(sd)))
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            smem_u32(&sd[0][0])),
+        "l"(&mld), "r"(grp * 32 * kTokRows), "r"(bt * TZ), "r"(bar)
+        : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            smem_u32(&sa[0][0])),
+        "l"(&mla), "r"(grp * 32 * kTokRows), "r"(bt * TZ), "r"(bar)
+        : "memory");
+  }
+  const uint32_t base = __ldg(reinterpret_cast<const uint32_t*>(a.TB) + 4 * bt);
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n @!p bra WAIT_%=;\n}" ::"r"(bar)
+      : "memory");
+  const uint32_t gx = tx * TX + lx, gy = ty * TY + ly, gz0 = tz * TZ;
+  if (gx >= d.X || gy >= d.Y) return;
+  const int nz = int(min(uint32_t(TZ), d.Z - gz0));
+  const uint32_t l = threadIdx.x;  // column within the CTA's rows
+  const uint32_t* fd = a.FD + base;
+  const uint32_t* fa = a.FA + base;
+  uint32_t gv = gx + d.X * (gy + d.Y * gz0);
+  Key lkey = Key(~Key(0));
+  uint32_t ltok = 0;
+  uint2 lgv = make_uint2(0, 0);
+  for (int z0 = 0; z0 < nz; z0 += kTokZ) {
+    uint32_t ld[kTokZ], la[kTokZ];
+#pragma unroll
+    for (int i = 0; i < kTokZ; ++i) {
+      if (z0 + i < nz) {
+        ld[i] = __ldg(fd + sd[z0 + i][l]);  // rank of the maximum
+        la[i] = __ldg(fa + sa[z0 + i][l]);  // rank of the minimum
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < kTokZ; ++i) {
+      if (z0 + i >= nz) break;
+      const Key key = kDense ? Key(la[i] * a.nmax + ld[i]) : Key((uint64_t(la[i]) << 32) | ld[i]);
+      if (key != lkey) {
+        if (kDense) {
+          ltok = uint32_t(key);
+          const uint32_t bit = 1u << (ltok & 31);
+          uint32_t* wp = a.bitmap + (ltok >> 5);
+          if (!(*wp & bit)) atomicOr(wp, bit);
+        } else {
+          const uint64_t slot = set_insert_slot(a.fset, a.fmask, uint64_t(key));
+          if (slot == ~uint64_t(0)) *a.overflow = 1;
+          ltok = uint32_t(slot);
+        }
+        lgv = make_uint2(__ldg(a.maxs + ld[i]), __ldg(a.mins + la[i]));
+        lkey = key;
+      }
+      a.desc[gv] = lgv.x;
+      a.asc[gv] = lgv.y;
+      a.ms[gv] = ltok;
+      gv += d.XY;
+    }
+  }
+}
+
 // Pass C2 (k_brick): cube classes and separator counts per 32-cube chunk
 // from the region tokens. CTA = RY cube rows of a brick; the vertex layers
 // z = 0..32 of those rows plus the +x / +y halo stream through a shared-memory
@@ -1170,6 +1254,21 @@ __global__ void __launch_bounds__(256) k_ms_ids(uint32_t* __restrict__ ms, uint6
 
 bool g_consts_ready[64] = {};
 
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeFn tensor_map_encoder() {
+  static EncodeFn encode = nullptr;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      encode = reinterpret_cast<EncodeFn>(fn);
+  }
+  return encode;
+}
+
 }  // namespace
 
 // Host driver of the fused pipeline. Returns false when the dims are outside
@@ -1210,17 +1309,7 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
   memset(&tmap, 0, sizeof tmap);
   bool use_tma = (g.X % 4) == 0 && (reinterpret_cast<uintptr_t>(field) & 15) == 0 && c.use_tma;
   if (use_tma) {
-    using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-    static EncodeFn encode = nullptr;
-    if (!encode) {
-      void* fn = nullptr;
-      cudaDriverEntryPointQueryResult q;
-      if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
-          q == cudaDriverEntryPointSuccess)
-        encode = reinterpret_cast<EncodeFn>(fn);
-    }
+    const EncodeFn encode = tensor_map_encoder();
     const cuuint64_t gdim[3] = {cuuint64_t(g.X), cuuint64_t(g.Y), cuuint64_t(g.Z)};
     const cuuint64_t gstride[2] = {cuuint64_t(g.X) * 4, cuuint64_t(g.X) * cuuint64_t(g.Y) * 4};
     const cuuint32_t box[3] = {HX, HY, HZ};
@@ -1238,6 +1327,21 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
   int* flag = reinterpret_cast<int*>(ctr_base + 128);
   uint16_t* ltd = c.get_t<uint16_t>(S_LTD, ntiles * TN);
   uint16_t* lta = c.get_t<uint16_t>(S_LTA, ntiles * TN);
+  // LT as a 2-D tensor (1024 cells of a brick layer, ntiles * 32 layers) for
+  // the token pass: one box = 8 rows x 32 layers of a brick
+  CUtensorMap mld, mla;
+  bool lt_tma = c.use_tma && tensor_map_encoder();
+  if (lt_tma) {
+    const cuuint64_t gdim[2] = {cuuint64_t(TX * TY), cuuint64_t(ntiles) * TZ};
+    const cuuint64_t gstride[1] = {cuuint64_t(TX * TY) * 2};
+    const cuuint32_t box[2] = {cuuint32_t(32 * kTokRows), cuuint32_t(TZ)};
+    const cuuint32_t estride[2] = {1, 1};
+    for (int k = 0; k < 2 && lt_tma; ++k)
+      lt_tma = tensor_map_encoder()(k ? &mla : &mld, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, k ? lta : ltd, gdim, gstride,
+                                    box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  }
   uint4* TB = c.get_t<uint4>(S_TB, ntiles);
   for (int attempt = 0;; ++attempt) {
     const uint64_t ext_cap = c.fused_ext_cap ? c.fused_ext_cap : uint64_t(g.n / 4 + 1024);
@@ -1362,7 +1466,10 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
         if (sl < d.tz) {
           BrickArgs bs = ba;
           bs.brick0 = sl * bpl;
-          k_tokens<true><<<bpl * (TY / kTokRows), 32 * kTokRows, 0, c.stream>>>(bs);
+          if (lt_tma)
+            k_tokens_tma<true><<<bpl * (TY / kTokRows), 32 * kTokRows, 0, c.stream>>>(mld, mla, bs);
+          else
+            k_tokens<true><<<bpl * (TY / kTokRows), 32 * kTokRows, 0, c.stream>>>(bs);
           CK_LAUNCH("k_tokens");
           CK(cudaEventRecord(c.slab_event(sl), c.stream));
         }
@@ -1400,7 +1507,10 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
         CK(cudaMemsetAsync(flag, 0, 4, c.stream));
         ba.fset = fset;
         ba.fmask = fcap - 1;
-        k_tokens<false><<<tgrid, 32 * kTokRows, 0, c.stream>>>(ba);
+        if (lt_tma)
+          k_tokens_tma<false><<<tgrid, 32 * kTokRows, 0, c.stream>>>(mld, mla, ba);
+        else
+          k_tokens<false><<<tgrid, 32 * kTokRows, 0, c.stream>>>(ba);
         CK_LAUNCH("k_tokens");
         CK(cudaMemcpyAsync(c.h_pinned, flag, 4, cudaMemcpyDeviceToHost, c.stream));
         c.sync();
