@@ -1106,6 +1106,124 @@ __global__ void __launch_bounds__(B_THREADS, 8) k_brick(const BrickArgs a) {
   }
 }
 
+// k_brick with the tokens staged by 3-D TMA tensor copies: batch b (cube
+// layers 8b .. 8b+7) needs vertex layers 8b .. 8b+8 of the CTA's rows plus
+// the +x / +y halo; one box {36 (x, padded), RY + 1, kBatch + 1} per batch,
+// double-buffered so the next batch's copy overlaps this batch's cubes.
+constexpr int TLW = 36;  // padded ring row (16-byte multiple of u32)
+__global__ void __launch_bounds__(B_THREADS, 8) k_brick_tma(const __grid_constant__ CUtensorMap mtok,
+                                                             const BrickArgs a) {
+  // each buffer starts on a 128-byte boundary (TMA destination)
+  constexpr int kBufWords = ((kBatch + 1) * (RY + 1) * TLW + 31) / 32 * 32;
+  __shared__ __align__(128) uint32_t bufraw[2][kBufWords];
+  using Buf = uint32_t[kBatch + 1][RY + 1][TLW];
+  Buf* buf[2] = {reinterpret_cast<Buf*>(bufraw[0]), reinterpret_cast<Buf*>(bufraw[1])};
+  __shared__ __align__(8) uint64_t s_bar[2];
+  const FDims& d = a.d;
+  const uint32_t bt = a.brick0 + blockIdx.x / (TY / RY), yb = (blockIdx.x % (TY / RY)) * RY;  // brick, first row
+  const uint32_t tx = bt % d.tx, ty = (bt / d.tx) % d.ty, tz = bt / (d.tx * d.ty);
+  const uint32_t gx0 = tx * TX, gy0 = ty * TY + yb, gz0 = tz * TZ;
+  if (gy0 >= d.Y) return;  // rows of a brick cut by the volume
+  const int tid = int(threadIdx.x), lane = tid & 31, w = tid >> 5;
+  const int ncl = int(min(uint32_t(TZ), d.Z - 1 - gz0));  // cube layers of the brick
+  const int nb = (ncl + kBatch - 1) / kBatch;
+  // this thread's cube column: x = lane, y = w
+  const uint32_t cy = gy0 + uint32_t(w);
+  const bool row_ok = cy + 1 < d.Y && tx < a.nxc;
+  const bool cube_ok = row_ok && gx0 + uint32_t(lane) + 1 < d.X;
+  const uint64_t CX = d.X - 1, CXY = uint64_t(d.X - 1) * (d.Y - 1);
+  uint8_t* clsp = a.cls + (uint64_t(gx0) + lane + CX * cy + CXY * gz0);
+  uint64_t* chp = a.chunk + (uint64_t(cy) + uint64_t(d.Y - 1) * gz0) * a.nxc + tx;
+  const uint64_t chstep = uint64_t(d.Y - 1) * a.nxc;
+  uint32_t pf[4] = {0, 0, 0, 0};  // top face of this thread's previous cube
+  bool have_prev = false;
+  if (tid == 0) {
+    for (int k = 0; k < 2; ++k) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s_bar[k])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int b) {
+    const uint32_t bar = smem_u32(&s_bar[b & 1]);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                 "r"(uint32_t(sizeof(Buf)))
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];" ::"r"(smem_u32(bufraw[b & 1])),
+        "l"(&mtok), "r"(int(gx0)), "r"(int(gy0)), "r"(int(gz0) + b * kBatch), "r"(bar)
+        : "memory");
+  };
+  if (tid == 0 && nb > 0) issue(0);
+  for (int b = 0; b < nb; ++b) {
+    if (tid == 0 && b + 1 < nb) issue(b + 1);  // the other buffer was released by the barrier below
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(
+            smem_u32(&s_bar[b & 1])),
+        "r"(uint32_t((b >> 1) & 1))
+        : "memory");
+    const int cn = min(kBatch, ncl - b * kBatch);
+    for (int cl = 0; cl < cn; ++cl) {
+      const uint32_t(&lo)[RY + 1][TLW] = (*buf[b & 1])[cl];
+      const uint32_t(&cur)[RY + 1][TLW] = (*buf[b & 1])[cl + 1];
+      uint32_t cnt = 0;
+      if (cube_ok) {
+        uint32_t c[8];
+        // bottom face = the previous cube layer's top face (registers)
+        if (have_prev) {
+          c[0] = pf[0];
+          c[1] = pf[1];
+          c[2] = pf[2];
+          c[3] = pf[3];
+        } else {
+          c[0] = lo[w][lane];
+          c[1] = lo[w][lane + 1];
+          c[2] = lo[w + 1][lane];
+          c[3] = lo[w + 1][lane + 1];
+        }
+        c[4] = cur[w][lane];
+        c[5] = cur[w][lane + 1];
+        c[6] = cur[w + 1][lane];
+        c[7] = cur[w + 1][lane + 1];
+        pf[0] = c[4];
+        pf[1] = c[5];
+        pf[2] = c[6];
+        pf[3] = c[7];
+        have_prev = true;
+        const bool uni = c[1] == c[0] && c[2] == c[0] && c[3] == c[0] && c[4] == c[0] && c[5] == c[0] &&
+                         c[6] == c[0] && c[7] == c[0];
+        uint32_t cls = 0;
+        if (!uni) {
+          // corners equal to corner 0 (bit i)
+          uint32_t m8 = 1u;
+#pragma unroll
+          for (int i = 1; i < 8; ++i) m8 |= uint32_t(c[i] == c[0]) << i;
+          // the lowest corner with another label; two labels iff every
+          // corner carries one of the two (the common case on a separator)
+          uint32_t bb = c[7];
+#pragma unroll
+          for (int i = 6; i >= 1; --i) bb = (m8 >> i) & 1u ? bb : c[i];
+          uint32_t mb = 0u;
+#pragma unroll
+          for (int i = 1; i < 8; ++i) mb |= uint32_t(c[i] == bb) << i;
+          if ((m8 | mb) == 0xffu) {
+            cnt = g_two_cnt[m8 >> 1];
+            cls = m8;
+          } else {
+            cube_codes(c, g_tlut, cnt);
+            cls = 0xffu;
+          }
+        }
+        *clsp = uint8_t(cls);
+      }
+      const uint32_t tot = __any_sync(0xffffffffu, cnt != 0) ? __reduce_add_sync(0xffffffffu, cnt) : 0u;
+      if (lane == 0 && row_ok) *chp = tot;
+      clsp += CXY;
+      chp += chstep;
+    }
+    __syncthreads();  // buffer b & 1 is free for batch b + 2
+  }
+}
+
 // Region token -> dense MS id.
 template <bool kDense>
 __device__ __forceinline__ uint32_t token_id(uint32_t k, const uint32_t* __restrict__ bitmap,
@@ -1447,6 +1565,19 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
     ba.cls = c.get_t<uint8_t>(S_MASK, uint64_t(g.cubes ? g.cubes : 1));
     const unsigned cgrid = unsigned((TY / RY) * ntiles);
     const unsigned tgrid = unsigned((TY / kTokRows) * ntiles);
+    // tokens (in ms) as a 3-D tensor for the count pass
+    CUtensorMap mtok;
+    bool tok_tma = lt_tma && (g.X % 4) == 0;
+    if (tok_tma) {
+      const cuuint64_t gdim[3] = {cuuint64_t(g.X), cuuint64_t(g.Y), cuuint64_t(g.Z)};
+      const cuuint64_t gstride[2] = {cuuint64_t(g.X) * 4, cuuint64_t(g.X) * cuuint64_t(g.Y) * 4};
+      const cuuint32_t box[3] = {cuuint32_t(TLW), cuuint32_t(RY + 1), cuuint32_t(kBatch + 1)};
+      const cuuint32_t estride[3] = {1, 1, 1};
+      tok_tma = tensor_map_encoder()(&mtok, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, ms, gdim, gstride, box, estride,
+                                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+                CUDA_SUCCESS;
+    }
     const uint64_t nbits = uint64_t(o.n_max) * uint64_t(o.n_min);
     const bool dense = nbits < (uint64_t(1) << 32) && c.combine_path != 2;  // PLMSS_OPT_COMBINE_PATH 2: hash
     uint64_t* keys = nullptr;
@@ -1477,7 +1608,10 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
           BrickArgs bs = ba;
           bs.brick0 = (sl - 1) * bpl;
           CK(cudaStreamWaitEvent(c.side, c.slab_event(std::min(sl, d.tz - 1)), 0));
-          k_brick<<<bpl * (TY / RY), B_THREADS, 0, c.side>>>(bs);
+          if (tok_tma)
+            k_brick_tma<<<bpl * (TY / RY), B_THREADS, 0, c.side>>>(mtok, bs);
+          else
+            k_brick<<<bpl * (TY / RY), B_THREADS, 0, c.side>>>(bs);
           CK_LAUNCH("k_brick");
         }
       }
@@ -1543,7 +1677,10 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
       CK(cudaStreamWaitEvent(c.stream, c.join, 0));  // count passes done
     } else {
       // cube classes and separator counts from the tokens
-      k_brick<<<cgrid, B_THREADS, 0, c.stream>>>(ba);
+      if (tok_tma)
+        k_brick_tma<<<cgrid, B_THREADS, 0, c.stream>>>(mtok, ba);
+      else
+        k_brick<<<cgrid, B_THREADS, 0, c.stream>>>(ba);
       CK_LAUNCH("k_brick");
     }
     const uint64_t total = nchunks ? exclusive_scan_u64(c, chunk, int64_t(nchunks), true) : 0;
