@@ -76,6 +76,13 @@ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
   return x;
 }
 
+// 1.0f when a == b, else 0.0f (also for NaN): one FSET instruction.
+__device__ __forceinline__ float feq(float a, float b) {
+  float r;
+  asm("set.eq.f32.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -247,15 +254,21 @@ __global__ void __launch_bounds__(A_THREADS, 1)
           M = fmaxf(M, fn[s]);
           m = fminf(m, fn[s]);
         }
-        uint32_t eu = 0, ed = 0;
+        // which neighbours attain M (m): 1.0 / 0.0 flags (PTX set, one ALU
+        // op each) summed with weights 2^s (2^(13-s)) on the FMA pipe; the
+        // highest weight present is the float's exponent. Exact: distinct
+        // powers of two below 2^14.
+        float au = 0.f, ad = 0.f;
 #pragma unroll
         for (int s = 0; s < 14; ++s) {
-          eu |= uint32_t(fn[s] == M) << s;
-          ed |= uint32_t(fn[s] == m) << s;
+          au = __fmaf_rn(feq(fn[s], M), float(1 << s), au);
+          ad = __fmaf_rn(feq(fn[s], m), float(1 << (13 - s)), ad);
         }
-        // eu == 0 only when every neighbour is missing (M is NaN): no hop
-        const uint32_t su = (M > fv || (M == fv && eu > 0x7fu)) ? uint32_t(31 - __clz(eu)) : 15u;
-        const uint32_t sd = (m < fv || (m == fv && (ed & 0x7fu) != 0)) ? uint32_t(__ffs(ed) - 1) : 15u;
+        // au == 0 only when every neighbour is missing (M is NaN): no hop
+        const uint32_t hu = uint32_t(__float_as_int(au) >> 23) - 127u;          // highest s attaining M
+        const uint32_t hd = 13u - (uint32_t(__float_as_int(ad) >> 23) - 127u);  // lowest s attaining m
+        const uint32_t su = (M > fv || (M == fv && au >= 128.f)) ? hu : 15u;
+        const uint32_t sd = (m < fv || (m == fv && ad >= 128.f)) ? hd : 15u;
         code[hc + (lz + 1) * PXY] = uint8_t(su | (sd << 4));
       }
       a0m = a0;
