@@ -311,8 +311,6 @@ __global__ void __launch_bounds__(A_THREADS, 1)
     if (cw >= kExitMark && w != h) code[w] = kExitMark;
     u += dup[cu];
     w += ddn[cw];
-    u += dup[code[u]];
-    w += ddn[code[w]];
     const int du = dup[code[u]], dw = ddn[code[w]];
     Pd[h] = uint16_t(u + du);
     Pa[h] = uint16_t(w + dw);
