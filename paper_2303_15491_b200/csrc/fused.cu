@@ -309,9 +309,7 @@ __global__ void __launch_bounds__(A_THREADS, 1)
     const uint32_t cu = code[u], cw = code[w];
     if (cu >= kExitMark && u != h) code[u] = kExitMark;
     if (cw >= kExitMark && w != h) code[w] = kExitMark;
-    u += dup[cu];
-    w += ddn[cw];
-    const int du = dup[code[u]], dw = ddn[code[w]];
+    const int du = dup[cu], dw = ddn[cw];
     Pd[h] = uint16_t(u + du);
     Pa[h] = uint16_t(w + dw);
     live_d |= uint32_t(du != 0 || dw != 0) << lz;  // pointer four hops ahead may not be a terminal
