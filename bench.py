@@ -42,7 +42,7 @@ UNIT = "Gvertices/s"
 B_PER_VERTEX = 16
 B_PER_TRI = 16
 # Per-stage algorithmic bytes per vertex.
-STAGES = ["tile_segment", "exit_resolve", "extrema_sort", "finalize_ids", "march"]
+STAGES = ["tile_segment", "extrema_sort", "exit_resolve", "finalize_ids", "march"]
 # Compulsory bytes per vertex of each fused stage: tile_segment
 # reads f and writes the two u16 terminal-index arrays; exit_resolve and
 # extrema_sort touch only the terminal tables (~0.13 entries per vertex);

@@ -504,21 +504,32 @@ __global__ void __launch_bounds__(A_THREADS, 1)
 // exit is the terminal of c in b': TB[b'].base + LT[c]; an extremum is its
 // own successor. Chains follow the steepest paths, so the graph is a forest
 // rooted at the extremum entries.
+// A resolved entry holds its extremum's rank with kFinal set; an exit
+// entry starts as its successor's index.
+constexpr uint32_t kFinal = 0x80000000u;
+
 __global__ void __launch_bounds__(256) k_tt_succ(const uint4* __restrict__ TB, const uint32_t* __restrict__ TT,
                                                  const uint16_t* __restrict__ ltd,
-                                                 const uint16_t* __restrict__ lta, uint32_t* __restrict__ SD,
-                                                 uint32_t* __restrict__ SA) {
+                                                 const uint16_t* __restrict__ lta, const uint32_t* __restrict__ RK,
+                                                 uint32_t* __restrict__ SD, uint32_t* __restrict__ SA) {
   const uint4 h = TB[blockIdx.x];
   const uint32_t n = h.y + h.z + h.w;
   const uint32_t* TBw = reinterpret_cast<const uint32_t*>(TB);
   for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
     const uint32_t k = h.x + i;
-    uint32_t sd = k, sa = k;
+    uint32_t sd, sa;
     if (i < h.y) {
       const uint32_t bm = __ldg(TT + k);
       const uint32_t nb = __ldg(TBw + 4 * (bm >> 15));
       sd = nb + __ldg(ltd + bm);
       sa = nb + __ldg(lta + bm);
+    } else {
+      // a maximum is only reached by descending-manifold chains, a minimum
+      // only by ascending ones
+      const uint32_t r = __ldg(RK + k) | kFinal;
+      const bool is_max = i < h.y + h.z;
+      sd = is_max ? r : kFinal;
+      sa = is_max ? kFinal : r;
     }
     SD[k] = sd;
     SA[k] = sa;
@@ -539,31 +550,16 @@ __global__ void __launch_bounds__(256) k_tt_jump(uint64_t nt, uint32_t* __restri
   if (i < nt) {
     const uint32_t d0 = SD[i], a0 = SA[i];
     uint32_t xd = d0, xa = a0;
-    bool dd = false, da = false;
 #pragma unroll 4
-    for (int k = 0; k < kChase && !(dd && da); ++k) {
-      const uint32_t nd = dd ? xd : SD[xd];
-      const uint32_t na = da ? xa : SA[xa];
-      dd = nd == xd;
-      da = na == xa;
-      xd = nd;
-      xa = na;
+    for (int k = 0; k < kChase && !(xd & xa & kFinal); ++k) {
+      if (!(xd & kFinal)) xd = SD[xd];
+      if (!(xa & kFinal)) xa = SA[xa];
     }
     if (xd != d0) SD[i] = xd;
     if (xa != a0) SA[i] = xa;
-    ch = !(dd && da);
+    ch = !(xd & xa & kFinal);
   }
   if (__any_sync(0xffffffffu, ch) && (threadIdx.x & 31) == 0) *changed = 1;
-}
-
-// Root entry -> final label as the root's rank in the sorted extremum list
-// (RK, written by k_rank_lists): SD/SA become per-entry ranks.
-__global__ void __launch_bounds__(256) k_tt_final(uint64_t nt, const uint32_t* __restrict__ RK,
-                                                  uint32_t* __restrict__ SD, uint32_t* __restrict__ SA) {
-  const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= nt) return;
-  SD[i] = __ldg(RK + SD[i]);
-  SA[i] = __ldg(RK + SA[i]);
 }
 
 // (gid, table entry) pairs of an extremum list for the radix sort
@@ -884,8 +880,8 @@ __global__ void __launch_bounds__(32 * kTokRows) k_tokens(const BrickArgs a) {
 #pragma unroll
     for (int i = 0; i < kTokZ; ++i) {
       if (z0 + i < nz) {
-        ld[i] = __ldg(fd + ld[i]);  // rank of the maximum
-        la[i] = __ldg(fa + la[i]);  // rank of the minimum
+        ld[i] = __ldg(fd + ld[i]) & ~kFinal;  // rank of the maximum
+        la[i] = __ldg(fa + la[i]) & ~kFinal;  // rank of the minimum
       }
     }
 #pragma unroll
@@ -968,8 +964,8 @@ __global__ void __launch_bounds__(32 * kTokRows) k_tokens_tma(const __grid_const
 #pragma unroll
     for (int i = 0; i < kTokZ; ++i) {
       if (z0 + i < nz) {
-        ld[i] = __ldg(fd + sd[z0 + i][l]);  // rank of the maximum
-        la[i] = __ldg(fa + sa[z0 + i][l]);  // rank of the minimum
+        ld[i] = __ldg(fd + sd[z0 + i][l]) & ~kFinal;  // rank of the maximum
+        la[i] = __ldg(fa + sa[z0 + i][l]) & ~kFinal;  // rank of the minimum
       }
     }
 #pragma unroll
@@ -1513,23 +1509,6 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
     o.n_max = int64_t(h.n_max);
     o.n_min = int64_t(h.n_min);
     const uint64_t nt = h.n_tt;
-    // ---- B: terminal-table forest -> final label of every table entry
-    uint32_t* SD = c.get_t<uint32_t>(S_SD, nt);
-    uint32_t* SA = c.get_t<uint32_t>(S_SA, nt);
-    k_tt_succ<<<unsigned(ntiles), 256, 0, c.stream>>>(TB, TT, ltd, lta, SD, SA);
-    CK_LAUNCH("k_tt_succ");
-    o.sweeps = 0;
-    for (;;) {
-      CK(cudaMemsetAsync(flag, 0, 4, c.stream));
-      k_tt_jump<<<blocks_for(int64_t(nt), 256), 256, 0, c.stream>>>(nt, SD, SA, flag);
-      CK_LAUNCH("k_tt_jump");
-      ++o.sweeps;
-      CK(cudaMemcpyAsync(c.h_pinned, flag, 4, cudaMemcpyDeviceToHost, c.stream));
-      c.sync();
-      if (*reinterpret_cast<int*>(c.h_pinned) == 0) break;
-      if (o.sweeps > 64) fail(PLMSS_ERR_LOGIC, "terminal forest did not converge");
-    }
-    c.mark(2);
     // ---- extrema lists sorted ascending; rank of every extremum table entry
     uint32_t* RK = c.get_t<uint32_t>(S_RK, nt);
     for (int dir = 0; dir < 2; ++dir) {
@@ -1549,8 +1528,23 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
       k_rank_lists<<<blocks_for(k, 256), 256, 0, c.stream>>>(kk, vv, k, list, RK);
       CK_LAUNCH("k_rank_lists");
     }
-    k_tt_final<<<blocks_for(int64_t(nt), 256), 256, 0, c.stream>>>(nt, RK, SD, SA);
-    CK_LAUNCH("k_tt_final");
+    c.mark(2);
+    // ---- B: terminal-table forest -> extremum rank of every table entry
+    uint32_t* SD = c.get_t<uint32_t>(S_SD, nt);
+    uint32_t* SA = c.get_t<uint32_t>(S_SA, nt);
+    k_tt_succ<<<unsigned(ntiles), 256, 0, c.stream>>>(TB, TT, ltd, lta, RK, SD, SA);
+    CK_LAUNCH("k_tt_succ");
+    o.sweeps = 0;
+    for (;;) {
+      CK(cudaMemsetAsync(flag, 0, 4, c.stream));
+      k_tt_jump<<<blocks_for(int64_t(nt), 256), 256, 0, c.stream>>>(nt, SD, SA, flag);
+      CK_LAUNCH("k_tt_jump");
+      ++o.sweeps;
+      CK(cudaMemcpyAsync(c.h_pinned, flag, 4, cudaMemcpyDeviceToHost, c.stream));
+      c.sync();
+      if (*reinterpret_cast<int*>(c.h_pinned) == 0) break;
+      if (o.sweeps > 64) fail(PLMSS_ERR_LOGIC, "terminal forest did not converge");
+    }
     c.mark(3);
     // ---- C: region tokens, desc/asc, cube classes, separator counts per chunk
     BrickArgs ba{};
