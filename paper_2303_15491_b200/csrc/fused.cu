@@ -1534,17 +1534,22 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
     uint32_t* SA = c.get_t<uint32_t>(S_SA, nt);
     k_tt_succ<<<unsigned(ntiles), 256, 0, c.stream>>>(TB, TT, ltd, lta, RK, SD, SA);
     CK_LAUNCH("k_tt_succ");
+    // Two sweeps are enqueued without waiting (they converge on smooth
+    // fields); passes C and D follow speculatively and the convergence flag
+    // of the last sweep is checked at the end — if it is set, the sweeps
+    // continue to the fixpoint and C, D are redone.
+    int* jflag = reinterpret_cast<int*>(ctr_base + 192);
     o.sweeps = 0;
-    for (;;) {
-      CK(cudaMemsetAsync(flag, 0, 4, c.stream));
-      k_tt_jump<<<blocks_for(int64_t(nt), 256), 256, 0, c.stream>>>(nt, SD, SA, flag);
+    auto sweep = [&]() {
+      CK(cudaMemsetAsync(jflag, 0, 4, c.stream));
+      k_tt_jump<<<blocks_for(int64_t(nt), 256), 256, 0, c.stream>>>(nt, SD, SA, jflag);
       CK_LAUNCH("k_tt_jump");
       ++o.sweeps;
-      CK(cudaMemcpyAsync(c.h_pinned, flag, 4, cudaMemcpyDeviceToHost, c.stream));
-      c.sync();
-      if (*reinterpret_cast<int*>(c.h_pinned) == 0) break;
-      if (o.sweeps > 64) fail(PLMSS_ERR_LOGIC, "terminal forest did not converge");
-    }
+    };
+    sweep();
+    sweep();
+    CK(cudaMemcpyAsync(reinterpret_cast<char*>(c.h_pinned) + 64, jflag, 4, cudaMemcpyDeviceToHost, c.stream));
+    for (int pass = 0;; ++pass) {
     c.mark(3);
     // ---- C: region tokens, desc/asc, cube classes, separator counts per chunk
     BrickArgs ba{};
@@ -1716,12 +1721,26 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
       CK_LAUNCH("k_emit_chunks");
     }
     c.mark(5);
+    c.sync();
+    if (*reinterpret_cast<int*>(reinterpret_cast<char*>(c.h_pinned) + 64) != 0) {
+      // not converged in two sweeps: finish the forest, redo C and D
+      if (pass > 0) fail(PLMSS_ERR_LOGIC, "terminal forest did not converge");
+      for (;;) {
+        sweep();
+        CK(cudaMemcpyAsync(reinterpret_cast<char*>(c.h_pinned) + 64, jflag, 4, cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
+        if (*reinterpret_cast<int*>(reinterpret_cast<char*>(c.h_pinned) + 64) == 0) break;
+        if (o.sweeps > 64) fail(PLMSS_ERR_LOGIC, "terminal forest did not converge");
+      }
+      continue;
+    }
     o.n_tris = int64_t(total);
     o.tris = tris;
     o.maxima = maxima;
     o.minima = minima;
     o.keys = keys;
     return o;
+    }
   }
 }
 
