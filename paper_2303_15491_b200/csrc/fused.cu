@@ -959,18 +959,20 @@ __global__ void __launch_bounds__(32 * kTokRows) k_tokens_tma(const __grid_const
   Key lkey = Key(~Key(0));
   uint32_t ltok = 0;
   uint2 lgv = make_uint2(0, 0);
-  for (int z0 = 0; z0 < nz; z0 += kTokZ) {
+  // kTokZ layers per group, unguarded for full bricks
+  auto group = [&](auto full, const int z0) {
+    constexpr bool kF = decltype(full)::value;
     uint32_t ld[kTokZ], la[kTokZ];
 #pragma unroll
     for (int i = 0; i < kTokZ; ++i) {
-      if (z0 + i < nz) {
+      if (kF || z0 + i < nz) {
         ld[i] = __ldg(fd + sd[z0 + i][l]) & ~kFinal;  // rank of the maximum
         la[i] = __ldg(fa + sa[z0 + i][l]) & ~kFinal;  // rank of the minimum
       }
     }
 #pragma unroll
     for (int i = 0; i < kTokZ; ++i) {
-      if (z0 + i >= nz) break;
+      if (!kF && z0 + i >= nz) break;
       const Key key = kDense ? Key(la[i] * a.nmax + ld[i]) : Key((uint64_t(la[i]) << 32) | ld[i]);
       if (key != lkey) {
         if (kDense) {
@@ -991,6 +993,13 @@ __global__ void __launch_bounds__(32 * kTokRows) k_tokens_tma(const __grid_const
       a.ms[gv] = ltok;
       gv += d.XY;
     }
+  };
+  if (nz == TZ) {
+#pragma unroll 1
+    for (int z0 = 0; z0 < TZ; z0 += kTokZ) group(std::true_type{}, z0);
+  } else {
+#pragma unroll 1
+    for (int z0 = 0; z0 < nz; z0 += kTokZ) group(std::false_type{}, z0);
   }
 }
 
