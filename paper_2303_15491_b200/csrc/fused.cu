@@ -730,7 +730,7 @@ __global__ void k_set_ids(const uint64_t* __restrict__ sorted_slots, int64_t r, 
 // reference cell order).
 // A CTA takes RY = 4 cube rows of a brick (warp w <-> row w): small CTAs,
 // many per SM, so one CTA's barriers overlap the others' work.
-constexpr int RY = 4, B_THREADS = 32 * RY;
+constexpr int RY = 8, B_THREADS = 32 * RY;
 constexpr int LW = TX + 1, LQ = LW * (RY + 1);  // 33 x 17 = 561 vertices per layer
 constexpr int kBatch = 8, kRing = 16;  // ring >= kBatch + 1, power of two
 static_assert(kRing >= kBatch + 1 && (kRing & (kRing - 1)) == 0, "ring size");
@@ -1007,7 +1007,7 @@ __global__ void __launch_bounds__(32 * kTokRows) k_tokens_tma(const __grid_const
 // from the region tokens. CTA = RY cube rows of a brick; the vertex layers
 // z = 0..32 of those rows plus the +x / +y halo stream through a shared-memory
 // ring kBatch layers at a time; warp w handles cube row w, lane = cube x.
-__global__ void __launch_bounds__(B_THREADS, 8) k_brick(const BrickArgs a) {
+__global__ void __launch_bounds__(B_THREADS, 4) k_brick(const BrickArgs a) {
   __shared__ uint32_t ring[kRing * LQ];
   const FDims& d = a.d;
   const uint32_t bt = a.brick0 + blockIdx.x / (TY / RY), yb = (blockIdx.x % (TY / RY)) * RY;  // brick, first row
