@@ -221,8 +221,17 @@ int plmss_b200_copy(plmss_ctx* ctx, void* dst, const void* d_src, int64_t bytes,
  *   PLMSS_OPT_PIPELINE_PATH 0 fused tile pipeline when the dims allow it,
  *                           1 staged kernels (segment/combine/emit);
  *   PLMSS_OPT_TMA           1 (default) TMA tensor loads of the field bricks,
- *                           0 plain load loop (both are exact). */
-enum plmss_option { PLMSS_OPT_COMBINE_PATH = 1, PLMSS_OPT_PIPELINE_PATH = 2, PLMSS_OPT_TMA = 3 };
+ *                           0 plain load loop (both are exact);
+ *   PLMSS_OPT_SPECULATIVE_SWEEPS  forest sweeps enqueued before the fused
+ *                           pipeline's passes C and D (default 2); if the
+ *                           forest has not converged by then, the sweeps
+ *                           continue and C, D are redone (0 forces that path). */
+enum plmss_option {
+  PLMSS_OPT_COMBINE_PATH = 1,
+  PLMSS_OPT_PIPELINE_PATH = 2,
+  PLMSS_OPT_TMA = 3,
+  PLMSS_OPT_SPECULATIVE_SWEEPS = 4
+};
 int plmss_b200_ctx_set_option(plmss_ctx* ctx, int option, int64_t value);
 
 /* End-to-end variant over HOST buffers: pinned or pageable h_field in; the

@@ -23,7 +23,7 @@ LIB_PATH = os.path.join(PKG, "libplmss_b200.so")
 
 KEY_F32, KEY_F64, KEY_RANK = 0, 1, 2
 ASCENDING, DESCENDING, BOTH = 0, 1, 2
-OPT_COMBINE_PATH = 1
+OPT_COMBINE_PATH, OPT_PIPELINE_PATH, OPT_TMA, OPT_SPECULATIVE_SWEEPS = 1, 2, 3, 4
 
 _ERR = {1: ValueError, 2: RuntimeError, 3: IndexError, 4: RuntimeError, 5: MemoryError}
 

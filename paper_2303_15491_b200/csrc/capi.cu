@@ -435,6 +435,11 @@ int plmss_b200_ctx_set_option(plmss_ctx* p, int option, int64_t value) {
       c.combine_path = int(value);
       return;
     }
+    if (option == PLMSS_OPT_SPECULATIVE_SWEEPS) {
+      if (value < 0 || value > 64) fail(PLMSS_ERR_INVALID_ARGUMENT, "speculative sweeps must be in [0, 64]");
+      c.spec_sweeps = int(value);
+      return;
+    }
     if (option == PLMSS_OPT_TMA) {
       c.use_tma = value != 0;
       return;

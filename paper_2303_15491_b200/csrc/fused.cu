@@ -1555,8 +1555,8 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
       CK_LAUNCH("k_tt_jump");
       ++o.sweeps;
     };
-    sweep();
-    sweep();
+    if (c.spec_sweeps == 0) CK(cudaMemsetAsync(jflag, 0xff, 4, c.stream));  // "not converged"
+    for (int i = 0; i < c.spec_sweeps; ++i) sweep();
     CK(cudaMemcpyAsync(reinterpret_cast<char*>(c.h_pinned) + 64, jflag, 4, cudaMemcpyDeviceToHost, c.stream));
     for (int pass = 0;; ++pass) {
     c.mark(3);

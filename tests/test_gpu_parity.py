@@ -323,3 +323,31 @@ def test_pipeline_brick_geometry(plmss, gpu, restatement, dims, kind, path):
     assert np.array_equal(m["source_cells"].cpu().numpy(), e["source_cells"])
     assert np.array_equal(m["regions"].cpu().numpy(), e["regions"])
     assert np.array_equal(m["points"].cpu().numpy(), e["points"])
+
+
+# Chains through many bricks (a ramp along x crosses 128 bricks) and the
+# fallback when the terminal forest has not converged after the speculative
+# sweeps: the sweeps continue and passes C and D are redone.
+@pytest.mark.parametrize("spec", [2, 0])
+def test_pipeline_long_forest_chains(plmss, gpu, restatement, spec):
+    dims = (4096, 6, 5)
+    x = np.arange(dims[0], dtype=np.float64)[None, None, :]
+    y = np.arange(dims[1], dtype=np.float64)[None, :, None]
+    z = np.arange(dims[2], dtype=np.float64)[:, None, None]
+    f = (x + 1e-3 * np.sin(y + 2 * z) + 0 * z).astype(np.float32).reshape(-1)
+    gpu.set_option(plmss.OPT_SPECULATIVE_SWEEPS, spec)
+    try:
+        res = plmss.pipeline(dims, dev(f), ctx=gpu)
+    finally:
+        gpu.set_option(plmss.OPT_SPECULATIVE_SWEEPS, 2)
+    out = plmss.fetch(gpu, res)
+    s = restatement.segment(dims, values=f.astype(np.float64))
+    ms, keys = restatement.combine_ms(s["asc"], s["desc"])
+    for k, ref in (("desc", s["desc"]), ("asc", s["asc"]), ("ms", ms)):
+        assert np.array_equal(u32(out[k]), ref), k
+    e = restatement.emit_separators(dims, ms)
+    assert res.n_tris == len(e["source_cells"])
+    assert res.sweeps >= 1
+    m = plmss.materialize_separators(dims, out["tris"], ctx=gpu)
+    assert np.array_equal(m["source_cells"].cpu().numpy(), e["source_cells"])
+    assert np.array_equal(m["regions"].cpu().numpy(), e["regions"])
