@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(A_THREADS, 1)
   //    columns by threads 0..131. A shell cell that is the hop target of a
   //    brick vertex is an exit: its code byte becomes kExitMark (readers
   //    treat 0xff and kExitMark alike).
-  uint32_t live_d = 0, mmax = 0, mmin = 0;
+  uint32_t live_d = 0, live_a = 0, mmax = 0, mmin = 0;
 #pragma unroll
   for (int i = 0; i < kShellPerThread; ++i) {
     const uint32_t j = uint32_t(tid + i * A_THREADS);
@@ -312,7 +312,8 @@ __global__ void __launch_bounds__(A_THREADS, 1)
     const int du = dup[cu], dw = ddn[cw];
     Pd[h] = uint16_t(u + du);
     Pa[h] = uint16_t(w + dw);
-    live_d |= uint32_t(du != 0 || dw != 0) << lz;  // pointer four hops ahead may not be a terminal
+    live_d |= uint32_t(du != 0) << lz;  // pointer two hops ahead may not be a terminal
+    live_a |= uint32_t(dw != 0) << lz;
     mmax |= uint32_t((c & 15) == 15) << lz;
     mmin |= uint32_t((c >> 4) == 15) << lz;
   }
@@ -325,10 +326,10 @@ __global__ void __launch_bounds__(A_THREADS, 1)
 
   // 4. pointer jumping, P <- P^4 per round in both directions; a vertex
   //    retires once both its pointers are terminals
-  uint32_t live = live_d;
   for (;;) {
-    uint32_t m = live, next = 0;
-    // two vertices per iteration: four independent load chains in flight
+    uint32_t m = live_d | live_a, nd = 0, na = 0;
+    // two vertices per iteration: up to four independent load chains, each
+    // direction only while it is live
     while (m) {
       const int lz = 31 - __clz(m);
       const uint32_t bit = 1u << lz;
@@ -337,19 +338,30 @@ __global__ void __launch_bounds__(A_THREADS, 1)
       const uint32_t bit2 = 1u << lz2;
       m &= ~bit2;
       const int h = hc + (lz + 1) * PXY, h2 = hc + (lz2 + 1) * PXY;
-      const uint32_t p1 = Pd[h], q1 = Pa[h], r1 = Pd[h2], s1 = Pa[h2];
-      const uint32_t p2 = Pd[p1], q2 = Pa[q1], r2 = Pd[r1], s2 = Pa[s1];
-      const uint32_t p3 = Pd[p2], q3 = Pa[q2], r3 = Pd[r2], s3 = Pa[s2];
-      const uint32_t p4 = Pd[p3], q4 = Pa[q3], r4 = Pd[r3], s4 = Pa[s3];
-      Pd[h] = uint16_t(p4);
-      Pa[h] = uint16_t(q4);
-      Pd[h2] = uint16_t(r4);
-      Pa[h2] = uint16_t(s4);
-      if (p4 != p3 || q4 != q3) next |= bit;
-      if (r4 != r3 || s4 != s3) next |= bit2;
+      if (live_d & (bit | bit2)) {
+        const uint32_t p1 = Pd[h], r1 = Pd[h2];
+        const uint32_t p2 = Pd[p1], r2 = Pd[r1];
+        const uint32_t p3 = Pd[p2], r3 = Pd[r2];
+        const uint32_t p4 = Pd[p3], r4 = Pd[r3];
+        Pd[h] = uint16_t(p4);
+        Pd[h2] = uint16_t(r4);
+        if (p4 != p3) nd |= bit;
+        if (r4 != r3) nd |= bit2;
+      }
+      if (live_a & (bit | bit2)) {
+        const uint32_t q1 = Pa[h], s1 = Pa[h2];
+        const uint32_t q2 = Pa[q1], s2 = Pa[s1];
+        const uint32_t q3 = Pa[q2], s3 = Pa[s2];
+        const uint32_t q4 = Pa[q3], s4 = Pa[s3];
+        Pa[h] = uint16_t(q4);
+        Pa[h2] = uint16_t(s4);
+        if (q4 != q3) na |= bit;
+        if (s4 != s3) na |= bit2;
+      }
     }
-    live = next;
-    if (!__syncthreads_or(live != 0)) break;
+    live_d = nd;
+    live_a = na;
+    if (!__syncthreads_or((live_d | live_a) != 0)) break;
   }
 
   // 5. terminal table of the brick: TT[base ..) = exit cells, then maxima,
