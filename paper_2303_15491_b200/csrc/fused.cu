@@ -1273,32 +1273,39 @@ struct EmitArgs {
 // records are dealt out one per lane (consecutive lanes write consecutive
 // 16-byte records).
 __global__ void __launch_bounds__(256) k_emit_chunks(const EmitArgs a) {
-  const int lane = threadIdx.x & 31;
+  __shared__ uint8_t s_own[256 / 32][32];  // record window position -> lane of the cube starting there
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const uint32_t CX = a.X - 1, CY = a.Y - 1, XY = a.X * a.Y;
   const uint64_t ngroups = (a.nchunks + 31) / 32;
   const uint64_t warps = uint64_t(gridDim.x) * (blockDim.x / 32);
+  auto corner_off = [&](uint32_t cn) { return (cn & 1) + a.X * ((cn >> 1) & 1) + XY * (cn >> 2); };
   // warps take groups of 32 consecutive chunks; one coalesced load of their
-  // offsets, then only the chunks with records
-  for (uint64_t grp = uint64_t(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5); grp < ngroups; grp += warps) {
+  // offsets and one division per lane for their coordinates, then only the
+  // chunks with records
+  for (uint64_t grp = uint64_t(blockIdx.x) * (blockDim.x / 32) + wib; grp < ngroups; grp += warps) {
     const uint64_t chl = grp * 32 + uint64_t(lane);
     const uint64_t my_off = chl < a.nchunks ? a.off[chl] : a.total;
     uint64_t nx_off = __shfl_down_sync(0xffffffffu, my_off, 1);
     if (lane == 31) nx_off = chl + 1 < a.nchunks ? a.off[chl + 1] : a.total;
     uint32_t todo = __ballot_sync(0xffffffffu, nx_off > my_off);
+    if (!todo) continue;
+    // this lane's chunk: cube row r = (cz, cy), x segment xs (nchunks < 2^32)
+    const uint32_t c32 = uint32_t(chl), r_l = c32 / a.nxc, xs_l = c32 - r_l * a.nxc;
+    const uint32_t cz_l = r_l / CY, cy_l = r_l - cz_l * CY;
+    const uint32_t x0_l = 32 * xs_l;
+    const uint32_t v0_l = x0_l + a.X * cy_l + XY * cz_l;  // min corner of the chunk's first cube
+    const uint64_t q0_l = uint64_t(x0_l) + uint64_t(CX) * r_l;
+    const uint32_t T_l = uint32_t(nx_off - my_off);
     while (todo) {
       const int k = __ffs(todo) - 1;
       todo &= todo - 1;
-      const uint64_t ch = grp * 32 + uint64_t(k);
       const uint64_t base = __shfl_sync(0xffffffffu, my_off, k);
-      const uint32_t T = uint32_t(__shfl_sync(0xffffffffu, nx_off, k) - base);
-      const uint32_t r = uint32_t(ch / a.nxc), xs = uint32_t(ch - uint64_t(r) * a.nxc);
-      const uint32_t cz = r / CY, cy = r - cz * CY;
-      const uint32_t cx = 32 * xs + uint32_t(lane);
-      const uint64_t q0 = uint64_t(32 * xs) + uint64_t(CX) * r;  // cube id of lane 0's cube
-      const uint32_t v0 = cx + a.X * cy + XY * cz;                // this lane's min corner
+      const uint32_t T = __shfl_sync(0xffffffffu, T_l, k);
+      const uint64_t q0 = __shfl_sync(0xffffffffu, q0_l, k);  // cube id of lane 0's cube
+      const uint32_t cx = __shfl_sync(0xffffffffu, x0_l, k) + uint32_t(lane);
+      const uint32_t v0 = __shfl_sync(0xffffffffu, v0_l, k) + uint32_t(lane);  // this lane's min corner
       const uint32_t cls = cx < CX ? a.cls[q0 + lane] : 0u;
       uint32_t cnt = 0, code6 = 0, lo2 = 0, hi2 = 0;
-      auto corner_off = [&](uint32_t cn) { return (cn & 1) + a.X * ((cn >> 1) & 1) + XY * (cn >> 2); };
       if (cls == 0xffu) {
         uint32_t c[8];
 #pragma unroll
@@ -1319,21 +1326,25 @@ __global__ void __launch_bounds__(256) k_emit_chunks(const EmitArgs a) {
         const uint32_t t = __shfl_up_sync(0xffffffffu, inc, s);
         if (lane >= s) inc += t;
       }
+      const uint32_t ex = inc - cnt;  // this cube's first record
+      int carry = 0;                  // owner of the window's records before its first start
       for (uint32_t j0 = 0; j0 < T; j0 += 32) {
+        // owner of record j0 + lane = the cube with the last start at or before it
+        const bool st = cnt != 0 && ex - j0 < 32u;
+        if (st) s_own[wib][ex - j0] = uint8_t(lane);
+        const uint32_t S = __reduce_or_sync(0xffffffffu, st ? 1u << (ex - j0) : 0u);
+        __syncwarp();
+        const uint32_t m = S & (0xffffffffu >> (31 - lane));
+        const int src = m ? int(s_own[wib][31 - __clz(m)]) : carry;
+        carry = __shfl_sync(0xffffffffu, src, 31);
+        __syncwarp();
         const uint32_t j = j0 + uint32_t(lane);
-        // owning lane of record j = number of lanes whose inclusive count <= j
-        int src = 0;
-#pragma unroll
-        for (int step = 16; step >= 1; step >>= 1) {
-          const uint32_t vv = __shfl_sync(0xffffffffu, inc, src + step - 1);
-          if (vv <= j) src += step;
-        }
-        const uint32_t c6 = __shfl_sync(0xffffffffu, code6, src & 31);
-        const uint32_t ex = __shfl_sync(0xffffffffu, inc - cnt, src & 31);
-        const uint32_t l2 = __shfl_sync(0xffffffffu, lo2, src & 31);
-        const uint32_t h2 = __shfl_sync(0xffffffffu, hi2, src & 31);
+        const uint32_t c6 = __shfl_sync(0xffffffffu, code6, src);
+        const uint32_t exs = __shfl_sync(0xffffffffu, ex, src);
+        const uint32_t l2 = __shfl_sync(0xffffffffu, lo2, src);
+        const uint32_t h2 = __shfl_sync(0xffffffffu, hi2, src);
         if (j >= T) continue;
-        uint32_t k = j - ex;
+        uint32_t k = j - exs;
         uint32_t t, rowi, la, lb;
         if (c6 >> 31) {
           // two-label cube: record list from the table, one region pair
