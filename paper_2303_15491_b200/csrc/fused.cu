@@ -925,7 +925,7 @@ __global__ void __launch_bounds__(32 * kTokRows) k_tokens(const BrickArgs a) {
 // k_tokens with the CTA's terminal indices (8 rows x 32 layers of its brick,
 // 2 x 16 KB) staged by two 2-D TMA tensor copies instead of per-thread loads.
 template <bool kDense>
-__global__ void __launch_bounds__(32 * kTokRows) k_tokens_tma(const __grid_constant__ CUtensorMap mld,
+__global__ void __launch_bounds__(32 * kTokRows, 4) k_tokens_tma(const __grid_constant__ CUtensorMap mld,
                                                              const __grid_constant__ CUtensorMap mla,
                                                              const BrickArgs a) {
   using Key = typename std::conditional<kDense, uint32_t, unsigned long long>::type;
