@@ -95,7 +95,8 @@ size_t plmss_b200_ctx_scratch_bytes(const plmss_ctx* ctx);
 int plmss_b200_ctx_set_timing(plmss_ctx* ctx, int enable);
 int plmss_b200_ctx_stage_ms(const plmss_ctx* ctx, float out[8]);
 /* Diagnostics of the last fused pipeline call: [0] exit-graph entries,
- * [1] pass-A capacity retries, [2] region-set capacity, [3] finalize retries. */
+ * [1] pass-A capacity retries, [2] region-set capacity (negative: bitmap
+ * words), [4] TMA field loads used. */
 int plmss_b200_ctx_stats(const plmss_ctx* ctx, int64_t out[8]);
 
 /* ---- order field --------------------------------------------------------
@@ -223,7 +224,7 @@ int plmss_b200_copy(plmss_ctx* ctx, void* dst, const void* d_src, int64_t bytes,
  *   PLMSS_OPT_TMA           1 (default) TMA tensor loads of the field bricks,
  *                           0 plain load loop (both are exact);
  *   PLMSS_OPT_SPECULATIVE_SWEEPS  forest sweeps enqueued before the fused
- *                           pipeline's passes C and D (default 2); if the
+ *                           pipeline's passes C and D (default 1); if the
  *                           forest has not converged by then, the sweeps
  *                           continue and C, D are redone (0 forces that path). */
 enum plmss_option {

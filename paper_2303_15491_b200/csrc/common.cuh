@@ -105,7 +105,7 @@ struct Ctx {
   int combine_path = 0;  // PLMSS_OPT_COMBINE_PATH
   int pipeline_path = 0; // PLMSS_OPT_PIPELINE_PATH: 0 fused when supported, 1 staged
   bool use_tma = true;   // PLMSS_OPT_TMA
-  int spec_sweeps = 2;   // PLMSS_OPT_SPECULATIVE_SWEEPS
+  int spec_sweeps = 1;   // PLMSS_OPT_SPECULATIVE_SWEEPS
   // Adaptive capacities of the fused pipeline (remembered between calls).
   uint64_t fused_exit_cap = 0, fused_pair_hint = 0, fused_tri_cap = 0, fused_ext_cap = 0;
   // Diagnostics of the last fused call: [0] exit entries, [1] pass-A retries,

@@ -553,7 +553,7 @@ __global__ void __launch_bounds__(256) k_tt_succ(const uint4* __restrict__ TB, c
 // stores the furthest entry reached. Values read from entries other threads
 // have already advanced only shorten the walk; every value lies on the
 // entry's chain, so concurrent updates are safe.
-constexpr int kChase = 16;
+constexpr int kChase = 64;
 
 __global__ void __launch_bounds__(256) k_tt_jump(uint64_t nt, uint32_t* __restrict__ SD, uint32_t* __restrict__ SA,
                                                  int* __restrict__ changed) {
