@@ -83,6 +83,17 @@ __device__ __forceinline__ float feq(float a, float b) {
   return r;
 }
 
+// m |= bit when (a op b): a compare and one predicated OR
+__device__ __forceinline__ void or_if_ne(uint32_t& m, uint32_t a, uint32_t b, uint32_t bit) {
+  asm("{\n .reg .pred q;\n setp.ne.u32 q, %1, %2;\n @q or.b32 %0, %0, %3;\n}" : "+r"(m) : "r"(a), "r"(b), "r"(bit));
+}
+__device__ __forceinline__ void or_if_eq(uint32_t& m, uint32_t a, uint32_t b, uint32_t bit) {
+  asm("{\n .reg .pred q;\n setp.eq.u32 q, %1, %2;\n @q or.b32 %0, %0, %3;\n}" : "+r"(m) : "r"(a), "r"(b), "r"(bit));
+}
+__device__ __forceinline__ void or_if_ge(uint32_t& m, uint32_t a, uint32_t b, uint32_t bit) {
+  asm("{\n .reg .pred q;\n setp.ge.u32 q, %1, %2;\n @q or.b32 %0, %0, %3;\n}" : "+r"(m) : "r"(a), "r"(b), "r"(bit));
+}
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -312,10 +323,11 @@ __global__ void __launch_bounds__(A_THREADS, 1)
     const int du = dup[cu], dw = ddn[cw];
     Pd[h] = uint16_t(u + du);
     Pa[h] = uint16_t(w + dw);
-    live_d |= uint32_t(du != 0) << lz;  // pointer two hops ahead may not be a terminal
-    live_a |= uint32_t(dw != 0) << lz;
-    mmax |= uint32_t((c & 15) == 15) << lz;
-    mmin |= uint32_t((c >> 4) == 15) << lz;
+    const uint32_t bit = 1u << lz;
+    or_if_ne(live_d, uint32_t(du), 0u, bit);  // pointer two hops ahead may not be a terminal
+    or_if_ne(live_a, uint32_t(dw), 0u, bit);
+    or_if_eq(mmax, c & 15u, 15u, bit);
+    or_if_ge(mmin, c, 0xf0u, bit);
   }
   {
     const uint32_t vmask = col_ok ? (nz >= 32 ? 0xffffffffu : ((1u << nz) - 1u)) : 0u;
@@ -345,8 +357,8 @@ __global__ void __launch_bounds__(A_THREADS, 1)
         const uint32_t p4 = Pd[p3], r4 = Pd[r3];
         Pd[h] = uint16_t(p4);
         Pd[h2] = uint16_t(r4);
-        if (p4 != p3) nd |= bit;
-        if (r4 != r3) nd |= bit2;
+        or_if_ne(nd, p4, p3, bit);
+        or_if_ne(nd, r4, r3, bit2);
       }
       if (live_a & (bit | bit2)) {
         const uint32_t q1 = Pa[h], s1 = Pa[h2];
@@ -355,8 +367,8 @@ __global__ void __launch_bounds__(A_THREADS, 1)
         const uint32_t q4 = Pa[q3], s4 = Pa[s3];
         Pa[h] = uint16_t(q4);
         Pa[h2] = uint16_t(s4);
-        if (q4 != q3) na |= bit;
-        if (s4 != s3) na |= bit2;
+        or_if_ne(na, q4, q3, bit);
+        or_if_ne(na, s4, s3, bit2);
       }
     }
     live_d = nd;
