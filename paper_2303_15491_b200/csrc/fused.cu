@@ -1308,29 +1308,69 @@ __global__ void __launch_bounds__(256) k_emit_chunks(const EmitArgs a) {
     const uint32_t v0_l = x0_l + a.X * cy_l + XY * cz_l;  // min corner of the chunk's first cube
     const uint64_t q0_l = uint64_t(x0_l) + uint64_t(CX) * r_l;
     const uint32_t T_l = uint32_t(nx_off - my_off);
-    while (todo) {
-      const int k = __ffs(todo) - 1;
-      todo &= todo - 1;
-      const uint64_t base = __shfl_sync(0xffffffffu, my_off, k);
-      const uint32_t T = __shfl_sync(0xffffffffu, T_l, k);
-      const uint64_t q0 = __shfl_sync(0xffffffffu, q0_l, k);  // cube id of lane 0's cube
+    // one busy chunk ahead: its classes and the ids of its cubes' four
+    // corner rows (lane i: corners 0, 2, 4, 6 of cube i; corners 1, 3, 5, 7
+    // come from lane i + 1, lane 31 loads them) are loaded while the current
+    // chunk is emitted
+    struct Pre {
+      uint32_t cls, r[4], e[4];
+    };
+    auto fetch = [&](int k, Pre& p) {
       const uint32_t cx = __shfl_sync(0xffffffffu, x0_l, k) + uint32_t(lane);
-      const uint32_t v0 = __shfl_sync(0xffffffffu, v0_l, k) + uint32_t(lane);  // this lane's min corner
-      const uint32_t cls = cx < CX ? a.cls[q0 + lane] : 0u;
+      const uint32_t v0 = __shfl_sync(0xffffffffu, v0_l, k) + uint32_t(lane);
+      const uint64_t q0 = __shfl_sync(0xffffffffu, q0_l, k);
+      p.cls = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) p.r[i] = p.e[i] = 0;
+      if (cx <= CX) {  // the vertex past the last cube is that cube's corner 1
+#pragma unroll
+        for (int i = 0; i < 4; ++i) p.r[i] = __ldg(a.ids + v0 + corner_off(uint32_t(2 * i)));
+      }
+      if (cx < CX) {
+        p.cls = a.cls[q0 + lane];
+        if (lane == 31) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) p.e[i] = __ldg(a.ids + v0 + corner_off(uint32_t(2 * i + 1)));
+        }
+      }
+    };
+    int kc = __ffs(todo) - 1;
+    todo &= todo - 1;
+    Pre cur;
+    fetch(kc, cur);
+    for (;;) {
+      const bool more = todo != 0;  // warp-uniform
+      int kn = 0;
+      Pre nxt;
+      if (more) {
+        kn = __ffs(todo) - 1;
+        todo &= todo - 1;
+        fetch(kn, nxt);
+      }
+      const uint64_t base = __shfl_sync(0xffffffffu, my_off, kc);
+      const uint32_t T = __shfl_sync(0xffffffffu, T_l, kc);
+      const uint64_t q0 = __shfl_sync(0xffffffffu, q0_l, kc);  // cube id of lane 0's cube
+      const uint32_t v0 = __shfl_sync(0xffffffffu, v0_l, kc) + uint32_t(lane);  // this lane's min corner
+      const uint32_t cls = cur.cls;
+      uint32_t c[8];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        c[2 * i] = cur.r[i];
+        const uint32_t nb = __shfl_down_sync(0xffffffffu, cur.r[i], 1);
+        c[2 * i + 1] = lane == 31 ? cur.e[i] : nb;
+      }
       uint32_t cnt = 0, code6 = 0, lo2 = 0, hi2 = 0;
       if (cls == 0xffu) {
-        uint32_t c[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) c[i] = __ldg(a.ids + v0 + corner_off(uint32_t(i)));
         code6 = cube_codes(c, g_tlut, cnt);
       } else if (cls != 0) {
         // two labels: corner 0's and that of the lowest corner outside its set
         cnt = g_two_cnt[cls >> 1];
         code6 = 0x80000000u | cls;
-        const uint32_t i0 = __ldg(a.ids + v0);
-        const uint32_t ib = __ldg(a.ids + v0 + corner_off(uint32_t(__ffs(~cls) - 1)));
-        lo2 = min(i0, ib);
-        hi2 = max(i0, ib);
+        uint32_t ib = c[7];
+#pragma unroll
+        for (int i = 6; i >= 1; --i) ib = (cls >> i) & 1u ? ib : c[i];
+        lo2 = min(c[0], ib);
+        hi2 = max(c[0], ib);
       }
       uint32_t inc = cnt;
 #pragma unroll
@@ -1388,6 +1428,9 @@ __global__ void __launch_bounds__(256) k_emit_chunks(const EmitArgs a) {
         *reinterpret_cast<uint4*>(a.out + base + j) =
             make_uint4(uint32_t(cr64), uint32_t(cr64 >> 32), min(la, lb), max(la, lb));
       }
+      if (!more) break;
+      kc = kn;
+      cur = nxt;
     }
   }
 }
