@@ -936,17 +936,17 @@ __global__ void __launch_bounds__(32 * kTokRows) k_tokens(const BrickArgs a) {
 
 // k_tokens with the CTA's terminal indices (8 rows x 32 layers of its brick,
 // 2 x 16 KB) staged by two 2-D TMA tensor copies instead of per-thread loads.
+constexpr int kTokSmem = 2 * TZ * 32 * kTokRows * 2;  // both index arrays
 template <bool kDense>
-__global__ void __launch_bounds__(32 * kTokRows, 4) k_tokens_tma(const __grid_constant__ CUtensorMap mld,
-                                                             const __grid_constant__ CUtensorMap mla,
-                                                             const BrickArgs a) {
+__device__ __forceinline__ void tokens_tma_body(const CUtensorMap& mld, const CUtensorMap& mla, const BrickArgs& a,
+                                                const uint32_t blk, unsigned char* smem) {
   using Key = typename std::conditional<kDense, uint32_t, unsigned long long>::type;
-  __shared__ __align__(128) uint16_t sd[TZ][32 * kTokRows];
-  __shared__ __align__(128) uint16_t sa[TZ][32 * kTokRows];
+  uint16_t(*sd)[32 * kTokRows] = reinterpret_cast<uint16_t(*)[32 * kTokRows]>(smem);  // 128-byte aligned
+  uint16_t(*sa)[32 * kTokRows] = reinterpret_cast<uint16_t(*)[32 * kTokRows]>(smem + kTokSmem / 2);
   __shared__ __align__(8) uint64_t s_bar;
   const FDims& d = a.d;
-  const uint32_t grp = blockIdx.x % (TY / kTokRows);
-  const uint32_t bt = a.brick0 + blockIdx.x / (TY / kTokRows);
+  const uint32_t grp = blk % (TY / kTokRows);
+  const uint32_t bt = a.brick0 + blk / (TY / kTokRows);
   const uint32_t tx = bt % d.tx, ty = (bt / d.tx) % d.ty, tz = bt / (d.tx * d.ty);
   const uint32_t lx = threadIdx.x & 31, ly = grp * kTokRows + (threadIdx.x >> 5);
   const uint32_t bar = smem_u32(&s_bar);
@@ -956,7 +956,7 @@ __global__ void __launch_bounds__(32 * kTokRows, 4) k_tokens_tma(const __grid_co
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(uint32_t(2 * sizeof(sd)))
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(uint32_t(kTokSmem))
                  : "memory");
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
@@ -1149,16 +1149,18 @@ __global__ void __launch_bounds__(B_THREADS, 4) k_brick(const BrickArgs a) {
 // the +x / +y halo; one box {36 (x, padded), RY + 1, kBatch + 1} per batch,
 // double-buffered so the next batch's copy overlaps this batch's cubes.
 constexpr int TLW = 36;  // padded ring row (16-byte multiple of u32)
-__global__ void __launch_bounds__(B_THREADS, 8) k_brick_tma(const __grid_constant__ CUtensorMap mtok,
-                                                             const BrickArgs a) {
+constexpr int kBrickBufWords = ((kBatch + 1) * (RY + 1) * TLW + 31) / 32 * 32;  // one staged batch
+constexpr int kBrickSmem = 2 * kBrickBufWords * 4;
+__device__ __forceinline__ void brick_tma_body(const CUtensorMap& mtok, const BrickArgs& a, const uint32_t blk,
+                                               unsigned char* smem) {
   // each buffer starts on a 128-byte boundary (TMA destination)
-  constexpr int kBufWords = ((kBatch + 1) * (RY + 1) * TLW + 31) / 32 * 32;
-  __shared__ __align__(128) uint32_t bufraw[2][kBufWords];
+  constexpr int kBufWords = kBrickBufWords;
+  uint32_t(*bufraw)[kBufWords] = reinterpret_cast<uint32_t(*)[kBufWords]>(smem);  // 128-byte aligned
   using Buf = uint32_t[kBatch + 1][RY + 1][TLW];
   Buf* buf[2] = {reinterpret_cast<Buf*>(bufraw[0]), reinterpret_cast<Buf*>(bufraw[1])};
   __shared__ __align__(8) uint64_t s_bar[2];
   const FDims& d = a.d;
-  const uint32_t bt = a.brick0 + blockIdx.x / (TY / RY), yb = (blockIdx.x % (TY / RY)) * RY;  // brick, first row
+  const uint32_t bt = a.brick0 + blk / (TY / RY), yb = (blk % (TY / RY)) * RY;  // brick, first row
   const uint32_t tx = bt % d.tx, ty = (bt / d.tx) % d.ty, tz = bt / (d.tx * d.ty);
   const uint32_t gx0 = tx * TX, gy0 = ty * TY + yb, gz0 = tz * TZ;
   if (gy0 >= d.Y) return;  // rows of a brick cut by the volume
@@ -1260,6 +1262,36 @@ __global__ void __launch_bounds__(B_THREADS, 8) k_brick_tma(const __grid_constan
     }
     __syncthreads();  // buffer b & 1 is free for batch b + 2
   }
+}
+
+__global__ void __launch_bounds__(B_THREADS, 8) k_brick_tma(const __grid_constant__ CUtensorMap mtok,
+                                                             const BrickArgs a) {
+  __shared__ __align__(128) unsigned char smem[kBrickSmem];
+  brick_tma_body(mtok, a, blockIdx.x, smem);
+}
+
+template <bool kDense>
+__global__ void __launch_bounds__(32 * kTokRows, 4) k_tokens_tma(const __grid_constant__ CUtensorMap mld,
+                                                                const __grid_constant__ CUtensorMap mla,
+                                                                const BrickArgs a) {
+  __shared__ __align__(128) unsigned char smem[kTokSmem];
+  tokens_tma_body<kDense>(mld, mla, a, blockIdx.x, smem);
+}
+
+// Pass C, one launch per brick z-layer s: the tokens of layer s and the
+// count pass of layer s - 2 (whose tokens and following layer are complete),
+// CTAs interleaved so that the memory-bound token work and the issue-bound
+// cube classification share every SM.
+static_assert(TY / kTokRows == TY / RY && 32 * kTokRows == B_THREADS, "token and count items must match");
+__global__ void __launch_bounds__(B_THREADS, 4) k_slab_tma(const __grid_constant__ CUtensorMap mld,
+                                                           const __grid_constant__ CUtensorMap mla,
+                                                           const __grid_constant__ CUtensorMap mtok,
+                                                           const BrickArgs ta, const BrickArgs ca) {
+  __shared__ __align__(128) unsigned char smem[kTokSmem > kBrickSmem ? kTokSmem : kBrickSmem];
+  if (blockIdx.x & 1)
+    brick_tma_body(mtok, ca, blockIdx.x >> 1, smem);
+  else
+    tokens_tma_body<true>(mld, mla, ta, blockIdx.x >> 1, smem);
 }
 
 // Region token -> dense MS id.
@@ -1688,6 +1720,31 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
       // count pass of layer s-1 (which reads layer s's first vertex layer)
       // on the side stream as soon as they are written
       const uint32_t bpl = d.tx * d.ty;
+      const unsigned items = bpl * (TY / kTokRows);
+      if (lt_tma && tok_tma) {
+        // one stream: launch L = tokens of layer L with the count pass of
+        // layer L - 2 in the same grid (see k_slab_tma), then the last two
+        // count passes together
+        for (uint32_t L = 0; L < d.tz; ++L) {
+          BrickArgs ts = ba;
+          ts.brick0 = L * bpl;
+          if (L >= 2) {
+            BrickArgs cs = ba;
+            cs.brick0 = (L - 2) * bpl;
+            k_slab_tma<<<2 * items, B_THREADS, 0, c.stream>>>(mld, mla, mtok, ts, cs);
+            CK_LAUNCH("k_slab_tma");
+          } else {
+            k_tokens_tma<true><<<items, 32 * kTokRows, 0, c.stream>>>(mld, mla, ts);
+            CK_LAUNCH("k_tokens");
+          }
+        }
+        BrickArgs cs = ba;
+        const uint32_t c0 = d.tz >= 2 ? d.tz - 2 : 0;
+        cs.brick0 = c0 * bpl;
+        k_brick_tma<<<(d.tz - c0) * items, B_THREADS, 0, c.stream>>>(mtok, cs);
+        CK_LAUNCH("k_brick");
+        CK(cudaEventRecord(c.join, c.stream));
+      } else
       for (uint32_t sl = 0; sl <= d.tz; ++sl) {
         if (sl < d.tz) {
           BrickArgs bs = ba;
@@ -1709,8 +1766,8 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
             k_brick<<<bpl * (TY / RY), B_THREADS, 0, c.side>>>(bs);
           CK_LAUNCH("k_brick");
         }
+        if (sl == d.tz) CK(cudaEventRecord(c.join, c.side));
       }
-      CK(cudaEventRecord(c.join, c.side));
       const int64_t nb = int64_t((nw + kWB - 1) / kWB);
       uint64_t* bsum = c.get_t<uint64_t>(S_HASH_V, nb);
       k_bitmap_count<<<unsigned(nb), 256, 0, c.stream>>>(bitmap, nw, bsum);
