@@ -1151,6 +1151,16 @@ __global__ void __launch_bounds__(B_THREADS, 4) k_brick(const BrickArgs a) {
 constexpr int TLW = 36;  // padded ring row (16-byte multiple of u32)
 constexpr int kBrickBufWords = ((kBatch + 1) * (RY + 1) * TLW + 31) / 32 * 32;  // one staged batch
 constexpr int kBrickSmem = 2 * kBrickBufWords * 4;
+// Record count of a cube with three or more labels (rare): out of line so
+// the unrolled count loop stays small in the instruction cache.
+__device__ __noinline__ uint32_t general_count(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t c4,
+                                               uint32_t c5, uint32_t c6, uint32_t c7) {
+  const uint32_t c[8] = {c0, c1, c2, c3, c4, c5, c6, c7};
+  uint32_t cnt = 0;
+  cube_codes(c, g_tlut, cnt);
+  return cnt;
+}
+
 __device__ __forceinline__ void brick_tma_body(const CUtensorMap& mtok, const BrickArgs& a, const uint32_t blk,
                                                unsigned char* smem) {
   // each buffer starts on a 128-byte boundary (TMA destination)
@@ -1176,7 +1186,7 @@ __device__ __forceinline__ void brick_tma_body(const CUtensorMap& mtok, const Br
   uint64_t* chp = a.chunk + (uint64_t(cy) + uint64_t(d.Y - 1) * gz0) * a.nxc + tx;
   const uint64_t chstep = uint64_t(d.Y - 1) * a.nxc;
   uint32_t pf[4] = {0, 0, 0, 0};  // top face of this thread's previous cube
-  bool have_prev = false;
+  bool pu = false;                 // ... and whether its four labels agree
   if (tid == 0) {
     for (int k = 0; k < 2; ++k) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s_bar[k])));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -1194,6 +1204,57 @@ __device__ __forceinline__ void brick_tma_body(const CUtensorMap& mtok, const Br
         : "memory");
   };
   if (tid == 0 && nb > 0) issue(0);
+  // one cube layer; the bottom face is the previous layer's top face, so a
+  // cube is uniform iff its top face is, the bottom one was, and one
+  // vertical edge agrees
+  auto cube = [&](const uint32_t(&cur)[RY + 1][TLW]) {
+    uint32_t cnt = 0;
+    if (cube_ok) {
+      uint32_t c[8];
+      c[0] = pf[0];
+      c[1] = pf[1];
+      c[2] = pf[2];
+      c[3] = pf[3];
+      c[4] = cur[w][lane];
+      c[5] = cur[w][lane + 1];
+      c[6] = cur[w + 1][lane];
+      c[7] = cur[w + 1][lane + 1];
+      const bool tu = c[5] == c[4] && c[6] == c[4] && c[7] == c[4];
+      const bool uni = tu && pu && c[4] == c[0];
+      pf[0] = c[4];
+      pf[1] = c[5];
+      pf[2] = c[6];
+      pf[3] = c[7];
+      pu = tu;
+      uint32_t cls = 0;
+      if (!uni) {
+        // corners equal to corner 0 (bit i)
+        uint32_t m8 = 1u;
+#pragma unroll
+        for (int i = 1; i < 8; ++i) m8 |= uint32_t(c[i] == c[0]) << i;
+        // the lowest corner with another label; two labels iff every
+        // corner carries one of the two (the common case on a separator)
+        uint32_t bb = c[7];
+#pragma unroll
+        for (int i = 6; i >= 1; --i) bb = (m8 >> i) & 1u ? bb : c[i];
+        uint32_t mb = 0u;
+#pragma unroll
+        for (int i = 1; i < 8; ++i) mb |= uint32_t(c[i] == bb) << i;
+        if ((m8 | mb) == 0xffu) {
+          cnt = g_two_cnt[m8 >> 1];
+          cls = m8;
+        } else {
+          cnt = general_count(c[0], c[1], c[2], c[3], c[4], c[5], c[6], c[7]);
+          cls = 0xffu;
+        }
+      }
+      *clsp = uint8_t(cls);
+    }
+    const uint32_t tot = __any_sync(0xffffffffu, cnt != 0) ? __reduce_add_sync(0xffffffffu, cnt) : 0u;
+    if (lane == 0 && row_ok) *chp = tot;
+    clsp += CXY;
+    chp += chstep;
+  };
   for (int b = 0; b < nb; ++b) {
     if (tid == 0 && b + 1 < nb) issue(b + 1);  // the other buffer was released by the barrier below
     asm volatile(
@@ -1201,65 +1262,17 @@ __device__ __forceinline__ void brick_tma_body(const CUtensorMap& mtok, const Br
             smem_u32(&s_bar[b & 1])),
         "r"(uint32_t((b >> 1) & 1))
         : "memory");
-    const int cn = min(kBatch, ncl - b * kBatch);
-    for (int cl = 0; cl < cn; ++cl) {
-      const uint32_t(&lo)[RY + 1][TLW] = (*buf[b & 1])[cl];
-      const uint32_t(&cur)[RY + 1][TLW] = (*buf[b & 1])[cl + 1];
-      uint32_t cnt = 0;
-      if (cube_ok) {
-        uint32_t c[8];
-        // bottom face = the previous cube layer's top face (registers)
-        if (have_prev) {
-          c[0] = pf[0];
-          c[1] = pf[1];
-          c[2] = pf[2];
-          c[3] = pf[3];
-        } else {
-          c[0] = lo[w][lane];
-          c[1] = lo[w][lane + 1];
-          c[2] = lo[w + 1][lane];
-          c[3] = lo[w + 1][lane + 1];
-        }
-        c[4] = cur[w][lane];
-        c[5] = cur[w][lane + 1];
-        c[6] = cur[w + 1][lane];
-        c[7] = cur[w + 1][lane + 1];
-        pf[0] = c[4];
-        pf[1] = c[5];
-        pf[2] = c[6];
-        pf[3] = c[7];
-        have_prev = true;
-        const bool uni = c[1] == c[0] && c[2] == c[0] && c[3] == c[0] && c[4] == c[0] && c[5] == c[0] &&
-                         c[6] == c[0] && c[7] == c[0];
-        uint32_t cls = 0;
-        if (!uni) {
-          // corners equal to corner 0 (bit i)
-          uint32_t m8 = 1u;
-#pragma unroll
-          for (int i = 1; i < 8; ++i) m8 |= uint32_t(c[i] == c[0]) << i;
-          // the lowest corner with another label; two labels iff every
-          // corner carries one of the two (the common case on a separator)
-          uint32_t bb = c[7];
-#pragma unroll
-          for (int i = 6; i >= 1; --i) bb = (m8 >> i) & 1u ? bb : c[i];
-          uint32_t mb = 0u;
-#pragma unroll
-          for (int i = 1; i < 8; ++i) mb |= uint32_t(c[i] == bb) << i;
-          if ((m8 | mb) == 0xffu) {
-            cnt = g_two_cnt[m8 >> 1];
-            cls = m8;
-          } else {
-            cube_codes(c, g_tlut, cnt);
-            cls = 0xffu;
-          }
-        }
-        *clsp = uint8_t(cls);
-      }
-      const uint32_t tot = __any_sync(0xffffffffu, cnt != 0) ? __reduce_add_sync(0xffffffffu, cnt) : 0u;
-      if (lane == 0 && row_ok) *chp = tot;
-      clsp += CXY;
-      chp += chstep;
+    const Buf& bb = *buf[b & 1];
+    if (b == 0 && cube_ok) {
+      pf[0] = bb[0][w][lane];
+      pf[1] = bb[0][w][lane + 1];
+      pf[2] = bb[0][w + 1][lane];
+      pf[3] = bb[0][w + 1][lane + 1];
+      pu = pf[1] == pf[0] && pf[2] == pf[0] && pf[3] == pf[0];
     }
+    const int cn = min(kBatch, ncl - b * kBatch);
+#pragma unroll 1
+    for (int cl = 0; cl < cn; ++cl) cube(bb[cl + 1]);
     __syncthreads();  // buffer b & 1 is free for batch b + 2
   }
 }
