@@ -1329,6 +1329,35 @@ struct EmitArgs {
 // marching.cpp:116-215). Warps walk whole cube rows; lane = cube of the chunk;
 // records are dealt out one per lane (consecutive lanes write consecutive
 // 16-byte records).
+// Rare emission paths (cubes with three or more labels), out of line: the
+// tet codes with the record count (count << 32 | codes), and a record's tet,
+// recipe row and the two cube corners whose labels it separates
+// (t | rowi << 8 | corner a << 16 | corner b << 24).
+__device__ __noinline__ uint64_t general_codes(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t c4,
+                                               uint32_t c5, uint32_t c6, uint32_t c7) {
+  const uint32_t c[8] = {c0, c1, c2, c3, c4, c5, c6, c7};
+  uint32_t cnt = 0;
+  const uint32_t code6 = cube_codes(c, g_tlut, cnt);
+  return uint64_t(cnt) << 32 | code6;
+}
+__device__ __noinline__ uint32_t general_record(uint32_t c6, uint32_t k) {
+  uint32_t t = 0;
+  uint32_t cs = g_cases[c6 & 31];
+#pragma unroll
+  for (int tt = 0; tt < 5; ++tt) {
+    if (k < (cs & 15)) break;
+    k -= cs & 15;
+    ++t;
+    cs = g_cases[(c6 >> (5 * t)) & 31];
+  }
+  const uint32_t rowi = (cs >> 4) + k;
+  const uint32_t row = g_rows[rowi];
+  // tet t = cube corners {0, cb, cc, 7}
+  const uint32_t cb = (0x442211u >> (4 * t)) & 15, cc = (0x656353u >> (4 * t)) & 15;
+  auto corner = [&](uint32_t p) { return p == 0 ? 0u : (p == 1 ? cb : (p == 2 ? cc : 7u)); };
+  return t | rowi << 8 | corner((row >> 12) & 3) << 16 | corner((row >> 14) & 3) << 24;
+}
+
 __global__ void __launch_bounds__(256) k_emit_chunks(const EmitArgs a) {
   __shared__ uint8_t s_own[256 / 32][32];  // record window position -> lane of the cube starting there
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -1406,7 +1435,9 @@ __global__ void __launch_bounds__(256) k_emit_chunks(const EmitArgs a) {
       }
       uint32_t cnt = 0, code6 = 0, lo2 = 0, hi2 = 0;
       if (cls == 0xffu) {
-        code6 = cube_codes(c, g_tlut, cnt);
+        const uint64_t g = general_codes(c[0], c[1], c[2], c[3], c[4], c[5], c[6], c[7]);
+        code6 = uint32_t(g);
+        cnt = uint32_t(g >> 32);
       } else if (cls != 0) {
         // two labels: corner 0's and that of the lowest corner outside its set
         cnt = g_two_cnt[cls >> 1];
@@ -1451,23 +1482,12 @@ __global__ void __launch_bounds__(256) k_emit_chunks(const EmitArgs a) {
           la = l2;
           lb = h2;
         } else {
-          t = 0;
-          uint32_t cs = g_cases[c6 & 31];
-#pragma unroll
-          for (int tt = 0; tt < 5; ++tt) {
-            if (k < (cs & 15)) break;
-            k -= cs & 15;
-            ++t;
-            cs = g_cases[(c6 >> (5 * t)) & 31];
-          }
-          rowi = (cs >> 4) + k;
-          const uint32_t row = g_rows[rowi];
-          // tet t = cube corners {0, cb, cc, 7}
-          const uint32_t cb = (0x442211u >> (4 * t)) & 15, cc = (0x656353u >> (4 * t)) & 15;
-          auto corner = [&](uint32_t p) { return p == 0 ? 0u : (p == 1 ? cb : (p == 2 ? cc : 7u)); };
+          const uint32_t r = general_record(c6, k);
+          t = r & 0xffu;
+          rowi = (r >> 8) & 0xffu;
           const uint32_t vs = v0 - uint32_t(lane) + uint32_t(src);
-          la = __ldg(a.ids + vs + corner_off(corner((row >> 12) & 3)));
-          lb = __ldg(a.ids + vs + corner_off(corner((row >> 14) & 3)));
+          la = __ldg(a.ids + vs + corner_off((r >> 16) & 0xffu));
+          lb = __ldg(a.ids + vs + corner_off(r >> 24));
         }
         const uint64_t cr64 = ((6ull * (q0 + uint32_t(src)) + t) << 6) | uint64_t(rowi);
         *reinterpret_cast<uint4*>(a.out + base + j) =
