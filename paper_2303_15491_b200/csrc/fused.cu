@@ -259,27 +259,35 @@ __global__ void __launch_bounds__(A_THREADS, 1)
         const float fv = a3;
         if (!isfinite(fv)) atomicMin(&ctr->bad, gv0 + d.XY * uint32_t(lz));
         const float fn[14] = {a0m, a1m, a2m, a3m, a0, a1, a2, a4, a5, a6, a3p, a4p, a5p, a6p};
-        float M = fn[0], m = fn[0];
+        // Maxima / minima of the lower (s < 7, ids below v) and upper
+        // (s >= 7) halves. The highest s attaining M lies in the upper half
+        // iff the upper half attains M; the lowest s attaining m lies in the
+        // lower half iff that one does. NaN (missing) neighbours never win.
+        float Ml = fn[0], ml = fn[0], Mh = fn[7], mh = fn[7];
 #pragma unroll
-        for (int s = 1; s < 14; ++s) {
-          M = fmaxf(M, fn[s]);
-          m = fminf(m, fn[s]);
+        for (int s = 1; s < 7; ++s) {
+          Ml = fmaxf(Ml, fn[s]);
+          ml = fminf(ml, fn[s]);
+          Mh = fmaxf(Mh, fn[7 + s]);
+          mh = fminf(mh, fn[7 + s]);
         }
-        // which neighbours attain M (m): 1.0 / 0.0 flags (PTX set, one ALU
-        // op each) summed with weights 2^s (2^(13-s)) on the FMA pipe; the
-        // highest weight present is the float's exponent. Exact: distinct
-        // powers of two below 2^14.
+        const float M = fmaxf(Ml, Mh), m = fminf(ml, mh);
+        const bool up_hi = Mh == M, dn_lo = ml == m;
+        // which of the chosen half's 7 neighbours attain M (m): 1.0 / 0.0
+        // flags (PTX set, one ALU op each) summed with weights 2^i
+        // (2^(6-i)) on the FMA pipe; the highest weight present is the
+        // float's exponent. Exact: distinct powers of two below 2^7.
         float au = 0.f, ad = 0.f;
 #pragma unroll
-        for (int s = 0; s < 14; ++s) {
-          au = __fmaf_rn(feq(fn[s], M), float(1 << s), au);
-          ad = __fmaf_rn(feq(fn[s], m), float(1 << (13 - s)), ad);
+        for (int i = 0; i < 7; ++i) {
+          au = __fmaf_rn(feq(up_hi ? fn[7 + i] : fn[i], M), float(1 << i), au);
+          ad = __fmaf_rn(feq(dn_lo ? fn[i] : fn[7 + i], m), float(1 << (6 - i)), ad);
         }
         // au == 0 only when every neighbour is missing (M is NaN): no hop
-        const uint32_t hu = uint32_t(__float_as_int(au) >> 23) - 127u;          // highest s attaining M
-        const uint32_t hd = 13u - (uint32_t(__float_as_int(ad) >> 23) - 127u);  // lowest s attaining m
-        const uint32_t su = (M > fv || (M == fv && au >= 128.f)) ? hu : 15u;
-        const uint32_t sd = (m < fv || (m == fv && ad >= 128.f)) ? hd : 15u;
+        const uint32_t hu = uint32_t(__float_as_int(au) >> 23) - 127u + (up_hi ? 7u : 0u);  // highest s attaining M
+        const uint32_t hd = (dn_lo ? 6u : 13u) - (uint32_t(__float_as_int(ad) >> 23) - 127u);  // lowest s attaining m
+        const uint32_t su = (M > fv || (M == fv && up_hi)) ? hu : 15u;
+        const uint32_t sd = (m < fv || (m == fv && dn_lo)) ? hd : 15u;
         code[hc + (lz + 1) * PXY] = uint8_t(su | (sd << 4));
       }
       a0m = a0;
