@@ -1388,31 +1388,37 @@ __global__ void __launch_bounds__(256) k_emit_chunks(const EmitArgs a) {
     const uint32_t cz_l = r_l / CY, cy_l = r_l - cz_l * CY;
     const uint32_t x0_l = 32 * xs_l;
     const uint32_t v0_l = x0_l + a.X * cy_l + XY * cz_l;  // min corner of the chunk's first cube
-    const uint64_t q0_l = uint64_t(x0_l) + uint64_t(CX) * r_l;
+    const uint32_t q0_l = x0_l + CX * r_l;  // cube ids < n < 2^32
     const uint32_t T_l = uint32_t(nx_off - my_off);
     // one busy chunk ahead: its classes and the ids of its cubes' four
     // corner rows (lane i: corners 0, 2, 4, 6 of cube i; corners 1, 3, 5, 7
     // come from lane i + 1, lane 31 loads them) are loaded while the current
     // chunk is emitted
     struct Pre {
-      uint32_t cls, r[4], e[4];
+      uint32_t cls, v0, q0, r[4], e[4];
     };
+    const uint32_t X = a.X;
     auto fetch = [&](int k, Pre& p) {
       const uint32_t cx = __shfl_sync(0xffffffffu, x0_l, k) + uint32_t(lane);
-      const uint32_t v0 = __shfl_sync(0xffffffffu, v0_l, k) + uint32_t(lane);
-      const uint64_t q0 = __shfl_sync(0xffffffffu, q0_l, k);
+      p.v0 = __shfl_sync(0xffffffffu, v0_l, k) + uint32_t(lane);
+      p.q0 = __shfl_sync(0xffffffffu, q0_l, k);
+      const uint32_t v0 = p.v0;
       p.cls = 0;
 #pragma unroll
       for (int i = 0; i < 4; ++i) p.r[i] = p.e[i] = 0;
       if (cx <= CX) {  // the vertex past the last cube is that cube's corner 1
-#pragma unroll
-        for (int i = 0; i < 4; ++i) p.r[i] = __ldg(a.ids + v0 + corner_off(uint32_t(2 * i)));
+        p.r[0] = __ldg(a.ids + v0);
+        p.r[1] = __ldg(a.ids + (v0 + X));
+        p.r[2] = __ldg(a.ids + (v0 + XY));
+        p.r[3] = __ldg(a.ids + (v0 + XY + X));
       }
       if (cx < CX) {
-        p.cls = a.cls[q0 + lane];
+        p.cls = a.cls[p.q0 + uint32_t(lane)];
         if (lane == 31) {
-#pragma unroll
-          for (int i = 0; i < 4; ++i) p.e[i] = __ldg(a.ids + v0 + corner_off(uint32_t(2 * i + 1)));
+          p.e[0] = __ldg(a.ids + (v0 + 1));
+          p.e[1] = __ldg(a.ids + (v0 + X + 1));
+          p.e[2] = __ldg(a.ids + (v0 + XY + 1));
+          p.e[3] = __ldg(a.ids + (v0 + XY + X + 1));
         }
       }
     };
@@ -1431,8 +1437,8 @@ __global__ void __launch_bounds__(256) k_emit_chunks(const EmitArgs a) {
       }
       const uint64_t base = __shfl_sync(0xffffffffu, my_off, kc);
       const uint32_t T = __shfl_sync(0xffffffffu, T_l, kc);
-      const uint64_t q0 = __shfl_sync(0xffffffffu, q0_l, kc);  // cube id of lane 0's cube
-      const uint32_t v0 = __shfl_sync(0xffffffffu, v0_l, kc) + uint32_t(lane);  // this lane's min corner
+      const uint32_t q0 = cur.q0;  // cube id of lane 0's cube
+      const uint32_t v0 = cur.v0;  // this lane's min corner
       const uint32_t cls = cur.cls;
       uint32_t c[8];
 #pragma unroll
@@ -1494,10 +1500,10 @@ __global__ void __launch_bounds__(256) k_emit_chunks(const EmitArgs a) {
           t = r & 0xffu;
           rowi = (r >> 8) & 0xffu;
           const uint32_t vs = v0 - uint32_t(lane) + uint32_t(src);
-          la = __ldg(a.ids + vs + corner_off((r >> 16) & 0xffu));
-          lb = __ldg(a.ids + vs + corner_off(r >> 24));
+          la = __ldg(a.ids + (vs + corner_off((r >> 16) & 0xffu)));
+          lb = __ldg(a.ids + (vs + corner_off(r >> 24)));
         }
-        const uint64_t cr64 = ((6ull * (q0 + uint32_t(src)) + t) << 6) | uint64_t(rowi);
+        const uint64_t cr64 = ((6ull * uint64_t(q0 + uint32_t(src)) + t) << 6) | uint64_t(rowi);
         *reinterpret_cast<uint4*>(a.out + base + j) =
             make_uint4(uint32_t(cr64), uint32_t(cr64 >> 32), min(la, lb), max(la, lb));
       }
