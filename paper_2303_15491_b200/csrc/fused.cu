@@ -1215,7 +1215,8 @@ __device__ __forceinline__ void brick_tma_body(const CUtensorMap& mtok, const Br
   // one cube layer; the bottom face is the previous layer's top face, so a
   // cube is uniform iff its top face is, the bottom one was, and one
   // vertical edge agrees
-  auto cube = [&](const uint32_t(&cur)[RY + 1][TLW]) {
+  uint32_t btot = 0;  // lane l: record count of cube layer l of the batch
+  auto cube = [&](const uint32_t(&cur)[RY + 1][TLW], const int cl) {
     uint32_t cnt = 0;
     if (cube_ok) {
       uint32_t c[8];
@@ -1258,10 +1259,9 @@ __device__ __forceinline__ void brick_tma_body(const CUtensorMap& mtok, const Br
       }
       *clsp = uint8_t(cls);
     }
-    const uint32_t tot = __any_sync(0xffffffffu, cnt != 0) ? __reduce_add_sync(0xffffffffu, cnt) : 0u;
-    if (lane == 0 && row_ok) *chp = tot;
+    const uint32_t tot = __reduce_add_sync(0xffffffffu, cnt);
+    if (lane == cl) btot = tot;
     clsp += CXY;
-    chp += chstep;
   };
   for (int b = 0; b < nb; ++b) {
     if (tid == 0 && b + 1 < nb) issue(b + 1);  // the other buffer was released by the barrier below
@@ -1280,7 +1280,10 @@ __device__ __forceinline__ void brick_tma_body(const CUtensorMap& mtok, const Br
     }
     const int cn = min(kBatch, ncl - b * kBatch);
 #pragma unroll 1
-    for (int cl = 0; cl < cn; ++cl) cube(bb[cl + 1]);
+    for (int cl = 0; cl < cn; ++cl) cube(bb[cl + 1], cl);
+    // the batch's chunk counts, one store per layer from lanes 0 .. cn-1
+    if (lane < cn && row_ok) chp[uint64_t(lane) * chstep] = btot;
+    chp += uint64_t(kBatch) * chstep;
     __syncthreads();  // buffer b & 1 is free for batch b + 2
   }
 }
