@@ -1194,7 +1194,7 @@ __device__ __forceinline__ void brick_tma_body(const CUtensorMap& mtok, const Br
   uint64_t* chp = a.chunk + (uint64_t(cy) + uint64_t(d.Y - 1) * gz0) * a.nxc + tx;
   const uint64_t chstep = uint64_t(d.Y - 1) * a.nxc;
   uint32_t pf[4] = {0, 0, 0, 0};  // top face of this thread's previous cube
-  bool pu = false;                 // ... and whether its four labels agree
+  uint32_t pu = 0;                 // ... and whether its four labels agree (0 / 1)
   if (tid == 0) {
     for (int k = 0; k < 2; ++k) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s_bar[k])));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -1228,8 +1228,8 @@ __device__ __forceinline__ void brick_tma_body(const CUtensorMap& mtok, const Br
       c[5] = cur[w][lane + 1];
       c[6] = cur[w + 1][lane];
       c[7] = cur[w + 1][lane + 1];
-      const bool tu = c[5] == c[4] && c[6] == c[4] && c[7] == c[4];
-      const bool uni = tu && pu && c[4] == c[0];
+      const uint32_t tu = c[5] == c[4] && c[6] == c[4] && c[7] == c[4];
+      const bool uni = (tu & pu) && c[4] == c[0];
       pf[0] = c[4];
       pf[1] = c[5];
       pf[2] = c[6];
@@ -1279,8 +1279,13 @@ __device__ __forceinline__ void brick_tma_body(const CUtensorMap& mtok, const Br
       pu = pf[1] == pf[0] && pf[2] == pf[0] && pf[3] == pf[0];
     }
     const int cn = min(kBatch, ncl - b * kBatch);
+    if (cn == kBatch) {
+#pragma unroll 2
+      for (int cl = 0; cl < kBatch; ++cl) cube(bb[cl + 1], cl);
+    } else {
 #pragma unroll 1
-    for (int cl = 0; cl < cn; ++cl) cube(bb[cl + 1], cl);
+      for (int cl = 0; cl < cn; ++cl) cube(bb[cl + 1], cl);
+    }
     // the batch's chunk counts, one store per layer from lanes 0 .. cn-1
     if (lane < cn && row_ok) chp[uint64_t(lane) * chstep] = btot;
     chp += uint64_t(kBatch) * chstep;
@@ -1288,7 +1293,7 @@ __device__ __forceinline__ void brick_tma_body(const CUtensorMap& mtok, const Br
   }
 }
 
-__global__ void __launch_bounds__(B_THREADS, 8) k_brick_tma(const __grid_constant__ CUtensorMap mtok,
+__global__ void __launch_bounds__(B_THREADS, 6) k_brick_tma(const __grid_constant__ CUtensorMap mtok,
                                                              const BrickArgs a) {
   __shared__ __align__(128) unsigned char smem[kBrickSmem];
   brick_tma_body(mtok, a, blockIdx.x, smem);
