@@ -879,7 +879,7 @@ struct BrickArgs {
 // vertex's slot in the region hash set; equal tokens <=> equal (asc, desc)
 // pairs. Thread per (x, y) column of a brick, kTokZ layers of loads in
 // flight per step; the last pair of the column is cached (runs along z).
-constexpr int kTokRows = 8, kTokZ = 16;
+constexpr int kTokRows = 8, kTokZ = 8;
 
 template <bool kDense>
 __global__ void __launch_bounds__(32 * kTokRows) k_tokens(const BrickArgs a) {
@@ -1312,7 +1312,7 @@ __global__ void __launch_bounds__(32 * kTokRows, 4) k_tokens_tma(const __grid_co
 // CTAs interleaved so that the memory-bound token work and the issue-bound
 // cube classification share every SM.
 static_assert(TY / kTokRows == TY / RY && 32 * kTokRows == B_THREADS, "token and count items must match");
-__global__ void __launch_bounds__(B_THREADS, 4) k_slab_tma(const __grid_constant__ CUtensorMap mld,
+__global__ void __launch_bounds__(B_THREADS, 5) k_slab_tma(const __grid_constant__ CUtensorMap mld,
                                                            const __grid_constant__ CUtensorMap mla,
                                                            const __grid_constant__ CUtensorMap mtok,
                                                            const BrickArgs ta, const BrickArgs ca) {
