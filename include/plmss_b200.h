@@ -39,7 +39,9 @@ enum plmss_status {
   PLMSS_ERR_LOGIC = 2,
   PLMSS_ERR_OUT_OF_RANGE = 3,
   PLMSS_ERR_CUDA = 4,
-  PLMSS_ERR_NOMEM = 5
+  PLMSS_ERR_NOMEM = 5,
+  PLMSS_ERR_FORMAT = 6, /* io.hpp FormatError: malformed file or dims  */
+  PLMSS_ERR_IO = 7      /* io.hpp IoError: open / read / write failure */
 };
 
 /* Scalar key types accepted by segmentation. */
@@ -227,6 +229,45 @@ int plmss_b200_copy(plmss_ctx* ctx, void* dst, const void* d_src, int64_t bytes,
  *                           pipeline's passes C and D (default 1); if the
  *                           forest has not converged by then, the sweeps
  *                           continue and C, D are redone (0 forces that path). */
+/* ---- callers either side of the path ------------------
+ * weld_points (marching.hpp:138-140, marching.cpp:400-417): merges
+ * bitwise-identical points of a separator soup in place, the first occurrence
+ * of each point keeping its place in order; d_points is (n_points, 3) float64
+ * (the reference's column-major Matrix3Xd), d_indices are remapped.
+ * *n_unique receives the new point count. Out-of-range indices:
+ * PLMSS_ERR_OUT_OF_RANGE. */
+int plmss_b200_weld_points(plmss_ctx* ctx, double* d_points, int64_t n_points, int64_t* d_indices,
+                           int64_t n_indices, int64_t* n_unique);
+
+/* read_volume (io.hpp:46-55, io.cpp:90-124): headerless little-endian raw
+ * volume, x fastest, streamed through pinned staging buffers into device
+ * memory: d_out is float64 (out_f64 = 1, like the reference's ScalarField) or
+ * float32 (out_f64 = 0, the pipeline's input; refused for f64le files). File
+ * size != X*Y*Z*sizeof(dtype): PLMSS_ERR_FORMAT with the reference's text. */
+enum plmss_dtype {
+  PLMSS_DTYPE_F32LE = 0,
+  PLMSS_DTYPE_F64LE = 1,
+  PLMSS_DTYPE_U8 = 2,
+  PLMSS_DTYPE_U16LE = 3,
+  PLMSS_DTYPE_I16LE = 4
+};
+int plmss_b200_read_volume(plmss_ctx* ctx, const char* path, const int64_t dims[3], int dtype, int out_f64,
+                           void* d_out);
+
+/* write_labels (io.hpp:66-70, io.cpp:216-235): "PLMSSLBL", u32 1, u64 n, then
+ * (u64 asc, u64 desc) per vertex, from device label arrays (label_type 0 =
+ * uint32, 1 = int64), streamed in chunks. */
+int plmss_b200_write_labels(plmss_ctx* ctx, const char* path, int label_type, const void* d_asc,
+                            const void* d_desc, int64_t n);
+
+/* write_surface_obj (io.hpp:79-83, io.cpp:268-299): the reference's OBJ text
+ * ("v %.17g %.17g %.17g", "g rA_rB" on region changes, 1-based "f"/"l"
+ * lines) from device arrays: points (n_points, 3) float64, indices
+ * (n_prims * verts_per_prim) int64, regions (n_prims, 2) int64. */
+int plmss_b200_write_surface_obj(plmss_ctx* ctx, const char* path, const double* d_points, int64_t n_points,
+                                 const int64_t* d_indices, const int64_t* d_regions, int64_t n_prims,
+                                 int verts_per_prim);
+
 enum plmss_option {
   PLMSS_OPT_COMBINE_PATH = 1,
   PLMSS_OPT_PIPELINE_PATH = 2,

@@ -207,7 +207,15 @@ class ReferenceError_(RuntimeError):
     pass
 
 
-_KIND = {1: ValueError, 2: RuntimeError, 3: IndexError, 4: RuntimeError}
+class RefFormatError(RuntimeError):
+    """plmss::FormatError raised by the compiled reference (io.hpp:22-24)."""
+
+
+class RefIoError(RuntimeError):
+    """plmss::IoError raised by the compiled reference (io.hpp:27-29)."""
+
+
+_KIND = {1: ValueError, 2: RuntimeError, 3: IndexError, 4: RuntimeError, 6: RefFormatError, 7: RefIoError}
 
 
 class Reference:
@@ -239,6 +247,40 @@ class Reference:
         L.cap_run_benchmark.argtypes = [_i64p, _f64p, C.c_int, C.c_int, C.c_int, _f64p]
         L.cap_run_once.argtypes = [_i64p, np.ctypeslib.ndpointer(np.float32, flags="C_CONTIGUOUS"), C.c_int,
                                    C.c_int, _f64p, _i64p]
+        if hasattr(L, "cap_weld"):
+            L.cap_weld.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.POINTER(C.c_int64)]
+            L.cap_read_volume.argtypes = [C.c_char_p, _i64p, C.c_char_p, C.c_void_p]
+            L.cap_write_labels.argtypes = [C.c_char_p, C.c_void_p, C.c_void_p, C.c_int64]
+            L.cap_write_obj.argtypes = [C.c_char_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_int64,
+                                        C.c_int]
+
+    # ---- callers either side of the path (io.cpp, marching.cpp:400-417)
+    def weld_points(self, points, indices):
+        """Reference weld_points on an (n, 3) soup; returns (points, indices)."""
+        p = np.array(points, dtype=np.float64, order="C").reshape(-1, 3).copy()
+        i = np.array(indices, dtype=np.int64).ravel().copy()
+        u = C.c_int64()
+        self._check(self.lib.cap_weld(p.ctypes.data, p.shape[0], i.ctypes.data, i.size, C.byref(u)))
+        return p[: u.value], i
+
+    def read_volume(self, path, dims, dtype="f32le"):
+        d = _dims(dims)
+        n = int(np.prod(d)) if (d > 0).all() else 0
+        out = np.zeros(max(n, 1), np.float64)
+        self._check(self.lib.cap_read_volume(os.fsencode(str(path)), d, dtype.encode(), out.ctypes.data))
+        return out[:n]
+
+    def write_labels(self, path, asc, desc):
+        a = np.ascontiguousarray(asc, dtype=np.int64)
+        b = np.ascontiguousarray(desc, dtype=np.int64)
+        self._check(self.lib.cap_write_labels(os.fsencode(str(path)), a.ctypes.data, b.ctypes.data, a.size))
+
+    def write_surface_obj(self, path, points, indices, regions, verts_per_prim=3):
+        p = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 3)
+        i = np.ascontiguousarray(indices, dtype=np.int64).ravel()
+        r = np.ascontiguousarray(regions, dtype=np.int64).reshape(-1, 2)
+        self._check(self.lib.cap_write_obj(os.fsencode(str(path)), p.ctypes.data, p.shape[0], i.ctypes.data,
+                                           r.ctypes.data, r.shape[0], verts_per_prim))
 
     def run_once(self, dims, values_f32, workers, mode=2):
         """One reference pipeline pass (bench.cpp:62-87); returns (phase

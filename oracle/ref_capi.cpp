@@ -13,7 +13,7 @@
 // Every entry point forwards to the reference public API declared in
 // proj/include/plmss/{orderfield,segmentation,marching,bench}.hpp and converts
 // C++ exceptions into (status, message): 1 invalid_argument, 2 logic_error,
-// 3 out_of_range, 4 other.
+// 3 out_of_range, 4 other, 6 io FormatError, 7 io IoError.
 #include <chrono>
 #include <cstdint>
 #include <cstring>
@@ -25,6 +25,7 @@
 
 #include "plmss/bench.hpp"
 #include "plmss/complex.hpp"
+#include "plmss/io.hpp"
 #include "plmss/marching.hpp"
 #include "plmss/orderfield.hpp"
 #include "plmss/segmentation.hpp"
@@ -47,6 +48,12 @@ int guarded(F&& f) {
   } catch (const std::logic_error& e) {
     g_error = e.what();
     return 2;
+  } catch (const plmss::FormatError& e) {
+    g_error = e.what();
+    return 6;
+  } catch (const plmss::IoError& e) {
+    g_error = e.what();
+    return 7;
   } catch (const std::exception& e) {
     g_error = e.what();
     return 4;
@@ -310,6 +317,59 @@ int cap_run_once(const int64_t* dims, const float* values, int workers, int mode
     }
     counts_out[0] = seg.num_regions();
     counts_out[1] = prims;
+  });
+}
+
+// weld_points (marching.cpp:400-417) on a soup given as (n, 3) points and
+// indices; both are overwritten, *n_unique = points kept.
+int cap_weld(double* points, int64_t n, int64_t* indices, int64_t m, int64_t* n_unique) {
+  return guarded([&] {
+    plmss::SeparatingMesh mesh;
+    mesh.points.resize(3, n);
+    if (n) std::memcpy(mesh.points.data(), points, sizeof(double) * 3 * static_cast<size_t>(n));
+    mesh.indices.assign(indices, indices + m);
+    plmss::weld_points(mesh);
+    *n_unique = mesh.points.cols();
+    if (mesh.points.cols())
+      std::memcpy(points, mesh.points.data(), sizeof(double) * 3 * static_cast<size_t>(mesh.points.cols()));
+    if (m) std::memcpy(indices, mesh.indices.data(), sizeof(int64_t) * static_cast<size_t>(m));
+  });
+}
+
+// read_volume (io.cpp:90-124): values as doubles into out (X*Y*Z).
+int cap_read_volume(const char* path, const int64_t* dims, const char* dtype, double* out) {
+  return guarded([&] {
+    plmss::VolumeSpec spec;
+    spec.path = path;
+    spec.dims = {dims[0], dims[1], dims[2]};
+    spec.dtype = plmss::parse_dtype(dtype);
+    const plmss::VolumeData d = plmss::read_volume(spec);
+    std::memcpy(out, d.field.values.data(), sizeof(double) * static_cast<size_t>(d.field.values.size()));
+  });
+}
+
+int cap_write_labels(const char* path, const int64_t* asc, const int64_t* desc, int64_t n) {
+  return guarded([&] {
+    plmss::SegmentationResult seg;
+    seg.asc.assign(asc, asc + n);
+    seg.desc.assign(desc, desc + n);
+    plmss::write_labels(seg, path);
+  });
+}
+
+// write_surface_obj (io.cpp:268-299); regions are (n_prims, 2).
+int cap_write_obj(const char* path, const double* points, int64_t n_points, const int64_t* indices,
+                  const int64_t* regions, int64_t n_prims, int verts_per_prim) {
+  return guarded([&] {
+    plmss::SeparatingMesh mesh;
+    mesh.verts_per_primitive = verts_per_prim;
+    mesh.points.resize(3, n_points);
+    if (n_points) std::memcpy(mesh.points.data(), points, sizeof(double) * 3 * static_cast<size_t>(n_points));
+    mesh.indices.assign(indices, indices + n_prims * verts_per_prim);
+    mesh.regions.resize(static_cast<size_t>(n_prims));
+    for (int64_t i = 0; i < n_prims; ++i) mesh.regions[i] = {regions[2 * i], regions[2 * i + 1]};
+    mesh.source_cells.assign(static_cast<size_t>(n_prims), 0);
+    plmss::write_surface_obj(mesh, path);
   });
 }
 

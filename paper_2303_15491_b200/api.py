@@ -7,7 +7,8 @@ comes from torch (plumbing only). Every call runs on the B200 through
 missing CUDA device raises immediately.
 
 Error behaviour mirrors the reference exceptions: std::invalid_argument ->
-ValueError, std::logic_error -> RuntimeError, std::out_of_range -> IndexError.
+ValueError, std::logic_error -> RuntimeError, std::out_of_range -> IndexError,
+io.hpp FormatError -> FormatError, IoError -> IoError.
 """
 from __future__ import annotations
 
@@ -25,7 +26,16 @@ KEY_F32, KEY_F64, KEY_RANK = 0, 1, 2
 ASCENDING, DESCENDING, BOTH = 0, 1, 2
 OPT_COMBINE_PATH, OPT_PIPELINE_PATH, OPT_TMA, OPT_SPECULATIVE_SWEEPS = 1, 2, 3, 4
 
-_ERR = {1: ValueError, 2: RuntimeError, 3: IndexError, 4: RuntimeError, 5: MemoryError}
+class FormatError(RuntimeError):
+    """io.hpp:22-24: malformed input (sizes, magic, unknown dtype)."""
+
+
+class IoError(RuntimeError):
+    """io.hpp:27-29: underlying read/write failure."""
+
+
+_ERR = {1: ValueError, 2: RuntimeError, 3: IndexError, 4: RuntimeError, 5: MemoryError, 6: FormatError, 7: IoError}
+DTYPES = {"f32le": 0, "f64le": 1, "u8": 2, "u16le": 3, "i16le": 4}
 
 HEADER_FUNCTIONS = [
     "plmss_b200_tet_table", "plmss_b200_last_error", "plmss_b200_version", "plmss_b200_ctx_create",
@@ -35,7 +45,8 @@ HEADER_FUNCTIONS = [
     "plmss_b200_materialize_separators", "plmss_b200_emit_boundaries", "plmss_b200_pipeline",
     "plmss_b200_result", "plmss_b200_copy", "plmss_b200_ctx_set_option", "plmss_b200_pipeline_host",
     "plmss_b200_synth", "plmss_b200_launch_count", "plmss_b200_ctx_stats", "plmss_b200_count_by_cell_ranges",
-    "plmss_b200_compress_sweep", "plmss_b200_segment_slab",
+    "plmss_b200_compress_sweep", "plmss_b200_segment_slab", "plmss_b200_weld_points", "plmss_b200_read_volume",
+    "plmss_b200_write_labels", "plmss_b200_write_surface_obj",
 ]
 
 
@@ -86,6 +97,10 @@ def lib() -> C.CDLL:
         L.plmss_b200_copy.argtypes = [vp, vp, vp, i64, i32]
         L.plmss_b200_pipeline_host.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i64, C.POINTER(PlmssResult)]
         L.plmss_b200_synth.argtypes = [vp, vp, i32, vp, i32, C.c_double, C.c_uint64, i32, vp]
+        L.plmss_b200_weld_points.argtypes = [vp, vp, i64, vp, i64, C.POINTER(i64)]
+        L.plmss_b200_read_volume.argtypes = [vp, C.c_char_p, vp, i32, i32, vp]
+        L.plmss_b200_write_labels.argtypes = [vp, C.c_char_p, i32, vp, vp, i64]
+        L.plmss_b200_write_surface_obj.argtypes = [vp, C.c_char_p, vp, i64, vp, vp, i64, i32]
         L.plmss_b200_tet_table.argtypes = [vp, vp]
         L.plmss_b200_tet_table.restype = None
         L.plmss_b200_launch_count.restype = C.c_ulonglong
@@ -525,3 +540,63 @@ def synth_field(dims, kind: str = "gaussians", gaussians=None, noise_amp: float 
     _check(lib().plmss_b200_synth(ctx.h, d.ctypes.data, k, g.ctypes.data, g.shape[0], noise_amp, seed, levels,
                                   _ptr(f)))
     return f
+
+
+# ---------------------------------------------------------------------------
+# Callers either side of the path: volume ingest, the
+# reference file formats, point welding.
+
+def weld_points(points, indices, ctx: Optional[Context] = None):
+    """marching.cpp:400-417 on the device: merge bitwise-identical points
+    ((n, 3) float64), the first occurrence keeping its place; indices (int64)
+    are remapped in place. Returns (points[:unique], indices)."""
+    ctx = ctx or default_context()
+    if points.dtype != _torch().float64 or indices.dtype != _torch().int64:
+        raise ValueError("weld_points needs float64 points and int64 indices")
+    pts, idx = points.contiguous(), indices.contiguous()
+    u = C.c_int64()
+    _check(lib().plmss_b200_weld_points(ctx.h, _ptr(pts), pts.shape[0] if pts.numel() else 0, _ptr(idx),
+                                        idx.numel(), C.byref(u)))
+    if idx.data_ptr() != indices.data_ptr():
+        indices.copy_(idx)
+    if pts.data_ptr() != points.data_ptr():
+        points.copy_(pts)
+    return points[: u.value], indices
+
+
+def read_volume(path, dims, dtype: str = "f32le", out: str = "f32", ctx: Optional[Context] = None):
+    """io.cpp:90-124: a raw little-endian volume (x fastest) streamed into a
+    device tensor — float32 (the pipeline's input) or float64 (the reference's
+    ScalarField values)."""
+    torch = _torch()
+    ctx = ctx or default_context()
+    if dtype not in DTYPES:
+        raise FormatError(f"unknown dtype '{dtype}' (expected f32le, f64le, u8, u16le, or i16le)")
+    d = _dims(dims)
+    n = int(np.prod(d)) if (d > 0).all() else 0
+    t = torch.empty(max(n, 1), dtype=torch.float64 if out == "f64" else torch.float32, device=f"cuda:{ctx.device}")
+    _check(lib().plmss_b200_read_volume(ctx.h, os.fsencode(str(path)), d.ctypes.data, DTYPES[dtype],
+                                        1 if out == "f64" else 0, _ptr(t)))
+    return t[:n]
+
+
+def write_labels(path, asc, desc, ctx: Optional[Context] = None):
+    """io.cpp:216-235: "PLMSSLBL", u32 1, u64 n, (u64 asc, u64 desc) per
+    vertex, from device label arrays (uint32 or int64)."""
+    ctx = ctx or default_context()
+    a, b = asc.contiguous(), desc.contiguous()
+    if a.shape != b.shape or a.dtype != b.dtype:
+        raise ValueError("label output needs matching ascending and descending arrays")
+    lt = _label_type(a)
+    _check(lib().plmss_b200_write_labels(ctx.h, os.fsencode(str(path)), lt, _ptr(a), _ptr(b), a.numel()))
+
+
+def write_surface_obj(path, points, indices, regions, verts_per_prim: int = 3, ctx: Optional[Context] = None):
+    """io.cpp:268-299: the reference's OBJ text from device arrays (points
+    (n, 3) float64, indices int64, regions (m, 2) int64)."""
+    ctx = ctx or default_context()
+    pts, idx, reg = points.contiguous(), indices.contiguous(), regions.contiguous()
+    n_prims = reg.shape[0] if reg.numel() else 0
+    _check(lib().plmss_b200_write_surface_obj(ctx.h, os.fsencode(str(path)), _ptr(pts),
+                                              pts.shape[0] if pts.numel() else 0, _ptr(idx), _ptr(reg), n_prims,
+                                              verts_per_prim))

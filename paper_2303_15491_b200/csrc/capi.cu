@@ -504,4 +504,45 @@ int plmss_b200_synth(plmss_ctx* p, const int64_t dims[3], int kind, const double
   });
 }
 
+int plmss_b200_weld_points(plmss_ctx* p, double* d_points, int64_t n_points, int64_t* d_indices, int64_t n_indices,
+                           int64_t* n_unique) {
+  return guarded([&] {
+    Ctx& c = C(p);
+    set_device(c);
+    if ((n_points && !d_points) || (n_indices && !d_indices)) fail(PLMSS_ERR_INVALID_ARGUMENT, "null array");
+    const int64_t u = weld_points(c, d_points, n_points, d_indices, n_indices);
+    if (n_unique) *n_unique = u;
+  });
+}
+
+int plmss_b200_read_volume(plmss_ctx* p, const char* path, const int64_t dims[3], int dtype, int out_f64,
+                           void* d_out) {
+  return guarded([&] {
+    Ctx& c = C(p);
+    set_device(c);
+    if (!dims || !d_out) fail(PLMSS_ERR_INVALID_ARGUMENT, "null dims or output");
+    read_volume(c, path, dims, dtype, out_f64, d_out);
+  });
+}
+
+int plmss_b200_write_labels(plmss_ctx* p, const char* path, int label_type, const void* d_asc, const void* d_desc,
+                            int64_t n) {
+  return guarded([&] {
+    Ctx& c = C(p);
+    set_device(c);
+    if (label_type != 0 && label_type != 1) fail(PLMSS_ERR_INVALID_ARGUMENT, "label_type must be 0 or 1");
+    write_labels(c, path, label_type, d_asc, d_desc, n);
+  });
+}
+
+int plmss_b200_write_surface_obj(plmss_ctx* p, const char* path, const double* d_points, int64_t n_points,
+                                 const int64_t* d_indices, const int64_t* d_regions, int64_t n_prims,
+                                 int verts_per_prim) {
+  return guarded([&] {
+    Ctx& c = C(p);
+    set_device(c);
+    write_surface_obj(c, path, d_points, n_points, d_indices, d_regions, n_prims, verts_per_prim);
+  });
+}
+
 }  // extern "C"

@@ -192,6 +192,12 @@ bool fused_supported(const Grid& g);
 FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* desc, uint32_t* asc, uint32_t* ms);
 
 // synth.cu
+// io.cu: callers either side of the path
+int64_t weld_points(Ctx& c, double* d_points, int64_t n, int64_t* d_indices, int64_t m);
+void read_volume(Ctx& c, const char* path, const int64_t dims[3], int dtype, int out_f64, void* d_out);
+void write_labels(Ctx& c, const char* path, int label_type, const void* d_asc, const void* d_desc, int64_t n);
+void write_surface_obj(Ctx& c, const char* path, const double* d_points, int64_t n_points, const int64_t* d_indices,
+                       const int64_t* d_regions, int64_t n_prims, int verts_per_prim);
 void synth(Ctx& c, const Grid& g, int kind, const double* h_gauss, int n_gauss, double noise_amp,
            uint64_t seed, int levels, float* field);
 

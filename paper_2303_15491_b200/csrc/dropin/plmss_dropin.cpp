@@ -525,10 +525,23 @@ void append_mesh(SeparatingMesh& mesh, const SeparatingMesh& extra) {
   mesh.source_cells.insert(mesh.source_cells.end(), extra.source_cells.begin(), extra.source_cells.end());
 }
 
-void weld_points(SeparatingMesh&) {
-  throw std::logic_error(
-      "weld_points (marching.cpp:400-417) is post-processing outside the B200 hot path and not provided by the "
-      "drop-in");
+void weld_points(SeparatingMesh& mesh) {
+  // marching.cpp:400-417 on the device (plmss_b200_weld_points): the first
+  // occurrence of every bitwise-distinct point keeps its place in order
+  const int64_t n = mesh.points.cols(), m = static_cast<int64_t>(mesh.indices.size());
+  if (n == 0) {
+    if (m) throw std::out_of_range("point index out of range");
+    return;
+  }
+  DevBuf<double> dp(3 * n);
+  DevBuf<int64_t> di(m);
+  dp.up(mesh.points.data(), 3 * n);
+  di.up(mesh.indices.data(), m);
+  int64_t unique = 0;
+  check(plmss_b200_weld_points(ctx(), dp.p, n, di.p, m, &unique));
+  dp.down(mesh.points.data(), 3 * unique);
+  mesh.points.conservativeResize(3, unique);
+  di.down(mesh.indices.data(), m);
 }
 
 }  // namespace plmss

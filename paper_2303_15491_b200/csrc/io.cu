@@ -1,0 +1,376 @@
+// Callers either side of the hot path:
+//  * weld_points (marching.cpp:400-417): merge bitwise-identical separator
+//    points, first occurrence wins, indices remapped — on the device;
+//  * read_volume (io.cpp:90-124): a raw little-endian volume streamed from
+//    the file through pinned staging buffers straight into device memory
+//    (f32 for the pipeline, or f64 like the reference's ScalarField);
+//  * write_labels (io.cpp:216-235) and write_surface_obj (io.cpp:268-299):
+//    the reference file formats written from device arrays, streamed in
+//    chunks (device -> pinned host -> file), OBJ text formatted by host
+//    threads in order.
+#include <errno.h>
+#include <fcntl.h>
+#include <stdio.h>
+#include <string.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "common.cuh"
+
+namespace plmss_b200 {
+
+namespace {
+
+// ------------------------------------------------------------ weld_points --
+// Open-addressing table of point indices keyed by the point's 3 x 64 bits.
+// A slot holds some index of its point class; atomicMin keeps the lowest, so
+// once all inserts are done the slot names the class's first occurrence.
+constexpr unsigned long long kNoSlot = ~0ull;
+
+__device__ __forceinline__ uint64_t point_hash(uint64_t x, uint64_t y, uint64_t z) {
+  uint64_t h = x * 0x9E3779B97F4A7C15ull ^ (y + 0x632BE59BD9B4E019ull) * 0xC2B2AE3D27D4EB4Full ^
+               (z + 0x165667B19E3779F9ull) * 0xD6E8FEB86659FD93ull;
+  h ^= h >> 32;
+  h *= 0xD6E8FEB86659FD93ull;
+  h ^= h >> 29;
+  return h;
+}
+
+__device__ __forceinline__ bool same_point(const uint64_t* __restrict__ p, uint64_t j, uint64_t x, uint64_t y,
+                                           uint64_t z) {
+  return p[3 * j] == x && p[3 * j + 1] == y && p[3 * j + 2] == z;
+}
+
+__global__ void k_weld_insert(const uint64_t* __restrict__ p, int64_t n, unsigned long long* __restrict__ table,
+                              uint64_t mask) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint64_t x = p[3 * i], y = p[3 * i + 1], z = p[3 * i + 2];
+  for (uint64_t h = point_hash(x, y, z) & mask;; h = (h + 1) & mask) {
+    unsigned long long cur = table[h];
+    if (cur == kNoSlot) {
+      cur = atomicCAS(&table[h], kNoSlot, (unsigned long long)i);
+      if (cur == kNoSlot) return;
+    }
+    // every index a slot ever holds belongs to the same point class
+    if (same_point(p, cur, x, y, z)) {
+      atomicMin(&table[h], (unsigned long long)i);
+      return;
+    }
+  }
+}
+
+// rep[i] = first occurrence of point i's class; flag[i] = 1 when i is it
+__global__ void k_weld_rep(const uint64_t* __restrict__ p, int64_t n, const unsigned long long* __restrict__ table,
+                           uint64_t mask, int64_t* __restrict__ rep, uint64_t* __restrict__ flag) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint64_t x = p[3 * i], y = p[3 * i + 1], z = p[3 * i + 2];
+  for (uint64_t h = point_hash(x, y, z) & mask;; h = (h + 1) & mask) {
+    const unsigned long long cur = table[h];
+    if (same_point(p, cur, x, y, z)) {
+      rep[i] = int64_t(cur);
+      flag[i] = cur == (unsigned long long)i;
+      return;
+    }
+  }
+}
+
+// first occurrences move to their rank (into a copy); rep becomes the remap
+__global__ void k_weld_compact(const uint64_t* __restrict__ p, int64_t n, const int64_t* __restrict__ rep,
+                               const uint64_t* __restrict__ rank, uint64_t* __restrict__ out) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n || rep[i] != i) return;
+  const uint64_t r = rank[i];
+  out[3 * r] = p[3 * i];
+  out[3 * r + 1] = p[3 * i + 1];
+  out[3 * r + 2] = p[3 * i + 2];
+}
+
+__global__ void k_weld_remap(int64_t* __restrict__ idx, int64_t m, const int64_t* __restrict__ rep,
+                             const uint64_t* __restrict__ rank, int64_t n, int* __restrict__ bad) {
+  const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= m) return;
+  const int64_t v = idx[k];
+  if (v < 0 || v >= n) {
+    *bad = 1;
+    return;
+  }
+  idx[k] = int64_t(rank[rep[v]]);
+}
+
+// ------------------------------------------------------------ read_volume --
+__global__ void k_convert_volume(const unsigned char* __restrict__ src, int64_t count, int dtype, int out_f64,
+                                 void* __restrict__ dst) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  double v;
+  switch (dtype) {
+    case PLMSS_DTYPE_F32LE: v = double(reinterpret_cast<const float*>(src)[i]); break;
+    case PLMSS_DTYPE_F64LE: v = reinterpret_cast<const double*>(src)[i]; break;
+    case PLMSS_DTYPE_U8: v = double(src[i]); break;
+    case PLMSS_DTYPE_U16LE: v = double(reinterpret_cast<const uint16_t*>(src)[i]); break;
+    default: v = double(reinterpret_cast<const int16_t*>(src)[i]); break;
+  }
+  if (out_f64)
+    static_cast<double*>(dst)[i] = v;
+  else  // exact for every dtype but f64 (refused by the host side)
+    static_cast<float*>(dst)[i] = float(v);
+}
+
+size_t dtype_bytes(int dtype) {
+  switch (dtype) {
+    case PLMSS_DTYPE_F32LE: return 4;
+    case PLMSS_DTYPE_F64LE: return 8;
+    case PLMSS_DTYPE_U8: return 1;
+    case PLMSS_DTYPE_U16LE:
+    case PLMSS_DTYPE_I16LE: return 2;
+  }
+  fail(PLMSS_ERR_FORMAT, "unknown dtype " + std::to_string(dtype) + " (expected f32le, f64le, u8, u16le, or i16le)");
+}
+
+// Pinned staging buffers owned by one call.
+struct Pinned {
+  void* p = nullptr;
+  explicit Pinned(size_t bytes) { CK(cudaMallocHost(&p, bytes)); }
+  ~Pinned() {
+    if (p) cudaFreeHost(p);
+  }
+  unsigned char* b() const { return static_cast<unsigned char*>(p); }
+};
+
+struct File {
+  int fd = -1;
+  File(const char* path, int flags, const std::string& what) {
+    fd = ::open(path, flags, 0644);
+    if (fd < 0) fail(PLMSS_ERR_IO, "cannot open " + std::string(path) + what);
+  }
+  ~File() {
+    if (fd >= 0) ::close(fd);
+  }
+};
+
+void write_all(int fd, const void* data, size_t bytes, const char* path) {
+  const char* p = static_cast<const char*>(data);
+  while (bytes) {
+    const ssize_t w = ::write(fd, p, bytes);
+    if (w < 0 && errno == EINTR) continue;
+    if (w <= 0) fail(PLMSS_ERR_IO, "write failed on " + std::string(path));
+    p += w;
+    bytes -= size_t(w);
+  }
+}
+
+constexpr size_t kChunk = size_t(64) << 20;  // staging chunk (bytes)
+
+}  // namespace
+
+int64_t weld_points(Ctx& c, double* d_points, int64_t n, int64_t* d_indices, int64_t m) {
+  if (n < 0 || m < 0) fail(PLMSS_ERR_INVALID_ARGUMENT, "negative size");
+  if (n == 0) {
+    if (m) fail(PLMSS_ERR_OUT_OF_RANGE, "point index out of range");
+    return 0;
+  }
+  uint64_t cap = 1024;
+  while (cap < 2 * uint64_t(n)) cap <<= 1;
+  auto* table = c.get_t<unsigned long long>(S_HASH_V, cap);
+  auto* rep = c.get_t<int64_t>(S_SORT_A, n);
+  auto* rank = c.get_t<uint64_t>(S_SORT_B, n);
+  auto* copy = c.get_t<uint64_t>(S_SORT_C, 3 * uint64_t(n));
+  int* bad = static_cast<int*>(c.get(S_FLAGS, 1024)) + 40;
+  const uint64_t* p = reinterpret_cast<const uint64_t*>(d_points);
+  CK(cudaMemsetAsync(table, 0xff, cap * 8, c.stream));
+  CK(cudaMemsetAsync(bad, 0, 4, c.stream));
+  k_weld_insert<<<blocks_for(n, 256), 256, 0, c.stream>>>(p, n, table, cap - 1);
+  CK_LAUNCH("k_weld_insert");
+  k_weld_rep<<<blocks_for(n, 256), 256, 0, c.stream>>>(p, n, table, cap - 1, rep, rank);
+  CK_LAUNCH("k_weld_rep");
+  const int64_t unique = int64_t(exclusive_scan_u64(c, rank, n, true));  // flags -> ranks of first occurrences
+  k_weld_compact<<<blocks_for(n, 256), 256, 0, c.stream>>>(p, n, rep, rank, copy);
+  CK_LAUNCH("k_weld_compact");
+  if (m) {
+    k_weld_remap<<<blocks_for(m, 256), 256, 0, c.stream>>>(d_indices, m, rep, rank, n, bad);
+    CK_LAUNCH("k_weld_remap");
+  }
+  CK(cudaMemcpyAsync(d_points, copy, size_t(unique) * 24, cudaMemcpyDeviceToDevice, c.stream));
+  CK(cudaMemcpyAsync(c.h_pinned + 3, bad, 4, cudaMemcpyDeviceToHost, c.stream));
+  c.sync();
+  if (*reinterpret_cast<int*>(c.h_pinned + 3)) fail(PLMSS_ERR_OUT_OF_RANGE, "point index out of range");
+  return unique;
+}
+
+void read_volume(Ctx& c, const char* path, const int64_t dims[3], int dtype, int out_f64, void* d_out) {
+  if (!path) fail(PLMSS_ERR_INVALID_ARGUMENT, "null path");
+  const int64_t n = dims[0] * dims[1] * dims[2];
+  if (dims[0] <= 0 || dims[1] <= 0 || dims[2] <= 0) fail(PLMSS_ERR_FORMAT, "volume dims must be positive");
+  const size_t elem = dtype_bytes(dtype);
+  if (!out_f64 && dtype == PLMSS_DTYPE_F64LE)
+    fail(PLMSS_ERR_INVALID_ARGUMENT, "f64le volumes need a float64 destination");
+  const uint64_t expected = uint64_t(n) * elem;
+  struct stat st;
+  if (::stat(path, &st) != 0) fail(PLMSS_ERR_IO, "cannot stat " + std::string(path) + ": " + strerror(errno));
+  if (uint64_t(st.st_size) != expected)
+    fail(PLMSS_ERR_FORMAT, std::string(path) + ": expected " + std::to_string(expected) + " bytes, got " +
+                               std::to_string(uint64_t(st.st_size)));
+  File f(path, O_RDONLY, "");
+  // two pinned chunks: the file read of one overlaps the copy + conversion
+  // of the other
+  const size_t chunk = kChunk / 8 * 8;
+  Pinned stage(2 * chunk);
+  unsigned char* dev = c.get_t<unsigned char>(S_TMP0, 2 * chunk);
+  cudaEvent_t done[2];
+  for (auto& e : done) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  try {
+    uint64_t off = 0;
+    for (int k = 0; off < expected; ++k) {
+      const int b = k & 1;
+      const size_t len = size_t(std::min<uint64_t>(chunk, expected - off));
+      CK(cudaEventSynchronize(done[b]));  // buffer b is free again
+      size_t got = 0;
+      while (got < len) {
+        const ssize_t r = ::pread(f.fd, stage.b() + b * chunk + got, len - got, off_t(off + got));
+        if (r < 0 && errno == EINTR) continue;
+        if (r <= 0) fail(PLMSS_ERR_IO, "short read on " + std::string(path));
+        got += size_t(r);
+      }
+      CK(cudaMemcpyAsync(dev + b * chunk, stage.b() + b * chunk, len, cudaMemcpyHostToDevice, c.stream));
+      const int64_t cnt = int64_t(len / elem), first = int64_t(off / elem);
+      void* dst = out_f64 ? static_cast<void*>(static_cast<double*>(d_out) + first)
+                          : static_cast<void*>(static_cast<float*>(d_out) + first);
+      k_convert_volume<<<blocks_for(cnt, 256), 256, 0, c.stream>>>(dev + b * chunk, cnt, dtype, out_f64, dst);
+      CK_LAUNCH("k_convert_volume");
+      CK(cudaEventRecord(done[b], c.stream));
+      off += len;
+    }
+    c.sync();
+  } catch (...) {
+    cudaStreamSynchronize(c.stream);
+    for (auto& e : done) cudaEventDestroy(e);
+    throw;
+  }
+  for (auto& e : done) CK(cudaEventDestroy(e));
+}
+
+void write_labels(Ctx& c, const char* path, int label_type, const void* d_asc, const void* d_desc, int64_t n) {
+  if (!path) fail(PLMSS_ERR_INVALID_ARGUMENT, "null path");
+  if (!d_asc || !d_desc || n < 0)
+    fail(PLMSS_ERR_INVALID_ARGUMENT, "label output needs matching ascending and descending arrays");
+  const size_t w = label_type == 0 ? 4 : 8;
+  File f(path, O_WRONLY | O_CREAT | O_TRUNC, " for writing");
+  unsigned char head[20] = {'P', 'L', 'M', 'S', 'S', 'L', 'B', 'L', 1, 0, 0, 0};
+  for (int i = 0; i < 8; ++i) head[12 + i] = uint8_t(uint64_t(n) >> (8 * i));
+  write_all(f.fd, head, sizeof head, path);
+  const int64_t per = int64_t(kChunk / 16);
+  Pinned raw(2 * size_t(per) * w);
+  std::vector<uint64_t> rec;
+  for (int64_t v0 = 0; v0 < n; v0 += per) {
+    const int64_t cnt = std::min(per, n - v0);
+    CK(cudaMemcpyAsync(raw.b(), static_cast<const char*>(d_asc) + v0 * w, size_t(cnt) * w, cudaMemcpyDeviceToHost,
+                       c.stream));
+    CK(cudaMemcpyAsync(raw.b() + size_t(per) * w, static_cast<const char*>(d_desc) + v0 * w, size_t(cnt) * w,
+                       cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    rec.resize(2 * size_t(cnt));
+    auto at = [&](const unsigned char* base, int64_t i) -> uint64_t {
+      if (w == 4) return reinterpret_cast<const uint32_t*>(base)[i];
+      return reinterpret_cast<const uint64_t*>(base)[i];
+    };
+    for (int64_t i = 0; i < cnt; ++i) {  // little-endian host: records are the words themselves
+      rec[2 * i] = at(raw.b(), i);
+      rec[2 * i + 1] = at(raw.b() + size_t(per) * w, i);
+    }
+    write_all(f.fd, rec.data(), rec.size() * 8, path);
+  }
+}
+
+void write_surface_obj(Ctx& c, const char* path, const double* d_points, int64_t n_points, const int64_t* d_indices,
+                       const int64_t* d_regions, int64_t n_prims, int verts_per_prim) {
+  if (!path) fail(PLMSS_ERR_INVALID_ARGUMENT, "null path");
+  if (verts_per_prim != 2 && verts_per_prim != 3) fail(PLMSS_ERR_INVALID_ARGUMENT, "verts_per_prim must be 2 or 3");
+  if (n_points < 0 || n_prims < 0) fail(PLMSS_ERR_INVALID_ARGUMENT, "negative size");
+  File f(path, O_WRONLY | O_CREAT | O_TRUNC, " for writing");
+  {
+    const std::string head = "# separating geometry: " + std::to_string(n_points) + " points, " +
+                             std::to_string(n_prims) + (verts_per_prim == 3 ? " triangles\n" : " segments\n");
+    write_all(f.fd, head.data(), head.size(), path);
+  }
+  const unsigned nthreads = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+  // format [0, cnt) items of a chunk on nthreads threads, then write in order
+  auto parallel_format = [&](int64_t cnt, const std::function<void(int64_t, int64_t, std::string&)>& fmt) {
+    std::vector<std::string> parts(nthreads);
+    std::vector<std::thread> th;
+    const int64_t per = (cnt + nthreads - 1) / nthreads;
+    for (unsigned t = 0; t < nthreads; ++t) {
+      const int64_t b = std::min(cnt, int64_t(t) * per), e = std::min(cnt, b + per);
+      th.emplace_back([&, t, b, e] { fmt(b, e, parts[t]); });
+    }
+    for (auto& x : th) x.join();
+    for (auto& s : parts) write_all(f.fd, s.data(), s.size(), path);
+  };
+  // points: "v %.17g %.17g %.17g"
+  {
+    const int64_t per = int64_t(kChunk / 24);
+    Pinned buf(size_t(per) * 24);
+    const double* hp = reinterpret_cast<const double*>(buf.p);
+    for (int64_t p0 = 0; p0 < n_points; p0 += per) {
+      const int64_t cnt = std::min(per, n_points - p0);
+      CK(cudaMemcpyAsync(buf.p, d_points + 3 * p0, size_t(cnt) * 24, cudaMemcpyDeviceToHost, c.stream));
+      c.sync();
+      parallel_format(cnt, [&](int64_t b, int64_t e, std::string& s) {
+        char line[96];
+        s.reserve(size_t(e - b) * 60);
+        for (int64_t i = b; i < e; ++i) {
+          const int len = snprintf(line, sizeof line, "v %.17g %.17g %.17g\n", hp[3 * i], hp[3 * i + 1], hp[3 * i + 2]);
+          s.append(line, size_t(len));
+        }
+      });
+    }
+  }
+  // primitives: "g rA[_rB]" whenever the region pair changes, then
+  // "f i j k" / "l i j" with 1-based indices
+  {
+    const int64_t per = int64_t(kChunk / 48);
+    const int vp = verts_per_prim;
+    Pinned ibuf(size_t(per) * vp * 8), rbuf(size_t(per) * 16);
+    const int64_t* hi = reinterpret_cast<const int64_t*>(ibuf.p);
+    const int64_t* hr = reinterpret_cast<const int64_t*>(rbuf.p);
+    int64_t prev[2] = {-2, -2};  // region pair of the primitive before the chunk
+    for (int64_t q0 = 0; q0 < n_prims; q0 += per) {
+      const int64_t cnt = std::min(per, n_prims - q0);
+      CK(cudaMemcpyAsync(ibuf.p, d_indices + q0 * vp, size_t(cnt) * vp * 8, cudaMemcpyDeviceToHost, c.stream));
+      CK(cudaMemcpyAsync(rbuf.p, d_regions + 2 * q0, size_t(cnt) * 16, cudaMemcpyDeviceToHost, c.stream));
+      c.sync();
+      const int64_t p0a = prev[0], p0b = prev[1];
+      parallel_format(cnt, [&](int64_t b, int64_t e, std::string& s) {
+        int64_t ca = b ? hr[2 * (b - 1)] : p0a, cb = b ? hr[2 * (b - 1) + 1] : p0b;
+        s.reserve(size_t(e - b) * 40);
+        char line[96];
+        for (int64_t i = b; i < e; ++i) {
+          if (hr[2 * i] != ca || hr[2 * i + 1] != cb) {
+            ca = hr[2 * i];
+            cb = hr[2 * i + 1];
+            const int len = cb >= 0 ? snprintf(line, sizeof line, "g r%lld_r%lld\n", (long long)ca, (long long)cb)
+                                    : snprintf(line, sizeof line, "g r%lld\n", (long long)ca);
+            s.append(line, size_t(len));
+          }
+          int len = 0;
+          if (vp == 3)
+            len = snprintf(line, sizeof line, "f %lld %lld %lld\n", (long long)(hi[3 * i] + 1),
+                           (long long)(hi[3 * i + 1] + 1), (long long)(hi[3 * i + 2] + 1));
+          else
+            len = snprintf(line, sizeof line, "l %lld %lld\n", (long long)(hi[2 * i] + 1), (long long)(hi[2 * i + 1] + 1));
+          s.append(line, size_t(len));
+        }
+      });
+      prev[0] = hr[2 * (cnt - 1)];
+      prev[1] = hr[2 * (cnt - 1) + 1];
+    }
+  }
+}
+
+}  // namespace plmss_b200

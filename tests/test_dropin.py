@@ -109,3 +109,16 @@ def test_reference_harness_runs_the_b200_path(gpu, dropin):
     ph = dropin.run_benchmark(dims, g["field"].astype(np.float64), workers=2, repeats=3)
     assert set(ph) == {"order", "segmentation", "combine", "index", "geometry"}
     assert all(v >= 0 for v in ph.values())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["gauss_17x13x11", "noise_12x12x12"])
+def test_dropin_weld_points_matches_reference(gpu, dropin, reference, name):
+    # marching.cpp:400-417 through the reference API, served by the device weld
+    g = load_case(name)
+    dims = tuple(int(x) for x in g["dims"])
+    sep = reference.emit_separators(dims, g["ms_region"])
+    rp, ri = reference.weld_points(sep["points"], sep["indices"])
+    dp, di = dropin.weld_points(sep["points"], sep["indices"])
+    assert rp.shape[0] < sep["points"].shape[0]
+    assert np.array_equal(dp.view(np.uint64), rp.view(np.uint64)) and np.array_equal(di, ri)
