@@ -373,7 +373,7 @@ def main():
     pipe_gbs = b_alg / (ms * 1e-3) / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tp):
+    if os.path.exists(tp) and args.config == "cfg5":  # the captured workload (profiles/traffic.json _source)
         traffic = json.load(open(tp)).get(dom)
 
     # ---- end to end through the C-ABI over pinned host buffers -----------
