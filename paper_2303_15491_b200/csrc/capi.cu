@@ -148,6 +148,7 @@ void plmss_b200_ctx_destroy(plmss_ctx* p) {
   if (c.join) cudaEventDestroy(c.join);
   for (auto& e : c.slab_ev) cudaEventDestroy(e);
   if (c.h_pinned) cudaFreeHost(c.h_pinned);
+  if (c.h_stage) cudaFreeHost(c.h_stage);
   if (c.own_stream) cudaStreamDestroy(c.stream);
   delete p;
 }

@@ -85,6 +85,20 @@ struct Ctx {
   void* buf[S_COUNT] = {};
   size_t cap[S_COUNT] = {};
   uint64_t* h_pinned = nullptr;  // small pinned host staging for counters
+  // pinned staging for the file streams (io.cu), kept across calls: pinning
+  // costs more than the copy of a small volume
+  unsigned char* h_stage = nullptr;
+  size_t h_stage_bytes = 0;
+  unsigned char* stage(size_t bytes) {
+    if (h_stage_bytes < bytes) {
+      if (h_stage) CK(cudaFreeHost(h_stage));
+      h_stage = nullptr;
+      h_stage_bytes = 0;
+      CK(cudaMallocHost(reinterpret_cast<void**>(&h_stage), bytes));
+      h_stage_bytes = bytes;
+    }
+    return h_stage;
+  }
   bool timing = false;
   float stage_ms[8] = {};
   cudaEvent_t ev[9] = {};

@@ -16,6 +16,8 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <exception>
+#include <functional>
 #include <string>
 #include <thread>
 #include <vector>
@@ -134,16 +136,6 @@ size_t dtype_bytes(int dtype) {
   fail(PLMSS_ERR_FORMAT, "unknown dtype " + std::to_string(dtype) + " (expected f32le, f64le, u8, u16le, or i16le)");
 }
 
-// Pinned staging buffers owned by one call.
-struct Pinned {
-  void* p = nullptr;
-  explicit Pinned(size_t bytes) { CK(cudaMallocHost(&p, bytes)); }
-  ~Pinned() {
-    if (p) cudaFreeHost(p);
-  }
-  unsigned char* b() const { return static_cast<unsigned char*>(p); }
-};
-
 struct File {
   int fd = -1;
   File(const char* path, int flags, const std::string& what) {
@@ -165,6 +157,37 @@ void write_all(int fd, const void* data, size_t bytes, const char* path) {
     bytes -= size_t(w);
   }
 }
+
+void pwrite_all(int fd, const void* data, size_t bytes, uint64_t off, const char* path) {
+  const char* p = static_cast<const char*>(data);
+  while (bytes) {
+    const ssize_t w = ::pwrite(fd, p, bytes, off_t(off));
+    if (w < 0 && errno == EINTR) continue;
+    if (w <= 0) fail(PLMSS_ERR_IO, "write failed on " + std::string(path));
+    p += w;
+    off += uint64_t(w);
+    bytes -= size_t(w);
+  }
+}
+
+// Runs fn(t) on nt host threads; the first failure is rethrown.
+void on_threads(unsigned nt, const std::function<void(unsigned)>& fn) {
+  std::vector<std::thread> th;
+  std::vector<std::exception_ptr> err(nt);
+  for (unsigned t = 0; t < nt; ++t)
+    th.emplace_back([&, t] {
+      try {
+        fn(t);
+      } catch (...) {
+        err[t] = std::current_exception();
+      }
+    });
+  for (auto& x : th) x.join();
+  for (auto& e : err)
+    if (e) std::rethrow_exception(e);
+}
+
+unsigned host_threads() { return std::max(1u, std::min(16u, std::thread::hardware_concurrency())); }
 
 constexpr size_t kChunk = size_t(64) << 20;  // staging chunk (bytes)
 
@@ -221,7 +244,7 @@ void read_volume(Ctx& c, const char* path, const int64_t dims[3], int dtype, int
   // two pinned chunks: the file read of one overlaps the copy + conversion
   // of the other
   const size_t chunk = kChunk / 8 * 8;
-  Pinned stage(2 * chunk);
+  unsigned char* stage = c.stage(2 * chunk);
   unsigned char* dev = c.get_t<unsigned char>(S_TMP0, 2 * chunk);
   cudaEvent_t done[2];
   for (auto& e : done) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -231,14 +254,31 @@ void read_volume(Ctx& c, const char* path, const int64_t dims[3], int dtype, int
       const int b = k & 1;
       const size_t len = size_t(std::min<uint64_t>(chunk, expected - off));
       CK(cudaEventSynchronize(done[b]));  // buffer b is free again
-      size_t got = 0;
-      while (got < len) {
-        const ssize_t r = ::pread(f.fd, stage.b() + b * chunk + got, len - got, off_t(off + got));
-        if (r < 0 && errno == EINTR) continue;
-        if (r <= 0) fail(PLMSS_ERR_IO, "short read on " + std::string(path));
-        got += size_t(r);
+      // the chunk is read by several threads (one page-cache copy stream is
+      // slower than PCIe)
+      const unsigned nt = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+      const size_t part = (len / nt + 4095) / 4096 * 4096;
+      std::vector<std::thread> th;
+      std::vector<int> ok(nt, 1);
+      for (unsigned t = 0; t < nt; ++t) {
+        const size_t p0 = std::min(len, size_t(t) * part), p1 = std::min(len, p0 + part);
+        th.emplace_back([&, t, p0, p1] {
+          size_t got = p0;
+          while (got < p1) {
+            const ssize_t r = ::pread(f.fd, stage + b * chunk + got, p1 - got, off_t(off + got));
+            if (r < 0 && errno == EINTR) continue;
+            if (r <= 0) {
+              ok[t] = 0;
+              return;
+            }
+            got += size_t(r);
+          }
+        });
       }
-      CK(cudaMemcpyAsync(dev + b * chunk, stage.b() + b * chunk, len, cudaMemcpyHostToDevice, c.stream));
+      for (auto& x : th) x.join();
+      for (int v : ok)
+        if (!v) fail(PLMSS_ERR_IO, "short read on " + std::string(path));
+      CK(cudaMemcpyAsync(dev + b * chunk, stage + b * chunk, len, cudaMemcpyHostToDevice, c.stream));
       const int64_t cnt = int64_t(len / elem), first = int64_t(off / elem);
       void* dst = out_f64 ? static_cast<void*>(static_cast<double*>(d_out) + first)
                           : static_cast<void*>(static_cast<float*>(d_out) + first);
@@ -266,13 +306,14 @@ void write_labels(Ctx& c, const char* path, int label_type, const void* d_asc, c
   for (int i = 0; i < 8; ++i) head[12 + i] = uint8_t(uint64_t(n) >> (8 * i));
   write_all(f.fd, head, sizeof head, path);
   const int64_t per = int64_t(kChunk / 16);
-  Pinned raw(2 * size_t(per) * w);
+  unsigned char* raw = c.stage(2 * size_t(per) * w);
   std::vector<uint64_t> rec;
+  const unsigned nt = host_threads();
   for (int64_t v0 = 0; v0 < n; v0 += per) {
     const int64_t cnt = std::min(per, n - v0);
-    CK(cudaMemcpyAsync(raw.b(), static_cast<const char*>(d_asc) + v0 * w, size_t(cnt) * w, cudaMemcpyDeviceToHost,
+    CK(cudaMemcpyAsync(raw, static_cast<const char*>(d_asc) + v0 * w, size_t(cnt) * w, cudaMemcpyDeviceToHost,
                        c.stream));
-    CK(cudaMemcpyAsync(raw.b() + size_t(per) * w, static_cast<const char*>(d_desc) + v0 * w, size_t(cnt) * w,
+    CK(cudaMemcpyAsync(raw + size_t(per) * w, static_cast<const char*>(d_desc) + v0 * w, size_t(cnt) * w,
                        cudaMemcpyDeviceToHost, c.stream));
     c.sync();
     rec.resize(2 * size_t(cnt));
@@ -280,11 +321,17 @@ void write_labels(Ctx& c, const char* path, int label_type, const void* d_asc, c
       if (w == 4) return reinterpret_cast<const uint32_t*>(base)[i];
       return reinterpret_cast<const uint64_t*>(base)[i];
     };
-    for (int64_t i = 0; i < cnt; ++i) {  // little-endian host: records are the words themselves
-      rec[2 * i] = at(raw.b(), i);
-      rec[2 * i + 1] = at(raw.b() + size_t(per) * w, i);
-    }
-    write_all(f.fd, rec.data(), rec.size() * 8, path);
+    // records packed and written at their file offsets by host threads
+    // (little-endian host: a record is the two words themselves)
+    const int64_t part = (cnt + nt - 1) / nt;
+    on_threads(nt, [&](unsigned t) {
+      const int64_t b = std::min(cnt, int64_t(t) * part), e = std::min(cnt, b + part);
+      for (int64_t i = b; i < e; ++i) {
+        rec[2 * i] = at(raw, i);
+        rec[2 * i + 1] = at(raw + size_t(per) * w, i);
+      }
+      if (e > b) pwrite_all(f.fd, rec.data() + 2 * b, size_t(e - b) * 16, 20 + uint64_t(v0 + b) * 16, path);
+    });
   }
 }
 
@@ -294,32 +341,37 @@ void write_surface_obj(Ctx& c, const char* path, const double* d_points, int64_t
   if (verts_per_prim != 2 && verts_per_prim != 3) fail(PLMSS_ERR_INVALID_ARGUMENT, "verts_per_prim must be 2 or 3");
   if (n_points < 0 || n_prims < 0) fail(PLMSS_ERR_INVALID_ARGUMENT, "negative size");
   File f(path, O_WRONLY | O_CREAT | O_TRUNC, " for writing");
+  uint64_t fpos = 0;  // file offset of the next part
   {
     const std::string head = "# separating geometry: " + std::to_string(n_points) + " points, " +
                              std::to_string(n_prims) + (verts_per_prim == 3 ? " triangles\n" : " segments\n");
     write_all(f.fd, head.data(), head.size(), path);
+    fpos = head.size();
   }
-  const unsigned nthreads = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+  const unsigned nthreads = host_threads();
   // format [0, cnt) items of a chunk on nthreads threads, then write in order
   auto parallel_format = [&](int64_t cnt, const std::function<void(int64_t, int64_t, std::string&)>& fmt) {
     std::vector<std::string> parts(nthreads);
-    std::vector<std::thread> th;
     const int64_t per = (cnt + nthreads - 1) / nthreads;
-    for (unsigned t = 0; t < nthreads; ++t) {
+    on_threads(nthreads, [&](unsigned t) {
       const int64_t b = std::min(cnt, int64_t(t) * per), e = std::min(cnt, b + per);
-      th.emplace_back([&, t, b, e] { fmt(b, e, parts[t]); });
+      fmt(b, e, parts[t]);
+    });
+    std::vector<uint64_t> at(nthreads);
+    for (unsigned t = 0; t < nthreads; ++t) {
+      at[t] = fpos;
+      fpos += parts[t].size();
     }
-    for (auto& x : th) x.join();
-    for (auto& s : parts) write_all(f.fd, s.data(), s.size(), path);
+    on_threads(nthreads, [&](unsigned t) { pwrite_all(f.fd, parts[t].data(), parts[t].size(), at[t], path); });
   };
   // points: "v %.17g %.17g %.17g"
   {
     const int64_t per = int64_t(kChunk / 24);
-    Pinned buf(size_t(per) * 24);
-    const double* hp = reinterpret_cast<const double*>(buf.p);
+    unsigned char* buf = c.stage(size_t(per) * 24);
+    const double* hp = reinterpret_cast<const double*>(buf);
     for (int64_t p0 = 0; p0 < n_points; p0 += per) {
       const int64_t cnt = std::min(per, n_points - p0);
-      CK(cudaMemcpyAsync(buf.p, d_points + 3 * p0, size_t(cnt) * 24, cudaMemcpyDeviceToHost, c.stream));
+      CK(cudaMemcpyAsync(buf, d_points + 3 * p0, size_t(cnt) * 24, cudaMemcpyDeviceToHost, c.stream));
       c.sync();
       parallel_format(cnt, [&](int64_t b, int64_t e, std::string& s) {
         char line[96];
@@ -336,14 +388,15 @@ void write_surface_obj(Ctx& c, const char* path, const double* d_points, int64_t
   {
     const int64_t per = int64_t(kChunk / 48);
     const int vp = verts_per_prim;
-    Pinned ibuf(size_t(per) * vp * 8), rbuf(size_t(per) * 16);
-    const int64_t* hi = reinterpret_cast<const int64_t*>(ibuf.p);
-    const int64_t* hr = reinterpret_cast<const int64_t*>(rbuf.p);
+    unsigned char* ibuf = c.stage(size_t(per) * vp * 8 + size_t(per) * 16);
+    unsigned char* rbuf = ibuf + size_t(per) * vp * 8;
+    const int64_t* hi = reinterpret_cast<const int64_t*>(ibuf);
+    const int64_t* hr = reinterpret_cast<const int64_t*>(rbuf);
     int64_t prev[2] = {-2, -2};  // region pair of the primitive before the chunk
     for (int64_t q0 = 0; q0 < n_prims; q0 += per) {
       const int64_t cnt = std::min(per, n_prims - q0);
-      CK(cudaMemcpyAsync(ibuf.p, d_indices + q0 * vp, size_t(cnt) * vp * 8, cudaMemcpyDeviceToHost, c.stream));
-      CK(cudaMemcpyAsync(rbuf.p, d_regions + 2 * q0, size_t(cnt) * 16, cudaMemcpyDeviceToHost, c.stream));
+      CK(cudaMemcpyAsync(ibuf, d_indices + q0 * vp, size_t(cnt) * vp * 8, cudaMemcpyDeviceToHost, c.stream));
+      CK(cudaMemcpyAsync(rbuf, d_regions + 2 * q0, size_t(cnt) * 16, cudaMemcpyDeviceToHost, c.stream));
       c.sync();
       const int64_t p0a = prev[0], p0b = prev[1];
       parallel_format(cnt, [&](int64_t b, int64_t e, std::string& s) {
