@@ -576,19 +576,30 @@ constexpr int kChase = 64;
 
 __global__ void __launch_bounds__(256) k_tt_jump(uint64_t nt, uint32_t* __restrict__ SD, uint32_t* __restrict__ SA,
                                                  int* __restrict__ changed) {
+  // two entries per thread (i, i + half): four independent chains in flight
+  const uint64_t half = (nt + 1) / 2;
   const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   bool ch = false;
-  if (i < nt) {
+  if (i < half) {
+    const uint64_t j = i + half;
+    const bool two = j < nt;
     const uint32_t d0 = SD[i], a0 = SA[i];
-    uint32_t xd = d0, xa = a0;
+    const uint32_t e0 = two ? SD[j] : kFinal, b0 = two ? SA[j] : kFinal;
+    uint32_t xd = d0, xa = a0, yd = e0, ya = b0;
 #pragma unroll 4
-    for (int k = 0; k < kChase && !(xd & xa & kFinal); ++k) {
+    for (int k = 0; k < kChase && !(xd & xa & yd & ya & kFinal); ++k) {
       if (!(xd & kFinal)) xd = SD[xd];
       if (!(xa & kFinal)) xa = SA[xa];
+      if (!(yd & kFinal)) yd = SD[yd];
+      if (!(ya & kFinal)) ya = SA[ya];
     }
     if (xd != d0) SD[i] = xd;
     if (xa != a0) SA[i] = xa;
-    ch = !(xd & xa & kFinal);
+    if (two) {
+      if (yd != e0) SD[j] = yd;
+      if (ya != b0) SA[j] = ya;
+    }
+    ch = !(xd & xa & yd & ya & kFinal);
   }
   if (__any_sync(0xffffffffu, ch) && (threadIdx.x & 31) == 0) *changed = 1;
 }
@@ -1715,7 +1726,7 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
     o.sweeps = 0;
     auto sweep = [&]() {
       CK(cudaMemsetAsync(jflag, 0, 4, c.stream));
-      k_tt_jump<<<blocks_for(int64_t(nt), 256), 256, 0, c.stream>>>(nt, SD, SA, jflag);
+      k_tt_jump<<<blocks_for(int64_t((nt + 1) / 2), 256), 256, 0, c.stream>>>(nt, SD, SA, jflag);
       CK_LAUNCH("k_tt_jump");
       ++o.sweeps;
     };
