@@ -295,6 +295,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--slab", action="store_true",
+                    help="run the z-slab (multi-GPU) path even at world size 1 (torchrun --nproc-per-node 1)")
     ap.add_argument("--cpu-sample", type=int, default=1 << 23, help="vertices in the CPU-baseline sample")
     ap.add_argument("--ref-sample", type=int, default=1 << 23, help="vertices per --impl reference step")
     args = ap.parse_args()
@@ -310,7 +312,7 @@ def main():
 
     torch.cuda.set_device(local)
     pg = None
-    if world > 1:
+    if world > 1 or args.slab:
         import torch.distributed as dist
 
         dist.init_process_group("nccl")
@@ -323,7 +325,7 @@ def main():
     field = P.synth_field(dims, kind=cfg.kind, gaussians=cfg.gaussians() if cfg.kind == "gaussians" else None,
                           noise_amp=cfg.noise, seed=cfg.seed, levels=cfg.levels, ctx=ctx)
     torch.cuda.synchronize()
-    if world > 1:
+    if world > 1 or args.slab:
         return run_multi(args, cfg, ctx, field, rank, world, local)
 
     for _ in range(max(args.warmup, 0)):

@@ -154,7 +154,12 @@ class Context:
             stream = torch.cuda.current_stream(device)
         self.stream = stream
         h = C.c_void_p()
-        _check(lib().plmss_b200_ctx_create(device, C.c_void_p(stream.cuda_stream), C.byref(h)))
+        # torch's default stream has handle 0, which the C-ABI reads as "make
+        # your own non-blocking stream": library kernels would then race with
+        # the torch ops that produce their inputs. Pass cudaStreamLegacy (0x1)
+        # instead so both sides share one ordered stream.
+        handle = stream.cuda_stream or 1
+        _check(lib().plmss_b200_ctx_create(device, C.c_void_p(handle), C.byref(h)))
         self.h = h
 
     def close(self):

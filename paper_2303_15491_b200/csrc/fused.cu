@@ -1592,10 +1592,14 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
   if (c.device >= 0 && c.device < 64 && !g_consts_ready[c.device]) {
     CK(cudaFuncSetAttribute(k_tile_segment<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kASmem));
     CK(cudaFuncSetAttribute(k_tile_segment<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kASmem));
-    CK(cudaMemcpyToSymbol(c_mrows, kTetRowsPacked, sizeof(kTetRowsPacked)));
-    CK(cudaMemcpyToSymbol(c_mcases, kTetCasePacked, sizeof(kTetCasePacked)));
+    // on the context stream (a non-blocking stream does not wait on the legacy one)
+    CK(cudaMemcpyToSymbolAsync(c_mrows, kTetRowsPacked, sizeof(kTetRowsPacked), 0, cudaMemcpyHostToDevice,
+                               c.stream));
+    CK(cudaMemcpyToSymbolAsync(c_mcases, kTetCasePacked, sizeof(kTetCasePacked), 0, cudaMemcpyHostToDevice,
+                               c.stream));
     k_march_init<<<1, 128, 0, c.stream>>>();
     CK_LAUNCH("k_march_init");
+    c.sync();  // other contexts (other streams) may use the tables next
     g_consts_ready[c.device] = true;
   }
   FDims d;

@@ -484,11 +484,15 @@ bool g_tables_ready[64] = {};
 
 void ensure_tables(Ctx& c) {
   if (c.device >= 0 && c.device < 64 && g_tables_ready[c.device]) return;
-  CK(cudaMemcpyToSymbol(c_rows, kTetRowsPacked, sizeof(kTetRowsPacked)));
-  CK(cudaMemcpyToSymbol(c_cases, kTetCasePacked, sizeof(kTetCasePacked)));
+  // Uploaded on the context stream and waited for: a plain cudaMemcpyToSymbol
+  // runs on the legacy stream, which a non-blocking context stream does not
+  // wait on (the first count kernel then saw half-written tables).
+  CK(cudaMemcpyToSymbolAsync(c_rows, kTetRowsPacked, sizeof(kTetRowsPacked), 0, cudaMemcpyHostToDevice, c.stream));
+  CK(cudaMemcpyToSymbolAsync(c_cases, kTetCasePacked, sizeof(kTetCasePacked), 0, cudaMemcpyHostToDevice, c.stream));
   const std::vector<FaceType> ft = build_face_types();
   if (ft.size() != 12) fail(PLMSS_ERR_LOGIC, "face type table must have 12 entries");
-  CK(cudaMemcpyToSymbol(c_faces, ft.data(), sizeof(FaceType) * 12));
+  CK(cudaMemcpyToSymbolAsync(c_faces, ft.data(), sizeof(FaceType) * 12, 0, cudaMemcpyHostToDevice, c.stream));
+  c.sync();
   if (c.device >= 0 && c.device < 64) g_tables_ready[c.device] = true;
 }
 

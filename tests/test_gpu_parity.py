@@ -351,3 +351,63 @@ def test_pipeline_long_forest_chains(plmss, gpu, restatement, spec):
     m = plmss.materialize_separators(dims, out["tris"], ctx=gpu)
     assert np.array_equal(m["source_cells"].cpu().numpy(), e["source_cells"])
     assert np.array_equal(m["regions"].cpu().numpy(), e["regions"])
+
+
+@pytest.mark.gpu
+def test_library_is_ordered_after_torch_default_stream(plmss, gpu):
+    """Inputs produced by torch ops on the default stream, then a library call
+    with no host sync in between (the z-slab path's pattern,
+    distributed.py): the context must run on the same stream as torch."""
+    import torch
+
+    from paper_2303_15491_b200 import api
+
+    dims = (192, 160, 128)
+    n = dims[0] * dims[1] * dims[2]
+    g = torch.Generator(device="cuda").manual_seed(7)
+    base = torch.randint(0, 1 << 20, (n,), device="cuda", generator=g)
+    torch.cuda.synchronize()
+    got = []
+    for _ in range(3):
+        lab = torch.sort(base)[0] // 4096  # slow enough to still run when the library starts
+        got.append(api.index_separators(dims, lab, ctx=gpu)[1])
+        del lab
+    torch.cuda.synchronize()
+    lab = torch.sort(base)[0] // 4096
+    torch.cuda.synchronize()
+    want = api.index_separators(dims, lab, ctx=gpu)[1]
+    assert want > 0 and got == [want] * 3
+    r = api.emit_separators(dims, torch.sort(base)[0] // 4096, ctx=gpu)
+    assert r.shape[0] == want
+
+
+@pytest.mark.gpu
+def test_slab_backend_single_rank_nccl_matches_pipeline(plmss, gpu):
+    """bench.py --slab path at world size 1 over NCCL: labels, ids and the
+    triangle total equal the fused pipeline's on a 96x80x64 Gaussian field."""
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2303_15491_b200.configs import CONFIGS, scaled
+    from paper_2303_15491_b200.distributed import B200Backend, ms_segmentation
+
+    cfg = scaled(CONFIGS["cfg2"], (96, 80, 64))
+    f = plmss.synth_field(cfg.dims, kind=cfg.kind, gaussians=cfg.gaussians(), noise_amp=cfg.noise, seed=cfg.seed,
+                          ctx=gpu)
+    res = plmss.pipeline(cfg.dims, f, ctx=gpu)
+    out = plmss.fetch(gpu, res)
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29547")
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        s = ms_segmentation(f, cfg.dims, B200Backend(gpu))
+        torch.cuda.synchronize()
+    finally:
+        dist.destroy_process_group()
+    u = lambda t: (t.to(torch.int64) & 0xFFFFFFFF).cpu()  # noqa: E731
+    assert torch.equal(s.desc.cpu(), u(out["desc"]))
+    assert torch.equal(s.asc.cpu(), u(out["asc"]))
+    assert torch.equal(s.ms.cpu(), u(out["ms"]))
+    assert s.tri_total == res.n_tris
