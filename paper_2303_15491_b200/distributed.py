@@ -80,6 +80,16 @@ class B200Backend:
                                                  a._ptr(asc), C.byref(sweeps)))
         return desc.to(torch.int64) & 0xFFFFFFFF, asc.to(torch.int64) & 0xFFFFFFFF
 
+    def local_regions(self, asc: torch.Tensor, desc: torch.Tensor, N: int):
+        """combine_ms on this slab's (global-id) labels: local dense ids and
+        the sorted distinct keys asc * N + desc they index."""
+        a = self.api
+        seg = a.SegmentationResult(desc=desc.to(torch.int32), asc=asc.to(torch.int32))
+        a.combine_ms(seg, ctx=self.ctx)
+        k = seg.region_keys
+        uniq = (k >> 32) * N + (k & 0xFFFFFFFF)
+        return seg.ms_region.to(torch.int64) & 0xFFFFFFFF, uniq
+
     def march_slab(self, dims, ms_ext: torch.Tensor):
         recs = self.api.emit_separators(dims, ms_ext.contiguous(), ctx=self.ctx)
         return recs[:, 0] >> 6, recs[:, 1], recs[:, 2]
@@ -189,10 +199,14 @@ def ms_segmentation(field_owned: torch.Tensor, dims, backend, group=None) -> Sla
     minima = torch.cat(_all_gather_var(ids[asc == ids], group))
 
     # 5. Morse-Smale ids: lexicographic (asc, desc) == key asc * N + desc
-    key = asc * N + desc
-    uniq = torch.unique(key)
+    local_regions = getattr(backend, "local_regions", None)
+    if local_regions is not None:  # dense local ids from the device hash (no sort of the slab)
+        local, uniq = local_regions(asc, desc, N)
+    else:
+        key = asc * N + desc
+        uniq, local = torch.unique(key, return_inverse=True)
     gkeys = torch.unique(torch.cat(_all_gather_var(uniq, group)))
-    ms = torch.searchsorted(gkeys, key)
+    ms = torch.searchsorted(gkeys, uniq)[local]
     region_keys = torch.stack([gkeys // N, gkeys % N], dim=1)
 
     # 6. marching: owned cube layers need the next rank's first layer of ids
