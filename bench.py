@@ -119,28 +119,43 @@ def dist_setup():
     return rank, world, local
 
 
-def cpu_sample(cfg, field_host_fn, target_vertices):
-    """A bounded sample of the workload: the first k z-layers of the field."""
-    X, Y, Z = cfg.dims
-    k = max(2, min(Z, target_vertices // (X * Y)))
-    return (X, Y, k), field_host_fn(k)
+def load_configs():
+    """paper_2303_15491_b200/configs.py loaded by path: the reference arm must
+    not import (and so not load the native library of) the B200 package."""
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location("plmss_bench_configs",
+                                                  os.path.join(ROOT, "paper_2303_15491_b200", "configs.py"))
+    mod = importlib.util.module_from_spec(spec)
+    sys.modules[spec.name] = mod  # dataclasses resolve the module by name
+    spec.loader.exec_module(mod)
+    return mod
 
 
 def run_reference_arm(args, rank, world):
-    import oracle
-    from paper_2303_15491_b200.configs import CONFIGS
-
+    """The reference's own CPU implementation (oracle/_ref: proj/src compiled
+    unchanged) on all host cores, one bounded z-slab sample of the configured
+    field per step (run_benchmark's MorseSmale pass, proj/src/bench.cpp:62-87).
+    The sample is generated on the host by the oracle's C loop of the input
+    definition (include/plmss_synth.h) — no B200 code in this process."""
     if rank != 0:
         return 0
-    cfg = CONFIGS[args.config]
+    import oracle
+
+    cfg = load_configs().CONFIGS[args.config]
     ref = oracle.Reference()
     cores = os.cpu_count() or 1
-    dims, f = reference_sample(cfg, args.ref_sample)
-    nv = int(np.prod(dims))
+    X, Y, Z = cfg.dims
+    k = max(2, min(Z, args.ref_layers))
+    dims = (X, Y, k)
+    f = oracle.Restatement().synth(cfg, z0=0, nz=k) if cfg.levels == 0 else \
+        oracle.Restatement().synth(cfg)[: X * Y * k]
+    nv = X * Y * k
     for _ in range(args.warmup):
         ref.run_once(dims, f, cores)
     times = []
     phases_acc = np.zeros(5)
+    regions = prims = 0
     for _ in range(args.steps):
         t0 = time.perf_counter()
         ph, regions, prims = ref.run_once(dims, f, cores)
@@ -148,12 +163,12 @@ def run_reference_arm(args, rank, world):
         phases_acc += np.array(list(ph.values()))
     t = float(np.mean(times))
     value = nv / t / 1e9
-    sample = (f"z-slab {dims[0]}x{dims[1]}x{dims[2]} ({nv} vertices) of {cfg.name}; reference run_benchmark pass "
-              f"(compute_order+segment+combine_ms+index+geometry, MorseSmale) per step")
+    sample = (f"z-slab {X}x{Y}x{k} ({nv} vertices, the first {k} of {Z} layers) of {cfg.name}; reference "
+              f"run_benchmark pass (compute_order+segment+combine_ms+index+geometry, MorseSmale) per step")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64/int64", "data": "synthetic",
+        "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak" if world > 1
+        else "strong", "vs_baseline": None, "dtype": "f64/int64", "data": "synthetic",
         "config": {"workload": cfg.name, "dims": list(cfg.dims), "sample_dims": list(dims)},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -163,30 +178,6 @@ def run_reference_arm(args, rank, world):
     }
     print(json.dumps(line), flush=True)
     return 0
-
-
-def reference_sample(cfg, target):
-    """Host copy of the first k z-layers of the configured field (generated on
-    the GPU when one is present, else on the host at the sample size)."""
-    from paper_2303_15491_b200.configs import Config, host_field
-
-    X, Y, Z = cfg.dims
-    k = max(2, min(Z, target // (X * Y)))
-    dims = (X, Y, k)
-    try:
-        import torch
-
-        if torch.cuda.is_available():
-            import paper_2303_15491_b200 as P
-
-            f = P.synth_field(cfg.dims if k == Z else dims, kind=cfg.kind, gaussians=cfg.gaussians()
-                              if cfg.kind == "gaussians" else None, noise_amp=cfg.noise, seed=cfg.seed,
-                              levels=cfg.levels)
-            return dims, f[: X * Y * k].cpu().numpy()
-    except Exception:
-        pass
-    sub = Config(cfg.name, dims, cfg.kind, cfg.n_gauss, cfg.sigma, cfg.noise, cfg.levels, cfg.seed)
-    return dims, host_field(sub)
 
 
 def run_multi(args, cfg, ctx, field, rank, world, local):
@@ -297,8 +288,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--slab", action="store_true",
                     help="run the z-slab (multi-GPU) path even at world size 1 (torchrun --nproc-per-node 1)")
-    ap.add_argument("--cpu-sample", type=int, default=1 << 23, help="vertices in the CPU-baseline sample")
-    ap.add_argument("--ref-sample", type=int, default=1 << 23, help="vertices per --impl reference step")
+    ap.add_argument("--ref-layers", type=int, default=64,
+                    help="z-layers of the configured field in the CPU sample (reference arm and cpu_baseline)")
     args = ap.parse_args()
     rank, world, local = dist_setup()
 

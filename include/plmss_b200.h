@@ -286,13 +286,18 @@ int plmss_b200_pipeline_host(plmss_ctx* ctx, const int64_t dims[3], const float*
                              plmss_tri* h_tris, int64_t tri_capacity, plmss_result* out);
 
 /* ---- synthetic inputs (benchmark/test harness utility) -------------------
- * value(x,y,z) = sum_k amp_k * exp(-|p - c_k|^2 / (2 sigma_k^2)) + noise_amp *
- * u(seed, v), u uniform in [-1, 1) from a splitmix64 hash of (seed, v);
- * kind 1 = i.i.d. uniform [0, 1) from the same hash (no Gaussians);
- * levels > 0 quantises to that many levels over [min, max].
- * gaussians: n_gauss x 5 doubles (cx, cy, cz, sigma, amp). */
+ * The input definition of include/plmss_synth.h (bit-identical to its host
+ * loop): value(x,y,z) = sum_k amp_k * ex_k(x) * ey_k(y) * ez_k(z) (separable
+ * Gaussians, float32 axis tables) + noise_amp * (2u - 1), u uniform in [0, 1)
+ * from a splitmix64 hash of (seed, v); kind 1 = i.i.d. uniform [0, 1) from
+ * the same hash (no Gaussians); levels > 0 quantises to that many levels over
+ * [min, max]. gaussians: n_gauss x 5 doubles (cx, cy, cz, sigma, amp). */
 int plmss_b200_synth(plmss_ctx* ctx, const int64_t dims[3], int kind, const double* h_gaussians,
                      int n_gauss, double noise_amp, uint64_t seed, int levels, float* d_field);
+/* Vertex layers [z0, z0 + nz) of the same field (no quantisation) into
+ * d_field (X * Y * nz floats): a rank's slab plus halo layers. */
+int plmss_b200_synth_layers(plmss_ctx* ctx, const int64_t dims[3], int kind, const double* h_gaussians,
+                            int n_gauss, double noise_amp, uint64_t seed, int64_t z0, int64_t nz, float* d_field);
 
 #ifdef __cplusplus
 }

@@ -29,6 +29,8 @@ REF_SO = os.path.join(HERE, "_ref", "libplmss_ref.so")
 REF_SRC = "/root/reference/proj"
 
 _i64p = np.ctypeslib.ndpointer(np.int64, flags="C_CONTIGUOUS")
+# one separator triangle record (plmss_tri of include/plmss_b200.h / orc_tri)
+TRI_DTYPE = np.dtype([("cellrow", "<u8"), ("lo", "<u4"), ("hi", "<u4")])
 _f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
 _u8p = np.ctypeslib.ndpointer(np.uint8, flags="C_CONTIGUOUS")
 
@@ -84,6 +86,71 @@ class Restatement:
         L.orc_emit_geometry.argtypes = [_i64p, _f64p, _f64p, _i64p, _u8p, _f64p, _i64p, _i64p]
         L.orc_emit_boundaries.restype = None
         L.orc_emit_boundaries.argtypes = [_i64p, _f64p, _f64p, _i64p, C.c_int, C.c_int64, _i64p] + [C.c_void_p] * 5
+
+        f32p = np.ctypeslib.ndpointer(np.float32, flags="C_CONTIGUOUS")
+        u32p = np.ctypeslib.ndpointer(np.uint32, flags="C_CONTIGUOUS")
+        L.orc_synth.restype = C.c_int
+        L.orc_synth.argtypes = [_i64p, C.c_int, C.c_void_p, C.c_int, C.c_double, C.c_uint64, C.c_int, C.c_int64,
+                                C.c_int64, f32p]
+        L.orc_seed_hops_f32.restype = C.c_int64
+        L.orc_seed_hops_f32.argtypes = [_i64p, f32p, u32p, u32p]
+        L.orc_compress_u32.restype = C.c_int
+        L.orc_compress_u32.argtypes = [C.c_int64, u32p, u32p]
+        L.orc_extrema_u32.restype = C.c_int64
+        L.orc_extrema_u32.argtypes = [C.c_int64, u32p, C.c_void_p]
+        L.orc_combine_ms_u32.restype = C.c_int64
+        L.orc_combine_ms_u32.argtypes = [C.c_int64, u32p, u32p, u32p, C.c_void_p, C.c_int64]
+        L.orc_separator_records.restype = C.c_int64
+        L.orc_separator_records.argtypes = [_i64p, u32p, C.c_int64, C.c_int64, C.c_void_p]
+
+    # -- full-size grids (plmss_oracle_big.c) ----------------------------------
+    def synth(self, cfg, z0=0, nz=None):
+        """The BASELINE config's field (include/plmss_synth.h), layers [z0, z0+nz)."""
+        d = _dims(cfg.dims)
+        nz = int(d[2]) if nz is None else int(nz)
+        out = np.empty(int(d[0]) * int(d[1]) * nz, np.float32)
+        g = np.ascontiguousarray(cfg.gaussians() if cfg.kind == "gaussians" else np.zeros((0, 5)), np.float64)
+        st = self.lib.orc_synth(d, 0 if cfg.kind == "gaussians" else 1, g.ctypes.data, g.shape[0], cfg.noise,
+                                cfg.seed, cfg.levels, z0, nz, out)
+        if st != 0:
+            raise ValueError("orc_synth: bad layer range")
+        return out
+
+    def segment_u32(self, dims, f32):
+        """seed_hops_both + compression on float32 values, uint32 labels."""
+        d = _dims(dims)
+        f = np.ascontiguousarray(f32, dtype=np.float32).ravel()
+        desc = np.empty(f.size, np.uint32)
+        asc = np.empty(f.size, np.uint32)
+        bad = self.lib.orc_seed_hops_f32(d, f, desc, asc)
+        if bad >= 0:
+            raise ValueError(f"non-finite scalar value at vertex {bad}")
+        sweeps = self.lib.orc_compress_u32(f.size, desc, asc)
+        return dict(desc=desc, asc=asc, maxima=self.extrema_u32(desc), minima=self.extrema_u32(asc), sweeps=sweeps)
+
+    def extrema_u32(self, labels):
+        k = self.lib.orc_extrema_u32(labels.size, labels, None)
+        out = np.empty(max(k, 1), np.uint32)
+        self.lib.orc_extrema_u32(labels.size, labels, out.ctypes.data)
+        return out[:k]
+
+    def combine_ms_u32(self, asc, desc):
+        """(ms uint32, sorted region keys uint64 = asc << 32 | desc)."""
+        ms = np.empty(asc.size, np.uint32)
+        r = self.lib.orc_combine_ms_u32(asc.size, asc, desc, ms, None, 0)
+        keys = np.empty(max(r, 1), np.uint64)
+        self.lib.orc_combine_ms_u32(asc.size, asc, desc, ms, keys.ctypes.data, r)
+        return ms, keys[:r]
+
+    def separator_records(self, dims, labels_u32, cz0, cz1):
+        """(cell << 6 | row, lo, hi) records of cube layers [cz0, cz1),
+        structured array of TRI_DTYPE, reference emission order."""
+        d = _dims(dims)
+        lab = np.ascontiguousarray(labels_u32, dtype=np.uint32).ravel()
+        k = self.lib.orc_separator_records(d, lab, cz0, cz1, None)
+        out = np.empty(max(k, 1), TRI_DTYPE)
+        self.lib.orc_separator_records(d, lab, cz0, cz1, out.ctypes.data)
+        return out[:k]
 
     # -- order / segmentation -------------------------------------------------
     def compute_order(self, values):
@@ -247,6 +314,13 @@ class Reference:
         L.cap_run_benchmark.argtypes = [_i64p, _f64p, C.c_int, C.c_int, C.c_int, _f64p]
         L.cap_run_once.argtypes = [_i64p, np.ctypeslib.ndpointer(np.float32, flags="C_CONTIGUOUS"), C.c_int,
                                    C.c_int, _f64p, _i64p]
+        if hasattr(L, "cap_records_chunk"):
+            L.cap_records_chunk.argtypes = [_i64p, _i64p, C.c_int64, C.c_int64, C.c_int, C.POINTER(C.c_void_p),
+                                            C.POINTER(C.c_int64)]
+            L.cap_records_copy.argtypes = [C.c_void_p, C.c_void_p]
+            L.cap_records_copy.restype = None
+            L.cap_records_free.argtypes = [C.c_void_p]
+            L.cap_records_free.restype = None
         if hasattr(L, "cap_weld"):
             L.cap_weld.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.POINTER(C.c_int64)]
             L.cap_read_volume.argtypes = [C.c_char_p, _i64p, C.c_char_p, C.c_void_p]
@@ -281,6 +355,23 @@ class Reference:
         r = np.ascontiguousarray(regions, dtype=np.int64).reshape(-1, 2)
         self._check(self.lib.cap_write_obj(os.fsencode(str(path)), p.ctypes.data, p.shape[0], i.ctypes.data,
                                            r.ctypes.data, r.shape[0], verts_per_prim))
+
+    def records_chunk(self, dims, labels_slab, cz0, cz1, workers=1):
+        """Reference separator records (TRI_DTYPE) of cube layers [cz0, cz1)
+        of a (X, Y, Z) grid; labels_slab = int64 labels of vertex layers
+        [cz0, cz1] (ref_capi.cpp cap_records_chunk)."""
+        d = _dims(dims)
+        lab = np.ascontiguousarray(labels_slab, dtype=np.int64).ravel()
+        assert lab.size == int(d[0]) * int(d[1]) * (cz1 - cz0 + 1)
+        k = C.c_int64()
+        h = C.c_void_p()
+        self._check(self.lib.cap_records_chunk(d, lab, cz0, cz1, workers, C.byref(h), C.byref(k)))
+        try:
+            out = np.empty(max(k.value, 1), TRI_DTYPE)
+            self.lib.cap_records_copy(h, out.ctypes.data)
+        finally:
+            self.lib.cap_records_free(h)
+        return out[: k.value]
 
     def run_once(self, dims, values_f32, workers, mode=2):
         """One reference pipeline pass (bench.cpp:62-87); returns (phase

@@ -68,6 +68,26 @@ void orc_emit_boundaries(const int64_t dims[3], const double spacing[3], const d
                          int64_t* faces_out, int64_t* tags, int64_t* cells, double* points,
                          int64_t* indices);
 
+/* ---- full-size grids (plmss_oracle_big.c): uint32 ids, float32 values,
+ * OpenMP workers. ---- */
+
+/* One separator triangle: (global cell << 6 | recipe row), region pair. */
+typedef struct {
+  uint64_t cellrow;
+  uint32_t lo, hi;
+} orc_tri;
+
+/* The input definition of include/plmss_synth.h, vertex layers [z0, z0+nz). */
+int orc_synth(const int64_t dims[3], int kind, const double* gauss, int ng, double noise, uint64_t seed,
+              int levels, int64_t z0, int64_t nz, float* out);
+int64_t orc_seed_hops_f32(const int64_t dims[3], const float* f, uint32_t* desc, uint32_t* asc);
+int orc_compress_u32(int64_t n, uint32_t* desc, uint32_t* asc);
+int64_t orc_extrema_u32(int64_t n, const uint32_t* labels, uint32_t* out);
+int64_t orc_combine_ms_u32(int64_t n, const uint32_t* asc, const uint32_t* desc, uint32_t* ms, uint64_t* keys_out,
+                           int64_t keys_cap);
+int64_t orc_separator_records(const int64_t dims[3], const uint32_t* labels, int64_t cz0, int64_t cz1,
+                              orc_tri* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -14,6 +14,8 @@
 // proj/include/plmss/{orderfield,segmentation,marching,bench}.hpp and converts
 // C++ exceptions into (status, message): 1 invalid_argument, 2 logic_error,
 // 3 out_of_range, 4 other, 6 io FormatError, 7 io IoError.
+#include <array>
+#include <algorithm>
 #include <chrono>
 #include <cstdint>
 #include <cstring>
@@ -372,5 +374,85 @@ int cap_write_obj(const char* path, const double* points, int64_t n_points, cons
     plmss::write_surface_obj(mesh, path);
   });
 }
+
+// Separator records of cube layers [cz0, cz1) of a (X, Y, Z) grid from the
+// reference itself: emit_separators (marching.cpp:208-215) on the z-chunk
+// grid implicit_grid({X, Y, cz1 - cz0 + 1}, spacing 1, origin (0, 0, cz0))
+// over the label slice of vertex layers [cz0, cz1], each
+// triangle converted to the 16-byte record (global cell << 6 | recipe row,
+// lo, hi). The recipe row of the k-th triangle of cell c is
+// tetra_case(code(c))[k] (marching.cpp:160-195 emits a cell's rows in table
+// order); the row is CHECKED by recomputing its three corner points (mean of
+// the masked tet vertex positions, ascending corner order) and its region
+// pair against the reference's own output, bit for bit. out == nullptr:
+// count only. *count = records.
+struct RecordsOut {
+  struct Rec {
+    uint64_t cellrow;
+    uint32_t lo, hi;
+  };
+  std::vector<Rec> rec;
+};
+
+int cap_records_chunk(const int64_t* dims, const int64_t* labels, int64_t cz0, int64_t cz1, int workers,
+                      void** handle, int64_t* count) {
+  return guarded([&] {
+    const int64_t X = dims[0], Y = dims[1];
+    const int64_t nzv = cz1 - cz0 + 1;
+    const int64_t cdims[3] = {X, Y, nzv};
+    const double og[3] = {0.0, 0.0, double(cz0)};
+    const auto grid = make_grid(cdims, nullptr, og);
+    std::span<const plmss::Label> lab(labels, static_cast<size_t>(X * Y * nzv));
+    const plmss::SeparatingMesh mesh = plmss::emit_separators(grid, lab, workers);
+    const int64_t np = mesh.num_primitives();
+    auto* res = new RecordsOut();
+    *handle = res;
+    *count = np;
+    res->rec.resize(size_t(np));
+    // kTetraData row offsets (the GPU table numbering, marching_tables.cpp:48-116)
+    const auto* data0 = plmss::tables::tetra_case(3).data();
+    RecordsOut::Rec* rec = res->rec.data();
+    const int64_t cell_base = 6 * (X - 1) * (Y - 1) * cz0;
+    int64_t prev_cell = -1, k = 0;
+    for (int64_t j = 0; j < np; ++j) {
+      const int64_t c = mesh.source_cells[j];
+      k = c == prev_cell ? k + 1 : 0;
+      prev_cell = c;
+      const auto verts = grid.cell(c);
+      std::array<plmss::Label, 4> l{};
+      for (int i = 0; i < 4; ++i) l[i] = labels[verts[i]];
+      const auto code = plmss::tetra_code(l).code;
+      const auto rows = plmss::tables::tetra_case(code);
+      if (k >= int64_t(rows.size())) throw std::logic_error("cap_records_chunk: row count");
+      const auto& row = rows[k];
+      for (int q = 0; q < 3; ++q) {
+        Eigen::Vector3d sum = Eigen::Vector3d::Zero();
+        int cnt = 0;
+        for (int i = 0; i < 4; ++i)
+          if (row.p[q] & (1 << i)) {
+            sum += grid.position(verts[i]);
+            ++cnt;
+          }
+        const Eigen::Vector3d pt = sum / double(cnt);
+        for (int a = 0; a < 3; ++a)
+          if (pt[a] != mesh.points(a, mesh.indices[3 * j + q]))
+            throw std::logic_error("cap_records_chunk: recipe point mismatch at triangle " + std::to_string(j));
+      }
+      const plmss::Label la = l[row.pairA], lb = l[row.pairB];
+      if (mesh.regions[j][0] != std::min(la, lb) || mesh.regions[j][1] != std::max(la, lb))
+        throw std::logic_error("cap_records_chunk: region pair mismatch");
+      rec[j].cellrow = (uint64_t(cell_base + c) << 6) | uint64_t(&row - data0);
+      rec[j].lo = uint32_t(mesh.regions[j][0]);
+      rec[j].hi = uint32_t(mesh.regions[j][1]);
+    }
+  });
+}
+
+void cap_records_copy(void* handle, void* out) {
+  auto* r = static_cast<RecordsOut*>(handle);
+  if (!r->rec.empty()) std::memcpy(out, r->rec.data(), r->rec.size() * sizeof(RecordsOut::Rec));
+}
+
+void cap_records_free(void* handle) { delete static_cast<RecordsOut*>(handle); }
 
 }  // extern "C"

@@ -20,7 +20,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 SOURCES = ["capi.cu", "segment.cu", "combine.cu", "marching.cu", "scan.cu", "synth.cu", "fused.cu", "io.cu"]
 NVCC_FLAGS = ARCH + [
-    "-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr",
+    "-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O2,-ffp-contract=off", "--expt-relaxed-constexpr",
     "-I" + INCLUDE, "-I" + CSRC,
 ]
 

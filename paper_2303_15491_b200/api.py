@@ -46,7 +46,7 @@ HEADER_FUNCTIONS = [
     "plmss_b200_result", "plmss_b200_copy", "plmss_b200_ctx_set_option", "plmss_b200_pipeline_host",
     "plmss_b200_synth", "plmss_b200_launch_count", "plmss_b200_ctx_stats", "plmss_b200_count_by_cell_ranges",
     "plmss_b200_compress_sweep", "plmss_b200_segment_slab", "plmss_b200_weld_points", "plmss_b200_read_volume",
-    "plmss_b200_write_labels", "plmss_b200_write_surface_obj",
+    "plmss_b200_write_labels", "plmss_b200_write_surface_obj", "plmss_b200_synth_layers",
 ]
 
 
@@ -97,6 +97,7 @@ def lib() -> C.CDLL:
         L.plmss_b200_copy.argtypes = [vp, vp, vp, i64, i32]
         L.plmss_b200_pipeline_host.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i64, C.POINTER(PlmssResult)]
         L.plmss_b200_synth.argtypes = [vp, vp, i32, vp, i32, C.c_double, C.c_uint64, i32, vp]
+        L.plmss_b200_synth_layers.argtypes = [vp, vp, i32, vp, i32, C.c_double, C.c_uint64, i64, i64, vp]
         L.plmss_b200_weld_points.argtypes = [vp, vp, i64, vp, i64, C.POINTER(i64)]
         L.plmss_b200_read_volume.argtypes = [vp, C.c_char_p, vp, i32, i32, vp]
         L.plmss_b200_write_labels.argtypes = [vp, C.c_char_p, i32, vp, vp, i64]
@@ -489,6 +490,33 @@ def fetch(ctx: Context, res: PipelineResult, names=("desc", "asc", "ms", "maxima
     return out
 
 
+def result_digests(ctx: Context, res: PipelineResult, names=("desc", "asc", "ms", "maxima", "minima",
+                                                               "region_keys", "tris"), piece_bytes: int = 1 << 30):
+    """Chunked SHA-256 (digest.py) of pipeline outputs in the context, read
+    back to the host in pieces (the full-size parity tests: cfg3's records
+    alone are 86 GB, more than a second device copy would leave room for)."""
+    from .digest import BLOCK, ChunkedSha256
+
+    r = res.raw
+    spec = {"desc": (r.d_desc, 4 * r.n_vertices), "asc": (r.d_asc, 4 * r.n_vertices),
+            "ms": (r.d_ms, 4 * r.n_vertices), "maxima": (r.d_maxima, 4 * r.n_maxima),
+            "minima": (r.d_minima, 4 * r.n_minima), "region_keys": (r.d_region_keys, 8 * r.n_regions),
+            "tris": (r.d_tris, 16 * r.n_tris)}
+    out = {}
+    for name in names:
+        ptr, nbytes = spec[name]
+        h = ChunkedSha256()
+        for off in range(0, nbytes, piece_bytes):
+            k = min(piece_bytes, nbytes - off)
+            buf = np.empty(k, np.uint8)
+            _check(lib().plmss_b200_copy(ctx.h, buf.ctypes.data, C.c_void_p(ptr + off), k, 1))
+            h.update(buf)
+            for f in h._futs[:-4 * max(piece_bytes // BLOCK, 1)]:  # bound host memory
+                f.result()
+        out[name] = h.hexdigest()
+    return out
+
+
 def pipeline_host(dims, h_field: np.ndarray, ctx: Optional[Context] = None, want=("desc", "asc", "ms", "maxima",
                                                                                   "minima", "region_keys", "tris"),
                   out_buffers: Optional[dict] = None):
@@ -544,6 +572,21 @@ def synth_field(dims, kind: str = "gaussians", gaussians=None, noise_amp: float 
     k = {"gaussians": 0, "uniform": 1}[kind]
     _check(lib().plmss_b200_synth(ctx.h, d.ctypes.data, k, g.ctypes.data, g.shape[0], noise_amp, seed, levels,
                                   _ptr(f)))
+    return f
+
+
+def synth_layers(dims, z0: int, nz: int, kind: str = "gaussians", gaussians=None, noise_amp: float = 0.0,
+                 seed: int = 0, ctx: Optional[Context] = None):
+    """Vertex layers [z0, z0 + nz) of the synth_field volume (a rank's slab
+    plus its halo layers; no quantisation)."""
+    torch = _torch()
+    ctx = ctx or default_context()
+    d = _dims(dims)
+    f = torch.empty(int(d[0]) * int(d[1]) * int(nz), dtype=torch.float32, device=f"cuda:{ctx.device}")
+    g = np.ascontiguousarray(np.zeros((0, 5)) if gaussians is None else gaussians, dtype=np.float64)
+    k = {"gaussians": 0, "uniform": 1}[kind]
+    _check(lib().plmss_b200_synth_layers(ctx.h, d.ctypes.data, k, g.ctypes.data, g.shape[0], noise_amp, seed,
+                                         int(z0), int(nz), _ptr(f)))
     return f
 
 

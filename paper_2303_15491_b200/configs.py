@@ -5,9 +5,10 @@ PAPER.md:1118,1123) that are not available here; BASELINE.json names seeded
 synthetic stand-ins with the same sizes. Parameters are drawn with the
 reference's RNG convention, std::mt19937_64 and u = (rng() >> 11) * 2^-53
 (proj/src/synth.cpp:15-17), in the order (cx, cy, cz, sigma, amp) per
-Gaussian. Per-voxel noise uses a counter-based splitmix64 hash of
-(seed, vertex id) so the 2^30-voxel field can be produced on the device
-(csrc/synth.cu); the generated bytes are shared with the CPU oracle.
+Gaussian. The field itself is include/plmss_synth.h: separable Gaussians
+from float32 axis tables, per-voxel noise from a counter-based splitmix64
+hash of (seed, vertex id); the device (csrc/synth.cu), the oracle's C loop
+and host_field() below produce identical bytes.
 """
 from __future__ import annotations
 
@@ -107,10 +108,37 @@ def splitmix64_np(x: np.ndarray) -> np.ndarray:
     return x ^ (x >> np.uint64(31))
 
 
+_INV_FACT = [1.0 / 479001600.0, 1.0 / 39916800.0, 1.0 / 3628800.0, 1.0 / 362880.0, 1.0 / 40320.0, 1.0 / 5040.0,
+             1.0 / 720.0, 1.0 / 120.0, 1.0 / 24.0, 1.0 / 6.0, 1.0 / 2.0, 1.0, 1.0]
+
+
+def synth_exp_np(x: np.ndarray) -> np.ndarray:
+    """plmss_synth_exp (include/plmss_synth.h) elementwise, same IEEE ops."""
+    x = np.minimum(np.asarray(x, np.float64), 0.0)
+    t = x * 1.4426950408889634
+    n = np.trunc(t - 0.5)
+    r = (x - n * 6.93147180369123816490e-01) - n * 1.90821492927058770002e-10
+    p = np.full_like(r, 1.0 / 6227020800.0)
+    for c in _INV_FACT:
+        p = p * r + c
+    n = n.astype(np.int64)
+    sub = n < -1022
+    p = np.where(sub, p * 2.0 ** -600, p)
+    e = np.where(sub, n + 600, n)
+    out = p * np.ldexp(1.0, e)
+    return np.where(x < -740.0, 0.0, out)
+
+
+def axis_table_np(c: float, sigma: float, length: int) -> np.ndarray:
+    d = np.arange(length, dtype=np.float64) - c
+    return synth_exp_np(-(d * d) / (2.0 * sigma * sigma)).astype(np.float32)
+
+
 def host_field(cfg: Config) -> np.ndarray:
-    """CPU generator of the same distribution (float64 accumulation, so the
-    bytes may differ from the device generator in the last ulp; it is used
-    only where the field is generated on the host and shared from there)."""
+    """The input definition of include/plmss_synth.h in numpy — the same
+    bytes as the device generator (csrc/synth.cu) and the oracle's C loop:
+    float32 separable Gaussian sums (every product / sum rounded), double
+    noise, optional quantisation. Practical up to ~256^3 on the host."""
     X, Y, Z = cfg.dims
     v = np.arange(cfg.n, dtype=np.uint64)
     with np.errstate(over="ignore"):
@@ -118,12 +146,12 @@ def host_field(cfg: Config) -> np.ndarray:
             np.float64) * 2.0 ** -53
     if cfg.kind == "uniform":
         return u.astype(np.float32)
-    z, y, x = np.meshgrid(np.arange(Z, dtype=np.float64), np.arange(Y, dtype=np.float64),
-                          np.arange(X, dtype=np.float64), indexing="ij")
-    s = np.zeros((Z, Y, X), np.float64)
+    s = np.zeros((Z, Y, X), np.float32)
     for cx, cy, cz, sig, amp in cfg.gaussians():
-        s += amp * np.exp(-((x - cx) ** 2 + (y - cy) ** 2 + (z - cz) ** 2) / (2 * sig * sig))
-    f = (s.reshape(-1) + cfg.noise * (2.0 * u - 1.0)).astype(np.float32)
+        ex, ey, ez = axis_table_np(cx, sig, X), axis_table_np(cy, sig, Y), axis_table_np(cz, sig, Z)
+        w = np.float32(amp) * (ey[None, :] * ez[:, None])  # (Z, Y), float32 products
+        s = s + ex[None, None, :] * w[:, :, None]
+    f = (s.reshape(-1).astype(np.float64) + cfg.noise * (2.0 * u - 1.0)).astype(np.float32)
     if cfg.levels:
         lo, hi = float(f.min()), float(f.max())
         t = (f.astype(np.float64) - lo) / (hi - lo) if hi > lo else np.zeros_like(f, dtype=np.float64)

@@ -501,7 +501,17 @@ int plmss_b200_synth(plmss_ctx* p, const int64_t dims[3], int kind, const double
     Ctx& c = C(p);
     set_device(c);
     const Grid g = make_grid(dims);
-    synth(c, g, kind, h_gaussians, n_gauss, noise_amp, seed, levels, d_field);
+    synth(c, g, kind, h_gaussians, n_gauss, noise_amp, seed, levels, d_field, 0, g.Z);
+  });
+}
+
+int plmss_b200_synth_layers(plmss_ctx* p, const int64_t dims[3], int kind, const double* h_gaussians, int n_gauss,
+                            double noise_amp, uint64_t seed, int64_t z0, int64_t nz, float* d_field) {
+  return guarded([&] {
+    Ctx& c = C(p);
+    set_device(c);
+    const Grid g = make_grid(dims);
+    synth(c, g, kind, h_gaussians, n_gauss, noise_amp, seed, 0, d_field, z0, nz);
   });
 }
 

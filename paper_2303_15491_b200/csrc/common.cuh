@@ -213,6 +213,6 @@ void write_labels(Ctx& c, const char* path, int label_type, const void* d_asc, c
 void write_surface_obj(Ctx& c, const char* path, const double* d_points, int64_t n_points, const int64_t* d_indices,
                        const int64_t* d_regions, int64_t n_prims, int verts_per_prim);
 void synth(Ctx& c, const Grid& g, int kind, const double* h_gauss, int n_gauss, double noise_amp,
-           uint64_t seed, int levels, float* field);
+           uint64_t seed, int levels, float* field, int64_t z0, int64_t nz);
 
 }  // namespace plmss_b200

@@ -28,6 +28,8 @@
 #include <math.h>
 
 #include <algorithm>
+#include <atomic>
+#include <mutex>
 #include <type_traits>
 
 #include <cuda.h>
@@ -922,13 +924,24 @@ __global__ void __launch_bounds__(32 * kTokRows) k_tokens(const BrickArgs a) {
 #pragma unroll
     for (int i = 0; i < kTokZ; ++i) {
       if (z0 + i < nz) {
-        ld[i] = __ldg(fd + ld[i]) & ~kFinal;  // rank of the maximum
-        la[i] = __ldg(fa + la[i]) & ~kFinal;  // rank of the minimum
+        ld[i] = __ldg(fd + ld[i]);  // rank of the maximum | kFinal
+        la[i] = __ldg(fa + la[i]);  // rank of the minimum | kFinal
       }
     }
 #pragma unroll
     for (int i = 0; i < kTokZ; ++i) {
       if (z0 + i >= nz) break;
+      // An entry the speculative forest sweep left unresolved holds a table
+      // index, not a rank: no set insert and no extremum gather for it (the
+      // pass is redone after the forest converges).
+      if (!(ld[i] & la[i] & kFinal)) {
+        a.desc[gv] = a.asc[gv] = a.ms[gv] = 0u;
+        lkey = Key(~Key(0));
+        gv += d.XY;
+        continue;
+      }
+      ld[i] &= ~kFinal;
+      la[i] &= ~kFinal;
       const Key key = kDense ? Key(la[i] * a.nmax + ld[i]) : Key((uint64_t(la[i]) << 32) | ld[i]);
       if (key != lkey) {
         if (kDense) {
@@ -1008,13 +1021,24 @@ __device__ __forceinline__ void tokens_tma_body(const CUtensorMap& mld, const CU
 #pragma unroll
     for (int i = 0; i < kTokZ; ++i) {
       if (kF || z0 + i < nz) {
-        ld[i] = __ldg(fd + sd[z0 + i][l]) & ~kFinal;  // rank of the maximum
-        la[i] = __ldg(fa + sa[z0 + i][l]) & ~kFinal;  // rank of the minimum
+        ld[i] = __ldg(fd + sd[z0 + i][l]);  // rank of the maximum | kFinal
+        la[i] = __ldg(fa + sa[z0 + i][l]);  // rank of the minimum | kFinal
       }
     }
 #pragma unroll
     for (int i = 0; i < kTokZ; ++i) {
       if (!kF && z0 + i >= nz) break;
+      // An entry the speculative forest sweep left unresolved holds a table
+      // index, not a rank: no set insert and no extremum gather for it (the
+      // pass is redone after the forest converges).
+      if (!(ld[i] & la[i] & kFinal)) {
+        a.desc[gv] = a.asc[gv] = a.ms[gv] = 0u;
+        lkey = Key(~Key(0));
+        gv += d.XY;
+        continue;
+      }
+      ld[i] &= ~kFinal;
+      la[i] &= ~kFinal;
       const Key key = kDense ? Key(la[i] * a.nmax + ld[i]) : Key((uint64_t(la[i]) << 32) | ld[i]);
       if (key != lkey) {
         if (kDense) {
@@ -1559,7 +1583,8 @@ __global__ void __launch_bounds__(256) k_ms_ids(uint32_t* __restrict__ ms, uint6
   }
 }
 
-bool g_consts_ready[64] = {};
+std::atomic<bool> g_consts_ready[64] = {};
+std::mutex g_consts_mu;
 
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -1589,7 +1614,10 @@ bool fused_supported(const Grid& g) {
 FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* desc, uint32_t* asc, uint32_t* ms) {
   FusedOut o{};
   for (auto& s : c.stats) s = 0;
-  if (c.device >= 0 && c.device < 64 && !g_consts_ready[c.device]) {
+  if (c.device >= 0 && c.device < 64 && !g_consts_ready[c.device].load(std::memory_order_acquire)) {
+    // one upload per device even when several host threads arrive together
+    std::lock_guard<std::mutex> lock(g_consts_mu);
+    if (!g_consts_ready[c.device].load(std::memory_order_acquire)) {
     CK(cudaFuncSetAttribute(k_tile_segment<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kASmem));
     CK(cudaFuncSetAttribute(k_tile_segment<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kASmem));
     // on the context stream (a non-blocking stream does not wait on the legacy one)
@@ -1600,7 +1628,8 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
     k_march_init<<<1, 128, 0, c.stream>>>();
     CK_LAUNCH("k_march_init");
     c.sync();  // other contexts (other streams) may use the tables next
-    g_consts_ready[c.device] = true;
+    g_consts_ready[c.device].store(true, std::memory_order_release);
+    }
   }
   FDims d;
   d.X = uint32_t(g.X);

@@ -13,6 +13,9 @@
 #include <functional>
 #include <vector>
 
+#include <atomic>
+#include <mutex>
+
 #include "common.cuh"
 #include "tet_tables.h"
 
@@ -480,10 +483,14 @@ __global__ void __launch_bounds__(kMThreads) k_count_ranges(const L* __restrict_
     if (s_cnt[i]) atomicAdd(&counts[i], s_cnt[i]);
 }
 
-bool g_tables_ready[64] = {};
+std::atomic<bool> g_tables_ready[64] = {};
+std::mutex g_tables_mu;
 
 void ensure_tables(Ctx& c) {
-  if (c.device >= 0 && c.device < 64 && g_tables_ready[c.device]) return;
+  if (c.device >= 0 && c.device < 64 && g_tables_ready[c.device].load(std::memory_order_acquire)) return;
+  // one upload per device even when several host threads arrive together
+  std::lock_guard<std::mutex> lock(g_tables_mu);
+  if (c.device >= 0 && c.device < 64 && g_tables_ready[c.device].load(std::memory_order_acquire)) return;
   // Uploaded on the context stream and waited for: a plain cudaMemcpyToSymbol
   // runs on the legacy stream, which a non-blocking context stream does not
   // wait on (the first count kernel then saw half-written tables).
@@ -493,7 +500,7 @@ void ensure_tables(Ctx& c) {
   if (ft.size() != 12) fail(PLMSS_ERR_LOGIC, "face type table must have 12 entries");
   CK(cudaMemcpyToSymbolAsync(c_faces, ft.data(), sizeof(FaceType) * 12, 0, cudaMemcpyHostToDevice, c.stream));
   c.sync();
-  if (c.device >= 0 && c.device < 64) g_tables_ready[c.device] = true;
+  if (c.device >= 0 && c.device < 64) g_tables_ready[c.device].store(true, std::memory_order_release);
 }
 
 template <class L>

@@ -199,7 +199,9 @@ def ms_segmentation(field_owned: torch.Tensor, dims, backend, group=None) -> Sla
     minima = torch.cat(_all_gather_var(ids[asc == ids], group))
 
     # 5. Morse-Smale ids: lexicographic (asc, desc) == key asc * N + desc
-    local_regions = getattr(backend, "local_regions", None)
+    # The device combine_ms indexes its rank maps by slab-local vertex index,
+    # so it only applies while global ids equal local ones (one rank).
+    local_regions = getattr(backend, "local_regions", None) if world == 1 else None
     if local_regions is not None:  # dense local ids from the device hash (no sort of the slab)
         local, uniq = local_regions(asc, desc, N)
     else:

@@ -1,0 +1,68 @@
+"""Bit-exactness on the five BASELINE configs at FULL size (north star:
+"bit-exact labels and separators vs the CPU oracle on all 5 configs").
+
+The oracle results (the compiled reference + the full-size C restatement,
+tests/golden/make_digests.py) are committed as digests; here the device
+generates each field (checked byte-for-byte against the host input
+definition through its digest), runs the fused pipeline, and every output's
+digest must equal the oracle's: desc, asc, maxima, minima, dense MS ids,
+region keys and all separator records in reference order
+(proj/tests/acceptance.cpp:94-117 oracle equivalence, :279-298 exact counts).
+"""
+import json
+import os
+
+import pytest
+
+from conftest import GOLDEN
+
+CFGS = ["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"]
+NAMES = ("desc", "asc", "ms", "maxima", "minima", "region_keys", "tris")
+
+
+def golden(name):
+    p = os.path.join(GOLDEN, f"{name}_digest.json")
+    if not os.path.exists(p):
+        pytest.skip(f"{p} not generated")
+    return json.load(open(p))
+
+
+@pytest.mark.parametrize("name", CFGS)
+def test_golden_digest_files_are_complete(name):
+    g = golden(name)
+    for k in ("field", "n_maxima", "n_minima", "n_regions", "n_tris") + NAMES:
+        assert k in g, k
+    assert sum(g["tri_chunk_counts"]) == g["n_tris"]
+
+
+# (config, combine path): 0 = the pipeline's own choice (dense region bitmap
+# unless n_max * n_min >= 2^32, i.e. the hash set for cfg3), 2 = the hash set
+# forced, so both region-key modes run at full size.
+CASES = [("cfg1", 0), ("cfg2", 0), ("cfg2", 2), ("cfg3", 0), ("cfg4", 0), ("cfg5", 0), ("cfg5", 2)]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,path", CASES)
+def test_full_size_matches_oracle(plmss, gpu, name, path):
+    import torch
+
+    from paper_2303_15491_b200.configs import CONFIGS
+    from paper_2303_15491_b200.digest import digest_device
+
+    g = golden(name)
+    cfg = CONFIGS[name]
+    f = plmss.synth_field(cfg.dims, kind=cfg.kind, gaussians=cfg.gaussians() if cfg.kind == "gaussians" else None,
+                          noise_amp=cfg.noise, seed=cfg.seed, levels=cfg.levels, ctx=gpu)
+    torch.cuda.synchronize()
+    assert digest_device(f) == g["field"], "device generator differs from the host input definition"
+    gpu.set_option(plmss.OPT_COMBINE_PATH, path)
+    try:
+        res = plmss.pipeline(cfg.dims, f, ctx=gpu)
+    finally:
+        gpu.set_option(plmss.OPT_COMBINE_PATH, 0)
+    del f
+    assert (res.n_maxima, res.n_minima, res.n_regions, res.n_tris) == (g["n_maxima"], g["n_minima"],
+                                                                       g["n_regions"], g["n_tris"])
+    got = plmss.result_digests(gpu, res)
+    bad = [k for k in NAMES if got[k] != g[k]]
+    assert not bad, f"{name}: digests differ for {bad}"

@@ -398,9 +398,14 @@ def test_slab_backend_single_rank_nccl_matches_pipeline(plmss, gpu):
                           ctx=gpu)
     res = plmss.pipeline(cfg.dims, f, ctx=gpu)
     out = plmss.fetch(gpu, res)
-    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-    os.environ.setdefault("MASTER_PORT", "29547")
-    dist.init_process_group("nccl", rank=0, world_size=1)
+    if dist.is_initialized() or not dist.is_nccl_available():
+        pytest.skip("a process group is already open / NCCL unavailable")
+    import socket
+
+    with socket.socket() as sk:  # a free port
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
     try:
         s = ms_segmentation(f, cfg.dims, B200Backend(gpu))
         torch.cuda.synchronize()
