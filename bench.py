@@ -132,12 +132,31 @@ def load_configs():
     return mod
 
 
+def cpu_sample(cfg, args):
+    """The bounded CPU sample of the configured field, shared by the
+    reference arm and the cpu_baseline leg: vertex layers [0, ref_layers)
+    cropped to x, y < ref_xy, generated on the host by the oracle's C loop of
+    the input definition (include/plmss_synth.h; the same bytes as the
+    device generator). Returns (dims, f32 values, description)."""
+    import oracle
+
+    X, Y, Z = cfg.dims
+    k = max(2, min(Z, args.ref_layers))
+    xs, ys = min(X, args.ref_xy), min(Y, args.ref_xy)
+    R = oracle.Restatement()
+    f = R.synth(cfg, z0=0, nz=k) if cfg.levels == 0 else R.synth(cfg)[: X * Y * k]
+    f = np.ascontiguousarray(f.reshape(k, Y, X)[:, :ys, :xs]).reshape(-1)
+    desc = (f"sub-box x<{xs}, y<{ys}, z<{k} ({xs * ys * k} vertices) of {cfg.name} {X}x{Y}x{Z}; reference "
+            f"run_benchmark pass (compute_order, segment, combine_ms, index_separators, emit_geometry; MorseSmale)")
+    return (xs, ys, k), f, desc
+
+
 def run_reference_arm(args, rank, world):
     """The reference's own CPU implementation (oracle/_ref: proj/src compiled
-    unchanged) on all host cores, one bounded z-slab sample of the configured
-    field per step (run_benchmark's MorseSmale pass, proj/src/bench.cpp:62-87).
-    The sample is generated on the host by the oracle's C loop of the input
-    definition (include/plmss_synth.h) — no B200 code in this process."""
+    unchanged) on all host cores, one bounded sample of the configured field
+    per step (run_benchmark's MorseSmale pass, proj/src/bench.cpp:62-87). The
+    sample is generated on the host (cpu_sample) — no B200 code in this
+    process."""
     if rank != 0:
         return 0
     import oracle
@@ -145,12 +164,8 @@ def run_reference_arm(args, rank, world):
     cfg = load_configs().CONFIGS[args.config]
     ref = oracle.Reference()
     cores = os.cpu_count() or 1
-    X, Y, Z = cfg.dims
-    k = max(2, min(Z, args.ref_layers))
-    dims = (X, Y, k)
-    f = oracle.Restatement().synth(cfg, z0=0, nz=k) if cfg.levels == 0 else \
-        oracle.Restatement().synth(cfg)[: X * Y * k]
-    nv = X * Y * k
+    dims, f, sample = cpu_sample(cfg, args)
+    nv = int(np.prod(dims))
     for _ in range(args.warmup):
         ref.run_once(dims, f, cores)
     times = []
@@ -163,8 +178,6 @@ def run_reference_arm(args, rank, world):
         phases_acc += np.array(list(ph.values()))
     t = float(np.mean(times))
     value = nv / t / 1e9
-    sample = (f"z-slab {X}x{Y}x{k} ({nv} vertices, the first {k} of {Z} layers) of {cfg.name}; reference "
-              f"run_benchmark pass (compute_order+segment+combine_ms+index+geometry, MorseSmale) per step")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak" if world > 1
@@ -180,25 +193,73 @@ def run_reference_arm(args, rank, world):
     return 0
 
 
-def run_multi(args, cfg, ctx, field, rank, world, local):
-    """N > 1: the volume is z-slab partitioned (paper_2303_15491_b200/
-    distributed.py) — strong scaling of the one configured volume; every
-    rank's slab pipeline plus the NCCL exchanges is timed, max over ranks."""
+def gather_digest(t, rank, world, dist, piece=1 << 28):
+    """Chunked SHA-256 (digest.py) of the rank-order concatenation of a 1-D
+    device tensor held in pieces by every rank: rank 0 receives the other
+    ranks' pieces over NCCL and hashes the stream in order."""
+    import torch
+
+    from paper_2303_15491_b200.digest import ChunkedSha256
+
+    t = t.reshape(-1)
+    n = torch.tensor([t.numel()], dtype=torch.int64, device=t.device)
+    ns = torch.empty(world, dtype=torch.int64, device=t.device)
+    dist.all_gather_into_tensor(ns, n)
+    ns = ns.cpu().tolist()
+    h = ChunkedSha256() if rank == 0 else None
+    stage = torch.empty(piece, dtype=t.dtype, device=t.device) if rank == 0 else None
+    for r in range(world):
+        for i in range(0, ns[r], piece):
+            k = min(piece, ns[r] - i)
+            if r == 0 and rank == 0:
+                h.update(t[i:i + k].cpu().numpy()).drain()
+            elif rank == 0:
+                dist.recv(stage[:k], src=r)
+                h.update(stage[:k].cpu().numpy()).drain()
+            elif rank == r:
+                dist.send(t[i:i + k].contiguous(), dst=0)
+    return h.hexdigest() if rank == 0 else None
+
+
+def run_multi(args, cfg, ctx, rank, world, local):
+    """The z-slab pipeline (paper_2303_15491_b200/distributed.py): rank r owns
+    slab_bounds(Z, world, r) of the one configured volume (strong scaling);
+    every step is the whole multi-GPU pass — field halo exchange, the four
+    device stages and their NCCL collectives — timed on each rank's stream,
+    max over ranks."""
     import torch
     import torch.distributed as dist
 
-    from paper_2303_15491_b200.distributed import B200Backend, ms_segmentation, slab_bounds
+    import paper_2303_15491_b200 as P
+    from paper_2303_15491_b200.distributed import (B200SlabBackend, TorchComm, halo_bounds, slab_bounds,
+                                                   slab_step)
 
     X, Y, Z = cfg.dims
+    XY = X * Y
     z0, z1 = slab_bounds(Z, world, rank)
-    own = field[z0 * X * Y: z1 * X * Y].contiguous()
-    del field
-    backend = B200Backend(ctx)
-    stream = ctx.stream
-    for _ in range(max(args.warmup, 0)):
-        ms_segmentation(own, cfg.dims, backend)
+    h0, h1 = halo_bounds(Z, world, rank)
+    nown = (z1 - z0) * XY
+    buf = torch.empty((h1 - h0) * XY, dtype=torch.float32, device="cuda")
+    own = buf[(z0 - h0) * XY:(z1 - h0) * XY]
+    g = cfg.gaussians() if cfg.kind == "gaussians" else None
+    if cfg.levels:  # quantised: the levels span the whole volume
+        own.copy_(P.synth_field(cfg.dims, kind=cfg.kind, gaussians=g, noise_amp=cfg.noise, seed=cfg.seed,
+                                levels=cfg.levels, ctx=ctx)[z0 * XY:z1 * XY])
+    else:
+        own.copy_(P.api.synth_layers(cfg.dims, z0, z1 - z0, kind=cfg.kind, gaussians=g, noise_amp=cfg.noise,
+                                     seed=cfg.seed, ctx=ctx))
     torch.cuda.synchronize()
-    launches0 = __import__("paper_2303_15491_b200").api.launch_count()
+    backend = B200SlabBackend(ctx)
+    comm = TorchComm()
+    stream = ctx.stream
+
+    def step():
+        return comm.run(slab_step(backend, cfg.dims, rank, world, buf))
+
+    for _ in range(max(args.warmup, 0)):
+        step()
+    torch.cuda.synchronize()
+    launches0 = P.api.launch_count()
     clocks = Clocks(local)
     clocks.start()
     time.sleep(0.3)
@@ -209,12 +270,12 @@ def run_multi(args, cfg, ctx, field, rank, world, local):
     start.record(stream)
     res = None
     for _ in range(args.steps):
-        res = ms_segmentation(own, cfg.dims, backend)
+        res = step()
     stop.record(stream)
     torch.cuda.synchronize()
     dist.barrier()
     clk = clocks.stop()
-    launches = __import__("paper_2303_15491_b200").api.launch_count() - launches0
+    launches = P.api.launch_count() - launches0
     ms = start.elapsed_time(stop) / args.steps
     t = torch.tensor([ms], device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -223,16 +284,33 @@ def run_multi(args, cfg, ctx, field, rank, world, local):
     value = nv / (ms * 1e-3) / 1e9
     peak, peak_src = peaks()
     b_alg = B_PER_VERTEX * nv + B_PER_TRI * res.tri_total
-    # aggregate device bandwidth: the algorithmic bytes of the whole volume
-    # against world x the per-GPU peak
-    frac = b_alg / (ms * 1e-3) / 1e9 / (peak * world)
+    pipe_gbs = b_alg / (ms * 1e-3) / 1e9
+    frac = pipe_gbs / (peak * world)
+
+    # parity: the concatenated rank outputs against the single-volume digests
+    parity = None
+    gp = os.path.join(ROOT, "tests", "golden", f"{args.config}_digest.json")
+    if not args.no_parity and os.path.exists(gp):
+        gd = json.load(open(gp))
+        got = {k: gather_digest(getattr(res, k), rank, world, dist) for k in ("desc", "asc", "ms", "tris")}
+        if rank == 0:
+            from paper_2303_15491_b200.digest import digest_device
+
+            for k in ("maxima", "minima", "region_keys"):
+                got[k] = digest_device(getattr(res, k))
+            bad = [k for k in got if got[k] != gd[k]]
+            if (res.maxima.numel(), res.minima.numel(), res.region_keys.numel(), res.tri_total) != \
+                    (gd["n_maxima"], gd["n_minima"], gd["n_regions"], gd["n_tris"]):
+                bad.append("counts")
+            parity = {"oracle": f"tests/golden/{args.config}_digest.json", "checked": sorted(got) + ["counts"],
+                      "match": not bad, "mismatched": bad}
 
     e2e = None
     if not args.no_e2e:
-        h_own = torch.empty(own.numel(), dtype=torch.float32, pin_memory=True)
+        h_own = torch.empty(nown, dtype=torch.float32, pin_memory=True)
         h_own.copy_(own.cpu())
-        nown = own.numel()
-        outs = {k: torch.empty(nown, dtype=torch.int64, pin_memory=True) for k in ("desc", "asc", "ms")}
+        outs = {k: torch.empty(nown, dtype=torch.int32, pin_memory=True) for k in ("desc", "asc", "ms")}
+        h_tris = torch.empty((max(res.tris.shape[0], 1) * 2, 2), dtype=torch.int64, pin_memory=True)
         dist.barrier()
         torch.cuda.synchronize()
         e_start = torch.cuda.Event(enable_timing=True)
@@ -240,12 +318,14 @@ def run_multi(args, cfg, ctx, field, rank, world, local):
         e_start.record(stream)
         nrec = 0
         for _ in range(args.e2e_steps):
-            d_own = h_own.to("cuda", non_blocking=True)
-            r2 = ms_segmentation(d_own, cfg.dims, backend)
+            own.copy_(h_own, non_blocking=True)
+            r2 = step()
             for k in ("desc", "asc", "ms"):
                 outs[k].copy_(getattr(r2, k), non_blocking=True)
-            recs = torch.stack([r2.cells, r2.lo, r2.hi], dim=1).cpu()
-            nrec = recs.shape[0]
+            nrec = r2.tris.shape[0]
+            if nrec > h_tris.shape[0]:
+                h_tris = torch.empty((nrec, 2), dtype=torch.int64, pin_memory=True)
+            h_tris[:nrec].copy_(r2.tris, non_blocking=True)
         e_stop.record(stream)
         torch.cuda.synchronize()
         e_ms = e_start.elapsed_time(e_stop) / args.e2e_steps
@@ -253,27 +333,45 @@ def run_multi(args, cfg, ctx, field, rank, world, local):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e_ms = float(t.item())
         e2e = {"value": nv / (e_ms * 1e-3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": 4 * nown,
-               "d2h_bytes_per_step": 3 * 8 * nown + 24 * nrec, "ms_per_step": round(e_ms, 3),
-               "note": "per-rank bytes; rank-0 values"}
+               "d2h_bytes_per_step": 3 * 4 * nown + 16 * nrec, "ms_per_step": round(e_ms, 3),
+               "note": "per-rank bytes (rank 0); the slab's field in, its labels and records out"}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
         "data": "synthetic",
         "config": {"workload": cfg.name, "dims": list(cfg.dims), "parallelism": f"z-slab x{world}",
+                   "input": "float32 slab (+ halo layers) resident in each GPU's HBM",
                    "l2": "inputs larger than L2", "vertices": nv, "triangles": res.tri_total,
-                   "regions": int(res.region_keys.shape[0])},
-        "roofline": {"bound": "hbm", "kernel": "whole z-slab pipeline (all ranks)",
-                     "achieved": round(b_alg / (ms * 1e-3) / 1e9, 1), "peak": peak * world, "unit": "GB/s",
-                     "frac": round(frac, 4), "traffic": None, "peak_source": peak_src, "alg_bytes": b_alg},
-        "roofline_pipeline": {"bound": "hbm", "achieved": round(b_alg / (ms * 1e-3) / 1e9, 1), "peak": peak * world,
-                              "unit": "GB/s", "frac": round(frac, 4), "alg_bytes": b_alg, "peak_source": peak_src},
-        "clocks": clk, "gpu_launches": launches, "e2e": e2e, "cpu_baseline": None,
+                   "regions": int(res.region_keys.numel()), "slab_layers": [z0, z1]},
+        "roofline": {"bound": "hbm", "kernel": "whole z-slab pipeline (all ranks)", "achieved": round(pipe_gbs, 1),
+                     "peak": peak * world, "unit": "GB/s", "frac": round(frac, 4), "traffic": None,
+                     "peak_source": peak_src, "alg_bytes": b_alg},
+        "roofline_pipeline": {"bound": "hbm", "achieved": round(pipe_gbs, 1), "peak": peak * world, "unit": "GB/s",
+                              "frac": round(frac, 4), "alg_bytes": b_alg, "peak_source": peak_src},
+        "clocks": clk, "gpu_launches": launches, "e2e": e2e, "cpu_baseline": None, "parity": parity,
+        "nccl": {"backend": dist.get_backend(), "world": world},
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
     ctx.close()
     dist.destroy_process_group()
+    if parity is not None and not parity["match"]:
+        print(f"PARITY FAILURE vs {parity['oracle']}: {parity['mismatched']}", file=sys.stderr)
+        return 3
     return 0
+
+
+def relaunch_under_torchrun(n):
+    """bench.py --gpus N without a torchrun environment: start N ranks."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    print(f"bench.py: starting {n} ranks: {' '.join(cmd[2:])}", file=sys.stderr, flush=True)
+    return subprocess.call(cmd)
 
 
 def main():
@@ -288,10 +386,15 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--slab", action="store_true",
                     help="run the z-slab (multi-GPU) path even at world size 1 (torchrun --nproc-per-node 1)")
+    ap.add_argument("--cpu-runs", type=int, default=3, help="timed runs of the cpu_baseline sample")
+    ap.add_argument("--no-parity", action="store_true", help="skip the digest check of the last step's outputs")
     ap.add_argument("--ref-layers", type=int, default=64,
                     help="z-layers of the configured field in the CPU sample (reference arm and cpu_baseline)")
+    ap.add_argument("--ref-xy", type=int, default=512, help="x / y extent of the CPU sample")
     args = ap.parse_args()
     rank, world, local = dist_setup()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch_under_torchrun(args.gpus)
 
     if args.impl == "reference":
         return run_reference_arm(args, rank, world)
@@ -302,22 +405,21 @@ def main():
     from paper_2303_15491_b200.configs import CONFIGS
 
     torch.cuda.set_device(local)
-    pg = None
+    cfg = CONFIGS[args.config]
+    ctx = P.Context(local)
     if world > 1 or args.slab:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl")
-        pg = dist
-    cfg = CONFIGS[args.config]
-    ctx = P.Context(local)
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator init in the log
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        return run_multi(args, cfg, ctx, rank, world, local)
+    pg = None
     stream = ctx.stream
     dims = cfg.dims
     nv = cfg.n
     field = P.synth_field(dims, kind=cfg.kind, gaussians=cfg.gaussians() if cfg.kind == "gaussians" else None,
                           noise_amp=cfg.noise, seed=cfg.seed, levels=cfg.levels, ctx=ctx)
     torch.cuda.synchronize()
-    if world > 1 or args.slab:
-        return run_multi(args, cfg, ctx, field, rank, world, local)
 
     for _ in range(max(args.warmup, 0)):
         P.pipeline(dims, field, ctx=ctx)
@@ -369,6 +471,20 @@ def main():
     if os.path.exists(tp) and args.config == "cfg5":  # the captured workload (profiles/traffic.json _source)
         traffic = json.load(open(tp)).get(dom)
 
+    # ---- parity: the last timed step's outputs against the oracle digests --
+    parity = None
+    gp = os.path.join(ROOT, "tests", "golden", f"{args.config}_digest.json")
+    if not args.no_parity and os.path.exists(gp):
+        g = json.load(open(gp))
+        names = ("desc", "asc", "ms", "maxima", "minima", "region_keys", "tris")
+        got = P.result_digests(ctx, res, names)
+        counts = (res.n_maxima, res.n_minima, res.n_regions, res.n_tris)
+        bad = [k for k in names if got[k] != g[k]]
+        if counts != (g["n_maxima"], g["n_minima"], g["n_regions"], g["n_tris"]):
+            bad.append("counts")
+        parity = {"oracle": f"tests/golden/{args.config}_digest.json", "checked": list(names) + ["counts"],
+                  "match": not bad, "mismatched": bad}
+
     # ---- end to end through the C-ABI over pinned host buffers -----------
     e2e = None
     if not args.no_e2e:
@@ -408,20 +524,17 @@ def main():
             import oracle
 
             ref = oracle.Reference()
-            X, Y, Z = dims
-            k = max(2, min(Z, args.cpu_sample // (X * Y)))
-            fs = field[: X * Y * k].cpu().numpy()
+            sdims, fs, sample = cpu_sample(cfg, args)
             cores = os.cpu_count() or 1
             ts = []
-            for _ in range(3):
+            for _ in range(args.cpu_runs):
                 t0 = time.perf_counter()
-                ref.run_once((X, Y, k), fs, cores)
+                ref.run_once(sdims, fs, cores)
                 ts.append(time.perf_counter() - t0)
             ts.sort()
-            tcpu = ts[1]  # drop best and worst (bench.cpp:22-44)
-            cpu = {"value": X * Y * k / tcpu / 1e9, "unit": UNIT, "cores": cores, "kind": "reference",
-                   "sample": f"z-slab {X}x{Y}x{k} of {cfg.name}, reference pipeline pass (compute_order, segment, "
-                             f"combine_ms, index_separators, emit_geometry; MorseSmale), median of 3 runs"}
+            tcpu = ts[len(ts) // 2]  # median (3 runs: drop best and worst, bench.cpp:22-44)
+            cpu = {"value": int(np.prod(sdims)) / tcpu / 1e9, "unit": UNIT, "cores": cores, "kind": "reference",
+                   "sample": f"{sample}, median of {len(ts)} runs"}
         except Exception as e:  # reported, never fatal
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"unavailable: {e}"}
@@ -445,12 +558,16 @@ def main():
         "gpu_launches": launches,
         "e2e": e2e,
         "cpu_baseline": cpu,
+        "parity": parity,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
     ctx.close()
     if pg:
         pg.destroy_process_group()
+    if parity is not None and not parity["match"]:
+        print(f"PARITY FAILURE vs {parity['oracle']}: {parity['mismatched']}", file=sys.stderr)
+        return 3
     return 0
 
 

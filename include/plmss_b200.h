@@ -129,6 +129,59 @@ int plmss_b200_segment(plmss_ctx* ctx, const int64_t dims[3], int key_type, cons
 int plmss_b200_segment_slab(plmss_ctx* ctx, const int64_t dims[3], int key_type, const void* d_keys,
                             int halo_lo, int halo_hi, uint32_t* d_desc, uint32_t* d_asc, int32_t* sweeps);
 
+/* ---- z-slab pipeline (multi-GPU) --------------------------
+ * The fused pipeline on one rank's z-slab, in four stages; the caller runs
+ * the exchanges between them (paper_2303_15491_b200/distributed.py, NCCL):
+ *   1 slab_segment : pass A on the slab's bricks (field halo layers as real
+ *                    data), sorted extremum lists, the terminal forest inside
+ *                    the slab; chains leaving the slab end at portals.
+ *     -> all_gather counts, extremum lists, boundary layers
+ *   2 slab_resolve : portals resolved through every rank's boundary layers,
+ *                    desc / asc (global vertex ids), region tokens, the slab's
+ *                    distinct rank pairs.
+ *     -> all_gather the rank pairs
+ *   3 slab_ids     : global dense MS ids (the combine_ms order) into ms.
+ *     -> the next rank's first layer of ids into ms's extra layer
+ *   4 slab_emit    : separator records of the owned cube layers, global cell
+ *                    ids, reference order.
+ * No reference counterpart (the reference is one process, parallel.hpp:27-57
+ * splits work among threads); results equal the single-volume pipeline's.
+ * Slabs are whole 32-layer brick layers: z0 % 32 == 0, z1 % 32 == 0 or
+ * z1 == Z. All device pointers handed to a stage must stay valid until
+ * slab_emit returns. */
+typedef struct plmss_slab_info {
+  int64_t n_maxima, n_minima;      /* stage 1: the slab's; stage 2+: global */
+  const uint32_t* d_maxima;        /* stage 1: the slab's sorted extrema (global vertex ids) */
+  const uint32_t* d_minima;
+  const uint32_t* d_boundary;      /* stage 1: [desc, asc] x [first, last owned layer] x X*Y words */
+  int64_t n_keys;                  /* stage 2: the slab's distinct (rank_min << 32 | rank_max) */
+  const uint64_t* d_keys;
+  int64_t n_regions;               /* stage 3: global region count and keys (asc << 32 | desc, sorted) */
+  const uint64_t* d_region_keys;
+  int64_t n_tris;                  /* stage 4: this slab's separator records */
+  const plmss_tri* d_tris;
+  int32_t sweeps;                  /* forest sweeps inside the slab */
+  int32_t dense;                   /* 1: rank-product bitmap, 0: region hash set */
+} plmss_slab_info;
+
+/* d_field: vertex layers [z0 - 1, z1 + 1) clipped to [0, Z) (halos of the
+ * ranks below / above). */
+int plmss_b200_slab_segment(plmss_ctx* ctx, const int64_t dims[3], int64_t z0, int64_t z1, const float* d_field,
+                            plmss_slab_info* info);
+/* d_boundary_all: every rank's d_boundary, rank order (world * 4 * X*Y);
+ * h_max_counts / h_min_counts: every rank's n_maxima / n_minima (host);
+ * d_maxima_all / d_minima_all: the concatenated lists (rank order = id
+ * order). Outputs: d_desc, d_asc (owned vertices), d_ms (owned vertices +
+ * one more layer when z1 < Z; region tokens until slab_ids). */
+int plmss_b200_slab_resolve(plmss_ctx* ctx, const uint32_t* d_boundary_all, int world, int rank,
+                            const int64_t* h_max_counts, const int64_t* h_min_counts, const uint32_t* d_maxima_all,
+                            const uint32_t* d_minima_all, uint32_t* d_desc, uint32_t* d_asc, uint32_t* d_ms,
+                            plmss_slab_info* info);
+/* d_keys_all: every rank's d_keys concatenated (duplicates allowed). */
+int plmss_b200_slab_ids(plmss_ctx* ctx, const uint64_t* d_keys_all, int64_t n_keys_all, plmss_slab_info* info);
+/* The layer z1 of d_ms holds the next rank's first layer of ids (z1 < Z). */
+int plmss_b200_slab_emit(plmss_ctx* ctx, plmss_slab_info* info);
+
 /* Step 1 only (detail::seed_hops_both, segmentation.cpp:60-85): hop targets. */
 int plmss_b200_seed_hops(plmss_ctx* ctx, const int64_t dims[3], int key_type, const void* d_keys,
                          uint32_t* d_desc, uint32_t* d_asc);

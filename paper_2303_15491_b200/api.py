@@ -47,6 +47,7 @@ HEADER_FUNCTIONS = [
     "plmss_b200_synth", "plmss_b200_launch_count", "plmss_b200_ctx_stats", "plmss_b200_count_by_cell_ranges",
     "plmss_b200_compress_sweep", "plmss_b200_segment_slab", "plmss_b200_weld_points", "plmss_b200_read_volume",
     "plmss_b200_write_labels", "plmss_b200_write_surface_obj", "plmss_b200_synth_layers",
+    "plmss_b200_slab_segment", "plmss_b200_slab_resolve", "plmss_b200_slab_ids", "plmss_b200_slab_emit",
 ]
 
 
@@ -56,6 +57,16 @@ class PlmssResult(C.Structure):
         ("d_minima", C.c_void_p), ("d_region_keys", C.c_void_p), ("d_tris", C.c_void_p),
         ("n_vertices", C.c_int64), ("n_maxima", C.c_int64), ("n_minima", C.c_int64),
         ("n_regions", C.c_int64), ("n_tris", C.c_int64), ("sweeps", C.c_int32),
+    ]
+
+
+class PlmssSlabInfo(C.Structure):
+    """plmss_slab_info (include/plmss_b200.h): z-slab stage outputs."""
+    _fields_ = [
+        ("n_maxima", C.c_int64), ("n_minima", C.c_int64), ("d_maxima", C.c_void_p), ("d_minima", C.c_void_p),
+        ("d_boundary", C.c_void_p), ("n_keys", C.c_int64), ("d_keys", C.c_void_p), ("n_regions", C.c_int64),
+        ("d_region_keys", C.c_void_p), ("n_tris", C.c_int64), ("d_tris", C.c_void_p), ("sweeps", C.c_int32),
+        ("dense", C.c_int32),
     ]
 
 
@@ -102,6 +113,11 @@ def lib() -> C.CDLL:
         L.plmss_b200_read_volume.argtypes = [vp, C.c_char_p, vp, i32, i32, vp]
         L.plmss_b200_write_labels.argtypes = [vp, C.c_char_p, i32, vp, vp, i64]
         L.plmss_b200_write_surface_obj.argtypes = [vp, C.c_char_p, vp, i64, vp, vp, i64, i32]
+        SI = C.POINTER(PlmssSlabInfo)
+        L.plmss_b200_slab_segment.argtypes = [vp, vp, i64, i64, vp, SI]
+        L.plmss_b200_slab_resolve.argtypes = [vp, vp, i32, i32, vp, vp, vp, vp, vp, vp, vp, SI]
+        L.plmss_b200_slab_ids.argtypes = [vp, vp, i64, SI]
+        L.plmss_b200_slab_emit.argtypes = [vp, SI]
         L.plmss_b200_tet_table.argtypes = [vp, vp]
         L.plmss_b200_tet_table.restype = None
         L.plmss_b200_launch_count.restype = C.c_ulonglong
@@ -511,8 +527,7 @@ def result_digests(ctx: Context, res: PipelineResult, names=("desc", "asc", "ms"
             buf = np.empty(k, np.uint8)
             _check(lib().plmss_b200_copy(ctx.h, buf.ctypes.data, C.c_void_p(ptr + off), k, 1))
             h.update(buf)
-            for f in h._futs[:-4 * max(piece_bytes // BLOCK, 1)]:  # bound host memory
-                f.result()
+            h.drain(4 * max(piece_bytes // BLOCK, 1))  # bound host memory
         out[name] = h.hexdigest()
     return out
 

@@ -515,6 +515,45 @@ int plmss_b200_synth_layers(plmss_ctx* p, const int64_t dims[3], int kind, const
   });
 }
 
+// ---- z-slab pipeline (fused.cu slab_*) ----------------------------------
+int plmss_b200_slab_segment(plmss_ctx* p, const int64_t dims[3], int64_t z0, int64_t z1, const float* d_field,
+                            plmss_slab_info* info) {
+  return guarded([&] {
+    Ctx& c = C(p);
+    set_device(c);
+    if (!d_field) fail(PLMSS_ERR_INVALID_ARGUMENT, "field is null");
+    slab_segment(c, make_grid(dims), z0, z1, d_field, info);
+  });
+}
+
+int plmss_b200_slab_resolve(plmss_ctx* p, const uint32_t* d_boundary_all, int world, int rank,
+                            const int64_t* h_max_counts, const int64_t* h_min_counts, const uint32_t* d_maxima_all,
+                            const uint32_t* d_minima_all, uint32_t* d_desc, uint32_t* d_asc, uint32_t* d_ms,
+                            plmss_slab_info* info) {
+  return guarded([&] {
+    Ctx& c = C(p);
+    set_device(c);
+    slab_resolve(c, d_boundary_all, world, rank, h_max_counts, h_min_counts, d_maxima_all, d_minima_all, d_desc,
+                 d_asc, d_ms, info);
+  });
+}
+
+int plmss_b200_slab_ids(plmss_ctx* p, const uint64_t* d_keys_all, int64_t n_keys_all, plmss_slab_info* info) {
+  return guarded([&] {
+    Ctx& c = C(p);
+    set_device(c);
+    slab_ids(c, d_keys_all, n_keys_all, info);
+  });
+}
+
+int plmss_b200_slab_emit(plmss_ctx* p, plmss_slab_info* info) {
+  return guarded([&] {
+    Ctx& c = C(p);
+    set_device(c);
+    slab_emit(c, info);
+  });
+}
+
 int plmss_b200_weld_points(plmss_ctx* p, double* d_points, int64_t n_points, int64_t* d_indices, int64_t n_indices,
                            int64_t* n_unique) {
   return guarded([&] {

@@ -75,11 +75,31 @@ enum Slot {
   S_BITMAP, S_HASH_K, S_HASH_V, S_SORT_A, S_SORT_B, S_SORT_C, S_SORT_D,
   S_TMP0, S_TMP1, S_TMP2, S_FIELD, S_MASK,
   S_LTD, S_LTA, S_TB, S_SD, S_SA, S_RK,  // fused pipeline: terminal indices, brick headers, table labels
+  S_SLAB_BND,                             // z-slab pipeline: boundary layers
   S_COUNT
+};
+
+// State of the z-slab pipeline between its four C-ABI stages (fused.cu).
+struct SlabState {
+  int stage = 0;            // last completed stage (0: none)
+  Grid g{};                 // the global grid
+  int64_t z0 = 0, z1 = 0;   // owned vertex layers
+  int has_down = 0, has_up = 0;
+  uint64_t ntiles = 0, nt = 0;
+  int64_t n_max_l = 0, n_min_l = 0, n_max_g = 0, n_min_g = 0;
+  bool dense = true;
+  uint64_t fcap = 0;        // hash mode: region set slots
+  int64_t n_keys = 0, R = 0, n_tris = 0;
+  int sweeps = 0;
+  const uint32_t *maxs_g = nullptr, *mins_g = nullptr;
+  uint32_t *desc = nullptr, *asc = nullptr, *ms = nullptr;
+  uint64_t* keys = nullptr;
+  plmss_tri* tris = nullptr;
 };
 
 struct Ctx {
   int device = 0;
+  SlabState slab;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   void* buf[S_COUNT] = {};
@@ -204,6 +224,13 @@ struct FusedOut {
 };
 bool fused_supported(const Grid& g);
 FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* desc, uint32_t* asc, uint32_t* ms);
+// z-slab pipeline (multi-GPU), fused.cu; the stages of include/plmss_b200.h
+void slab_segment(Ctx& c, const Grid& g, int64_t z0, int64_t z1, const float* field, plmss_slab_info* info);
+void slab_resolve(Ctx& c, const uint32_t* G, int world, int rank, const int64_t* max_counts,
+                  const int64_t* min_counts, const uint32_t* maxs_g, const uint32_t* mins_g, uint32_t* desc,
+                  uint32_t* asc, uint32_t* ms, plmss_slab_info* info);
+void slab_ids(Ctx& c, const uint64_t* keys_all, int64_t n_keys_all, plmss_slab_info* info);
+void slab_emit(Ctx& c, plmss_slab_info* info);
 
 // synth.cu
 // io.cu: callers either side of the path

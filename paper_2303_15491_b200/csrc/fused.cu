@@ -66,6 +66,14 @@ constexpr uint64_t kEmpty = ~uint64_t(0);
 struct FDims {
   uint32_t X, Y, Z, XY, n;
   uint32_t tx, ty, tz;  // tile counts
+  // Field buffer layers relative to the grid: local z in [zf0, zf0 + zfn)
+  // (a z-slab's halo layers: zf0 = -1 with a rank below, zfn = Z + halos).
+  int32_t zf0;
+  uint32_t zfn;
+  // z-slab pipeline: table entries >= pbase (= bricks << 15) are portals,
+  // pbase + side * XY + x + X * y for the vertex (x, y) of the halo layer
+  // below (side 0) / above (side 1) that a chain reaches; 0 = no portals.
+  uint32_t pbase;
 };
 
 
@@ -196,7 +204,7 @@ __global__ void __launch_bounds__(A_THREADS, 1)
       asm volatile(
           "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
           "%4}], [%5];" ::"r"(smem_u32(f)),
-          "l"(&tmap), "r"(gx0 - HXO), "r"(gy0 - 1), "r"(gz0 - 1), "r"(bar)
+          "l"(&tmap), "r"(gx0 - HXO), "r"(gy0 - 1), "r"(gz0 - 1 - d.zf0), "r"(bar)
           : "memory");
     }
   } else {
@@ -208,8 +216,9 @@ __global__ void __launch_bounds__(A_THREADS, 1)
         const int hx = i % HX, hy = (i / HX) % HY, hz = i / HXY;
         const int gx = gx0 + hx - HXO, gy = gy0 + hy - 1, gz = gz0 + hz - 1;
         v[k] = __int_as_float(0x7fc00000);
-        if (i < HN && gx >= 0 && gx < int(d.X) && gy >= 0 && gy < int(d.Y) && gz >= 0 && gz < int(d.Z))
-          v[k] = __ldg(field + (uint32_t(gx) + d.X * (uint32_t(gy) + d.Y * uint32_t(gz))));
+        if (i < HN && gx >= 0 && gx < int(d.X) && gy >= 0 && gy < int(d.Y) && gz >= d.zf0 &&
+            gz < d.zf0 + int(d.zfn))
+          v[k] = __ldg(field + (uint32_t(gx) + d.X * (uint32_t(gy) + d.Y * uint32_t(gz - d.zf0))));
       }
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
@@ -479,8 +488,13 @@ __global__ void __launch_bounds__(A_THREADS, 1)
     const int hz = int(h / PXY), r = int(h) - hz * PXY, hy = r / PX, hx = r - hy * PX;
     const uint32_t nb = uint32_t(int(tx) + ((hx - 1) >> 5)) +
                         d.tx * (uint32_t(int(ty) + ((hy - 1) >> 5)) + d.ty * uint32_t(int(tz) + ((hz - 1) >> 5)));
-    const uint32_t bm = (nb << 15) | uint32_t((hx - 1) & 31) | uint32_t((hy - 1) & 31) << 5 |
-                        uint32_t((hz - 1) & 31) << 10;
+    uint32_t bm = (nb << 15) | uint32_t((hx - 1) & 31) | uint32_t((hy - 1) & 31) << 5 |
+                  uint32_t((hz - 1) & 31) << 10;
+    // z-slab: a chain leaving the slab through a halo layer (only halo
+    // layers hold real values outside the slab in z) -> portal entry
+    const int gzc = gz0 + hz - 1;
+    if (d.pbase && (gzc < 0 || gzc >= int(d.Z)))
+      bm = d.pbase + (gzc < 0 ? 0u : d.XY) + uint32_t(gx0 + hx - 1) + d.X * uint32_t(gy0 + hy - 1);
     if (tbase + lk[0] < tt_cap) TT[tbase + lk[0]] = bm;
     Pd[h] = uint16_t(lk[0]);
     Pa[h] = uint16_t(lk[0]);
@@ -541,10 +555,13 @@ __global__ void __launch_bounds__(A_THREADS, 1)
 // entry starts as its successor's index.
 constexpr uint32_t kFinal = 0x80000000u;
 
+constexpr uint32_t kPortal = 0x40000000u;  // with kFinal: a z-slab portal (pbase-relative index below)
+
 __global__ void __launch_bounds__(256) k_tt_succ(const uint4* __restrict__ TB, const uint32_t* __restrict__ TT,
                                                  const uint16_t* __restrict__ ltd,
                                                  const uint16_t* __restrict__ lta, const uint32_t* __restrict__ RK,
-                                                 uint32_t* __restrict__ SD, uint32_t* __restrict__ SA) {
+                                                 uint32_t* __restrict__ SD, uint32_t* __restrict__ SA,
+                                                 uint32_t pbase) {
   const uint4 h = TB[blockIdx.x];
   const uint32_t n = h.y + h.z + h.w;
   const uint32_t* TBw = reinterpret_cast<const uint32_t*>(TB);
@@ -553,9 +570,13 @@ __global__ void __launch_bounds__(256) k_tt_succ(const uint4* __restrict__ TB, c
     uint32_t sd, sa;
     if (i < h.y) {
       const uint32_t bm = __ldg(TT + k);
-      const uint32_t nb = __ldg(TBw + 4 * (bm >> 15));
-      sd = nb + __ldg(ltd + bm);
-      sa = nb + __ldg(lta + bm);
+      if (pbase && bm >= pbase) {
+        sd = sa = kFinal | kPortal | (bm - pbase);  // resolved across ranks (slab_resolve)
+      } else {
+        const uint32_t nb = __ldg(TBw + 4 * (bm >> 15));
+        sd = nb + __ldg(ltd + bm);
+        sa = nb + __ldg(lta + bm);
+      }
     } else {
       // a maximum is only reached by descending-manifold chains, a minimum
       // only by ascending ones
@@ -618,10 +639,10 @@ __global__ void k_list_pairs(const uint32_t* __restrict__ list, const uint32_t* 
 
 // sorted pairs -> ascending list and the rank of every extremum table entry
 __global__ void k_rank_lists(const uint64_t* __restrict__ keys, const uint64_t* __restrict__ vals, int64_t n,
-                             uint32_t* __restrict__ list, uint32_t* __restrict__ RK) {
+                             uint32_t* __restrict__ list, uint32_t* __restrict__ RK, uint32_t id0) {
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i < n) {
-    list[i] = uint32_t(keys[i]);
+    list[i] = uint32_t(keys[i]) + id0;  // id0: the slab's first vertex id (z-slab lists are global)
     RK[vals[i]] = uint32_t(i);
   }
 }
@@ -652,7 +673,7 @@ __global__ void __launch_bounds__(kWB) k_bitmap_ids(const uint32_t* __restrict__
                                                     const uint64_t* __restrict__ boff, uint32_t nmax,
                                                     const uint32_t* __restrict__ maxs,
                                                     const uint32_t* __restrict__ mins, uint32_t* __restrict__ prefix,
-                                                    uint64_t* __restrict__ keys) {
+                                                    uint64_t* __restrict__ keys, bool rank_keys = false) {
   __shared__ uint32_t ws[kWB / 32];
   const uint64_t wi = uint64_t(blockIdx.x) * kWB + threadIdx.x;
   const uint32_t word = wi < nw ? bm[wi] : 0u;
@@ -686,7 +707,8 @@ __global__ void __launch_bounds__(kWB) k_bitmap_ids(const uint32_t* __restrict__
     m &= m - 1;
     const uint64_t key = wi * 32 + b;
     const uint32_t ra = uint32_t(key / nmax), rd = uint32_t(key - uint64_t(ra) * nmax);
-    keys[id++] = (uint64_t(__ldg(mins + ra)) << 32) | __ldg(maxs + rd);
+    // region key in vertex ids, or (z-slab) the rank pair
+    keys[id++] = rank_keys ? (uint64_t(ra) << 32 | rd) : (uint64_t(__ldg(mins + ra)) << 32) | __ldg(maxs + rd);
   }
 }
 
@@ -1368,6 +1390,7 @@ __device__ __forceinline__ uint32_t token_id(uint32_t k, const uint32_t* __restr
 struct EmitArgs {
   uint32_t X, Y, Z, nxc;
   uint64_t nchunks, total;
+  uint64_t cube0;        // global id of cube 0 (z-slab pipeline; 0 otherwise)
   const uint64_t* off;   // exclusive chunk offsets
   const uint8_t* cls;
   const uint32_t* ids;   // ms (dense MS ids)
@@ -1545,7 +1568,7 @@ __global__ void __launch_bounds__(256) k_emit_chunks(const EmitArgs a) {
           la = __ldg(a.ids + (vs + corner_off((r >> 16) & 0xffu)));
           lb = __ldg(a.ids + (vs + corner_off(r >> 24)));
         }
-        const uint64_t cr64 = ((6ull * uint64_t(q0 + uint32_t(src)) + t) << 6) | uint64_t(rowi);
+        const uint64_t cr64 = ((6ull * (a.cube0 + uint64_t(q0 + uint32_t(src))) + t) << 6) | uint64_t(rowi);
         *reinterpret_cast<uint4*>(a.out + base + j) =
             make_uint4(uint32_t(cr64), uint32_t(cr64 >> 32), min(la, lb), max(la, lb));
       }
@@ -1583,6 +1606,113 @@ __global__ void __launch_bounds__(256) k_ms_ids(uint32_t* __restrict__ ms, uint6
   }
 }
 
+// ------------------------------------------------- z-slab pipeline (e) --
+// A rank's slab is a grid of its own (owned layers, local vertex ids) whose
+// field buffer carries the neighbours' boundary layers as halos; chains that
+// leave the slab end at portal entries (k_tt_succ), resolved across ranks
+// through the gathered boundary layers (k_slab_patch).
+
+// Resolved value of the owned first (side 0) / last (side 1) layer vertex
+// (x, y): [desc first, desc last, asc first, asc last] x XY words, each
+// kFinal | slab-local rank, or kFinal | kPortal | portal index.
+__global__ void k_slab_boundary(const FDims d, const uint4* __restrict__ TB, const uint16_t* __restrict__ ltd,
+                                const uint16_t* __restrict__ lta, const uint32_t* __restrict__ SD,
+                                const uint32_t* __restrict__ SA, uint32_t* __restrict__ out) {
+  const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= 2ull * d.XY) return;
+  const uint32_t side = uint32_t(i / d.XY), xy = uint32_t(i - uint64_t(side) * d.XY);
+  const uint32_t x = xy % d.X, y = xy / d.X, z = side ? d.Z - 1 : 0;
+  const uint32_t bt = (x >> 5) + d.tx * ((y >> 5) + d.ty * (z >> 5));
+  const uint32_t bm = bt << 15 | (x & 31) | (y & 31) << 5 | (z & 31) << 10;
+  const uint32_t base = __ldg(reinterpret_cast<const uint32_t*>(TB) + 4 * bt);
+  out[i] = SD[base + __ldg(ltd + bm)];
+  out[2ull * d.XY + i] = SA[base + __ldg(lta + bm)];
+}
+
+// The final value of portal p of rank r: follow it through the gathered
+// boundary layers G[world][4][XY] (steepest chains are strictly monotone, so
+// the walk ends) and offset the extremum's slab rank by its rank's prefix.
+__device__ uint32_t slab_chase(const uint32_t* __restrict__ G, uint32_t dir, int r, uint32_t p, uint32_t XY,
+                               int world, const uint32_t* __restrict__ pre, int* __restrict__ err) {
+#pragma unroll 1
+  for (int it = 0; it < (1 << 24); ++it) {
+    const uint32_t side = p >= XY ? 1u : 0u, xy = p - side * XY;
+    const int r2 = side ? r + 1 : r - 1;  // the rank owning the halo layer
+    if (r2 < 0 || r2 >= world) break;
+    // its first layer when the chain went up, its last when it went down
+    const uint32_t v = __ldg(G + (uint64_t(r2) * 4 + dir * 2 + (side ? 0u : 1u)) * XY + xy);
+    if (!(v & kFinal)) break;
+    if (!(v & kPortal)) return kFinal | ((v & ~kFinal) + __ldg(pre + r2));
+    r = r2;
+    p = v & ~(kFinal | kPortal);
+  }
+  atomicExch(err, 1);
+  return kFinal;
+}
+
+// Every table entry of this rank -> kFinal | global extremum rank.
+__global__ void k_slab_patch(uint64_t nt, uint32_t* __restrict__ SD, uint32_t* __restrict__ SA,
+                             const uint32_t* __restrict__ G, int world, int rank, uint32_t XY,
+                             const uint32_t* __restrict__ pre_max, const uint32_t* __restrict__ pre_min,
+                             int* __restrict__ err) {
+  const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= nt) return;
+  uint32_t* S[2] = {SD, SA};
+  const uint32_t* pre[2] = {pre_max, pre_min};
+#pragma unroll
+  for (uint32_t dir = 0; dir < 2; ++dir) {
+    uint32_t v = S[dir][i];
+    if (!(v & kFinal)) {
+      atomicExch(err, 2);  // the slab forest had not converged
+      continue;
+    }
+    if (v & kPortal)
+      v = slab_chase(G, dir, rank, v & ~(kFinal | kPortal), XY, world, pre[dir], err);
+    else
+      v = kFinal | ((v & ~kFinal) + __ldg(pre[dir] + rank));
+    S[dir][i] = v;
+  }
+}
+
+// Dense region bitmap from gathered rank-pair keys (rank_min << 32 | rank_max).
+__global__ void k_set_bits(const uint64_t* __restrict__ keys, int64_t n, uint32_t* __restrict__ bitmap,
+                           uint32_t nmax) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint64_t k = keys[i];
+  const uint64_t b = (k >> 32) * uint64_t(nmax) + uint32_t(k);
+  const uint32_t bit = 1u << (b & 31);
+  uint32_t* w = bitmap + (b >> 5);
+  if (!(*w & bit)) atomicOr(w, bit);
+}
+
+// sorted keys -> 1 at the first occurrence of each value
+__global__ void k_first_flags(const uint64_t* __restrict__ k, int64_t n, uint64_t* __restrict__ flags) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) flags[i] = (i == 0 || k[i] != k[i - 1]) ? 1u : 0u;
+}
+__global__ void k_compact_first(const uint64_t* __restrict__ k, int64_t n, const uint64_t* __restrict__ pos,
+                                uint64_t* __restrict__ out) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n && (i == 0 || k[i] != k[i - 1])) out[pos[i]] = k[i];
+}
+
+// hash mode: every occupied slot of the slab's region set -> its position in
+// the global sorted unique keys
+__global__ void k_slot_ids(const unsigned long long* __restrict__ fset, uint64_t fcap,
+                           const uint64_t* __restrict__ ukeys, int64_t R, uint32_t* __restrict__ slot_id) {
+  const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= fcap) return;
+  const unsigned long long k = fset[i];
+  if (k == kEmpty) return;
+  int64_t lo = 0, hi = R;
+  while (lo < hi) {
+    const int64_t m = (lo + hi) >> 1;
+    if (__ldg(ukeys + m) < k) lo = m + 1; else hi = m;
+  }
+  slot_id[i] = uint32_t(lo);
+}
+
 std::atomic<bool> g_consts_ready[64] = {};
 std::mutex g_consts_mu;
 
@@ -1611,27 +1741,32 @@ bool fused_supported(const Grid& g) {
   return g.n < (int64_t(1) << 32) - 1 && bricks * TN <= (int64_t(1) << 32);
 }
 
-FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* desc, uint32_t* asc, uint32_t* ms) {
-  FusedOut o{};
-  for (auto& s : c.stats) s = 0;
+// One-time per device: kernel attributes, recipe tables, marching tables.
+static void ensure_consts(Ctx& c) {
   if (c.device >= 0 && c.device < 64 && !g_consts_ready[c.device].load(std::memory_order_acquire)) {
     // one upload per device even when several host threads arrive together
     std::lock_guard<std::mutex> lock(g_consts_mu);
     if (!g_consts_ready[c.device].load(std::memory_order_acquire)) {
-    CK(cudaFuncSetAttribute(k_tile_segment<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kASmem));
-    CK(cudaFuncSetAttribute(k_tile_segment<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kASmem));
-    // on the context stream (a non-blocking stream does not wait on the legacy one)
-    CK(cudaMemcpyToSymbolAsync(c_mrows, kTetRowsPacked, sizeof(kTetRowsPacked), 0, cudaMemcpyHostToDevice,
-                               c.stream));
-    CK(cudaMemcpyToSymbolAsync(c_mcases, kTetCasePacked, sizeof(kTetCasePacked), 0, cudaMemcpyHostToDevice,
-                               c.stream));
-    k_march_init<<<1, 128, 0, c.stream>>>();
-    CK_LAUNCH("k_march_init");
-    c.sync();  // other contexts (other streams) may use the tables next
-    g_consts_ready[c.device].store(true, std::memory_order_release);
+      CK(cudaFuncSetAttribute(k_tile_segment<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kASmem));
+      CK(cudaFuncSetAttribute(k_tile_segment<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kASmem));
+      // on the context stream (a non-blocking stream does not wait on the legacy one)
+      CK(cudaMemcpyToSymbolAsync(c_mrows, kTetRowsPacked, sizeof(kTetRowsPacked), 0, cudaMemcpyHostToDevice,
+                                 c.stream));
+      CK(cudaMemcpyToSymbolAsync(c_mcases, kTetCasePacked, sizeof(kTetCasePacked), 0, cudaMemcpyHostToDevice,
+                                 c.stream));
+      k_march_init<<<1, 128, 0, c.stream>>>();
+      CK_LAUNCH("k_march_init");
+      c.sync();  // other contexts (other streams) may use the tables next
+      g_consts_ready[c.device].store(true, std::memory_order_release);
     }
   }
-  FDims d;
+}
+
+FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* desc, uint32_t* asc, uint32_t* ms) {
+  FusedOut o{};
+  for (auto& s : c.stats) s = 0;
+  ensure_consts(c);
+  FDims d{};
   d.X = uint32_t(g.X);
   d.Y = uint32_t(g.Y);
   d.Z = uint32_t(g.Z);
@@ -1640,6 +1775,9 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
   d.tx = uint32_t((g.X + TX - 1) / TX);
   d.ty = uint32_t((g.Y + TY - 1) / TY);
   d.tz = uint32_t((g.Z + TZ - 1) / TZ);
+  d.zf0 = 0;
+  d.zfn = d.Z;
+  d.pbase = 0;
   const uint64_t ntiles = uint64_t(d.tx) * d.ty * d.tz;
 
   // TMA descriptor of the field (3-D, float32, NaN out-of-bounds fill). The
@@ -1742,14 +1880,14 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
         while ((uint64_t(1) << bits) < uint64_t(g.n)) ++bits;
         radix_sort_pairs(c, kk, vv, k, bits);
       }
-      k_rank_lists<<<blocks_for(k, 256), 256, 0, c.stream>>>(kk, vv, k, list, RK);
+      k_rank_lists<<<blocks_for(k, 256), 256, 0, c.stream>>>(kk, vv, k, list, RK, 0u);
       CK_LAUNCH("k_rank_lists");
     }
     c.mark(2);
     // ---- B: terminal-table forest -> extremum rank of every table entry
     uint32_t* SD = c.get_t<uint32_t>(S_SD, nt);
     uint32_t* SA = c.get_t<uint32_t>(S_SA, nt);
-    k_tt_succ<<<unsigned(ntiles), 256, 0, c.stream>>>(TB, TT, ltd, lta, RK, SD, SA);
+    k_tt_succ<<<unsigned(ntiles), 256, 0, c.stream>>>(TB, TT, ltd, lta, RK, SD, SA, 0u);
     CK_LAUNCH("k_tt_succ");
     // Two sweeps are enqueued without waiting (they converge on smooth
     // fields); passes C and D follow speculatively and the convergence flag
@@ -1983,6 +2121,457 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
     o.keys = keys;
     return o;
     }
+  }
+}
+
+}  // namespace plmss_b200
+
+// ===================================================== z-slab pipeline (e) ==
+// The fused passes on one rank's slab (include/plmss_b200.h, stages 1-4).
+namespace plmss_b200 {
+namespace {
+
+FDims slab_dims(const SlabState& st) {
+  FDims d{};
+  const int64_t nz = st.z1 - st.z0;
+  d.X = uint32_t(st.g.X);
+  d.Y = uint32_t(st.g.Y);
+  d.Z = uint32_t(nz);
+  d.XY = d.X * d.Y;
+  d.n = uint32_t(st.g.X * st.g.Y * nz);
+  d.tx = uint32_t((st.g.X + TX - 1) / TX);
+  d.ty = uint32_t((st.g.Y + TY - 1) / TY);
+  d.tz = uint32_t((nz + TZ - 1) / TZ);
+  d.zf0 = -st.has_down;
+  d.zfn = uint32_t(nz + st.has_down + st.has_up);
+  d.pbase = uint32_t(uint64_t(d.tx) * d.ty * d.tz << 15);
+  return d;
+}
+
+bool encode_lt_maps(Ctx& c, uint64_t ntiles, uint16_t* ltd, uint16_t* lta, CUtensorMap* mld, CUtensorMap* mla) {
+  if (!c.use_tma || !tensor_map_encoder()) return false;
+  const cuuint64_t gdim[2] = {cuuint64_t(TX * TY), cuuint64_t(ntiles) * TZ};
+  const cuuint64_t gstride[1] = {cuuint64_t(TX * TY) * 2};
+  const cuuint32_t box[2] = {cuuint32_t(32 * kTokRows), cuuint32_t(TZ)};
+  const cuuint32_t estride[2] = {1, 1};
+  for (int k = 0; k < 2; ++k)
+    if (tensor_map_encoder()(k ? mla : mld, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, k ? lta : ltd, gdim, gstride, box,
+                             estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return false;
+  return true;
+}
+
+bool encode_tok_map(Ctx& c, uint32_t* ms, uint32_t X, uint32_t Y, uint32_t Z, CUtensorMap* m) {
+  if (!c.use_tma || !tensor_map_encoder() || (X % 4) != 0 || (reinterpret_cast<uintptr_t>(ms) & 15) != 0)
+    return false;
+  const cuuint64_t gdim[3] = {cuuint64_t(X), cuuint64_t(Y), cuuint64_t(Z)};
+  const cuuint64_t gstride[2] = {cuuint64_t(X) * 4, cuuint64_t(X) * cuuint64_t(Y) * 4};
+  const cuuint32_t box[3] = {cuuint32_t(TLW), cuuint32_t(RY + 1), cuuint32_t(kBatch + 1)};
+  const cuuint32_t estride[3] = {1, 1, 1};
+  return tensor_map_encoder()(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, ms, gdim, gstride, box, estride,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+void need_stage(const Ctx& c, int s, const char* what) {
+  if (c.slab.stage != s)
+    fail(PLMSS_ERR_LOGIC, std::string(what) + " called out of order (z-slab stage " + std::to_string(c.slab.stage) +
+                              " completed, " + std::to_string(s) + " required)");
+}
+
+}  // namespace
+
+// Stage 1: pass A on the slab's bricks, the extremum lists, the forest.
+void slab_segment(Ctx& c, const Grid& g, int64_t z0, int64_t z1, const float* field, plmss_slab_info* info) {
+  if (!fused_supported(g)) fail(PLMSS_ERR_INVALID_ARGUMENT, "grid outside the fused pipeline's envelope");
+  if (z0 < 0 || z1 > g.Z || z0 >= z1) fail(PLMSS_ERR_INVALID_ARGUMENT, "slab layers outside the grid");
+  if (z0 % TZ != 0 || (z1 % TZ != 0 && z1 != g.Z))
+    fail(PLMSS_ERR_INVALID_ARGUMENT, "slabs must be whole 32-layer brick layers (z0 % 32 == 0, z1 % 32 == 0 or z1 == Z)");
+  ensure_consts(c);
+  for (auto& s : c.stats) s = 0;
+  SlabState& st = c.slab;
+  st = SlabState{};
+  st.g = g;
+  st.z0 = z0;
+  st.z1 = z1;
+  st.has_down = z0 > 0;
+  st.has_up = z1 < g.Z;
+  const FDims d = slab_dims(st);
+  const uint64_t ntiles = uint64_t(d.tx) * d.ty * d.tz;
+  st.ntiles = ntiles;
+  if ((ntiles << 15) + 2 * uint64_t(d.XY) >= (uint64_t(1) << 32) || 2 * uint64_t(d.XY) >= (uint64_t(1) << 30))
+    fail(PLMSS_ERR_INVALID_ARGUMENT, "slab too large for u32 portal entries");
+
+  CUtensorMap tmap;
+  memset(&tmap, 0, sizeof tmap);
+  bool use_tma = (g.X % 4) == 0 && (reinterpret_cast<uintptr_t>(field) & 15) == 0 && c.use_tma;
+  if (use_tma) {
+    const EncodeFn encode = tensor_map_encoder();
+    const cuuint64_t gdim[3] = {cuuint64_t(g.X), cuuint64_t(g.Y), cuuint64_t(d.zfn)};
+    const cuuint64_t gstride[2] = {cuuint64_t(g.X) * 4, cuuint64_t(g.X) * cuuint64_t(g.Y) * 4};
+    const cuuint32_t box[3] = {HX, HY, HZ};
+    const cuuint32_t estride[3] = {1, 1, 1};
+    use_tma = encode && encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(field), gdim, gstride,
+                               box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NAN_REQUEST_ZERO_FMA) == CUDA_SUCCESS;
+  }
+  c.stats[4] = use_tma ? 1 : 0;
+  char* ctr_base = static_cast<char*>(c.get(S_FLAGS, 1024));
+  ACounters* ctr = reinterpret_cast<ACounters*>(ctr_base);
+  uint16_t* ltd = c.get_t<uint16_t>(S_LTD, ntiles * TN);
+  uint16_t* lta = c.get_t<uint16_t>(S_LTA, ntiles * TN);
+  uint4* TB = c.get_t<uint4>(S_TB, ntiles);
+  const uint64_t nloc = uint64_t(d.n);
+  uint32_t *maxima = nullptr, *minima = nullptr, *max_tt = nullptr, *min_tt = nullptr, *TT = nullptr;
+  ACounters h;
+  for (int attempt = 0;; ++attempt) {
+    const uint64_t ext_cap = c.fused_ext_cap ? c.fused_ext_cap : uint64_t(nloc / 4 + 1024);
+    maxima = c.get_t<uint32_t>(S_MAXIMA, ext_cap);
+    minima = c.get_t<uint32_t>(S_MINIMA, ext_cap);
+    max_tt = c.get_t<uint32_t>(S_RANK_MAX, ext_cap);
+    min_tt = c.get_t<uint32_t>(S_RANK_MIN, ext_cap);
+    const uint64_t tt_cap = c.fused_exit_cap ? c.fused_exit_cap : uint64_t(nloc / 4 + 1024);
+    TT = c.get_t<uint32_t>(S_TMP0, tt_cap);
+    CK(cudaMemsetAsync(ctr, 0, sizeof(ACounters), c.stream));
+    CK(cudaMemsetAsync(&ctr->bad, 0xff, 4, c.stream));
+    const unsigned grid = unsigned(std::min<uint64_t>(ntiles, uint64_t(c.sm_count)));
+    if (use_tma)
+      k_tile_segment<true><<<grid, A_THREADS, kASmem, c.stream>>>(tmap, field, d, maxima, minima, max_tt, min_tt,
+                                                                  ext_cap, TT, tt_cap, TB, ltd, lta, ctr);
+    else
+      k_tile_segment<false><<<grid, A_THREADS, kASmem, c.stream>>>(tmap, field, d, maxima, minima, max_tt, min_tt,
+                                                                   ext_cap, TT, tt_cap, TB, ltd, lta, ctr);
+    CK_LAUNCH("k_tile_segment");
+    CK(cudaMemcpyAsync(c.h_pinned, ctr, sizeof(ACounters), cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    memcpy(&h, c.h_pinned, sizeof h);
+    if (h.bad != 0xffffffffu)
+      fail(PLMSS_ERR_INVALID_ARGUMENT,
+           "non-finite scalar value at vertex " + std::to_string(uint64_t(h.bad) + uint64_t(z0) * d.XY));
+    bool retry = false;
+    if (h.n_tt > tt_cap) {
+      c.fused_exit_cap = h.n_tt + h.n_tt / 4 + 1024;
+      retry = true;
+    }
+    if (h.n_max > ext_cap || h.n_min > ext_cap) {
+      c.fused_ext_cap = std::max(h.n_max, h.n_min) + 1024;
+      retry = true;
+    }
+    if (!retry) break;
+    if (attempt > 6) fail(PLMSS_ERR_LOGIC, "z-slab pass A capacity retries exhausted");
+  }
+  if (h.n_max >= (1ull << 30) || h.n_min >= (1ull << 30))
+    fail(PLMSS_ERR_INVALID_ARGUMENT, "z-slab: more than 2^30 extrema in one slab");
+  c.stats[0] = int64_t(h.n_exit);
+  st.n_max_l = int64_t(h.n_max);
+  st.n_min_l = int64_t(h.n_min);
+  const uint64_t nt = h.n_tt;
+  st.nt = nt;
+  // extremum lists sorted by id (global ids: + z0 * XY), rank of every extremum entry
+  uint32_t* RK = c.get_t<uint32_t>(S_RK, nt);
+  for (int dir = 0; dir < 2; ++dir) {
+    uint32_t* list = dir ? minima : maxima;
+    const uint32_t* ltt = dir ? min_tt : max_tt;
+    const int64_t k = dir ? st.n_min_l : st.n_max_l;
+    if (k < 1) continue;
+    uint64_t* kk = c.get_t<uint64_t>(S_SORT_A, k);
+    uint64_t* vv = c.get_t<uint64_t>(S_SORT_B, k);
+    k_list_pairs<<<blocks_for(k, 256), 256, 0, c.stream>>>(list, ltt, k, kk, vv);
+    CK_LAUNCH("k_list_pairs");
+    if (k > 1) {
+      int bits = 0;
+      while ((uint64_t(1) << bits) < nloc) ++bits;
+      radix_sort_pairs(c, kk, vv, k, bits);
+    }
+    k_rank_lists<<<blocks_for(k, 256), 256, 0, c.stream>>>(kk, vv, k, list, RK, uint32_t(uint64_t(z0) * d.XY));
+    CK_LAUNCH("k_rank_lists");
+  }
+  // the forest inside the slab, to its fixpoint (portals are roots)
+  uint32_t* SD = c.get_t<uint32_t>(S_SD, nt);
+  uint32_t* SA = c.get_t<uint32_t>(S_SA, nt);
+  k_tt_succ<<<unsigned(ntiles), 256, 0, c.stream>>>(TB, TT, ltd, lta, RK, SD, SA, d.pbase);
+  CK_LAUNCH("k_tt_succ");
+  int* jflag = reinterpret_cast<int*>(ctr_base + 192);
+  for (;;) {
+    CK(cudaMemsetAsync(jflag, 0, 4, c.stream));
+    k_tt_jump<<<blocks_for(int64_t((nt + 1) / 2), 256), 256, 0, c.stream>>>(nt, SD, SA, jflag);
+    CK_LAUNCH("k_tt_jump");
+    ++st.sweeps;
+    CK(cudaMemcpyAsync(reinterpret_cast<char*>(c.h_pinned) + 64, jflag, 4, cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    if (*reinterpret_cast<int*>(reinterpret_cast<char*>(c.h_pinned) + 64) == 0) break;
+    if (st.sweeps > 64) fail(PLMSS_ERR_LOGIC, "z-slab terminal forest did not converge");
+  }
+  uint32_t* bnd = c.get_t<uint32_t>(S_SLAB_BND, 4 * uint64_t(d.XY));
+  k_slab_boundary<<<blocks_for(2 * int64_t(d.XY), 256), 256, 0, c.stream>>>(d, TB, ltd, lta, SD, SA, bnd);
+  CK_LAUNCH("k_slab_boundary");
+  c.sync();
+  st.stage = 1;
+  if (info) {
+    *info = plmss_slab_info{};
+    info->n_maxima = st.n_max_l;
+    info->n_minima = st.n_min_l;
+    info->d_maxima = maxima;
+    info->d_minima = minima;
+    info->d_boundary = bnd;
+    info->sweeps = st.sweeps;
+  }
+}
+
+// Stage 2: portals -> global ranks; desc / asc; region tokens; the slab's pairs.
+void slab_resolve(Ctx& c, const uint32_t* G, int world, int rank, const int64_t* max_counts,
+                  const int64_t* min_counts, const uint32_t* maxs_g, const uint32_t* mins_g, uint32_t* desc,
+                  uint32_t* asc, uint32_t* ms, plmss_slab_info* info) {
+  need_stage(c, 1, "slab_resolve");
+  SlabState& st = c.slab;
+  if (world < 1 || rank < 0 || rank >= world || !G || !max_counts || !min_counts || !desc || !asc || !ms)
+    fail(PLMSS_ERR_INVALID_ARGUMENT, "slab_resolve: bad arguments");
+  const FDims d = slab_dims(st);
+  // rank prefixes of the extremum counts (rank order == vertex id order)
+  std::vector<uint32_t> pre(2 * size_t(world) + 2, 0);
+  int64_t smax = 0, smin = 0;
+  for (int r = 0; r < world; ++r) {
+    pre[r] = uint32_t(smax);
+    pre[world + 1 + r] = uint32_t(smin);
+    smax += max_counts[r];
+    smin += min_counts[r];
+  }
+  if (max_counts[rank] != st.n_max_l || min_counts[rank] != st.n_min_l)
+    fail(PLMSS_ERR_INVALID_ARGUMENT, "slab_resolve: this rank's counts differ from slab_segment's");
+  if (smax >= (int64_t(1) << 30) || smin >= (int64_t(1) << 30))
+    fail(PLMSS_ERR_INVALID_ARGUMENT, "z-slab: more than 2^30 extrema");
+  st.n_max_g = smax;
+  st.n_min_g = smin;
+  st.maxs_g = maxs_g;
+  st.mins_g = mins_g;
+  st.desc = desc;
+  st.asc = asc;
+  st.ms = ms;
+  uint32_t* d_pre = c.get_t<uint32_t>(S_SCAN_C, pre.size());
+  CK(cudaMemcpyAsync(d_pre, pre.data(), pre.size() * 4, cudaMemcpyHostToDevice, c.stream));
+  char* ctr_base = static_cast<char*>(c.get(S_FLAGS, 1024));
+  int* err = reinterpret_cast<int*>(ctr_base + 256);
+  int* flag = reinterpret_cast<int*>(ctr_base + 128);
+  CK(cudaMemsetAsync(err, 0, 4, c.stream));
+  uint32_t* SD = static_cast<uint32_t*>(c.buf[S_SD]);
+  uint32_t* SA = static_cast<uint32_t*>(c.buf[S_SA]);
+  k_slab_patch<<<blocks_for(int64_t(st.nt), 256), 256, 0, c.stream>>>(st.nt, SD, SA, G, world, rank, d.XY, d_pre,
+                                                                     d_pre + world + 1, err);
+  CK_LAUNCH("k_slab_patch");
+  // tokens
+  BrickArgs ba{};
+  ba.d = d;
+  ba.nxc = uint32_t((st.g.X - 1 + 31) / 32);
+  ba.TB = static_cast<const uint4*>(c.buf[S_TB]);
+  ba.ltd = static_cast<const uint16_t*>(c.buf[S_LTD]);
+  ba.lta = static_cast<const uint16_t*>(c.buf[S_LTA]);
+  ba.FD = SD;
+  ba.FA = SA;
+  ba.maxs = maxs_g;
+  ba.mins = mins_g;
+  ba.nmax = uint32_t(smax);
+  ba.desc = desc;
+  ba.asc = asc;
+  ba.ms = ms;
+  ba.overflow = flag;
+  CUtensorMap mld, mla;
+  const bool lt_tma = encode_lt_maps(c, st.ntiles, static_cast<uint16_t*>(c.buf[S_LTD]),
+                                     static_cast<uint16_t*>(c.buf[S_LTA]), &mld, &mla);
+  const unsigned tgrid = unsigned((TY / kTokRows) * st.ntiles);
+  const uint64_t nbits = uint64_t(smax) * uint64_t(smin);
+  st.dense = nbits < (uint64_t(1) << 32) && c.combine_path != 2;
+  if (st.dense) {
+    const uint64_t nw = (nbits + 31) / 32;
+    uint32_t* bitmap = c.get_t<uint32_t>(S_BITMAP, nw);
+    CK(cudaMemsetAsync(bitmap, 0, nw * 4, c.stream));
+    ba.bitmap = bitmap;
+    if (lt_tma)
+      k_tokens_tma<true><<<tgrid, 32 * kTokRows, 0, c.stream>>>(mld, mla, ba);
+    else
+      k_tokens<true><<<tgrid, 32 * kTokRows, 0, c.stream>>>(ba);
+    CK_LAUNCH("k_tokens");
+    // the slab's pairs, as rank keys in key order
+    const int64_t nb = int64_t((nw + kWB - 1) / kWB);
+    uint64_t* bsum = c.get_t<uint64_t>(S_HASH_V, nb);
+    k_bitmap_count<<<unsigned(nb), 256, 0, c.stream>>>(bitmap, nw, bsum);
+    CK_LAUNCH("k_bitmap_count");
+    st.n_keys = int64_t(exclusive_scan_u64(c, bsum, nb, true));
+    st.keys = c.get_t<uint64_t>(S_KEYS, st.n_keys);
+    uint32_t* prefix = c.get_t<uint32_t>(S_HASH_K, nw);
+    k_bitmap_ids<<<unsigned(nb), kWB, 0, c.stream>>>(bitmap, nw, bsum, ba.nmax, maxs_g, mins_g, prefix, st.keys,
+                                                      true);
+    CK_LAUNCH("k_bitmap_ids");
+  } else {
+    uint64_t fcap = 1024;
+    {
+      const uint64_t want = c.fused_pair_hint ? c.fused_pair_hint * 2 : uint64_t(1) << 20;
+      while (fcap < want) fcap <<= 1;
+    }
+    unsigned long long* fset = nullptr;
+    for (int tries = 0;; ++tries) {
+      if (fcap > (uint64_t(1) << 32)) fail(PLMSS_ERR_LOGIC, "region set larger than 2^32 slots");
+      fset = c.get_t<unsigned long long>(S_HASH_V, fcap);
+      CK(cudaMemsetAsync(fset, 0xff, fcap * 8, c.stream));
+      CK(cudaMemsetAsync(flag, 0, 4, c.stream));
+      ba.fset = fset;
+      ba.fmask = fcap - 1;
+      if (lt_tma)
+        k_tokens_tma<false><<<tgrid, 32 * kTokRows, 0, c.stream>>>(mld, mla, ba);
+      else
+        k_tokens<false><<<tgrid, 32 * kTokRows, 0, c.stream>>>(ba);
+      CK_LAUNCH("k_tokens");
+      CK(cudaMemcpyAsync(c.h_pinned, flag, 4, cudaMemcpyDeviceToHost, c.stream));
+      c.sync();
+      if (*reinterpret_cast<int*>(c.h_pinned) == 0) break;
+      if (fcap >= 4 * uint64_t(d.n) || tries > 8) fail(PLMSS_ERR_LOGIC, "region set overflow");
+      fcap <<= 2;
+    }
+    st.fcap = fcap;
+    const int64_t fb = int64_t((fcap + kCTile - 1) / kCTile);
+    uint64_t* fcounts = c.get_t<uint64_t>(S_TMP2, fb);
+    k_count_occ<<<unsigned(fb), kCThreads, 0, c.stream>>>(fset, fcap, fcounts);
+    CK_LAUNCH("k_count_occ");
+    st.n_keys = int64_t(exclusive_scan_u64(c, fcounts, fb, true));
+    c.fused_pair_hint = uint64_t(st.n_keys);
+    st.keys = c.get_t<uint64_t>(S_KEYS, st.n_keys);
+    k_write_occ<<<unsigned(fb), kCThreads, 0, c.stream>>>(fset, fcap, fcounts, st.keys, nullptr);
+    CK_LAUNCH("k_write_occ");
+  }
+  CK(cudaMemcpyAsync(c.h_pinned, err, 4, cudaMemcpyDeviceToHost, c.stream));
+  c.sync();
+  const int e = *reinterpret_cast<int*>(c.h_pinned);
+  if (e) fail(PLMSS_ERR_LOGIC, e == 2 ? "z-slab forest entry unresolved" : "z-slab portal chain broken");
+  st.stage = 2;
+  if (info) {
+    info->n_maxima = smax;
+    info->n_minima = smin;
+    info->n_keys = st.n_keys;
+    info->d_keys = st.keys;
+    info->dense = st.dense ? 1 : 0;
+  }
+}
+
+// Stage 3: the gathered pairs -> global dense ids (combine_ms order) in ms.
+void slab_ids(Ctx& c, const uint64_t* keys_all, int64_t n_keys_all, plmss_slab_info* info) {
+  need_stage(c, 2, "slab_ids");
+  SlabState& st = c.slab;
+  if (n_keys_all < 0 || (n_keys_all > 0 && !keys_all)) fail(PLMSS_ERR_INVALID_ARGUMENT, "slab_ids: bad keys");
+  const FDims d = slab_dims(st);
+  const uint64_t nown = uint64_t(d.n);
+  const unsigned mgrid = unsigned((nown + 1023) / 1024);
+  if (st.dense) {
+    const uint64_t nbits = uint64_t(st.n_max_g) * uint64_t(st.n_min_g);
+    const uint64_t nw = (nbits + 31) / 32;
+    uint32_t* bitmap = static_cast<uint32_t*>(c.buf[S_BITMAP]);  // holds this slab's pairs already
+    if (n_keys_all)
+      k_set_bits<<<blocks_for(n_keys_all, 256), 256, 0, c.stream>>>(keys_all, n_keys_all, bitmap,
+                                                                     uint32_t(st.n_max_g));
+    CK_LAUNCH("k_set_bits");
+    const int64_t nb = int64_t((nw + kWB - 1) / kWB);
+    uint64_t* bsum = c.get_t<uint64_t>(S_HASH_V, nb);
+    k_bitmap_count<<<unsigned(nb), 256, 0, c.stream>>>(bitmap, nw, bsum);
+    CK_LAUNCH("k_bitmap_count");
+    st.R = int64_t(exclusive_scan_u64(c, bsum, nb, true));
+    st.keys = c.get_t<uint64_t>(S_KEYS, st.R);
+    uint32_t* prefix = c.get_t<uint32_t>(S_HASH_K, nw);
+    k_bitmap_ids<<<unsigned(nb), kWB, 0, c.stream>>>(bitmap, nw, bsum, uint32_t(st.n_max_g), st.maxs_g, st.mins_g,
+                                                      prefix, st.keys, false);
+    CK_LAUNCH("k_bitmap_ids");
+    k_ms_ids<true><<<mgrid, 256, 0, c.stream>>>(st.ms, nown, bitmap, prefix, nullptr);
+    CK_LAUNCH("k_ms_ids");
+  } else {
+    // sort + unique of the gathered rank pairs
+    const int64_t n = std::max<int64_t>(n_keys_all, 1);
+    uint64_t* kk = c.get_t<uint64_t>(S_SORT_A, n);
+    uint64_t* vv = c.get_t<uint64_t>(S_SORT_C, n);
+    if (n_keys_all) CK(cudaMemcpyAsync(kk, keys_all, n_keys_all * 8, cudaMemcpyDeviceToDevice, c.stream));
+    int kb = 32;
+    while ((uint64_t(1) << (kb - 32)) < uint64_t(std::max<int64_t>(st.n_min_g, 1))) ++kb;
+    if (n_keys_all > 1) radix_sort_pairs(c, kk, vv, n_keys_all, kb);
+    uint64_t* pos = c.get_t<uint64_t>(S_SORT_D, n);
+    k_first_flags<<<blocks_for(n, 256), 256, 0, c.stream>>>(kk, n_keys_all, pos);
+    CK_LAUNCH("k_first_flags");
+    st.R = n_keys_all ? int64_t(exclusive_scan_u64(c, pos, n_keys_all, true)) : 0;
+    st.keys = c.get_t<uint64_t>(S_KEYS, std::max<int64_t>(st.R, 1));
+    k_compact_first<<<blocks_for(n, 256), 256, 0, c.stream>>>(kk, n_keys_all, pos, st.keys);
+    CK_LAUNCH("k_compact_first");
+    uint32_t* slot_id = c.get_t<uint32_t>(S_BITMAP, st.fcap);
+    k_slot_ids<<<blocks_for(int64_t(st.fcap), 256), 256, 0, c.stream>>>(
+        static_cast<const unsigned long long*>(c.buf[S_HASH_V]), st.fcap, st.keys, st.R, slot_id);
+    CK_LAUNCH("k_slot_ids");
+    k_ms_ids<false><<<mgrid, 256, 0, c.stream>>>(st.ms, nown, nullptr, nullptr, slot_id);
+    CK_LAUNCH("k_ms_ids");
+    if (st.R) k_keys_to_gid<<<blocks_for(st.R, 256), 256, 0, c.stream>>>(st.keys, st.R, st.maxs_g, st.mins_g);
+    CK_LAUNCH("k_keys_to_gid");
+  }
+  c.sync();
+  st.stage = 3;
+  if (info) {
+    info->n_regions = st.R;
+    info->d_region_keys = st.keys;
+  }
+}
+
+// Stage 4: separator records of the owned cube layers (+ the layer shared
+// with the next rank), global cell ids.
+void slab_emit(Ctx& c, plmss_slab_info* info) {
+  need_stage(c, 3, "slab_emit");
+  SlabState& st = c.slab;
+  FDims d = slab_dims(st);
+  const uint32_t Zc = d.Z + uint32_t(st.has_up);  // vertex layers in ms
+  d.Z = Zc;
+  const uint64_t ncl = Zc - 1;                    // cube layers
+  const uint32_t nxc = uint32_t((st.g.X - 1 + 31) / 32);
+  const uint64_t nchunks = uint64_t(nxc) * uint64_t(st.g.Y - 1) * ncl;
+  uint64_t total = 0;
+  plmss_tri* tris = nullptr;
+  if (nchunks) {
+    BrickArgs ba{};
+    ba.d = d;
+    ba.nxc = nxc;
+    uint64_t* chunk = c.get_t<uint64_t>(S_TMP1, nchunks);
+    ba.chunk = chunk;
+    ba.cls = c.get_t<uint8_t>(S_MASK, uint64_t(st.g.X - 1) * uint64_t(st.g.Y - 1) * ncl);
+    ba.ms = st.ms;
+    const unsigned cgrid = unsigned((TY / RY) * st.ntiles);
+    CUtensorMap mtok;
+    if (encode_tok_map(c, st.ms, d.X, d.Y, Zc, &mtok))
+      k_brick_tma<<<cgrid, B_THREADS, 0, c.stream>>>(mtok, ba);
+    else
+      k_brick<<<cgrid, B_THREADS, 0, c.stream>>>(ba);
+    CK_LAUNCH("k_brick");
+    total = exclusive_scan_u64(c, chunk, int64_t(nchunks), true);
+    tris = c.get_t<plmss_tri>(S_TRIS, total ? total : 1);
+    if (total) {
+      EmitArgs ea{};
+      ea.X = d.X;
+      ea.Y = d.Y;
+      ea.Z = Zc;
+      ea.nxc = nxc;
+      ea.nchunks = nchunks;
+      ea.total = total;
+      ea.cube0 = uint64_t(st.z0) * uint64_t(st.g.X - 1) * uint64_t(st.g.Y - 1);
+      ea.off = chunk;
+      ea.cls = ba.cls;
+      ea.ids = st.ms;
+      ea.out = tris;
+      const uint64_t nrows = uint64_t(st.g.Y - 1) * ncl;
+      const unsigned egrid = unsigned(std::min<uint64_t>((nrows + 7) / 8, uint64_t(c.sm_count) * 256));
+      k_emit_chunks<<<egrid, 256, 0, c.stream>>>(ea);
+      CK_LAUNCH("k_emit_chunks");
+    }
+  } else {
+    tris = c.get_t<plmss_tri>(S_TRIS, 1);
+  }
+  c.sync();
+  st.n_tris = int64_t(total);
+  st.tris = tris;
+  st.stage = 4;
+  if (info) {
+    info->n_tris = st.n_tris;
+    info->d_tris = tris;
   }
 }
 

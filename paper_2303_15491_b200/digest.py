@@ -53,6 +53,13 @@ class ChunkedSha256:
             self._pending += mv[full:]
         return self
 
+    def drain(self, keep_blocks: int = 64) -> "ChunkedSha256":
+        """Wait for all but the last keep_blocks block hashes (bounds the host
+        memory held by pending blocks when streaming large arrays)."""
+        for f in self._futs[:-keep_blocks] if keep_blocks else self._futs:
+            f.result()
+        return self
+
     def hexdigest(self) -> str:
         if self._pending:
             self._futs.append(_POOL.submit(_h, bytes(self._pending)))
@@ -74,6 +81,5 @@ def digest_device(t, piece_bytes: int = 1 << 30) -> str:
     flat = t.reshape(-1).view(__import__("torch").uint8)
     for i in range(0, flat.numel(), piece_bytes):
         h.update(flat[i:i + piece_bytes].cpu().numpy())
-        for f in h._futs[:-4 * (piece_bytes // BLOCK)]:  # bound host memory
-            f.result()
+        h.drain(4 * max(piece_bytes // BLOCK, 1))  # bound host memory
     return h.hexdigest()

@@ -1,228 +1,319 @@
-"""Z-slab decomposition of the full Morse-Smale segmentation over ranks.
+"""Z-slab decomposition of the full Morse-Smale segmentation over ranks
+(SURVEY.md §8(e)): one process per GPU, torch.distributed over NCCL for the
+exchanges, the fused brick pipeline on every slab (include/plmss_b200.h,
+plmss_b200_slab_*).
 
-One process per GPU (torch.distributed, NCCL on B200 / gloo on CPU). Rank r
-owns the z-layers [z0, z1) = [Z*r/P, Z*(r+1)/P) — whole layers, so rank order
-is the reference's global vertex and cell order. Exchange
-steps, each one collective:
+Rank r owns whole 32-layer brick layers [z0, z1) (slab_bounds: the even split
+of parallel.hpp:27-29 applied to brick layers), so rank order is the
+reference's global vertex and cell order. One step:
 
-1. field halo: the neighbours' boundary layers (one X*Y layer each way,
-   point-to-point);
-2. slab segmentation on the device with the halo layers as terminals
-   (plmss_b200_segment_slab): every owned label is then a root of the slab or
-   a halo vertex;
-3. boundary graph: all_gather of every rank's two boundary layers of labels;
-   every rank resolves the (acyclic: strictly monotone chains) boundary graph
-   by pointer jumping and fixes its halo-pointing labels — one exchange, no
-   iteration across ranks;
-4. extrema: all_gather of counts and the per-rank sorted lists (rank order is
-   id order);
-5. Morse-Smale ids: all_gather of each rank's sorted unique (asc, desc) keys,
-   global sorted merge -> identical dense ids everywhere (combine_ms order);
-6. marching: the next rank's first layer of ids (point-to-point), local
-   separator records for the owned cube layers, global cell ids, and base
-   offsets from an all_gather of the per-rank counts.
+0. field halo: the neighbours' boundary layers of f (point-to-point, into
+   the slab buffer's halo layers);
+1. slab_segment (device): pass A on the slab's bricks with the halo layers as
+   real data, the sorted extremum lists, the terminal forest inside the slab;
+   a chain that leaves the slab ends at a portal (the halo vertex it enters);
+   -> all_gather: extremum counts, extremum lists, boundary layers (the
+   resolved value of every vertex of the first / last owned layer);
+2. slab_resolve (device): every portal followed through the gathered boundary
+   layers to its extremum (chains are strictly monotone, so one exchange
+   suffices: no iteration across ranks), desc / asc, region tokens, the
+   slab's distinct (rank_min, rank_max) pairs;
+   -> all_gather of the pairs;
+3. slab_ids (device): global dense MS ids in the combine_ms order
+   (segmentation.cpp:170-196) into ms;
+   -> the next rank's first layer of ids (point-to-point) into ms's extra layer;
+4. slab_emit (device): separator records of the owned cube layers with
+   global cell ids, reference order (marching.cpp:116-215); concatenated in
+   rank order they are the single-volume record list.
 
-The per-slab device work is delegated to a backend (``B200Backend`` below, the
-product path over the C-ABI). Everything here is plain tensor plumbing and
-runs unchanged on CPU tensors with gloo (tests/test_distributed.py).
+The step is written once, as a generator (``slab_step``) that yields its
+collectives. ``TorchComm`` runs it over torch.distributed (NCCL on B200,
+gloo on CPU); ``run_ranks_inprocess`` runs world ranks in one process,
+advancing every rank to its next collective and performing it in memory —
+ranks never wait on each other inside a kernel, so this reproduces the
+multi-GPU results exactly on one device (tests/test_gpu_parity.py). Backends:
+``B200SlabBackend`` (the product path, C-ABI); tests/test_distributed.py has a
+numpy backend with the same contract for the gloo tests.
 """
 from __future__ import annotations
 
+import ctypes as C
 from dataclasses import dataclass
+from typing import Optional
 
 import numpy as np
 import torch
 import torch.distributed as dist
 
+BRICK = 32
+FINAL, PORTAL = 0x80000000, 0x40000000  # boundary-layer value flags (fused.cu kFinal / kPortal)
+
 
 def slab_bounds(Z: int, world: int, rank: int):
-    """Owned z-layers of a rank (the even split of parallel.hpp:27-29)."""
-    return Z * rank // world, Z * (rank + 1) // world
+    """Owned z-layers [z0, z1) of a rank: brick layers split evenly
+    (parallel.hpp:27-29 on ceil(Z / 32) units), the last slab clipped to Z."""
+    nb = (Z + BRICK - 1) // BRICK
+    if world > nb:
+        raise ValueError(f"{world} ranks for {nb} brick layers: at most one rank per 32 z-layers")
+    b0, b1 = nb * rank // world, nb * (rank + 1) // world
+    return b0 * BRICK, min(b1 * BRICK, Z)
+
+
+def halo_bounds(Z: int, world: int, rank: int):
+    """Field layers a rank's slab buffer holds: [z0 - 1, z1 + 1) clipped."""
+    z0, z1 = slab_bounds(Z, world, rank)
+    return max(z0 - 1, 0), min(z1 + 1, Z)
 
 
 @dataclass
 class SlabResult:
     z0: int
     z1: int
-    desc: torch.Tensor        # int64 global extremum ids of the owned vertices
-    asc: torch.Tensor
-    ms: torch.Tensor          # int64 dense region ids of the owned vertices
-    maxima: torch.Tensor      # global, ascending (identical on every rank)
+    desc: torch.Tensor         # owned vertices: vertex id of the maximum (uint32 in int32 storage)
+    asc: torch.Tensor          # ... of the minimum
+    ms: torch.Tensor           # owned vertices: dense MS region id
+    maxima: torch.Tensor       # global sorted extremum lists (identical on every rank)
     minima: torch.Tensor
-    region_keys: torch.Tensor  # (R, 2) int64 (min id, max id), global
-    cells: torch.Tensor       # this rank's separator records, reference order
-    lo: torch.Tensor
-    hi: torch.Tensor
-    tri_base: int             # offset of this rank's records in the global list
+    region_keys: torch.Tensor  # global (asc << 32 | desc) per region, sorted (int64 storage)
+    tris: torch.Tensor         # this rank's separator records (T, 2) int64: [cell << 6 | row, lo | hi << 32]
+    tri_base: int              # offset of this rank's records in the global list
     tri_total: int
+    sweeps: int
 
 
-class B200Backend:
-    """Per-slab device work through libplmss_b200 (the product path)."""
+# ------------------------------------------------------------ the step -----
+def slab_step(backend, dims, rank: int, world: int, field_buf: torch.Tensor):
+    """One z-slab step as a generator of collectives (module docstring).
+    ``field_buf`` holds halo_bounds(Z, world, rank) layers with this rank's
+    owned layers filled; the halo layers are filled by step 0."""
+    X, Y, Z = (int(v) for v in dims)
+    XY = X * Y
+    z0, z1 = slab_bounds(Z, world, rank)
+    h0, h1 = halo_bounds(Z, world, rank)
+    lo = z0 - h0
+    f = field_buf.view(h1 - h0, XY)
+    # 0. field halo
+    yield ("exchange", f[lo], f[lo + z1 - z0 - 1], f[0] if lo else None, f[-1] if h1 > z1 else None)
+    # 1. the slab
+    s = backend.segment(dims, z0, z1, field_buf)
+    counts = yield ("allgather", torch.tensor([s["n_max"], s["n_min"]], dtype=torch.int64, device=f.device))
+    counts = counts.cpu().numpy()
+    maxima = yield ("allgather_var", s["maxima"], [int(c) for c in counts[:, 0]])
+    minima = yield ("allgather_var", s["minima"], [int(c) for c in counts[:, 1]])
+    G = yield ("allgather", s["boundary"])
+    # 2. portals, labels, the slab's region pairs
+    keys, nk = backend.resolve(G, world, rank, counts[:, 0].copy(), counts[:, 1].copy(), maxima, minima)
+    nks = yield ("allgather", torch.tensor([nk], dtype=torch.int64, device=f.device))
+    keys_all = yield ("allgather_var", keys, [int(c) for c in nks.cpu().numpy().reshape(-1)])
+    # 3. dense ids
+    region_keys = backend.ids(keys_all)
+    # 4. marching: the next rank's first layer of ids
+    ms_ext = backend.ms_ext()
+    nz = z1 - z0
+    yield ("exchange", ms_ext[:XY], None, None, ms_ext[nz * XY:(nz + 1) * XY] if z1 < Z else None)
+    tris = backend.emit()
+    nts = yield ("allgather", torch.tensor([tris.shape[0]], dtype=torch.int64, device=f.device))
+    nts = [int(c) for c in nts.cpu().numpy().reshape(-1)]
+    return SlabResult(z0, z1, backend.desc(), backend.asc(), ms_ext[:nz * XY], maxima, minima, region_keys, tris,
+                      sum(nts[:rank]), sum(nts), s["sweeps"])
+
+
+# ------------------------------------------------------- communicators -----
+class TorchComm:
+    """The step's collectives over torch.distributed (NCCL / gloo)."""
+
+    def __init__(self, group=None):
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+
+    def allgather(self, t):
+        out = torch.empty(self.world * t.numel(), dtype=t.dtype, device=t.device)
+        dist.all_gather_into_tensor(out, t.contiguous().view(-1), group=self.group)
+        return out.view((self.world,) + tuple(t.shape))
+
+    def allgather_var(self, t, counts):
+        m = max(max(counts), 1)
+        pad = torch.zeros((m,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+        pad[: t.shape[0]] = t
+        out = self.allgather(pad)
+        return torch.cat([out[r, : counts[r]] for r in range(self.world)])
+
+    def exchange(self, send_down, send_up, recv_below, recv_above):
+        """send_down -> rank - 1 (its recv_above), send_up -> rank + 1 (its
+        recv_below); None entries skip a direction, ends skip the edge."""
+        ops = []
+        r, w, g = self.rank, self.world, self.group
+        if r > 0 and send_down is not None:
+            ops.append(dist.P2POp(dist.isend, send_down.contiguous(), r - 1, g))
+        if r > 0 and recv_below is not None:
+            ops.append(dist.P2POp(dist.irecv, recv_below, r - 1, g))
+        if r + 1 < w and send_up is not None:
+            ops.append(dist.P2POp(dist.isend, send_up.contiguous(), r + 1, g))
+        if r + 1 < w and recv_above is not None:
+            ops.append(dist.P2POp(dist.irecv, recv_above, r + 1, g))
+        if ops:
+            for q in dist.batch_isend_irecv(ops):
+                q.wait()
+
+    def run(self, gen):
+        """Drive a step generator to completion; returns its result."""
+        try:
+            req = next(gen)
+            while True:
+                kind = req[0]
+                if kind == "allgather":
+                    res = self.allgather(req[1])
+                elif kind == "allgather_var":
+                    res = self.allgather_var(req[1], req[2])
+                elif kind == "exchange":
+                    self.exchange(*req[1:])
+                    res = None
+                else:
+                    raise ValueError(kind)
+                req = gen.send(res)
+        except StopIteration as e:
+            return e.value
+
+
+def run_ranks_inprocess(gens):
+    """Run the step generators of all ranks in one process: every rank is
+    advanced to its next collective, the collective is performed in memory,
+    and the results are sent back (lockstep; the ranks' device work never
+    waits on another rank inside a kernel)."""
+    world = len(gens)
+    reqs = [next(g) for g in gens]
+    results = [None] * world
+    done = [False] * world
+    while not all(done):
+        kinds = {r[0] for r, d in zip(reqs, done) if not d}
+        if len(kinds) != 1 or any(done):
+            raise RuntimeError(f"ranks diverged: {kinds}")
+        kind = kinds.pop()
+        if kind == "allgather":
+            stacked = torch.stack([r[1].to(reqs[0][1].device) for r in reqs])
+            outs = [stacked.to(r[1].device) for r in reqs]
+        elif kind == "allgather_var":
+            cat = torch.cat([r[1][: r[2][i]].to(reqs[0][1].device) for i, r in enumerate(reqs)])
+            outs = [cat.to(r[1].device) for r in reqs]
+        elif kind == "exchange":
+            for i, r in enumerate(reqs):
+                _, sd, su, rb, ra = r
+                if i > 0 and rb is not None:
+                    rb.copy_(reqs[i - 1][2])
+                if i + 1 < world and ra is not None:
+                    ra.copy_(reqs[i + 1][1])
+            outs = [None] * world
+        else:
+            raise ValueError(kind)
+        for i, g in enumerate(gens):
+            try:
+                reqs[i] = g.send(outs[i])
+            except StopIteration as e:
+                results[i] = e.value
+                done[i] = True
+    return results
+
+
+def ms_segmentation(field_buf: torch.Tensor, dims, backend, group=None) -> SlabResult:
+    """Full MS segmentation of a z-slab decomposed volume on this rank:
+    ``field_buf`` holds halo_bounds(Z, world, rank) layers (owned ones
+    filled), ``dims`` the global (X, Y, Z)."""
+    comm = TorchComm(group)
+    return comm.run(slab_step(backend, dims, comm.rank, comm.world, field_buf))
+
+
+# --------------------------------------------------------- B200 backend ----
+class _DevView:
+    """Zero-copy torch view of context-owned device memory."""
+
+    def __init__(self, ptr, n, typestr):
+        self.__cuda_array_interface__ = {"shape": (int(n),), "typestr": typestr, "data": (int(ptr or 0), False),
+                                         "version": 3}
+
+
+def _view(ptr, n, dtype, device):
+    ts = {torch.int32: "<i4", torch.int64: "<i8"}[dtype]
+    if n == 0 or not ptr:
+        return torch.empty(0, dtype=dtype, device=device)
+    return torch.as_tensor(_DevView(ptr, n, ts), device=device)
+
+
+class B200SlabBackend:
+    """The slab stages through libplmss_b200 (the product path). Device
+    outputs are views of buffers owned by this backend / its context, valid
+    until the next step."""
 
     def __init__(self, ctx=None):
         from . import api
 
         self.api = api
         self.ctx = ctx or api.default_context()
+        self.info = api.PlmssSlabInfo()
+        self._bufs = {}
+        self.dev = torch.device(f"cuda:{self.ctx.device}")
 
-    def segment_slab(self, dims, field_ext: torch.Tensor, halo_lo: bool, halo_hi: bool):
-        import ctypes as C
+    def _buf(self, name, n):
+        b = self._bufs.get(name)
+        if b is None or b.numel() < n:
+            b = self._bufs[name] = torch.empty(max(n, 1), dtype=torch.int32, device=self.dev)
+        return b[:n]
 
+    def segment(self, dims, z0, z1, field_buf):
         a = self.api
         d = a._dims(dims)
-        n = int(np.prod(d))
-        desc = torch.empty(n, dtype=torch.int32, device=field_ext.device)
-        asc = torch.empty(n, dtype=torch.int32, device=field_ext.device)
-        sweeps = C.c_int32()
-        a._check(a.lib().plmss_b200_segment_slab(self.ctx.h, d.ctypes.data, a._key_type(field_ext),
-                                                 a._ptr(field_ext), int(halo_lo), int(halo_hi), a._ptr(desc),
-                                                 a._ptr(asc), C.byref(sweeps)))
-        return desc.to(torch.int64) & 0xFFFFFFFF, asc.to(torch.int64) & 0xFFFFFFFF
+        self.XY = int(d[0]) * int(d[1])
+        self.nz = z1 - z0
+        self.has_up = z1 < int(d[2])
+        a._check(a.lib().plmss_b200_slab_segment(self.ctx.h, d.ctypes.data, z0, z1, a._ptr(field_buf),
+                                                 C.byref(self.info)))
+        i = self.info
+        return {"n_max": i.n_maxima, "n_min": i.n_minima,
+                "maxima": _view(i.d_maxima, i.n_maxima, torch.int32, self.dev),
+                "minima": _view(i.d_minima, i.n_minima, torch.int32, self.dev),
+                "boundary": _view(i.d_boundary, 4 * self.XY, torch.int32, self.dev).view(4, self.XY),
+                "sweeps": i.sweeps}
 
-    def local_regions(self, asc: torch.Tensor, desc: torch.Tensor, N: int):
-        """combine_ms on this slab's (global-id) labels: local dense ids and
-        the sorted distinct keys asc * N + desc they index."""
+    def resolve(self, G, world, rank, max_counts, min_counts, maxima, minima):
         a = self.api
-        seg = a.SegmentationResult(desc=desc.to(torch.int32), asc=asc.to(torch.int32))
-        a.combine_ms(seg, ctx=self.ctx)
-        k = seg.region_keys
-        uniq = (k >> 32) * N + (k & 0xFFFFFFFF)
-        return seg.ms_region.to(torch.int64) & 0xFFFFFFFF, uniq
+        n = self.nz * self.XY
+        desc, asc = self._buf("desc", n), self._buf("asc", n)
+        ms = self._buf("ms", n + (self.XY if self.has_up else 0))
+        self._keep = (G, maxima, minima)  # alive until slab_emit
+        mc = np.ascontiguousarray(max_counts, dtype=np.int64)
+        nc = np.ascontiguousarray(min_counts, dtype=np.int64)
+        a._check(a.lib().plmss_b200_slab_resolve(self.ctx.h, a._ptr(G.contiguous()), world, rank, mc.ctypes.data,
+                                                 nc.ctypes.data, a._ptr(maxima), a._ptr(minima), a._ptr(desc),
+                                                 a._ptr(asc), a._ptr(ms), C.byref(self.info)))
+        return _view(self.info.d_keys, self.info.n_keys, torch.int64, self.dev), self.info.n_keys
 
-    def march_slab(self, dims, ms_ext: torch.Tensor):
-        recs = self.api.emit_separators(dims, ms_ext.contiguous(), ctx=self.ctx)
-        return recs[:, 0] >> 6, recs[:, 1], recs[:, 2]
+    def ids(self, keys_all):
+        a = self.api
+        a._check(a.lib().plmss_b200_slab_ids(self.ctx.h, a._ptr(keys_all), keys_all.numel(), C.byref(self.info)))
+        return _view(self.info.d_region_keys, self.info.n_regions, torch.int64, self.dev)
 
+    def ms_ext(self):
+        return self._bufs["ms"][: self.nz * self.XY + (self.XY if self.has_up else 0)]
 
-def _all_gather_var(t: torch.Tensor, group=None):
-    """all_gather of variable-length 1-D/2-D tensors (pad to the max)."""
-    world = dist.get_world_size(group)
-    n = torch.tensor([t.shape[0]], dtype=torch.int64, device=t.device)
-    ns = [torch.zeros_like(n) for _ in range(world)]
-    dist.all_gather(ns, n, group=group)
-    ns = [int(x.item()) for x in ns]
-    m = max(ns) if ns else 0
-    pad = torch.zeros((m,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
-    pad[: t.shape[0]] = t
-    outs = [torch.empty_like(pad) for _ in range(world)]
-    dist.all_gather(outs, pad, group=group)
-    return [o[:k] for o, k in zip(outs, ns)]
+    def desc(self):
+        return self._bufs["desc"][: self.nz * self.XY]
 
+    def asc(self):
+        return self._bufs["asc"][: self.nz * self.XY]
 
-def _exchange_layers(bottom: torch.Tensor, top: torch.Tensor, rank: int, world: int, group=None):
-    """Send my bottom layer down and top layer up; return (from_below,
-    from_above) — the neighbours' top / bottom layers (None at the ends)."""
-    ops, below, above = [], None, None
-    if rank > 0:
-        below = torch.empty_like(top)
-        ops.append(dist.P2POp(dist.isend, bottom.contiguous(), rank - 1, group))
-        ops.append(dist.P2POp(dist.irecv, below, rank - 1, group))
-    if rank + 1 < world:
-        above = torch.empty_like(bottom)
-        ops.append(dist.P2POp(dist.isend, top.contiguous(), rank + 1, group))
-        ops.append(dist.P2POp(dist.irecv, above, rank + 1, group))
-    if ops:
-        for r in dist.batch_isend_irecv(ops):
-            r.wait()
-    return below, above
+    def emit(self):
+        a = self.api
+        a._check(a.lib().plmss_b200_slab_emit(self.ctx.h, C.byref(self.info)))
+        self._keep = None
+        return _view(self.info.d_tris, 2 * self.info.n_tris, torch.int64, self.dev).view(-1, 2)
 
 
-def ms_segmentation(field_owned: torch.Tensor, dims, backend, group=None) -> SlabResult:
-    """Full MS segmentation of a z-slab decomposed volume. ``field_owned`` is
-    this rank's owned layers (x fastest), ``dims`` the global (X, Y, Z)."""
+def slab_field_buffer(dims, world: int, rank: int, device, owned: Optional[torch.Tensor] = None):
+    """A rank's field buffer (halo_bounds layers); ``owned`` copied in."""
     X, Y, Z = (int(v) for v in dims)
-    XY, N = X * Y, X * Y * Z
-    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    h0, h1 = halo_bounds(Z, world, rank)
     z0, z1 = slab_bounds(Z, world, rank)
-    nz = z1 - z0
-    f = field_owned.reshape(nz, XY)
-    dev = f.device
-
-    # 1. field halo
-    below, above = _exchange_layers(f[0], f[-1], rank, world, group)
-    parts = ([below[None]] if below is not None else []) + [f] + ([above[None]] if above is not None else [])
-    f_ext = torch.cat(parts).reshape(-1)
-    lo = 1 if below is not None else 0
-    nz_ext = nz + lo + (1 if above is not None else 0)
-    zbase = z0 - lo  # global layer of extended layer 0
-
-    # 2. slab segmentation (halo layers are terminals)
-    d_ext, a_ext = backend.segment_slab((X, Y, nz_ext), f_ext, below is not None, above is not None)
-    off = zbase * XY
-    own = slice(lo * XY, (lo + nz) * XY)
-    desc = d_ext[own] + off
-    asc = a_ext[own] + off
-
-    # 3. boundary graph over every rank's bottom and top owned layers
-    bnd = torch.stack([desc[:XY], desc[-XY:], asc[:XY], asc[-XY:]])
-    allb = [torch.empty_like(bnd) for _ in range(world)]
-    dist.all_gather(allb, bnd, group=group)
-    layers = []  # global z of each boundary row, rank-major: bottom, top
-    for r in range(world):
-        a0, a1 = slab_bounds(Z, world, r)
-        layers += [a0, a1 - 1]
-    layer_slot = torch.full((Z,), -1, dtype=torch.int64, device=dev)
-    for i, zl in enumerate(layers):
-        if layer_slot[zl] < 0:
-            layer_slot[zl] = i
-    nodes_d = torch.stack([b[k] for b in allb for k in (0, 1)]).reshape(-1)
-    nodes_a = torch.stack([b[k] for b in allb for k in (2, 3)]).reshape(-1)
-
-    def slot_of(g):  # global vertex id -> boundary slot (or -1)
-        s = layer_slot[g // XY]
-        return torch.where(s >= 0, s * XY + g % XY, torch.full_like(g, -1))
-
-    def resolve(nodes):
-        lab = nodes.clone()
-        for _ in range(64):
-            s = slot_of(lab)
-            nxt = torch.where(s >= 0, lab[s.clamp(min=0)], lab)
-            if torch.equal(nxt, lab):
-                return lab
-            lab = nxt
-        raise RuntimeError("boundary graph did not converge")
-
-    fin_d, fin_a = resolve(nodes_d), resolve(nodes_a)
-
-    def fix(lab, fin):  # owned labels that point at halo vertices
-        z = lab // XY
-        halo = (z < z0) | (z >= z1)
-        s = slot_of(lab)
-        return torch.where(halo, fin[s.clamp(min=0)], lab)
-
-    desc, asc = fix(desc, fin_d), fix(asc, fin_a)
-
-    # 4. extrema (owned roots, id order; rank order = global order)
-    ids = torch.arange(z0 * XY, z1 * XY, dtype=torch.int64, device=dev)
-    maxima = torch.cat(_all_gather_var(ids[desc == ids], group))
-    minima = torch.cat(_all_gather_var(ids[asc == ids], group))
-
-    # 5. Morse-Smale ids: lexicographic (asc, desc) == key asc * N + desc
-    # The device combine_ms indexes its rank maps by slab-local vertex index,
-    # so it only applies while global ids equal local ones (one rank).
-    local_regions = getattr(backend, "local_regions", None) if world == 1 else None
-    if local_regions is not None:  # dense local ids from the device hash (no sort of the slab)
-        local, uniq = local_regions(asc, desc, N)
-    else:
-        key = asc * N + desc
-        uniq, local = torch.unique(key, return_inverse=True)
-    gkeys = torch.unique(torch.cat(_all_gather_var(uniq, group)))
-    ms = torch.searchsorted(gkeys, uniq)[local]
-    region_keys = torch.stack([gkeys // N, gkeys % N], dim=1)
-
-    # 6. marching: owned cube layers need the next rank's first layer of ids
-    _, ms_above = _exchange_layers(ms[:XY], ms[-XY:], rank, world, group)
-    ms_ext = torch.cat([ms] + ([ms_above] if ms_above is not None else []))
-    nz_m = nz + (1 if ms_above is not None else 0)
-    if nz_m >= 2:
-        cells, tlo, thi = backend.march_slab((X, Y, nz_m), ms_ext)
-        cells = cells + 6 * (X - 1) * (Y - 1) * z0
-    else:
-        cells = tlo = thi = torch.empty(0, dtype=torch.int64, device=dev)
-    cnt = torch.tensor([cells.shape[0]], dtype=torch.int64, device=dev)
-    cnts = [torch.zeros_like(cnt) for _ in range(world)]
-    dist.all_gather(cnts, cnt, group=group)
-    cnts = [int(c.item()) for c in cnts]
-    return SlabResult(z0, z1, desc, asc, ms, maxima, minima, region_keys, cells, tlo, thi, sum(cnts[:rank]),
-                      sum(cnts))
+    buf = torch.empty((h1 - h0) * X * Y, dtype=torch.float32, device=device)
+    if owned is not None:
+        buf[(z0 - h0) * X * Y:(z1 - h0) * X * Y].copy_(owned.reshape(-1))
+    return buf

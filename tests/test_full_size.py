@@ -35,15 +35,19 @@ def test_golden_digest_files_are_complete(name):
     assert sum(g["tri_chunk_counts"]) == g["n_tris"]
 
 
-# (config, combine path): 0 = the pipeline's own choice (dense region bitmap
-# unless n_max * n_min >= 2^32, i.e. the hash set for cfg3), 2 = the hash set
-# forced, so both region-key modes run at full size.
-CASES = [("cfg1", 0), ("cfg2", 0), ("cfg2", 2), ("cfg3", 0), ("cfg4", 0), ("cfg5", 0), ("cfg5", 2)]
+# (config, combine path, speculative sweeps). Combine path 0 = the pipeline's
+# own choice (dense region bitmap unless n_max * n_min >= 2^32, i.e. the hash
+# set for cfg3), 2 = the hash set forced, so both region-key modes run at
+# full size. Speculative sweeps 0 = passes C and D first run on the
+# unswept terminal forest (nearly every entry unresolved), then the redo
+# path: the unresolved-entry guard of the token pass at scale.
+CASES = [("cfg1", 0, 1), ("cfg1", 0, 0), ("cfg2", 0, 1), ("cfg2", 2, 1), ("cfg2", 0, 0), ("cfg3", 0, 1),
+         ("cfg4", 0, 1), ("cfg4", 0, 0), ("cfg5", 0, 1), ("cfg5", 2, 1)]
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name,path", CASES)
-def test_full_size_matches_oracle(plmss, gpu, name, path):
+@pytest.mark.parametrize("name,path,spec", CASES)
+def test_full_size_matches_oracle(plmss, gpu, name, path, spec):
     import torch
 
     from paper_2303_15491_b200.configs import CONFIGS
@@ -56,10 +60,12 @@ def test_full_size_matches_oracle(plmss, gpu, name, path):
     torch.cuda.synchronize()
     assert digest_device(f) == g["field"], "device generator differs from the host input definition"
     gpu.set_option(plmss.OPT_COMBINE_PATH, path)
+    gpu.set_option(plmss.OPT_SPECULATIVE_SWEEPS, spec)
     try:
         res = plmss.pipeline(cfg.dims, f, ctx=gpu)
     finally:
         gpu.set_option(plmss.OPT_COMBINE_PATH, 0)
+        gpu.set_option(plmss.OPT_SPECULATIVE_SWEEPS, 1)
     del f
     assert (res.n_maxima, res.n_minima, res.n_regions, res.n_tris) == (g["n_maxima"], g["n_minima"],
                                                                        g["n_regions"], g["n_tris"])

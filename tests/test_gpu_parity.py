@@ -206,30 +206,6 @@ def test_boundaries_region_filter(plmss, gpu, restatement):
             assert np.array_equal(b[k].cpu().numpy(), rb[k]), (flt, k)
 
 
-# ------------------------------------------------ z-slab device backend --
-@pytest.mark.parametrize("lo,hi", [(False, False), (True, False), (False, True), (True, True)])
-def test_slab_backend_matches_oracle_backend(plmss, gpu, lo, hi):
-    """The per-slab device work of the multi-GPU path (halo layers as
-    terminals, int64-label marching) against the CPU test backend."""
-    import torch
-
-    from paper_2303_15491_b200.distributed import B200Backend
-    from test_distributed import OracleBackend
-
-    rng = np.random.default_rng(5)
-    dims = (11, 9, 7)
-    f = rng.integers(0, 4, int(np.prod(dims))).astype(np.float32)
-    gb, cb = B200Backend(gpu), OracleBackend()
-    d1, a1 = gb.segment_slab(dims, torch.from_numpy(f).cuda(), lo, hi)
-    d2, a2 = cb.segment_slab(dims, torch.from_numpy(f), lo, hi)
-    assert np.array_equal(d1.cpu().numpy(), d2.numpy()) and np.array_equal(a1.cpu().numpy(), a2.numpy())
-    ms = torch.from_numpy(rng.integers(0, 5, int(np.prod(dims))).astype(np.int64) * 7 + 3)
-    c1, l1, h1 = gb.march_slab(dims, ms.cuda())
-    c2, l2, h2 = cb.march_slab(dims, ms)
-    for x, y in ((c1, c2), (l1, l2), (h1, h2)):
-        assert np.array_equal(x.cpu().numpy(), y.numpy())
-
-
 # ---------------------------------------------------------- order field --
 def test_compute_order(plmss, gpu, restatement):
     rng = np.random.default_rng(11)
@@ -380,39 +356,3 @@ def test_library_is_ordered_after_torch_default_stream(plmss, gpu):
     r = api.emit_separators(dims, torch.sort(base)[0] // 4096, ctx=gpu)
     assert r.shape[0] == want
 
-
-@pytest.mark.gpu
-def test_slab_backend_single_rank_nccl_matches_pipeline(plmss, gpu):
-    """bench.py --slab path at world size 1 over NCCL: labels, ids and the
-    triangle total equal the fused pipeline's on a 96x80x64 Gaussian field."""
-    import os
-
-    import torch
-    import torch.distributed as dist
-
-    from paper_2303_15491_b200.configs import CONFIGS, scaled
-    from paper_2303_15491_b200.distributed import B200Backend, ms_segmentation
-
-    cfg = scaled(CONFIGS["cfg2"], (96, 80, 64))
-    f = plmss.synth_field(cfg.dims, kind=cfg.kind, gaussians=cfg.gaussians(), noise_amp=cfg.noise, seed=cfg.seed,
-                          ctx=gpu)
-    res = plmss.pipeline(cfg.dims, f, ctx=gpu)
-    out = plmss.fetch(gpu, res)
-    if dist.is_initialized() or not dist.is_nccl_available():
-        pytest.skip("a process group is already open / NCCL unavailable")
-    import socket
-
-    with socket.socket() as sk:  # a free port
-        sk.bind(("127.0.0.1", 0))
-        port = sk.getsockname()[1]
-    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
-    try:
-        s = ms_segmentation(f, cfg.dims, B200Backend(gpu))
-        torch.cuda.synchronize()
-    finally:
-        dist.destroy_process_group()
-    u = lambda t: (t.to(torch.int64) & 0xFFFFFFFF).cpu()  # noqa: E731
-    assert torch.equal(s.desc.cpu(), u(out["desc"]))
-    assert torch.equal(s.asc.cpu(), u(out["asc"]))
-    assert torch.equal(s.ms.cpu(), u(out["ms"]))
-    assert s.tri_total == res.n_tris
