@@ -235,6 +235,19 @@ int plmss_b200_materialize_separators(plmss_ctx* ctx, const int64_t dims[3], con
                                       int64_t n, double* d_points, int64_t* d_regions,
                                       int64_t* d_source_cells);
 
+/* The same SeparatingMesh arrays streamed chunk by chunk into a host sink
+ * (outputs larger than device or host memory: cfg3's 5.4 G triangles are
+ * ~520 GB of geometry). The sink gets triangles [first, first + count):
+ * points 9 doubles, regions 2 int64, source cells 1 int64 per triangle, in
+ * pinned host buffers valid until it returns; a nonzero return stops the
+ * stream (PLMSS_ERR_LOGIC). chunk <= 0: 4 Mi triangles. The device
+ * materialisation and copy of the next chunk overlap the sink. */
+typedef int (*plmss_geometry_sink)(void* user, int64_t first, int64_t count, const double* points,
+                                   const int64_t* regions, const int64_t* source_cells);
+int plmss_b200_materialize_separators_chunked(plmss_ctx* ctx, const int64_t dims[3], const double spacing[3],
+                                              const double origin[3], int label_type, const void* d_tris,
+                                              int64_t n, int64_t chunk, plmss_geometry_sink sink, void* user);
+
 /* emit_boundaries (marching.hpp:123-126, marching.cpp:236-326): faces whose
  * 3 vertices share a label that the 4th tet vertex lacks, one per face
  * (lowest generating cell), in (v0, v1, v2) order. Two calls: with
@@ -320,6 +333,15 @@ int plmss_b200_write_labels(plmss_ctx* ctx, const char* path, int label_type, co
 int plmss_b200_write_surface_obj(plmss_ctx* ctx, const char* path, const double* d_points, int64_t n_points,
                                  const int64_t* d_indices, const int64_t* d_regions, int64_t n_prims,
                                  int verts_per_prim);
+
+/* write_surface_obj(path, emit_separators(...)) of the reference (io.cpp:268-299
+ * over the SeparatingMesh, marching.hpp:65-76) straight from the compact
+ * records, streamed: points materialised on the device chunk by chunk, the
+ * identity faces and region groups formatted on host threads. Byte-identical
+ * to the reference file; the mesh is never held whole. */
+int plmss_b200_write_separators_obj(plmss_ctx* ctx, const char* path, const int64_t dims[3],
+                                    const double spacing[3], const double origin[3], int label_type,
+                                    const void* d_tris, int64_t n);
 
 enum plmss_option {
   PLMSS_OPT_COMBINE_PATH = 1,

@@ -48,7 +48,11 @@ HEADER_FUNCTIONS = [
     "plmss_b200_compress_sweep", "plmss_b200_segment_slab", "plmss_b200_weld_points", "plmss_b200_read_volume",
     "plmss_b200_write_labels", "plmss_b200_write_surface_obj", "plmss_b200_synth_layers",
     "plmss_b200_slab_segment", "plmss_b200_slab_resolve", "plmss_b200_slab_ids", "plmss_b200_slab_emit",
+    "plmss_b200_materialize_separators_chunked", "plmss_b200_write_separators_obj",
 ]
+
+GEOMETRY_SINK = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int64, C.c_int64, C.POINTER(C.c_double),
+                            C.POINTER(C.c_int64), C.POINTER(C.c_int64))
 
 
 class PlmssResult(C.Structure):
@@ -113,6 +117,8 @@ def lib() -> C.CDLL:
         L.plmss_b200_read_volume.argtypes = [vp, C.c_char_p, vp, i32, i32, vp]
         L.plmss_b200_write_labels.argtypes = [vp, C.c_char_p, i32, vp, vp, i64]
         L.plmss_b200_write_surface_obj.argtypes = [vp, C.c_char_p, vp, i64, vp, vp, i64, i32]
+        L.plmss_b200_materialize_separators_chunked.argtypes = [vp, vp, vp, vp, i32, vp, i64, i64, GEOMETRY_SINK, vp]
+        L.plmss_b200_write_separators_obj.argtypes = [vp, C.c_char_p, vp, vp, vp, i32, vp, i64]
         SI = C.POINTER(PlmssSlabInfo)
         L.plmss_b200_slab_segment.argtypes = [vp, vp, i64, i64, vp, SI]
         L.plmss_b200_slab_resolve.argtypes = [vp, vp, i32, i32, vp, vp, vp, vp, vp, vp, vp, SI]
@@ -394,6 +400,51 @@ def materialize_separators(dims, records, spacing=None, origin=None, ctx: Option
     _check(lib().plmss_b200_materialize_separators(ctx.h, d.ctypes.data, sp.ctypes.data, og.ctypes.data, lt,
                                                    _ptr(recs), T, _ptr(pts), _ptr(reg), _ptr(src)))
     return dict(points=pts[: 3 * T], indices=torch.arange(3 * T, device=dev), regions=reg[:T], source_cells=src[:T])
+
+
+def materialize_separators_chunked(dims, records, sink, chunk: int = 1 << 22, spacing=None, origin=None,
+                                   ctx: Optional[Context] = None):
+    """The SeparatingMesh arrays of `records` streamed chunk by chunk (never
+    held whole): sink(first, points (3k, 3) f64, regions (k, 2) i64,
+    source_cells (k,) i64) is called per chunk of k triangles with numpy
+    views of pinned host buffers, valid only during the call; a truthy
+    return value stops the stream (RuntimeError)."""
+    ctx = ctx or default_context()
+    d = _dims(dims)
+    recs = records.contiguous()
+    T = recs.shape[0]
+    lt = 0 if recs.shape[1] == 2 else 1
+    sp, og = _vec3(spacing, (1, 1, 1)), _vec3(origin, (0, 0, 0))
+    err = []
+
+    def _cb(_user, first, count, p, r, c):
+        try:
+            pts = np.ctypeslib.as_array(p, shape=(3 * count, 3))
+            reg = np.ctypeslib.as_array(r, shape=(count, 2))
+            src = np.ctypeslib.as_array(c, shape=(count,))
+            return 1 if sink(first, pts, reg, src) else 0
+        except Exception as e:  # noqa: BLE001  (re-raised below)
+            err.append(e)
+            return 2
+
+    cb = GEOMETRY_SINK(_cb)
+    st = lib().plmss_b200_materialize_separators_chunked(ctx.h, d.ctypes.data, sp.ctypes.data, og.ctypes.data, lt,
+                                                        _ptr(recs), T, chunk, cb, None)
+    if err:
+        raise err[0]
+    _check(st)
+
+
+def write_separators_obj(path, dims, records, spacing=None, origin=None, ctx: Optional[Context] = None):
+    """io.cpp:268-299 write_surface_obj of emit_separators' mesh, streamed
+    from the compact records (plmss_b200_write_separators_obj)."""
+    ctx = ctx or default_context()
+    d = _dims(dims)
+    recs = records.contiguous()
+    lt = 0 if recs.shape[1] == 2 else 1
+    sp, og = _vec3(spacing, (1, 1, 1)), _vec3(origin, (0, 0, 0))
+    _check(lib().plmss_b200_write_separators_obj(ctx.h, os.fsencode(str(path)), d.ctypes.data, sp.ctypes.data,
+                                                 og.ctypes.data, lt, _ptr(recs), recs.shape[0]))
 
 
 def emit_boundaries(dims, labels, region_filter=None, workers: int = 1, spacing=None, origin=None,

@@ -515,6 +515,27 @@ int plmss_b200_synth_layers(plmss_ctx* p, const int64_t dims[3], int kind, const
   });
 }
 
+int plmss_b200_materialize_separators_chunked(plmss_ctx* p, const int64_t dims[3], const double spacing[3],
+                                              const double origin[3], int label_type, const void* d_tris,
+                                              int64_t n, int64_t chunk, plmss_geometry_sink sink, void* user) {
+  return guarded([&] {
+    Ctx& c = C(p);
+    set_device(c);
+    if (label_type != 0 && label_type != 1) fail(PLMSS_ERR_INVALID_ARGUMENT, "label_type must be 0 or 1");
+    materialize_chunks(c, make_grid(dims), spacing, origin, label_type, d_tris, n, chunk, sink, user);
+  });
+}
+
+int plmss_b200_write_separators_obj(plmss_ctx* p, const char* path, const int64_t dims[3], const double spacing[3],
+                                    const double origin[3], int label_type, const void* d_tris, int64_t n) {
+  return guarded([&] {
+    Ctx& c = C(p);
+    set_device(c);
+    if (label_type != 0 && label_type != 1) fail(PLMSS_ERR_INVALID_ARGUMENT, "label_type must be 0 or 1");
+    write_separators_obj(c, path, make_grid(dims), spacing, origin, label_type, d_tris, n);
+  });
+}
+
 // ---- z-slab pipeline (fused.cu slab_*) ----------------------------------
 int plmss_b200_slab_segment(plmss_ctx* p, const int64_t dims[3], int64_t z0, int64_t z1, const float* d_field,
                             plmss_slab_info* info) {

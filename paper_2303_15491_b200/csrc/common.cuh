@@ -239,6 +239,10 @@ void read_volume(Ctx& c, const char* path, const int64_t dims[3], int dtype, int
 void write_labels(Ctx& c, const char* path, int label_type, const void* d_asc, const void* d_desc, int64_t n);
 void write_surface_obj(Ctx& c, const char* path, const double* d_points, int64_t n_points, const int64_t* d_indices,
                        const int64_t* d_regions, int64_t n_prims, int verts_per_prim);
+void write_separators_obj(Ctx& c, const char* path, const Grid& g, const double* sp, const double* og,
+                          int label_type, const void* d_tris, int64_t n);
+void materialize_chunks(Ctx& c, const Grid& g, const double* sp, const double* og, int label_type,
+                        const void* d_tris, int64_t n, int64_t chunk, plmss_geometry_sink sink, void* user);
 void synth(Ctx& c, const Grid& g, int kind, const double* h_gauss, int n_gauss, double noise_amp,
            uint64_t seed, int levels, float* field, int64_t z0, int64_t nz);
 

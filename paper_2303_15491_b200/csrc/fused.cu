@@ -2485,7 +2485,7 @@ void slab_ids(Ctx& c, const uint64_t* keys_all, int64_t n_keys_all, plmss_slab_i
     // sort + unique of the gathered rank pairs
     const int64_t n = std::max<int64_t>(n_keys_all, 1);
     uint64_t* kk = c.get_t<uint64_t>(S_SORT_A, n);
-    uint64_t* vv = c.get_t<uint64_t>(S_SORT_C, n);
+    uint64_t* vv = c.get_t<uint64_t>(S_SORT_B, n);  // (radix_sort_pairs uses S_SORT_C / S_SORT_D)
     if (n_keys_all) CK(cudaMemcpyAsync(kk, keys_all, n_keys_all * 8, cudaMemcpyDeviceToDevice, c.stream));
     int kb = 32;
     while ((uint64_t(1) << (kb - 32)) < uint64_t(std::max<int64_t>(st.n_min_g, 1))) ++kb;

@@ -335,11 +335,15 @@ void write_labels(Ctx& c, const char* path, int label_type, const void* d_asc, c
   }
 }
 
-void write_surface_obj(Ctx& c, const char* path, const double* d_points, int64_t n_points, const int64_t* d_indices,
-                       const int64_t* d_regions, int64_t n_prims, int verts_per_prim) {
-  if (!path) fail(PLMSS_ERR_INVALID_ARGUMENT, "null path");
-  if (verts_per_prim != 2 && verts_per_prim != 3) fail(PLMSS_ERR_INVALID_ARGUMENT, "verts_per_prim must be 2 or 3");
-  if (n_points < 0 || n_prims < 0) fail(PLMSS_ERR_INVALID_ARGUMENT, "negative size");
+// The reference OBJ text (io.cpp:268-299) from two chunk fetchers: points
+// [p0, p0 + cnt) into host doubles, primitives [q0, q0 + cnt) into host
+// indices and region pairs. Formatting on host threads, written in order.
+using PointFetch = std::function<void(int64_t, int64_t, double*)>;
+using PrimFetch = std::function<void(int64_t, int64_t, int64_t*, int64_t*)>;
+
+static void write_obj_core(Ctx& c, const char* path, int64_t n_points, int64_t n_prims, int verts_per_prim,
+                           int64_t point_chunk, int64_t prim_chunk, const PointFetch& fetch_points,
+                           const PrimFetch& fetch_prims) {
   File f(path, O_WRONLY | O_CREAT | O_TRUNC, " for writing");
   uint64_t fpos = 0;  // file offset of the next part
   {
@@ -366,13 +370,12 @@ void write_surface_obj(Ctx& c, const char* path, const double* d_points, int64_t
   };
   // points: "v %.17g %.17g %.17g"
   {
-    const int64_t per = int64_t(kChunk / 24);
-    unsigned char* buf = c.stage(size_t(per) * 24);
-    const double* hp = reinterpret_cast<const double*>(buf);
+    const int64_t per = point_chunk;
+    std::vector<double> hpv(size_t(std::max<int64_t>(per, 1)) * 3);
+    const double* hp = hpv.data();
     for (int64_t p0 = 0; p0 < n_points; p0 += per) {
       const int64_t cnt = std::min(per, n_points - p0);
-      CK(cudaMemcpyAsync(buf, d_points + 3 * p0, size_t(cnt) * 24, cudaMemcpyDeviceToHost, c.stream));
-      c.sync();
+      fetch_points(p0, cnt, hpv.data());
       parallel_format(cnt, [&](int64_t b, int64_t e, std::string& s) {
         char line[96];
         s.reserve(size_t(e - b) * 60);
@@ -386,18 +389,15 @@ void write_surface_obj(Ctx& c, const char* path, const double* d_points, int64_t
   // primitives: "g rA[_rB]" whenever the region pair changes, then
   // "f i j k" / "l i j" with 1-based indices
   {
-    const int64_t per = int64_t(kChunk / 48);
+    const int64_t per = prim_chunk;
     const int vp = verts_per_prim;
-    unsigned char* ibuf = c.stage(size_t(per) * vp * 8 + size_t(per) * 16);
-    unsigned char* rbuf = ibuf + size_t(per) * vp * 8;
-    const int64_t* hi = reinterpret_cast<const int64_t*>(ibuf);
-    const int64_t* hr = reinterpret_cast<const int64_t*>(rbuf);
+    std::vector<int64_t> hiv(size_t(std::max<int64_t>(per, 1)) * vp), hrv(size_t(std::max<int64_t>(per, 1)) * 2);
+    const int64_t* hi = hiv.data();
+    const int64_t* hr = hrv.data();
     int64_t prev[2] = {-2, -2};  // region pair of the primitive before the chunk
     for (int64_t q0 = 0; q0 < n_prims; q0 += per) {
       const int64_t cnt = std::min(per, n_prims - q0);
-      CK(cudaMemcpyAsync(ibuf, d_indices + q0 * vp, size_t(cnt) * vp * 8, cudaMemcpyDeviceToHost, c.stream));
-      CK(cudaMemcpyAsync(rbuf, d_regions + 2 * q0, size_t(cnt) * 16, cudaMemcpyDeviceToHost, c.stream));
-      c.sync();
+      fetch_prims(q0, cnt, hiv.data(), hrv.data());
       const int64_t p0a = prev[0], p0b = prev[1];
       parallel_format(cnt, [&](int64_t b, int64_t e, std::string& s) {
         int64_t ca = b ? hr[2 * (b - 1)] : p0a, cb = b ? hr[2 * (b - 1) + 1] : p0b;
@@ -424,6 +424,121 @@ void write_surface_obj(Ctx& c, const char* path, const double* d_points, int64_t
       prev[1] = hr[2 * (cnt - 1) + 1];
     }
   }
+}
+
+void write_surface_obj(Ctx& c, const char* path, const double* d_points, int64_t n_points, const int64_t* d_indices,
+                       const int64_t* d_regions, int64_t n_prims, int verts_per_prim) {
+  if (!path) fail(PLMSS_ERR_INVALID_ARGUMENT, "null path");
+  if (verts_per_prim != 2 && verts_per_prim != 3) fail(PLMSS_ERR_INVALID_ARGUMENT, "verts_per_prim must be 2 or 3");
+  if (n_points < 0 || n_prims < 0) fail(PLMSS_ERR_INVALID_ARGUMENT, "negative size");
+  const int vp = verts_per_prim;
+  unsigned char* stage = c.stage(kChunk);
+  write_obj_core(
+      c, path, n_points, n_prims, vp, int64_t(kChunk / 24), int64_t(kChunk / (8 * vp + 16)),
+      [&](int64_t p0, int64_t cnt, double* out) {
+        CK(cudaMemcpyAsync(stage, d_points + 3 * p0, size_t(cnt) * 24, cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
+        memcpy(out, stage, size_t(cnt) * 24);
+      },
+      [&](int64_t q0, int64_t cnt, int64_t* idx, int64_t* reg) {
+        CK(cudaMemcpyAsync(stage, d_indices + q0 * vp, size_t(cnt) * vp * 8, cudaMemcpyDeviceToHost, c.stream));
+        CK(cudaMemcpyAsync(stage + size_t(cnt) * vp * 8, d_regions + 2 * q0, size_t(cnt) * 16, cudaMemcpyDeviceToHost,
+                           c.stream));
+        c.sync();
+        memcpy(idx, stage, size_t(cnt) * vp * 8);
+        memcpy(reg, stage + size_t(cnt) * vp * 8, size_t(cnt) * 16);
+      });
+}
+
+// The reference write_surface_obj of emit_separators' mesh, streamed from the
+// compact records: points materialised on the device chunk by chunk
+// (marching.cu materialize), faces are the identity soup (3j, 3j+1, 3j+2),
+// regions from the records — the SeparatingMesh (marching.hpp:65-76) is
+// never held whole, on the device or on the host.
+void write_separators_obj(Ctx& c, const char* path, const Grid& g, const double* sp, const double* og,
+                          int label_type, const void* d_tris, int64_t n) {
+  if (!path) fail(PLMSS_ERR_INVALID_ARGUMENT, "null path");
+  if (n < 0 || (n > 0 && !d_tris)) fail(PLMSS_ERR_INVALID_ARGUMENT, "bad separator records");
+  const size_t rec = label_type == 0 ? sizeof(plmss_tri) : sizeof(plmss_tri64);
+  const int64_t per_tri = int64_t(kChunk / 72);  // triangles per points chunk
+  double* d_pts = c.get_t<double>(S_TMP2, size_t(per_tri) * 9);
+  int64_t* d_reg = c.get_t<int64_t>(S_SCAN_C, size_t(per_tri) * 2);
+  unsigned char* stage = c.stage(kChunk);
+  write_obj_core(
+      c, path, 3 * n, n, 3, 3 * per_tri, per_tri,
+      [&](int64_t p0, int64_t cnt, double* out) {  // p0, cnt: multiples of 3 except at the end
+        const int64_t t0 = p0 / 3, tn = (cnt + 2) / 3;
+        materialize(c, g, sp, og, label_type, static_cast<const char*>(d_tris) + size_t(t0) * rec, tn, d_pts, nullptr,
+                    nullptr);
+        CK(cudaMemcpyAsync(stage, d_pts, size_t(cnt) * 24, cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
+        memcpy(out, stage, size_t(cnt) * 24);
+      },
+      [&](int64_t q0, int64_t cnt, int64_t* idx, int64_t* reg) {
+        materialize(c, g, sp, og, label_type, static_cast<const char*>(d_tris) + size_t(q0) * rec, cnt, nullptr, d_reg,
+                    nullptr);
+        CK(cudaMemcpyAsync(stage, d_reg, size_t(cnt) * 16, cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
+        memcpy(reg, stage, size_t(cnt) * 16);
+        for (int64_t i = 0; i < 3 * cnt; ++i) idx[i] = 3 * q0 + i;
+      });
+}
+
+// The SeparatingMesh arrays of the records, chunk by chunk into a host sink:
+// device materialisation of chunk k+1 and its copy overlap the sink's work
+// on chunk k (two pinned buffers).
+void materialize_chunks(Ctx& c, const Grid& g, const double* sp, const double* og, int label_type,
+                        const void* d_tris, int64_t n, int64_t chunk, plmss_geometry_sink sink, void* user) {
+  if (!sink) fail(PLMSS_ERR_INVALID_ARGUMENT, "null sink");
+  if (n < 0 || (n > 0 && !d_tris)) fail(PLMSS_ERR_INVALID_ARGUMENT, "bad separator records");
+  if (chunk <= 0) chunk = int64_t(1) << 22;
+  chunk = std::min(chunk, std::max<int64_t>(n, 1));
+  const size_t rec = label_type == 0 ? sizeof(plmss_tri) : sizeof(plmss_tri64);
+  const size_t per = size_t(chunk) * (72 + 16 + 8);  // points, regions, cells per triangle
+  char* dbuf = static_cast<char*>(c.get(S_TMP2, 2 * per));
+  char* hbuf = nullptr;
+  CK(cudaMallocHost(reinterpret_cast<void**>(&hbuf), 2 * per));
+  cudaEvent_t ev[2] = {};
+  int status = 0;
+  try {
+    for (int k = 0; k < 2; ++k) CK(cudaEventCreateWithFlags(&ev[k], cudaEventDisableTiming));
+    auto parts = [&](char* base, int64_t cnt, double*& p, int64_t*& r, int64_t*& cl) {
+      p = reinterpret_cast<double*>(base);
+      r = reinterpret_cast<int64_t*>(base + size_t(cnt) * 72);
+      cl = reinterpret_cast<int64_t*>(base + size_t(cnt) * 88);
+    };
+    const int64_t nch = (n + chunk - 1) / chunk;
+    for (int64_t k = 0; k <= nch && status == 0; ++k) {
+      if (k < nch) {
+        const int64_t t0 = k * chunk, cnt = std::min(chunk, n - t0);
+        const int s = int(k & 1);
+        double* p;
+        int64_t *r, *cl;
+        parts(dbuf + s * per, cnt, p, r, cl);
+        materialize(c, g, sp, og, label_type, static_cast<const char*>(d_tris) + size_t(t0) * rec, cnt, p, r, cl);
+        CK(cudaMemcpyAsync(hbuf + s * per, dbuf + s * per, size_t(cnt) * 96, cudaMemcpyDeviceToHost, c.stream));
+        CK(cudaEventRecord(ev[s], c.stream));
+      }
+      if (k >= 1) {  // hand chunk k-1 to the sink while chunk k is in flight
+        const int64_t t0 = (k - 1) * chunk, cnt = std::min(chunk, n - t0);
+        const int s = int((k - 1) & 1);
+        CK(cudaEventSynchronize(ev[s]));
+        double* p;
+        int64_t *r, *cl;
+        parts(hbuf + s * per, cnt, p, r, cl);
+        status = sink(user, t0, cnt, p, r, cl);
+      }
+    }
+    c.sync();
+  } catch (...) {
+    for (auto e : ev)
+      if (e) cudaEventDestroy(e);
+    cudaFreeHost(hbuf);
+    throw;
+  }
+  for (auto e : ev) cudaEventDestroy(e);
+  CK(cudaFreeHost(hbuf));
+  if (status) fail(PLMSS_ERR_LOGIC, "geometry sink stopped the stream (status " + std::to_string(status) + ")");
 }
 
 }  // namespace plmss_b200
