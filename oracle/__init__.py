@@ -321,6 +321,8 @@ class Reference:
             L.cap_records_copy.restype = None
             L.cap_records_free.argtypes = [C.c_void_p]
             L.cap_records_free.restype = None
+            L.cap_records_geometry.argtypes = [C.c_void_p] * 4
+            L.cap_records_geometry.restype = None
         if hasattr(L, "cap_weld"):
             L.cap_weld.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.POINTER(C.c_int64)]
             L.cap_read_volume.argtypes = [C.c_char_p, _i64p, C.c_char_p, C.c_void_p]
@@ -356,7 +358,7 @@ class Reference:
         self._check(self.lib.cap_write_obj(os.fsencode(str(path)), p.ctypes.data, p.shape[0], i.ctypes.data,
                                            r.ctypes.data, r.shape[0], verts_per_prim))
 
-    def records_chunk(self, dims, labels_slab, cz0, cz1, workers=1):
+    def records_chunk(self, dims, labels_slab, cz0, cz1, workers=1, geometry=False):
         """Reference separator records (TRI_DTYPE) of cube layers [cz0, cz1)
         of a (X, Y, Z) grid; labels_slab = int64 labels of vertex layers
         [cz0, cz1] (ref_capi.cpp cap_records_chunk)."""
@@ -369,6 +371,13 @@ class Reference:
         try:
             out = np.empty(max(k.value, 1), TRI_DTYPE)
             self.lib.cap_records_copy(h, out.ctypes.data)
+            if geometry:  # + the reference SeparatingMesh arrays of the chunk
+                n = k.value
+                pts = np.empty((max(3 * n, 1), 3), np.float64)
+                reg = np.empty((max(n, 1), 2), np.int64)
+                cel = np.empty(max(n, 1), np.int64)
+                self.lib.cap_records_geometry(h, pts.ctypes.data, reg.ctypes.data, cel.ctypes.data)
+                return out[:n], dict(points=pts[: 3 * n], regions=reg[:n], source_cells=cel[:n])
         finally:
             self.lib.cap_records_free(h)
         return out[: k.value]

@@ -392,6 +392,9 @@ struct RecordsOut {
     uint32_t lo, hi;
   };
   std::vector<Rec> rec;
+  // the reference mesh of the chunk (global cell ids), for geometry digests
+  std::vector<double> points;
+  std::vector<int64_t> regions, cells;
 };
 
 int cap_records_chunk(const int64_t* dims, const int64_t* labels, int64_t cz0, int64_t cz1, int workers,
@@ -409,6 +412,9 @@ int cap_records_chunk(const int64_t* dims, const int64_t* labels, int64_t cz0, i
     *handle = res;
     *count = np;
     res->rec.resize(size_t(np));
+    res->regions.resize(2 * size_t(np));
+    res->cells.resize(size_t(np));
+    res->points.assign(mesh.points.data(), mesh.points.data() + 3 * mesh.points.cols());  // column-major 3 x N
     // kTetraData row offsets (the GPU table numbering, marching_tables.cpp:48-116)
     const auto* data0 = plmss::tables::tetra_case(3).data();
     RecordsOut::Rec* rec = res->rec.data();
@@ -442,6 +448,9 @@ int cap_records_chunk(const int64_t* dims, const int64_t* labels, int64_t cz0, i
       if (mesh.regions[j][0] != std::min(la, lb) || mesh.regions[j][1] != std::max(la, lb))
         throw std::logic_error("cap_records_chunk: region pair mismatch");
       rec[j].cellrow = (uint64_t(cell_base + c) << 6) | uint64_t(&row - data0);
+      res->regions[2 * j] = mesh.regions[j][0];
+      res->regions[2 * j + 1] = mesh.regions[j][1];
+      res->cells[j] = cell_base + c;
       rec[j].lo = uint32_t(mesh.regions[j][0]);
       rec[j].hi = uint32_t(mesh.regions[j][1]);
     }
@@ -454,5 +463,14 @@ void cap_records_copy(void* handle, void* out) {
 }
 
 void cap_records_free(void* handle) { delete static_cast<RecordsOut*>(handle); }
+
+// The chunk's SeparatingMesh arrays: points (3 per corner, 9 per triangle),
+// regions (2 per triangle), source cells (global).
+void cap_records_geometry(void* handle, double* points, int64_t* regions, int64_t* cells) {
+  auto* r = static_cast<RecordsOut*>(handle);
+  if (points && !r->points.empty()) std::memcpy(points, r->points.data(), r->points.size() * sizeof(double));
+  if (regions && !r->regions.empty()) std::memcpy(regions, r->regions.data(), r->regions.size() * sizeof(int64_t));
+  if (cells && !r->cells.empty()) std::memcpy(cells, r->cells.data(), r->cells.size() * sizeof(int64_t));
+}
 
 }  // extern "C"

@@ -102,14 +102,52 @@ def make(name: str, workers: int, chunk_layers: int) -> dict:
     return out
 
 
+def add_geometry(name: str, workers: int, chunk_layers: int) -> dict:
+    """Digests of the reference SeparatingMesh arrays (marching.hpp:65-76:
+    points, regions, source_cells) of an existing digest file's config, from
+    the compiled reference's emit_separators in z-chunks; the chunks' records
+    must reproduce the file's record digest."""
+    path = os.path.join(HERE, f"{name}_digest.json")
+    out = json.load(open(path))
+    cfg = CONFIGS[name]
+    X, Y, Z = cfg.dims
+    XY = X * Y
+    R = oracle.Restatement()
+    F = oracle.Reference()
+    t0 = time.time()
+    s = R.segment_u32(cfg.dims, R.synth(cfg))
+    ms, _ = R.combine_ms_u32(s["asc"], s["desc"])
+    del s
+    hs = {k: ChunkedSha256() for k in ("tris", "points", "regions", "source_cells")}
+    for cz0 in range(0, Z - 1, chunk_layers):
+        cz1 = min(cz0 + chunk_layers, Z - 1)
+        rec, geo = F.records_chunk(cfg.dims, ms[cz0 * XY:(cz1 + 1) * XY].astype(np.int64), cz0, cz1,
+                                   workers=workers, geometry=True)
+        hs["tris"].update(rec)
+        for k in ("points", "regions", "source_cells"):
+            hs[k].update(geo[k])
+        del rec, geo
+        for h in hs.values():
+            h.drain()
+    got = {k: h.hexdigest() for k, h in hs.items()}
+    if got.pop("tris") != out["tris"]:
+        raise SystemExit(f"{name}: geometry pass records differ from the stored record digest")
+    out["geometry"] = dict(got, source="compiled reference emit_separators in z-chunks (SeparatingMesh arrays: "
+                                       "points f64 x3 per corner, regions i64 x2, source_cells i64)")
+    log(name, "geometry", f"{time.time() - t0:.1f}s")
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("configs", nargs="*", default=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
     ap.add_argument("--workers", type=int, default=os.cpu_count() or 1)
     ap.add_argument("--chunk-layers", type=int, default=16)
+    ap.add_argument("--geometry", action="store_true", help="add SeparatingMesh digests to existing files")
     args = ap.parse_args()
     for name in args.configs:
-        d = make(name, args.workers, args.chunk_layers)
+        d = add_geometry(name, args.workers, args.chunk_layers) if args.geometry else \
+            make(name, args.workers, args.chunk_layers)
         with open(os.path.join(HERE, f"{name}_digest.json"), "w") as fh:
             json.dump(d, fh, indent=1)
             fh.write("\n")
