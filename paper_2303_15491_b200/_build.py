@@ -32,20 +32,26 @@ def _stale(target: str, deps: list[str]) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build_cuda(force: bool = False, verbose: bool = False) -> str:
+LIB_CHECKED = os.path.join(PKG, "libplmss_b200_checked.so")
+
+
+def build_cuda(force: bool = False, verbose: bool = False, checked: bool = False) -> str:
+    """checked=True: libplmss_b200_checked.so with the device bounds checks
+    (-DPLMSS_CHECKED, fused.cu DCHECK), loaded when PLMSS_B200_LIB points at it."""
+    lib_path = LIB_CHECKED if checked else LIB
     deps = [os.path.join(CSRC, s) for s in SOURCES]
     deps += [os.path.join(CSRC, h) for h in os.listdir(CSRC) if h.endswith((".cuh", ".h"))]
     deps.append(os.path.join(INCLUDE, "plmss_b200.h"))
-    if not force and not _stale(LIB, deps):
-        return LIB
-    objdir = os.path.join(PKG, "_obj")
+    if not force and not _stale(lib_path, deps):
+        return lib_path
+    objdir = os.path.join(PKG, "_obj_checked" if checked else "_obj")
     os.makedirs(objdir, exist_ok=True)
     objs = []
     procs = []
     for s in SOURCES:
         obj = os.path.join(objdir, s.replace(".cu", ".o"))
         objs.append(obj)
-        cmd = [NVCC] + NVCC_FLAGS + ["-c", os.path.join(CSRC, s), "-o", obj]
+        cmd = [NVCC] + NVCC_FLAGS + (["-DPLMSS_CHECKED"] if checked else []) + ["-c", os.path.join(CSRC, s), "-o", obj]
         if verbose:
             print(" ".join(cmd))
         procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
@@ -55,9 +61,9 @@ def build_cuda(force: bool = False, verbose: bool = False) -> str:
             raise RuntimeError("nvcc failed: " + " ".join(cmd) + "\n" + out.decode())
         if verbose and out:
             print(out.decode())
-    link = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcudart"]
+    link = [NVCC] + ARCH + ["-shared", "-o", lib_path] + objs + ["-lcudart"]
     subprocess.run(link, check=True)
-    return LIB
+    return lib_path
 
 
 DROPIN_DIR = os.path.join(CSRC, "dropin")

@@ -20,7 +20,9 @@ from typing import Optional
 import numpy as np
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libplmss_b200.so")
+# PLMSS_B200_LIB: an alternative build of the same library (the checked
+# build, libplmss_b200_checked.so, tools/checked_run.py)
+LIB_PATH = os.environ.get("PLMSS_B200_LIB") or os.path.join(PKG, "libplmss_b200.so")
 
 KEY_F32, KEY_F64, KEY_RANK = 0, 1, 2
 ASCENDING, DESCENDING, BOTH = 0, 1, 2

@@ -39,6 +39,23 @@
 
 namespace plmss_b200 {
 
+// Checked build (libplmss_b200_checked.so, _build.build_cuda(checked=True)):
+// bounds of every computed index into a table, list, bitmap or output of the
+// fused and z-slab passes are asserted on the device; the first failure's
+// code is reported by the host driver as PLMSS_ERR_LOGIC. compute-sanitizer
+// is not available on the GPU pool, this is its stand-in (tools/checked_run.py).
+#ifdef PLMSS_CHECKED
+__device__ unsigned long long g_check_fail;
+#define DCHECK(cond, code)                                                                 \
+  do {                                                                                     \
+    if (!(cond)) atomicCAS(&::plmss_b200::g_check_fail, 0ull, (unsigned long long)(code)); \
+  } while (0)
+#else
+#define DCHECK(cond, code) \
+  do {                     \
+  } while (0)
+#endif
+
 namespace {
 
 constexpr int TX = 32, TY = 32, TZ = 32;
@@ -372,7 +389,9 @@ __global__ void __launch_bounds__(A_THREADS, 1)
       const int h = hc + (lz + 1) * PXY, h2 = hc + (lz2 + 1) * PXY;
       if (live_d & (bit | bit2)) {
         const uint32_t p1 = Pd[h], r1 = Pd[h2];
+        DCHECK(p1 < PN && r1 < PN, 101);
         const uint32_t p2 = Pd[p1], r2 = Pd[r1];
+        DCHECK(p2 < PN && r2 < PN, 101);
         const uint32_t p3 = Pd[p2], r3 = Pd[r2];
         Pd[h] = uint16_t(p3);
         Pd[h2] = uint16_t(r3);
@@ -381,7 +400,9 @@ __global__ void __launch_bounds__(A_THREADS, 1)
       }
       if (live_a & (bit | bit2)) {
         const uint32_t q1 = Pa[h], s1 = Pa[h2];
+        DCHECK(q1 < PN && s1 < PN, 102);
         const uint32_t q2 = Pa[q1], s2 = Pa[s1];
+        DCHECK(q2 < PN && s2 < PN, 102);
         const uint32_t q3 = Pa[q2], s3 = Pa[s2];
         Pa[h] = uint16_t(q3);
         Pa[h2] = uint16_t(s3);
@@ -537,6 +558,7 @@ __global__ void __launch_bounds__(A_THREADS, 1)
       const int h = hc + (lz + 1) * PXY;
       const uint32_t bit = 1u << lz;
       const uint32_t pd = Pd[h], pa = Pa[h];
+      DCHECK(pd < PN && pa < PN, 103);
       od[TX * TY * lz] = (mmax & bit) ? uint16_t(pd) : Pd[pd];
       oa[TX * TY * lz] = (mmin & bit) ? uint16_t(pa) : Pa[pa];
     }
@@ -561,7 +583,7 @@ __global__ void __launch_bounds__(256) k_tt_succ(const uint4* __restrict__ TB, c
                                                  const uint16_t* __restrict__ ltd,
                                                  const uint16_t* __restrict__ lta, const uint32_t* __restrict__ RK,
                                                  uint32_t* __restrict__ SD, uint32_t* __restrict__ SA,
-                                                 uint32_t pbase) {
+                                                 uint32_t pbase, uint64_t nt) {
   const uint4 h = TB[blockIdx.x];
   const uint32_t n = h.y + h.z + h.w;
   const uint32_t* TBw = reinterpret_cast<const uint32_t*>(TB);
@@ -573,9 +595,11 @@ __global__ void __launch_bounds__(256) k_tt_succ(const uint4* __restrict__ TB, c
       if (pbase && bm >= pbase) {
         sd = sa = kFinal | kPortal | (bm - pbase);  // resolved across ranks (slab_resolve)
       } else {
+        DCHECK((bm >> 15) < gridDim.x, 201);
         const uint32_t nb = __ldg(TBw + 4 * (bm >> 15));
         sd = nb + __ldg(ltd + bm);
         sa = nb + __ldg(lta + bm);
+        DCHECK(sd < nt && sa < nt, 202);
       }
     } else {
       // a maximum is only reached by descending-manifold chains, a minimum
@@ -585,6 +609,7 @@ __global__ void __launch_bounds__(256) k_tt_succ(const uint4* __restrict__ TB, c
       sd = is_max ? r : kFinal;
       sa = is_max ? kFinal : r;
     }
+    DCHECK(k < nt, 203);
     SD[k] = sd;
     SA[k] = sa;
   }
@@ -611,6 +636,8 @@ __global__ void __launch_bounds__(256) k_tt_jump(uint64_t nt, uint32_t* __restri
     uint32_t xd = d0, xa = a0, yd = e0, ya = b0;
 #pragma unroll 4
     for (int k = 0; k < kChase && !(xd & xa & yd & ya & kFinal); ++k) {
+      DCHECK(((xd & kFinal) || xd < nt) && ((xa & kFinal) || xa < nt) && ((yd & kFinal) || yd < nt) &&
+                 ((ya & kFinal) || ya < nt), 301);
       if (!(xd & kFinal)) xd = SD[xd];
       if (!(xa & kFinal)) xa = SA[xa];
       if (!(yd & kFinal)) yd = SD[yd];
@@ -898,6 +925,8 @@ struct BrickArgs {
   const uint32_t *FD, *FA;        // per table entry: rank of the maximum / minimum
   const uint32_t *maxs, *mins;    // sorted extremum lists (rank -> vertex id)
   uint32_t nmax;                  // dense mode: key = rank_min * nmax + rank_max
+  uint32_t nmin;                  // (checked build: bounds)
+  uint64_t nt, nw;                // table entries, bitmap words (checked build: bounds)
   uint32_t* bitmap;               // dense mode: region bitmap
   unsigned long long* fset;       // hash mode: region set of (rank_min << 32 | rank_max)
   uint64_t fmask;
@@ -946,6 +975,7 @@ __global__ void __launch_bounds__(32 * kTokRows) k_tokens(const BrickArgs a) {
 #pragma unroll
     for (int i = 0; i < kTokZ; ++i) {
       if (z0 + i < nz) {
+        DCHECK(base + ld[i] < a.nt && base + la[i] < a.nt, 403);
         ld[i] = __ldg(fd + ld[i]);  // rank of the maximum | kFinal
         la[i] = __ldg(fa + la[i]);  // rank of the minimum | kFinal
       }
@@ -964,11 +994,13 @@ __global__ void __launch_bounds__(32 * kTokRows) k_tokens(const BrickArgs a) {
       }
       ld[i] &= ~kFinal;
       la[i] &= ~kFinal;
+      DCHECK(ld[i] < a.nmax && la[i] < a.nmin, 401);
       const Key key = kDense ? Key(la[i] * a.nmax + ld[i]) : Key((uint64_t(la[i]) << 32) | ld[i]);
       if (key != lkey) {
         if (kDense) {
           ltok = uint32_t(key);
           const uint32_t bit = 1u << (ltok & 31);
+          DCHECK((ltok >> 5) < a.nw, 402);
           uint32_t* wp = a.bitmap + (ltok >> 5);
           if (!(*wp & bit)) atomicOr(wp, bit);
         } else {
@@ -1043,6 +1075,7 @@ __device__ __forceinline__ void tokens_tma_body(const CUtensorMap& mld, const CU
 #pragma unroll
     for (int i = 0; i < kTokZ; ++i) {
       if (kF || z0 + i < nz) {
+        DCHECK(base + sd[z0 + i][l] < a.nt && base + sa[z0 + i][l] < a.nt, 404);
         ld[i] = __ldg(fd + sd[z0 + i][l]);  // rank of the maximum | kFinal
         la[i] = __ldg(fa + sa[z0 + i][l]);  // rank of the minimum | kFinal
       }
@@ -1061,11 +1094,13 @@ __device__ __forceinline__ void tokens_tma_body(const CUtensorMap& mld, const CU
       }
       ld[i] &= ~kFinal;
       la[i] &= ~kFinal;
+      DCHECK(ld[i] < a.nmax && la[i] < a.nmin, 401);
       const Key key = kDense ? Key(la[i] * a.nmax + ld[i]) : Key((uint64_t(la[i]) << 32) | ld[i]);
       if (key != lkey) {
         if (kDense) {
           ltok = uint32_t(key);
           const uint32_t bit = 1u << (ltok & 31);
+          DCHECK((ltok >> 5) < a.nw, 402);
           uint32_t* wp = a.bitmap + (ltok >> 5);
           if (!(*wp & bit)) atomicOr(wp, bit);
         } else {
@@ -1569,6 +1604,7 @@ __global__ void __launch_bounds__(256) k_emit_chunks(const EmitArgs a) {
           lb = __ldg(a.ids + (vs + corner_off(r >> 24)));
         }
         const uint64_t cr64 = ((6ull * (a.cube0 + uint64_t(q0 + uint32_t(src))) + t) << 6) | uint64_t(rowi);
+        DCHECK(base + j < a.total, 501);
         *reinterpret_cast<uint4*>(a.out + base + j) =
             make_uint4(uint32_t(cr64), uint32_t(cr64 >> 32), min(la, lb), max(la, lb));
       }
@@ -1762,6 +1798,24 @@ static void ensure_consts(Ctx& c) {
   }
 }
 
+// Checked build: fail on the first device bounds check that did not hold.
+static void check_device(Ctx& c, const char* where) {
+#ifdef PLMSS_CHECKED
+  unsigned long long v = 0;
+  CK(cudaMemcpyFromSymbolAsync(&v, g_check_fail, sizeof v, 0, cudaMemcpyDeviceToHost, c.stream));
+  c.sync();
+  if (v) {
+    const unsigned long long zero = 0;
+    CK(cudaMemcpyToSymbolAsync(g_check_fail, &zero, sizeof zero, 0, cudaMemcpyHostToDevice, c.stream));
+    c.sync();
+    fail(PLMSS_ERR_LOGIC, std::string("device bounds check ") + std::to_string(v) + " failed in " + where);
+  }
+#else
+  (void)c;
+  (void)where;
+#endif
+}
+
 FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* desc, uint32_t* asc, uint32_t* ms) {
   FusedOut o{};
   for (auto& s : c.stats) s = 0;
@@ -1887,7 +1941,7 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
     // ---- B: terminal-table forest -> extremum rank of every table entry
     uint32_t* SD = c.get_t<uint32_t>(S_SD, nt);
     uint32_t* SA = c.get_t<uint32_t>(S_SA, nt);
-    k_tt_succ<<<unsigned(ntiles), 256, 0, c.stream>>>(TB, TT, ltd, lta, RK, SD, SA, 0u);
+    k_tt_succ<<<unsigned(ntiles), 256, 0, c.stream>>>(TB, TT, ltd, lta, RK, SD, SA, 0u, nt);
     CK_LAUNCH("k_tt_succ");
     // Two sweeps are enqueued without waiting (they converge on smooth
     // fields); passes C and D follow speculatively and the convergence flag
@@ -1918,6 +1972,8 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
     ba.maxs = maxima;
     ba.mins = minima;
     ba.nmax = uint32_t(o.n_max);
+    ba.nmin = uint32_t(o.n_min);
+    ba.nt = nt;
     ba.desc = desc;
     ba.asc = asc;
     ba.ms = ms;
@@ -1952,6 +2008,7 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
       bitmap = c.get_t<uint32_t>(S_BITMAP, nw);
       CK(cudaMemsetAsync(bitmap, 0, nw * 4, c.stream));
       ba.bitmap = bitmap;
+      ba.nw = nw;
       // z-slab pipeline: tokens of brick layer s on the main stream; the
       // count pass of layer s-1 (which reads layer s's first vertex layer)
       // on the side stream as soon as they are written
@@ -2114,6 +2171,7 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
       }
       continue;
     }
+    check_device(c, "fused_pipeline");
     o.n_tris = int64_t(total);
     o.tris = tris;
     o.maxima = maxima;
@@ -2291,7 +2349,7 @@ void slab_segment(Ctx& c, const Grid& g, int64_t z0, int64_t z1, const float* fi
   // the forest inside the slab, to its fixpoint (portals are roots)
   uint32_t* SD = c.get_t<uint32_t>(S_SD, nt);
   uint32_t* SA = c.get_t<uint32_t>(S_SA, nt);
-  k_tt_succ<<<unsigned(ntiles), 256, 0, c.stream>>>(TB, TT, ltd, lta, RK, SD, SA, d.pbase);
+  k_tt_succ<<<unsigned(ntiles), 256, 0, c.stream>>>(TB, TT, ltd, lta, RK, SD, SA, d.pbase, nt);
   CK_LAUNCH("k_tt_succ");
   int* jflag = reinterpret_cast<int*>(ctr_base + 192);
   for (;;) {
@@ -2308,6 +2366,7 @@ void slab_segment(Ctx& c, const Grid& g, int64_t z0, int64_t z1, const float* fi
   k_slab_boundary<<<blocks_for(2 * int64_t(d.XY), 256), 256, 0, c.stream>>>(d, TB, ltd, lta, SD, SA, bnd);
   CK_LAUNCH("k_slab_boundary");
   c.sync();
+  check_device(c, "slab_segment");
   st.stage = 1;
   if (info) {
     *info = plmss_slab_info{};
@@ -2372,6 +2431,8 @@ void slab_resolve(Ctx& c, const uint32_t* G, int world, int rank, const int64_t*
   ba.maxs = maxs_g;
   ba.mins = mins_g;
   ba.nmax = uint32_t(smax);
+  ba.nmin = uint32_t(smin);
+  ba.nt = st.nt;
   ba.desc = desc;
   ba.asc = asc;
   ba.ms = ms;
@@ -2387,6 +2448,7 @@ void slab_resolve(Ctx& c, const uint32_t* G, int world, int rank, const int64_t*
     uint32_t* bitmap = c.get_t<uint32_t>(S_BITMAP, nw);
     CK(cudaMemsetAsync(bitmap, 0, nw * 4, c.stream));
     ba.bitmap = bitmap;
+    ba.nw = nw;
     if (lt_tma)
       k_tokens_tma<true><<<tgrid, 32 * kTokRows, 0, c.stream>>>(mld, mla, ba);
     else
@@ -2443,6 +2505,7 @@ void slab_resolve(Ctx& c, const uint32_t* G, int world, int rank, const int64_t*
   c.sync();
   const int e = *reinterpret_cast<int*>(c.h_pinned);
   if (e) fail(PLMSS_ERR_LOGIC, e == 2 ? "z-slab forest entry unresolved" : "z-slab portal chain broken");
+  check_device(c, "slab_resolve");
   st.stage = 2;
   if (info) {
     info->n_maxima = smax;
@@ -2507,6 +2570,7 @@ void slab_ids(Ctx& c, const uint64_t* keys_all, int64_t n_keys_all, plmss_slab_i
     CK_LAUNCH("k_keys_to_gid");
   }
   c.sync();
+  check_device(c, "slab_ids");
   st.stage = 3;
   if (info) {
     info->n_regions = st.R;
@@ -2568,6 +2632,7 @@ void slab_emit(Ctx& c, plmss_slab_info* info) {
   c.sync();
   st.n_tris = int64_t(total);
   st.tris = tris;
+  check_device(c, "slab_emit");
   st.stage = 4;
   if (info) {
     info->n_tris = st.n_tris;
