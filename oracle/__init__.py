@@ -314,6 +314,10 @@ class Reference:
         L.cap_run_benchmark.argtypes = [_i64p, _f64p, C.c_int, C.c_int, C.c_int, _f64p]
         L.cap_run_once.argtypes = [_i64p, np.ctypeslib.ndpointer(np.float32, flags="C_CONTIGUOUS"), C.c_int,
                                    C.c_int, _f64p, _i64p]
+        if hasattr(L, "cap_seed_hops"):
+            L.cap_seed_hops.argtypes = [_i64p, _i64p, C.c_int64, C.c_int, C.c_int64, C.c_int64] + [C.c_void_p] * 8
+            L.cap_compress_sweep.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p,
+                                             C.c_void_p]
         if hasattr(L, "cap_records_chunk"):
             L.cap_records_chunk.argtypes = [_i64p, _i64p, C.c_int64, C.c_int64, C.c_int, C.POINTER(C.c_void_p),
                                             C.POINTER(C.c_int64)]
@@ -357,6 +361,30 @@ class Reference:
         r = np.ascontiguousarray(regions, dtype=np.int64).reshape(-1, 2)
         self._check(self.lib.cap_write_obj(os.fsencode(str(path)), p.ctypes.data, p.shape[0], i.ctypes.data,
                                            r.ctypes.data, r.shape[0], verts_per_prim))
+
+    def detail_seed_hops(self, dims, rank, mode, begin=0, end=None):
+        """detail::seed_hops (mode 0 descending / 1 ascending) or
+        seed_hops_both (mode 2) over [begin, end) (segmentation.hpp:90-113):
+        (desc, asc, active, extrema1, extrema2); unset label entries are -1."""
+        d = _dims(dims)
+        r = np.ascontiguousarray(rank, dtype=np.int64).ravel()
+        n = r.size
+        end = n if end is None else end
+        out = [np.empty(n, np.int64) for _ in range(5)]
+        cnt = [C.c_int64() for _ in range(3)]
+        self._check(self.lib.cap_seed_hops(d, r, n, mode, begin, end, out[0].ctypes.data, out[1].ctypes.data,
+                                           out[2].ctypes.data, C.byref(cnt[0]), out[3].ctypes.data, C.byref(cnt[1]),
+                                           out[4].ctypes.data, C.byref(cnt[2])))
+        return out[0], out[1], out[2][: cnt[0].value], out[3][: cnt[1].value], out[4][: cnt[2].value]
+
+    def detail_compress_sweep(self, desc, asc, active):
+        """One detail::compress_sweep(_both) in place (asc None: single)."""
+        act = np.ascontiguousarray(active, dtype=np.int64)
+        nxt = np.empty(max(act.size, 1), np.int64)
+        k = C.c_int64()
+        self._check(self.lib.cap_compress_sweep(desc.ctypes.data, None if asc is None else asc.ctypes.data, desc.size,
+                                                act.ctypes.data, act.size, nxt.ctypes.data, C.byref(k)))
+        return nxt[: k.value]
 
     def records_chunk(self, dims, labels_slab, cz0, cz1, workers=1, geometry=False):
         """Reference separator records (TRI_DTYPE) of cube layers [cz0, cz1)

@@ -157,6 +157,46 @@ void cap_seg_copy(void* handle, int which, int64_t* out) {
 
 void cap_seg_free(void* handle) { delete static_cast<plmss::SegmentationResult*>(handle); }
 
+// detail:: step functions (segmentation.hpp:90-121) of whichever library this
+// file is linked against (the compiled reference or the B200 drop-in).
+// mode 0 / 1: seed_hops descending / ascending into desc; 2: seed_hops_both.
+int cap_seed_hops(const int64_t* dims, const int64_t* rank, int64_t n, int mode, int64_t begin, int64_t end,
+                  int64_t* desc, int64_t* asc, int64_t* active, int64_t* n_active, int64_t* ext1, int64_t* n_ext1,
+                  int64_t* ext2, int64_t* n_ext2) {
+  return guarded([&] {
+    const auto grid = make_grid(dims, nullptr, nullptr);
+    const auto order = order_from(rank, n);
+    std::vector<plmss::VertexId> d(size_t(n), -1), a(size_t(n), -1), act, e1, e2;
+    if (mode == 2)
+      plmss::detail::seed_hops_both(grid, order, begin, end, d, a, act, e1, e2);
+    else
+      plmss::detail::seed_hops(grid, order, mode == 1, begin, end, d, act, e1);
+    std::memcpy(desc, d.data(), sizeof(int64_t) * size_t(n));
+    if (asc) std::memcpy(asc, a.data(), sizeof(int64_t) * size_t(n));
+    auto out = [](const std::vector<plmss::VertexId>& v, int64_t* dst, int64_t* cnt) {
+      *cnt = int64_t(v.size());
+      if (dst && !v.empty()) std::memcpy(dst, v.data(), sizeof(int64_t) * v.size());
+    };
+    out(act, active, n_active);
+    out(e1, ext1, n_ext1);
+    out(e2, ext2, n_ext2);
+  });
+}
+
+// One compress_sweep (asc == NULL) / compress_sweep_both, labels in place.
+int cap_compress_sweep(int64_t* desc, int64_t* asc, int64_t n, const int64_t* active, int64_t na, int64_t* next,
+                       int64_t* n_next) {
+  return guarded([&] {
+    std::span<plmss::VertexId> d(desc, size_t(n));
+    std::span<const plmss::VertexId> act(active, size_t(na));
+    const std::vector<plmss::VertexId> nx =
+        asc ? plmss::detail::compress_sweep_both(d, std::span<plmss::VertexId>(asc, size_t(n)), act)
+            : plmss::detail::compress_sweep(d, act);
+    *n_next = int64_t(nx.size());
+    if (!nx.empty()) std::memcpy(next, nx.data(), sizeof(int64_t) * nx.size());
+  });
+}
+
 int cap_oracle_walk(const int64_t* dims, const int64_t* rank, int64_t n, int64_t v,
                     int direction, int64_t* out) {
   return guarded([&] {

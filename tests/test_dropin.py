@@ -122,3 +122,88 @@ def test_dropin_weld_points_matches_reference(gpu, dropin, reference, name):
     dp, di = dropin.weld_points(sep["points"], sep["indices"])
     assert rp.shape[0] < sep["points"].shape[0]
     assert np.array_equal(dp.view(np.uint64), rp.view(np.uint64)) and np.array_equal(di, ri)
+
+
+# ------------------------------------------------ detail:: step exports --
+def _detail_fields():
+    rng = np.random.default_rng(23)
+    out = []
+    for dims, kind in (((7, 6, 5), "ties"), ((12, 9, 8), "noise"), ((33, 5, 6), "ties")):
+        n = int(np.prod(dims))
+        f = rng.integers(0, 3, n).astype(np.float64) if kind == "ties" else rng.random(n)
+        out.append((dims, f))
+    g = load_case("gauss_17x13x11")
+    out.append((tuple(int(x) for x in g["dims"]), g["field"].astype(np.float64)))
+    return out
+
+
+def _on_chain(hop, v, lab):
+    """lab lies on v's steepest chain (hop = the seed hops)."""
+    x = v
+    for _ in range(hop.size + 1):
+        if x == lab:
+            return True
+        if hop[x] == x:
+            return False
+        x = hop[x]
+    return False
+
+
+@pytest.mark.gpu
+def test_dropin_detail_seed_hops_match_reference(gpu, dropin, reference):
+    """detail::seed_hops / seed_hops_both (segmentation.cpp:26-85) through the
+    drop-in: labels over [begin, end) and the active / extremum lists equal
+    the compiled reference's, including partial ranges."""
+    for dims, f in _detail_fields():
+        rank = reference.compute_order(f)
+        n = rank.size
+        for begin, end in ((0, n), (n // 3, 2 * n // 3 + 1)):
+            for mode in (0, 1, 2):
+                got = dropin.detail_seed_hops(dims, rank, mode, begin, end)
+                want = reference.detail_seed_hops(dims, rank, mode, begin, end)
+                sl = slice(begin, end)
+                assert np.array_equal(got[0][sl], want[0][sl]), (dims, mode)
+                if mode == 2:
+                    assert np.array_equal(got[1][sl], want[1][sl]), (dims, mode)
+                for k in (2, 3, 4):
+                    assert np.array_equal(got[k], want[k]), (dims, mode, k)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("both", [False, True])
+def test_dropin_detail_compress_sweeps_reach_the_reference_fixpoint(gpu, dropin, reference, both):
+    """detail::compress_sweep(_both) (segmentation.cpp:46-105): the reference's
+    own sweeps are schedule-dependent across workers (relaxed atomics), so
+    the contract checked per sweep is the pointer-jumping one — every label
+    stays on its vertex's steepest chain, the next list is an in-order subset
+    of the active list holding every vertex not yet settled — and the
+    fixpoint after the last sweep equals the reference's exactly."""
+    for dims, f in _detail_fields():
+        rank = reference.compute_order(f)
+        mode = 2 if both else 0
+        d0, a0, act0, _, _ = reference.detail_seed_hops(dims, rank, mode)
+        ref = [d0.copy(), a0.copy() if both else None]
+        act = act0.copy()
+        while act.size:
+            act = reference.detail_compress_sweep(ref[0], ref[1], act)
+        mine = [d0.copy(), a0.copy() if both else None]
+        act = act0.copy()
+        for _ in range(64):
+            if not act.size:
+                break
+            prev = act
+            act = dropin.detail_compress_sweep(mine[0], mine[1], act)
+            pos = {int(v): i for i, v in enumerate(prev)}
+            idx = [pos[int(v)] for v in act]
+            assert idx == sorted(idx) and len(set(idx)) == len(idx), "next is an in-order subset of active"
+            for arr, hop in ((mine[0], d0), (mine[1], a0)):
+                if arr is None:
+                    continue
+                for v in prev[:: max(1, prev.size // 200)]:
+                    assert _on_chain(hop, int(v), int(arr[v])), "label left the steepest chain"
+                unsettled = [int(v) for v in prev if arr[arr[v]] != arr[v]]
+                assert set(unsettled) <= set(int(v) for v in act), "an unsettled vertex was dropped"
+        assert not act.size
+        assert np.array_equal(mine[0], ref[0])
+        if both:
+            assert np.array_equal(mine[1], ref[1])

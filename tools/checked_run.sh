@@ -10,6 +10,7 @@ cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
 export PLMSS_B200_LIB=$PWD/paper_2303_15491_b200/libplmss_b200_checked.so
 test -f "$PLMSS_B200_LIB" || { echo "missing $PLMSS_B200_LIB (run __graft_entry__.build())"; exit 2; }
+python -c "import paper_2303_15491_b200.api as a; print(\"library:\", a.LIB_PATH)"
 timeout 2000 python -m pytest tests/test_full_size.py tests/test_gpu_slab.py tests/test_gpu_parity.py -m gpu -q \
   -k "not streamed" > gpurun_out/checked_run.log 2>&1
 echo "checked run rc=$?"
