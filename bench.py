@@ -387,6 +387,8 @@ def main():
     ap.add_argument("--slab", action="store_true",
                     help="run the z-slab (multi-GPU) path even at world size 1 (torchrun --nproc-per-node 1)")
     ap.add_argument("--cpu-runs", type=int, default=3, help="timed runs of the cpu_baseline sample")
+    ap.add_argument("--option", action="append", default=[], metavar="NAME=VALUE",
+                    help="context option (api.OPT_*, e.g. PASS_A_SPLIT=1); repeatable")
     ap.add_argument("--no-parity", action="store_true", help="skip the digest check of the last step's outputs")
     ap.add_argument("--ref-layers", type=int, default=64,
                     help="z-layers of the configured field in the CPU sample (reference arm and cpu_baseline)")
@@ -407,6 +409,9 @@ def main():
     torch.cuda.set_device(local)
     cfg = CONFIGS[args.config]
     ctx = P.Context(local)
+    for o in args.option:
+        name, val = o.split("=")
+        ctx.set_option(getattr(P.api, "OPT_" + name.upper()), int(val))
     if world > 1 or args.slab:
         import torch.distributed as dist
 

@@ -294,7 +294,10 @@ int plmss_b200_copy(plmss_ctx* ctx, void* dst, const void* d_src, int64_t bytes,
  *   PLMSS_OPT_SPECULATIVE_SWEEPS  forest sweeps enqueued before the fused
  *                           pipeline's passes C and D (default 1); if the
  *                           forest has not converged by then, the sweeps
- *                           continue and C, D are redone (0 forces that path). */
+ *                           continue and C, D are redone (0 forces that path);
+ *   PLMSS_OPT_PASS_A_SPLIT  1: pass A as two kernels (hop codes at high
+ *                           occupancy, then the brick compression from the
+ *                           codes), 0: one fused kernel (both are exact). */
 /* ---- callers either side of the path ------------------
  * weld_points (marching.hpp:138-140, marching.cpp:400-417): merges
  * bitwise-identical points of a separator soup in place, the first occurrence
@@ -347,7 +350,8 @@ enum plmss_option {
   PLMSS_OPT_COMBINE_PATH = 1,
   PLMSS_OPT_PIPELINE_PATH = 2,
   PLMSS_OPT_TMA = 3,
-  PLMSS_OPT_SPECULATIVE_SWEEPS = 4
+  PLMSS_OPT_SPECULATIVE_SWEEPS = 4,
+  PLMSS_OPT_PASS_A_SPLIT = 5
 };
 int plmss_b200_ctx_set_option(plmss_ctx* ctx, int option, int64_t value);
 

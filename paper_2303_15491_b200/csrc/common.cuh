@@ -76,6 +76,7 @@ enum Slot {
   S_TMP0, S_TMP1, S_TMP2, S_FIELD, S_MASK,
   S_LTD, S_LTA, S_TB, S_SD, S_SA, S_RK,  // fused pipeline: terminal indices, brick headers, table labels
   S_SLAB_BND,                             // z-slab pipeline: boundary layers
+  S_CODES,                                // split pass A: hop codes (1 B per padded brick cell)
   S_COUNT
 };
 
@@ -140,6 +141,7 @@ struct Ctx {
   int pipeline_path = 0; // PLMSS_OPT_PIPELINE_PATH: 0 fused when supported, 1 staged
   bool use_tma = true;   // PLMSS_OPT_TMA
   int spec_sweeps = 1;   // PLMSS_OPT_SPECULATIVE_SWEEPS
+  bool pass_a_split = false;  // PLMSS_OPT_PASS_A_SPLIT
   // Adaptive capacities of the fused pipeline (remembered between calls).
   uint64_t fused_exit_cap = 0, fused_pair_hint = 0, fused_tri_cap = 0, fused_ext_cap = 0;
   // Diagnostics of the last fused call: [0] exit entries, [1] pass-A retries,

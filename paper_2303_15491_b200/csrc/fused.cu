@@ -153,6 +153,77 @@ struct ACounters {
   uint32_t bad;
 };
 
+// Steepest hops of one (x, y) column of 32 vertices (segmentation.cpp:60-85)
+// from a shared-memory field box with row stride kHX and plane stride kHXY;
+// fc = the column's vertex at brick layer -1 (the box's first plane). Per
+// in-volume layer lz < nz: emit(lz, up | down << 4), 15 = no hop. The thread
+// walks its column in z keeping the 7 stencil columns in registers (7 shared
+// loads per vertex). With M = max f over the neighbours, steepest-up under
+// the (f, id) order is the highest s with f == M when M > f(v), or when
+// M == f(v) and s > 6; otherwise none. Steepest-down mirrors it (lowest s,
+// s < 7). NaN (missing) neighbours never win.
+template <int kHX, int kHXY, class Emit>
+__device__ __forceinline__ void hop_column(const float* __restrict__ fc, const int nz, const uint32_t gv0,
+                                           const uint32_t XY, ACounters* __restrict__ ctr, Emit&& emit) {
+    // stencil columns (dx, dy): c0 (-1,-1) c1 (0,-1) c2 (-1,0) c3 (0,0)
+    // c4 (1,0) c5 (0,1) c6 (1,1); s -> (column, plane):
+    //   s0-3 = c0-c3 @ z-1, s4-6 = c0-c2 @ z, s7-9 = c4-c6 @ z, s10-13 = c3-c6 @ z+1
+    float a0m = fc[-1 - kHX], a1m = fc[-kHX], a2m = fc[-1], a3m = fc[0];
+    float a0 = fc[kHXY - 1 - kHX], a1 = fc[kHXY - kHX], a2 = fc[kHXY - 1], a3 = fc[kHXY], a4 = fc[kHXY + 1],
+          a5 = fc[kHXY + kHX], a6 = fc[kHXY + kHX + 1];
+#pragma unroll 4
+    for (int lz = 0; lz < TZ; ++lz) {
+      const float* p = fc + (lz + 2) * kHXY;  // plane z+1
+      const float a3p = p[0], a4p = p[1], a5p = p[kHX], a6p = p[kHX + 1];
+      if (lz < nz) {
+        const float fv = a3;
+        if (!isfinite(fv)) atomicMin(&ctr->bad, gv0 + XY * uint32_t(lz));
+        const float fn[14] = {a0m, a1m, a2m, a3m, a0, a1, a2, a4, a5, a6, a3p, a4p, a5p, a6p};
+        // Maxima / minima of the lower (s < 7, ids below v) and upper
+        // (s >= 7) halves. The highest s attaining M lies in the upper half
+        // iff the upper half attains M; the lowest s attaining m lies in the
+        // lower half iff that one does. NaN (missing) neighbours never win.
+        float Ml = fn[0], ml = fn[0], Mh = fn[7], mh = fn[7];
+#pragma unroll
+        for (int s = 1; s < 7; ++s) {
+          Ml = fmaxf(Ml, fn[s]);
+          ml = fminf(ml, fn[s]);
+          Mh = fmaxf(Mh, fn[7 + s]);
+          mh = fminf(mh, fn[7 + s]);
+        }
+        const float M = fmaxf(Ml, Mh), m = fminf(ml, mh);
+        const bool up_hi = Mh == M, dn_lo = ml == m;
+        // which of the chosen half's 7 neighbours attain M (m): 1.0 / 0.0
+        // flags (PTX set, one ALU op each) summed with weights 2^i
+        // (2^(6-i)) on the FMA pipe; the highest weight present is the
+        // float's exponent. Exact: distinct powers of two below 2^7.
+        float au = 0.f, ad = 0.f;
+#pragma unroll
+        for (int i = 0; i < 7; ++i) {
+          au = __fmaf_rn(feq(up_hi ? fn[7 + i] : fn[i], M), float(1 << i), au);
+          ad = __fmaf_rn(feq(dn_lo ? fn[i] : fn[7 + i], m), float(1 << (6 - i)), ad);
+        }
+        // au == 0 only when every neighbour is missing (M is NaN): no hop
+        const uint32_t hu = uint32_t(__float_as_int(au) >> 23) - 127u + (up_hi ? 7u : 0u);  // highest s attaining M
+        const uint32_t hd = (dn_lo ? 6u : 13u) - (uint32_t(__float_as_int(ad) >> 23) - 127u);  // lowest s attaining m
+        const uint32_t su = (M > fv || (M == fv && up_hi)) ? hu : 15u;
+        const uint32_t sd = (m < fv || (m == fv && dn_lo)) ? hd : 15u;
+        emit(lz, uint8_t(su | (sd << 4)));
+      }
+      a0m = a0;
+      a1m = a1;
+      a2m = a2;
+      a3m = a3;
+      a0 = p[-1 - kHX];
+      a1 = p[-kHX];
+      a2 = p[-1];
+      a3 = a3p;
+      a4 = a4p;
+      a5 = a5p;
+      a6 = a6p;
+    }
+  }
+
 // ---------------------------------------------------------------- pass A --
 // One CTA (1024 threads, one per (x, y) column of 32 vertices) per 32^3
 // brick.
@@ -174,9 +245,10 @@ struct ACounters {
 //     The global id of that terminal is the vertex's partial label.
 //  5. Extrema and the distinct exit (shell) cells are appended to global
 //     lists, aggregated per brick.
-template <bool kTMA>
+template <bool kTMA, bool kCodes = false>
 __global__ void __launch_bounds__(A_THREADS, 1)
-    k_tile_segment(const __grid_constant__ CUtensorMap tmap, const float* __restrict__ field, FDims d,
+    k_tile_segment(const __grid_constant__ CUtensorMap tmap, const float* __restrict__ field,
+                   const uint8_t* __restrict__ gcodes, FDims d,
                    uint32_t* __restrict__ maxima, uint32_t* __restrict__ minima, uint32_t* __restrict__ max_tt,
                    uint32_t* __restrict__ min_tt, uint64_t ext_cap,
                    uint32_t* __restrict__ TT, uint64_t tt_cap, uint4* __restrict__ TB, uint16_t* __restrict__ ltd,
@@ -200,7 +272,7 @@ __global__ void __launch_bounds__(A_THREADS, 1)
   const int tid = int(threadIdx.x);
   const int lane = tid & 31;
   const int lx = tid & 31, ly = tid >> 5;
-  if (kTMA && tid == 0) {
+  if ((kTMA || kCodes) && tid == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s_bar)));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -212,8 +284,20 @@ __global__ void __launch_bounds__(A_THREADS, 1)
   const uint32_t tx = bt % d.tx, ty = (bt / d.tx) % d.ty, tz = bt / (d.tx * d.ty);
   const int gx0 = int(tx * TX), gy0 = int(ty * TY), gz0 = int(tz * TZ);
 
-  // 1. field box
-  if (kTMA) {
+  // 1. field box (kCodes: the brick's hop codes, one 32 KB bulk copy into
+  //    the pointer area; k_hop_codes computed them)
+  if (kCodes) {
+    if (tid == 0) {
+      const uint32_t bar = smem_u32(&s_bar);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(uint32_t(TN))
+                   : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              smem_u32(Pd)),
+          "l"(gcodes + (uint64_t(bt) << 15)), "r"(uint32_t(TN)), "r"(bar)
+          : "memory");
+    }
+  } else if (kTMA) {
     const uint32_t bar = smem_u32(&s_bar);
     if (tid == 0) {
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(uint32_t(HN * 4))
@@ -257,7 +341,7 @@ __global__ void __launch_bounds__(A_THREADS, 1)
     }
     dup[tid] = dl;  // dup[256 + c] == ddn[c]
   }
-  if (kTMA) {
+  if (kTMA || kCodes) {
     asm volatile(
         "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(
             smem_u32(&s_bar)), "r"(phase)
@@ -271,65 +355,14 @@ __global__ void __launch_bounds__(A_THREADS, 1)
   const int nz = min(TZ, int(d.Z) - gz0);  // in-volume layers of the brick
   const int hc = (lx + 1) + PX * (ly + 1);  // column in the pointer space (shell layer z = 0)
   const uint32_t gv0 = uint32_t(gx) + d.X * uint32_t(gy) + d.XY * uint32_t(gz0);
-  if (col_ok) {
-    // stencil columns (dx, dy): c0 (-1,-1) c1 (0,-1) c2 (-1,0) c3 (0,0)
-    // c4 (1,0) c5 (0,1) c6 (1,1); s -> (column, plane):
-    //   s0-3 = c0-c3 @ z-1, s4-6 = c0-c2 @ z, s7-9 = c4-c6 @ z, s10-13 = c3-c6 @ z+1
-    const float* fc = f + (ly + 1) * HX + (lx + HXO);
-    float a0m = fc[-1 - HX], a1m = fc[-HX], a2m = fc[-1], a3m = fc[0];
-    float a0 = fc[HXY - 1 - HX], a1 = fc[HXY - HX], a2 = fc[HXY - 1], a3 = fc[HXY], a4 = fc[HXY + 1],
-          a5 = fc[HXY + HX], a6 = fc[HXY + HX + 1];
-#pragma unroll 4
-    for (int lz = 0; lz < TZ; ++lz) {
-      const float* p = fc + (lz + 2) * HXY;  // plane z+1
-      const float a3p = p[0], a4p = p[1], a5p = p[HX], a6p = p[HX + 1];
-      if (lz < nz) {
-        const float fv = a3;
-        if (!isfinite(fv)) atomicMin(&ctr->bad, gv0 + d.XY * uint32_t(lz));
-        const float fn[14] = {a0m, a1m, a2m, a3m, a0, a1, a2, a4, a5, a6, a3p, a4p, a5p, a6p};
-        // Maxima / minima of the lower (s < 7, ids below v) and upper
-        // (s >= 7) halves. The highest s attaining M lies in the upper half
-        // iff the upper half attains M; the lowest s attaining m lies in the
-        // lower half iff that one does. NaN (missing) neighbours never win.
-        float Ml = fn[0], ml = fn[0], Mh = fn[7], mh = fn[7];
-#pragma unroll
-        for (int s = 1; s < 7; ++s) {
-          Ml = fmaxf(Ml, fn[s]);
-          ml = fminf(ml, fn[s]);
-          Mh = fmaxf(Mh, fn[7 + s]);
-          mh = fminf(mh, fn[7 + s]);
-        }
-        const float M = fmaxf(Ml, Mh), m = fminf(ml, mh);
-        const bool up_hi = Mh == M, dn_lo = ml == m;
-        // which of the chosen half's 7 neighbours attain M (m): 1.0 / 0.0
-        // flags (PTX set, one ALU op each) summed with weights 2^i
-        // (2^(6-i)) on the FMA pipe; the highest weight present is the
-        // float's exponent. Exact: distinct powers of two below 2^7.
-        float au = 0.f, ad = 0.f;
-#pragma unroll
-        for (int i = 0; i < 7; ++i) {
-          au = __fmaf_rn(feq(up_hi ? fn[7 + i] : fn[i], M), float(1 << i), au);
-          ad = __fmaf_rn(feq(dn_lo ? fn[i] : fn[7 + i], m), float(1 << (6 - i)), ad);
-        }
-        // au == 0 only when every neighbour is missing (M is NaN): no hop
-        const uint32_t hu = uint32_t(__float_as_int(au) >> 23) - 127u + (up_hi ? 7u : 0u);  // highest s attaining M
-        const uint32_t hd = (dn_lo ? 6u : 13u) - (uint32_t(__float_as_int(ad) >> 23) - 127u);  // lowest s attaining m
-        const uint32_t su = (M > fv || (M == fv && up_hi)) ? hu : 15u;
-        const uint32_t sd = (m < fv || (m == fv && dn_lo)) ? hd : 15u;
-        code[hc + (lz + 1) * PXY] = uint8_t(su | (sd << 4));
-      }
-      a0m = a0;
-      a1m = a1;
-      a2m = a2;
-      a3m = a3;
-      a0 = p[-1 - HX];
-      a1 = p[-HX];
-      a2 = p[-1];
-      a3 = a3p;
-      a4 = a4p;
-      a5 = a5p;
-      a6 = a6p;
-    }
+  if (!kCodes && col_ok)
+    hop_column<HX, HXY>(f + (ly + 1) * HX + (lx + HXO), nz, gv0, d.XY, ctr,
+                        [&](int lz, uint8_t b) { code[hc + (lz + 1) * PXY] = b; });
+  if (kCodes) {
+    // the brick's codes (k_hop_codes, brick-major) staged in the pointer area
+    const uint8_t* st = reinterpret_cast<const uint8_t*>(Pd);
+#pragma unroll 8
+    for (int lz = 0; lz < TZ; ++lz) code[hc + (lz + 1) * PXY] = st[(lz << 10) | (ly << 5) | lx];
   }
   __syncthreads();
 
@@ -565,6 +598,70 @@ __global__ void __launch_bounds__(A_THREADS, 1)
   }
   __syncthreads();  // shared memory is reused by the next brick
   }
+}
+
+// Pass A1 (split mode, PLMSS_OPT_PASS_A_SPLIT): the steepest hops alone, at
+// high occupancy. CTA = 8 rows x 32 columns x 32 layers of a brick; its field
+// box (40 x 10 x 34 floats, 53 KB) arrives by one TMA copy (OOB = NaN), four
+// CTAs per SM; codes out in the brick-major layout k_tile_segment<*, true>
+// bulk-copies (one byte per padded brick cell, 0xff outside the volume).
+constexpr int HR = 8;
+constexpr int CXY = HX * (HR + 2);
+constexpr int CN = CXY * HZ;
+constexpr int kCSmem = CN * 4 + 128;
+
+template <bool kTMA>
+__global__ void __launch_bounds__(32 * HR, 4)
+    k_hop_codes(const __grid_constant__ CUtensorMap tmap, const float* __restrict__ field, const FDims d,
+                uint8_t* __restrict__ codes, ACounters* __restrict__ ctr) {
+  extern __shared__ __align__(16) unsigned char h_smem_raw[];
+  float* f = reinterpret_cast<float*>(h_smem_raw + ((128u - (smem_u32(h_smem_raw) & 127u)) & 127u));
+  __shared__ __align__(8) uint64_t s_bar;
+  const int tid = int(threadIdx.x), lx = tid & 31, ly = tid >> 5;
+  const uint32_t bt = blockIdx.x / (TY / HR), rg = blockIdx.x % (TY / HR);
+  const uint32_t tx = bt % d.tx, ty = (bt / d.tx) % d.ty, tz = bt / (d.tx * d.ty);
+  const int gx0 = int(tx * TX), gy0 = int(ty * TY + rg * HR), gz0 = int(tz * TZ);
+  const int gx = gx0 + lx, gy = gy0 + ly;
+  const bool col_ok = gx < int(d.X) && gy < int(d.Y);
+  const int nz = min(TZ, int(d.Z) - gz0);
+  uint8_t* out = codes + ((uint64_t(bt) << 15) | uint32_t((rg * HR + ly) << 5) | uint32_t(lx));
+  if (gy0 < int(d.Y)) {
+    if (kTMA) {
+      if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s_bar)));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&s_bar)),
+                     "r"(uint32_t(CN * 4))
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+            "%4}], [%5];" ::"r"(smem_u32(f)),
+            "l"(&tmap), "r"(gx0 - HXO), "r"(gy0 - 1), "r"(gz0 - 1 - d.zf0), "r"(smem_u32(&s_bar))
+            : "memory");
+      }
+      __syncthreads();
+      asm volatile(
+          "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n @!p bra WAIT_%=;\n}" ::"r"(
+              smem_u32(&s_bar))
+          : "memory");
+    } else {
+      for (int i = tid; i < CN; i += 32 * HR) {
+        const int hx = i % HX, hy = (i / HX) % (HR + 2), hz = i / CXY;
+        const int x = gx0 + hx - HXO, y = gy0 + hy - 1, z = gz0 + hz - 1;
+        float v = __int_as_float(0x7fc00000);
+        if (x >= 0 && x < int(d.X) && y >= 0 && y < int(d.Y) && z >= d.zf0 && z < d.zf0 + int(d.zfn))
+          v = __ldg(field + (uint32_t(x) + d.X * (uint32_t(y) + d.Y * uint32_t(z - d.zf0))));
+        f[i] = v;
+      }
+      __syncthreads();
+    }
+    if (col_ok) {
+      const uint32_t gv0 = uint32_t(gx) + d.X * uint32_t(gy) + d.XY * uint32_t(gz0);
+      hop_column<HX, CXY>(f + (ly + 1) * HX + (lx + HXO), nz, gv0, d.XY, ctr,
+                          [&](int lz, uint8_t b) { out[lz << 10] = b; });
+    }
+  }
+  for (int lz = col_ok ? nz : 0; lz < TZ; ++lz) out[lz << 10] = 0xff;  // outside the volume: no hop
 }
 
 // ---------------------------------------------------------------- pass B --
@@ -1785,6 +1882,9 @@ static void ensure_consts(Ctx& c) {
     if (!g_consts_ready[c.device].load(std::memory_order_acquire)) {
       CK(cudaFuncSetAttribute(k_tile_segment<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kASmem));
       CK(cudaFuncSetAttribute(k_tile_segment<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kASmem));
+      CK(cudaFuncSetAttribute(k_tile_segment<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kASmem));
+      CK(cudaFuncSetAttribute(k_hop_codes<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kCSmem));
+      CK(cudaFuncSetAttribute(k_hop_codes<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kCSmem));
       // on the context stream (a non-blocking stream does not wait on the legacy one)
       CK(cudaMemcpyToSymbolAsync(c_mrows, kTetRowsPacked, sizeof(kTetRowsPacked), 0, cudaMemcpyHostToDevice,
                                  c.stream));
@@ -1796,6 +1896,48 @@ static void ensure_consts(Ctx& c) {
       g_consts_ready[c.device].store(true, std::memory_order_release);
     }
   }
+}
+
+// Pass A launch: the fused kernel, or (PLMSS_OPT_PASS_A_SPLIT) the hop-code
+// kernel followed by the brick compression fed by the codes.
+static void launch_pass_a(Ctx& c, const FDims& d, uint64_t ntiles, bool use_tma, const CUtensorMap& tmap,
+                          const float* field, uint32_t* maxima, uint32_t* minima, uint32_t* max_tt, uint32_t* min_tt,
+                          uint64_t ext_cap, uint32_t* TT, uint64_t tt_cap, uint4* TB, uint16_t* ltd, uint16_t* lta,
+                          ACounters* ctr) {
+  const unsigned grid = unsigned(std::min<uint64_t>(ntiles, uint64_t(c.sm_count)));
+  if (c.pass_a_split) {
+    uint8_t* codes = c.get_t<uint8_t>(S_CODES, ntiles * TN);
+    CUtensorMap hmap;
+    memset(&hmap, 0, sizeof hmap);
+    bool hop_tma = false;
+    if (use_tma) {
+      const cuuint64_t gdim[3] = {cuuint64_t(d.X), cuuint64_t(d.Y), cuuint64_t(d.zfn)};
+      const cuuint64_t gstride[2] = {cuuint64_t(d.X) * 4, cuuint64_t(d.X) * cuuint64_t(d.Y) * 4};
+      const cuuint32_t box[3] = {HX, HR + 2, HZ};
+      const cuuint32_t estride[3] = {1, 1, 1};
+      hop_tma = tensor_map_encoder()(&hmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(field), gdim,
+                                     gstride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NAN_REQUEST_ZERO_FMA) == CUDA_SUCCESS;
+    }
+    const unsigned hgrid = unsigned(ntiles * (TY / HR));
+    if (hop_tma)
+      k_hop_codes<true><<<hgrid, 32 * HR, kCSmem, c.stream>>>(hmap, field, d, codes, ctr);
+    else
+      k_hop_codes<false><<<hgrid, 32 * HR, kCSmem, c.stream>>>(hmap, field, d, codes, ctr);
+    CK_LAUNCH("k_hop_codes");
+    k_tile_segment<false, true><<<grid, A_THREADS, kASmem, c.stream>>>(
+        tmap, field, codes, d, maxima, minima, max_tt, min_tt, ext_cap, TT, tt_cap, TB, ltd, lta, ctr);
+    CK_LAUNCH("k_tile_segment");
+    return;
+  }
+  if (use_tma)
+    k_tile_segment<true><<<grid, A_THREADS, kASmem, c.stream>>>(tmap, field, nullptr, d, maxima, minima, max_tt,
+                                                                min_tt, ext_cap, TT, tt_cap, TB, ltd, lta, ctr);
+  else
+    k_tile_segment<false><<<grid, A_THREADS, kASmem, c.stream>>>(tmap, field, nullptr, d, maxima, minima, max_tt,
+                                                                 min_tt, ext_cap, TT, tt_cap, TB, ltd, lta, ctr);
+  CK_LAUNCH("k_tile_segment");
 }
 
 // Checked build: fail on the first device bounds check that did not hold.
@@ -1886,13 +2028,8 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
     CK(cudaMemsetAsync(ctr, 0, sizeof(ACounters), c.stream));
     CK(cudaMemsetAsync(&ctr->bad, 0xff, 4, c.stream));
     c.mark(0);
-    if (use_tma)
-      k_tile_segment<true><<<unsigned(std::min<uint64_t>(ntiles, uint64_t(c.sm_count))), A_THREADS, kASmem, c.stream>>>(
-          tmap, field, d, maxima, minima, max_tt, min_tt, ext_cap, TT, tt_cap, TB, ltd, lta, ctr);
-    else
-      k_tile_segment<false><<<unsigned(std::min<uint64_t>(ntiles, uint64_t(c.sm_count))), A_THREADS, kASmem, c.stream>>>(
-          tmap, field, d, maxima, minima, max_tt, min_tt, ext_cap, TT, tt_cap, TB, ltd, lta, ctr);
-    CK_LAUNCH("k_tile_segment");
+    launch_pass_a(c, d, ntiles, use_tma, tmap, field, maxima, minima, max_tt, min_tt, ext_cap, TT, tt_cap, TB, ltd,
+                  lta, ctr);
     c.mark(1);
     ACounters h;
     CK(cudaMemcpyAsync(c.h_pinned, ctr, sizeof(ACounters), cudaMemcpyDeviceToHost, c.stream));
@@ -2294,14 +2431,8 @@ void slab_segment(Ctx& c, const Grid& g, int64_t z0, int64_t z1, const float* fi
     TT = c.get_t<uint32_t>(S_TMP0, tt_cap);
     CK(cudaMemsetAsync(ctr, 0, sizeof(ACounters), c.stream));
     CK(cudaMemsetAsync(&ctr->bad, 0xff, 4, c.stream));
-    const unsigned grid = unsigned(std::min<uint64_t>(ntiles, uint64_t(c.sm_count)));
-    if (use_tma)
-      k_tile_segment<true><<<grid, A_THREADS, kASmem, c.stream>>>(tmap, field, d, maxima, minima, max_tt, min_tt,
-                                                                  ext_cap, TT, tt_cap, TB, ltd, lta, ctr);
-    else
-      k_tile_segment<false><<<grid, A_THREADS, kASmem, c.stream>>>(tmap, field, d, maxima, minima, max_tt, min_tt,
-                                                                   ext_cap, TT, tt_cap, TB, ltd, lta, ctr);
-    CK_LAUNCH("k_tile_segment");
+    launch_pass_a(c, d, ntiles, use_tma, tmap, field, maxima, minima, max_tt, min_tt, ext_cap, TT, tt_cap, TB, ltd,
+                  lta, ctr);
     CK(cudaMemcpyAsync(c.h_pinned, ctr, sizeof(ACounters), cudaMemcpyDeviceToHost, c.stream));
     c.sync();
     memcpy(&h, c.h_pinned, sizeof h);
