@@ -387,6 +387,8 @@ def main():
     ap.add_argument("--slab", action="store_true",
                     help="run the z-slab (multi-GPU) path even at world size 1 (torchrun --nproc-per-node 1)")
     ap.add_argument("--cpu-runs", type=int, default=3, help="timed runs of the cpu_baseline sample")
+    ap.add_argument("--dropin-config", default="cfg2",
+                    help="config of the drop-in leg (reference benchmark pass through the plmss:: API); '' skips")
     ap.add_argument("--option", action="append", default=[], metavar="NAME=VALUE",
                     help="context option (api.OPT_*, e.g. PASS_A_SPLIT=1); repeatable")
     ap.add_argument("--no-parity", action="store_true", help="skip the digest check of the last step's outputs")
@@ -544,6 +546,40 @@ def main():
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"unavailable: {e}"}
 
+    # ---- the drop-in: the reference's own benchmark pass (bench.cpp:62-87)
+    # through its plmss:: API, served by the B200 (build/libplmss_dropin.so),
+    # beside the compiled reference on the same host field
+    dropin = None
+    harness = os.path.join(ROOT, "build", "libplmss_dropin_harness.so")
+    if args.dropin_config and rank == 0 and os.path.exists(harness):
+        try:
+            import oracle
+
+            dcfg = CONFIGS[args.dropin_config]
+            fd = oracle.Restatement().synth(dcfg)
+            cores = os.cpu_count() or 1
+            D, R = oracle.Reference(harness), oracle.Reference()
+            D.run_once(dcfg.dims, fd, cores)  # warm (contexts, tables)
+            runs = []
+            for _ in range(3):
+                t0 = time.perf_counter()
+                ph, regions_d, prims_d = D.run_once(dcfg.dims, fd, cores)
+                runs.append((time.perf_counter() - t0, ph))
+            runs.sort(key=lambda x: x[0])
+            td, phd = runs[1]
+            t0 = time.perf_counter()
+            phr, regions_r, prims_r = R.run_once(dcfg.dims, fd, cores)
+            tr = time.perf_counter() - t0
+            dropin = {"config": dcfg.name, "dims": list(dcfg.dims),
+                      "api": "compute_order, segment(Both), combine_ms, index_separators + emit_geometry "
+                             "(MorseSmale) through the reference's plmss:: entry points, host vectors in and out",
+                      "b200_dropin_s": round(td, 4), "b200_phases_s": {k: round(v, 4) for k, v in phd.items()},
+                      "reference_s": round(tr, 4), "reference_phases_s": {k: round(v, 4) for k, v in phr.items()},
+                      "speedup": round(tr / td, 2), "cores": cores,
+                      "same_output": bool(regions_d == regions_r and prims_d == prims_r)}
+        except Exception as e:  # reported, never fatal
+            dropin = {"unavailable": str(e)}
+
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
@@ -564,6 +600,7 @@ def main():
         "e2e": e2e,
         "cpu_baseline": cpu,
         "parity": parity,
+        "dropin": dropin,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)

@@ -91,6 +91,9 @@ int plmss_b200_ctx_create(int device, void* stream, plmss_ctx** out);
 void plmss_b200_ctx_destroy(plmss_ctx* ctx);
 /* Bytes of device scratch currently held by the context. */
 size_t plmss_b200_ctx_scratch_bytes(const plmss_ctx* ctx);
+/* Frees the context's scratch arena (every result pointer it handed out
+ * becomes invalid) and trims the device memory pool. */
+int plmss_b200_ctx_release(plmss_ctx* ctx);
 /* Device time (ms) of the last kernel stage named by `stage` (see
  * plmss_b200_pipeline): 0 hops, 1 compress, 2 extrema, 3 combine, 4 marching.
  * Only filled when timing is enabled. */

@@ -50,7 +50,7 @@ HEADER_FUNCTIONS = [
     "plmss_b200_compress_sweep", "plmss_b200_segment_slab", "plmss_b200_weld_points", "plmss_b200_read_volume",
     "plmss_b200_write_labels", "plmss_b200_write_surface_obj", "plmss_b200_synth_layers",
     "plmss_b200_slab_segment", "plmss_b200_slab_resolve", "plmss_b200_slab_ids", "plmss_b200_slab_emit",
-    "plmss_b200_materialize_separators_chunked", "plmss_b200_write_separators_obj",
+    "plmss_b200_materialize_separators_chunked", "plmss_b200_write_separators_obj", "plmss_b200_ctx_release",
 ]
 
 GEOMETRY_SINK = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int64, C.c_int64, C.POINTER(C.c_double),
@@ -94,6 +94,7 @@ def lib() -> C.CDLL:
         L.plmss_b200_ctx_destroy.restype = None
         L.plmss_b200_ctx_scratch_bytes.argtypes = [vp]
         L.plmss_b200_ctx_scratch_bytes.restype = C.c_size_t
+        L.plmss_b200_ctx_release.argtypes = [vp]
         L.plmss_b200_ctx_set_timing.argtypes = [vp, i32]
         L.plmss_b200_ctx_stage_ms.argtypes = [vp, vp]
         L.plmss_b200_ctx_stats.argtypes = [vp, vp]
@@ -216,6 +217,10 @@ class Context:
 
     def scratch_bytes(self) -> int:
         return lib().plmss_b200_ctx_scratch_bytes(self.h)
+
+    def release(self):
+        """Free the scratch arena (results of earlier calls become invalid)."""
+        _check(lib().plmss_b200_ctx_release(self.h))
 
 
 _default: dict = {}

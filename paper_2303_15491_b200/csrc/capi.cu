@@ -160,6 +160,25 @@ size_t plmss_b200_ctx_scratch_bytes(const plmss_ctx* p) {
   return s;
 }
 
+int plmss_b200_ctx_release(plmss_ctx* p) {
+  return guarded([&] {
+    Ctx& c = C(p);
+    set_device(c);
+    c.sync();
+    for (int s = 0; s < S_COUNT; ++s) {
+      if (c.buf[s]) CK(cudaFreeAsync(c.buf[s], c.stream));
+      c.buf[s] = nullptr;
+      c.cap[s] = 0;
+    }
+    c.sync();
+    c.result = plmss_result{};
+    c.slab = SlabState{};
+    // return the freed blocks of the context's pool to the device
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, c.device) == cudaSuccess) CK(cudaMemPoolTrimTo(pool, 0));
+  });
+}
+
 int plmss_b200_ctx_set_timing(plmss_ctx* p, int enable) {
   return guarded([&] { C(p).timing = enable != 0; });
 }
@@ -234,6 +253,17 @@ int plmss_b200_compress_sweep(plmss_ctx* p, uint32_t* d_desc, uint32_t* d_asc, c
   });
 }
 
+// OrderField ranks -> float32 keys with the same order (bit patterns of
+// non-negative floats order like the integers); flags a rank outside [0, 2^30).
+__global__ void k_rank_keys(const int64_t* __restrict__ rank, int64_t n, float* __restrict__ out,
+                            int* __restrict__ bad) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t r = rank[i];
+  if (r < 0 || r >= (int64_t(1) << 30)) *bad = 1;
+  out[i] = __uint_as_float(uint32_t(r) & 0x3fffffffu);
+}
+
 int plmss_b200_segment(plmss_ctx* p, const int64_t dims[3], int key_type, const void* d_keys, int direction,
                        uint32_t* d_desc, uint32_t* d_asc, uint32_t* d_maxima, uint32_t* d_minima,
                        int64_t* n_maxima, int64_t* n_minima, int32_t* sweeps) {
@@ -244,6 +274,36 @@ int plmss_b200_segment(plmss_ctx* p, const int64_t dims[3], int key_type, const 
     if (direction < 0 || direction > 2) fail(PLMSS_ERR_INVALID_ARGUMENT, "bad direction");
     if (direction != PLMSS_ASCENDING && !d_desc) fail(PLMSS_ERR_INVALID_ARGUMENT, "d_desc required");
     if (direction != PLMSS_DESCENDING && !d_asc) fail(PLMSS_ERR_INVALID_ARGUMENT, "d_asc required");
+    // The fused passes (fused.cu fused_segment) for float32 values and
+    // OrderField ranks on grids inside the fused envelope; float64 values and
+    // PLMSS_OPT_PIPELINE_PATH 1 take the staged kernels.
+    if (c.pipeline_path == 0 && fused_supported(g) && (key_type == PLMSS_KEY_F32 || key_type == PLMSS_KEY_RANK)) {
+      const float* f = static_cast<const float*>(d_keys);
+      bool ok = true;
+      if (key_type == PLMSS_KEY_RANK) {
+        float* fk = c.get_t<float>(S_FIELD, g.n);
+        int* bad = reinterpret_cast<int*>(static_cast<char*>(c.get(S_FLAGS, 1024)) + 320);
+        CK(cudaMemsetAsync(bad, 0, 4, c.stream));
+        k_rank_keys<<<blocks_for(g.n, 256), 256, 0, c.stream>>>(static_cast<const int64_t*>(d_keys), g.n, fk, bad);
+        CK_LAUNCH("k_rank_keys");
+        CK(cudaMemcpyAsync(c.h_pinned + 3, bad, 4, cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
+        ok = *reinterpret_cast<int*>(c.h_pinned + 3) == 0;
+        f = fk;
+      }
+      if (ok) {
+        uint32_t* dd = d_desc ? d_desc : c.get_t<uint32_t>(S_DESC, g.n);
+        uint32_t* da = d_asc ? d_asc : c.get_t<uint32_t>(S_ASC, g.n);
+        int64_t nmx = 0, nmn = 0;
+        int32_t sw = 0;
+        fused_segment(c, g, f, dd, da, direction != PLMSS_ASCENDING ? d_maxima : nullptr,
+                      direction != PLMSS_DESCENDING ? d_minima : nullptr, &nmx, &nmn, &sw);
+        if (n_maxima) *n_maxima = direction != PLMSS_ASCENDING ? nmx : 0;
+        if (n_minima) *n_minima = direction != PLMSS_DESCENDING ? nmn : 0;
+        if (sweeps) *sweeps = sw;
+        return;
+      }
+    }
     SegOut o = run_segment(
         c, g, key_type, d_keys, direction, d_desc, d_asc, [&](int64_t) { return d_maxima; },
         [&](int64_t) { return d_minima; }, nullptr, nullptr);

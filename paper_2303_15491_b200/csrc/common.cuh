@@ -225,6 +225,8 @@ struct FusedOut {
   plmss_tri* tris;
 };
 bool fused_supported(const Grid& g);
+void fused_segment(Ctx& c, const Grid& g, const float* field, uint32_t* desc, uint32_t* asc, uint32_t* maxima_out,
+                   uint32_t* minima_out, int64_t* n_max_out, int64_t* n_min_out, int32_t* sweeps_out);
 FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* desc, uint32_t* asc, uint32_t* ms);
 // z-slab pipeline (multi-GPU), fused.cu; the stages of include/plmss_b200.h
 void slab_segment(Ctx& c, const Grid& g, int64_t z0, int64_t z1, const float* field, plmss_slab_info* info);

@@ -1029,7 +1029,7 @@ struct BrickArgs {
   uint64_t fmask;
   uint64_t* chunk;                // separator count per 32-cube chunk
   uint8_t* cls;                   // per cube: 0 one region, m8 two labels, 0xff more
-  uint32_t *desc, *asc, *ms;      // ms holds the region token until k_ms_ids
+  uint32_t *desc, *asc, *ms;      // ms holds the region token until k_ms_ids (null: labels only)
   int* overflow;
 };
 
@@ -1084,7 +1084,8 @@ __global__ void __launch_bounds__(32 * kTokRows) k_tokens(const BrickArgs a) {
       // index, not a rank: no set insert and no extremum gather for it (the
       // pass is redone after the forest converges).
       if (!(ld[i] & la[i] & kFinal)) {
-        a.desc[gv] = a.asc[gv] = a.ms[gv] = 0u;
+        a.desc[gv] = a.asc[gv] = 0u;
+        if (a.ms) a.ms[gv] = 0u;
         lkey = Key(~Key(0));
         gv += d.XY;
         continue;
@@ -1094,7 +1095,9 @@ __global__ void __launch_bounds__(32 * kTokRows) k_tokens(const BrickArgs a) {
       DCHECK(ld[i] < a.nmax && la[i] < a.nmin, 401);
       const Key key = kDense ? Key(la[i] * a.nmax + ld[i]) : Key((uint64_t(la[i]) << 32) | ld[i]);
       if (key != lkey) {
-        if (kDense) {
+        if (!a.ms) {
+          // labels only (fused_segment): no region set
+        } else if (kDense) {
           ltok = uint32_t(key);
           const uint32_t bit = 1u << (ltok & 31);
           DCHECK((ltok >> 5) < a.nw, 402);
@@ -1110,7 +1113,7 @@ __global__ void __launch_bounds__(32 * kTokRows) k_tokens(const BrickArgs a) {
       }
       a.desc[gv] = lgv.x;
       a.asc[gv] = lgv.y;
-      a.ms[gv] = ltok;
+      if (a.ms) a.ms[gv] = ltok;
       gv += d.XY;
     }
   }
@@ -1184,7 +1187,8 @@ __device__ __forceinline__ void tokens_tma_body(const CUtensorMap& mld, const CU
       // index, not a rank: no set insert and no extremum gather for it (the
       // pass is redone after the forest converges).
       if (!(ld[i] & la[i] & kFinal)) {
-        a.desc[gv] = a.asc[gv] = a.ms[gv] = 0u;
+        a.desc[gv] = a.asc[gv] = 0u;
+        if (a.ms) a.ms[gv] = 0u;
         lkey = Key(~Key(0));
         gv += d.XY;
         continue;
@@ -1194,7 +1198,9 @@ __device__ __forceinline__ void tokens_tma_body(const CUtensorMap& mld, const CU
       DCHECK(ld[i] < a.nmax && la[i] < a.nmin, 401);
       const Key key = kDense ? Key(la[i] * a.nmax + ld[i]) : Key((uint64_t(la[i]) << 32) | ld[i]);
       if (key != lkey) {
-        if (kDense) {
+        if (!a.ms) {
+          // labels only (fused_segment): no region set
+        } else if (kDense) {
           ltok = uint32_t(key);
           const uint32_t bit = 1u << (ltok & 31);
           DCHECK((ltok >> 5) < a.nw, 402);
@@ -1210,7 +1216,7 @@ __device__ __forceinline__ void tokens_tma_body(const CUtensorMap& mld, const CU
       }
       a.desc[gv] = lgv.x;
       a.asc[gv] = lgv.y;
-      a.ms[gv] = ltok;
+      if (a.ms) a.ms[gv] = ltok;
       gv += d.XY;
     }
   };
@@ -2317,6 +2323,160 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
     return o;
     }
   }
+}
+
+
+// segment (segmentation.hpp:74-76) on the fused passes: pass A, the extremum
+// lists, the forest to its fixpoint, then a token pass that writes only the
+// labels (global vertex ids of the maximum / minimum of every vertex). Keys
+// are float32 values; OrderField ranks arrive bit-cast to float32 (ranks
+// < 2^30: non-negative finite floats whose order is the rank order, no ties).
+void fused_segment(Ctx& c, const Grid& g, const float* field, uint32_t* desc, uint32_t* asc, uint32_t* maxima_out,
+                   uint32_t* minima_out, int64_t* n_max_out, int64_t* n_min_out, int32_t* sweeps_out) {
+  ensure_consts(c);
+  FDims d{};
+  d.X = uint32_t(g.X);
+  d.Y = uint32_t(g.Y);
+  d.Z = uint32_t(g.Z);
+  d.XY = d.X * d.Y;
+  d.n = uint32_t(g.n);
+  d.tx = uint32_t((g.X + TX - 1) / TX);
+  d.ty = uint32_t((g.Y + TY - 1) / TY);
+  d.tz = uint32_t((g.Z + TZ - 1) / TZ);
+  d.zf0 = 0;
+  d.zfn = d.Z;
+  d.pbase = 0;
+  const uint64_t ntiles = uint64_t(d.tx) * d.ty * d.tz;
+  CUtensorMap tmap;
+  memset(&tmap, 0, sizeof tmap);
+  bool use_tma = (g.X % 4) == 0 && (reinterpret_cast<uintptr_t>(field) & 15) == 0 && c.use_tma;
+  if (use_tma) {
+    const EncodeFn encode = tensor_map_encoder();
+    const cuuint64_t gdim[3] = {cuuint64_t(g.X), cuuint64_t(g.Y), cuuint64_t(g.Z)};
+    const cuuint64_t gstride[2] = {cuuint64_t(g.X) * 4, cuuint64_t(g.X) * cuuint64_t(g.Y) * 4};
+    const cuuint32_t box[3] = {HX, HY, HZ};
+    const cuuint32_t estride[3] = {1, 1, 1};
+    use_tma = encode && encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(field), gdim, gstride,
+                               box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NAN_REQUEST_ZERO_FMA) == CUDA_SUCCESS;
+  }
+  char* ctr_base = static_cast<char*>(c.get(S_FLAGS, 1024));
+  ACounters* ctr = reinterpret_cast<ACounters*>(ctr_base);
+  uint16_t* ltd = c.get_t<uint16_t>(S_LTD, ntiles * TN);
+  uint16_t* lta = c.get_t<uint16_t>(S_LTA, ntiles * TN);
+  uint4* TB = c.get_t<uint4>(S_TB, ntiles);
+  uint32_t *maxima = nullptr, *minima = nullptr, *max_tt = nullptr, *min_tt = nullptr, *TT = nullptr;
+  ACounters h;
+  for (int attempt = 0;; ++attempt) {
+    const uint64_t ext_cap = c.fused_ext_cap ? c.fused_ext_cap : uint64_t(g.n / 4 + 1024);
+    maxima = c.get_t<uint32_t>(S_MAXIMA, ext_cap);
+    minima = c.get_t<uint32_t>(S_MINIMA, ext_cap);
+    max_tt = c.get_t<uint32_t>(S_RANK_MAX, ext_cap);
+    min_tt = c.get_t<uint32_t>(S_RANK_MIN, ext_cap);
+    const uint64_t tt_cap = c.fused_exit_cap ? c.fused_exit_cap : uint64_t(g.n / 4 + 1024);
+    TT = c.get_t<uint32_t>(S_TMP0, tt_cap);
+    CK(cudaMemsetAsync(ctr, 0, sizeof(ACounters), c.stream));
+    CK(cudaMemsetAsync(&ctr->bad, 0xff, 4, c.stream));
+    launch_pass_a(c, d, ntiles, use_tma, tmap, field, maxima, minima, max_tt, min_tt, ext_cap, TT, tt_cap, TB, ltd,
+                  lta, ctr);
+    CK(cudaMemcpyAsync(c.h_pinned, ctr, sizeof(ACounters), cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    memcpy(&h, c.h_pinned, sizeof h);
+    if (h.bad != 0xffffffffu)
+      fail(PLMSS_ERR_INVALID_ARGUMENT, "non-finite scalar value at vertex " + std::to_string(h.bad));
+    bool retry = false;
+    if (h.n_tt > tt_cap) {
+      c.fused_exit_cap = h.n_tt + h.n_tt / 4 + 1024;
+      retry = true;
+    }
+    if (h.n_max > ext_cap || h.n_min > ext_cap) {
+      c.fused_ext_cap = std::max(h.n_max, h.n_min) + 1024;
+      retry = true;
+    }
+    if (!retry) break;
+    if (attempt > 6) fail(PLMSS_ERR_LOGIC, "fused segment capacity retries exhausted");
+  }
+  const int64_t n_max = int64_t(h.n_max), n_min = int64_t(h.n_min);
+  const uint64_t nt = h.n_tt;
+  uint32_t* RK = c.get_t<uint32_t>(S_RK, nt);
+  for (int dir = 0; dir < 2; ++dir) {
+    uint32_t* list = dir ? minima : maxima;
+    const uint32_t* ltt = dir ? min_tt : max_tt;
+    const int64_t k = dir ? n_min : n_max;
+    if (k < 1) continue;
+    uint64_t* kk = c.get_t<uint64_t>(S_SORT_A, k);
+    uint64_t* vv = c.get_t<uint64_t>(S_SORT_B, k);
+    k_list_pairs<<<blocks_for(k, 256), 256, 0, c.stream>>>(list, ltt, k, kk, vv);
+    CK_LAUNCH("k_list_pairs");
+    if (k > 1) {
+      int bits = 0;
+      while ((uint64_t(1) << bits) < uint64_t(g.n)) ++bits;
+      radix_sort_pairs(c, kk, vv, k, bits);
+    }
+    k_rank_lists<<<blocks_for(k, 256), 256, 0, c.stream>>>(kk, vv, k, list, RK, 0u);
+    CK_LAUNCH("k_rank_lists");
+  }
+  uint32_t* SD = c.get_t<uint32_t>(S_SD, nt);
+  uint32_t* SA = c.get_t<uint32_t>(S_SA, nt);
+  k_tt_succ<<<unsigned(ntiles), 256, 0, c.stream>>>(TB, TT, ltd, lta, RK, SD, SA, 0u, nt);
+  CK_LAUNCH("k_tt_succ");
+  int* jflag = reinterpret_cast<int*>(ctr_base + 192);
+  int sweeps = 0;
+  for (;;) {
+    CK(cudaMemsetAsync(jflag, 0, 4, c.stream));
+    k_tt_jump<<<blocks_for(int64_t((nt + 1) / 2), 256), 256, 0, c.stream>>>(nt, SD, SA, jflag);
+    CK_LAUNCH("k_tt_jump");
+    ++sweeps;
+    CK(cudaMemcpyAsync(reinterpret_cast<char*>(c.h_pinned) + 64, jflag, 4, cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    if (*reinterpret_cast<int*>(reinterpret_cast<char*>(c.h_pinned) + 64) == 0) break;
+    if (sweeps > 64) fail(PLMSS_ERR_LOGIC, "terminal forest did not converge");
+  }
+  BrickArgs ba{};
+  ba.d = d;
+  ba.nxc = uint32_t((g.X - 1 + 31) / 32);
+  ba.TB = TB;
+  ba.ltd = ltd;
+  ba.lta = lta;
+  ba.FD = SD;
+  ba.FA = SA;
+  ba.maxs = maxima;
+  ba.mins = minima;
+  ba.nmax = uint32_t(n_max);
+  ba.nmin = uint32_t(n_min);
+  ba.nt = nt;
+  ba.desc = desc;
+  ba.asc = asc;
+  ba.ms = nullptr;  // labels only
+  CUtensorMap mld, mla;
+  bool lt_tma = c.use_tma && tensor_map_encoder();
+  if (lt_tma) {
+    const cuuint64_t gdim[2] = {cuuint64_t(TX * TY), cuuint64_t(ntiles) * TZ};
+    const cuuint64_t gstride[1] = {cuuint64_t(TX * TY) * 2};
+    const cuuint32_t box[2] = {cuuint32_t(32 * kTokRows), cuuint32_t(TZ)};
+    const cuuint32_t estride[2] = {1, 1};
+    for (int k = 0; k < 2 && lt_tma; ++k)
+      lt_tma = tensor_map_encoder()(k ? &mla : &mld, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, k ? lta : ltd, gdim, gstride,
+                                    box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  }
+  const unsigned tgrid = unsigned((TY / kTokRows) * ntiles);
+  if (lt_tma)
+    k_tokens_tma<true><<<tgrid, 32 * kTokRows, 0, c.stream>>>(mld, mla, ba);
+  else
+    k_tokens<true><<<tgrid, 32 * kTokRows, 0, c.stream>>>(ba);
+  CK_LAUNCH("k_tokens");
+  if (maxima_out && n_max)
+    CK(cudaMemcpyAsync(maxima_out, maxima, size_t(n_max) * 4, cudaMemcpyDeviceToDevice, c.stream));
+  if (minima_out && n_min)
+    CK(cudaMemcpyAsync(minima_out, minima, size_t(n_min) * 4, cudaMemcpyDeviceToDevice, c.stream));
+  check_device(c, "fused_segment");
+  c.sync();
+  if (n_max_out) *n_max_out = n_max;
+  if (n_min_out) *n_min_out = n_min;
+  if (sweeps_out) *sweeps_out = sweeps;
 }
 
 }  // namespace plmss_b200

@@ -136,25 +136,30 @@ def test_slab_full_size_matches_oracle_digests(plmss, gpu, name, world, path):
         pytest.skip(f"{p} not generated")
     g = json.load(open(p))
     cfg = CONFIGS[name]
+    gpu.release()  # the single-volume tests' buffers (cfg3: ~100 GB) are not needed here
+    torch.cuda.empty_cache()
     f = plmss.synth_field(cfg.dims, kind=cfg.kind, gaussians=cfg.gaussians() if cfg.kind == "gaussians" else None,
                           noise_amp=cfg.noise, seed=cfg.seed, levels=cfg.levels, ctx=gpu)
     torch.cuda.synchronize()
     res, ctxs = run_slabs(plmss, cfg.dims, world, f, path)
     del f
-    h = {k: ChunkedSha256() for k in ("desc", "asc", "ms", "tris")}
-    for r in res:
-        for k in h:
-            t = getattr(r, k).reshape(-1)
-            for i in range(0, t.numel(), 1 << 28):
-                h[k].update(t[i:i + (1 << 28)].cpu().numpy())
-    got = {k: v.hexdigest() for k, v in h.items()}
-    got["maxima"] = digest_device(res[0].maxima)
-    got["minima"] = digest_device(res[0].minima)
-    got["region_keys"] = digest_device(res[0].region_keys)
-    assert res[0].tri_total == g["n_tris"]
-    assert (res[0].maxima.numel(), res[0].minima.numel(), res[0].region_keys.numel()) == \
-        (g["n_maxima"], g["n_minima"], g["n_regions"])
-    bad = [k for k in got if got[k] != g[k]]
-    assert not bad, f"{name} over {world} slabs: digests differ for {bad}"
-    for c in ctxs:
-        c.close()
+    try:
+        h = {k: ChunkedSha256() for k in ("desc", "asc", "ms", "tris")}
+        for r in res:
+            for k in h:
+                t = getattr(r, k).reshape(-1)
+                for i in range(0, t.numel(), 1 << 28):
+                    h[k].update(t[i:i + (1 << 28)].cpu().numpy()).drain()
+        got = {k: v.hexdigest() for k, v in h.items()}
+        got["maxima"] = digest_device(res[0].maxima)
+        got["minima"] = digest_device(res[0].minima)
+        got["region_keys"] = digest_device(res[0].region_keys)
+        assert res[0].tri_total == g["n_tris"]
+        assert (res[0].maxima.numel(), res[0].minima.numel(), res[0].region_keys.numel()) == \
+            (g["n_maxima"], g["n_minima"], g["n_regions"])
+        bad = [k for k in got if got[k] != g[k]]
+        assert not bad, f"{name} over {world} slabs: digests differ for {bad}"
+    finally:
+        del res
+        for c in ctxs:
+            c.close()
