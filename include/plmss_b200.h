@@ -300,7 +300,9 @@ int plmss_b200_copy(plmss_ctx* ctx, void* dst, const void* d_src, int64_t bytes,
  *                           continue and C, D are redone (0 forces that path);
  *   PLMSS_OPT_PASS_A_SPLIT  1: pass A as two kernels (hop codes at high
  *                           occupancy, then the brick compression from the
- *                           codes), 0: one fused kernel (both are exact). */
+ *                           codes), 0: one fused kernel (both are exact);
+ *   PLMSS_OPT_HOP_CUBE      1: steepest hops from shared 2x2 quads / unit
+ *                           cubes, 0: per-vertex equality masks (both exact). */
 /* ---- callers either side of the path ------------------
  * weld_points (marching.hpp:138-140, marching.cpp:400-417): merges
  * bitwise-identical points of a separator soup in place, the first occurrence
@@ -354,7 +356,8 @@ enum plmss_option {
   PLMSS_OPT_PIPELINE_PATH = 2,
   PLMSS_OPT_TMA = 3,
   PLMSS_OPT_SPECULATIVE_SWEEPS = 4,
-  PLMSS_OPT_PASS_A_SPLIT = 5
+  PLMSS_OPT_PASS_A_SPLIT = 5,
+  PLMSS_OPT_HOP_CUBE = 6
 };
 int plmss_b200_ctx_set_option(plmss_ctx* ctx, int option, int64_t value);
 

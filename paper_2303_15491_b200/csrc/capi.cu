@@ -509,6 +509,10 @@ int plmss_b200_ctx_set_option(plmss_ctx* p, int option, int64_t value) {
       c.pass_a_split = value != 0;
       return;
     }
+    if (option == PLMSS_OPT_HOP_CUBE) {
+      c.hop_cube = value != 0;
+      return;
+    }
     if (option == PLMSS_OPT_PIPELINE_PATH) {
       if (value < 0 || value > 1) fail(PLMSS_ERR_INVALID_ARGUMENT, "pipeline path must be 0 or 1");
       c.pipeline_path = int(value);

@@ -15,6 +15,7 @@
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "plmss/marching.hpp"
@@ -73,12 +74,8 @@ struct DevBuf {
   }
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
-  void up(const T* h, size_t n) {
-    if (n) cuda(cudaMemcpy(p, h, n * sizeof(T), cudaMemcpyHostToDevice), "H2D");
-  }
-  void down(T* h, size_t n) const {
-    if (n) cuda(cudaMemcpy(h, p, n * sizeof(T), cudaMemcpyDeviceToHost), "D2H");
-  }
+  void up(const T* h, size_t n);
+  void down(T* h, size_t n) const;
 };
 
 std::array<int64_t, 3> grid_of(const SimplicialComplex3& complex) {
@@ -87,6 +84,124 @@ std::array<int64_t, 3> grid_of(const SimplicialComplex3& complex) {
         "the plmss B200 drop-in handles implicit 3-D grids only (explicit meshes and 2-D grids are out of scope)");
   const auto& d = complex.grid_dims();
   return {d[0], d[1], d[2]};
+}
+
+// ---- host <-> device transfers through pinned staging, host side on threads
+// (the reference containers are pageable std::vector / Eigen storage: a plain
+// cudaMemcpy from them runs at pageable speed on one thread).
+constexpr size_t kStage = size_t(64) << 20;
+
+unsigned host_threads() { return std::max(1u, std::min(16u, std::thread::hardware_concurrency())); }
+
+template <class F>
+void parallel_for(int64_t n, F&& f) {  // f(begin, end)
+  const unsigned nt = n < (int64_t(1) << 16) ? 1u : host_threads();
+  if (nt == 1) {
+    f(int64_t(0), n);
+    return;
+  }
+  std::vector<std::thread> th;
+  const int64_t per = (n + nt - 1) / nt;
+  for (unsigned t = 0; t < nt; ++t) {
+    const int64_t b = std::min(n, int64_t(t) * per), e = std::min(n, b + per);
+    if (b < e) th.emplace_back([&f, b, e] { f(b, e); });
+  }
+  for (auto& x : th) x.join();
+}
+
+struct Stage {
+  unsigned char* buf[2] = {nullptr, nullptr};
+  cudaStream_t st = nullptr;
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  Stage() {
+    for (auto& b : buf) cuda(cudaMallocHost(reinterpret_cast<void**>(&b), kStage), "cudaMallocHost");
+    cuda(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate");
+    for (auto& e : ev) cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+  }
+};
+
+Stage& stage() {
+  thread_local Stage s;  // one per host thread, like the contexts
+  return s;
+}
+
+// Device -> host: chunk k is copied into pinned buffer k % 2 while the host
+// threads convert chunk k - 1 out of the other one. conv(dst_index0,
+// staged source, count) writes count source elements.
+template <class S, class Conv>
+void down_conv(const S* d_src, int64_t n, Conv&& conv) {
+  if (n <= 0) return;
+  Stage& g = stage();
+  cuda(cudaDeviceSynchronize(), "sync");
+  const int64_t per = int64_t(kStage / sizeof(S));
+  const int64_t nch = (n + per - 1) / per;
+  for (int64_t k = 0; k <= nch; ++k) {
+    if (k < nch) {
+      const int64_t i0 = k * per, cnt = std::min(per, n - i0);
+      cuda(cudaMemcpyAsync(g.buf[k & 1], d_src + i0, size_t(cnt) * sizeof(S), cudaMemcpyDeviceToHost, g.st), "D2H");
+      cuda(cudaEventRecord(g.ev[k & 1], g.st), "event");
+    }
+    if (k >= 1) {
+      const int64_t j = k - 1, i0 = j * per, cnt = std::min(per, n - i0);
+      cuda(cudaEventSynchronize(g.ev[j & 1]), "event sync");
+      const S* src = reinterpret_cast<const S*>(g.buf[j & 1]);
+      parallel_for(cnt, [&](int64_t b, int64_t e) { conv(i0 + b, src + b, e - b); });
+    }
+  }
+}
+
+// Host -> device: the host threads fill pinned buffer k % 2 (conversion
+// included) while chunk k - 1 is in flight. fill(dst staged, src_index0, count).
+template <class D, class Fill>
+void up_conv(D* d_dst, int64_t n, Fill&& fill) {
+  if (n <= 0) return;
+  Stage& g = stage();
+  const int64_t per = int64_t(kStage / sizeof(D));
+  const int64_t nch = (n + per - 1) / per;
+  for (int64_t k = 0; k < nch; ++k) {
+    const int64_t i0 = k * per, cnt = std::min(per, n - i0);
+    if (k >= 2) cuda(cudaEventSynchronize(g.ev[k & 1]), "event sync");  // buffer k % 2 free again
+    D* dst = reinterpret_cast<D*>(g.buf[k & 1]);
+    parallel_for(cnt, [&](int64_t b, int64_t e) { fill(dst + b, i0 + b, e - b); });
+    cuda(cudaMemcpyAsync(d_dst + i0, dst, size_t(cnt) * sizeof(D), cudaMemcpyHostToDevice, g.st), "H2D");
+    cuda(cudaEventRecord(g.ev[k & 1], g.st), "event");
+  }
+  cuda(cudaStreamSynchronize(g.st), "sync");
+}
+
+template <class T>
+void down_copy(T* h_dst, const T* d_src, int64_t n) {
+  down_conv(d_src, n, [&](int64_t i0, const T* s, int64_t c) { std::memcpy(h_dst + i0, s, size_t(c) * sizeof(T)); });
+}
+template <class T>
+void up_copy(T* d_dst, const T* h_src, int64_t n) {
+  up_conv(d_dst, n, [&](T* d, int64_t i0, int64_t c) { std::memcpy(d, h_src + i0, size_t(c) * sizeof(T)); });
+}
+// labels: device uint32 <-> host int64
+void down_widen(int64_t* h_dst, const uint32_t* d_src, int64_t n) {
+  down_conv(d_src, n, [&](int64_t i0, const uint32_t* s, int64_t c) {
+    for (int64_t i = 0; i < c; ++i) h_dst[i0 + i] = s[i];
+  });
+}
+void up_narrow(uint32_t* d_dst, const int64_t* h_src, int64_t n) {
+  up_conv(d_dst, n, [&](uint32_t* d, int64_t i0, int64_t c) {
+    for (int64_t i = 0; i < c; ++i) d[i] = static_cast<uint32_t>(h_src[i0 + i]);
+  });
+}
+
+template <class T>
+void DevBuf<T>::up(const T* h, size_t n) {
+  if (n < (size_t(1) << 16))
+    cuda(cudaMemcpy(p, h, n * sizeof(T), cudaMemcpyHostToDevice), "H2D");
+  else
+    up_copy(p, h, int64_t(n));
+}
+template <class T>
+void DevBuf<T>::down(T* h, size_t n) const {
+  if (n < (size_t(1) << 16))
+    cuda(cudaMemcpy(h, p, n * sizeof(T), cudaMemcpyDeviceToHost), "D2H");
+  else
+    down_copy(h, p, int64_t(n));
 }
 
 std::vector<uint32_t> narrow(std::span<const int64_t> v) {
@@ -185,22 +300,17 @@ SegmentationResult segment(const SimplicialComplex3& complex, const OrderField& 
   check(plmss_b200_segment(ctx(), dims.data(), PLMSS_KEY_RANK, dk.p, int(direction), dd.p, da.p, dmx.p, dmn.p,
                            &nmax, &nmin, &sweeps));
   SegmentationResult seg;
-  std::vector<uint32_t> tmp;
   if (want_desc) {
-    tmp.resize(n);
-    dd.down(tmp.data(), n);
-    seg.desc = widen(tmp);
-    tmp.resize(nmax);
-    dmx.down(tmp.data(), nmax);
-    seg.maxima = widen(tmp);
+    seg.desc.resize(n);
+    down_widen(seg.desc.data(), dd.p, n);
+    seg.maxima.resize(nmax);
+    down_widen(seg.maxima.data(), dmx.p, nmax);
   }
   if (want_asc) {
-    tmp.resize(n);
-    da.down(tmp.data(), n);
-    seg.asc = widen(tmp);
-    tmp.resize(nmin);
-    dmn.down(tmp.data(), nmin);
-    seg.minima = widen(tmp);
+    seg.asc.resize(n);
+    down_widen(seg.asc.data(), da.p, n);
+    seg.minima.resize(nmin);
+    down_widen(seg.minima.data(), dmn.p, nmin);
   }
   seg.sweeps = sweeps;
   return seg;
@@ -211,16 +321,14 @@ void combine_ms(SegmentationResult& seg, int workers) {
     throw std::invalid_argument("combine_ms needs both ascending and descending labels");
   if (workers < 1) throw std::invalid_argument("workers must be >= 1");
   const int64_t n = static_cast<int64_t>(seg.desc.size());
-  const auto a32 = narrow(seg.asc), d32 = narrow(seg.desc);
   DevBuf<uint32_t> da(n), dd(n), dm(n);
   DevBuf<uint64_t> dk(n);
-  da.up(a32.data(), n);
-  dd.up(d32.data(), n);
+  up_narrow(da.p, seg.asc.data(), n);
+  up_narrow(dd.p, seg.desc.data(), n);
   int64_t r = 0;
   check(plmss_b200_combine_ms(ctx(), n, da.p, dd.p, dm.p, dk.p, &r));
-  std::vector<uint32_t> ms(n);
-  dm.down(ms.data(), n);
-  seg.ms_region = widen(ms);
+  seg.ms_region.resize(n);
+  down_widen(seg.ms_region.data(), dm.p, n);
   std::vector<uint64_t> keys(r);
   dk.down(keys.data(), r);
   seg.region_keys.resize(r);
@@ -435,11 +543,13 @@ SeparatingMesh emit_geometry(const SimplicialComplex3& complex, std::span<const 
     DevBuf<int64_t> dr(2 * total), ds(total);
     check(plmss_b200_materialize_separators(ctx(), dims.data(), spv, ogv, 1, dt.p, total, dp.p, dr.p, ds.p));
     dp.down(mesh.points.data(), 9 * total);
-    std::vector<int64_t> reg(2 * total);
-    dr.down(reg.data(), 2 * total);
-    for (int64_t i = 0; i < total; ++i) mesh.regions[i] = {reg[2 * i], reg[2 * i + 1]};
+    static_assert(sizeof(std::array<Label, 2>) == 2 * sizeof(int64_t), "region pair layout");
+    dr.down(reinterpret_cast<int64_t*>(mesh.regions.data()), 2 * total);
     ds.down(mesh.source_cells.data(), total);
-    for (int64_t i = 0; i < 3 * total; ++i) mesh.indices[i] = i;
+    int64_t* idx = mesh.indices.data();
+    parallel_for(3 * total, [&](int64_t b, int64_t e) {
+      for (int64_t i = b; i < e; ++i) idx[i] = i;
+    });
   }
   return mesh;
 }

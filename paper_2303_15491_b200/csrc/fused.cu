@@ -224,6 +224,95 @@ __device__ __forceinline__ void hop_column(const float* __restrict__ fc, const i
     }
   }
 
+// Cube-shared steepest hops (the same result as hop_column, fewer ALU-pipe
+// instructions). The 14 neighbours of v are the corners of its upper unit
+// cube [x, x+1] x [y, y+1] x [z, z+1] and of its lower one [x-1, x] x ...,
+// v itself excepted; in id order they are the lower cube's corners
+// k = dx + 2 dy + 4 dz (s = 0..6), v, then the upper cube's (s = 6 + k). A
+// cube is two 2x2 quads stacked in z; a quad is reused by the next layer's
+// cube, so per vertex two quads, two cube merges and one final merge per
+// direction. Within every merge the second operand's corners all have higher
+// ids than the first's, so "the highest id attaining the maximum" (the
+// simulation of simplicity order, F5) is: take the second operand iff it
+// attains the maximum (FMNMX + FSET on the ALU pipe); the winner's corner
+// index rides along as a small float updated by FFMA blends (FMA pipe).
+// NaN (missing) neighbours never attain a maximum or minimum.
+struct HopQuad {
+  float M, tM;  // max and the highest corner attaining it (0..3, + base)
+  float m, tm;  // min and the lowest corner attaining it
+};
+
+// quad corners a < b < c < d in id order; tags offset by `base`
+__device__ __forceinline__ HopQuad hop_quad(float a, float b, float c, float d, float base) {
+  HopQuad q;
+  q.M = fmaxf(fmaxf(a, b), fmaxf(c, d));
+  q.m = fminf(fminf(a, b), fminf(c, d));
+  float t = base + feq(b, q.M);
+  t = __fmaf_rn(feq(c, q.M), (base + 2.f) - t, t);
+  t = __fmaf_rn(feq(d, q.M), (base + 3.f) - t, t);
+  q.tM = t;
+  float u = (base + 3.f) - feq(c, q.m);
+  u = __fmaf_rn(feq(b, q.m), (base + 1.f) - u, u);
+  u = __fmaf_rn(feq(a, q.m), base - u, u);
+  q.tm = u;
+  return q;
+}
+
+// cube = quad lo (corners +0) stacked under quad hi (corners +4)
+__device__ __forceinline__ HopQuad hop_cube(const HopQuad& lo, const HopQuad& hi) {
+  HopQuad c;
+  c.M = fmaxf(lo.M, hi.M);
+  c.tM = __fmaf_rn(feq(hi.M, c.M), (hi.tM + 4.f) - lo.tM, lo.tM);
+  c.m = fminf(lo.m, hi.m);
+  c.tm = __fmaf_rn(feq(lo.m, c.m), lo.tm - (hi.tm + 4.f), hi.tm + 4.f);
+  return c;
+}
+
+// position (0..6 lower cube, 7 = v, 8..14 upper cube) -> stencil s, 15 = none
+__device__ __forceinline__ uint32_t hop_code(float pos) {
+  const uint32_t p = __float_as_uint(pos + 12582912.0f) & 15u;  // exact small integer
+  return uint32_t(0x0DCBA987F6543210ull >> (4 * p)) & 15u;
+}
+
+template <int kHX, int kHXY, class Emit>
+__device__ __forceinline__ void hop_column_cube(const float* __restrict__ fc, const int nz, const uint32_t gv0,
+                                                const uint32_t XY, ACounters* __restrict__ ctr, Emit&& emit) {
+  // stencil columns (dx, dy): c0 (-1,-1) c1 (0,-1) c2 (-1,0) c3 (0,0)
+  // c4 (1,0) c5 (0,1) c6 (1,1); fc = column (0, 0) at brick layer -1
+  // plane z-1 (brick layer -1): the lower quad
+  HopQuad L = hop_quad(fc[-1 - kHX], fc[-kHX], fc[-1], fc[0], 0.f);
+  // plane z (layer 0)
+  const float* p0 = fc + kHXY;
+  float b0 = p0[-1 - kHX], b1 = p0[-kHX], b2 = p0[-1], b3 = p0[0];
+  HopQuad U = hop_quad(b3, p0[1], p0[kHX], p0[kHX + 1], 8.f);  // upper quad, positions 8.. (v's upper cube)
+#pragma unroll 2
+  for (int lz = 0; lz < TZ; ++lz) {
+    const float* p = fc + (lz + 2) * kHXY;  // plane z+1
+    const float n0 = p[-1 - kHX], n1 = p[-kHX], n2 = p[-1], n3 = p[0], n4 = p[1], n5 = p[kHX], n6 = p[kHX + 1];
+    const HopQuad Ln = hop_quad(b0, b1, b2, b3, 0.f);   // lower quad at plane z
+    const HopQuad Un = hop_quad(n3, n4, n5, n6, 8.f);   // upper quad at plane z+1
+    if (lz < nz) {
+      const float fv = b3;
+      if (!isfinite(fv)) atomicMin(&ctr->bad, gv0 + XY * uint32_t(lz));
+      // lower cube of v: L (plane z-1, corners 0..3) under Ln (plane z, 4..7);
+      // upper cube: U (plane z, positions 8..) under Un (plane z+1, +4)
+      const HopQuad cl = hop_cube(L, Ln);
+      const HopQuad cu = hop_cube(U, Un);
+      // U's corner 0 is v: position 8 -> 7 (v) after the -1 below
+      const float M = fmaxf(cl.M, cu.M), m = fminf(cl.m, cu.m);
+      const float pu = __fmaf_rn(feq(cu.M, M), (cu.tM - 1.f) - cl.tM, cl.tM);
+      const float pd = __fmaf_rn(feq(cl.m, m), cl.tm - (cu.tm - 1.f), cu.tm - 1.f);
+      emit(lz, uint8_t(hop_code(pu) | hop_code(pd) << 4));
+    }
+    L = Ln;
+    U = Un;
+    b0 = n0;
+    b1 = n1;
+    b2 = n2;
+    b3 = n3;
+  }
+}
+
 // ---------------------------------------------------------------- pass A --
 // One CTA (1024 threads, one per (x, y) column of 32 vertices) per 32^3
 // brick.
@@ -245,7 +334,7 @@ __device__ __forceinline__ void hop_column(const float* __restrict__ fc, const i
 //     The global id of that terminal is the vertex's partial label.
 //  5. Extrema and the distinct exit (shell) cells are appended to global
 //     lists, aggregated per brick.
-template <bool kTMA, bool kCodes = false>
+template <bool kTMA, bool kCodes = false, bool kCube = false>
 __global__ void __launch_bounds__(A_THREADS, 1)
     k_tile_segment(const __grid_constant__ CUtensorMap tmap, const float* __restrict__ field,
                    const uint8_t* __restrict__ gcodes, FDims d,
@@ -355,9 +444,14 @@ __global__ void __launch_bounds__(A_THREADS, 1)
   const int nz = min(TZ, int(d.Z) - gz0);  // in-volume layers of the brick
   const int hc = (lx + 1) + PX * (ly + 1);  // column in the pointer space (shell layer z = 0)
   const uint32_t gv0 = uint32_t(gx) + d.X * uint32_t(gy) + d.XY * uint32_t(gz0);
-  if (!kCodes && col_ok)
-    hop_column<HX, HXY>(f + (ly + 1) * HX + (lx + HXO), nz, gv0, d.XY, ctr,
-                        [&](int lz, uint8_t b) { code[hc + (lz + 1) * PXY] = b; });
+  if (!kCodes && col_ok) {
+    if (kCube)
+      hop_column_cube<HX, HXY>(f + (ly + 1) * HX + (lx + HXO), nz, gv0, d.XY, ctr,
+                               [&](int lz, uint8_t b) { code[hc + (lz + 1) * PXY] = b; });
+    else
+      hop_column<HX, HXY>(f + (ly + 1) * HX + (lx + HXO), nz, gv0, d.XY, ctr,
+                          [&](int lz, uint8_t b) { code[hc + (lz + 1) * PXY] = b; });
+  }
   if (kCodes) {
     // the brick's codes (k_hop_codes, brick-major) staged in the pointer area
     const uint8_t* st = reinterpret_cast<const uint8_t*>(Pd);
@@ -610,7 +704,7 @@ constexpr int CXY = HX * (HR + 2);
 constexpr int CN = CXY * HZ;
 constexpr int kCSmem = CN * 4 + 128;
 
-template <bool kTMA>
+template <bool kTMA, bool kCube = false>
 __global__ void __launch_bounds__(32 * HR, 4)
     k_hop_codes(const __grid_constant__ CUtensorMap tmap, const float* __restrict__ field, const FDims d,
                 uint8_t* __restrict__ codes, ACounters* __restrict__ ctr) {
@@ -657,8 +751,12 @@ __global__ void __launch_bounds__(32 * HR, 4)
     }
     if (col_ok) {
       const uint32_t gv0 = uint32_t(gx) + d.X * uint32_t(gy) + d.XY * uint32_t(gz0);
-      hop_column<HX, CXY>(f + (ly + 1) * HX + (lx + HXO), nz, gv0, d.XY, ctr,
-                          [&](int lz, uint8_t b) { out[lz << 10] = b; });
+      if (kCube)
+        hop_column_cube<HX, CXY>(f + (ly + 1) * HX + (lx + HXO), nz, gv0, d.XY, ctr,
+                                 [&](int lz, uint8_t b) { out[lz << 10] = b; });
+      else
+        hop_column<HX, CXY>(f + (ly + 1) * HX + (lx + HXO), nz, gv0, d.XY, ctr,
+                            [&](int lz, uint8_t b) { out[lz << 10] = b; });
     }
   }
   for (int lz = col_ok ? nz : 0; lz < TZ; ++lz) out[lz << 10] = 0xff;  // outside the volume: no hop
@@ -1890,6 +1988,11 @@ static void ensure_consts(Ctx& c) {
       CK(cudaFuncSetAttribute(k_tile_segment<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kASmem));
       CK(cudaFuncSetAttribute(k_tile_segment<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kASmem));
       CK(cudaFuncSetAttribute(k_hop_codes<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kCSmem));
+      CK(cudaFuncSetAttribute(k_hop_codes<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kCSmem));
+      CK(cudaFuncSetAttribute(k_hop_codes<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kCSmem));
+      CK(cudaFuncSetAttribute(k_tile_segment<true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kASmem));
+      CK(cudaFuncSetAttribute(k_tile_segment<false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              kASmem));
       CK(cudaFuncSetAttribute(k_hop_codes<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kCSmem));
       // on the context stream (a non-blocking stream does not wait on the legacy one)
       CK(cudaMemcpyToSymbolAsync(c_mrows, kTetRowsPacked, sizeof(kTetRowsPacked), 0, cudaMemcpyHostToDevice,
@@ -1927,8 +2030,12 @@ static void launch_pass_a(Ctx& c, const FDims& d, uint64_t ntiles, bool use_tma,
                                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NAN_REQUEST_ZERO_FMA) == CUDA_SUCCESS;
     }
     const unsigned hgrid = unsigned(ntiles * (TY / HR));
-    if (hop_tma)
+    if (hop_tma && c.hop_cube)
+      k_hop_codes<true, true><<<hgrid, 32 * HR, kCSmem, c.stream>>>(hmap, field, d, codes, ctr);
+    else if (hop_tma)
       k_hop_codes<true><<<hgrid, 32 * HR, kCSmem, c.stream>>>(hmap, field, d, codes, ctr);
+    else if (c.hop_cube)
+      k_hop_codes<false, true><<<hgrid, 32 * HR, kCSmem, c.stream>>>(hmap, field, d, codes, ctr);
     else
       k_hop_codes<false><<<hgrid, 32 * HR, kCSmem, c.stream>>>(hmap, field, d, codes, ctr);
     CK_LAUNCH("k_hop_codes");
@@ -1937,9 +2044,15 @@ static void launch_pass_a(Ctx& c, const FDims& d, uint64_t ntiles, bool use_tma,
     CK_LAUNCH("k_tile_segment");
     return;
   }
-  if (use_tma)
+  if (use_tma && c.hop_cube)
+    k_tile_segment<true, false, true><<<grid, A_THREADS, kASmem, c.stream>>>(
+        tmap, field, nullptr, d, maxima, minima, max_tt, min_tt, ext_cap, TT, tt_cap, TB, ltd, lta, ctr);
+  else if (use_tma)
     k_tile_segment<true><<<grid, A_THREADS, kASmem, c.stream>>>(tmap, field, nullptr, d, maxima, minima, max_tt,
                                                                 min_tt, ext_cap, TT, tt_cap, TB, ltd, lta, ctr);
+  else if (c.hop_cube)
+    k_tile_segment<false, false, true><<<grid, A_THREADS, kASmem, c.stream>>>(
+        tmap, field, nullptr, d, maxima, minima, max_tt, min_tt, ext_cap, TT, tt_cap, TB, ltd, lta, ctr);
   else
     k_tile_segment<false><<<grid, A_THREADS, kASmem, c.stream>>>(tmap, field, nullptr, d, maxima, minima, max_tt,
                                                                  min_tt, ext_cap, TT, tt_cap, TB, ltd, lta, ctr);

@@ -43,14 +43,15 @@ def test_golden_digest_files_are_complete(name):
 # path: the unresolved-entry guard of the token pass at scale.
 # Split (third field): pass A as the hop-code kernel + the code-fed brick
 # compression (PLMSS_OPT_PASS_A_SPLIT), else the single fused kernel.
-CASES = [("cfg1", 0, 1, 0), ("cfg1", 0, 0, 1), ("cfg2", 0, 1, 0), ("cfg2", 2, 1, 1), ("cfg2", 0, 0, 0),
-         ("cfg3", 0, 1, 0), ("cfg3", 0, 1, 1), ("cfg4", 0, 1, 0), ("cfg4", 0, 0, 1), ("cfg5", 0, 1, 0),
-         ("cfg5", 2, 1, 0), ("cfg5", 0, 1, 1)]
+# Hop (fourth field): 1 = the cube-shared steepest hops (PLMSS_OPT_HOP_CUBE).
+CASES = [("cfg1", 0, 1, 0, 0), ("cfg1", 0, 0, 1, 1), ("cfg2", 0, 1, 0, 0), ("cfg2", 2, 1, 1, 0), ("cfg2", 0, 0, 0, 1),
+         ("cfg3", 0, 1, 0, 0), ("cfg3", 0, 1, 1, 1), ("cfg4", 0, 1, 0, 0), ("cfg4", 0, 0, 1, 0), ("cfg4", 0, 1, 0, 1),
+         ("cfg5", 0, 1, 0, 0), ("cfg5", 2, 1, 0, 0), ("cfg5", 0, 1, 1, 0), ("cfg5", 0, 1, 0, 1)]
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name,path,spec,split", CASES)
-def test_full_size_matches_oracle(plmss, gpu, name, path, spec, split):
+@pytest.mark.parametrize("name,path,spec,split,hop", CASES)
+def test_full_size_matches_oracle(plmss, gpu, name, path, spec, split, hop):
     import torch
 
     from paper_2303_15491_b200.configs import CONFIGS
@@ -65,12 +66,14 @@ def test_full_size_matches_oracle(plmss, gpu, name, path, spec, split):
     gpu.set_option(plmss.OPT_COMBINE_PATH, path)
     gpu.set_option(plmss.OPT_SPECULATIVE_SWEEPS, spec)
     gpu.set_option(plmss.OPT_PASS_A_SPLIT, split)
+    gpu.set_option(plmss.OPT_HOP_CUBE, hop)
     try:
         res = plmss.pipeline(cfg.dims, f, ctx=gpu)
     finally:
         gpu.set_option(plmss.OPT_COMBINE_PATH, 0)
         gpu.set_option(plmss.OPT_SPECULATIVE_SWEEPS, 1)
         gpu.set_option(plmss.OPT_PASS_A_SPLIT, 0)
+        gpu.set_option(plmss.OPT_HOP_CUBE, 0)
     del f
     assert (res.n_maxima, res.n_minima, res.n_regions, res.n_tris) == (g["n_maxima"], g["n_minima"],
                                                                        g["n_regions"], g["n_tris"])
