@@ -301,7 +301,7 @@ int plmss_b200_copy(plmss_ctx* ctx, void* dst, const void* d_src, int64_t bytes,
  *   PLMSS_OPT_PASS_A_SPLIT  1: pass A as two kernels (hop codes at high
  *                           occupancy, then the brick compression from the
  *                           codes), 0: one fused kernel (both are exact);
- *   PLMSS_OPT_HOP_CUBE      1: steepest hops from shared 2x2 quads / unit
+ *   PLMSS_OPT_HOP_CUBE      1 (default): steepest hops from shared 2x2 quads / unit
  *                           cubes, 0: per-vertex equality masks (both exact). */
 /* ---- callers either side of the path ------------------
  * weld_points (marching.hpp:138-140, marching.cpp:400-417): merges
