@@ -302,7 +302,11 @@ int plmss_b200_copy(plmss_ctx* ctx, void* dst, const void* d_src, int64_t bytes,
  *                           occupancy, then the brick compression from the
  *                           codes), 0: one fused kernel (both are exact);
  *   PLMSS_OPT_HOP_CUBE      1 (default): steepest hops from shared 2x2 quads / unit
- *                           cubes, 0: per-vertex equality masks (both exact). */
+ *                           cubes, 0: per-vertex equality masks (both exact);
+ *   PLMSS_OPT_IDS_IN_COUNT  1: region tokens in a scratch array, the count pass
+ *                           writes the dense ids (no in-place id pass over
+ *                           ms), 0: tokens in ms, counts interleaved with the
+ *                           token pass, then the id pass (both exact). */
 /* ---- callers either side of the path ------------------
  * weld_points (marching.hpp:138-140, marching.cpp:400-417): merges
  * bitwise-identical points of a separator soup in place, the first occurrence
@@ -357,7 +361,8 @@ enum plmss_option {
   PLMSS_OPT_TMA = 3,
   PLMSS_OPT_SPECULATIVE_SWEEPS = 4,
   PLMSS_OPT_PASS_A_SPLIT = 5,
-  PLMSS_OPT_HOP_CUBE = 6
+  PLMSS_OPT_HOP_CUBE = 6,
+  PLMSS_OPT_IDS_IN_COUNT = 7
 };
 int plmss_b200_ctx_set_option(plmss_ctx* ctx, int option, int64_t value);
 

@@ -8,7 +8,7 @@ kernels (csrc/, libplmss_b200.so) behind the C-ABI of include/plmss_b200.h;
 this package is the Python mirror of the reference interface on top of it.
 """
 from .api import (  # noqa: F401
-    ASCENDING, BOTH, DESCENDING, OPT_COMBINE_PATH, OPT_PIPELINE_PATH, OPT_HOP_CUBE, OPT_PASS_A_SPLIT, OPT_SPECULATIVE_SWEEPS, OPT_TMA,
+    ASCENDING, BOTH, DESCENDING, OPT_COMBINE_PATH, OPT_PIPELINE_PATH, OPT_HOP_CUBE, OPT_IDS_IN_COUNT, OPT_PASS_A_SPLIT, OPT_SPECULATIVE_SWEEPS, OPT_TMA,
     Context,
     FormatError, IoError, SegmentationResult, combine_ms, compute_order, default_context, emit_boundaries,
     emit_separators, fetch, index_separators, lib, materialize_separators, materialize_separators_chunked, pipeline,

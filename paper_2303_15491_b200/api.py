@@ -26,7 +26,8 @@ LIB_PATH = os.environ.get("PLMSS_B200_LIB") or os.path.join(PKG, "libplmss_b200.
 
 KEY_F32, KEY_F64, KEY_RANK = 0, 1, 2
 ASCENDING, DESCENDING, BOTH = 0, 1, 2
-OPT_COMBINE_PATH, OPT_PIPELINE_PATH, OPT_TMA, OPT_SPECULATIVE_SWEEPS, OPT_PASS_A_SPLIT, OPT_HOP_CUBE = 1, 2, 3, 4, 5, 6
+(OPT_COMBINE_PATH, OPT_PIPELINE_PATH, OPT_TMA, OPT_SPECULATIVE_SWEEPS, OPT_PASS_A_SPLIT, OPT_HOP_CUBE,
+ OPT_IDS_IN_COUNT) = 1, 2, 3, 4, 5, 6, 7
 
 class FormatError(RuntimeError):
     """io.hpp:22-24: malformed input (sizes, magic, unknown dtype)."""

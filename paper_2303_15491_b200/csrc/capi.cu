@@ -513,6 +513,10 @@ int plmss_b200_ctx_set_option(plmss_ctx* p, int option, int64_t value) {
       c.hop_cube = value != 0;
       return;
     }
+    if (option == PLMSS_OPT_IDS_IN_COUNT) {
+      c.ids_in_count = value != 0;
+      return;
+    }
     if (option == PLMSS_OPT_PIPELINE_PATH) {
       if (value < 0 || value > 1) fail(PLMSS_ERR_INVALID_ARGUMENT, "pipeline path must be 0 or 1");
       c.pipeline_path = int(value);

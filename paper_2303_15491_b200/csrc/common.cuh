@@ -77,6 +77,7 @@ enum Slot {
   S_LTD, S_LTA, S_TB, S_SD, S_SA, S_RK,  // fused pipeline: terminal indices, brick headers, table labels
   S_SLAB_BND,                             // z-slab pipeline: boundary layers
   S_CODES,                                // split pass A: hop codes (1 B per padded brick cell)
+  S_TOKENS,                               // region tokens when the count pass writes the ids
   S_COUNT
 };
 
@@ -143,6 +144,7 @@ struct Ctx {
   int spec_sweeps = 1;   // PLMSS_OPT_SPECULATIVE_SWEEPS
   bool pass_a_split = false;  // PLMSS_OPT_PASS_A_SPLIT
   bool hop_cube = true;       // PLMSS_OPT_HOP_CUBE
+  bool ids_in_count = false;  // PLMSS_OPT_IDS_IN_COUNT
   // Adaptive capacities of the fused pipeline (remembered between calls).
   uint64_t fused_exit_cap = 0, fused_pair_hint = 0, fused_tri_cap = 0, fused_ext_cap = 0;
   // Diagnostics of the last fused call: [0] exit entries, [1] pass-A retries,

@@ -1129,7 +1129,18 @@ struct BrickArgs {
   uint8_t* cls;                   // per cube: 0 one region, m8 two labels, 0xff more
   uint32_t *desc, *asc, *ms;      // ms holds the region token until k_ms_ids (null: labels only)
   int* overflow;
+  // count pass with ids (PLMSS_OPT_IDS_IN_COUNT): ms holds the tokens, the
+  // count pass writes every owned vertex's dense id into ids_out (dense:
+  // bitmap word prefix, hash: slot -> id), so no id pass over ms is needed
+  uint32_t* ids_out;
+  const uint32_t *prefix, *slot_id;
 };
+
+// region token -> dense MS id, the count pass's copy of token_id
+__device__ __forceinline__ uint32_t brick_token_id(const BrickArgs& a, uint32_t k) {
+  if (a.prefix) return __ldg(a.prefix + (k >> 5)) + __popc(__ldg(a.bitmap + (k >> 5)) & ((1u << (k & 31)) - 1u));
+  return __ldg(a.slot_id + k);
+}
 
 // Pass C1 (k_tokens): every vertex's final pair from its LT indices and its
 // brick's table, written as desc/asc (vertex ids of the two extrema) and as
@@ -1380,6 +1391,19 @@ __global__ void __launch_bounds__(B_THREADS, 4) k_brick(const BrickArgs a) {
         if (i < zn) ring[((z0 + i) & (kRing - 1)) * LQ + q] = t[i];
     }
     __syncthreads();
+    if (a.ids_out && gx0 + uint32_t(lane) < d.X && cy < d.Y) {
+      // the owned layers of this thread's vertex column (x = lane, y = w)
+      uint32_t lt = ~0u, lid = 0;
+      uint32_t* o = a.ids_out + (uint64_t(gx0 + lane) + uint64_t(d.X) * (uint64_t(cy) + uint64_t(d.Y) * gz0));
+      for (int z = z0; z < z0 + zn && z < TZ; ++z) {
+        const uint32_t tk = ring[(z & (kRing - 1)) * LQ + w * LW + lane];
+        if (tk != lt) {
+          lt = tk;
+          lid = brick_token_id(a, tk);
+        }
+        o[uint64_t(z) * d.XY] = lid;
+      }
+    }
     // ---- cube layers z-1 whose two vertex layers are loaded
     for (int z = max(z0, 1); z < z0 + zn; ++z) {
       const uint32_t* lo = ring + ((z - 1) & (kRing - 1)) * LQ;
@@ -1487,6 +1511,14 @@ __device__ __forceinline__ void brick_tma_body(const CUtensorMap& mtok, const Br
   const uint64_t chstep = uint64_t(d.Y - 1) * a.nxc;
   uint32_t pf[4] = {0, 0, 0, 0};  // top face of this thread's previous cube
   uint32_t pu = 0;                 // ... and whether its four labels agree (0 / 1)
+  // ids (a.ids_out): this thread's vertex column
+  const bool vert_ok = gx0 + uint32_t(lane) < d.X && cy < d.Y;
+  uint32_t* ids_col = a.ids_out ? a.ids_out + (uint64_t(gx0 + lane) + uint64_t(d.X) * (uint64_t(cy) + uint64_t(d.Y) * gz0))
+                                : nullptr;
+  if (a.ids_out && vert_ok && ncl == 0 && gz0 == d.Z - 1) {
+    // a brick made of the volume's last vertex layer only: no cube layers
+    *ids_col = brick_token_id(a, __ldg(a.ms + (uint64_t(gx0 + lane) + uint64_t(d.X) * (uint64_t(cy) + uint64_t(d.Y) * gz0))));
+  }
   if (tid == 0) {
     for (int k = 0; k < 2; ++k) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s_bar[k])));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -1577,6 +1609,21 @@ __device__ __forceinline__ void brick_tma_body(const CUtensorMap& mtok, const Br
     } else {
 #pragma unroll 1
       for (int cl = 0; cl < cn; ++cl) cube(bb[cl + 1], cl);
+    }
+    if (a.ids_out && vert_ok) {
+      // this thread's vertex column: the batch's bottom layers, and the
+      // volume's top layer when the batch ends there
+      const int nv = cn + ((gz0 + uint32_t(b * kBatch + cn) == d.Z - 1) ? 1 : 0);
+      uint32_t* o = ids_col + uint64_t(b * kBatch) * d.XY;
+      uint32_t lt = ~0u, lid = 0;
+      for (int i = 0; i < nv; ++i) {
+        const uint32_t tk = bb[i][w][lane];
+        if (tk != lt) {
+          lt = tk;
+          lid = brick_token_id(a, tk);
+        }
+        o[uint64_t(i) * d.XY] = lid;
+      }
     }
     // the batch's chunk counts, one store per layer from lanes 0 .. cn-1
     if (lane < cn && row_ok) chp[uint64_t(lane) * chstep] = btot;
@@ -2240,7 +2287,12 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
     ba.cls = c.get_t<uint8_t>(S_MASK, uint64_t(g.cubes ? g.cubes : 1));
     const unsigned cgrid = unsigned((TY / RY) * ntiles);
     const unsigned tgrid = unsigned((TY / kTokRows) * ntiles);
-    // tokens (in ms) as a 3-D tensor for the count pass
+    // tokens as a 3-D tensor for the count pass: in ms (ids rewritten in
+    // place by k_ms_ids), or (PLMSS_OPT_IDS_IN_COUNT) in a scratch array the
+    // count pass translates into ms
+    const bool ids_in_count = c.ids_in_count;
+    uint32_t* tokbuf = ids_in_count ? c.get_t<uint32_t>(S_TOKENS, uint64_t(g.n)) : ms;
+    ba.ms = tokbuf;
     CUtensorMap mtok;
     bool tok_tma = lt_tma && (g.X % 4) == 0;
     if (tok_tma) {
@@ -2248,7 +2300,7 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
       const cuuint64_t gstride[2] = {cuuint64_t(g.X) * 4, cuuint64_t(g.X) * cuuint64_t(g.Y) * 4};
       const cuuint32_t box[3] = {cuuint32_t(TLW), cuuint32_t(RY + 1), cuuint32_t(kBatch + 1)};
       const cuuint32_t estride[3] = {1, 1, 1};
-      tok_tma = tensor_map_encoder()(&mtok, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, ms, gdim, gstride, box, estride,
+      tok_tma = tensor_map_encoder()(&mtok, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, tokbuf, gdim, gstride, box, estride,
                                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
                 CUDA_SUCCESS;
@@ -2270,7 +2322,14 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
       // on the side stream as soon as they are written
       const uint32_t bpl = d.tx * d.ty;
       const unsigned items = bpl * (TY / kTokRows);
-      if (lt_tma && tok_tma) {
+      if (ids_in_count) {
+        // all tokens first; the count pass (ids) runs once the set is complete
+        if (lt_tma)
+          k_tokens_tma<true><<<tgrid, 32 * kTokRows, 0, c.stream>>>(mld, mla, ba);
+        else
+          k_tokens<true><<<tgrid, 32 * kTokRows, 0, c.stream>>>(ba);
+        CK_LAUNCH("k_tokens");
+      } else if (lt_tma && tok_tma) {
         // one stream: launch L = tokens of layer L with the count pass of
         // layer L - 2 in the same grid (see k_slab_tma), then the last two
         // count passes together
@@ -2374,7 +2433,19 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
       c.stats[2] = int64_t(fcap);
     }
     o.n_regions = R;
-    if (dense) {
+    if (ids_in_count) {
+      // cube classes, separator counts and the dense ids of every vertex
+      BrickArgs cb = ba;
+      cb.ids_out = ms;
+      cb.bitmap = bitmap;
+      cb.prefix = dense ? prefix : nullptr;
+      cb.slot_id = slot_id;
+      if (tok_tma)
+        k_brick_tma<<<cgrid, B_THREADS, 0, c.stream>>>(mtok, cb);
+      else
+        k_brick<<<cgrid, B_THREADS, 0, c.stream>>>(cb);
+      CK_LAUNCH("k_brick");
+    } else if (dense) {
       CK(cudaStreamWaitEvent(c.stream, c.join, 0));  // count passes done
     } else {
       // cube classes and separator counts from the tokens
@@ -2387,7 +2458,7 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
     const uint64_t total = nchunks ? exclusive_scan_u64(c, chunk, int64_t(nchunks), true) : 0;
     c.mark(4);
     // ---- D: ms tokens -> dense ids; separator records at their chunk offsets
-    {
+    if (!ids_in_count) {
       const unsigned mgrid = unsigned((uint64_t(g.n) + 1023) / 1024);
       if (dense)
         k_ms_ids<true><<<mgrid, 256, 0, c.stream>>>(ms, uint64_t(g.n), bitmap, prefix, slot_id);

@@ -44,9 +44,11 @@ def test_golden_digest_files_are_complete(name):
 # Split (third field): pass A as the hop-code kernel + the code-fed brick
 # compression (PLMSS_OPT_PASS_A_SPLIT), else the single fused kernel.
 # Hop (fourth field): 1 = the cube-shared steepest hops (PLMSS_OPT_HOP_CUBE).
+# Hop 2 = cube hops + the count pass writing the ids (PLMSS_OPT_IDS_IN_COUNT).
 CASES = [("cfg1", 0, 1, 0, 0), ("cfg1", 0, 0, 1, 1), ("cfg2", 0, 1, 0, 0), ("cfg2", 2, 1, 1, 0), ("cfg2", 0, 0, 0, 1),
-         ("cfg3", 0, 1, 0, 0), ("cfg3", 0, 1, 1, 1), ("cfg4", 0, 1, 0, 0), ("cfg4", 0, 0, 1, 0), ("cfg4", 0, 1, 0, 1),
-         ("cfg5", 0, 1, 0, 0), ("cfg5", 2, 1, 0, 0), ("cfg5", 0, 1, 1, 0), ("cfg5", 0, 1, 0, 1)]
+         ("cfg2", 0, 1, 0, 2), ("cfg3", 0, 1, 0, 0), ("cfg3", 0, 1, 1, 1), ("cfg3", 0, 1, 0, 2), ("cfg4", 0, 1, 0, 0),
+         ("cfg4", 0, 0, 1, 0), ("cfg4", 0, 1, 0, 1), ("cfg4", 0, 0, 0, 2), ("cfg5", 0, 1, 0, 0), ("cfg5", 2, 1, 0, 0),
+         ("cfg5", 0, 1, 1, 0), ("cfg5", 0, 1, 0, 1), ("cfg5", 0, 1, 0, 2), ("cfg5", 2, 1, 0, 2)]
 
 
 @pytest.mark.gpu
@@ -66,14 +68,16 @@ def test_full_size_matches_oracle(plmss, gpu, name, path, spec, split, hop):
     gpu.set_option(plmss.OPT_COMBINE_PATH, path)
     gpu.set_option(plmss.OPT_SPECULATIVE_SWEEPS, spec)
     gpu.set_option(plmss.OPT_PASS_A_SPLIT, split)
-    gpu.set_option(plmss.OPT_HOP_CUBE, hop)
+    gpu.set_option(plmss.OPT_HOP_CUBE, 1 if hop else 0)
+    gpu.set_option(plmss.OPT_IDS_IN_COUNT, 1 if hop == 2 else 0)
     try:
         res = plmss.pipeline(cfg.dims, f, ctx=gpu)
     finally:
         gpu.set_option(plmss.OPT_COMBINE_PATH, 0)
         gpu.set_option(plmss.OPT_SPECULATIVE_SWEEPS, 1)
         gpu.set_option(plmss.OPT_PASS_A_SPLIT, 0)
-        gpu.set_option(plmss.OPT_HOP_CUBE, 0)
+        gpu.set_option(plmss.OPT_HOP_CUBE, 1)
+        gpu.set_option(plmss.OPT_IDS_IN_COUNT, 0)
     del f
     assert (res.n_maxima, res.n_minima, res.n_regions, res.n_tris) == (g["n_maxima"], g["n_minima"],
                                                                        g["n_regions"], g["n_tris"])

@@ -224,23 +224,28 @@ def test_compute_order(plmss, gpu, restatement):
 # path: 0 fused (dense rank-product region bitmap), 1 staged kernels,
 #       2 fused with the hash-set region keys (the path for n_max * n_min >= 2^32),
 #       3 fused with pass A split into the hop-code and brick kernels,
-#       4 fused with the cube-shared steepest hops, 5 = 3 + 4
-@pytest.mark.parametrize("path", [0, 1, 2, 3, 4, 5])
+#       (paths 0-3 with the per-vertex equality-mask hops, 4-7 with the
+#       cube-shared hops, the default)
+#       4 fused with the cube-shared steepest hops, 5 = 3 + 4,
+#       6 fused with the ids written by the count pass, 7 = 6 + hash-set keys
+@pytest.mark.parametrize("path", [0, 1, 2, 3, 4, 5, 6, 7])
 @pytest.mark.parametrize("name", golden_cases())
 def test_pipeline_matches_reference(plmss, gpu, name, path):
     g = load_case(name)
     dims = tuple(int(x) for x in g["dims"])
     gpu.set_option(2, 1 if path == 1 else 0)  # PIPELINE_PATH: 0 fused, 1 staged
-    gpu.set_option(1, 2 if path == 2 else 0)  # COMBINE_PATH: 2 hash
+    gpu.set_option(1, 2 if path in (2, 7) else 0)  # COMBINE_PATH: 2 hash
     gpu.set_option(plmss.OPT_PASS_A_SPLIT, 1 if path in (3, 5) else 0)
-    gpu.set_option(plmss.OPT_HOP_CUBE, 1 if path in (4, 5) else 0)
+    gpu.set_option(plmss.OPT_HOP_CUBE, 1 if path in (4, 5, 6, 7) else 0)
+    gpu.set_option(plmss.OPT_IDS_IN_COUNT, 1 if path in (6, 7) else 0)
     try:
         res = plmss.pipeline(dims, dev(g["field"]), ctx=gpu)
     finally:
         gpu.set_option(2, 0)
         gpu.set_option(1, 0)
         gpu.set_option(plmss.OPT_PASS_A_SPLIT, 0)
-        gpu.set_option(plmss.OPT_HOP_CUBE, 0)
+        gpu.set_option(plmss.OPT_HOP_CUBE, 1)  # the default
+        gpu.set_option(plmss.OPT_IDS_IN_COUNT, 0)
     out = plmss.fetch(gpu, res)
     for k, gk in (("desc", "desc"), ("asc", "asc"), ("ms", "ms_region"), ("maxima", "maxima"), ("minima", "minima")):
         assert np.array_equal(u32(out[k]), g[gk]), k
@@ -280,20 +285,22 @@ def _field(kind, dims, seed):
     return host_field(scaled(CONFIGS["cfg2"], dims))
 
 
-@pytest.mark.parametrize("path", [0, 2, 3, 4, 5])
+@pytest.mark.parametrize("path", [0, 2, 3, 4, 5, 6, 7])
 @pytest.mark.parametrize("dims,kind", [((97, 66, 40), "gauss"), ((33, 33, 33), "noise"), ((64, 31, 65), "ties"),
-                                       ((128, 96, 70), "gauss"), ((70, 40, 36), "noise")])
+                                       ((128, 96, 70), "gauss"), ((70, 40, 36), "noise"), ((36, 20, 33), "ties")])
 def test_pipeline_brick_geometry(plmss, gpu, restatement, dims, kind, path):
     f = _field(kind, dims, sum(dims))
-    gpu.set_option(1, 2 if path == 2 else 0)
+    gpu.set_option(1, 2 if path in (2, 7) else 0)
     gpu.set_option(plmss.OPT_PASS_A_SPLIT, 1 if path in (3, 5) else 0)
-    gpu.set_option(plmss.OPT_HOP_CUBE, 1 if path in (4, 5) else 0)
+    gpu.set_option(plmss.OPT_HOP_CUBE, 1 if path in (4, 5, 6, 7) else 0)
+    gpu.set_option(plmss.OPT_IDS_IN_COUNT, 1 if path in (6, 7) else 0)
     try:
         res = plmss.pipeline(dims, dev(f), ctx=gpu)
     finally:
         gpu.set_option(1, 0)
         gpu.set_option(plmss.OPT_PASS_A_SPLIT, 0)
-        gpu.set_option(plmss.OPT_HOP_CUBE, 0)
+        gpu.set_option(plmss.OPT_HOP_CUBE, 1)  # the default
+        gpu.set_option(plmss.OPT_IDS_IN_COUNT, 0)
     out = plmss.fetch(gpu, res)
     s = restatement.segment(dims, values=f.astype(np.float64))
     ms, keys = restatement.combine_ms(s["asc"], s["desc"])
