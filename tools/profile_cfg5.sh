@@ -12,7 +12,7 @@ python bench.py --steps 10 --warmup 3 > gpurun_out/bench_${TAG}.json 2> gpurun_o
 cat gpurun_out/bench_${TAG}.json
 ncu --metrics gpu__time_duration.sum,smsp__inst_executed.sum,smsp__issue_active.avg.pct_of_peak_sustained_active,dram__bytes_read.sum,dram__bytes_write.sum \
     --clock-control none --csv --log-file gpurun_out/launches_${TAG}.csv \
-    python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu-baseline > gpurun_out/ncu_launch_${TAG}.log 2>&1 || true
+    python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu-baseline --dropin-config "" --no-parity > gpurun_out/ncu_launch_${TAG}.log 2>&1 || true
 ncu --set full --import-source on --clock-control none -k "regex:${KRE}" -c 6 \
-    -o gpurun_out/prof_${TAG} -f python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu-baseline > gpurun_out/ncu_full_${TAG}.log 2>&1 || true
+    -o gpurun_out/prof_${TAG} -f python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu-baseline --dropin-config "" --no-parity > gpurun_out/ncu_full_${TAG}.log 2>&1 || true
 tail -3 gpurun_out/ncu_full_${TAG}.log
