@@ -303,7 +303,7 @@ int plmss_b200_copy(plmss_ctx* ctx, void* dst, const void* d_src, int64_t bytes,
  *                           codes), 0: one fused kernel (both are exact);
  *   PLMSS_OPT_HOP_CUBE      1 (default): steepest hops from shared 2x2 quads / unit
  *                           cubes, 0: per-vertex equality masks (both exact);
- *   PLMSS_OPT_IDS_IN_COUNT  1: region tokens in a scratch array, the count pass
+ *   PLMSS_OPT_IDS_IN_COUNT  1 (default): region tokens in a scratch array, the count pass
  *                           writes the dense ids (no in-place id pass over
  *                           ms), 0: tokens in ms, counts interleaved with the
  *                           token pass, then the id pass (both exact). */

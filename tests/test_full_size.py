@@ -77,7 +77,7 @@ def test_full_size_matches_oracle(plmss, gpu, name, path, spec, split, hop):
         gpu.set_option(plmss.OPT_SPECULATIVE_SWEEPS, 1)
         gpu.set_option(plmss.OPT_PASS_A_SPLIT, 0)
         gpu.set_option(plmss.OPT_HOP_CUBE, 1)
-        gpu.set_option(plmss.OPT_IDS_IN_COUNT, 0)
+        gpu.set_option(plmss.OPT_IDS_IN_COUNT, 1)
     del f
     assert (res.n_maxima, res.n_minima, res.n_regions, res.n_tris) == (g["n_maxima"], g["n_minima"],
                                                                        g["n_regions"], g["n_tris"])

@@ -227,7 +227,9 @@ def test_compute_order(plmss, gpu, restatement):
 #       (paths 0-3 with the per-vertex equality-mask hops, 4-7 with the
 #       cube-shared hops, the default)
 #       4 fused with the cube-shared steepest hops, 5 = 3 + 4,
-#       6 fused with the ids written by the count pass, 7 = 6 + hash-set keys
+#       6 fused with the ids written by the count pass (the default), 7 = 6 +
+#       hash-set keys; paths 0-5 run the interleaved token / count passes and
+#       the in-place id pass
 @pytest.mark.parametrize("path", [0, 1, 2, 3, 4, 5, 6, 7])
 @pytest.mark.parametrize("name", golden_cases())
 def test_pipeline_matches_reference(plmss, gpu, name, path):
@@ -245,7 +247,7 @@ def test_pipeline_matches_reference(plmss, gpu, name, path):
         gpu.set_option(1, 0)
         gpu.set_option(plmss.OPT_PASS_A_SPLIT, 0)
         gpu.set_option(plmss.OPT_HOP_CUBE, 1)  # the default
-        gpu.set_option(plmss.OPT_IDS_IN_COUNT, 0)
+        gpu.set_option(plmss.OPT_IDS_IN_COUNT, 1)  # the default
     out = plmss.fetch(gpu, res)
     for k, gk in (("desc", "desc"), ("asc", "asc"), ("ms", "ms_region"), ("maxima", "maxima"), ("minima", "minima")):
         assert np.array_equal(u32(out[k]), g[gk]), k
@@ -300,7 +302,7 @@ def test_pipeline_brick_geometry(plmss, gpu, restatement, dims, kind, path):
         gpu.set_option(1, 0)
         gpu.set_option(plmss.OPT_PASS_A_SPLIT, 0)
         gpu.set_option(plmss.OPT_HOP_CUBE, 1)  # the default
-        gpu.set_option(plmss.OPT_IDS_IN_COUNT, 0)
+        gpu.set_option(plmss.OPT_IDS_IN_COUNT, 1)  # the default
     out = plmss.fetch(gpu, res)
     s = restatement.segment(dims, values=f.astype(np.float64))
     ms, keys = restatement.combine_ms(s["asc"], s["desc"])
