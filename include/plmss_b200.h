@@ -143,10 +143,13 @@ int plmss_b200_segment_slab(plmss_ctx* ctx, const int64_t dims[3], int key_type,
  *                    desc / asc (global vertex ids), region tokens, the slab's
  *                    distinct rank pairs.
  *     -> all_gather the rank pairs
- *   3 slab_ids     : global dense MS ids (the combine_ms order) into ms.
- *     -> the next rank's first layer of ids into ms's extra layer
- *   4 slab_emit    : separator records of the owned cube layers, global cell
- *                    ids, reference order.
+ *   3 slab_ids     : the global region table (combine_ms order); the hash
+ *                    mode writes the dense ids into ms, the dense mode keeps
+ *                    its (globally consistent) region tokens there.
+ *     -> the next rank's first layer of ms into ms's extra layer
+ *   4 slab_emit    : the dense ids of the owned vertices (+ the extra layer)
+ *                    into d_ids, separator records of the owned cube layers,
+ *                    global cell ids, reference order.
  * No reference counterpart (the reference is one process, parallel.hpp:27-57
  * splits work among threads); results equal the single-volume pipeline's.
  * Slabs are whole 32-layer brick layers: z0 % 32 == 0, z1 % 32 == 0 or
@@ -182,8 +185,9 @@ int plmss_b200_slab_resolve(plmss_ctx* ctx, const uint32_t* d_boundary_all, int 
                             plmss_slab_info* info);
 /* d_keys_all: every rank's d_keys concatenated (duplicates allowed). */
 int plmss_b200_slab_ids(plmss_ctx* ctx, const uint64_t* d_keys_all, int64_t n_keys_all, plmss_slab_info* info);
-/* The layer z1 of d_ms holds the next rank's first layer of ids (z1 < Z). */
-int plmss_b200_slab_emit(plmss_ctx* ctx, plmss_slab_info* info);
+/* The layer z1 of d_ms holds the next rank's first layer of d_ms (z1 < Z);
+ * d_ids has the layout of d_ms and receives the dense MS ids. */
+int plmss_b200_slab_emit(plmss_ctx* ctx, uint32_t* d_ids, plmss_slab_info* info);
 
 /* Step 1 only (detail::seed_hops_both, segmentation.cpp:60-85): hop targets. */
 int plmss_b200_seed_hops(plmss_ctx* ctx, const int64_t dims[3], int key_type, const void* d_keys,

@@ -127,7 +127,7 @@ def lib() -> C.CDLL:
         L.plmss_b200_slab_segment.argtypes = [vp, vp, i64, i64, vp, SI]
         L.plmss_b200_slab_resolve.argtypes = [vp, vp, i32, i32, vp, vp, vp, vp, vp, vp, vp, SI]
         L.plmss_b200_slab_ids.argtypes = [vp, vp, i64, SI]
-        L.plmss_b200_slab_emit.argtypes = [vp, SI]
+        L.plmss_b200_slab_emit.argtypes = [vp, vp, SI]
         L.plmss_b200_tet_table.argtypes = [vp, vp]
         L.plmss_b200_tet_table.restype = None
         L.plmss_b200_launch_count.restype = C.c_ulonglong

@@ -639,11 +639,11 @@ int plmss_b200_slab_ids(plmss_ctx* p, const uint64_t* d_keys_all, int64_t n_keys
   });
 }
 
-int plmss_b200_slab_emit(plmss_ctx* p, plmss_slab_info* info) {
+int plmss_b200_slab_emit(plmss_ctx* p, uint32_t* d_ids, plmss_slab_info* info) {
   return guarded([&] {
     Ctx& c = C(p);
     set_device(c);
-    slab_emit(c, info);
+    slab_emit(c, d_ids, info);
   });
 }
 

@@ -95,6 +95,7 @@ struct SlabState {
   int sweeps = 0;
   const uint32_t *maxs_g = nullptr, *mins_g = nullptr;
   uint32_t *desc = nullptr, *asc = nullptr, *ms = nullptr;
+  uint32_t *bitmap = nullptr, *prefix = nullptr;  // dense mode: the global region bitmap and word prefix
   uint64_t* keys = nullptr;
   plmss_tri* tris = nullptr;
 };
@@ -237,7 +238,7 @@ void slab_resolve(Ctx& c, const uint32_t* G, int world, int rank, const int64_t*
                   const int64_t* min_counts, const uint32_t* maxs_g, const uint32_t* mins_g, uint32_t* desc,
                   uint32_t* asc, uint32_t* ms, plmss_slab_info* info);
 void slab_ids(Ctx& c, const uint64_t* keys_all, int64_t n_keys_all, plmss_slab_info* info);
-void slab_emit(Ctx& c, plmss_slab_info* info);
+void slab_emit(Ctx& c, uint32_t* ids, plmss_slab_info* info);
 
 // synth.cu
 // io.cu: callers either side of the path

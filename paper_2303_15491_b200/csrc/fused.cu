@@ -1139,7 +1139,8 @@ struct BrickArgs {
 // region token -> dense MS id, the count pass's copy of token_id
 __device__ __forceinline__ uint32_t brick_token_id(const BrickArgs& a, uint32_t k) {
   if (a.prefix) return __ldg(a.prefix + (k >> 5)) + __popc(__ldg(a.bitmap + (k >> 5)) & ((1u << (k & 31)) - 1u));
-  return __ldg(a.slot_id + k);
+  if (a.slot_id) return __ldg(a.slot_id + k);
+  return k;  // ms already holds the ids (copied out)
 }
 
 // Pass C1 (k_tokens): every vertex's final pair from its LT indices and its
@@ -1395,7 +1396,9 @@ __global__ void __launch_bounds__(B_THREADS, 4) k_brick(const BrickArgs a) {
       // the owned layers of this thread's vertex column (x = lane, y = w)
       uint32_t lt = ~0u, lid = 0;
       uint32_t* o = a.ids_out + (uint64_t(gx0 + lane) + uint64_t(d.X) * (uint64_t(cy) + uint64_t(d.Y) * gz0));
-      for (int z = z0; z < z0 + zn && z < TZ; ++z) {
+      // the brick's own layers, and the grid's last layer when it is this
+      // brick's layer 32 (a z-slab's extra layer)
+      for (int z = z0; z < z0 + zn && (z < TZ || gz0 + uint32_t(z) == d.Z - 1); ++z) {
         const uint32_t tk = ring[(z & (kRing - 1)) * LQ + w * LW + lane];
         if (tk != lt) {
           lt = tk;
@@ -3017,8 +3020,11 @@ void slab_ids(Ctx& c, const uint64_t* keys_all, int64_t n_keys_all, plmss_slab_i
     k_bitmap_ids<<<unsigned(nb), kWB, 0, c.stream>>>(bitmap, nw, bsum, uint32_t(st.n_max_g), st.maxs_g, st.mins_g,
                                                       prefix, st.keys, false);
     CK_LAUNCH("k_bitmap_ids");
-    k_ms_ids<true><<<mgrid, 256, 0, c.stream>>>(st.ms, nown, bitmap, prefix, nullptr);
-    CK_LAUNCH("k_ms_ids");
+    // ms keeps the (globally consistent) dense-key tokens: the count pass of
+    // slab_emit writes the ids, the halo layer exchanged is tokens too
+    st.bitmap = bitmap;
+    st.prefix = prefix;
+    (void)mgrid;
   } else {
     // sort + unique of the gathered rank pairs
     const int64_t n = std::max<int64_t>(n_keys_all, 1);
@@ -3055,8 +3061,9 @@ void slab_ids(Ctx& c, const uint64_t* keys_all, int64_t n_keys_all, plmss_slab_i
 
 // Stage 4: separator records of the owned cube layers (+ the layer shared
 // with the next rank), global cell ids.
-void slab_emit(Ctx& c, plmss_slab_info* info) {
+void slab_emit(Ctx& c, uint32_t* ids, plmss_slab_info* info) {
   need_stage(c, 3, "slab_emit");
+  if (!ids) fail(PLMSS_ERR_INVALID_ARGUMENT, "slab_emit: ids output is null");
   SlabState& st = c.slab;
   FDims d = slab_dims(st);
   const uint32_t Zc = d.Z + uint32_t(st.has_up);  // vertex layers in ms
@@ -3074,6 +3081,11 @@ void slab_emit(Ctx& c, plmss_slab_info* info) {
     ba.chunk = chunk;
     ba.cls = c.get_t<uint8_t>(S_MASK, uint64_t(st.g.X - 1) * uint64_t(st.g.Y - 1) * ncl);
     ba.ms = st.ms;
+    // dense: ms holds the tokens -> ids; hash: ms holds the ids -> copied
+    ba.ids_out = ids;
+    ba.bitmap = st.dense ? st.bitmap : nullptr;
+    ba.prefix = st.dense ? st.prefix : nullptr;
+    ba.slot_id = nullptr;
     const unsigned cgrid = unsigned((TY / RY) * st.ntiles);
     CUtensorMap mtok;
     if (encode_tok_map(c, st.ms, d.X, d.Y, Zc, &mtok))
@@ -3094,7 +3106,7 @@ void slab_emit(Ctx& c, plmss_slab_info* info) {
       ea.cube0 = uint64_t(st.z0) * uint64_t(st.g.X - 1) * uint64_t(st.g.Y - 1);
       ea.off = chunk;
       ea.cls = ba.cls;
-      ea.ids = st.ms;
+      ea.ids = ids;
       ea.out = tris;
       const uint64_t nrows = uint64_t(st.g.Y - 1) * ncl;
       const unsigned egrid = unsigned(std::min<uint64_t>((nrows + 7) / 8, uint64_t(c.sm_count) * 256));

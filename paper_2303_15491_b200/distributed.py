@@ -19,12 +19,14 @@ reference's global vertex and cell order. One step:
    suffices: no iteration across ranks), desc / asc, region tokens, the
    slab's distinct (rank_min, rank_max) pairs;
    -> all_gather of the pairs;
-3. slab_ids (device): global dense MS ids in the combine_ms order
-   (segmentation.cpp:170-196) into ms;
-   -> the next rank's first layer of ids (point-to-point) into ms's extra layer;
-4. slab_emit (device): separator records of the owned cube layers with
-   global cell ids, reference order (marching.cpp:116-215); concatenated in
-   rank order they are the single-volume record list.
+3. slab_ids (device): the global region table in the combine_ms order
+   (segmentation.cpp:170-196); ms holds globally consistent region tokens
+   (dense mode) or the dense ids (hash mode);
+   -> the next rank's first layer of ms (point-to-point) into ms's extra layer;
+4. slab_emit (device): the dense ids (from the tokens, in the count pass),
+   separator records of the owned cube layers with global cell ids, reference
+   order (marching.cpp:116-215); concatenated in rank order they are the
+   single-volume record list.
 
 The step is written once, as a generator (``slab_step``) that yields its
 collectives. ``TorchComm`` runs it over torch.distributed (NCCL on B200,
@@ -114,7 +116,7 @@ def slab_step(backend, dims, rank: int, world: int, field_buf: torch.Tensor):
     tris = backend.emit()
     nts = yield ("allgather", torch.tensor([tris.shape[0]], dtype=torch.int64, device=f.device))
     nts = [int(c) for c in nts.cpu().numpy().reshape(-1)]
-    return SlabResult(z0, z1, backend.desc(), backend.asc(), ms_ext[:nz * XY], maxima, minima, region_keys, tris,
+    return SlabResult(z0, z1, backend.desc(), backend.asc(), backend.ms(), maxima, minima, region_keys, tris,
                       sum(nts[:rank]), sum(nts), s["sweeps"])
 
 
@@ -293,7 +295,13 @@ class B200SlabBackend:
         return _view(self.info.d_region_keys, self.info.n_regions, torch.int64, self.dev)
 
     def ms_ext(self):
+        """ms of the owned layers + the next rank's first layer (region
+        tokens in dense mode, ids in hash mode: exchanged as they are)."""
         return self._bufs["ms"][: self.nz * self.XY + (self.XY if self.has_up else 0)]
+
+    def ms(self):
+        """Dense MS ids of the owned vertices (after emit)."""
+        return self._bufs["ids"][: self.nz * self.XY]
 
     def desc(self):
         return self._bufs["desc"][: self.nz * self.XY]
@@ -303,7 +311,8 @@ class B200SlabBackend:
 
     def emit(self):
         a = self.api
-        a._check(a.lib().plmss_b200_slab_emit(self.ctx.h, C.byref(self.info)))
+        ids = self._buf("ids", self.nz * self.XY + (self.XY if self.has_up else 0))
+        a._check(a.lib().plmss_b200_slab_emit(self.ctx.h, a._ptr(ids), C.byref(self.info)))
         self._keep = None
         return _view(self.info.d_tris, 2 * self.info.n_tris, torch.int64, self.dev).view(-1, 2)
 

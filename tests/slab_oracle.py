@@ -132,6 +132,9 @@ class OracleSlabBackend:
     def ms_ext(self):
         return self._ms_ext
 
+    def ms(self):
+        return self._ms_ext[: self.nz * self.XY]
+
     def desc(self):
         return torch.from_numpy(self._desc.view(np.int32))
 
