@@ -3114,7 +3114,15 @@ void slab_emit(Ctx& c, uint32_t* ids, plmss_slab_info* info) {
       CK_LAUNCH("k_emit_chunks");
     }
   } else {
+    // no cube layer (a one-layer slab at the top of the volume): the ids of
+    // the owned layer straight from ms
     tris = c.get_t<plmss_tri>(S_TRIS, 1);
+    const uint64_t nv = uint64_t(Zc) * d.XY;
+    CK(cudaMemcpyAsync(ids, st.ms, nv * 4, cudaMemcpyDeviceToDevice, c.stream));
+    if (st.dense) {
+      k_ms_ids<true><<<unsigned((nv + 1023) / 1024), 256, 0, c.stream>>>(ids, nv, st.bitmap, st.prefix, nullptr);
+      CK_LAUNCH("k_ms_ids");
+    }
   }
   c.sync();
   st.n_tris = int64_t(total);
