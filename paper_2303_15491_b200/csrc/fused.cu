@@ -340,8 +340,8 @@ __global__ void __launch_bounds__(A_THREADS, 1)
                    const uint8_t* __restrict__ gcodes, FDims d,
                    uint32_t* __restrict__ maxima, uint32_t* __restrict__ minima, uint32_t* __restrict__ max_tt,
                    uint32_t* __restrict__ min_tt, uint64_t ext_cap,
-                   uint32_t* __restrict__ TT, uint64_t tt_cap, uint4* __restrict__ TB, uint16_t* __restrict__ ltd,
-                   uint16_t* __restrict__ lta, ACounters* __restrict__ ctr) {
+                   uint32_t* __restrict__ TT, uint64_t tt_cap, uint4* __restrict__ TB, uint32_t* __restrict__ lt,
+                   ACounters* __restrict__ ctr) {
   extern __shared__ __align__(16) unsigned char a_smem_raw[];
   // TMA destinations must be 128-byte aligned: round the window up (the
   // launch reserves 1024 extra bytes for this).
@@ -678,16 +678,15 @@ __global__ void __launch_bounds__(A_THREADS, 1)
   // 6. LT: the terminal index of every in-volume vertex (an extremum reads
   //    its own entry, any other vertex its terminal's)
   if (col_ok) {
-    uint16_t* od = ltd + bm0 + lx + TX * ly;
-    uint16_t* oa = lta + bm0 + lx + TX * ly;
+    uint32_t* ol = lt + bm0 + lx + TX * ly;
 #pragma unroll 4
     for (int lz = 0; lz < nz; ++lz) {
       const int h = hc + (lz + 1) * PXY;
       const uint32_t bit = 1u << lz;
       const uint32_t pd = Pd[h], pa = Pa[h];
       DCHECK(pd < PN && pa < PN, 103);
-      od[TX * TY * lz] = (mmax & bit) ? uint16_t(pd) : Pd[pd];
-      oa[TX * TY * lz] = (mmin & bit) ? uint16_t(pa) : Pa[pa];
+      // both directions' terminal indices in one word: desc | asc << 16
+      ol[TX * TY * lz] = uint32_t((mmax & bit) ? pd : Pd[pd]) | uint32_t((mmin & bit) ? pa : Pa[pa]) << 16;
     }
   }
   __syncthreads();  // shared memory is reused by the next brick
@@ -775,8 +774,7 @@ constexpr uint32_t kFinal = 0x80000000u;
 constexpr uint32_t kPortal = 0x40000000u;  // with kFinal: a z-slab portal (pbase-relative index below)
 
 __global__ void __launch_bounds__(256) k_tt_succ(const uint4* __restrict__ TB, const uint32_t* __restrict__ TT,
-                                                 const uint16_t* __restrict__ ltd,
-                                                 const uint16_t* __restrict__ lta, const uint32_t* __restrict__ RK,
+                                                 const uint32_t* __restrict__ lt, const uint32_t* __restrict__ RK,
                                                  uint32_t* __restrict__ SD, uint32_t* __restrict__ SA,
                                                  uint32_t pbase, uint64_t nt) {
   const uint4 h = TB[blockIdx.x];
@@ -792,8 +790,9 @@ __global__ void __launch_bounds__(256) k_tt_succ(const uint4* __restrict__ TB, c
       } else {
         DCHECK((bm >> 15) < gridDim.x, 201);
         const uint32_t nb = __ldg(TBw + 4 * (bm >> 15));
-        sd = nb + __ldg(ltd + bm);
-        sa = nb + __ldg(lta + bm);
+        const uint32_t l = __ldg(lt + bm);  // desc | asc << 16
+        sd = nb + (l & 0xffffu);
+        sa = nb + (l >> 16);
         DCHECK(sd < nt && sa < nt, 202);
       }
     } else {
@@ -1116,7 +1115,7 @@ struct BrickArgs {
   uint32_t brick0;  // first brick of the launch (z-slab pipelining)
   uint32_t nxc;  // 32-cube chunks per cube row
   const uint4* TB;
-  const uint16_t *ltd, *lta;
+  const uint32_t* lt;             // per vertex: desc | asc << 16 terminal indices (brick-major)
   const uint32_t *FD, *FA;        // per table entry: rank of the maximum / minimum
   const uint32_t *maxs, *mins;    // sorted extremum lists (rank -> vertex id)
   uint32_t nmax;                  // dense mode: key = rank_min * nmax + rank_max
@@ -1162,8 +1161,7 @@ __global__ void __launch_bounds__(32 * kTokRows) k_tokens(const BrickArgs a) {
   if (gx >= d.X || gy >= d.Y) return;
   const int nz = int(min(uint32_t(TZ), d.Z - gz0));
   const uint32_t base = __ldg(reinterpret_cast<const uint32_t*>(a.TB) + 4 * bt);
-  const uint16_t* pd = a.ltd + ((size_t(bt) << 15) | ly << 5 | lx);
-  const uint16_t* pa = a.lta + ((size_t(bt) << 15) | ly << 5 | lx);
+  const uint32_t* pl = a.lt + ((size_t(bt) << 15) | ly << 5 | lx);
   const uint32_t* fd = a.FD + base;
   const uint32_t* fa = a.FA + base;
   uint32_t gv = gx + d.X * (gy + d.Y * gz0);
@@ -1175,8 +1173,9 @@ __global__ void __launch_bounds__(32 * kTokRows) k_tokens(const BrickArgs a) {
 #pragma unroll
     for (int i = 0; i < kTokZ; ++i) {
       if (z0 + i < nz) {
-        ld[i] = __ldg(pd + (z0 + i) * TX * TY);
-        la[i] = __ldg(pa + (z0 + i) * TX * TY);
+        const uint32_t l = __ldg(pl + (z0 + i) * TX * TY);
+        ld[i] = l & 0xffffu;
+        la[i] = l >> 16;
       }
     }
 #pragma unroll
@@ -1233,11 +1232,10 @@ __global__ void __launch_bounds__(32 * kTokRows) k_tokens(const BrickArgs a) {
 // 2 x 16 KB) staged by two 2-D TMA tensor copies instead of per-thread loads.
 constexpr int kTokSmem = 2 * TZ * 32 * kTokRows * 2;  // both index arrays
 template <bool kDense>
-__device__ __forceinline__ void tokens_tma_body(const CUtensorMap& mld, const CUtensorMap& mla, const BrickArgs& a,
-                                                const uint32_t blk, unsigned char* smem) {
+__device__ __forceinline__ void tokens_tma_body(const CUtensorMap& mlt, const BrickArgs& a, const uint32_t blk,
+                                                unsigned char* smem) {
   using Key = typename std::conditional<kDense, uint32_t, unsigned long long>::type;
-  uint16_t(*sd)[32 * kTokRows] = reinterpret_cast<uint16_t(*)[32 * kTokRows]>(smem);  // 128-byte aligned
-  uint16_t(*sa)[32 * kTokRows] = reinterpret_cast<uint16_t(*)[32 * kTokRows]>(smem + kTokSmem / 2);
+  uint32_t(*sl)[32 * kTokRows] = reinterpret_cast<uint32_t(*)[32 * kTokRows]>(smem);  // 128-byte aligned
   __shared__ __align__(8) uint64_t s_bar;
   const FDims& d = a.d;
   const uint32_t grp = blk % (TY / kTokRows);
@@ -1255,13 +1253,8 @@ __device__ __forceinline__ void tokens_tma_body(const CUtensorMap& mld, const CU
                  : "memory");
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-            smem_u32(&sd[0][0])),
-        "l"(&mld), "r"(grp * 32 * kTokRows), "r"(bt * TZ), "r"(bar)
-        : "memory");
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-            smem_u32(&sa[0][0])),
-        "l"(&mla), "r"(grp * 32 * kTokRows), "r"(bt * TZ), "r"(bar)
+            smem_u32(&sl[0][0])),
+        "l"(&mlt), "r"(grp * 32 * kTokRows), "r"(bt * TZ), "r"(bar)
         : "memory");
   }
   const uint32_t base = __ldg(reinterpret_cast<const uint32_t*>(a.TB) + 4 * bt);
@@ -1285,9 +1278,10 @@ __device__ __forceinline__ void tokens_tma_body(const CUtensorMap& mld, const CU
 #pragma unroll
     for (int i = 0; i < kTokZ; ++i) {
       if (kF || z0 + i < nz) {
-        DCHECK(base + sd[z0 + i][l] < a.nt && base + sa[z0 + i][l] < a.nt, 404);
-        ld[i] = __ldg(fd + sd[z0 + i][l]);  // rank of the maximum | kFinal
-        la[i] = __ldg(fa + sa[z0 + i][l]);  // rank of the minimum | kFinal
+        const uint32_t lv = sl[z0 + i][l];
+        DCHECK(base + (lv & 0xffffu) < a.nt && base + (lv >> 16) < a.nt, 404);
+        ld[i] = __ldg(fd + (lv & 0xffffu));  // rank of the maximum | kFinal
+        la[i] = __ldg(fa + (lv >> 16));      // rank of the minimum | kFinal
       }
     }
 #pragma unroll
@@ -1642,11 +1636,10 @@ __global__ void __launch_bounds__(B_THREADS, 6) k_brick_tma(const __grid_constan
 }
 
 template <bool kDense>
-__global__ void __launch_bounds__(32 * kTokRows, 4) k_tokens_tma(const __grid_constant__ CUtensorMap mld,
-                                                                const __grid_constant__ CUtensorMap mla,
+__global__ void __launch_bounds__(32 * kTokRows, 4) k_tokens_tma(const __grid_constant__ CUtensorMap mlt,
                                                                 const BrickArgs a) {
   __shared__ __align__(128) unsigned char smem[kTokSmem];
-  tokens_tma_body<kDense>(mld, mla, a, blockIdx.x, smem);
+  tokens_tma_body<kDense>(mlt, a, blockIdx.x, smem);
 }
 
 // Pass C, one launch per brick z-layer s: the tokens of layer s and the
@@ -1654,15 +1647,14 @@ __global__ void __launch_bounds__(32 * kTokRows, 4) k_tokens_tma(const __grid_co
 // CTAs interleaved so that the memory-bound token work and the issue-bound
 // cube classification share every SM.
 static_assert(TY / kTokRows == TY / RY && 32 * kTokRows == B_THREADS, "token and count items must match");
-__global__ void __launch_bounds__(B_THREADS, 5) k_slab_tma(const __grid_constant__ CUtensorMap mld,
-                                                           const __grid_constant__ CUtensorMap mla,
+__global__ void __launch_bounds__(B_THREADS, 5) k_slab_tma(const __grid_constant__ CUtensorMap mlt,
                                                            const __grid_constant__ CUtensorMap mtok,
                                                            const BrickArgs ta, const BrickArgs ca) {
   __shared__ __align__(128) unsigned char smem[kTokSmem > kBrickSmem ? kTokSmem : kBrickSmem];
   if (blockIdx.x & 1)
     brick_tma_body(mtok, ca, blockIdx.x >> 1, smem);
   else
-    tokens_tma_body<true>(mld, mla, ta, blockIdx.x >> 1, smem);
+    tokens_tma_body<true>(mlt, ta, blockIdx.x >> 1, smem);
 }
 
 // Region token -> dense MS id.
@@ -1902,8 +1894,8 @@ __global__ void __launch_bounds__(256) k_ms_ids(uint32_t* __restrict__ ms, uint6
 // Resolved value of the owned first (side 0) / last (side 1) layer vertex
 // (x, y): [desc first, desc last, asc first, asc last] x XY words, each
 // kFinal | slab-local rank, or kFinal | kPortal | portal index.
-__global__ void k_slab_boundary(const FDims d, const uint4* __restrict__ TB, const uint16_t* __restrict__ ltd,
-                                const uint16_t* __restrict__ lta, const uint32_t* __restrict__ SD,
+__global__ void k_slab_boundary(const FDims d, const uint4* __restrict__ TB, const uint32_t* __restrict__ lt,
+                                const uint32_t* __restrict__ SD,
                                 const uint32_t* __restrict__ SA, uint32_t* __restrict__ out) {
   const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= 2ull * d.XY) return;
@@ -1912,8 +1904,9 @@ __global__ void k_slab_boundary(const FDims d, const uint4* __restrict__ TB, con
   const uint32_t bt = (x >> 5) + d.tx * ((y >> 5) + d.ty * (z >> 5));
   const uint32_t bm = bt << 15 | (x & 31) | (y & 31) << 5 | (z & 31) << 10;
   const uint32_t base = __ldg(reinterpret_cast<const uint32_t*>(TB) + 4 * bt);
-  out[i] = SD[base + __ldg(ltd + bm)];
-  out[2ull * d.XY + i] = SA[base + __ldg(lta + bm)];
+  const uint32_t l = __ldg(lt + bm);
+  out[i] = SD[base + (l & 0xffffu)];
+  out[2ull * d.XY + i] = SA[base + (l >> 16)];
 }
 
 // The final value of portal p of rank r: follow it through the gathered
@@ -2018,6 +2011,19 @@ EncodeFn tensor_map_encoder() {
   return encode;
 }
 
+// LT as a 2-D tensor (1024 cells of a brick layer, ntiles * 32 layers) for
+// the token pass: one box = 8 rows x 32 layers of a brick
+bool encode_lt_map(Ctx& c, uint64_t ntiles, uint32_t* lt, CUtensorMap* mlt) {
+  if (!c.use_tma || !tensor_map_encoder()) return false;
+  const cuuint64_t gdim[2] = {cuuint64_t(TX * TY), cuuint64_t(ntiles) * TZ};
+  const cuuint64_t gstride[1] = {cuuint64_t(TX * TY) * 4};
+  const cuuint32_t box[2] = {cuuint32_t(32 * kTokRows), cuuint32_t(TZ)};
+  const cuuint32_t estride[2] = {1, 1};
+  return tensor_map_encoder()(mlt, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, lt, gdim, gstride, box, estride,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 }  // namespace
 
 // Host driver of the fused pipeline. Returns false when the dims are outside
@@ -2061,7 +2067,7 @@ static void ensure_consts(Ctx& c) {
 // kernel followed by the brick compression fed by the codes.
 static void launch_pass_a(Ctx& c, const FDims& d, uint64_t ntiles, bool use_tma, const CUtensorMap& tmap,
                           const float* field, uint32_t* maxima, uint32_t* minima, uint32_t* max_tt, uint32_t* min_tt,
-                          uint64_t ext_cap, uint32_t* TT, uint64_t tt_cap, uint4* TB, uint16_t* ltd, uint16_t* lta,
+                          uint64_t ext_cap, uint32_t* TT, uint64_t tt_cap, uint4* TB, uint32_t* lt,
                           ACounters* ctr) {
   const unsigned grid = unsigned(std::min<uint64_t>(ntiles, uint64_t(c.sm_count)));
   if (c.pass_a_split) {
@@ -2090,22 +2096,22 @@ static void launch_pass_a(Ctx& c, const FDims& d, uint64_t ntiles, bool use_tma,
       k_hop_codes<false><<<hgrid, 32 * HR, kCSmem, c.stream>>>(hmap, field, d, codes, ctr);
     CK_LAUNCH("k_hop_codes");
     k_tile_segment<false, true><<<grid, A_THREADS, kASmem, c.stream>>>(
-        tmap, field, codes, d, maxima, minima, max_tt, min_tt, ext_cap, TT, tt_cap, TB, ltd, lta, ctr);
+        tmap, field, codes, d, maxima, minima, max_tt, min_tt, ext_cap, TT, tt_cap, TB, lt, ctr);
     CK_LAUNCH("k_tile_segment");
     return;
   }
   if (use_tma && c.hop_cube)
     k_tile_segment<true, false, true><<<grid, A_THREADS, kASmem, c.stream>>>(
-        tmap, field, nullptr, d, maxima, minima, max_tt, min_tt, ext_cap, TT, tt_cap, TB, ltd, lta, ctr);
+        tmap, field, nullptr, d, maxima, minima, max_tt, min_tt, ext_cap, TT, tt_cap, TB, lt, ctr);
   else if (use_tma)
     k_tile_segment<true><<<grid, A_THREADS, kASmem, c.stream>>>(tmap, field, nullptr, d, maxima, minima, max_tt,
-                                                                min_tt, ext_cap, TT, tt_cap, TB, ltd, lta, ctr);
+                                                                min_tt, ext_cap, TT, tt_cap, TB, lt, ctr);
   else if (c.hop_cube)
     k_tile_segment<false, false, true><<<grid, A_THREADS, kASmem, c.stream>>>(
-        tmap, field, nullptr, d, maxima, minima, max_tt, min_tt, ext_cap, TT, tt_cap, TB, ltd, lta, ctr);
+        tmap, field, nullptr, d, maxima, minima, max_tt, min_tt, ext_cap, TT, tt_cap, TB, lt, ctr);
   else
     k_tile_segment<false><<<grid, A_THREADS, kASmem, c.stream>>>(tmap, field, nullptr, d, maxima, minima, max_tt,
-                                                                 min_tt, ext_cap, TT, tt_cap, TB, ltd, lta, ctr);
+                                                                 min_tt, ext_cap, TT, tt_cap, TB, lt, ctr);
   CK_LAUNCH("k_tile_segment");
 }
 
@@ -2168,23 +2174,11 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
   char* ctr_base = static_cast<char*>(c.get(S_FLAGS, 1024));
   ACounters* ctr = reinterpret_cast<ACounters*>(ctr_base);
   int* flag = reinterpret_cast<int*>(ctr_base + 128);
-  uint16_t* ltd = c.get_t<uint16_t>(S_LTD, ntiles * TN);
-  uint16_t* lta = c.get_t<uint16_t>(S_LTA, ntiles * TN);
+  uint32_t* lt = c.get_t<uint32_t>(S_LTD, ntiles * TN);  // desc | asc << 16
   // LT as a 2-D tensor (1024 cells of a brick layer, ntiles * 32 layers) for
   // the token pass: one box = 8 rows x 32 layers of a brick
-  CUtensorMap mld, mla;
-  bool lt_tma = c.use_tma && tensor_map_encoder();
-  if (lt_tma) {
-    const cuuint64_t gdim[2] = {cuuint64_t(TX * TY), cuuint64_t(ntiles) * TZ};
-    const cuuint64_t gstride[1] = {cuuint64_t(TX * TY) * 2};
-    const cuuint32_t box[2] = {cuuint32_t(32 * kTokRows), cuuint32_t(TZ)};
-    const cuuint32_t estride[2] = {1, 1};
-    for (int k = 0; k < 2 && lt_tma; ++k)
-      lt_tma = tensor_map_encoder()(k ? &mla : &mld, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, k ? lta : ltd, gdim, gstride,
-                                    box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-  }
+  CUtensorMap mlt;
+  const bool lt_tma = encode_lt_map(c, ntiles, lt, &mlt);
   uint4* TB = c.get_t<uint4>(S_TB, ntiles);
   for (int attempt = 0;; ++attempt) {
     const uint64_t ext_cap = c.fused_ext_cap ? c.fused_ext_cap : uint64_t(g.n / 4 + 1024);
@@ -2197,8 +2191,8 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
     CK(cudaMemsetAsync(ctr, 0, sizeof(ACounters), c.stream));
     CK(cudaMemsetAsync(&ctr->bad, 0xff, 4, c.stream));
     c.mark(0);
-    launch_pass_a(c, d, ntiles, use_tma, tmap, field, maxima, minima, max_tt, min_tt, ext_cap, TT, tt_cap, TB, ltd,
-                  lta, ctr);
+    launch_pass_a(c, d, ntiles, use_tma, tmap, field, maxima, minima, max_tt, min_tt, ext_cap, TT, tt_cap, TB, lt,
+                  ctr);
     c.mark(1);
     ACounters h;
     CK(cudaMemcpyAsync(c.h_pinned, ctr, sizeof(ACounters), cudaMemcpyDeviceToHost, c.stream));
@@ -2247,7 +2241,7 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
     // ---- B: terminal-table forest -> extremum rank of every table entry
     uint32_t* SD = c.get_t<uint32_t>(S_SD, nt);
     uint32_t* SA = c.get_t<uint32_t>(S_SA, nt);
-    k_tt_succ<<<unsigned(ntiles), 256, 0, c.stream>>>(TB, TT, ltd, lta, RK, SD, SA, 0u, nt);
+    k_tt_succ<<<unsigned(ntiles), 256, 0, c.stream>>>(TB, TT, lt, RK, SD, SA, 0u, nt);
     CK_LAUNCH("k_tt_succ");
     // Two sweeps are enqueued without waiting (they converge on smooth
     // fields); passes C and D follow speculatively and the convergence flag
@@ -2271,8 +2265,7 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
     ba.d = d;
     ba.nxc = uint32_t((g.X - 1 + 31) / 32);
     ba.TB = TB;
-    ba.ltd = ltd;
-    ba.lta = lta;
+    ba.lt = lt;
     ba.FD = SD;
     ba.FA = SA;
     ba.maxs = maxima;
@@ -2328,7 +2321,7 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
       if (ids_in_count) {
         // all tokens first; the count pass (ids) runs once the set is complete
         if (lt_tma)
-          k_tokens_tma<true><<<tgrid, 32 * kTokRows, 0, c.stream>>>(mld, mla, ba);
+          k_tokens_tma<true><<<tgrid, 32 * kTokRows, 0, c.stream>>>(mlt, ba);
         else
           k_tokens<true><<<tgrid, 32 * kTokRows, 0, c.stream>>>(ba);
         CK_LAUNCH("k_tokens");
@@ -2342,10 +2335,10 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
           if (L >= 2) {
             BrickArgs cs = ba;
             cs.brick0 = (L - 2) * bpl;
-            k_slab_tma<<<2 * items, B_THREADS, 0, c.stream>>>(mld, mla, mtok, ts, cs);
+            k_slab_tma<<<2 * items, B_THREADS, 0, c.stream>>>(mlt, mtok, ts, cs);
             CK_LAUNCH("k_slab_tma");
           } else {
-            k_tokens_tma<true><<<items, 32 * kTokRows, 0, c.stream>>>(mld, mla, ts);
+            k_tokens_tma<true><<<items, 32 * kTokRows, 0, c.stream>>>(mlt, ts);
             CK_LAUNCH("k_tokens");
           }
         }
@@ -2361,7 +2354,7 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
           BrickArgs bs = ba;
           bs.brick0 = sl * bpl;
           if (lt_tma)
-            k_tokens_tma<true><<<bpl * (TY / kTokRows), 32 * kTokRows, 0, c.stream>>>(mld, mla, bs);
+            k_tokens_tma<true><<<bpl * (TY / kTokRows), 32 * kTokRows, 0, c.stream>>>(mlt, bs);
           else
             k_tokens<true><<<bpl * (TY / kTokRows), 32 * kTokRows, 0, c.stream>>>(bs);
           CK_LAUNCH("k_tokens");
@@ -2405,7 +2398,7 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
         ba.fset = fset;
         ba.fmask = fcap - 1;
         if (lt_tma)
-          k_tokens_tma<false><<<tgrid, 32 * kTokRows, 0, c.stream>>>(mld, mla, ba);
+          k_tokens_tma<false><<<tgrid, 32 * kTokRows, 0, c.stream>>>(mlt, ba);
         else
           k_tokens<false><<<tgrid, 32 * kTokRows, 0, c.stream>>>(ba);
         CK_LAUNCH("k_tokens");
@@ -2550,8 +2543,7 @@ void fused_segment(Ctx& c, const Grid& g, const float* field, uint32_t* desc, ui
   }
   char* ctr_base = static_cast<char*>(c.get(S_FLAGS, 1024));
   ACounters* ctr = reinterpret_cast<ACounters*>(ctr_base);
-  uint16_t* ltd = c.get_t<uint16_t>(S_LTD, ntiles * TN);
-  uint16_t* lta = c.get_t<uint16_t>(S_LTA, ntiles * TN);
+  uint32_t* lt = c.get_t<uint32_t>(S_LTD, ntiles * TN);  // desc | asc << 16
   uint4* TB = c.get_t<uint4>(S_TB, ntiles);
   uint32_t *maxima = nullptr, *minima = nullptr, *max_tt = nullptr, *min_tt = nullptr, *TT = nullptr;
   ACounters h;
@@ -2565,8 +2557,8 @@ void fused_segment(Ctx& c, const Grid& g, const float* field, uint32_t* desc, ui
     TT = c.get_t<uint32_t>(S_TMP0, tt_cap);
     CK(cudaMemsetAsync(ctr, 0, sizeof(ACounters), c.stream));
     CK(cudaMemsetAsync(&ctr->bad, 0xff, 4, c.stream));
-    launch_pass_a(c, d, ntiles, use_tma, tmap, field, maxima, minima, max_tt, min_tt, ext_cap, TT, tt_cap, TB, ltd,
-                  lta, ctr);
+    launch_pass_a(c, d, ntiles, use_tma, tmap, field, maxima, minima, max_tt, min_tt, ext_cap, TT, tt_cap, TB, lt,
+                  ctr);
     CK(cudaMemcpyAsync(c.h_pinned, ctr, sizeof(ACounters), cudaMemcpyDeviceToHost, c.stream));
     c.sync();
     memcpy(&h, c.h_pinned, sizeof h);
@@ -2606,7 +2598,7 @@ void fused_segment(Ctx& c, const Grid& g, const float* field, uint32_t* desc, ui
   }
   uint32_t* SD = c.get_t<uint32_t>(S_SD, nt);
   uint32_t* SA = c.get_t<uint32_t>(S_SA, nt);
-  k_tt_succ<<<unsigned(ntiles), 256, 0, c.stream>>>(TB, TT, ltd, lta, RK, SD, SA, 0u, nt);
+  k_tt_succ<<<unsigned(ntiles), 256, 0, c.stream>>>(TB, TT, lt, RK, SD, SA, 0u, nt);
   CK_LAUNCH("k_tt_succ");
   int* jflag = reinterpret_cast<int*>(ctr_base + 192);
   int sweeps = 0;
@@ -2624,8 +2616,7 @@ void fused_segment(Ctx& c, const Grid& g, const float* field, uint32_t* desc, ui
   ba.d = d;
   ba.nxc = uint32_t((g.X - 1 + 31) / 32);
   ba.TB = TB;
-  ba.ltd = ltd;
-  ba.lta = lta;
+  ba.lt = lt;
   ba.FD = SD;
   ba.FA = SA;
   ba.maxs = maxima;
@@ -2636,22 +2627,11 @@ void fused_segment(Ctx& c, const Grid& g, const float* field, uint32_t* desc, ui
   ba.desc = desc;
   ba.asc = asc;
   ba.ms = nullptr;  // labels only
-  CUtensorMap mld, mla;
-  bool lt_tma = c.use_tma && tensor_map_encoder();
-  if (lt_tma) {
-    const cuuint64_t gdim[2] = {cuuint64_t(TX * TY), cuuint64_t(ntiles) * TZ};
-    const cuuint64_t gstride[1] = {cuuint64_t(TX * TY) * 2};
-    const cuuint32_t box[2] = {cuuint32_t(32 * kTokRows), cuuint32_t(TZ)};
-    const cuuint32_t estride[2] = {1, 1};
-    for (int k = 0; k < 2 && lt_tma; ++k)
-      lt_tma = tensor_map_encoder()(k ? &mla : &mld, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, k ? lta : ltd, gdim, gstride,
-                                    box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-  }
+  CUtensorMap mlt;
+  const bool lt_tma = encode_lt_map(c, ntiles, lt, &mlt);
   const unsigned tgrid = unsigned((TY / kTokRows) * ntiles);
   if (lt_tma)
-    k_tokens_tma<true><<<tgrid, 32 * kTokRows, 0, c.stream>>>(mld, mla, ba);
+    k_tokens_tma<true><<<tgrid, 32 * kTokRows, 0, c.stream>>>(mlt, ba);
   else
     k_tokens<true><<<tgrid, 32 * kTokRows, 0, c.stream>>>(ba);
   CK_LAUNCH("k_tokens");
@@ -2690,19 +2670,6 @@ FDims slab_dims(const SlabState& st) {
   return d;
 }
 
-bool encode_lt_maps(Ctx& c, uint64_t ntiles, uint16_t* ltd, uint16_t* lta, CUtensorMap* mld, CUtensorMap* mla) {
-  if (!c.use_tma || !tensor_map_encoder()) return false;
-  const cuuint64_t gdim[2] = {cuuint64_t(TX * TY), cuuint64_t(ntiles) * TZ};
-  const cuuint64_t gstride[1] = {cuuint64_t(TX * TY) * 2};
-  const cuuint32_t box[2] = {cuuint32_t(32 * kTokRows), cuuint32_t(TZ)};
-  const cuuint32_t estride[2] = {1, 1};
-  for (int k = 0; k < 2; ++k)
-    if (tensor_map_encoder()(k ? mla : mld, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, k ? lta : ltd, gdim, gstride, box,
-                             estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-      return false;
-  return true;
-}
 
 bool encode_tok_map(Ctx& c, uint32_t* ms, uint32_t X, uint32_t Y, uint32_t Z, CUtensorMap* m) {
   if (!c.use_tma || !tensor_map_encoder() || (X % 4) != 0 || (reinterpret_cast<uintptr_t>(ms) & 15) != 0)
@@ -2762,8 +2729,7 @@ void slab_segment(Ctx& c, const Grid& g, int64_t z0, int64_t z1, const float* fi
   c.stats[4] = use_tma ? 1 : 0;
   char* ctr_base = static_cast<char*>(c.get(S_FLAGS, 1024));
   ACounters* ctr = reinterpret_cast<ACounters*>(ctr_base);
-  uint16_t* ltd = c.get_t<uint16_t>(S_LTD, ntiles * TN);
-  uint16_t* lta = c.get_t<uint16_t>(S_LTA, ntiles * TN);
+  uint32_t* lt = c.get_t<uint32_t>(S_LTD, ntiles * TN);  // desc | asc << 16
   uint4* TB = c.get_t<uint4>(S_TB, ntiles);
   const uint64_t nloc = uint64_t(d.n);
   uint32_t *maxima = nullptr, *minima = nullptr, *max_tt = nullptr, *min_tt = nullptr, *TT = nullptr;
@@ -2778,8 +2744,8 @@ void slab_segment(Ctx& c, const Grid& g, int64_t z0, int64_t z1, const float* fi
     TT = c.get_t<uint32_t>(S_TMP0, tt_cap);
     CK(cudaMemsetAsync(ctr, 0, sizeof(ACounters), c.stream));
     CK(cudaMemsetAsync(&ctr->bad, 0xff, 4, c.stream));
-    launch_pass_a(c, d, ntiles, use_tma, tmap, field, maxima, minima, max_tt, min_tt, ext_cap, TT, tt_cap, TB, ltd,
-                  lta, ctr);
+    launch_pass_a(c, d, ntiles, use_tma, tmap, field, maxima, minima, max_tt, min_tt, ext_cap, TT, tt_cap, TB, lt,
+                  ctr);
     CK(cudaMemcpyAsync(c.h_pinned, ctr, sizeof(ACounters), cudaMemcpyDeviceToHost, c.stream));
     c.sync();
     memcpy(&h, c.h_pinned, sizeof h);
@@ -2827,7 +2793,7 @@ void slab_segment(Ctx& c, const Grid& g, int64_t z0, int64_t z1, const float* fi
   // the forest inside the slab, to its fixpoint (portals are roots)
   uint32_t* SD = c.get_t<uint32_t>(S_SD, nt);
   uint32_t* SA = c.get_t<uint32_t>(S_SA, nt);
-  k_tt_succ<<<unsigned(ntiles), 256, 0, c.stream>>>(TB, TT, ltd, lta, RK, SD, SA, d.pbase, nt);
+  k_tt_succ<<<unsigned(ntiles), 256, 0, c.stream>>>(TB, TT, lt, RK, SD, SA, d.pbase, nt);
   CK_LAUNCH("k_tt_succ");
   int* jflag = reinterpret_cast<int*>(ctr_base + 192);
   for (;;) {
@@ -2841,7 +2807,7 @@ void slab_segment(Ctx& c, const Grid& g, int64_t z0, int64_t z1, const float* fi
     if (st.sweeps > 64) fail(PLMSS_ERR_LOGIC, "z-slab terminal forest did not converge");
   }
   uint32_t* bnd = c.get_t<uint32_t>(S_SLAB_BND, 4 * uint64_t(d.XY));
-  k_slab_boundary<<<blocks_for(2 * int64_t(d.XY), 256), 256, 0, c.stream>>>(d, TB, ltd, lta, SD, SA, bnd);
+  k_slab_boundary<<<blocks_for(2 * int64_t(d.XY), 256), 256, 0, c.stream>>>(d, TB, lt, SD, SA, bnd);
   CK_LAUNCH("k_slab_boundary");
   c.sync();
   check_device(c, "slab_segment");
@@ -2902,8 +2868,7 @@ void slab_resolve(Ctx& c, const uint32_t* G, int world, int rank, const int64_t*
   ba.d = d;
   ba.nxc = uint32_t((st.g.X - 1 + 31) / 32);
   ba.TB = static_cast<const uint4*>(c.buf[S_TB]);
-  ba.ltd = static_cast<const uint16_t*>(c.buf[S_LTD]);
-  ba.lta = static_cast<const uint16_t*>(c.buf[S_LTA]);
+  ba.lt = static_cast<const uint32_t*>(c.buf[S_LTD]);
   ba.FD = SD;
   ba.FA = SA;
   ba.maxs = maxs_g;
@@ -2915,9 +2880,8 @@ void slab_resolve(Ctx& c, const uint32_t* G, int world, int rank, const int64_t*
   ba.asc = asc;
   ba.ms = ms;
   ba.overflow = flag;
-  CUtensorMap mld, mla;
-  const bool lt_tma = encode_lt_maps(c, st.ntiles, static_cast<uint16_t*>(c.buf[S_LTD]),
-                                     static_cast<uint16_t*>(c.buf[S_LTA]), &mld, &mla);
+  CUtensorMap mlt;
+  const bool lt_tma = encode_lt_map(c, st.ntiles, static_cast<uint32_t*>(c.buf[S_LTD]), &mlt);
   const unsigned tgrid = unsigned((TY / kTokRows) * st.ntiles);
   const uint64_t nbits = uint64_t(smax) * uint64_t(smin);
   st.dense = nbits < (uint64_t(1) << 32) && c.combine_path != 2;
@@ -2928,7 +2892,7 @@ void slab_resolve(Ctx& c, const uint32_t* G, int world, int rank, const int64_t*
     ba.bitmap = bitmap;
     ba.nw = nw;
     if (lt_tma)
-      k_tokens_tma<true><<<tgrid, 32 * kTokRows, 0, c.stream>>>(mld, mla, ba);
+      k_tokens_tma<true><<<tgrid, 32 * kTokRows, 0, c.stream>>>(mlt, ba);
     else
       k_tokens<true><<<tgrid, 32 * kTokRows, 0, c.stream>>>(ba);
     CK_LAUNCH("k_tokens");
@@ -2958,7 +2922,7 @@ void slab_resolve(Ctx& c, const uint32_t* G, int world, int rank, const int64_t*
       ba.fset = fset;
       ba.fmask = fcap - 1;
       if (lt_tma)
-        k_tokens_tma<false><<<tgrid, 32 * kTokRows, 0, c.stream>>>(mld, mla, ba);
+        k_tokens_tma<false><<<tgrid, 32 * kTokRows, 0, c.stream>>>(mlt, ba);
       else
         k_tokens<false><<<tgrid, 32 * kTokRows, 0, c.stream>>>(ba);
       CK_LAUNCH("k_tokens");
