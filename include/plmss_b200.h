@@ -311,6 +311,24 @@ int plmss_b200_copy(plmss_ctx* ctx, void* dst, const void* d_src, int64_t bytes,
  *                           writes the dense ids (no in-place id pass over
  *                           ms), 0: tokens in ms, counts interleaved with the
  *                           token pass, then the id pass (both exact). */
+/* pipeline_host over a sequence of volumes of the same dims, double-buffered:
+ * two internal contexts (own non-blocking streams, created on first use,
+ * options copied from ctx) take alternate volumes on two host threads, so
+ * volume i+1's upload and compute overlap volume i's download (host <-> device
+ * copies run in both directions at once). Each volume's outputs and counts
+ * as in pipeline_host; result device pointers are not valid after return.
+ * Returns the first failing volume's status (each one's in ->status). */
+typedef struct plmss_host_volume {
+  const float* h_field;
+  uint32_t *h_desc, *h_asc, *h_ms, *h_maxima, *h_minima;
+  uint64_t* h_region_keys;
+  plmss_tri* h_tris;
+  int64_t tri_capacity;
+  plmss_result result;
+  int32_t status;
+} plmss_host_volume;
+int plmss_b200_pipeline_host_batch(plmss_ctx* ctx, const int64_t dims[3], plmss_host_volume* volumes, int64_t n);
+
 /* ---- callers either side of the path ------------------
  * weld_points (marching.hpp:138-140, marching.cpp:400-417): merges
  * bitwise-identical points of a separator soup in place, the first occurrence

@@ -52,6 +52,7 @@ HEADER_FUNCTIONS = [
     "plmss_b200_write_labels", "plmss_b200_write_surface_obj", "plmss_b200_synth_layers",
     "plmss_b200_slab_segment", "plmss_b200_slab_resolve", "plmss_b200_slab_ids", "plmss_b200_slab_emit",
     "plmss_b200_materialize_separators_chunked", "plmss_b200_write_separators_obj", "plmss_b200_ctx_release",
+    "plmss_b200_pipeline_host_batch",
 ]
 
 GEOMETRY_SINK = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int64, C.c_int64, C.POINTER(C.c_double),
@@ -64,6 +65,15 @@ class PlmssResult(C.Structure):
         ("d_minima", C.c_void_p), ("d_region_keys", C.c_void_p), ("d_tris", C.c_void_p),
         ("n_vertices", C.c_int64), ("n_maxima", C.c_int64), ("n_minima", C.c_int64),
         ("n_regions", C.c_int64), ("n_tris", C.c_int64), ("sweeps", C.c_int32),
+    ]
+
+
+class PlmssHostVolume(C.Structure):
+    """plmss_host_volume (include/plmss_b200.h): one volume of a host batch."""
+    _fields_ = [
+        ("h_field", C.c_void_p), ("h_desc", C.c_void_p), ("h_asc", C.c_void_p), ("h_ms", C.c_void_p),
+        ("h_maxima", C.c_void_p), ("h_minima", C.c_void_p), ("h_region_keys", C.c_void_p), ("h_tris", C.c_void_p),
+        ("tri_capacity", C.c_int64), ("result", PlmssResult), ("status", C.c_int32),
     ]
 
 
@@ -115,6 +125,7 @@ def lib() -> C.CDLL:
         L.plmss_b200_result.argtypes = [vp, C.POINTER(PlmssResult)]
         L.plmss_b200_copy.argtypes = [vp, vp, vp, i64, i32]
         L.plmss_b200_pipeline_host.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i64, C.POINTER(PlmssResult)]
+        L.plmss_b200_pipeline_host_batch.argtypes = [vp, vp, C.POINTER(PlmssHostVolume), i64]
         L.plmss_b200_synth.argtypes = [vp, vp, i32, vp, i32, C.c_double, C.c_uint64, i32, vp]
         L.plmss_b200_synth_layers.argtypes = [vp, vp, i32, vp, i32, C.c_double, C.c_uint64, i64, i64, vp]
         L.plmss_b200_weld_points.argtypes = [vp, vp, i64, vp, i64, C.POINTER(i64)]
@@ -632,6 +643,31 @@ def pipeline_host(dims, h_field: np.ndarray, ctx: Optional[Context] = None, want
         if name in out:
             out[name] = out[name][:cnt]
     return res, out
+
+
+def pipeline_host_batch(dims, volumes, ctx: Optional[Context] = None):
+    """plmss_b200_pipeline_host_batch: a sequence of host volumes, each a dict
+    with "field" (float32 numpy, ideally pinned) and optional numpy output
+    buffers "desc", "asc", "ms" (uint32 N), "maxima", "minima" (uint32),
+    "region_keys" (uint64), "tris" (uint64 (T, 2)); double-buffered so one
+    volume's download overlaps the next one's upload and compute. Returns the
+    PipelineResult counts per volume."""
+    ctx = ctx or default_context()
+    d = _dims(dims)
+    arr = (PlmssHostVolume * len(volumes))()
+    keep = []
+    for v, vol in zip(arr, volumes):
+        f = np.ascontiguousarray(vol["field"], dtype=np.float32).reshape(-1)
+        keep.append(f)
+        v.h_field = f.ctypes.data
+        for k in ("desc", "asc", "ms", "maxima", "minima", "region_keys", "tris"):
+            b = vol.get(k)
+            setattr(v, "h_" + k, b.ctypes.data if b is not None else None)
+        t = vol.get("tris")
+        v.tri_capacity = 0 if t is None else t.shape[0]
+    _check(lib().plmss_b200_pipeline_host_batch(ctx.h, d.ctypes.data, arr, len(volumes)))
+    return [PipelineResult(v.result.n_vertices, v.result.n_maxima, v.result.n_minima, v.result.n_regions,
+                           v.result.n_tris, v.result.sweeps, None) for v in arr]
 
 
 def synth_field(dims, kind: str = "gaussians", gaussians=None, noise_amp: float = 0.0, seed: int = 0,

@@ -3,6 +3,8 @@
 #include <string.h>
 
 #include <string>
+#include <thread>
+#include <mutex>
 
 #include "common.cuh"
 #include "tet_tables.h"
@@ -13,6 +15,9 @@ unsigned long long plmss_b200::g_launches = 0;
 
 struct plmss_ctx {
   Ctx c;
+  // pipeline_host_batch: two internal contexts (own non-blocking streams)
+  // that take alternate volumes on two host threads
+  plmss_ctx* peer[2] = {nullptr, nullptr};
 };
 
 namespace {
@@ -132,6 +137,12 @@ int plmss_b200_ctx_create(int device, void* stream, plmss_ctx** out) {
 }
 
 void plmss_b200_ctx_destroy(plmss_ctx* p) {
+  if (p)
+    for (auto& q : p->peer)
+      if (q) {
+        plmss_b200_ctx_destroy(q);
+        q = nullptr;
+      }
   if (!p) return;
   Ctx& c = p->c;
   cudaSetDevice(c.device);
@@ -162,6 +173,12 @@ size_t plmss_b200_ctx_scratch_bytes(const plmss_ctx* p) {
 
 int plmss_b200_ctx_release(plmss_ctx* p) {
   return guarded([&] {
+    if (p)
+      for (auto* q : p->peer)
+        if (q) {
+          const int s2 = plmss_b200_ctx_release(q);
+          if (s2) fail(s2, plmss_b200_last_error());
+        }
     Ctx& c = C(p);
     set_device(c);
     c.sync();
@@ -565,6 +582,51 @@ int plmss_b200_pipeline_host(plmss_ctx* p, const int64_t dims[3], const float* h
     if (h_tris && r.n_tris > tri_capacity)
       fail(PLMSS_ERR_LOGIC, "separator records exceed the host capacity (" + std::to_string(r.n_tris) + ")");
   });
+}
+
+int plmss_b200_pipeline_host_batch(plmss_ctx* p, const int64_t dims[3], plmss_host_volume* vols, int64_t n) {
+  int st = guarded([&] {
+    if (!p) fail(PLMSS_ERR_INVALID_ARGUMENT, "null context");
+    if (n < 0 || (n > 0 && !vols)) fail(PLMSS_ERR_INVALID_ARGUMENT, "bad volume list");
+    for (auto& q : p->peer)
+      if (!q) {
+        const int s2 = plmss_b200_ctx_create(p->c.device, nullptr, &q);
+        if (s2) fail(s2, "peer context: " + std::string(plmss_b200_last_error()));
+      }
+    for (auto* q : p->peer) {  // the caller's options
+      q->c.combine_path = p->c.combine_path;
+      q->c.pipeline_path = p->c.pipeline_path;
+      q->c.use_tma = p->c.use_tma;
+      q->c.spec_sweeps = p->c.spec_sweeps;
+      q->c.pass_a_split = p->c.pass_a_split;
+      q->c.hop_cube = p->c.hop_cube;
+      q->c.ids_in_count = p->c.ids_in_count;
+    }
+  });
+  if (st) return st;
+  int first_err = 0;
+  std::string first_msg;
+  std::mutex mu;
+  auto worker = [&](int k) {
+    for (int64_t i = k; i < n; i += 2) {
+      plmss_host_volume& v = vols[i];
+      v.status = plmss_b200_pipeline_host(p->peer[k], dims, v.h_field, v.h_desc, v.h_asc, v.h_ms, v.h_maxima,
+                                          v.h_minima, v.h_region_keys, v.h_tris, v.tri_capacity, &v.result);
+      if (v.status) {
+        std::lock_guard<std::mutex> lock(mu);
+        if (!first_err) {
+          first_err = v.status;
+          first_msg = plmss_b200_last_error();
+        }
+        return;
+      }
+    }
+  };
+  std::thread t1(worker, 1);
+  worker(0);
+  t1.join();
+  if (first_err) g_err = first_msg;
+  return first_err;
 }
 
 int plmss_b200_synth(plmss_ctx* p, const int64_t dims[3], int kind, const double* h_gaussians, int n_gauss,

@@ -375,3 +375,25 @@ def test_library_is_ordered_after_torch_default_stream(plmss, gpu):
     r = api.emit_separators(dims, torch.sort(base)[0] // 4096, ctx=gpu)
     assert r.shape[0] == want
 
+
+
+def test_pipeline_host_batch_matches_single_calls(plmss, gpu):
+    """plmss_b200_pipeline_host_batch (two internal contexts, alternate
+    volumes) returns every volume's outputs exactly as pipeline_host."""
+    from paper_2303_15491_b200.configs import CONFIGS, host_field, scaled
+
+    vols, refs = [], []
+    for i, dims in enumerate([(40, 36, 33), (40, 36, 33), (40, 36, 33), (40, 36, 33), (40, 36, 33)]):
+        f = host_field(scaled(CONFIGS["cfg2" if i % 2 else "cfg1"], dims))
+        res, out = plmss.pipeline_host(dims, f, ctx=gpu,
+                                       out_buffers={"tris": np.empty((400000, 2), np.uint64)})
+        refs.append((res, out))
+        v = {"field": f, "desc": np.empty(f.size, np.uint32), "asc": np.empty(f.size, np.uint32),
+             "ms": np.empty(f.size, np.uint32), "tris": np.empty((res.n_tris, 2), np.uint64)}
+        vols.append(v)
+    rb = plmss.pipeline_host_batch((40, 36, 33), vols, ctx=gpu)
+    for (res, out), v, r in zip(refs, vols, rb):
+        assert (r.n_tris, r.n_regions, r.n_maxima) == (res.n_tris, res.n_regions, res.n_maxima)
+        for k in ("desc", "asc", "ms"):
+            assert np.array_equal(v[k], out[k]), k
+        assert np.array_equal(v["tris"], out["tris"][: res.n_tris])
