@@ -386,7 +386,7 @@ def test_pipeline_host_batch_matches_single_calls(plmss, gpu):
     for i, dims in enumerate([(40, 36, 33), (40, 36, 33), (40, 36, 33), (40, 36, 33), (40, 36, 33)]):
         f = host_field(scaled(CONFIGS["cfg2" if i % 2 else "cfg1"], dims))
         res, out = plmss.pipeline_host(dims, f, ctx=gpu,
-                                       out_buffers={"tris": np.empty((400000, 2), np.uint64)})
+                                       out_buffers={"tris": np.empty((4000000, 2), np.uint64)})
         refs.append((res, out))
         v = {"field": f, "desc": np.empty(f.size, np.uint32), "asc": np.empty(f.size, np.uint32),
              "ms": np.empty(f.size, np.uint32), "tris": np.empty((res.n_tris, 2), np.uint64)}
