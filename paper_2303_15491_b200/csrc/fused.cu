@@ -780,32 +780,49 @@ __global__ void __launch_bounds__(256) k_tt_succ(const uint4* __restrict__ TB, c
   const uint4 h = TB[blockIdx.x];
   const uint32_t n = h.y + h.z + h.w;
   const uint32_t* TBw = reinterpret_cast<const uint32_t*>(TB);
-  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-    const uint32_t k = h.x + i;
-    uint32_t sd, sa;
-    if (i < h.y) {
-      const uint32_t bm = __ldg(TT + k);
-      if (pbase && bm >= pbase) {
-        sd = sa = kFinal | kPortal | (bm - pbase);  // resolved across ranks (slab_resolve)
-      } else {
-        DCHECK((bm >> 15) < gridDim.x, 201);
-        const uint32_t nb = __ldg(TBw + 4 * (bm >> 15));
-        const uint32_t l = __ldg(lt + bm);  // desc | asc << 16
-        sd = nb + (l & 0xffffu);
-        sa = nb + (l >> 16);
-        DCHECK(sd < nt && sa < nt, 202);
-      }
-    } else {
-      // a maximum is only reached by descending-manifold chains, a minimum
-      // only by ascending ones
-      const uint32_t r = __ldg(RK + k) | kFinal;
-      const bool is_max = i < h.y + h.z;
-      sd = is_max ? r : kFinal;
-      sa = is_max ? kFinal : r;
+  // four entries per thread and step: all their table / LT gathers in flight
+  constexpr int kU = 4;
+  for (uint32_t i0 = threadIdx.x; i0 < n; i0 += kU * blockDim.x) {
+    uint32_t bm[kU], nb[kU], l[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const uint32_t i = i0 + u * blockDim.x;
+      bm[u] = i < h.y ? __ldg(TT + h.x + i) : 0u;
     }
-    DCHECK(k < nt, 203);
-    SD[k] = sd;
-    SA[k] = sa;
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const uint32_t i = i0 + u * blockDim.x;
+      const bool gather = i < h.y && !(pbase && bm[u] >= pbase);
+      DCHECK(!gather || (bm[u] >> 15) < gridDim.x, 201);
+      nb[u] = gather ? __ldg(TBw + 4 * (bm[u] >> 15)) : 0u;
+      l[u] = gather ? __ldg(lt + bm[u]) : 0u;  // desc | asc << 16
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const uint32_t i = i0 + u * blockDim.x;
+      if (i >= n) break;
+      const uint32_t k = h.x + i;
+      uint32_t sd, sa;
+      if (i < h.y) {
+        if (pbase && bm[u] >= pbase) {
+          sd = sa = kFinal | kPortal | (bm[u] - pbase);  // resolved across ranks (slab_resolve)
+        } else {
+          sd = nb[u] + (l[u] & 0xffffu);
+          sa = nb[u] + (l[u] >> 16);
+          DCHECK(sd < nt && sa < nt, 202);
+        }
+      } else {
+        // a maximum is only reached by descending-manifold chains, a minimum
+        // only by ascending ones
+        const uint32_t r = __ldg(RK + k) | kFinal;
+        const bool is_max = i < h.y + h.z;
+        sd = is_max ? r : kFinal;
+        sa = is_max ? kFinal : r;
+      }
+      DCHECK(k < nt, 203);
+      SD[k] = sd;
+      SA[k] = sa;
+    }
   }
 }
 
@@ -816,34 +833,46 @@ __global__ void __launch_bounds__(256) k_tt_succ(const uint4* __restrict__ TB, c
 // entry's chain, so concurrent updates are safe.
 constexpr int kChase = 64;
 
+constexpr int kJumpE = 4;  // table entries per thread: 2 * kJumpE chains in flight
 __global__ void __launch_bounds__(256) k_tt_jump(uint64_t nt, uint32_t* __restrict__ SD, uint32_t* __restrict__ SA,
                                                  int* __restrict__ changed) {
-  // two entries per thread (i, i + half): four independent chains in flight
-  const uint64_t half = (nt + 1) / 2;
+  // entries i + e * q (q = ceil(nt / kJumpE)), both directions each
+  const uint64_t q = (nt + kJumpE - 1) / kJumpE;
   const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   bool ch = false;
-  if (i < half) {
-    const uint64_t j = i + half;
-    const bool two = j < nt;
-    const uint32_t d0 = SD[i], a0 = SA[i];
-    const uint32_t e0 = two ? SD[j] : kFinal, b0 = two ? SA[j] : kFinal;
-    uint32_t xd = d0, xa = a0, yd = e0, ya = b0;
-#pragma unroll 4
-    for (int k = 0; k < kChase && !(xd & xa & yd & ya & kFinal); ++k) {
-      DCHECK(((xd & kFinal) || xd < nt) && ((xa & kFinal) || xa < nt) && ((yd & kFinal) || yd < nt) &&
-                 ((ya & kFinal) || ya < nt), 301);
-      if (!(xd & kFinal)) xd = SD[xd];
-      if (!(xa & kFinal)) xa = SA[xa];
-      if (!(yd & kFinal)) yd = SD[yd];
-      if (!(ya & kFinal)) ya = SA[ya];
+  if (i < q) {
+    uint32_t x0[2 * kJumpE], x[2 * kJumpE];
+#pragma unroll
+    for (int e = 0; e < kJumpE; ++e) {
+      const uint64_t j = i + e * q;
+      x0[2 * e] = j < nt ? SD[j] : kFinal;
+      x0[2 * e + 1] = j < nt ? SA[j] : kFinal;
     }
-    if (xd != d0) SD[i] = xd;
-    if (xa != a0) SA[i] = xa;
-    if (two) {
-      if (yd != e0) SD[j] = yd;
-      if (ya != b0) SA[j] = ya;
+    uint32_t all = kFinal;
+#pragma unroll
+    for (int c = 0; c < 2 * kJumpE; ++c) {
+      x[c] = x0[c];
+      all &= x[c];
     }
-    ch = !(xd & xa & yd & ya & kFinal);
+#pragma unroll 2
+    for (int k = 0; k < kChase && !(all & kFinal); ++k) {
+      all = kFinal;
+#pragma unroll
+      for (int c = 0; c < 2 * kJumpE; ++c) {
+        DCHECK((x[c] & kFinal) || x[c] < nt, 301);
+        if (!(x[c] & kFinal)) x[c] = (c & 1) ? SA[x[c]] : SD[x[c]];
+        all &= x[c];
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < kJumpE; ++e) {
+      const uint64_t j = i + e * q;
+      if (j < nt) {
+        if (x[2 * e] != x0[2 * e]) SD[j] = x[2 * e];
+        if (x[2 * e + 1] != x0[2 * e + 1]) SA[j] = x[2 * e + 1];
+      }
+    }
+    ch = !(all & kFinal);
   }
   if (__any_sync(0xffffffffu, ch) && (threadIdx.x & 31) == 0) *changed = 1;
 }
@@ -2251,7 +2280,7 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
     o.sweeps = 0;
     auto sweep = [&]() {
       CK(cudaMemsetAsync(jflag, 0, 4, c.stream));
-      k_tt_jump<<<blocks_for(int64_t((nt + 1) / 2), 256), 256, 0, c.stream>>>(nt, SD, SA, jflag);
+      k_tt_jump<<<blocks_for(int64_t((nt + kJumpE - 1) / kJumpE), 256), 256, 0, c.stream>>>(nt, SD, SA, jflag);
       CK_LAUNCH("k_tt_jump");
       ++o.sweeps;
     };
@@ -2604,7 +2633,7 @@ void fused_segment(Ctx& c, const Grid& g, const float* field, uint32_t* desc, ui
   int sweeps = 0;
   for (;;) {
     CK(cudaMemsetAsync(jflag, 0, 4, c.stream));
-    k_tt_jump<<<blocks_for(int64_t((nt + 1) / 2), 256), 256, 0, c.stream>>>(nt, SD, SA, jflag);
+    k_tt_jump<<<blocks_for(int64_t((nt + kJumpE - 1) / kJumpE), 256), 256, 0, c.stream>>>(nt, SD, SA, jflag);
     CK_LAUNCH("k_tt_jump");
     ++sweeps;
     CK(cudaMemcpyAsync(reinterpret_cast<char*>(c.h_pinned) + 64, jflag, 4, cudaMemcpyDeviceToHost, c.stream));
@@ -2798,7 +2827,7 @@ void slab_segment(Ctx& c, const Grid& g, int64_t z0, int64_t z1, const float* fi
   int* jflag = reinterpret_cast<int*>(ctr_base + 192);
   for (;;) {
     CK(cudaMemsetAsync(jflag, 0, 4, c.stream));
-    k_tt_jump<<<blocks_for(int64_t((nt + 1) / 2), 256), 256, 0, c.stream>>>(nt, SD, SA, jflag);
+    k_tt_jump<<<blocks_for(int64_t((nt + kJumpE - 1) / kJumpE), 256), 256, 0, c.stream>>>(nt, SD, SA, jflag);
     CK_LAUNCH("k_tt_jump");
     ++st.sweeps;
     CK(cudaMemcpyAsync(reinterpret_cast<char*>(c.h_pinned) + 64, jflag, 4, cudaMemcpyDeviceToHost, c.stream));
