@@ -780,49 +780,32 @@ __global__ void __launch_bounds__(256) k_tt_succ(const uint4* __restrict__ TB, c
   const uint4 h = TB[blockIdx.x];
   const uint32_t n = h.y + h.z + h.w;
   const uint32_t* TBw = reinterpret_cast<const uint32_t*>(TB);
-  // four entries per thread and step: all their table / LT gathers in flight
-  constexpr int kU = 4;
-  for (uint32_t i0 = threadIdx.x; i0 < n; i0 += kU * blockDim.x) {
-    uint32_t bm[kU], nb[kU], l[kU];
-#pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      const uint32_t i = i0 + u * blockDim.x;
-      bm[u] = i < h.y ? __ldg(TT + h.x + i) : 0u;
-    }
-#pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      const uint32_t i = i0 + u * blockDim.x;
-      const bool gather = i < h.y && !(pbase && bm[u] >= pbase);
-      DCHECK(!gather || (bm[u] >> 15) < gridDim.x, 201);
-      nb[u] = gather ? __ldg(TBw + 4 * (bm[u] >> 15)) : 0u;
-      l[u] = gather ? __ldg(lt + bm[u]) : 0u;  // desc | asc << 16
-    }
-#pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      const uint32_t i = i0 + u * blockDim.x;
-      if (i >= n) break;
-      const uint32_t k = h.x + i;
-      uint32_t sd, sa;
-      if (i < h.y) {
-        if (pbase && bm[u] >= pbase) {
-          sd = sa = kFinal | kPortal | (bm[u] - pbase);  // resolved across ranks (slab_resolve)
-        } else {
-          sd = nb[u] + (l[u] & 0xffffu);
-          sa = nb[u] + (l[u] >> 16);
-          DCHECK(sd < nt && sa < nt, 202);
-        }
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const uint32_t k = h.x + i;
+    uint32_t sd, sa;
+    if (i < h.y) {
+      const uint32_t bm = __ldg(TT + k);
+      if (pbase && bm >= pbase) {
+        sd = sa = kFinal | kPortal | (bm - pbase);  // resolved across ranks (slab_resolve)
       } else {
-        // a maximum is only reached by descending-manifold chains, a minimum
-        // only by ascending ones
-        const uint32_t r = __ldg(RK + k) | kFinal;
-        const bool is_max = i < h.y + h.z;
-        sd = is_max ? r : kFinal;
-        sa = is_max ? kFinal : r;
+        DCHECK((bm >> 15) < gridDim.x, 201);
+        const uint32_t nb = __ldg(TBw + 4 * (bm >> 15));
+        const uint32_t l = __ldg(lt + bm);  // desc | asc << 16
+        sd = nb + (l & 0xffffu);
+        sa = nb + (l >> 16);
+        DCHECK(sd < nt && sa < nt, 202);
       }
-      DCHECK(k < nt, 203);
-      SD[k] = sd;
-      SA[k] = sa;
+    } else {
+      // a maximum is only reached by descending-manifold chains, a minimum
+      // only by ascending ones
+      const uint32_t r = __ldg(RK + k) | kFinal;
+      const bool is_max = i < h.y + h.z;
+      sd = is_max ? r : kFinal;
+      sa = is_max ? kFinal : r;
     }
+    DCHECK(k < nt, 203);
+    SD[k] = sd;
+    SA[k] = sa;
   }
 }
 
@@ -833,46 +816,34 @@ __global__ void __launch_bounds__(256) k_tt_succ(const uint4* __restrict__ TB, c
 // entry's chain, so concurrent updates are safe.
 constexpr int kChase = 64;
 
-constexpr int kJumpE = 4;  // table entries per thread: 2 * kJumpE chains in flight
 __global__ void __launch_bounds__(256) k_tt_jump(uint64_t nt, uint32_t* __restrict__ SD, uint32_t* __restrict__ SA,
                                                  int* __restrict__ changed) {
-  // entries i + e * q (q = ceil(nt / kJumpE)), both directions each
-  const uint64_t q = (nt + kJumpE - 1) / kJumpE;
+  // two entries per thread (i, i + half): four independent chains in flight
+  const uint64_t half = (nt + 1) / 2;
   const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   bool ch = false;
-  if (i < q) {
-    uint32_t x0[2 * kJumpE], x[2 * kJumpE];
-#pragma unroll
-    for (int e = 0; e < kJumpE; ++e) {
-      const uint64_t j = i + e * q;
-      x0[2 * e] = j < nt ? SD[j] : kFinal;
-      x0[2 * e + 1] = j < nt ? SA[j] : kFinal;
+  if (i < half) {
+    const uint64_t j = i + half;
+    const bool two = j < nt;
+    const uint32_t d0 = SD[i], a0 = SA[i];
+    const uint32_t e0 = two ? SD[j] : kFinal, b0 = two ? SA[j] : kFinal;
+    uint32_t xd = d0, xa = a0, yd = e0, ya = b0;
+#pragma unroll 4
+    for (int k = 0; k < kChase && !(xd & xa & yd & ya & kFinal); ++k) {
+      DCHECK(((xd & kFinal) || xd < nt) && ((xa & kFinal) || xa < nt) && ((yd & kFinal) || yd < nt) &&
+                 ((ya & kFinal) || ya < nt), 301);
+      if (!(xd & kFinal)) xd = SD[xd];
+      if (!(xa & kFinal)) xa = SA[xa];
+      if (!(yd & kFinal)) yd = SD[yd];
+      if (!(ya & kFinal)) ya = SA[ya];
     }
-    uint32_t all = kFinal;
-#pragma unroll
-    for (int c = 0; c < 2 * kJumpE; ++c) {
-      x[c] = x0[c];
-      all &= x[c];
+    if (xd != d0) SD[i] = xd;
+    if (xa != a0) SA[i] = xa;
+    if (two) {
+      if (yd != e0) SD[j] = yd;
+      if (ya != b0) SA[j] = ya;
     }
-#pragma unroll 2
-    for (int k = 0; k < kChase && !(all & kFinal); ++k) {
-      all = kFinal;
-#pragma unroll
-      for (int c = 0; c < 2 * kJumpE; ++c) {
-        DCHECK((x[c] & kFinal) || x[c] < nt, 301);
-        if (!(x[c] & kFinal)) x[c] = (c & 1) ? SA[x[c]] : SD[x[c]];
-        all &= x[c];
-      }
-    }
-#pragma unroll
-    for (int e = 0; e < kJumpE; ++e) {
-      const uint64_t j = i + e * q;
-      if (j < nt) {
-        if (x[2 * e] != x0[2 * e]) SD[j] = x[2 * e];
-        if (x[2 * e + 1] != x0[2 * e + 1]) SA[j] = x[2 * e + 1];
-      }
-    }
-    ch = !(all & kFinal);
+    ch = !(xd & xa & yd & ya & kFinal);
   }
   if (__any_sync(0xffffffffu, ch) && (threadIdx.x & 31) == 0) *changed = 1;
 }
@@ -1162,7 +1133,25 @@ struct BrickArgs {
   // bitmap word prefix, hash: slot -> id), so no id pass over ms is needed
   uint32_t* ids_out;
   const uint32_t *prefix, *slot_id;
+  // ... and the labels (desc / asc vertex ids) from the tokens when the token
+  // pass skipped them (desc == nullptr there)
+  uint32_t *desc_out, *asc_out;
 };
+
+// region token -> (vertex id of the maximum, of the minimum): dense key
+// rank_min * nmax + rank_max, or the hash set's (rank_min << 32 | rank_max)
+__device__ __forceinline__ uint2 brick_token_labels(const BrickArgs& a, uint32_t k) {
+  uint32_t ra, rd;
+  if (a.prefix) {
+    ra = k / a.nmax;
+    rd = k - ra * a.nmax;
+  } else {
+    const unsigned long long key = __ldg(a.fset + k);
+    ra = uint32_t(key >> 32);
+    rd = uint32_t(key);
+  }
+  return make_uint2(__ldg(a.maxs + rd), __ldg(a.mins + ra));
+}
 
 // region token -> dense MS id, the count pass's copy of token_id
 __device__ __forceinline__ uint32_t brick_token_id(const BrickArgs& a, uint32_t k) {
@@ -1222,7 +1211,7 @@ __global__ void __launch_bounds__(32 * kTokRows) k_tokens(const BrickArgs a) {
       // index, not a rank: no set insert and no extremum gather for it (the
       // pass is redone after the forest converges).
       if (!(ld[i] & la[i] & kFinal)) {
-        a.desc[gv] = a.asc[gv] = 0u;
+        if (a.desc) a.desc[gv] = a.asc[gv] = 0u;
         if (a.ms) a.ms[gv] = 0u;
         lkey = Key(~Key(0));
         gv += d.XY;
@@ -1246,11 +1235,13 @@ __global__ void __launch_bounds__(32 * kTokRows) k_tokens(const BrickArgs a) {
           if (slot == ~uint64_t(0)) *a.overflow = 1;
           ltok = uint32_t(slot);
         }
-        lgv = make_uint2(__ldg(a.maxs + ld[i]), __ldg(a.mins + la[i]));
+        if (a.desc) lgv = make_uint2(__ldg(a.maxs + ld[i]), __ldg(a.mins + la[i]));
         lkey = key;
       }
-      a.desc[gv] = lgv.x;
-      a.asc[gv] = lgv.y;
+      if (a.desc) {
+        a.desc[gv] = lgv.x;
+        a.asc[gv] = lgv.y;
+      }
       if (a.ms) a.ms[gv] = ltok;
       gv += d.XY;
     }
@@ -1320,7 +1311,7 @@ __device__ __forceinline__ void tokens_tma_body(const CUtensorMap& mlt, const Br
       // index, not a rank: no set insert and no extremum gather for it (the
       // pass is redone after the forest converges).
       if (!(ld[i] & la[i] & kFinal)) {
-        a.desc[gv] = a.asc[gv] = 0u;
+        if (a.desc) a.desc[gv] = a.asc[gv] = 0u;
         if (a.ms) a.ms[gv] = 0u;
         lkey = Key(~Key(0));
         gv += d.XY;
@@ -1344,11 +1335,13 @@ __device__ __forceinline__ void tokens_tma_body(const CUtensorMap& mlt, const Br
           if (slot == ~uint64_t(0)) *a.overflow = 1;
           ltok = uint32_t(slot);
         }
-        lgv = make_uint2(__ldg(a.maxs + ld[i]), __ldg(a.mins + la[i]));
+        if (a.desc) lgv = make_uint2(__ldg(a.maxs + ld[i]), __ldg(a.mins + la[i]));
         lkey = key;
       }
-      a.desc[gv] = lgv.x;
-      a.asc[gv] = lgv.y;
+      if (a.desc) {
+        a.desc[gv] = lgv.x;
+        a.asc[gv] = lgv.y;
+      }
       if (a.ms) a.ms[gv] = ltok;
       gv += d.XY;
     }
@@ -1418,7 +1411,8 @@ __global__ void __launch_bounds__(B_THREADS, 4) k_brick(const BrickArgs a) {
     if (a.ids_out && gx0 + uint32_t(lane) < d.X && cy < d.Y) {
       // the owned layers of this thread's vertex column (x = lane, y = w)
       uint32_t lt = ~0u, lid = 0;
-      uint32_t* o = a.ids_out + (uint64_t(gx0 + lane) + uint64_t(d.X) * (uint64_t(cy) + uint64_t(d.Y) * gz0));
+      uint2 lab = make_uint2(0, 0);
+      const uint64_t vo = uint64_t(gx0 + lane) + uint64_t(d.X) * (uint64_t(cy) + uint64_t(d.Y) * gz0);
       // the brick's own layers, and the grid's last layer when it is this
       // brick's layer 32 (a z-slab's extra layer)
       for (int z = z0; z < z0 + zn && (z < TZ || gz0 + uint32_t(z) == d.Z - 1); ++z) {
@@ -1426,8 +1420,14 @@ __global__ void __launch_bounds__(B_THREADS, 4) k_brick(const BrickArgs a) {
         if (tk != lt) {
           lt = tk;
           lid = brick_token_id(a, tk);
+          if (a.desc_out) lab = brick_token_labels(a, tk);
         }
-        o[uint64_t(z) * d.XY] = lid;
+        const uint64_t v = vo + uint64_t(z) * d.XY;
+        a.ids_out[v] = lid;
+        if (a.desc_out) {
+          a.desc_out[v] = lab.x;
+          a.asc_out[v] = lab.y;
+        }
       }
     }
     // ---- cube layers z-1 whose two vertex layers are loaded
@@ -1539,11 +1539,16 @@ __device__ __forceinline__ void brick_tma_body(const CUtensorMap& mtok, const Br
   uint32_t pu = 0;                 // ... and whether its four labels agree (0 / 1)
   // ids (a.ids_out): this thread's vertex column
   const bool vert_ok = gx0 + uint32_t(lane) < d.X && cy < d.Y;
-  uint32_t* ids_col = a.ids_out ? a.ids_out + (uint64_t(gx0 + lane) + uint64_t(d.X) * (uint64_t(cy) + uint64_t(d.Y) * gz0))
-                                : nullptr;
+  const uint64_t ids_v0 = uint64_t(gx0 + lane) + uint64_t(d.X) * (uint64_t(cy) + uint64_t(d.Y) * gz0);
   if (a.ids_out && vert_ok && ncl == 0 && gz0 == d.Z - 1) {
     // a brick made of the volume's last vertex layer only: no cube layers
-    *ids_col = brick_token_id(a, __ldg(a.ms + (uint64_t(gx0 + lane) + uint64_t(d.X) * (uint64_t(cy) + uint64_t(d.Y) * gz0))));
+    const uint32_t tk = __ldg(a.ms + ids_v0);
+    a.ids_out[ids_v0] = brick_token_id(a, tk);
+    if (a.desc_out) {
+      const uint2 lab = brick_token_labels(a, tk);
+      a.desc_out[ids_v0] = lab.x;
+      a.asc_out[ids_v0] = lab.y;
+    }
   }
   if (tid == 0) {
     for (int k = 0; k < 2; ++k) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s_bar[k])));
@@ -1640,15 +1645,22 @@ __device__ __forceinline__ void brick_tma_body(const CUtensorMap& mtok, const Br
       // this thread's vertex column: the batch's bottom layers, and the
       // volume's top layer when the batch ends there
       const int nv = cn + ((gz0 + uint32_t(b * kBatch + cn) == d.Z - 1) ? 1 : 0);
-      uint32_t* o = ids_col + uint64_t(b * kBatch) * d.XY;
+      const uint64_t vo = ids_v0 + uint64_t(b * kBatch) * d.XY;
       uint32_t lt = ~0u, lid = 0;
+      uint2 lab = make_uint2(0, 0);
       for (int i = 0; i < nv; ++i) {
         const uint32_t tk = bb[i][w][lane];
         if (tk != lt) {
           lt = tk;
           lid = brick_token_id(a, tk);
+          if (a.desc_out) lab = brick_token_labels(a, tk);
         }
-        o[uint64_t(i) * d.XY] = lid;
+        const uint64_t v = vo + uint64_t(i) * d.XY;
+        a.ids_out[v] = lid;
+        if (a.desc_out) {
+          a.desc_out[v] = lab.x;
+          a.asc_out[v] = lab.y;
+        }
       }
     }
     // the batch's chunk counts, one store per layer from lanes 0 .. cn-1
@@ -2280,7 +2292,7 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
     o.sweeps = 0;
     auto sweep = [&]() {
       CK(cudaMemsetAsync(jflag, 0, 4, c.stream));
-      k_tt_jump<<<blocks_for(int64_t((nt + kJumpE - 1) / kJumpE), 256), 256, 0, c.stream>>>(nt, SD, SA, jflag);
+      k_tt_jump<<<blocks_for(int64_t((nt + 1) / 2), 256), 256, 0, c.stream>>>(nt, SD, SA, jflag);
       CK_LAUNCH("k_tt_jump");
       ++o.sweeps;
     };
@@ -2318,6 +2330,7 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
     const bool ids_in_count = c.ids_in_count;
     uint32_t* tokbuf = ids_in_count ? c.get_t<uint32_t>(S_TOKENS, uint64_t(g.n)) : ms;
     ba.ms = tokbuf;
+    if (ids_in_count) ba.desc = ba.asc = nullptr;  // the count pass writes the labels from the tokens
     CUtensorMap mtok;
     bool tok_tma = lt_tma && (g.X % 4) == 0;
     if (tok_tma) {
@@ -2462,6 +2475,8 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
       // cube classes, separator counts and the dense ids of every vertex
       BrickArgs cb = ba;
       cb.ids_out = ms;
+      cb.desc_out = desc;
+      cb.asc_out = asc;
       cb.bitmap = bitmap;
       cb.prefix = dense ? prefix : nullptr;
       cb.slot_id = slot_id;
@@ -2633,7 +2648,7 @@ void fused_segment(Ctx& c, const Grid& g, const float* field, uint32_t* desc, ui
   int sweeps = 0;
   for (;;) {
     CK(cudaMemsetAsync(jflag, 0, 4, c.stream));
-    k_tt_jump<<<blocks_for(int64_t((nt + kJumpE - 1) / kJumpE), 256), 256, 0, c.stream>>>(nt, SD, SA, jflag);
+    k_tt_jump<<<blocks_for(int64_t((nt + 1) / 2), 256), 256, 0, c.stream>>>(nt, SD, SA, jflag);
     CK_LAUNCH("k_tt_jump");
     ++sweeps;
     CK(cudaMemcpyAsync(reinterpret_cast<char*>(c.h_pinned) + 64, jflag, 4, cudaMemcpyDeviceToHost, c.stream));
@@ -2827,7 +2842,7 @@ void slab_segment(Ctx& c, const Grid& g, int64_t z0, int64_t z1, const float* fi
   int* jflag = reinterpret_cast<int*>(ctr_base + 192);
   for (;;) {
     CK(cudaMemsetAsync(jflag, 0, 4, c.stream));
-    k_tt_jump<<<blocks_for(int64_t((nt + kJumpE - 1) / kJumpE), 256), 256, 0, c.stream>>>(nt, SD, SA, jflag);
+    k_tt_jump<<<blocks_for(int64_t((nt + 1) / 2), 256), 256, 0, c.stream>>>(nt, SD, SA, jflag);
     CK_LAUNCH("k_tt_jump");
     ++st.sweeps;
     CK(cudaMemcpyAsync(reinterpret_cast<char*>(c.h_pinned) + 64, jflag, 4, cudaMemcpyDeviceToHost, c.stream));
