@@ -2853,7 +2853,8 @@ void slab_segment(Ctx& c, const Grid& g, int64_t z0, int64_t z1, const float* fi
   uint32_t* bnd = c.get_t<uint32_t>(S_SLAB_BND, 4 * uint64_t(d.XY));
   k_slab_boundary<<<blocks_for(2 * int64_t(d.XY), 256), 256, 0, c.stream>>>(d, TB, lt, SD, SA, bnd);
   CK_LAUNCH("k_slab_boundary");
-  c.sync();
+  // no device sync: the boundary layers and lists are ordered on the context
+  // stream, where the caller's collectives read them
   check_device(c, "slab_segment");
   st.stage = 1;
   if (info) {
@@ -2907,6 +2908,7 @@ void slab_resolve(Ctx& c, const uint32_t* G, int world, int rank, const int64_t*
   k_slab_patch<<<blocks_for(int64_t(st.nt), 256), 256, 0, c.stream>>>(st.nt, SD, SA, G, world, rank, d.XY, d_pre,
                                                                      d_pre + world + 1, err);
   CK_LAUNCH("k_slab_patch");
+  CK(cudaMemcpyAsync(reinterpret_cast<char*>(c.h_pinned) + 96, err, 4, cudaMemcpyDeviceToHost, c.stream));
   // tokens
   BrickArgs ba{};
   ba.d = d;
@@ -2987,9 +2989,9 @@ void slab_resolve(Ctx& c, const uint32_t* G, int world, int rank, const int64_t*
     k_write_occ<<<unsigned(fb), kCThreads, 0, c.stream>>>(fset, fcap, fcounts, st.keys, nullptr);
     CK_LAUNCH("k_write_occ");
   }
-  CK(cudaMemcpyAsync(c.h_pinned, err, 4, cudaMemcpyDeviceToHost, c.stream));
-  c.sync();
-  const int e = *reinterpret_cast<int*>(c.h_pinned);
+  // the patch kernel's error flag was copied out before the key compaction,
+  // whose scan synchronised the stream
+  const int e = *reinterpret_cast<volatile int*>(reinterpret_cast<char*>(c.h_pinned) + 96);
   if (e) fail(PLMSS_ERR_LOGIC, e == 2 ? "z-slab forest entry unresolved" : "z-slab portal chain broken");
   check_device(c, "slab_resolve");
   st.stage = 2;
@@ -3058,8 +3060,7 @@ void slab_ids(Ctx& c, const uint64_t* keys_all, int64_t n_keys_all, plmss_slab_i
     if (st.R) k_keys_to_gid<<<blocks_for(st.R, 256), 256, 0, c.stream>>>(st.keys, st.R, st.maxs_g, st.mins_g);
     CK_LAUNCH("k_keys_to_gid");
   }
-  c.sync();
-  check_device(c, "slab_ids");
+  check_device(c, "slab_ids");  // (stream-ordered: no device sync)
   st.stage = 3;
   if (info) {
     info->n_regions = st.R;
