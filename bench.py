@@ -132,6 +132,27 @@ def load_configs():
     return mod
 
 
+# The reference's benchmark CSV schema (proj/include/plmss/bench.hpp:56-58)
+# plus GPU columns. Phases map onto the fused pipeline's stages: order 0 (no
+# order field is needed), segmentation = pass A + extremum sort + forest,
+# combine = tokens, region table, ids and the separator counts (marching
+# phase 1 runs inside it, so index 0), geometry = the record emission.
+CSV_HEADER = ("dataset,workers,repeats,order_s,segmentation_s,combine_s,index_s,geometry_s,total_s,speedup,"
+              "efficiency,gpus,gvertices_per_s,hbm_roofline_frac")
+
+
+def write_csv(path, dataset, gpus, repeats, stage, ms, value, frac):
+    seg = (stage.get("tile_segment", 0) + stage.get("extrema_sort", 0) + stage.get("exit_resolve", 0)) * 1e-3
+    comb = stage.get("finalize_ids", 0) * 1e-3
+    geo = stage.get("march", 0) * 1e-3
+    new = not os.path.exists(path)
+    with open(path, "a") as fh:
+        if new:
+            fh.write(CSV_HEADER + "\n")
+        fh.write(f"{dataset},{gpus},{repeats},{0.0:.6f},{seg:.6f},{comb:.6f},{0.0:.6f},{geo:.6f},{ms * 1e-3:.6f},"
+                 f"1.000,1.000,{gpus},{value:.3f},{frac:.4f}\n")
+
+
 def cpu_sample(cfg, args):
     """The bounded CPU sample of the configured field, shared by the
     reference arm and the cpu_baseline leg: vertex layers [0, ref_layers)
@@ -376,7 +397,10 @@ def relaunch_under_torchrun(n):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--gpus", type=int, default=int(os.environ.get("PLMSS_GPUS", "1")),
+                    help="GPUs (one rank each); default $PLMSS_GPUS or 1 (the analogue of PLMSS_WORKERS)")
+    ap.add_argument("--csv", default="", help="also append the reference's benchmark CSV row (bench.hpp:56-58) "
+                                              "with GPU columns to this file")
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
@@ -641,6 +665,9 @@ def main():
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
+        if args.csv:
+            write_csv(args.csv, cfg.name, world, args.steps, stage, ms, value,
+                      line["roofline_pipeline"]["frac"])
     ctx.close()
     if pg:
         pg.destroy_process_group()

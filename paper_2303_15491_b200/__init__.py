@@ -12,6 +12,6 @@ from .api import (  # noqa: F401
     Context,
     FormatError, IoError, SegmentationResult, combine_ms, compute_order, default_context, emit_boundaries,
     emit_separators, fetch, index_separators, lib, materialize_separators, materialize_separators_chunked, pipeline,
-    pipeline_host, pipeline_host_batch, read_volume, result, result_digests, seed_hops, segment, select_labels, synth_field, synth_layers,
+    pipeline_host, pipeline_host_batch, read_volume, result, result_digests, result_view, seed_hops, segment, select_labels, synth_field, synth_layers,
     tet_table, weld_points, write_labels, write_separators_obj, write_surface_obj,
 )

@@ -576,6 +576,30 @@ def fetch(ctx: Context, res: PipelineResult, names=("desc", "asc", "ms", "maxima
     return out
 
 
+class _DevArray:
+    """__cuda_array_interface__ of context-owned device memory (zero-copy)."""
+
+    def __init__(self, ptr, shape, typestr):
+        self.__cuda_array_interface__ = {"shape": tuple(int(x) for x in shape), "typestr": typestr,
+                                         "data": (int(ptr or 0), False), "version": 3}
+
+
+def result_view(ctx: Context, res: PipelineResult, name: str):
+    """Zero-copy torch view of one pipeline output inside the context (valid
+    until the context's next call): no second device copy of e.g. cfg3's
+    86 GB of separator records."""
+    torch = _torch()
+    r = res.raw
+    spec = {"desc": (r.d_desc, (r.n_vertices,), "<i4"), "asc": (r.d_asc, (r.n_vertices,), "<i4"),
+            "ms": (r.d_ms, (r.n_vertices,), "<i4"), "maxima": (r.d_maxima, (r.n_maxima,), "<i4"),
+            "minima": (r.d_minima, (r.n_minima,), "<i4"), "region_keys": (r.d_region_keys, (r.n_regions,), "<i8"),
+            "tris": (r.d_tris, (r.n_tris, 2), "<i8")}
+    ptr, shape, ts = spec[name]
+    if not ptr or 0 in shape:
+        return torch.empty(shape, dtype=torch.int32 if ts == "<i4" else torch.int64, device=f"cuda:{ctx.device}")
+    return torch.as_tensor(_DevArray(ptr, shape, ts), device=f"cuda:{ctx.device}")
+
+
 def result_digests(ctx: Context, res: PipelineResult, names=("desc", "asc", "ms", "maxima", "minima",
                                                                "region_keys", "tris"), piece_bytes: int = 1 << 30):
     """Chunked SHA-256 (digest.py) of pipeline outputs in the context, read

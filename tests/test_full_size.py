@@ -104,7 +104,7 @@ def test_full_size_streamed_geometry_matches_reference(plmss, gpu, name):
                           noise_amp=cfg.noise, seed=cfg.seed, levels=cfg.levels, ctx=gpu)
     res = plmss.pipeline(cfg.dims, f, ctx=gpu)
     del f
-    tris = plmss.fetch(gpu, res, names=("tris",))["tris"]
+    tris = plmss.result_view(gpu, res, "tris")  # in place: cfg3's records alone are 86 GB
     hs = {k: ChunkedSha256() for k in ("points", "regions", "source_cells")}
     seen = [0]
 

@@ -397,3 +397,24 @@ def test_pipeline_host_batch_matches_single_calls(plmss, gpu):
         for k in ("desc", "asc", "ms"):
             assert np.array_equal(v[k], out[k]), k
         assert np.array_equal(v["tris"], out["tris"][: res.n_tris])
+
+
+@pytest.mark.parametrize("dims", [(2, 2, 2), (3, 2, 2), (2, 3, 2), (2, 2, 3), (33, 2, 2), (2, 2, 65), (4, 33, 2),
+                                  (65, 3, 34)])
+def test_pipeline_degenerate_extents(plmss, gpu, restatement, dims):
+    """Extents of 2 (one cube layer), single partial bricks and bricks cut
+    to one vertex in some axis, against the restatement."""
+    rng = np.random.default_rng(sum(dims))
+    f = rng.integers(0, 3, int(np.prod(dims))).astype(np.float32)
+    res = plmss.pipeline(dims, dev(f), ctx=gpu)
+    out = plmss.fetch(gpu, res)
+    s = restatement.segment(dims, values=f.astype(np.float64))
+    ms, keys = restatement.combine_ms(s["asc"], s["desc"])
+    for k, ref in (("desc", s["desc"]), ("asc", s["asc"]), ("ms", ms)):
+        assert np.array_equal(u32(out[k]), ref), k
+    e = restatement.emit_separators(dims, ms)
+    assert res.n_tris == len(e["source_cells"])
+    if res.n_tris:
+        m = plmss.materialize_separators(dims, out["tris"], ctx=gpu)
+        assert np.array_equal(m["source_cells"].cpu().numpy(), e["source_cells"])
+        assert np.array_equal(m["points"].cpu().numpy(), e["points"])
