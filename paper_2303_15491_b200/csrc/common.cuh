@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 #include <stdint.h>
 
 #include <functional>
@@ -169,8 +170,16 @@ struct Ctx {
     return static_cast<T*>(get(s, count * sizeof(T)));
   }
   void sync() { CK(cudaStreamSynchronize(stream)); }
+  // stage boundaries of the fused pipeline: CUDA events (stage_ms) when
+  // timing, and NVTX ranges (ncu --nvtx --nvtx-include "plmss.passA/")
+  bool nvtx_open = false;
   void mark(int i) {
     if (timing) CK(cudaEventRecord(ev[i], stream));
+    static const char* const kStage[5] = {"plmss.passA", "plmss.extrema_sort", "plmss.exit_resolve",
+                                          "plmss.finalize_ids", "plmss.march"};
+    if (nvtx_open) nvtxRangePop();
+    nvtx_open = i < 5;
+    if (nvtx_open) nvtxRangePushA(kStage[i]);
   }
 };
 
