@@ -35,23 +35,27 @@ def _stale(target: str, deps: list[str]) -> bool:
 LIB_CHECKED = os.path.join(PKG, "libplmss_b200_checked.so")
 
 
-def build_cuda(force: bool = False, verbose: bool = False, checked: bool = False) -> str:
+def build_cuda(force: bool = False, verbose: bool = False, checked: bool = False, variant: str = "",
+               defines: tuple = ()) -> str:
     """checked=True: libplmss_b200_checked.so with the device bounds checks
-    (-DPLMSS_CHECKED, fused.cu DCHECK), loaded when PLMSS_B200_LIB points at it."""
-    lib_path = LIB_CHECKED if checked else LIB
+    (-DPLMSS_CHECKED, fused.cu DCHECK), loaded when PLMSS_B200_LIB points at it.
+    variant="x", defines=("-DFOO",): libplmss_b200_x.so, an A/B build of the same
+    sources (same-box comparisons through PLMSS_B200_LIB)."""
+    lib_path = LIB_CHECKED if checked else (os.path.join(PKG, f"libplmss_b200_{variant}.so") if variant else LIB)
     deps = [os.path.join(CSRC, s) for s in SOURCES]
     deps += [os.path.join(CSRC, h) for h in os.listdir(CSRC) if h.endswith((".cuh", ".h"))]
     deps.append(os.path.join(INCLUDE, "plmss_b200.h"))
     if not force and not _stale(lib_path, deps):
         return lib_path
-    objdir = os.path.join(PKG, "_obj_checked" if checked else "_obj")
+    objdir = os.path.join(PKG, "_obj_checked" if checked else (f"_obj_{variant}" if variant else "_obj"))
     os.makedirs(objdir, exist_ok=True)
     objs = []
     procs = []
     for s in SOURCES:
         obj = os.path.join(objdir, s.replace(".cu", ".o"))
         objs.append(obj)
-        cmd = [NVCC] + NVCC_FLAGS + (["-DPLMSS_CHECKED"] if checked else []) + ["-c", os.path.join(CSRC, s), "-o", obj]
+        cmd = [NVCC] + NVCC_FLAGS + (["-DPLMSS_CHECKED"] if checked else []) + list(defines) + \
+            ["-c", os.path.join(CSRC, s), "-o", obj]
         if verbose:
             print(" ".join(cmd))
         procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
