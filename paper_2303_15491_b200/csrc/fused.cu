@@ -1752,9 +1752,6 @@ __device__ __noinline__ uint32_t general_record(uint32_t c6, uint32_t k) {
 
 __global__ void __launch_bounds__(256) k_emit_chunks(const EmitArgs a) {
   __shared__ uint8_t s_own[256 / 32][32];  // record window position -> lane of the cube starting there
-  // the current chunk's four corner rows of ids (33 columns), staged when it
-  // has multi-label cubes: their records pick two corners each
-  __shared__ uint32_t s_ids[256 / 32][4][33];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const uint32_t CX = a.X - 1, CY = a.Y - 1, XY = a.X * a.Y;
   const uint64_t ngroups = (a.nchunks + 31) / 32;
@@ -1849,17 +1846,6 @@ __global__ void __launch_bounds__(256) k_emit_chunks(const EmitArgs a) {
         lo2 = min(c[0], ib);
         hi2 = max(c[0], ib);
       }
-#ifndef PLMSS_NO_EMIT_STAGE
-      if (__any_sync(0xffffffffu, cls == 0xffu)) {
-        __syncwarp();  // the previous chunk's records have read s_ids
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          s_ids[wib][i][lane] = cur.r[i];
-          if (lane == 31) s_ids[wib][i][32] = cur.e[i];
-        }
-        __syncwarp();
-      }
-#endif
       uint32_t inc = cnt;
 #pragma unroll
       for (int s = 1; s < 32; s <<= 1) {
@@ -1897,16 +1883,9 @@ __global__ void __launch_bounds__(256) k_emit_chunks(const EmitArgs a) {
           const uint32_t r = general_record(c6, k);
           t = r & 0xffu;
           rowi = (r >> 8) & 0xffu;
-#ifndef PLMSS_NO_EMIT_STAGE
-          // corner c of cube src: row c >> 1, column src + (c & 1)
-          const uint32_t ca = (r >> 16) & 0xffu, cb2 = r >> 24;
-          la = s_ids[wib][ca >> 1][uint32_t(src) + (ca & 1u)];
-          lb = s_ids[wib][cb2 >> 1][uint32_t(src) + (cb2 & 1u)];
-#else
           const uint32_t vs = v0 - uint32_t(lane) + uint32_t(src);
           la = __ldg(a.ids + (vs + corner_off((r >> 16) & 0xffu)));
           lb = __ldg(a.ids + (vs + corner_off(r >> 24)));
-#endif
         }
         const uint64_t cr64 = ((6ull * (a.cube0 + uint64_t(q0 + uint32_t(src))) + t) << 6) | uint64_t(rowi);
         DCHECK(base + j < a.total, 501);
