@@ -408,7 +408,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--e2e-batch", type=int, default=6, help="volumes in the pipelined end-to-end batch (0: off)")
+    ap.add_argument("--e2e-batch", type=int, default=10, help="volumes in the pipelined end-to-end batch (0: off)")
     ap.add_argument("--slab", action="store_true",
                     help="run the z-slab (multi-GPU) path even at world size 1 (torchrun --nproc-per-node 1)")
     ap.add_argument("--cpu-runs", type=int, default=3, help="timed runs of the cpu_baseline sample")

@@ -285,7 +285,11 @@ __device__ __forceinline__ void hop_column_cube(const float* __restrict__ fc, co
   const float* p0 = fc + kHXY;
   float b0 = p0[-1 - kHX], b1 = p0[-kHX], b2 = p0[-1], b3 = p0[0];
   HopQuad U = hop_quad(b3, p0[1], p0[kHX], p0[kHX + 1], 8.f);  // upper quad, positions 8.. (v's upper cube)
+#ifdef PLMSS_HOP_UNROLL4
+#pragma unroll 4
+#else
 #pragma unroll 2
+#endif
   for (int lz = 0; lz < TZ; ++lz) {
     const float* p = fc + (lz + 2) * kHXY;  // plane z+1
     const float n0 = p[-1 - kHX], n1 = p[-kHX], n2 = p[-1], n3 = p[0], n4 = p[1], n5 = p[kHX], n6 = p[kHX + 1];
@@ -475,7 +479,11 @@ __global__ void __launch_bounds__(A_THREADS, 1)
       Pa[h] = uint16_t(h);
     }
   }
+#ifdef PLMSS_INIT_UNROLL4
+#pragma unroll 4
+#else
 #pragma unroll 2
+#endif
   for (int lz = 0; lz < TZ; ++lz) {
     const int h = hc + (lz + 1) * PXY;
     const uint32_t c = code[h];
@@ -506,6 +514,51 @@ __global__ void __launch_bounds__(A_THREADS, 1)
     uint32_t m = live_d | live_a, nd = 0, na = 0;
     // two vertices per iteration: up to four independent load chains, each
     // direction only while it is live
+#ifdef PLMSS_JUMP4
+    // four vertices per iteration: up to eight independent load chains
+    while (m) {
+      int lzv[4];
+      uint32_t bv[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        lzv[k] = m ? 31 - __clz(m) : lzv[k > 0 ? k - 1 : 0];
+        bv[k] = 1u << lzv[k];
+        m &= ~bv[k];
+      }
+      int hv[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) hv[k] = hc + (lzv[k] + 1) * PXY;
+      const uint32_t any = bv[0] | bv[1] | bv[2] | bv[3];
+      if (live_d & any) {
+        uint32_t p1[4], p2[4], p3[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) p1[k] = Pd[hv[k]];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) p2[k] = Pd[p1[k]];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) p3[k] = Pd[p2[k]];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          Pd[hv[k]] = uint16_t(p3[k]);
+          or_if_ne(nd, p3[k], p2[k], bv[k]);
+        }
+      }
+      if (live_a & any) {
+        uint32_t q1[4], q2[4], q3[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) q1[k] = Pa[hv[k]];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) q2[k] = Pa[q1[k]];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) q3[k] = Pa[q2[k]];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          Pa[hv[k]] = uint16_t(q3[k]);
+          or_if_ne(na, q3[k], q2[k], bv[k]);
+        }
+      }
+    }
+#else
     while (m) {
       const int lz = 31 - __clz(m);
       const uint32_t bit = 1u << lz;
@@ -537,6 +590,7 @@ __global__ void __launch_bounds__(A_THREADS, 1)
         or_if_ne(na, s3, s2, bit2);
       }
     }
+#endif
     live_d = nd;
     live_a = na;
     // asynchronous rounds (no barrier per round: measured 0.2 ms faster on
