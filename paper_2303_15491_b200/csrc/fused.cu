@@ -274,6 +274,69 @@ __device__ __forceinline__ uint32_t hop_code(float pos) {
   return uint32_t(0x0DCBA987F6543210ull >> (4 * p)) & 15u;
 }
 
+#ifdef PLMSS_HOP_W2
+// Variant (A/B, PLMSS_HOP_W2): the winner carried as power-of-two weights
+// instead of corner indices. Quad: W = sum over the corners attaining the
+// extremum of 2^bit (max: bit = corner, min: bit = 3 - corner), so the
+// highest set bit is the winner; merges scale the preferred operand's weight
+// past the other's bits (x16 within a cube, x128 between the cubes), and the
+// final position is the float exponent of W.
+struct HopW {
+  float M, WM, m, Wm;
+};
+__device__ __forceinline__ HopW hop_quad_w(float a, float b, float c, float d) {
+  HopW q;
+  q.M = fmaxf(fmaxf(a, b), fmaxf(c, d));
+  q.m = fminf(fminf(a, b), fminf(c, d));
+  q.WM = __fmaf_rn(feq(d, q.M), 8.f, __fmaf_rn(feq(c, q.M), 4.f, __fmaf_rn(feq(b, q.M), 2.f, feq(a, q.M))));
+  q.Wm = __fmaf_rn(feq(a, q.m), 8.f, __fmaf_rn(feq(b, q.m), 4.f, __fmaf_rn(feq(c, q.m), 2.f, feq(d, q.m))));
+  return q;
+}
+// max prefers hi (higher ids), min prefers lo
+__device__ __forceinline__ HopW hop_cube_w(const HopW& lo, const HopW& hi) {
+  HopW c;
+  c.M = fmaxf(lo.M, hi.M);
+  c.WM = __fmaf_rn(feq(hi.M, c.M), __fmaf_rn(16.f, hi.WM, -lo.WM), lo.WM);
+  c.m = fminf(lo.m, hi.m);
+  c.Wm = __fmaf_rn(feq(lo.m, c.m), __fmaf_rn(16.f, lo.Wm, -hi.Wm), hi.Wm);
+  return c;
+}
+__device__ __forceinline__ uint32_t w_exp(float w) { return (__float_as_uint(w) >> 23) - 127u; }
+
+template <int kHX, int kHXY, class Emit>
+__device__ __forceinline__ void hop_column_cube(const float* __restrict__ fc, const int nz, const uint32_t gv0,
+                                                const uint32_t XY, ACounters* __restrict__ ctr, Emit&& emit) {
+  HopW L = hop_quad_w(fc[-1 - kHX], fc[-kHX], fc[-1], fc[0]);
+  const float* p0 = fc + kHXY;
+  float b0 = p0[-1 - kHX], b1 = p0[-kHX], b2 = p0[-1], b3 = p0[0];
+  HopW U = hop_quad_w(b3, p0[1], p0[kHX], p0[kHX + 1]);
+#pragma unroll 2
+  for (int lz = 0; lz < TZ; ++lz) {
+    const float* p = fc + (lz + 2) * kHXY;
+    const float n0 = p[-1 - kHX], n1 = p[-kHX], n2 = p[-1], n3 = p[0], n4 = p[1], n5 = p[kHX], n6 = p[kHX + 1];
+    const HopW Ln = hop_quad_w(b0, b1, b2, b3);
+    const HopW Un = hop_quad_w(n3, n4, n5, n6);
+    if (lz < nz) {
+      const float fv = b3;
+      if (!isfinite(fv)) atomicMin(&ctr->bad, gv0 + XY * uint32_t(lz));
+      const HopW cl = hop_cube_w(L, Ln), cu = hop_cube_w(U, Un);
+      const float M = fmaxf(cl.M, cu.M), m = fminf(cl.m, cu.m);
+      // positions: lower cube corner k -> k, upper cube corner k -> 7 + k
+      const uint32_t pu = w_exp(__fmaf_rn(feq(cu.M, M), __fmaf_rn(128.f, cu.WM, -cl.WM), cl.WM));
+      const uint32_t pd = 14u - w_exp(__fmaf_rn(feq(cl.m, m), __fmaf_rn(128.f, cl.Wm, -cu.Wm), cu.Wm));
+      const uint32_t su = uint32_t(0x0DCBA987F6543210ull >> (4 * pu)) & 15u;
+      const uint32_t sd = uint32_t(0x0DCBA987F6543210ull >> (4 * pd)) & 15u;
+      emit(lz, uint8_t(su | sd << 4));
+    }
+    L = Ln;
+    U = Un;
+    b0 = n0;
+    b1 = n1;
+    b2 = n2;
+    b3 = n3;
+  }
+}
+#else
 template <int kHX, int kHXY, class Emit>
 __device__ __forceinline__ void hop_column_cube(const float* __restrict__ fc, const int nz, const uint32_t gv0,
                                                 const uint32_t XY, ACounters* __restrict__ ctr, Emit&& emit) {
@@ -316,6 +379,7 @@ __device__ __forceinline__ void hop_column_cube(const float* __restrict__ fc, co
     b3 = n3;
   }
 }
+#endif  // PLMSS_HOP_W2
 
 // ---------------------------------------------------------------- pass A --
 // One CTA (1024 threads, one per (x, y) column of 32 vertices) per 32^3
