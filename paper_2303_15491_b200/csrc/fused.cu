@@ -234,49 +234,12 @@ __device__ __forceinline__ void hop_column(const float* __restrict__ fc, const i
 // direction. Within every merge the second operand's corners all have higher
 // ids than the first's, so "the highest id attaining the maximum" (the
 // simulation of simplicity order, F5) is: take the second operand iff it
-// attains the maximum (FMNMX + FSET on the ALU pipe); the winner's corner
-// index rides along as a small float updated by FFMA blends (FMA pipe).
-// NaN (missing) neighbours never attain a maximum or minimum.
-struct HopQuad {
-  float M, tM;  // max and the highest corner attaining it (0..3, + base)
-  float m, tm;  // min and the lowest corner attaining it
-};
-
-// quad corners a < b < c < d in id order; tags offset by `base`
-__device__ __forceinline__ HopQuad hop_quad(float a, float b, float c, float d, float base) {
-  HopQuad q;
-  q.M = fmaxf(fmaxf(a, b), fmaxf(c, d));
-  q.m = fminf(fminf(a, b), fminf(c, d));
-  float t = base + feq(b, q.M);
-  t = __fmaf_rn(feq(c, q.M), (base + 2.f) - t, t);
-  t = __fmaf_rn(feq(d, q.M), (base + 3.f) - t, t);
-  q.tM = t;
-  float u = (base + 3.f) - feq(c, q.m);
-  u = __fmaf_rn(feq(b, q.m), (base + 1.f) - u, u);
-  u = __fmaf_rn(feq(a, q.m), base - u, u);
-  q.tm = u;
-  return q;
-}
-
-// cube = quad lo (corners +0) stacked under quad hi (corners +4)
-__device__ __forceinline__ HopQuad hop_cube(const HopQuad& lo, const HopQuad& hi) {
-  HopQuad c;
-  c.M = fmaxf(lo.M, hi.M);
-  c.tM = __fmaf_rn(feq(hi.M, c.M), (hi.tM + 4.f) - lo.tM, lo.tM);
-  c.m = fminf(lo.m, hi.m);
-  c.tm = __fmaf_rn(feq(lo.m, c.m), lo.tm - (hi.tm + 4.f), hi.tm + 4.f);
-  return c;
-}
-
-// position (0..6 lower cube, 7 = v, 8..14 upper cube) -> stencil s, 15 = none
-__device__ __forceinline__ uint32_t hop_code(float pos) {
-  const uint32_t p = __float_as_uint(pos + 12582912.0f) & 15u;  // exact small integer
-  return uint32_t(0x0DCBA987F6543210ull >> (4 * p)) & 15u;
-}
-
-#ifdef PLMSS_HOP_W2
-// Variant (A/B, PLMSS_HOP_W2): the winner carried as power-of-two weights
-// instead of corner indices. Quad: W = sum over the corners attaining the
+// attains the maximum (FMNMX + FSET on the ALU pipe); the winner rides
+// along as a power-of-two weight updated by FFMAs (FMA pipe): measured
+// faster than the per-vertex equality masks of hop_column and than corner
+// indices blended by FFMA. NaN (missing) neighbours never attain a maximum
+// or minimum.
+// Quad: W = sum over the corners attaining the
 // extremum of 2^bit (max: bit = corner, min: bit = 3 - corner), so the
 // highest set bit is the winner; merges scale the preferred operand's weight
 // past the other's bits (x16 within a cube, x128 between the cubes), and the
@@ -336,50 +299,6 @@ __device__ __forceinline__ void hop_column_cube(const float* __restrict__ fc, co
     b3 = n3;
   }
 }
-#else
-template <int kHX, int kHXY, class Emit>
-__device__ __forceinline__ void hop_column_cube(const float* __restrict__ fc, const int nz, const uint32_t gv0,
-                                                const uint32_t XY, ACounters* __restrict__ ctr, Emit&& emit) {
-  // stencil columns (dx, dy): c0 (-1,-1) c1 (0,-1) c2 (-1,0) c3 (0,0)
-  // c4 (1,0) c5 (0,1) c6 (1,1); fc = column (0, 0) at brick layer -1
-  // plane z-1 (brick layer -1): the lower quad
-  HopQuad L = hop_quad(fc[-1 - kHX], fc[-kHX], fc[-1], fc[0], 0.f);
-  // plane z (layer 0)
-  const float* p0 = fc + kHXY;
-  float b0 = p0[-1 - kHX], b1 = p0[-kHX], b2 = p0[-1], b3 = p0[0];
-  HopQuad U = hop_quad(b3, p0[1], p0[kHX], p0[kHX + 1], 8.f);  // upper quad, positions 8.. (v's upper cube)
-#ifdef PLMSS_HOP_UNROLL4
-#pragma unroll 4
-#else
-#pragma unroll 2
-#endif
-  for (int lz = 0; lz < TZ; ++lz) {
-    const float* p = fc + (lz + 2) * kHXY;  // plane z+1
-    const float n0 = p[-1 - kHX], n1 = p[-kHX], n2 = p[-1], n3 = p[0], n4 = p[1], n5 = p[kHX], n6 = p[kHX + 1];
-    const HopQuad Ln = hop_quad(b0, b1, b2, b3, 0.f);   // lower quad at plane z
-    const HopQuad Un = hop_quad(n3, n4, n5, n6, 8.f);   // upper quad at plane z+1
-    if (lz < nz) {
-      const float fv = b3;
-      if (!isfinite(fv)) atomicMin(&ctr->bad, gv0 + XY * uint32_t(lz));
-      // lower cube of v: L (plane z-1, corners 0..3) under Ln (plane z, 4..7);
-      // upper cube: U (plane z, positions 8..) under Un (plane z+1, +4)
-      const HopQuad cl = hop_cube(L, Ln);
-      const HopQuad cu = hop_cube(U, Un);
-      // U's corner 0 is v: position 8 -> 7 (v) after the -1 below
-      const float M = fmaxf(cl.M, cu.M), m = fminf(cl.m, cu.m);
-      const float pu = __fmaf_rn(feq(cu.M, M), (cu.tM - 1.f) - cl.tM, cl.tM);
-      const float pd = __fmaf_rn(feq(cl.m, m), cl.tm - (cu.tm - 1.f), cu.tm - 1.f);
-      emit(lz, uint8_t(hop_code(pu) | hop_code(pd) << 4));
-    }
-    L = Ln;
-    U = Un;
-    b0 = n0;
-    b1 = n1;
-    b2 = n2;
-    b3 = n3;
-  }
-}
-#endif  // PLMSS_HOP_W2
 
 // ---------------------------------------------------------------- pass A --
 // One CTA (1024 threads, one per (x, y) column of 32 vertices) per 32^3
