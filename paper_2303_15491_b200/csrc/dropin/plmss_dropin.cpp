@@ -8,6 +8,7 @@
 // std::invalid_argument (there is no CPU fallback). Status codes map back
 // to the reference exception types with the reference messages.
 #include <cuda_runtime.h>
+#include <sys/mman.h>
 
 #include <algorithm>
 #include <array>
@@ -16,6 +17,7 @@
 #include <stdexcept>
 #include <string>
 #include <thread>
+#include <type_traits>
 #include <vector>
 
 #include "plmss/marching.hpp"
@@ -107,6 +109,33 @@ void parallel_for(int64_t n, F&& f) {  // f(begin, end)
     if (b < e) th.emplace_back([&f, b, e] { f(b, e); });
   }
   for (auto& x : th) x.join();
+}
+
+// ---- large host outputs. The reference containers are value-initialised by
+// resize() on one thread; at geometry sizes (cfg2: 12 GB of mesh) that is
+// page-fault bound, the kernel zeroing every 4 KB page on first touch. The
+// storage is reserved first, its pages faulted in on all host threads (2 MB
+// pages where the kernel allows them), and only then sized.
+void prefault(void* p, size_t bytes) {
+  if (!p || bytes < (size_t(64) << 20)) return;
+  constexpr uintptr_t kHuge = uintptr_t(2) << 20;
+  const uintptr_t b = reinterpret_cast<uintptr_t>(p), e = b + bytes;
+  const uintptr_t hb = (b + kHuge - 1) & ~(kHuge - 1), he = e & ~(kHuge - 1);
+  if (he > hb) madvise(reinterpret_cast<void*>(hb), he - hb, MADV_HUGEPAGE);  // advice only
+  unsigned char* c = static_cast<unsigned char*>(p);
+  parallel_for(int64_t((bytes + 4095) / 4096), [&](int64_t i0, int64_t i1) {
+    for (int64_t i = i0; i < i1; ++i) c[std::min(size_t(i) * 4096, bytes - 1)] = 0;
+  });
+}
+
+template <class T>
+void resize_out(std::vector<T>& v, size_t n) {
+  static_assert(std::is_trivially_copyable_v<T>, "raw storage prefault");
+  if (v.capacity() < n) {
+    v.reserve(n);
+    prefault(v.data() + v.size(), (n - v.size()) * sizeof(T));
+  }
+  v.resize(n);
 }
 
 struct Stage {
@@ -268,7 +297,7 @@ const Tables& tabs() {
 OrderField compute_order(const ScalarField& field) {
   const int64_t n = field.values.size();
   OrderField order;
-  order.rank.resize(static_cast<size_t>(n));
+  resize_out(order.rank, static_cast<size_t>(n));
   if (n == 0) return order;
   DevBuf<double> dv(n);
   DevBuf<int64_t> dr(n);
@@ -301,13 +330,13 @@ SegmentationResult segment(const SimplicialComplex3& complex, const OrderField& 
                            &nmax, &nmin, &sweeps));
   SegmentationResult seg;
   if (want_desc) {
-    seg.desc.resize(n);
+    resize_out(seg.desc, size_t(n));
     down_widen(seg.desc.data(), dd.p, n);
     seg.maxima.resize(nmax);
     down_widen(seg.maxima.data(), dmx.p, nmax);
   }
   if (want_asc) {
-    seg.asc.resize(n);
+    resize_out(seg.asc, size_t(n));
     down_widen(seg.asc.data(), da.p, n);
     seg.minima.resize(nmin);
     down_widen(seg.minima.data(), dmn.p, nmin);
@@ -327,7 +356,7 @@ void combine_ms(SegmentationResult& seg, int workers) {
   up_narrow(dd.p, seg.desc.data(), n);
   int64_t r = 0;
   check(plmss_b200_combine_ms(ctx(), n, da.p, dd.p, dm.p, dk.p, &r));
-  seg.ms_region.resize(n);
+  resize_out(seg.ms_region, size_t(n));
   down_widen(seg.ms_region.data(), dm.p, n);
   std::vector<uint64_t> keys(r);
   dk.down(keys.data(), r);
@@ -532,9 +561,10 @@ SeparatingMesh emit_geometry(const SimplicialComplex3& complex, std::span<const 
   SeparatingMesh mesh;
   mesh.verts_per_primitive = 3;
   mesh.points.resize(3, 3 * total);
-  mesh.indices.resize(static_cast<size_t>(3 * total));
-  mesh.regions.resize(static_cast<size_t>(total));
-  mesh.source_cells.resize(static_cast<size_t>(total));
+  prefault(mesh.points.data(), size_t(9 * total) * sizeof(double));
+  resize_out(mesh.indices, static_cast<size_t>(3 * total));
+  resize_out(mesh.regions, static_cast<size_t>(total));
+  resize_out(mesh.source_cells, static_cast<size_t>(total));
   if (total) {
     const auto& sp = complex.grid_spacing();
     const auto& og = complex.grid_origin();
@@ -587,14 +617,17 @@ SeparatingMesh emit_boundaries(const SimplicialComplex3& complex, std::span<cons
   SeparatingMesh mesh;
   mesh.verts_per_primitive = 3;
   mesh.points.resize(3, np);
+  prefault(mesh.points.data(), size_t(3 * np) * sizeof(double));
   dpts.down(mesh.points.data(), 3 * np);
-  mesh.indices.resize(static_cast<size_t>(3 * nf));
+  resize_out(mesh.indices, static_cast<size_t>(3 * nf));
   didx.down(mesh.indices.data(), 3 * nf);
   std::vector<int64_t> tags(nf);
   dtag.down(tags.data(), nf);
-  mesh.regions.resize(static_cast<size_t>(nf));
-  for (int64_t i = 0; i < nf; ++i) mesh.regions[i] = {tags[i], -1};
-  mesh.source_cells.resize(static_cast<size_t>(nf));
+  resize_out(mesh.regions, static_cast<size_t>(nf));
+  parallel_for(nf, [&](int64_t b, int64_t e) {
+    for (int64_t i = b; i < e; ++i) mesh.regions[i] = {tags[i], -1};
+  });
+  resize_out(mesh.source_cells, static_cast<size_t>(nf));
   dcell.down(mesh.source_cells.data(), nf);
   return mesh;
 }
