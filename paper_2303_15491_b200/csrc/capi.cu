@@ -1,6 +1,9 @@
 // extern "C" boundary of libplmss_b200.so (declared in include/plmss_b200.h).
 // Converts internal exceptions to status codes + a thread-local message.
 #include <string.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <vector>
 
 #include <string>
 #include <thread>
@@ -12,6 +15,40 @@
 using namespace plmss_b200;
 
 unsigned long long plmss_b200::g_launches = 0;
+thread_local cudaStream_t plmss_b200::g_trace_stream = nullptr;
+namespace plmss_b200 {
+namespace {
+struct TraceRec {
+  const char* name;
+  cudaEvent_t ev;
+};
+thread_local std::vector<TraceRec> g_trace;
+}  // namespace
+void trace_launch(const char* name) {
+  cudaEvent_t e;
+  if (cudaEventCreate(&e) != cudaSuccess) return;
+  cudaEventRecord(e, g_trace_stream);
+  g_trace.push_back({name, e});
+}
+// start: events from here on; stop: sync, print each launch's time since the
+// previous event (launch + any gap before it) to stderr, release
+void trace_begin(cudaStream_t s) {
+  g_trace_stream = s;
+  trace_launch("begin");
+}
+void trace_end() {
+  if (!g_trace_stream) return;
+  cudaStreamSynchronize(g_trace_stream);
+  for (size_t i = 1; i < g_trace.size(); ++i) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, g_trace[i - 1].ev, g_trace[i].ev);
+    fprintf(stderr, "[ktrace] %-22s %8.4f ms\n", g_trace[i].name, ms);
+  }
+  for (auto& r : g_trace) cudaEventDestroy(r.ev);
+  g_trace.clear();
+  g_trace_stream = nullptr;
+}
+}  // namespace plmss_b200
 
 struct plmss_ctx {
   Ctx c;
@@ -437,7 +474,10 @@ int plmss_b200_pipeline(plmss_ctx* p, const int64_t dims[3], const float* d_fiel
     uint32_t* asc = c.get_t<uint32_t>(S_ASC, g.n);
     uint32_t* ms = c.get_t<uint32_t>(S_MS, g.n);
     if (c.pipeline_path == 0 && fused_supported(g)) {
+      static const bool ktrace = getenv("PLMSS_KTRACE") != nullptr;
+      if (ktrace) trace_begin(c.stream);
       const FusedOut fo = fused_pipeline(c, g, d_field, desc, asc, ms);
+      if (ktrace) trace_end();
       c.sync();
       finish_timing(c, 6);
       plmss_result& r = c.result;

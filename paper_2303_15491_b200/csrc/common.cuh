@@ -31,10 +31,19 @@ inline void cuda_check(cudaError_t e, const char* what) {
 // Kernel launches issued by this library (reported by bench.py).
 extern unsigned long long g_launches;
 #define CK(x) ::plmss_b200::cuda_check((x), #x)
+// Launch trace (measurement aid, PLMSS_KTRACE=1): the fused pipeline sets
+// g_trace_stream, and every launch on it is followed by an event, so the
+// gaps between kernels in the real (concurrent, warm-cache) pipeline can be
+// read off — which ncu's serialised launch list cannot show.
+extern thread_local cudaStream_t g_trace_stream;
+void trace_launch(const char* name);
+void trace_begin(cudaStream_t s);
+void trace_end();
 #define CK_LAUNCH(name)                                      \
   do {                                                       \
     __atomic_fetch_add(&::plmss_b200::g_launches, 1ull, __ATOMIC_RELAXED); \
     ::plmss_b200::cuda_check(cudaGetLastError(), name);      \
+    if (::plmss_b200::g_trace_stream) ::plmss_b200::trace_launch(name); \
   } while (0)
 
 // ------------------------------------------------------------------ grid ---
@@ -79,6 +88,7 @@ enum Slot {
   S_SLAB_BND,                             // z-slab pipeline: boundary layers
   S_CODES,                                // split pass A: hop codes (1 B per padded brick cell)
   S_TOKENS,                               // region tokens when the count pass writes the ids
+  S_CHUNK_G,                              // record offset of every 32-chunk group
   S_COUNT
 };
 

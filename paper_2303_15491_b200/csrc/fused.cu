@@ -1166,7 +1166,7 @@ struct BrickArgs {
   uint32_t* bitmap;               // dense mode: region bitmap
   unsigned long long* fset;       // hash mode: region set of (rank_min << 32 | rank_max)
   uint64_t fmask;
-  uint64_t* chunk;                // separator count per 32-cube chunk
+  uint16_t* chunk;                // separator count per 32-cube chunk (<= 32 * 90)
   uint8_t* cls;                   // per cube: 0 one region, m8 two labels, 0xff more
   uint32_t *desc, *asc, *ms;      // ms holds the region token until k_ms_ids (null: labels only)
   int* overflow;
@@ -1418,7 +1418,7 @@ __global__ void __launch_bounds__(B_THREADS, 4) k_brick(const BrickArgs a) {
   // layer at a time
   const uint64_t CX = d.X - 1, CXY = uint64_t(d.X - 1) * (d.Y - 1);
   uint8_t* clsp = a.cls + (uint64_t(gx0) + lane + CX * cy + CXY * gz0);
-  uint64_t* chp = a.chunk + (uint64_t(cy) + uint64_t(d.Y - 1) * gz0) * a.nxc + tx;
+  uint16_t* chp = a.chunk + (uint64_t(cy) + uint64_t(d.Y - 1) * gz0) * a.nxc + tx;
   const uint64_t chstep = uint64_t(d.Y - 1) * a.nxc;
   uint32_t pf[4] = {0, 0, 0, 0};  // top face of this thread's previous cube
   bool have_prev = false;
@@ -1528,7 +1528,7 @@ __global__ void __launch_bounds__(B_THREADS, 4) k_brick(const BrickArgs a) {
         *clsp = uint8_t(cls);
       }
       const uint32_t tot = __any_sync(0xffffffffu, cnt != 0) ? __reduce_add_sync(0xffffffffu, cnt) : 0u;
-      if (lane == 0 && row_ok) *chp = tot;
+      if (lane == 0 && row_ok) *chp = uint16_t(tot);
       clsp += CXY;
       chp += chstep;
     }
@@ -1575,7 +1575,7 @@ __device__ __forceinline__ void brick_tma_body(const CUtensorMap& mtok, const Br
   const bool cube_ok = row_ok && gx0 + uint32_t(lane) + 1 < d.X;
   const uint64_t CX = d.X - 1, CXY = uint64_t(d.X - 1) * (d.Y - 1);
   uint8_t* clsp = a.cls + (uint64_t(gx0) + lane + CX * cy + CXY * gz0);
-  uint64_t* chp = a.chunk + (uint64_t(cy) + uint64_t(d.Y - 1) * gz0) * a.nxc + tx;
+  uint16_t* chp = a.chunk + (uint64_t(cy) + uint64_t(d.Y - 1) * gz0) * a.nxc + tx;
   const uint64_t chstep = uint64_t(d.Y - 1) * a.nxc;
   uint32_t pf[4] = {0, 0, 0, 0};  // top face of this thread's previous cube
   uint32_t pu = 0;                 // ... and whether its four labels agree (0 / 1)
@@ -1706,7 +1706,7 @@ __device__ __forceinline__ void brick_tma_body(const CUtensorMap& mtok, const Br
       }
     }
     // the batch's chunk counts, one store per layer from lanes 0 .. cn-1
-    if (lane < cn && row_ok) chp[uint64_t(lane) * chstep] = btot;
+    if (lane < cn && row_ok) chp[uint64_t(lane) * chstep] = uint16_t(btot);
     chp += uint64_t(kBatch) * chstep;
     __syncthreads();  // buffer b & 1 is free for batch b + 2
   }
@@ -1748,11 +1748,42 @@ __device__ __forceinline__ uint32_t token_id(uint32_t k, const uint32_t* __restr
   return __ldg(slot_id + k);
 }
 
+// Record total of every group of 32 consecutive chunks (the emit warps'
+// unit), scanned into the groups' record offsets.
+__global__ void __launch_bounds__(256) k_group_sums(const uint16_t* __restrict__ cnt, uint64_t nchunks,
+                                                    uint64_t* __restrict__ gsum) {
+  const uint64_t g = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const uint64_t c0 = g * 32;
+  if (c0 >= nchunks) return;
+  uint32_t t = 0;
+  if (c0 + 32 <= nchunks) {
+    const uint4* p = reinterpret_cast<const uint4*>(cnt + c0);  // 64-byte aligned
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint4 v = __ldg(p + k);
+      t += (v.x & 0xffffu) + (v.x >> 16) + (v.y & 0xffffu) + (v.y >> 16) + (v.z & 0xffffu) + (v.z >> 16) +
+           (v.w & 0xffffu) + (v.w >> 16);
+    }
+  } else {
+    for (uint64_t c = c0; c < nchunks; ++c) t += cnt[c];
+  }
+  gsum[g] = t;
+}
+
+// group record offsets (exclusive) into gbase; returns the record total
+uint64_t group_offsets(Ctx& c, const uint16_t* cnt, uint64_t nchunks, uint64_t* gbase) {
+  const uint64_t ngroups = (nchunks + 31) / 32;
+  k_group_sums<<<unsigned((ngroups + 255) / 256), 256, 0, c.stream>>>(cnt, nchunks, gbase);
+  CK_LAUNCH("k_group_sums");
+  return exclusive_scan_u64(c, gbase, int64_t(ngroups), true);
+}
+
 struct EmitArgs {
   uint32_t X, Y, Z, nxc;
   uint64_t nchunks, total;
   uint64_t cube0;        // global id of cube 0 (z-slab pipeline; 0 otherwise)
-  const uint64_t* off;   // exclusive chunk offsets
+  const uint16_t* cnt;   // records per chunk
+  const uint64_t* gbase; // exclusive record offset of every group of 32 chunks
   const uint8_t* cls;
   const uint32_t* ids;   // ms (dense MS ids)
   plmss_tri* out;
@@ -1804,18 +1835,24 @@ __global__ void __launch_bounds__(256) k_emit_chunks(const EmitArgs a) {
   // chunks with records
   for (uint64_t grp = uint64_t(blockIdx.x) * (blockDim.x / 32) + wib; grp < ngroups; grp += warps) {
     const uint64_t chl = grp * 32 + uint64_t(lane);
-    const uint64_t my_off = chl < a.nchunks ? a.off[chl] : a.total;
-    uint64_t nx_off = __shfl_down_sync(0xffffffffu, my_off, 1);
-    if (lane == 31) nx_off = chl + 1 < a.nchunks ? a.off[chl + 1] : a.total;
-    uint32_t todo = __ballot_sync(0xffffffffu, nx_off > my_off);
+    const uint32_t ccnt = chl < a.nchunks ? uint32_t(a.cnt[chl]) : 0u;
+    uint32_t todo = __ballot_sync(0xffffffffu, ccnt != 0);
     if (!todo) continue;
+    // the chunk's offset: the group's base plus the warp's exclusive prefix
+    uint32_t cinc = ccnt;
+#pragma unroll
+    for (int s = 1; s < 32; s <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, cinc, s);
+      if (lane >= s) cinc += t;
+    }
+    const uint64_t my_off = __ldg(a.gbase + grp) + (cinc - ccnt);
     // this lane's chunk: cube row r = (cz, cy), x segment xs (nchunks < 2^32)
     const uint32_t c32 = uint32_t(chl), r_l = c32 / a.nxc, xs_l = c32 - r_l * a.nxc;
     const uint32_t cz_l = r_l / CY, cy_l = r_l - cz_l * CY;
     const uint32_t x0_l = 32 * xs_l;
     const uint32_t v0_l = x0_l + a.X * cy_l + XY * cz_l;  // min corner of the chunk's first cube
     const uint32_t q0_l = x0_l + CX * r_l;  // cube ids < n < 2^32
-    const uint32_t T_l = uint32_t(nx_off - my_off);
+    const uint32_t T_l = ccnt;
     // one busy chunk ahead: its classes and the ids of its cubes' four
     // corner rows (lane i: corners 0, 2, 4, 6 of cube i; corners 1, 3, 5, 7
     // come from lane i + 1, lane 31 loads them) are loaded while the current
@@ -2361,7 +2398,7 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
     ba.ms = ms;
     ba.overflow = flag;
     const uint64_t nchunks = uint64_t(ba.nxc) * uint64_t(g.Y - 1) * uint64_t(g.Z - 1);
-    uint64_t* chunk = c.get_t<uint64_t>(S_TMP1, nchunks ? nchunks : 1);
+    uint16_t* chunk = c.get_t<uint16_t>(S_TMP1, nchunks ? nchunks : 1);
     ba.chunk = chunk;
     ba.cls = c.get_t<uint8_t>(S_MASK, uint64_t(g.cubes ? g.cubes : 1));
     const unsigned cgrid = unsigned((TY / RY) * ntiles);
@@ -2537,7 +2574,9 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
         k_brick<<<cgrid, B_THREADS, 0, c.stream>>>(ba);
       CK_LAUNCH("k_brick");
     }
-    const uint64_t total = nchunks ? exclusive_scan_u64(c, chunk, int64_t(nchunks), true) : 0;
+    const uint64_t ngroups = (nchunks + 31) / 32;
+    uint64_t* gbase = c.get_t<uint64_t>(S_CHUNK_G, ngroups ? ngroups : 1);
+    const uint64_t total = nchunks ? group_offsets(c, chunk, nchunks, gbase) : 0;
     c.mark(4);
     // ---- D: ms tokens -> dense ids; separator records at their chunk offsets
     if (!ids_in_count) {
@@ -2557,7 +2596,8 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
       ea.nxc = ba.nxc;
       ea.nchunks = nchunks;
       ea.total = total;
-      ea.off = chunk;
+      ea.cnt = chunk;
+      ea.gbase = gbase;
       ea.cls = ba.cls;
       ea.ids = ms;
       ea.out = tris;
@@ -3128,8 +3168,9 @@ void slab_emit(Ctx& c, uint32_t* ids, plmss_slab_info* info) {
     BrickArgs ba{};
     ba.d = d;
     ba.nxc = nxc;
-    uint64_t* chunk = c.get_t<uint64_t>(S_TMP1, nchunks);
+    uint16_t* chunk = c.get_t<uint16_t>(S_TMP1, nchunks);
     ba.chunk = chunk;
+    uint64_t* gbase = c.get_t<uint64_t>(S_CHUNK_G, (nchunks + 31) / 32);
     ba.cls = c.get_t<uint8_t>(S_MASK, uint64_t(st.g.X - 1) * uint64_t(st.g.Y - 1) * ncl);
     ba.ms = st.ms;
     // dense: ms holds the tokens -> ids; hash: ms holds the ids -> copied
@@ -3144,7 +3185,7 @@ void slab_emit(Ctx& c, uint32_t* ids, plmss_slab_info* info) {
     else
       k_brick<<<cgrid, B_THREADS, 0, c.stream>>>(ba);
     CK_LAUNCH("k_brick");
-    total = exclusive_scan_u64(c, chunk, int64_t(nchunks), true);
+    total = group_offsets(c, chunk, nchunks, gbase);
     tris = c.get_t<plmss_tri>(S_TRIS, total ? total : 1);
     if (total) {
       EmitArgs ea{};
@@ -3155,7 +3196,8 @@ void slab_emit(Ctx& c, uint32_t* ids, plmss_slab_info* info) {
       ea.nchunks = nchunks;
       ea.total = total;
       ea.cube0 = uint64_t(st.z0) * uint64_t(st.g.X - 1) * uint64_t(st.g.Y - 1);
-      ea.off = chunk;
+      ea.cnt = chunk;
+      ea.gbase = gbase;
       ea.cls = ba.cls;
       ea.ids = ids;
       ea.out = tris;
