@@ -71,6 +71,10 @@ constexpr int HN = HXY * HZ;      // 46240 floats
 // that reaches one has left the brick, and the shell cell is the hop target.
 constexpr int PX = TX + 2, PXY = PX * (TY + 2), PN = PXY * (TZ + 2);  // 34, 1156, 39304
 constexpr int TN = TX * TY * TZ;
+// x-face copies of LT: after the ntiles * TN words of LT, per brick the words
+// of its x = 0 and x = 31 faces, (side, z, y)-major, so that pass B's gathers
+// along a neighbour's x-face (consecutive exits step in y) are coalesced
+constexpr int kFaceX = 2 * TY * TZ;
 constexpr int A_THREADS = 1024;
 constexpr int kCodeOff = 4 * HN;                // hop codes after the field box
 constexpr int kTabOff = kCodeOff + (PN + 15) / 16 * 16;  // code byte -> pointer delta, up and down
@@ -355,6 +359,22 @@ __global__ void __launch_bounds__(A_THREADS, 1)
   __syncthreads();
   const uint32_t ntiles = d.tx * d.ty * d.tz;
   uint32_t phase = 0;
+  // x-face copies of the LT words (kFaceX), staged in the dead code bytes
+  // during step 6 and written out coalesced while the next brick's box is in
+  // flight: thread tid moves words tid and tid + 1024, exactly the words its
+  // own part of the code fill overwrites next
+  uint32_t* fstage = reinterpret_cast<uint32_t*>(code);
+  uint32_t prev_bt = ~0u;
+  auto flush_faces = [&] {
+#ifndef PLMSS_NO_FACEX
+    if (prev_bt != ~0u) {
+      uint32_t* fo = lt + uint64_t(ntiles) * TN + uint64_t(prev_bt) * kFaceX;
+      fo[tid] = fstage[tid];
+      fo[tid + A_THREADS] = fstage[tid + A_THREADS];
+    }
+#endif
+  };
+  static_assert(kFaceX == 2 * A_THREADS && kFaceX * 4 <= PN, "face staging");
   // persistent: one CTA per SM walks the bricks
   for (uint32_t bt = blockIdx.x; bt < ntiles; bt += gridDim.x, phase ^= 1u) {
   const uint32_t tx = bt % d.tx, ty = (bt / d.tx) % d.ty, tz = bt / (d.tx * d.ty);
@@ -407,6 +427,7 @@ __global__ void __launch_bounds__(A_THREADS, 1)
   // while the box is in flight: no-hop codes everywhere (step 2 overwrites
   // the in-volume brick cells) and the pointer delta of each code byte per
   // direction (0 for "none" and for shell bytes 0xff / kExitMark)
+  flush_faces();
   for (int i = 4 * tid; i < PN; i += 4 * A_THREADS) *reinterpret_cast<uint32_t*>(code + i) = 0xffffffffu;
   if (tid < 512) {
     const uint32_t c = uint32_t(tid & 255), sn = tid < 256 ? (c & 15) : (c >> 4);
@@ -721,6 +742,12 @@ __global__ void __launch_bounds__(A_THREADS, 1)
   //    its own entry, any other vertex its terminal's)
   if (col_ok) {
     uint32_t* ol = lt + bm0 + lx + TX * ly;
+#ifdef PLMSS_NO_FACEX
+    const bool face = false;
+#else
+    const bool face = lx == 0 || lx == TX - 1;
+#endif
+    uint32_t* of = fstage + (lx ? TY * TZ : 0) + ly;
 #pragma unroll 4
     for (int lz = 0; lz < nz; ++lz) {
       const int h = hc + (lz + 1) * PXY;
@@ -728,11 +755,15 @@ __global__ void __launch_bounds__(A_THREADS, 1)
       const uint32_t pd = Pd[h], pa = Pa[h];
       DCHECK(pd < PN && pa < PN, 103);
       // both directions' terminal indices in one word: desc | asc << 16
-      ol[TX * TY * lz] = uint32_t((mmax & bit) ? pd : Pd[pd]) | uint32_t((mmin & bit) ? pa : Pa[pa]) << 16;
+      const uint32_t w = uint32_t((mmax & bit) ? pd : Pd[pd]) | uint32_t((mmin & bit) ? pa : Pa[pa]) << 16;
+      ol[TX * TY * lz] = w;
+      if (face) of[TY * lz] = w;
     }
   }
+  prev_bt = bt;
   __syncthreads();  // shared memory is reused by the next brick
   }
+  flush_faces();
 }
 
 // Pass A1 (split mode, PLMSS_OPT_PASS_A_SPLIT): the steepest hops alone, at
@@ -832,7 +863,17 @@ __global__ void __launch_bounds__(256) k_tt_succ(const uint4* __restrict__ TB, c
       } else {
         DCHECK((bm >> 15) < gridDim.x, 201);
         const uint32_t nb = __ldg(TBw + 4 * (bm >> 15));
-        const uint32_t l = __ldg(lt + bm);  // desc | asc << 16
+        // desc | asc << 16; x-face cells from the face copy (grid = ntiles)
+        const uint32_t cx = bm & 31u;
+        const uint32_t l =
+#ifdef PLMSS_NO_FACEX
+            false
+#else
+            (cx == 0 || cx == TX - 1)
+#endif
+                ? __ldg(lt + uint64_t(gridDim.x) * TN + uint64_t(bm >> 15) * kFaceX + (cx ? TY * TZ : 0) +
+                        ((bm >> 5) & 31u) + TY * ((bm >> 10) & 31u))
+                : __ldg(lt + bm);
         sd = nb + (l & 0xffffu);
         sa = nb + (l >> 16);
         DCHECK(sd < nt && sa < nt, 202);
@@ -2294,7 +2335,7 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
   char* ctr_base = static_cast<char*>(c.get(S_FLAGS, 1024));
   ACounters* ctr = reinterpret_cast<ACounters*>(ctr_base);
   int* flag = reinterpret_cast<int*>(ctr_base + 128);
-  uint32_t* lt = c.get_t<uint32_t>(S_LTD, ntiles * TN);  // desc | asc << 16
+  uint32_t* lt = c.get_t<uint32_t>(S_LTD, ntiles * (TN + kFaceX));  // desc | asc << 16, then the x faces
   // LT as a 2-D tensor (1024 cells of a brick layer, ntiles * 32 layers) for
   // the token pass: one box = 8 rows x 32 layers of a brick
   CUtensorMap mlt;
@@ -2669,7 +2710,7 @@ void fused_segment(Ctx& c, const Grid& g, const float* field, uint32_t* desc, ui
   }
   char* ctr_base = static_cast<char*>(c.get(S_FLAGS, 1024));
   ACounters* ctr = reinterpret_cast<ACounters*>(ctr_base);
-  uint32_t* lt = c.get_t<uint32_t>(S_LTD, ntiles * TN);  // desc | asc << 16
+  uint32_t* lt = c.get_t<uint32_t>(S_LTD, ntiles * (TN + kFaceX));  // desc | asc << 16, then the x faces
   uint4* TB = c.get_t<uint4>(S_TB, ntiles);
   uint32_t *maxima = nullptr, *minima = nullptr, *max_tt = nullptr, *min_tt = nullptr, *TT = nullptr;
   ACounters h;
@@ -2855,7 +2896,7 @@ void slab_segment(Ctx& c, const Grid& g, int64_t z0, int64_t z1, const float* fi
   c.stats[4] = use_tma ? 1 : 0;
   char* ctr_base = static_cast<char*>(c.get(S_FLAGS, 1024));
   ACounters* ctr = reinterpret_cast<ACounters*>(ctr_base);
-  uint32_t* lt = c.get_t<uint32_t>(S_LTD, ntiles * TN);  // desc | asc << 16
+  uint32_t* lt = c.get_t<uint32_t>(S_LTD, ntiles * (TN + kFaceX));  // desc | asc << 16, then the x faces
   uint4* TB = c.get_t<uint4>(S_TB, ntiles);
   const uint64_t nloc = uint64_t(d.n);
   uint32_t *maxima = nullptr, *minima = nullptr, *max_tt = nullptr, *min_tt = nullptr, *TT = nullptr;
