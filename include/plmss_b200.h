@@ -310,7 +310,10 @@ int plmss_b200_copy(plmss_ctx* ctx, void* dst, const void* d_src, int64_t bytes,
  *   PLMSS_OPT_IDS_IN_COUNT  1 (default): region tokens in a scratch array, the count pass
  *                           writes the dense ids (no in-place id pass over
  *                           ms), 0: tokens in ms, counts interleaved with the
- *                           token pass, then the id pass (both exact). */
+ *                           token pass, then the id pass; 2: a mark pass builds
+ *                           the region bitmap first, the token pass writes the
+ *                           ids into ms, counts interleaved (dense keys; all
+ *                           exact). */
 /* pipeline_host over a sequence of volumes of the same dims, double-buffered:
  * two internal contexts (own non-blocking streams, created on first use,
  * options copied from ctx) take alternate volumes on two host threads, so

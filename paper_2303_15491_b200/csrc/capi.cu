@@ -571,7 +571,8 @@ int plmss_b200_ctx_set_option(plmss_ctx* p, int option, int64_t value) {
       return;
     }
     if (option == PLMSS_OPT_IDS_IN_COUNT) {
-      c.ids_in_count = value != 0;
+      if (value < 0 || value > 2) fail(PLMSS_ERR_INVALID_ARGUMENT, "ids mode must be 0, 1 or 2");
+      c.ids_mode = int(value);
       return;
     }
     if (option == PLMSS_OPT_PIPELINE_PATH) {
@@ -640,7 +641,7 @@ int plmss_b200_pipeline_host_batch(plmss_ctx* p, const int64_t dims[3], plmss_ho
       q->c.spec_sweeps = p->c.spec_sweeps;
       q->c.pass_a_split = p->c.pass_a_split;
       q->c.hop_cube = p->c.hop_cube;
-      q->c.ids_in_count = p->c.ids_in_count;
+      q->c.ids_mode = p->c.ids_mode;
     }
   });
   if (st) return st;

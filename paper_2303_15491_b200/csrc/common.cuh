@@ -156,7 +156,7 @@ struct Ctx {
   int spec_sweeps = 1;   // PLMSS_OPT_SPECULATIVE_SWEEPS
   bool pass_a_split = false;  // PLMSS_OPT_PASS_A_SPLIT
   bool hop_cube = true;       // PLMSS_OPT_HOP_CUBE
-  bool ids_in_count = true;   // PLMSS_OPT_IDS_IN_COUNT
+  int ids_mode = 1;           // PLMSS_OPT_IDS_IN_COUNT (0, 1, 2: mark pass)
   // Adaptive capacities of the fused pipeline (remembered between calls).
   uint64_t fused_exit_cap = 0, fused_pair_hint = 0, fused_tri_cap = 0, fused_ext_cap = 0;
   // Diagnostics of the last fused call: [0] exit entries, [1] pass-A retries,

@@ -1334,7 +1334,11 @@ __global__ void __launch_bounds__(32 * kTokRows) k_tokens(const BrickArgs a) {
 // k_tokens with the CTA's terminal indices (8 rows x 32 layers of its brick,
 // 2 x 16 KB) staged by two 2-D TMA tensor copies instead of per-thread loads.
 constexpr int kTokSmem = 2 * TZ * 32 * kTokRows * 2;  // both index arrays
-template <bool kDense>
+// kMode 0: region tokens (dense key / hash slot) and the labels; 1: mark
+// only (region bitmap bits, no writes: a gather only where a column's LT
+// word changes); 2: the dense ids straight into ms (bitmap and prefix
+// complete) and the labels.
+template <bool kDense, int kMode = 0>
 __device__ __forceinline__ void tokens_tma_body(const CUtensorMap& mlt, const BrickArgs& a, const uint32_t blk,
                                                 unsigned char* smem) {
   using Key = typename std::conditional<kDense, uint32_t, unsigned long long>::type;
@@ -1370,6 +1374,35 @@ __device__ __forceinline__ void tokens_tma_body(const CUtensorMap& mlt, const Br
   const uint32_t l = threadIdx.x;  // column within the CTA's rows
   const uint32_t* fd = a.FD + base;
   const uint32_t* fa = a.FA + base;
+  if (kMode == 1) {
+    static_assert(kDense || kMode != 1, "mark mode is dense only");
+    // kTokZ layers per group: all table gathers in flight first (a repeated
+    // word hits L1), then the bits where the column's word changed
+    uint32_t llv = ~0u;
+#pragma unroll 1
+    for (int z0 = 0; z0 < nz; z0 += kTokZ) {
+      uint32_t lv[kTokZ], rd[kTokZ], ra[kTokZ];
+#pragma unroll
+      for (int i = 0; i < kTokZ; ++i) {
+        lv[i] = z0 + i < nz ? sl[z0 + i][l] : llv;
+        DCHECK(base + (lv[i] & 0xffffu) < a.nt && base + (lv[i] >> 16) < a.nt, 405);
+        rd[i] = __ldg(fd + (lv[i] & 0xffffu));
+        ra[i] = __ldg(fa + (lv[i] >> 16));
+      }
+#pragma unroll
+      for (int i = 0; i < kTokZ; ++i) {
+        if (lv[i] == llv) continue;
+        llv = lv[i];
+        if (!(rd[i] & ra[i] & kFinal)) continue;  // unresolved (speculative sweep): redone
+        const uint32_t key = (ra[i] & ~kFinal) * a.nmax + (rd[i] & ~kFinal);
+        DCHECK((rd[i] & ~kFinal) < a.nmax && (ra[i] & ~kFinal) < a.nmin && (key >> 5) < a.nw, 406);
+        const uint32_t bit = 1u << (key & 31);
+        uint32_t* wp = a.bitmap + (key >> 5);
+        if (!(*wp & bit)) atomicOr(wp, bit);
+      }
+    }
+    return;
+  }
   uint32_t gv = gx + d.X * (gy + d.Y * gz0);
   Key lkey = Key(~Key(0));
   uint32_t ltok = 0;
@@ -1407,6 +1440,9 @@ __device__ __forceinline__ void tokens_tma_body(const CUtensorMap& mlt, const Br
       if (key != lkey) {
         if (!a.ms) {
           // labels only (fused_segment): no region set
+        } else if (kMode == 2) {
+          DCHECK((uint32_t(key) >> 5) < a.nw, 402);
+          ltok = brick_token_id(a, uint32_t(key));
         } else if (kDense) {
           ltok = uint32_t(key);
           const uint32_t bit = 1u << (ltok & 31);
@@ -1759,11 +1795,11 @@ __global__ void __launch_bounds__(B_THREADS, 6) k_brick_tma(const __grid_constan
   brick_tma_body(mtok, a, blockIdx.x, smem);
 }
 
-template <bool kDense>
+template <bool kDense, int kMode = 0>
 __global__ void __launch_bounds__(32 * kTokRows, 4) k_tokens_tma(const __grid_constant__ CUtensorMap mlt,
                                                                 const BrickArgs a) {
   __shared__ __align__(128) unsigned char smem[kTokSmem];
-  tokens_tma_body<kDense>(mlt, a, blockIdx.x, smem);
+  tokens_tma_body<kDense, kMode>(mlt, a, blockIdx.x, smem);
 }
 
 // Pass C, one launch per brick z-layer s: the tokens of layer s and the
@@ -1771,6 +1807,7 @@ __global__ void __launch_bounds__(32 * kTokRows, 4) k_tokens_tma(const __grid_co
 // CTAs interleaved so that the memory-bound token work and the issue-bound
 // cube classification share every SM.
 static_assert(TY / kTokRows == TY / RY && 32 * kTokRows == B_THREADS, "token and count items must match");
+template <int kMode = 0>
 __global__ void __launch_bounds__(B_THREADS, 5) k_slab_tma(const __grid_constant__ CUtensorMap mlt,
                                                            const __grid_constant__ CUtensorMap mtok,
                                                            const BrickArgs ta, const BrickArgs ca) {
@@ -1778,7 +1815,7 @@ __global__ void __launch_bounds__(B_THREADS, 5) k_slab_tma(const __grid_constant
   if (blockIdx.x & 1)
     brick_tma_body(mtok, ca, blockIdx.x >> 1, smem);
   else
-    tokens_tma_body<true>(mlt, ta, blockIdx.x >> 1, smem);
+    tokens_tma_body<true, kMode>(mlt, ta, blockIdx.x >> 1, smem);
 }
 
 // Region token -> dense MS id.
@@ -2447,7 +2484,13 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
     // tokens as a 3-D tensor for the count pass: in ms (ids rewritten in
     // place by k_ms_ids), or (PLMSS_OPT_IDS_IN_COUNT) in a scratch array the
     // count pass translates into ms
-    const bool ids_in_count = c.ids_in_count;
+    // PLMSS_OPT_IDS_IN_COUNT 2 (mark mode, dense keys with TMA): a mark pass
+    // builds the region bitmap from LT and the tables alone, so the token
+    // pass writes dense ids straight into ms and the count pass (no id
+    // writes) runs interleaved with it, layer by layer
+    const bool mark_mode = c.ids_mode == 2 && lt_tma && (g.X % 4) == 0 &&
+                           uint64_t(o.n_max) * uint64_t(o.n_min) < (uint64_t(1) << 32) && c.combine_path != 2;
+    const bool ids_in_count = !mark_mode && c.ids_mode != 0;
     uint32_t* tokbuf = ids_in_count ? c.get_t<uint32_t>(S_TOKENS, uint64_t(g.n)) : ms;
     ba.ms = tokbuf;
     // (the count pass can also write the labels from the tokens, desc_out /
@@ -2482,7 +2525,10 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
       // on the side stream as soon as they are written
       const uint32_t bpl = d.tx * d.ty;
       const unsigned items = bpl * (TY / kTokRows);
-      if (ids_in_count) {
+      if (mark_mode) {
+        k_tokens_tma<true, 1><<<tgrid, 32 * kTokRows, 0, c.stream>>>(mlt, ba);
+        CK_LAUNCH("k_mark");
+      } else if (ids_in_count) {
         // all tokens first; the count pass (ids) runs once the set is complete
         if (lt_tma)
           k_tokens_tma<true><<<tgrid, 32 * kTokRows, 0, c.stream>>>(mlt, ba);
@@ -2499,7 +2545,7 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
           if (L >= 2) {
             BrickArgs cs = ba;
             cs.brick0 = (L - 2) * bpl;
-            k_slab_tma<<<2 * items, B_THREADS, 0, c.stream>>>(mlt, mtok, ts, cs);
+            k_slab_tma<><<<2 * items, B_THREADS, 0, c.stream>>>(mlt, mtok, ts, cs);
             CK_LAUNCH("k_slab_tma");
           } else {
             k_tokens_tma<true><<<items, 32 * kTokRows, 0, c.stream>>>(mlt, ts);
@@ -2593,7 +2639,40 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
       c.stats[2] = int64_t(fcap);
     }
     o.n_regions = R;
-    if (ids_in_count) {
+    if (mark_mode) {
+      // token pass in id mode (labels + dense ids into ms) for brick layer
+      // L with the count pass of layer L - 2 in the same grid, then the
+      // last two count passes
+      BrickArgs ia = ba;
+      ia.prefix = prefix;
+      const uint32_t bpl = d.tx * d.ty;
+      const unsigned items = bpl * (TY / kTokRows);
+      if (tok_tma) {
+        for (uint32_t L = 0; L < d.tz; ++L) {
+          BrickArgs ts = ia;
+          ts.brick0 = L * bpl;
+          if (L >= 2) {
+            BrickArgs cs = ba;
+            cs.brick0 = (L - 2) * bpl;
+            k_slab_tma<2><<<2 * items, B_THREADS, 0, c.stream>>>(mlt, mtok, ts, cs);
+            CK_LAUNCH("k_slab_tma");
+          } else {
+            k_tokens_tma<true, 2><<<items, 32 * kTokRows, 0, c.stream>>>(mlt, ts);
+            CK_LAUNCH("k_tokens");
+          }
+        }
+        BrickArgs cs = ba;
+        const uint32_t c0 = d.tz >= 2 ? d.tz - 2 : 0;
+        cs.brick0 = c0 * bpl;
+        k_brick_tma<<<(d.tz - c0) * items, B_THREADS, 0, c.stream>>>(mtok, cs);
+        CK_LAUNCH("k_brick");
+      } else {
+        k_tokens_tma<true, 2><<<tgrid, 32 * kTokRows, 0, c.stream>>>(mlt, ia);
+        CK_LAUNCH("k_tokens");
+        k_brick<<<cgrid, B_THREADS, 0, c.stream>>>(ba);
+        CK_LAUNCH("k_brick");
+      }
+    } else if (ids_in_count) {
       // cube classes, separator counts and the dense ids of every vertex
       BrickArgs cb = ba;
       cb.ids_out = ms;
@@ -2620,7 +2699,7 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
     const uint64_t total = nchunks ? group_offsets(c, chunk, nchunks, gbase) : 0;
     c.mark(4);
     // ---- D: ms tokens -> dense ids; separator records at their chunk offsets
-    if (!ids_in_count) {
+    if (!ids_in_count && !mark_mode) {
       const unsigned mgrid = unsigned((uint64_t(g.n) + 1023) / 1024);
       if (dense)
         k_ms_ids<true><<<mgrid, 256, 0, c.stream>>>(ms, uint64_t(g.n), bitmap, prefix, slot_id);

@@ -44,11 +44,15 @@ def test_golden_digest_files_are_complete(name):
 # Split (third field): pass A as the hop-code kernel + the code-fed brick
 # compression (PLMSS_OPT_PASS_A_SPLIT), else the single fused kernel.
 # Hop (fourth field): 1 = the cube-shared steepest hops (PLMSS_OPT_HOP_CUBE).
-# Hop 2 = cube hops + the count pass writing the ids (PLMSS_OPT_IDS_IN_COUNT).
+# Hop 2 = cube hops + the count pass writing the ids (PLMSS_OPT_IDS_IN_COUNT 1),
+# hop 3 = cube hops + the mark pass (PLMSS_OPT_IDS_IN_COUNT 2; the hash-key
+# cfg3 falls back to 1).
 CASES = [("cfg1", 0, 1, 0, 0), ("cfg1", 0, 0, 1, 1), ("cfg2", 0, 1, 0, 0), ("cfg2", 2, 1, 1, 0), ("cfg2", 0, 0, 0, 1),
          ("cfg2", 0, 1, 0, 2), ("cfg3", 0, 1, 0, 0), ("cfg3", 0, 1, 1, 1), ("cfg3", 0, 1, 0, 2), ("cfg4", 0, 1, 0, 0),
          ("cfg4", 0, 0, 1, 0), ("cfg4", 0, 1, 0, 1), ("cfg4", 0, 0, 0, 2), ("cfg5", 0, 1, 0, 0), ("cfg5", 2, 1, 0, 0),
-         ("cfg5", 0, 1, 1, 0), ("cfg5", 0, 1, 0, 1), ("cfg5", 0, 1, 0, 2), ("cfg5", 2, 1, 0, 2)]
+         ("cfg5", 0, 1, 1, 0), ("cfg5", 0, 1, 0, 1), ("cfg5", 0, 1, 0, 2), ("cfg5", 2, 1, 0, 2),
+         ("cfg1", 0, 1, 0, 3), ("cfg2", 0, 0, 0, 3), ("cfg3", 0, 1, 0, 3), ("cfg4", 0, 1, 0, 3), ("cfg5", 0, 1, 0, 3),
+         ("cfg5", 0, 0, 0, 3)]
 
 
 @pytest.mark.gpu
@@ -69,7 +73,7 @@ def test_full_size_matches_oracle(plmss, gpu, name, path, spec, split, hop):
     gpu.set_option(plmss.OPT_SPECULATIVE_SWEEPS, spec)
     gpu.set_option(plmss.OPT_PASS_A_SPLIT, split)
     gpu.set_option(plmss.OPT_HOP_CUBE, 1 if hop else 0)
-    gpu.set_option(plmss.OPT_IDS_IN_COUNT, 1 if hop == 2 else 0)
+    gpu.set_option(plmss.OPT_IDS_IN_COUNT, {2: 1, 3: 2}.get(hop, 0))
     try:
         res = plmss.pipeline(cfg.dims, f, ctx=gpu)
     finally:

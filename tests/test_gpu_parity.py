@@ -229,8 +229,9 @@ def test_compute_order(plmss, gpu, restatement):
 #       4 fused with the cube-shared steepest hops, 5 = 3 + 4,
 #       6 fused with the ids written by the count pass (the default), 7 = 6 +
 #       hash-set keys; paths 0-5 run the interleaved token / count passes and
-#       the in-place id pass
-@pytest.mark.parametrize("path", [0, 1, 2, 3, 4, 5, 6, 7])
+#       the in-place id pass; 8 = the mark pass (region bitmap first, ids
+#       written by the token pass, count pass interleaved: IDS_IN_COUNT 2)
+@pytest.mark.parametrize("path", [0, 1, 2, 3, 4, 5, 6, 7, 8])
 @pytest.mark.parametrize("name", golden_cases())
 def test_pipeline_matches_reference(plmss, gpu, name, path):
     g = load_case(name)
@@ -238,8 +239,8 @@ def test_pipeline_matches_reference(plmss, gpu, name, path):
     gpu.set_option(2, 1 if path == 1 else 0)  # PIPELINE_PATH: 0 fused, 1 staged
     gpu.set_option(1, 2 if path in (2, 7) else 0)  # COMBINE_PATH: 2 hash
     gpu.set_option(plmss.OPT_PASS_A_SPLIT, 1 if path in (3, 5) else 0)
-    gpu.set_option(plmss.OPT_HOP_CUBE, 1 if path in (4, 5, 6, 7) else 0)
-    gpu.set_option(plmss.OPT_IDS_IN_COUNT, 1 if path in (6, 7) else 0)
+    gpu.set_option(plmss.OPT_HOP_CUBE, 1 if path in (4, 5, 6, 7, 8) else 0)
+    gpu.set_option(plmss.OPT_IDS_IN_COUNT, 2 if path == 8 else (1 if path in (6, 7) else 0))
     try:
         res = plmss.pipeline(dims, dev(g["field"]), ctx=gpu)
     finally:
@@ -287,15 +288,15 @@ def _field(kind, dims, seed):
     return host_field(scaled(CONFIGS["cfg2"], dims))
 
 
-@pytest.mark.parametrize("path", [0, 2, 3, 4, 5, 6, 7])
+@pytest.mark.parametrize("path", [0, 2, 3, 4, 5, 6, 7, 8])
 @pytest.mark.parametrize("dims,kind", [((97, 66, 40), "gauss"), ((33, 33, 33), "noise"), ((64, 31, 65), "ties"),
                                        ((128, 96, 70), "gauss"), ((70, 40, 36), "noise"), ((36, 20, 33), "ties")])
 def test_pipeline_brick_geometry(plmss, gpu, restatement, dims, kind, path):
     f = _field(kind, dims, sum(dims))
     gpu.set_option(1, 2 if path in (2, 7) else 0)
     gpu.set_option(plmss.OPT_PASS_A_SPLIT, 1 if path in (3, 5) else 0)
-    gpu.set_option(plmss.OPT_HOP_CUBE, 1 if path in (4, 5, 6, 7) else 0)
-    gpu.set_option(plmss.OPT_IDS_IN_COUNT, 1 if path in (6, 7) else 0)
+    gpu.set_option(plmss.OPT_HOP_CUBE, 1 if path in (4, 5, 6, 7, 8) else 0)
+    gpu.set_option(plmss.OPT_IDS_IN_COUNT, 2 if path == 8 else (1 if path in (6, 7) else 0))
     try:
         res = plmss.pipeline(dims, dev(f), ctx=gpu)
     finally:
