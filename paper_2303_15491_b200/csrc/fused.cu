@@ -1216,25 +1216,7 @@ struct BrickArgs {
   // bitmap word prefix, hash: slot -> id), so no id pass over ms is needed
   uint32_t* ids_out;
   const uint32_t *prefix, *slot_id;
-  // ... and the labels (desc / asc vertex ids) from the tokens when the token
-  // pass skipped them (desc == nullptr there)
-  uint32_t *desc_out, *asc_out;
 };
-
-// region token -> (vertex id of the maximum, of the minimum): dense key
-// rank_min * nmax + rank_max, or the hash set's (rank_min << 32 | rank_max)
-__device__ __forceinline__ uint2 brick_token_labels(const BrickArgs& a, uint32_t k) {
-  uint32_t ra, rd;
-  if (a.prefix) {
-    ra = k / a.nmax;
-    rd = k - ra * a.nmax;
-  } else {
-    const unsigned long long key = __ldg(a.fset + k);
-    ra = uint32_t(key >> 32);
-    rd = uint32_t(key);
-  }
-  return make_uint2(__ldg(a.maxs + rd), __ldg(a.mins + ra));
-}
 
 // region token -> dense MS id, the count pass's copy of token_id
 __device__ __forceinline__ uint32_t brick_token_id(const BrickArgs& a, uint32_t k) {
@@ -1384,13 +1366,14 @@ __device__ __forceinline__ void tokens_tma_body(const CUtensorMap& mlt, const Br
       uint32_t lv[kTokZ], rd[kTokZ], ra[kTokZ];
 #pragma unroll
       for (int i = 0; i < kTokZ; ++i) {
-        lv[i] = z0 + i < nz ? sl[z0 + i][l] : llv;
+        lv[i] = sl[min(z0 + i, nz - 1)][l];  // past the volume: a valid word, not used
         DCHECK(base + (lv[i] & 0xffffu) < a.nt && base + (lv[i] >> 16) < a.nt, 405);
         rd[i] = __ldg(fd + (lv[i] & 0xffffu));
         ra[i] = __ldg(fa + (lv[i] >> 16));
       }
 #pragma unroll
       for (int i = 0; i < kTokZ; ++i) {
+        if (z0 + i >= nz) break;
         if (lv[i] == llv) continue;
         llv = lv[i];
         if (!(rd[i] & ra[i] & kFinal)) continue;  // unresolved (speculative sweep): redone
@@ -1530,7 +1513,6 @@ __global__ void __launch_bounds__(B_THREADS, 4) k_brick(const BrickArgs a) {
     if (a.ids_out && gx0 + uint32_t(lane) < d.X && cy < d.Y) {
       // the owned layers of this thread's vertex column (x = lane, y = w)
       uint32_t lt = ~0u, lid = 0;
-      uint2 lab = make_uint2(0, 0);
       const uint64_t vo = uint64_t(gx0 + lane) + uint64_t(d.X) * (uint64_t(cy) + uint64_t(d.Y) * gz0);
       // the brick's own layers, and the grid's last layer when it is this
       // brick's layer 32 (a z-slab's extra layer)
@@ -1539,14 +1521,8 @@ __global__ void __launch_bounds__(B_THREADS, 4) k_brick(const BrickArgs a) {
         if (tk != lt) {
           lt = tk;
           lid = brick_token_id(a, tk);
-          if (a.desc_out) lab = brick_token_labels(a, tk);
         }
-        const uint64_t v = vo + uint64_t(z) * d.XY;
-        a.ids_out[v] = lid;
-        if (a.desc_out) {
-          a.desc_out[v] = lab.x;
-          a.asc_out[v] = lab.y;
-        }
+        a.ids_out[vo + uint64_t(z) * d.XY] = lid;
       }
     }
     // ---- cube layers z-1 whose two vertex layers are loaded
@@ -1661,13 +1637,7 @@ __device__ __forceinline__ void brick_tma_body(const CUtensorMap& mtok, const Br
   const uint64_t ids_v0 = uint64_t(gx0 + lane) + uint64_t(d.X) * (uint64_t(cy) + uint64_t(d.Y) * gz0);
   if (a.ids_out && vert_ok && ncl == 0 && gz0 == d.Z - 1) {
     // a brick made of the volume's last vertex layer only: no cube layers
-    const uint32_t tk = __ldg(a.ms + ids_v0);
-    a.ids_out[ids_v0] = brick_token_id(a, tk);
-    if (a.desc_out) {
-      const uint2 lab = brick_token_labels(a, tk);
-      a.desc_out[ids_v0] = lab.x;
-      a.asc_out[ids_v0] = lab.y;
-    }
+    a.ids_out[ids_v0] = brick_token_id(a, __ldg(a.ms + ids_v0));
   }
   if (tid == 0) {
     for (int k = 0; k < 2; ++k) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s_bar[k])));
@@ -1766,20 +1736,13 @@ __device__ __forceinline__ void brick_tma_body(const CUtensorMap& mtok, const Br
       const int nv = cn + ((gz0 + uint32_t(b * kBatch + cn) == d.Z - 1) ? 1 : 0);
       const uint64_t vo = ids_v0 + uint64_t(b * kBatch) * d.XY;
       uint32_t lt = ~0u, lid = 0;
-      uint2 lab = make_uint2(0, 0);
       for (int i = 0; i < nv; ++i) {
         const uint32_t tk = bb[i][w][lane];
         if (tk != lt) {
           lt = tk;
           lid = brick_token_id(a, tk);
-          if (a.desc_out) lab = brick_token_labels(a, tk);
         }
-        const uint64_t v = vo + uint64_t(i) * d.XY;
-        a.ids_out[v] = lid;
-        if (a.desc_out) {
-          a.desc_out[v] = lab.x;
-          a.asc_out[v] = lab.y;
-        }
+        a.ids_out[vo + uint64_t(i) * d.XY] = lid;
       }
     }
     // the batch's chunk counts, one store per layer from lanes 0 .. cn-1
@@ -2493,9 +2456,9 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
     const bool ids_in_count = !mark_mode && c.ids_mode != 0;
     uint32_t* tokbuf = ids_in_count ? c.get_t<uint32_t>(S_TOKENS, uint64_t(g.n)) : ms;
     ba.ms = tokbuf;
-    // (the count pass can also write the labels from the tokens, desc_out /
-    // asc_out, with the token pass skipping them: measured slower on cfg5,
-    // 7.36 vs 7.22 ms for the two passes, so the token pass writes them)
+    // (the count pass writing the labels from the tokens, the token pass
+    // skipping them, measured slower on cfg5: 7.36 vs 7.22 ms for the two
+    // passes, so the token pass writes them)
     CUtensorMap mtok;
     bool tok_tma = lt_tma && (g.X % 4) == 0;
     if (tok_tma) {

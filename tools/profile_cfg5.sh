@@ -6,7 +6,7 @@
 # Usage: tools/profile_cfg5.sh TAG [KERNEL_REGEX]
 set -e
 TAG=${1:-cur}
-KRE=${2:-"k_tile_segment|k_tt_succ|k_tt_jump|k_slab_tma|k_emit_chunks|k_ms_ids"}
+KRE=${2:-"k_tile_segment|k_tt_succ|k_tt_jump|k_tokens_tma|k_brick_tma|k_emit_chunks"}
 mkdir -p gpurun_out
 python bench.py --steps 10 --warmup 3 > gpurun_out/bench_${TAG}.json 2> gpurun_out/bench_${TAG}.err
 cat gpurun_out/bench_${TAG}.json
