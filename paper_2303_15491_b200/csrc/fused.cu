@@ -1752,14 +1752,20 @@ __device__ __forceinline__ void brick_tma_body(const CUtensorMap& mtok, const Br
   }
 }
 
-__global__ void __launch_bounds__(B_THREADS, 6) k_brick_tma(const __grid_constant__ CUtensorMap mtok,
+#ifndef PLMSS_BRICK_MINB
+#define PLMSS_BRICK_MINB 6
+#endif
+#ifndef PLMSS_TOK_MINB
+#define PLMSS_TOK_MINB 4
+#endif
+__global__ void __launch_bounds__(B_THREADS, PLMSS_BRICK_MINB) k_brick_tma(const __grid_constant__ CUtensorMap mtok,
                                                              const BrickArgs a) {
   __shared__ __align__(128) unsigned char smem[kBrickSmem];
   brick_tma_body(mtok, a, blockIdx.x, smem);
 }
 
 template <bool kDense, int kMode = 0>
-__global__ void __launch_bounds__(32 * kTokRows, 4) k_tokens_tma(const __grid_constant__ CUtensorMap mlt,
+__global__ void __launch_bounds__(32 * kTokRows, PLMSS_TOK_MINB) k_tokens_tma(const __grid_constant__ CUtensorMap mlt,
                                                                 const BrickArgs a) {
   __shared__ __align__(128) unsigned char smem[kTokSmem];
   tokens_tma_body<kDense, kMode>(mlt, a, blockIdx.x, smem);
