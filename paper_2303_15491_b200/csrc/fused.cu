@@ -1825,12 +1825,19 @@ uint64_t group_offsets(Ctx& c, const uint16_t* cnt, uint64_t nchunks, uint64_t* 
   return exclusive_scan_u64(c, gbase, int64_t(ngroups), true);
 }
 
+// Emission grid: warp tasks of whole 32-chunk groups, split into 2, 4, .. 32
+// tasks per group while there are fewer than ~256 warp tasks per SM (small
+// volumes: cfg1 has 248 groups of ~13 k records each). Sets ea.cshift.
+struct EmitArgs;
+unsigned emit_grid(const Ctx& c, EmitArgs& ea);
+
 struct EmitArgs {
   uint32_t X, Y, Z, nxc;
   uint64_t nchunks, total;
   uint64_t cube0;        // global id of cube 0 (z-slab pipeline; 0 otherwise)
   const uint16_t* cnt;   // records per chunk
   const uint64_t* gbase; // exclusive record offset of every group of 32 chunks
+  uint32_t cshift;       // a warp task = 32 >> cshift chunks of a group (small volumes: more tasks)
   const uint8_t* cls;
   const uint32_t* ids;   // ms (dense MS ids)
   plmss_tri* out;
@@ -1870,6 +1877,8 @@ __device__ __noinline__ uint32_t general_record(uint32_t c6, uint32_t k) {
   return t | rowi << 8 | corner((row >> 12) & 3) << 16 | corner((row >> 14) & 3) << 24;
 }
 
+// kSplit: warp tasks of 32 >> cshift chunks (small volumes), else whole groups
+template <bool kSplit>
 __global__ void __launch_bounds__(256) k_emit_chunks(const EmitArgs a) {
   __shared__ uint8_t s_own[256 / 32][32];  // record window position -> lane of the cube starting there
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -1880,10 +1889,16 @@ __global__ void __launch_bounds__(256) k_emit_chunks(const EmitArgs a) {
   // warps take groups of 32 consecutive chunks; one coalesced load of their
   // offsets and one division per lane for their coordinates, then only the
   // chunks with records
-  for (uint64_t grp = uint64_t(blockIdx.x) * (blockDim.x / 32) + wib; grp < ngroups; grp += warps) {
+  // (nchunks < 2^32: task and group indices fit 32 bits)
+  const uint32_t cshift = kSplit ? a.cshift : 0u;
+  const uint64_t ntasks = ngroups << cshift;
+  const uint32_t tmask = 0xffffffffu >> (32u - (32u >> cshift));  // this task's chunks, before the shift
+  for (uint64_t task = uint64_t(blockIdx.x) * (blockDim.x / 32) + wib; task < ntasks; task += warps) {
+    const uint64_t grp = task >> cshift;
     const uint64_t chl = grp * 32 + uint64_t(lane);
     const uint32_t ccnt = chl < a.nchunks ? uint32_t(a.cnt[chl]) : 0u;
     uint32_t todo = __ballot_sync(0xffffffffu, ccnt != 0);
+    if (kSplit) todo &= tmask << ((uint32_t(task) << (5u - cshift)) & 31u);
     if (!todo) continue;
     // the chunk's offset: the group's base plus the warp's exclusive prefix
     uint32_t cinc = ccnt;
@@ -2023,6 +2038,14 @@ __global__ void __launch_bounds__(256) k_emit_chunks(const EmitArgs a) {
       cur = nxt;
     }
   }
+}
+
+unsigned emit_grid(const Ctx& c, EmitArgs& ea) {
+  const uint64_t ngroups = (ea.nchunks + 31) / 32, target = uint64_t(c.sm_count) * 256;
+  ea.cshift = 0;
+  while (ea.cshift < 5 && (ngroups << ea.cshift) < target) ++ea.cshift;
+  const uint64_t tasks = ngroups << ea.cshift;
+  return unsigned(std::max<uint64_t>(1, std::min<uint64_t>((tasks + 7) / 8, uint64_t(c.sm_count) * 256)));
 }
 
 // ms: region token -> dense id, in place (4 vertices per thread, the last
@@ -2690,9 +2713,11 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
       ea.cls = ba.cls;
       ea.ids = ms;
       ea.out = tris;
-      const uint64_t nrows = uint64_t(g.Y - 1) * uint64_t(g.Z - 1);
-      const unsigned egrid = unsigned(std::min<uint64_t>((nrows + 7) / 8, uint64_t(c.sm_count) * 256));
-      k_emit_chunks<<<egrid, 256, 0, c.stream>>>(ea);
+      const unsigned egrid = emit_grid(c, ea);
+      if (ea.cshift)
+        k_emit_chunks<true><<<egrid, 256, 0, c.stream>>>(ea);
+      else
+        k_emit_chunks<false><<<egrid, 256, 0, c.stream>>>(ea);
       CK_LAUNCH("k_emit_chunks");
     }
     c.mark(5);
@@ -3290,9 +3315,11 @@ void slab_emit(Ctx& c, uint32_t* ids, plmss_slab_info* info) {
       ea.cls = ba.cls;
       ea.ids = ids;
       ea.out = tris;
-      const uint64_t nrows = uint64_t(st.g.Y - 1) * ncl;
-      const unsigned egrid = unsigned(std::min<uint64_t>((nrows + 7) / 8, uint64_t(c.sm_count) * 256));
-      k_emit_chunks<<<egrid, 256, 0, c.stream>>>(ea);
+      const unsigned egrid = emit_grid(c, ea);
+      if (ea.cshift)
+        k_emit_chunks<true><<<egrid, 256, 0, c.stream>>>(ea);
+      else
+        k_emit_chunks<false><<<egrid, 256, 0, c.stream>>>(ea);
       CK_LAUNCH("k_emit_chunks");
     }
   } else {
