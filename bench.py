@@ -422,7 +422,7 @@ def main():
     ap.add_argument("--ref-xy", type=int, default=512, help="x / y extent of the CPU sample")
     args = ap.parse_args()
     rank, world, local = dist_setup()
-    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+    if (args.gpus > 1 or args.slab) and "WORLD_SIZE" not in os.environ:
         return relaunch_under_torchrun(args.gpus)
 
     if args.impl == "reference":
