@@ -129,14 +129,12 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-// Stencil s = 0..13 in ascending id-delta order (complex.cpp:78-88) as
-// 2-bit-per-axis codes (dx+1 | (dy+1) << 2 | (dz+1) << 4); the vertex itself
-// sits between s = 6 and s = 7.
-__host__ __device__ constexpr uint32_t stencil_code(int s) {
-  return s == 0 ? 0x00 : s == 1 ? 0x01 : s == 2 ? 0x04 : s == 3 ? 0x05 : s == 4 ? 0x10 : s == 5 ? 0x11
-       : s == 6 ? 0x14 : s == 7 ? 0x16 : s == 8 ? 0x19 : s == 9 ? 0x1a : s == 10 ? 0x25 : s == 11 ? 0x26
-       : s == 12 ? 0x29 : 0x2a;
-}
+// Stencil s = 0..13 in ascending id-delta order (complex.cpp:78-88): s < 7
+// are the corners k = dx + 2 dy + 4 dz of the lower unit cube
+// [x-1, x] x [y-1, y] x [z-1, z] of v (s = k), s >= 7 the corners k of the
+// upper cube [x, x+1] x ... (s = 6 + k); the vertex itself sits between s = 6
+// and s = 7. Hop codes store cube positions p = s + (s >= 7), p = 7 for
+// "no hop" (v is the lower cube's corner 7 and the upper cube's corner 0).
 
 // Shell cell j of the 34^3 pointer space, j in [0, kShell): the z = 0 and
 // z = 33 layers, then the side walls layer by layer (rows y = 0, y = 33,
@@ -210,9 +208,10 @@ __device__ __forceinline__ void hop_column(const float* __restrict__ fc, const i
         // au == 0 only when every neighbour is missing (M is NaN): no hop
         const uint32_t hu = uint32_t(__float_as_int(au) >> 23) - 127u + (up_hi ? 7u : 0u);  // highest s attaining M
         const uint32_t hd = (dn_lo ? 6u : 13u) - (uint32_t(__float_as_int(ad) >> 23) - 127u);  // lowest s attaining m
-        const uint32_t su = (M > fv || (M == fv && up_hi)) ? hu : 15u;
-        const uint32_t sd = (m < fv || (m == fv && dn_lo)) ? hd : 15u;
-        emit(lz, uint8_t(su | (sd << 4)));
+        // hop code: cube positions (s < 7 -> s, s >= 7 -> s + 1, none -> 7)
+        const uint32_t pu = (M > fv || (M == fv && up_hi)) ? hu + (hu >= 7u) : 7u;
+        const uint32_t pd = (m < fv || (m == fv && dn_lo)) ? hd + (hd >= 7u) : 7u;
+        emit(lz, uint8_t(pu | (pd << 4)));
       }
       a0m = a0;
       a1m = a1;
@@ -253,7 +252,7 @@ struct HopW {
 };
 __device__ __forceinline__ HopW hop_quad_w(float a, float b, float c, float d) {
   HopW q;
-  q.M = fmaxf(fmaxf(a, b), fmaxf(c, d));
+  q.M = fmaxf(fmaxf(a, b), fmaxf(c, d));  // FMNMX3 + FMNMX (nvcc fuses the chain)
   q.m = fminf(fminf(a, b), fminf(c, d));
   q.WM = __fmaf_rn(feq(d, q.M), 8.f, __fmaf_rn(feq(c, q.M), 4.f, __fmaf_rn(feq(b, q.M), 2.f, feq(a, q.M))));
   q.Wm = __fmaf_rn(feq(a, q.m), 8.f, __fmaf_rn(feq(b, q.m), 4.f, __fmaf_rn(feq(c, q.m), 2.f, feq(d, q.m))));
@@ -289,11 +288,11 @@ __device__ __forceinline__ void hop_column_cube(const float* __restrict__ fc, co
       const HopW cl = hop_cube_w(L, Ln), cu = hop_cube_w(U, Un);
       const float M = fmaxf(cl.M, cu.M), m = fminf(cl.m, cu.m);
       // positions: lower cube corner k -> k, upper cube corner k -> 7 + k
-      const uint32_t pu = w_exp(__fmaf_rn(feq(cu.M, M), __fmaf_rn(128.f, cu.WM, -cl.WM), cl.WM));
-      const uint32_t pd = 14u - w_exp(__fmaf_rn(feq(cl.m, m), __fmaf_rn(128.f, cl.Wm, -cu.Wm), cu.Wm));
-      const uint32_t su = uint32_t(0x0DCBA987F6543210ull >> (4 * pu)) & 15u;
-      const uint32_t sd = uint32_t(0x0DCBA987F6543210ull >> (4 * pd)) & 15u;
-      emit(lz, uint8_t(su | sd << 4));
+      // (v itself -> 7: no hop); the hop code is pu | pd << 4, straight from
+      // the weights' exponents: pu = e_u - 127, pd = 14 - (e_d - 127)
+      const uint32_t eu = __float_as_uint(__fmaf_rn(feq(cu.M, M), __fmaf_rn(128.f, cu.WM, -cl.WM), cl.WM)) >> 23;
+      const uint32_t ed = __float_as_uint(__fmaf_rn(feq(cl.m, m), __fmaf_rn(128.f, cl.Wm, -cu.Wm), cu.Wm)) >> 23;
+      emit(lz, uint8_t(eu + 16u * (141u - ed) - 127u));
     }
     L = Ln;
     U = Un;
@@ -341,8 +340,9 @@ __global__ void __launch_bounds__(A_THREADS, 1)
   uint16_t* Pd = reinterpret_cast<uint16_t*>(a_smem);  // PN (steps 3+, aliases f)
   uint16_t* Pa = Pd + PN;                              // PN
   uint8_t* code = a_smem + kCodeOff;                   // PN
-  int* dup = reinterpret_cast<int*>(a_smem + kTabOff);  // 256: pointer delta of the up hop of a code byte
-  int* ddn = dup + 256;                                 // 256: ... of the down hop
+  // per code byte: pointer deltas of its up and down hops (one 8-byte load
+  // for both directions of the same byte)
+  int2* dtab = reinterpret_cast<int2*>(a_smem + kTabOff);
   __shared__ __align__(8) uint64_t s_bar;
   __shared__ uint32_t s_wcnt[A_THREADS / 32][3];
   __shared__ uint32_t s_tot[3];
@@ -369,8 +369,10 @@ __global__ void __launch_bounds__(A_THREADS, 1)
 #ifndef PLMSS_NO_FACEX
     if (prev_bt != ~0u) {
       uint32_t* fo = lt + uint64_t(ntiles) * TN + uint64_t(prev_bt) * kFaceX;
+      // the x = 31 face is staged with y ^ 16 (a different bank from the
+      // x = 0 word of the same (y, z)): un-swizzled here, still one segment
       fo[tid] = fstage[tid];
-      fo[tid + A_THREADS] = fstage[tid + A_THREADS];
+      fo[A_THREADS + (tid ^ 16)] = fstage[tid + A_THREADS];
     }
 #endif
   };
@@ -430,13 +432,16 @@ __global__ void __launch_bounds__(A_THREADS, 1)
   flush_faces();
   for (int i = 4 * tid; i < PN; i += 4 * A_THREADS) *reinterpret_cast<uint32_t*>(code + i) = 0xffffffffu;
   if (tid < 512) {
-    const uint32_t c = uint32_t(tid & 255), sn = tid < 256 ? (c & 15) : (c >> 4);
+    // hop codes hold cube positions: lower cube corner k = dx + 2 dy + 4 dz
+    // of [x-1, x] x [y-1, y] x [z-1, z] -> k, upper cube corner k -> 7 + k,
+    // 7 = no hop (v itself)
+    const uint32_t c = uint32_t(tid & 255), pn = tid < 256 ? (c & 15) : (c >> 4);
     int dl = 0;
-    if (sn < 14 && c < kExitMark) {
-      const uint32_t o = stencil_code(int(sn));
-      dl = (int(o & 3) - 1) + PX * (int((o >> 2) & 3) - 1) + PXY * (int((o >> 4) & 3) - 1);
+    if (pn != 7 && pn < 15 && c < kExitMark) {
+      const int k = pn < 7 ? int(pn) : int(pn) - 7, o = pn < 7 ? -1 : 0;
+      dl = ((k & 1) + o) + PX * (((k >> 1) & 1) + o) + PXY * ((k >> 2) + o);
     }
-    dup[tid] = dl;  // dup[256 + c] == ddn[c]
+    reinterpret_cast<int*>(dtab)[2 * c + (tid >> 8)] = dl;
   }
   if (kTMA || kCodes) {
     asm volatile(
@@ -491,18 +496,20 @@ __global__ void __launch_bounds__(A_THREADS, 1)
   for (int lz = 0; lz < TZ; ++lz) {
     const int h = hc + (lz + 1) * PXY;
     const uint32_t c = code[h];
-    int u = h + dup[c], w = h + ddn[c];
+    const int2 dc = dtab[c];
+    int u = h + dc.x, w = h + dc.y;
     const uint32_t cu = code[u], cw = code[w];
     if (cu >= kExitMark && u != h) code[u] = kExitMark;
     if (cw >= kExitMark && w != h) code[w] = kExitMark;
-    const int du = dup[cu], dw = ddn[cw];
+    const int du = dtab[cu].x, dw = dtab[cw].y;
     Pd[h] = uint16_t(u + du);
     Pa[h] = uint16_t(w + dw);
     const uint32_t bit = 1u << lz;
     or_if_ne(live_d, uint32_t(du), 0u, bit);  // pointer two hops ahead may not be a terminal
     or_if_ne(live_a, uint32_t(dw), 0u, bit);
-    or_if_eq(mmax, c & 15u, 15u, bit);
-    or_if_ge(mmin, c, 0xf0u, bit);
+    // extremum iff no hop (delta 0; out-of-volume bytes are masked below)
+    or_if_eq(mmax, uint32_t(dc.x), 0u, bit);
+    or_if_eq(mmin, uint32_t(dc.y), 0u, bit);
   }
   {
     const uint32_t vmask = col_ok ? (nz >= 32 ? 0xffffffffu : ((1u << nz) - 1u)) : 0u;
@@ -747,7 +754,7 @@ __global__ void __launch_bounds__(A_THREADS, 1)
 #else
     const bool face = lx == 0 || lx == TX - 1;
 #endif
-    uint32_t* of = fstage + (lx ? TY * TZ : 0) + ly;
+    uint32_t* of = fstage + (lx ? TY * TZ + (ly ^ 16) : ly);
 #pragma unroll 4
     for (int lz = 0; lz < nz; ++lz) {
       const int h = hc + (lz + 1) * PXY;
