@@ -269,6 +269,17 @@ __device__ __forceinline__ HopW hop_cube_w(const HopW& lo, const HopW& hi) {
 }
 __device__ __forceinline__ uint32_t w_exp(float w) { return (__float_as_uint(w) >> 23) - 127u; }
 
+// Hop code of a vertex from its lower and upper unit cubes: positions lower
+// cube corner k -> k, upper cube corner k -> 7 + k (v itself -> 7: no hop);
+// the code is pu | pd << 4, straight from the weights' exponents:
+// pu = e_u - 127, pd = 14 - (e_d - 127)
+__device__ __forceinline__ uint8_t hop_code(const HopW& cl, const HopW& cu) {
+  const float M = fmaxf(cl.M, cu.M), m = fminf(cl.m, cu.m);
+  const uint32_t eu = __float_as_uint(__fmaf_rn(feq(cu.M, M), __fmaf_rn(128.f, cu.WM, -cl.WM), cl.WM)) >> 23;
+  const uint32_t ed = __float_as_uint(__fmaf_rn(feq(cl.m, m), __fmaf_rn(128.f, cl.Wm, -cu.Wm), cu.Wm)) >> 23;
+  return uint8_t(eu + 16u * (141u - ed) - 127u);
+}
+
 template <int kHX, int kHXY, class Emit>
 __device__ __forceinline__ void hop_column_cube(const float* __restrict__ fc, const int nz, const uint32_t gv0,
                                                 const uint32_t XY, ACounters* __restrict__ ctr, Emit&& emit) {
@@ -285,14 +296,7 @@ __device__ __forceinline__ void hop_column_cube(const float* __restrict__ fc, co
     if (lz < nz) {
       const float fv = b3;
       if (!isfinite(fv)) atomicMin(&ctr->bad, gv0 + XY * uint32_t(lz));
-      const HopW cl = hop_cube_w(L, Ln), cu = hop_cube_w(U, Un);
-      const float M = fmaxf(cl.M, cu.M), m = fminf(cl.m, cu.m);
-      // positions: lower cube corner k -> k, upper cube corner k -> 7 + k
-      // (v itself -> 7: no hop); the hop code is pu | pd << 4, straight from
-      // the weights' exponents: pu = e_u - 127, pd = 14 - (e_d - 127)
-      const uint32_t eu = __float_as_uint(__fmaf_rn(feq(cu.M, M), __fmaf_rn(128.f, cu.WM, -cl.WM), cl.WM)) >> 23;
-      const uint32_t ed = __float_as_uint(__fmaf_rn(feq(cl.m, m), __fmaf_rn(128.f, cl.Wm, -cu.Wm), cu.Wm)) >> 23;
-      emit(lz, uint8_t(eu + 16u * (141u - ed) - 127u));
+      emit(lz, hop_code(hop_cube_w(L, Ln), hop_cube_w(U, Un)));
     }
     L = Ln;
     U = Un;
@@ -300,6 +304,55 @@ __device__ __forceinline__ void hop_column_cube(const float* __restrict__ fc, co
     b1 = n1;
     b2 = n2;
     b3 = n3;
+  }
+}
+
+// Cube-shared hops of two diagonal neighbours v1 = (x, y) and v2 = (x+1, y+1)
+// over brick layers [z0, z0 + nl): the upper cube of v1 at layer z is the
+// lower cube of v2 at layer z + 1, so per layer three new quads (columns
+// (x-1, y-1), (x, y), (x+1, y+1)) and three cube merges serve two vertices
+// (hop_column_cube: two of each per vertex), and ten shared loads instead of
+// fourteen. fc = v1's column at box plane 0; ok1 / ok2: the columns lie in
+// the volume; emit(which, lz, code).
+template <int kHX, int kHXY, class Emit>
+__device__ __forceinline__ void hop_pair_cube(const float* __restrict__ fc, const int z0, const int nl,
+                                              const bool ok1, const bool ok2, const uint32_t gv1,
+                                              const uint32_t gv2, const uint32_t XY, ACounters* __restrict__ ctr,
+                                              Emit&& emit) {
+  constexpr int D = kHX + 1;  // (x, y) -> (x+1, y+1)
+  const float* p = fc + z0 * kHXY;  // plane P0 - 1 (P0 = z0 + 1: first vertex plane)
+  // A = Q(x-1, y-1) at plane P0 - 1; B = Q(x, y) at P0 - 1 and P0; D = Q(x+1, y+1) at P0
+  HopW A = hop_quad_w(p[-D], p[-kHX], p[-1], p[0]);
+  const HopW B0 = hop_quad_w(p[0], p[1], p[kHX], p[D]);
+  p += kHXY;
+  float f1 = p[0], f2 = p[D];  // v1, v2 at plane P0
+  HopW B = hop_quad_w(f1, p[1], p[kHX], f2);
+  HopW Dq = hop_quad_w(f2, p[D + 1], p[D + kHX], p[2 * D]);
+  HopW cB = hop_cube_w(B0, B);  // lower cube of v2 at P0
+#pragma unroll 2
+  for (int i = 0; i < nl; ++i) {
+    const int lz = z0 + i;
+    const float* q = fc + (lz + 1) * kHXY;  // plane P
+    const float* n = q + kHXY;              // plane P + 1
+    const float g1 = n[0], g2 = n[D];
+    const HopW An = hop_quad_w(q[-D], q[-kHX], q[-1], f1);
+    const HopW Bn = hop_quad_w(g1, n[1], n[kHX], g2);
+    const HopW Dn = hop_quad_w(g2, n[D + 1], n[D + kHX], n[2 * D]);
+    const HopW cu1 = hop_cube_w(B, Bn);
+    if (ok1) {
+      if (!isfinite(f1)) atomicMin(&ctr->bad, gv1 + XY * uint32_t(lz));
+      emit(0, lz, hop_code(hop_cube_w(A, An), cu1));
+    }
+    if (ok2) {
+      if (!isfinite(f2)) atomicMin(&ctr->bad, gv2 + XY * uint32_t(lz));
+      emit(1, lz, hop_code(cB, hop_cube_w(Dq, Dn)));
+    }
+    A = An;
+    B = Bn;
+    Dq = Dn;
+    cB = cu1;
+    f1 = g1;
+    f2 = g2;
   }
 }
 
@@ -457,6 +510,33 @@ __global__ void __launch_bounds__(A_THREADS, 1)
   const int nz = min(TZ, int(d.Z) - gz0);  // in-volume layers of the brick
   const int hc = (lx + 1) + PX * (ly + 1);  // column in the pointer space (shell layer z = 0)
   const uint32_t gv0 = uint32_t(gx) + d.X * uint32_t(gy) + d.XY * uint32_t(gz0);
+#ifndef PLMSS_NO_HOP_PAIRS
+  if (!kCodes && kCube) {
+    // diagonal pairs (x, y), (x+1, y+1), y even, x < 31, over half the
+    // layers each (warps 0-30); the 32 columns left over ((31, y even) and
+    // (0, y odd)) one per lane of warp 31 over all layers
+    if (tid < 992) {
+      const int zh = tid >= 496, rq = tid - 496 * zh, r = rq / 31, x = rq - 31 * r, y = 2 * r;
+      const int z0 = 16 * zh, nl = min(16, nz - z0);
+      const int ax = gx0 + x, ay = gy0 + y;
+      const bool ok1 = ax < int(d.X) && ay < int(d.Y), ok2 = ax + 1 < int(d.X) && ay + 1 < int(d.Y);
+      const int h1 = (x + 1) + PX * (y + 1);
+      if (nl > 0 && (ok1 || ok2))
+        hop_pair_cube<HX, HXY>(f + (y + 1) * HX + (x + HXO), z0, nl, ok1, ok2,
+                               uint32_t(ax) + d.X * uint32_t(ay) + d.XY * uint32_t(gz0),
+                               uint32_t(ax + 1) + d.X * uint32_t(ay + 1) + d.XY * uint32_t(gz0), d.XY, ctr,
+                               [&](int which, int lz, uint8_t b) { code[h1 + which * (PX + 1) + (lz + 1) * PXY] = b; });
+    } else {
+      const int l = tid - 992, x = l < 16 ? 31 : 0, y = l < 16 ? 2 * l : 2 * (l - 16) + 1;
+      const int ax = gx0 + x, ay = gy0 + y;
+      const int h1 = (x + 1) + PX * (y + 1);
+      if (ax < int(d.X) && ay < int(d.Y))
+        hop_column_cube<HX, HXY>(f + (y + 1) * HX + (x + HXO), nz,
+                                 uint32_t(ax) + d.X * uint32_t(ay) + d.XY * uint32_t(gz0), d.XY, ctr,
+                                 [&](int lz, uint8_t b) { code[h1 + (lz + 1) * PXY] = b; });
+    }
+  } else
+#endif
   if (!kCodes && col_ok) {
     if (kCube)
       hop_column_cube<HX, HXY>(f + (ly + 1) * HX + (lx + HXO), nz, gv0, d.XY, ctr,
