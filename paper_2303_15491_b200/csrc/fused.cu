@@ -1717,8 +1717,10 @@ __device__ __forceinline__ void brick_tma_body(const CUtensorMap& mtok, const Br
   uint8_t* clsp = a.cls + (uint64_t(gx0) + lane + CX * cy + CXY * gz0);
   uint16_t* chp = a.chunk + (uint64_t(cy) + uint64_t(d.Y - 1) * gz0) * a.nxc + tx;
   const uint64_t chstep = uint64_t(d.Y - 1) * a.nxc;
-  uint32_t pf[4] = {0, 0, 0, 0};  // top face of this thread's previous cube
-  uint32_t pu = 0;                 // ... and whether its four labels agree (0 / 1)
+  uint32_t pf[1] = {0};  // corner 0 of this thread's previous cube's top face
+  uint32_t pu = 0;       // ... and whether its four labels agree (0 / 1)
+  __shared__ uint16_t s_q[RY][kBatch * 32];  // per warp: queued non-uniform cubes (layer << 5 | lane)
+  __shared__ uint32_t s_lt[RY][kBatch];      // per warp: record total of each cube layer of the batch
   // ids (a.ids_out): this thread's vertex column
   const bool vert_ok = gx0 + uint32_t(lane) < d.X && cy < d.Y;
   const uint64_t ids_v0 = uint64_t(gx0 + lane) + uint64_t(d.X) * (uint64_t(cy) + uint64_t(d.Y) * gz0);
@@ -1726,6 +1728,7 @@ __device__ __forceinline__ void brick_tma_body(const CUtensorMap& mtok, const Br
     // a brick made of the volume's last vertex layer only: no cube layers
     a.ids_out[ids_v0] = brick_token_id(a, __ldg(a.ms + ids_v0));
   }
+  if (lane < kBatch) s_lt[w][lane] = 0u;
   if (tid == 0) {
     for (int k = 0; k < 2; ++k) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s_bar[k])));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -1745,41 +1748,54 @@ __device__ __forceinline__ void brick_tma_body(const CUtensorMap& mtok, const Br
   if (tid == 0 && nb > 0) issue(0);
   // one cube layer; the bottom face is the previous layer's top face, so a
   // cube is uniform iff its top face is, the bottom one was, and one
-  // vertical edge agrees
-  uint32_t btot = 0;  // lane l: record count of cube layer l of the batch
-  auto cube = [&](const uint32_t(&cur)[RY + 1][TLW], const int cl) {
-    uint32_t cnt = 0;
+  // vertical edge agrees. Uniform cubes get class 0 here; the others are
+  // queued per warp (layer, lane) and classified after the batch with every
+  // lane busy (separator cubes are a few lanes of a row: classifying them
+  // in place would run the two-label path at low lane occupancy).
+  int qn = 0;  // warp-uniform: queued cubes of this batch
+  auto face = [&](const uint32_t(&cur)[RY + 1][TLW], const int cl) {
+    bool nu = false;
     if (cube_ok) {
-      uint32_t c[8];
-      c[0] = pf[0];
-      c[1] = pf[1];
-      c[2] = pf[2];
-      c[3] = pf[3];
-      c[4] = cur[w][lane];
-      c[5] = cur[w][lane + 1];
-      c[6] = cur[w + 1][lane];
-      c[7] = cur[w + 1][lane + 1];
-      const uint32_t tu = c[5] == c[4] && c[6] == c[4] && c[7] == c[4];
-      const bool uni = (tu & pu) && c[4] == c[0];
-      pf[0] = c[4];
-      pf[1] = c[5];
-      pf[2] = c[6];
-      pf[3] = c[7];
+      const uint32_t c4 = cur[w][lane], c5 = cur[w][lane + 1], c6 = cur[w + 1][lane], c7 = cur[w + 1][lane + 1];
+      const uint32_t tu = c5 == c4 && c6 == c4 && c7 == c4;
+      nu = !((tu & pu) && c4 == pf[0]);
+      pf[0] = c4;
       pu = tu;
-      uint32_t cls = 0;
-      if (!uni) {
+      if (!nu) *clsp = 0;
+    }
+    const uint32_t q = __ballot_sync(0xffffffffu, nu);
+    if (nu) s_q[w][qn + __popc(q & ((1u << lane) - 1u))] = uint16_t(cl << 5 | lane);
+    qn += __popc(q);
+    clsp += CXY;
+  };
+  // the queued cubes of a batch: corners from the staged layers, class byte,
+  // record count into the layer's total
+  auto classify = [&](const Buf& bb, uint8_t* cls0) {
+    for (int i0 = 0; i0 < qn; i0 += 32) {
+      if (i0 + lane < qn) {
+        const uint32_t e = s_q[w][i0 + lane], cl = e >> 5, x = e & 31u;
+        uint32_t c[8];
+        c[0] = bb[cl][w][x];
+        c[1] = bb[cl][w][x + 1];
+        c[2] = bb[cl][w + 1][x];
+        c[3] = bb[cl][w + 1][x + 1];
+        c[4] = bb[cl + 1][w][x];
+        c[5] = bb[cl + 1][w][x + 1];
+        c[6] = bb[cl + 1][w + 1][x];
+        c[7] = bb[cl + 1][w + 1][x + 1];
         // corners equal to corner 0 (bit i)
         uint32_t m8 = 1u;
 #pragma unroll
         for (int i = 1; i < 8; ++i) m8 |= uint32_t(c[i] == c[0]) << i;
         // the lowest corner with another label; two labels iff every
         // corner carries one of the two (the common case on a separator)
-        uint32_t bb = c[7];
+        uint32_t bl = c[7];
 #pragma unroll
-        for (int i = 6; i >= 1; --i) bb = (m8 >> i) & 1u ? bb : c[i];
+        for (int i = 6; i >= 1; --i) bl = (m8 >> i) & 1u ? bl : c[i];
         uint32_t mb = 0u;
 #pragma unroll
-        for (int i = 1; i < 8; ++i) mb |= uint32_t(c[i] == bb) << i;
+        for (int i = 1; i < 8; ++i) mb |= uint32_t(c[i] == bl) << i;
+        uint32_t cnt, cls;
         if ((m8 | mb) == 0xffu) {
           cnt = g_two_cnt[m8 >> 1];
           cls = m8;
@@ -1787,12 +1803,10 @@ __device__ __forceinline__ void brick_tma_body(const CUtensorMap& mtok, const Br
           cnt = general_count(c[0], c[1], c[2], c[3], c[4], c[5], c[6], c[7]);
           cls = 0xffu;
         }
+        cls0[uint64_t(cl) * CXY + x] = uint8_t(cls);
+        if (cnt) atomicAdd(&s_lt[w][cl], cnt);
       }
-      *clsp = uint8_t(cls);
     }
-    const uint32_t tot = __reduce_add_sync(0xffffffffu, cnt);
-    if (lane == cl) btot = tot;
-    clsp += CXY;
   };
   for (int b = 0; b < nb; ++b) {
     if (tid == 0 && b + 1 < nb) issue(b + 1);  // the other buffer was released by the barrier below
@@ -1804,19 +1818,24 @@ __device__ __forceinline__ void brick_tma_body(const CUtensorMap& mtok, const Br
     const Buf& bb = *buf[b & 1];
     if (b == 0 && cube_ok) {
       pf[0] = bb[0][w][lane];
-      pf[1] = bb[0][w][lane + 1];
-      pf[2] = bb[0][w + 1][lane];
-      pf[3] = bb[0][w + 1][lane + 1];
-      pu = pf[1] == pf[0] && pf[2] == pf[0] && pf[3] == pf[0];
+      pu = bb[0][w][lane + 1] == pf[0] && bb[0][w + 1][lane] == pf[0] && bb[0][w + 1][lane + 1] == pf[0];
     }
     const int cn = min(kBatch, ncl - b * kBatch);
+    uint8_t* const cls0 = clsp - uint64_t(lane);  // class byte of this batch's cube (0, row w, layer 0)
+    qn = 0;
     if (cn == kBatch) {
 #pragma unroll 2
-      for (int cl = 0; cl < kBatch; ++cl) cube(bb[cl + 1], cl);
+      for (int cl = 0; cl < kBatch; ++cl) face(bb[cl + 1], cl);
     } else {
 #pragma unroll 1
-      for (int cl = 0; cl < cn; ++cl) cube(bb[cl + 1], cl);
+      for (int cl = 0; cl < cn; ++cl) face(bb[cl + 1], cl);
     }
+    __syncwarp();
+    classify(bb, cls0);
+    __syncwarp();
+    const uint32_t btot = lane < kBatch ? s_lt[w][lane] : 0u;
+    __syncwarp();
+    if (lane < kBatch) s_lt[w][lane] = 0u;
     if (a.ids_out && vert_ok) {
       // this thread's vertex column: the batch's bottom layers, and the
       // volume's top layer when the batch ends there
