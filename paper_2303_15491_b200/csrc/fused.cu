@@ -78,7 +78,20 @@ constexpr int kFaceX = 2 * TY * TZ;
 constexpr int A_THREADS = 1024;
 constexpr int kCodeOff = 4 * HN;                // hop codes after the field box
 constexpr int kTabOff = kCodeOff + (PN + 15) / 16 * 16;  // code byte -> pointer delta, up and down
-constexpr int kASmem = kTabOff + 2 * 256 * 4 + 1024;      // + TMA alignment slack
+// CTA-wide scalars and scan scratch, also in the dynamic window: with no
+// static shared memory the window starts at a fixed, 1024-byte aligned offset
+// (checked at run time), so every shared access is an immediate offset from
+// the symbol (a runtime-aligned base is rematerialised in the loops under
+// register pressure)
+struct AStat {
+  uint64_t bar;
+  unsigned long long lbase[3];
+  uint32_t wcnt[A_THREADS / 32][3];
+  uint32_t tot[3];
+  uint32_t eoff[7][A_THREADS / 32];
+};
+constexpr int kStatOff = kTabOff + 2 * 256 * 4;
+constexpr int kASmem = kStatOff + int((sizeof(AStat) + 15) / 16 * 16);
 static_assert(2 * 2 * PN <= 4 * HN, "pointer arrays must fit in the field box");
 static_assert(kCodeOff % 16 == 0, "code array alignment");
 constexpr uint8_t kExitMark = 0xfe;  // shell cell reached by some brick vertex
@@ -385,10 +398,7 @@ __global__ void __launch_bounds__(A_THREADS, 1)
                    uint32_t* __restrict__ min_tt, uint64_t ext_cap,
                    uint32_t* __restrict__ TT, uint64_t tt_cap, uint4* __restrict__ TB, uint32_t* __restrict__ lt,
                    ACounters* __restrict__ ctr) {
-  extern __shared__ __align__(16) unsigned char a_smem_raw[];
-  // TMA destinations must be 128-byte aligned: round the window up (the
-  // launch reserves 1024 extra bytes for this).
-  unsigned char* a_smem = a_smem_raw + ((1024u - (smem_u32(a_smem_raw) & 1023u)) & 1023u);
+  extern __shared__ __align__(1024) unsigned char a_smem[];
   float* f = reinterpret_cast<float*>(a_smem);         // HN floats (steps 1-2)
   uint16_t* Pd = reinterpret_cast<uint16_t*>(a_smem);  // PN (steps 3+, aliases f)
   uint16_t* Pa = Pd + PN;                              // PN
@@ -396,15 +406,18 @@ __global__ void __launch_bounds__(A_THREADS, 1)
   // per code byte: pointer deltas of its up and down hops (one 8-byte load
   // for both directions of the same byte)
   int2* dtab = reinterpret_cast<int2*>(a_smem + kTabOff);
-  __shared__ __align__(8) uint64_t s_bar;
-  __shared__ uint32_t s_wcnt[A_THREADS / 32][3];
-  __shared__ uint32_t s_tot[3];
-  __shared__ uint32_t s_eoff[kShellPerThread][A_THREADS / 32];
-  __shared__ unsigned long long s_lbase[3];
+  AStat& st = *reinterpret_cast<AStat*>(a_smem + kStatOff);
+  uint64_t& s_bar = st.bar;
+  uint32_t(&s_wcnt)[A_THREADS / 32][3] = st.wcnt;
+  uint32_t(&s_tot)[3] = st.tot;
+  uint32_t(&s_eoff)[kShellPerThread][A_THREADS / 32] = st.eoff;
+  unsigned long long(&s_lbase)[3] = st.lbase;
 
   const int tid = int(threadIdx.x);
   const int lane = tid & 31;
   const int lx = tid & 31, ly = tid >> 5;
+  // TMA destinations must be 128-byte aligned
+  if (tid == 0 && (smem_u32(a_smem) & 127u)) __trap();
   if ((kTMA || kCodes) && tid == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&s_bar)));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -525,7 +538,10 @@ __global__ void __launch_bounds__(A_THREADS, 1)
         hop_pair_cube<HX, HXY>(f + (y + 1) * HX + (x + HXO), z0, nl, ok1, ok2,
                                uint32_t(ax) + d.X * uint32_t(ay) + d.XY * uint32_t(gz0),
                                uint32_t(ax + 1) + d.X * uint32_t(ay + 1) + d.XY * uint32_t(gz0), d.XY, ctr,
-                               [&](int which, int lz, uint8_t b) { code[h1 + which * (PX + 1) + (lz + 1) * PXY] = b; });
+                               [&](int which, int lz, uint8_t b) {
+                                 DCHECK(h1 + which * (PX + 1) + (lz + 1) * PXY < PN, 104);
+                                 code[h1 + which * (PX + 1) + (lz + 1) * PXY] = b;
+                               });
     } else {
       const int l = tid - 992, x = l < 16 ? 31 : 0, y = l < 16 ? 2 * l : 2 * (l - 16) + 1;
       const int ax = gx0 + x, ay = gy0 + y;
@@ -579,8 +595,10 @@ __global__ void __launch_bounds__(A_THREADS, 1)
     const int2 dc = dtab[c];
     int u = h + dc.x, w = h + dc.y;
     const uint32_t cu = code[u], cw = code[w];
-    if (cu >= kExitMark && u != h) code[u] = kExitMark;
-    if (cw >= kExitMark && w != h) code[w] = kExitMark;
+    // (no hop: u == h, whose own byte is a vertex code, or 0xff outside the
+    // volume, where the mark is harmless: no chain ever enters such a cell)
+    if (cu >= kExitMark) code[u] = kExitMark;
+    if (cw >= kExitMark) code[w] = kExitMark;
     const int du = dtab[cu].x, dw = dtab[cw].y;
     Pd[h] = uint16_t(u + du);
     Pa[h] = uint16_t(w + dw);
@@ -1036,6 +1054,24 @@ __global__ void k_rank_lists(const uint64_t* __restrict__ keys, const uint64_t* 
     list[i] = uint32_t(keys[i]) + id0;  // id0: the slab's first vertex id (z-slab lists are global)
     RK[vals[i]] = uint32_t(i);
   }
+}
+
+// One extremum list sorted ascending (list, in place) and the rank of each of
+// its table entries (RK); n_ids bounds the keys (radix bits).
+static void sort_extrema(Ctx& c, uint32_t* list, const uint32_t* ltt, int64_t k, uint64_t n_ids, uint32_t* RK,
+                         uint32_t id0) {
+  if (k < 1) return;
+  uint64_t* kk = c.get_t<uint64_t>(S_SORT_A, k);
+  uint64_t* vv = c.get_t<uint64_t>(S_SORT_B, k);
+  k_list_pairs<<<blocks_for(k, 256), 256, 0, c.stream>>>(list, ltt, k, kk, vv);
+  CK_LAUNCH("k_list_pairs");
+  if (k > 1) {
+    int bits = 0;
+    while ((uint64_t(1) << bits) < n_ids) ++bits;
+    radix_sort_pairs(c, kk, vv, k, bits);
+  }
+  k_rank_lists<<<blocks_for(k, 256), 256, 0, c.stream>>>(kk, vv, k, list, RK, id0);
+  CK_LAUNCH("k_rank_lists");
 }
 
 // Dense region bitmap (key = rank_min * n_max + rank_max, n_max * n_min <=
@@ -1774,6 +1810,7 @@ __device__ __forceinline__ void brick_tma_body(const CUtensorMap& mtok, const Br
     for (int i0 = 0; i0 < qn; i0 += 32) {
       if (i0 + lane < qn) {
         const uint32_t e = s_q[w][i0 + lane], cl = e >> 5, x = e & 31u;
+        DCHECK(cl < uint32_t(kBatch) && qn <= kBatch * 32, 601);
         uint32_t c[8];
         c[0] = bb[cl][w][x];
         c[1] = bb[cl][w][x + 1];
@@ -2516,23 +2553,8 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
     const uint64_t nt = h.n_tt;
     // ---- extrema lists sorted ascending; rank of every extremum table entry
     uint32_t* RK = c.get_t<uint32_t>(S_RK, nt);
-    for (int dir = 0; dir < 2; ++dir) {
-      uint32_t* list = dir ? minima : maxima;
-      const uint32_t* ltt = dir ? min_tt : max_tt;
-      const int64_t k = dir ? o.n_min : o.n_max;
-      if (k < 1) continue;
-      uint64_t* kk = c.get_t<uint64_t>(S_SORT_A, k);
-      uint64_t* vv = c.get_t<uint64_t>(S_SORT_B, k);
-      k_list_pairs<<<blocks_for(k, 256), 256, 0, c.stream>>>(list, ltt, k, kk, vv);
-      CK_LAUNCH("k_list_pairs");
-      if (k > 1) {
-        int bits = 0;
-        while ((uint64_t(1) << bits) < uint64_t(g.n)) ++bits;
-        radix_sort_pairs(c, kk, vv, k, bits);
-      }
-      k_rank_lists<<<blocks_for(k, 256), 256, 0, c.stream>>>(kk, vv, k, list, RK, 0u);
-      CK_LAUNCH("k_rank_lists");
-    }
+    sort_extrema(c, maxima, max_tt, o.n_max, uint64_t(g.n), RK, 0u);
+    sort_extrema(c, minima, min_tt, o.n_min, uint64_t(g.n), RK, 0u);
     c.mark(2);
     // ---- B: terminal-table forest -> extremum rank of every table entry
     uint32_t* SD = c.get_t<uint32_t>(S_SD, nt);
@@ -2925,23 +2947,8 @@ void fused_segment(Ctx& c, const Grid& g, const float* field, uint32_t* desc, ui
   const int64_t n_max = int64_t(h.n_max), n_min = int64_t(h.n_min);
   const uint64_t nt = h.n_tt;
   uint32_t* RK = c.get_t<uint32_t>(S_RK, nt);
-  for (int dir = 0; dir < 2; ++dir) {
-    uint32_t* list = dir ? minima : maxima;
-    const uint32_t* ltt = dir ? min_tt : max_tt;
-    const int64_t k = dir ? n_min : n_max;
-    if (k < 1) continue;
-    uint64_t* kk = c.get_t<uint64_t>(S_SORT_A, k);
-    uint64_t* vv = c.get_t<uint64_t>(S_SORT_B, k);
-    k_list_pairs<<<blocks_for(k, 256), 256, 0, c.stream>>>(list, ltt, k, kk, vv);
-    CK_LAUNCH("k_list_pairs");
-    if (k > 1) {
-      int bits = 0;
-      while ((uint64_t(1) << bits) < uint64_t(g.n)) ++bits;
-      radix_sort_pairs(c, kk, vv, k, bits);
-    }
-    k_rank_lists<<<blocks_for(k, 256), 256, 0, c.stream>>>(kk, vv, k, list, RK, 0u);
-    CK_LAUNCH("k_rank_lists");
-  }
+  sort_extrema(c, maxima, max_tt, n_max, uint64_t(g.n), RK, 0u);
+  sort_extrema(c, minima, min_tt, n_min, uint64_t(g.n), RK, 0u);
   uint32_t* SD = c.get_t<uint32_t>(S_SD, nt);
   uint32_t* SA = c.get_t<uint32_t>(S_SA, nt);
   k_tt_succ<<<unsigned(ntiles), 256, 0, c.stream>>>(TB, TT, lt, RK, SD, SA, 0u, nt);
@@ -3119,23 +3126,8 @@ void slab_segment(Ctx& c, const Grid& g, int64_t z0, int64_t z1, const float* fi
   st.nt = nt;
   // extremum lists sorted by id (global ids: + z0 * XY), rank of every extremum entry
   uint32_t* RK = c.get_t<uint32_t>(S_RK, nt);
-  for (int dir = 0; dir < 2; ++dir) {
-    uint32_t* list = dir ? minima : maxima;
-    const uint32_t* ltt = dir ? min_tt : max_tt;
-    const int64_t k = dir ? st.n_min_l : st.n_max_l;
-    if (k < 1) continue;
-    uint64_t* kk = c.get_t<uint64_t>(S_SORT_A, k);
-    uint64_t* vv = c.get_t<uint64_t>(S_SORT_B, k);
-    k_list_pairs<<<blocks_for(k, 256), 256, 0, c.stream>>>(list, ltt, k, kk, vv);
-    CK_LAUNCH("k_list_pairs");
-    if (k > 1) {
-      int bits = 0;
-      while ((uint64_t(1) << bits) < nloc) ++bits;
-      radix_sort_pairs(c, kk, vv, k, bits);
-    }
-    k_rank_lists<<<blocks_for(k, 256), 256, 0, c.stream>>>(kk, vv, k, list, RK, uint32_t(uint64_t(z0) * d.XY));
-    CK_LAUNCH("k_rank_lists");
-  }
+  sort_extrema(c, maxima, max_tt, st.n_max_l, nloc, RK, uint32_t(uint64_t(z0) * d.XY));
+  sort_extrema(c, minima, min_tt, st.n_min_l, nloc, RK, uint32_t(uint64_t(z0) * d.XY));
   // the forest inside the slab, to its fixpoint (portals are roots)
   uint32_t* SD = c.get_t<uint32_t>(S_SD, nt);
   uint32_t* SA = c.get_t<uint32_t>(S_SA, nt);
