@@ -112,6 +112,29 @@ class Clocks:
                 "samples": len(sm)}
 
 
+def pcie_copy_peaks(nbytes=1 << 30, reps=3):
+    """Measured pinned-host <-> device copy bandwidth (GB/s) of this box's
+    link, the roofline of the end-to-end number (cudaMemcpyAsync of 1 GiB,
+    CUDA events on the current stream)."""
+    import torch
+
+    dev = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    host = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    out = {}
+    for name, dst, src in (("d2h", host, dev), ("h2d", dev, host)):
+        dst.copy_(src, non_blocking=True)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            dst.copy_(src, non_blocking=True)
+        b.record()
+        torch.cuda.synchronize()
+        out[name] = reps * nbytes / (a.elapsed_time(b) * 1e-3) / 1e9
+    del dev, host
+    return out
+
+
 def dist_setup():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -585,6 +608,16 @@ def main():
                             "api": f"plmss_b200_pipeline_host_batch over {len(vols)} volumes (every volume's "
                                    "upload, pipeline and download; consecutive volumes overlap)",
                             "single_call_ms_per_step": round(e_ms, 3)})
+        # the link roofline: the step's D2H bytes at the measured copy rate
+        try:
+            pk = pcie_copy_peaks()
+            d2h_gbs = d2h / (e2e["ms_per_step"] * 1e-3) / 1e9
+            e2e["link"] = {"bound": "pcie d2h", "achieved_d2h_gbs": round(d2h_gbs, 2),
+                           "peak_d2h_gbs": round(pk["d2h"], 2), "peak_h2d_gbs": round(pk["h2d"], 2),
+                           "frac": round(d2h_gbs / pk["d2h"], 4),
+                           "peak_source": "measured here: cudaMemcpyAsync of 1 GiB pinned <-> device"}
+        except Exception as exc:  # noqa: BLE001 - the link figure is optional
+            e2e["link"] = {"error": str(exc)[:120]}
 
     cpu = None
     if not args.no_cpu_baseline and rank == 0:
