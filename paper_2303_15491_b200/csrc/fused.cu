@@ -1877,15 +1877,15 @@ __device__ __forceinline__ void brick_tma_body(const CUtensorMap& mtok, const Br
       // this thread's vertex column: the batch's bottom layers, and the
       // volume's top layer when the batch ends there
       const int nv = cn + ((gz0 + uint32_t(b * kBatch + cn) == d.Z - 1) ? 1 : 0);
-      const uint64_t vo = ids_v0 + uint64_t(b * kBatch) * d.XY;
+      uint32_t* op = a.ids_out + (ids_v0 + uint64_t(b * kBatch) * d.XY);
       uint32_t lt = ~0u, lid = 0;
-      for (int i = 0; i < nv; ++i) {
+      for (int i = 0; i < nv; ++i, op += d.XY) {
         const uint32_t tk = bb[i][w][lane];
         if (tk != lt) {
           lt = tk;
           lid = brick_token_id(a, tk);
         }
-        a.ids_out[vo + uint64_t(i) * d.XY] = lid;
+        *op = lid;
       }
     }
     // the batch's chunk counts, one store per layer from lanes 0 .. cn-1
