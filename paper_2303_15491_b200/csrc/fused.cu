@@ -1036,41 +1036,54 @@ __global__ void __launch_bounds__(256) k_tt_jump(uint64_t nt, uint32_t* __restri
   if (__any_sync(0xffffffffu, ch) && (threadIdx.x & 31) == 0) *changed = 1;
 }
 
-// (gid, table entry) pairs of an extremum list for the radix sort
-__global__ void k_list_pairs(const uint32_t* __restrict__ list, const uint32_t* __restrict__ tt, int64_t n,
-                             uint64_t* __restrict__ keys, uint64_t* __restrict__ vals) {
+// (list bit | gid, table entry) pairs of both extremum lists for one radix sort:
+// maxima first (list bit 0), then minima (list bit 1 above the id bits)
+__global__ void k_list_pairs(const uint32_t* __restrict__ maxima, const uint32_t* __restrict__ max_tt, int64_t n_max,
+                             const uint32_t* __restrict__ minima, const uint32_t* __restrict__ min_tt, int64_t n_min,
+                             int bits, uint64_t* __restrict__ keys, uint64_t* __restrict__ vals) {
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i < n) {
-    keys[i] = list[i];
-    vals[i] = tt[i];
+  if (i < n_max) {
+    keys[i] = maxima[i];
+    vals[i] = max_tt[i];
+  } else if (i < n_max + n_min) {
+    keys[i] = (uint64_t(1) << bits) | minima[i - n_max];
+    vals[i] = min_tt[i - n_max];
   }
 }
 
-// sorted pairs -> ascending list and the rank of every extremum table entry
-__global__ void k_rank_lists(const uint64_t* __restrict__ keys, const uint64_t* __restrict__ vals, int64_t n,
-                             uint32_t* __restrict__ list, uint32_t* __restrict__ RK, uint32_t id0) {
+// sorted pairs -> the two ascending lists and the rank (within its list) of
+// every extremum table entry
+__global__ void k_rank_lists(const uint64_t* __restrict__ keys, const uint64_t* __restrict__ vals, int64_t n_max,
+                             int64_t n_min, int bits, uint32_t* __restrict__ maxima,
+                             uint32_t* __restrict__ minima, uint32_t* __restrict__ RK, uint32_t id0) {
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i < n) {
-    list[i] = uint32_t(keys[i]) + id0;  // id0: the slab's first vertex id (z-slab lists are global)
+  if (i >= n_max + n_min) return;
+  // id0: the slab's first vertex id (z-slab lists are global)
+  if (i < n_max) {
+    maxima[i] = uint32_t(keys[i]) + id0;
     RK[vals[i]] = uint32_t(i);
+  } else {
+    minima[i - n_max] = uint32_t(keys[i] ^ (uint64_t(1) << bits)) + id0;  // without the list bit
+    RK[vals[i]] = uint32_t(i - n_max);
   }
 }
 
-// One extremum list sorted ascending (list, in place) and the rank of each of
-// its table entries (RK); n_ids bounds the keys (radix bits).
-static void sort_extrema(Ctx& c, uint32_t* list, const uint32_t* ltt, int64_t k, uint64_t n_ids, uint32_t* RK,
-                         uint32_t id0) {
+// Both extremum lists sorted ascending (in place) and the rank of each of
+// their table entries (RK), by one radix sort of the concatenated lists keyed
+// (list, id): half the launches of a sort per list, and these launches are
+// latency-bound (~2·10^4 entries). n_ids bounds the ids (radix bits).
+static void sort_extrema(Ctx& c, uint32_t* maxima, const uint32_t* max_tt, int64_t n_max, uint32_t* minima,
+                         const uint32_t* min_tt, int64_t n_min, uint64_t n_ids, uint32_t* RK, uint32_t id0) {
+  const int64_t k = n_max + n_min;
   if (k < 1) return;
   uint64_t* kk = c.get_t<uint64_t>(S_SORT_A, k);
   uint64_t* vv = c.get_t<uint64_t>(S_SORT_B, k);
-  k_list_pairs<<<blocks_for(k, 256), 256, 0, c.stream>>>(list, ltt, k, kk, vv);
+  int bits = 0;
+  while ((uint64_t(1) << bits) < n_ids) ++bits;
+  k_list_pairs<<<blocks_for(k, 256), 256, 0, c.stream>>>(maxima, max_tt, n_max, minima, min_tt, n_min, bits, kk, vv);
   CK_LAUNCH("k_list_pairs");
-  if (k > 1) {
-    int bits = 0;
-    while ((uint64_t(1) << bits) < n_ids) ++bits;
-    radix_sort_pairs(c, kk, vv, k, bits);
-  }
-  k_rank_lists<<<blocks_for(k, 256), 256, 0, c.stream>>>(kk, vv, k, list, RK, id0);
+  if (k > 1) radix_sort_pairs(c, kk, vv, k, bits + 1);
+  k_rank_lists<<<blocks_for(k, 256), 256, 0, c.stream>>>(kk, vv, n_max, n_min, bits, maxima, minima, RK, id0);
   CK_LAUNCH("k_rank_lists");
 }
 
@@ -2553,8 +2566,7 @@ FusedOut fused_pipeline(Ctx& c, const Grid& g, const float* field, uint32_t* des
     const uint64_t nt = h.n_tt;
     // ---- extrema lists sorted ascending; rank of every extremum table entry
     uint32_t* RK = c.get_t<uint32_t>(S_RK, nt);
-    sort_extrema(c, maxima, max_tt, o.n_max, uint64_t(g.n), RK, 0u);
-    sort_extrema(c, minima, min_tt, o.n_min, uint64_t(g.n), RK, 0u);
+    sort_extrema(c, maxima, max_tt, o.n_max, minima, min_tt, o.n_min, uint64_t(g.n), RK, 0u);
     c.mark(2);
     // ---- B: terminal-table forest -> extremum rank of every table entry
     uint32_t* SD = c.get_t<uint32_t>(S_SD, nt);
@@ -2947,8 +2959,7 @@ void fused_segment(Ctx& c, const Grid& g, const float* field, uint32_t* desc, ui
   const int64_t n_max = int64_t(h.n_max), n_min = int64_t(h.n_min);
   const uint64_t nt = h.n_tt;
   uint32_t* RK = c.get_t<uint32_t>(S_RK, nt);
-  sort_extrema(c, maxima, max_tt, n_max, uint64_t(g.n), RK, 0u);
-  sort_extrema(c, minima, min_tt, n_min, uint64_t(g.n), RK, 0u);
+  sort_extrema(c, maxima, max_tt, n_max, minima, min_tt, n_min, uint64_t(g.n), RK, 0u);
   uint32_t* SD = c.get_t<uint32_t>(S_SD, nt);
   uint32_t* SA = c.get_t<uint32_t>(S_SA, nt);
   k_tt_succ<<<unsigned(ntiles), 256, 0, c.stream>>>(TB, TT, lt, RK, SD, SA, 0u, nt);
@@ -3126,8 +3137,7 @@ void slab_segment(Ctx& c, const Grid& g, int64_t z0, int64_t z1, const float* fi
   st.nt = nt;
   // extremum lists sorted by id (global ids: + z0 * XY), rank of every extremum entry
   uint32_t* RK = c.get_t<uint32_t>(S_RK, nt);
-  sort_extrema(c, maxima, max_tt, st.n_max_l, nloc, RK, uint32_t(uint64_t(z0) * d.XY));
-  sort_extrema(c, minima, min_tt, st.n_min_l, nloc, RK, uint32_t(uint64_t(z0) * d.XY));
+  sort_extrema(c, maxima, max_tt, st.n_max_l, minima, min_tt, st.n_min_l, nloc, RK, uint32_t(uint64_t(z0) * d.XY));
   // the forest inside the slab, to its fixpoint (portals are roots)
   uint32_t* SD = c.get_t<uint32_t>(S_SD, nt);
   uint32_t* SA = c.get_t<uint32_t>(S_SA, nt);
